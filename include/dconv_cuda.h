@@ -1,0 +1,175 @@
+/*
+ * dconv_cuda.h -- C-ABI of the B200-native direct-convolution hot path.
+ *
+ * This is the drop-in boundary: plain pointers, sizes and integer error codes,
+ * no C++ or torch types.  Every device pointer is a CUDA global-memory
+ * address; every call is asynchronous on `stream` (a cudaStream_t passed as
+ * void*, NULL = legacy default stream).  The library owns no device memory:
+ * the callers pass every buffer, so the "zero memory overhead" contract of the
+ * reference holds -- no im2col buffer, no
+ * split-K scratch, no staging copy in global memory.
+ *
+ * Layouts are the reference's (tensor.hpp:50-141), with an outermost image
+ * dimension added (each image slice is byte-identical to the reference's
+ * batch-1 BlockedFeatureMap):
+ *   blocked map     [N][ceil(C/c_b)][H][W][c_b]    fp32, padded channels == 0
+ *   blocked kernel  [C_o/c_ob][C_i/c_ib][H_f][W_f][c_ib][c_ob]
+ *   dense map       [N][C][H][W]                   (first-layer reader input)
+ *   dense kernel    [C_i][C_o][H_f][W_f]           (KernelTensor, tensor.hpp:83-103)
+ *
+ * Reference interfaces replaced (file:line in /root/reference/proj/core/):
+ *   dconv_cuda_conv_direct      <- conv_direct (direct.cpp is
+ *                                  absent from the snapshot, CMakeLists.txt:29)
+ *                                  + the tile registry micro_kernel.hpp:37-51
+ *   dconv_cuda_conv_first_layer <- the unblocked first layer (PAPER.md:18-21,
+ *                                  SPEC.md:121 zero-pad alternative)
+ *   dconv_cuda_pack_kernel      <- pack_kernel        tensor.cpp:85-95
+ *   dconv_cuda_unpack_kernel    <- unpack_kernel      tensor.cpp:97-108
+ *   dconv_cuda_pack_feature_map <- pack_feature_map   tensor.cpp:65-73
+ *   dconv_cuda_unpack_feature_map <- unpack_feature_map tensor.cpp:75-83
+ *   dconv_cuda_relu_blocked     <- relu_blocked
+ *   dconv_cuda_add_blocked      <- skip layer, PAPER.md:4-7 (no reference code)
+ *   dconv_cuda_maxpool2x2_blocked <- subsampling, PAPER.md:9-10 (no reference code)
+ *   dconv_conv_shape            <- ConvShape::ConvShape shape.cpp:30-40
+ *   dconv_conv_flops            <- conv_flops         reference.cpp:106-109
+ */
+#ifndef DCONV_CUDA_H
+#define DCONV_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error codes (the C++ layer maps them back to the reference's exceptions:
+ * EINVAL_SHAPE/EPARAM -> std::invalid_argument, ELAYOUT -> std::invalid_argument
+ * "layout error", ECUDA/ENCCL -> std::runtime_error). */
+enum {
+  DCONV_OK = 0,
+  DCONV_EINVAL_SHAPE = 1,  /* ConvShape rules violated (shape.cpp:32-37) */
+  DCONV_ELAYOUT = 2,       /* block sizes / strides inconsistent */
+  DCONV_EPARAM = 3,        /* bad parameter (null pointer, bad epilogue...) */
+  DCONV_ECUDA = 4,         /* a CUDA runtime call failed */
+  DCONV_ENCCL = 5,         /* reserved for the multi-GPU layer */
+  DCONV_EUNSUPPORTED = 6   /* no kernel for this configuration */
+};
+
+/* Fused epilogue applied to the fp32 accumulator before the single store. */
+enum {
+  DCONV_EPI_NONE = 0,
+  DCONV_EPI_RELU = 1,      /* relu_blocked fused */
+  DCONV_EPI_ADD = 2,       /* + skip (same blocked geometry as the output) */
+  DCONV_EPI_ADD_RELU = 3   /* relu(conv + skip): ResNet block tail */
+};
+
+/* Kernel selection. */
+enum {
+  DCONV_ALGO_AUTO = 0,     /* fast FFMA path when c_ib == c_ob == 8, else generic */
+  DCONV_ALGO_FFMA = 1,     /* register-blocked FFMA kernel (c_ib == c_ob == 8) */
+  DCONV_ALGO_GENERIC = 2,  /* any (c_ib, c_ob); slow reference-order kernel */
+  DCONV_ALGO_TF32 = 3      /* tcgen05/TMEM TF32 variant (looser tolerance) */
+};
+
+/* One convolution layer over a batch of blocked feature maps.
+ * Geometry follows ConvShape (shape.hpp:29-45): valid convolution, exact
+ * stride division; h_o/w_o are filled in by dconv_conv_desc_init.
+ * Strides are in floats; 0 selects the dense value:
+ *   *_blk_stride = H*W*c_b, *_img_stride = n_blocks*blk_stride,
+ *   *_row_stride = W*c_b.
+ * Non-dense strides express views: a halo'd (pre-padded) buffer, a crop
+ * (ResNet stride-2 projections) or a C_o-shard of a larger map.  The pointers
+ * passed to the calls point at element (0, 0, 0) of the view. */
+typedef struct dconv_conv_desc {
+  int n, c_i, c_o, h_i, w_i, h_f, w_f, stride;
+  int h_o, w_o;
+  int c_ib, c_ob;
+  int64_t in_img_stride, in_blk_stride, in_row_stride;
+  int64_t out_img_stride, out_blk_stride, out_row_stride;
+  int64_t skip_img_stride, skip_blk_stride, skip_row_stride;
+  int epilogue;            /* DCONV_EPI_* */
+  int algo;                /* DCONV_ALGO_* */
+  int co_block_begin;      /* first output block j' computed (C_o sharding) */
+  int co_block_count;      /* number of output blocks computed; 0 = all */
+} dconv_conv_desc;
+
+/* Fills `d` for a dense layer and validates it like ConvShape's constructor.
+ * Returns DCONV_EINVAL_SHAPE when the reference would throw. */
+int dconv_conv_desc_init(dconv_conv_desc* d, int n, int c_i, int c_o, int h_i,
+                         int w_i, int h_f, int w_f, int stride, int c_ib,
+                         int c_ob);
+
+/* ConvShape validation alone (shape.cpp:30-40). */
+int dconv_conv_shape(int c_i, int c_o, int h_i, int w_i, int h_f, int w_f,
+                     int stride, int* h_o, int* w_o);
+
+/* conv_flops (reference.cpp:106-109) for one image. */
+int64_t dconv_conv_flops(int c_i, int c_o, int h_o, int w_o, int h_f, int w_f);
+
+/* Direct convolution (Alg. 3) on blocked tensors.
+ * in:   blocked input view, c_b == d->c_ib
+ * w:    blocked kernel (c_ob, c_ib), full C_o (sharding selects blocks)
+ * skip: blocked map like the output, read when epilogue has ADD (else NULL)
+ * out:  blocked output view, c_b == d->c_ob.  Every valid element of the
+ *       selected output blocks is written exactly once (no zero-init pass);
+ *       padded channel slots are written as exact 0. */
+int dconv_cuda_conv_direct(const dconv_conv_desc* d, const float* in,
+                           const float* w, const float* skip, float* out,
+                           void* stream);
+
+/* First layer: dense [N][C_i][H_i][W_i] input (the paper does not impose the
+ * blocked layout on network inputs) -> blocked output.
+ * d->c_ib is ignored for the input; the weights must be packed with
+ * c_ib = C_i (one input block holding every channel, no zero padding). */
+int dconv_cuda_conv_first_layer(const dconv_conv_desc* d, const float* in_dense,
+                                int64_t in_img_stride, const float* w,
+                                const float* skip, float* out, void* stream);
+
+/* pack_kernel: dense [C_i][C_o][H_f][W_f] -> blocked.  Bit-exact permutation,
+ * padded slots written 0.  `dst` holds round_up(C_o,c_ob)*round_up(C_i,c_ib)*H_f*W_f. */
+int dconv_cuda_pack_kernel(const float* src, int c_i, int c_o, int h_f, int w_f,
+                           int c_ob, int c_ib, float* dst, void* stream);
+int dconv_cuda_unpack_kernel(const float* src, int c_i, int c_o, int h_f,
+                             int w_f, int c_ob, int c_ib, float* dst,
+                             void* stream);
+
+/* pack_feature_map over n images: dense [n][c][h][w] -> blocked
+ * [n][ceil(c/c_b)][h + 2*halo][w + 2*halo][c_b]; the data lands in the
+ * interior, the halo ring and padded channels are written 0 (halo = 0 gives
+ * the reference layout exactly). */
+int dconv_cuda_pack_feature_map(const float* src, int n, int c, int h, int w,
+                                int c_b, int halo, float* dst, void* stream);
+int dconv_cuda_unpack_feature_map(const float* src, int n, int c, int h, int w,
+                                  int c_b, int halo, float* dst, void* stream);
+
+/* Element-wise / pooling kernels in the blocked layout (count in floats). */
+int dconv_cuda_relu_blocked(float* x, int64_t count, void* stream);
+int dconv_cuda_add_blocked(const float* a, const float* b, float* out,
+                           int64_t count, int relu, void* stream);
+/* 2x2 stride-2 max-pool per image block; writes into an output view with
+ * row stride / block stride / image stride (0 = dense) so it can land in the
+ * interior of the next layer's halo buffer. */
+int dconv_cuda_maxpool2x2_blocked(const float* in, int n, int n_blocks, int h,
+                                  int w, int c_b, float* out,
+                                  int64_t out_img_stride,
+                                  int64_t out_blk_stride,
+                                  int64_t out_row_stride, void* stream);
+
+/* Zeroes a float buffer (halo buffers are zeroed once, outside timing). */
+int dconv_cuda_zero(float* x, int64_t count, void* stream);
+
+/* Launch accounting: number of device kernels this library launched since
+ * load (for bench.py's gpu_launches claim) and the name of the last kernel. */
+int64_t dconv_cuda_launch_count(void);
+
+/* Peak FP32 FFMA throughput probe (TFLOP/s) measured with CUDA events on the
+ * current device: the roofline denominator for the FFMA kernel. */
+double dconv_cuda_fp32_peak_probe(void* stream);
+
+const char* dconv_cuda_strerror(int code);
+const char* dconv_cuda_last_error_detail(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

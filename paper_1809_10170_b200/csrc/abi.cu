@@ -1,0 +1,318 @@
+// abi.cu -- the extern "C" boundary (include/dconv_cuda.h): argument
+// validation with the reference's error semantics, kernel selection, and
+// launch accounting.  No device memory is allocated here.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+#include "conv_kernels.h"
+#include "layout_kernels.h"
+
+namespace {
+thread_local char g_detail[512] = "";
+std::atomic<int64_t> g_launches{0};
+
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+bool aligned16(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+}
+}  // namespace
+
+namespace dconv_host {
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_detail, sizeof(g_detail), fmt, ap);
+  va_end(ap);
+  return code;
+}
+int check_launch(const char* kernel) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    return set_error(DCONV_ECUDA, "%s: %s", kernel, cudaGetErrorString(e));
+  return DCONV_OK;
+}
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace dconv_host
+
+using dconv_host::set_error;
+
+extern "C" {
+
+int dconv_conv_shape(int c_i, int c_o, int h_i, int w_i, int h_f, int w_f,
+                     int s, int* h_o, int* w_o) {
+  // ConvShape::ConvShape, shape.cpp:32-39
+  if (!(c_i >= 1 && c_o >= 1 && h_i >= 1 && w_i >= 1 && h_f >= 1 && w_f >= 1))
+    return set_error(DCONV_EINVAL_SHAPE, "ConvShape: all counts must be >= 1");
+  if (s < 1) return set_error(DCONV_EINVAL_SHAPE, "ConvShape: stride must be >= 1");
+  if (!(h_f <= h_i && w_f <= w_i))
+    return set_error(DCONV_EINVAL_SHAPE,
+                     "ConvShape: filter must fit inside the input");
+  if ((h_i - h_f) % s != 0)
+    return set_error(DCONV_EINVAL_SHAPE,
+                     "ConvShape: (h_i - h_f) must be divisible by stride");
+  if ((w_i - w_f) % s != 0)
+    return set_error(DCONV_EINVAL_SHAPE,
+                     "ConvShape: (w_i - w_f) must be divisible by stride");
+  if (h_o) *h_o = (h_i - h_f) / s + 1;
+  if (w_o) *w_o = (w_i - w_f) / s + 1;
+  return DCONV_OK;
+}
+
+int64_t dconv_conv_flops(int c_i, int c_o, int h_o, int w_o, int h_f, int w_f) {
+  return 2LL * c_i * c_o * h_o * w_o * h_f * w_f;  // reference.cpp:106-109
+}
+
+int dconv_conv_desc_init(dconv_conv_desc* d, int n, int c_i, int c_o, int h_i,
+                         int w_i, int h_f, int w_f, int stride, int c_ib,
+                         int c_ob) {
+  if (!d) return set_error(DCONV_EPARAM, "desc is NULL");
+  std::memset(d, 0, sizeof(*d));
+  if (n < 1) return set_error(DCONV_EINVAL_SHAPE, "batch must be >= 1");
+  if (c_ib < 1 || c_ob < 1)
+    return set_error(DCONV_EPARAM, "block sizes must be >= 1");
+  int h_o = 0, w_o = 0;
+  const int rc = dconv_conv_shape(c_i, c_o, h_i, w_i, h_f, w_f, stride, &h_o, &w_o);
+  if (rc) return rc;
+  d->n = n; d->c_i = c_i; d->c_o = c_o; d->h_i = h_i; d->w_i = w_i;
+  d->h_f = h_f; d->w_f = w_f; d->stride = stride; d->h_o = h_o; d->w_o = w_o;
+  d->c_ib = c_ib; d->c_ob = c_ob;
+  return DCONV_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+struct Resolved {
+  int ib_n, jb_n, jb_begin, jb_count;
+  int64_t in_img, in_blk, in_row, out_img, out_blk, out_row, sk_img, sk_blk,
+      sk_row;
+};
+
+int resolve(const dconv_conv_desc* d, bool dense_input, int64_t dense_img,
+            const void* in, const void* w, const void* skip, const void* out,
+            Resolved* r) {
+  if (!d) return set_error(DCONV_EPARAM, "desc is NULL");
+  if (!in || !w || !out) return set_error(DCONV_EPARAM, "NULL tensor pointer");
+  int h_o = 0, w_o = 0;
+  int rc = dconv_conv_shape(d->c_i, d->c_o, d->h_i, d->w_i, d->h_f, d->w_f,
+                            d->stride, &h_o, &w_o);
+  if (rc) return rc;
+  if (d->n < 1) return set_error(DCONV_EINVAL_SHAPE, "batch must be >= 1");
+  if (h_o != d->h_o || w_o != d->w_o)
+    return set_error(DCONV_EINVAL_SHAPE, "desc h_o/w_o inconsistent with ConvShape");
+  if (d->c_ib < 1 || d->c_ob < 1)
+    return set_error(DCONV_EPARAM, "block sizes must be >= 1");
+  if (d->epilogue < 0 || d->epilogue > 3)
+    return set_error(DCONV_EPARAM, "unknown epilogue %d", d->epilogue);
+  if ((d->epilogue & DCONV_EPI_ADD) && !skip)
+    return set_error(DCONV_EPARAM, "ADD epilogue needs a skip tensor");
+  const int c_ib = dense_input ? d->c_i : d->c_ib;
+  r->ib_n = (d->c_i + c_ib - 1) / c_ib;
+  r->jb_n = (d->c_o + d->c_ob - 1) / d->c_ob;
+  r->jb_begin = d->co_block_begin;
+  r->jb_count = d->co_block_count ? d->co_block_count : r->jb_n - r->jb_begin;
+  if (r->jb_begin < 0 || r->jb_count < 1 || r->jb_begin + r->jb_count > r->jb_n)
+    return set_error(DCONV_EPARAM, "output block range [%d, %d) outside [0, %d)",
+                     r->jb_begin, r->jb_begin + r->jb_count, r->jb_n);
+  if (dense_input) {
+    r->in_row = d->w_i;
+    r->in_blk = (int64_t)d->h_i * d->w_i;  // channel plane
+    r->in_img = dense_img ? dense_img : (int64_t)d->c_i * d->h_i * d->w_i;
+  } else {
+    r->in_row = d->in_row_stride ? d->in_row_stride : (int64_t)d->w_i * d->c_ib;
+    r->in_blk = d->in_blk_stride ? d->in_blk_stride : (int64_t)d->h_i * r->in_row;
+    r->in_img = d->in_img_stride ? d->in_img_stride : (int64_t)r->ib_n * r->in_blk;
+    if (r->in_row < (int64_t)d->w_i * d->c_ib ||
+        r->in_blk < (int64_t)d->h_i * r->in_row)
+      return set_error(DCONV_ELAYOUT, "input view strides smaller than the map");
+  }
+  r->out_row = d->out_row_stride ? d->out_row_stride : (int64_t)d->w_o * d->c_ob;
+  r->out_blk = d->out_blk_stride ? d->out_blk_stride : (int64_t)d->h_o * r->out_row;
+  r->out_img = d->out_img_stride ? d->out_img_stride : (int64_t)r->jb_count * r->out_blk;
+  r->sk_row = d->skip_row_stride ? d->skip_row_stride : (int64_t)d->w_o * d->c_ob;
+  r->sk_blk = d->skip_blk_stride ? d->skip_blk_stride : (int64_t)d->h_o * r->sk_row;
+  r->sk_img = d->skip_img_stride ? d->skip_img_stride : (int64_t)r->jb_count * r->sk_blk;
+  if (r->out_row < (int64_t)d->w_o * d->c_ob || r->out_blk < (int64_t)d->h_o * r->out_row)
+    return set_error(DCONV_ELAYOUT, "output view strides smaller than the map");
+  return DCONV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dconv_cuda_conv_direct(const dconv_conv_desc* d, const float* in,
+                           const float* w, const float* skip, float* out,
+                           void* stream) {
+  Resolved r;
+  int rc = resolve(d, false, 0, in, w, skip, out, &r);
+  if (rc) return rc;
+  const bool ffma_ok =
+      d->c_ib == 8 && d->c_ob == 8 && aligned16(in) && aligned16(w) &&
+      aligned16(out) && (!skip || aligned16(skip)) &&
+      ((r.in_img | r.in_blk | r.in_row | r.out_img | r.out_blk | r.out_row |
+        r.sk_img | r.sk_blk | r.sk_row) & 3) == 0;
+  int algo = d->algo;
+  if (algo == DCONV_ALGO_AUTO) algo = ffma_ok ? DCONV_ALGO_FFMA : DCONV_ALGO_GENERIC;
+  if (algo == DCONV_ALGO_FFMA) {
+    if (!ffma_ok)
+      return set_error(DCONV_EUNSUPPORTED,
+                       "FFMA kernel needs c_ib == c_ob == 8 and 16-byte "
+                       "aligned views (got c_ib=%d c_ob=%d)", d->c_ib, d->c_ob);
+    dconv_dev::FfmaParams p{};
+    p.in = in; p.w = w; p.skip = skip; p.out = out;
+    p.n = d->n; p.h_i = d->h_i; p.w_i = d->w_i; p.h_o = d->h_o; p.w_o = d->w_o;
+    p.h_f = d->h_f; p.w_f = d->w_f; p.s = d->stride;
+    p.ib_n = r.ib_n; p.jb_n = r.jb_n; p.jb_begin = r.jb_begin; p.jb_count = r.jb_count;
+    p.in_img = r.in_img; p.in_blk = r.in_blk; p.in_row = r.in_row;
+    p.out_img = r.out_img; p.out_blk = r.out_blk; p.out_row = r.out_row;
+    p.sk_img = r.sk_img; p.sk_blk = r.sk_blk; p.sk_row = r.sk_row;
+    p.epi = d->epilogue;
+    return dconv_dev::launch_conv_ffma(p, as_stream(stream));
+  }
+  if (algo == DCONV_ALGO_GENERIC) {
+    dconv_dev::GenericParams p{};
+    p.in = in; p.w = w; p.skip = skip; p.out = out;
+    p.n = d->n; p.c_i = d->c_i; p.h_i = d->h_i; p.w_i = d->w_i;
+    p.h_o = d->h_o; p.w_o = d->w_o; p.h_f = d->h_f; p.w_f = d->w_f;
+    p.s = d->stride; p.c_ib = d->c_ib; p.c_ob = d->c_ob;
+    p.ib_n = r.ib_n; p.jb_n = r.jb_n; p.jb_begin = r.jb_begin; p.jb_count = r.jb_count;
+    p.in_img = r.in_img; p.in_blk = r.in_blk; p.in_row = r.in_row;
+    p.out_img = r.out_img; p.out_blk = r.out_blk; p.out_row = r.out_row;
+    p.sk_img = r.sk_img; p.sk_blk = r.sk_blk; p.sk_row = r.sk_row;
+    p.epi = d->epilogue;
+    return dconv_dev::launch_conv_generic(p, as_stream(stream));
+  }
+  return set_error(DCONV_EUNSUPPORTED, "algo %d not available", algo);
+}
+
+int dconv_cuda_conv_first_layer(const dconv_conv_desc* d, const float* in_dense,
+                                int64_t in_img_stride, const float* w,
+                                const float* skip, float* out, void* stream) {
+  Resolved r;
+  int rc = resolve(d, true, in_img_stride, in_dense, w, skip, out, &r);
+  if (rc) return rc;
+  dconv_dev::GenericParams p{};
+  p.in = in_dense; p.w = w; p.skip = skip; p.out = out;
+  p.n = d->n; p.c_i = d->c_i; p.h_i = d->h_i; p.w_i = d->w_i;
+  p.h_o = d->h_o; p.w_o = d->w_o; p.h_f = d->h_f; p.w_f = d->w_f;
+  p.s = d->stride; p.c_ib = d->c_i; p.c_ob = d->c_ob;
+  p.ib_n = 1; p.jb_n = r.jb_n; p.jb_begin = r.jb_begin; p.jb_count = r.jb_count;
+  p.in_img = r.in_img; p.in_blk = r.in_blk; p.in_row = r.in_row;
+  p.out_img = r.out_img; p.out_blk = r.out_blk; p.out_row = r.out_row;
+  p.sk_img = r.sk_img; p.sk_blk = r.sk_blk; p.sk_row = r.sk_row;
+  p.epi = d->epilogue;
+  p.dense_input = 1;
+  return dconv_dev::launch_conv_first_layer(p, as_stream(stream));
+}
+
+int dconv_cuda_pack_kernel(const float* src, int c_i, int c_o, int h_f, int w_f,
+                           int c_ob, int c_ib, float* dst, void* stream) {
+  if (!src || !dst) return set_error(DCONV_EPARAM, "NULL tensor pointer");
+  if (c_i < 1 || c_o < 1 || h_f < 1 || w_f < 1)
+    return set_error(DCONV_EINVAL_SHAPE, "BlockedKernel: dims must be >= 1");
+  if (c_ob < 1 || c_ib < 1)
+    return set_error(DCONV_EPARAM, "BlockedKernel: block sizes must be >= 1");
+  return dconv_dev::launch_pack_kernel(src, c_i, c_o, h_f, w_f, c_ob, c_ib, dst,
+                                       as_stream(stream));
+}
+
+int dconv_cuda_unpack_kernel(const float* src, int c_i, int c_o, int h_f,
+                             int w_f, int c_ob, int c_ib, float* dst,
+                             void* stream) {
+  if (!src || !dst) return set_error(DCONV_EPARAM, "NULL tensor pointer");
+  if (c_i < 1 || c_o < 1 || h_f < 1 || w_f < 1)
+    return set_error(DCONV_EINVAL_SHAPE, "KernelTensor: dims must be >= 1");
+  if (c_ob < 1 || c_ib < 1)
+    return set_error(DCONV_EPARAM, "BlockedKernel: block sizes must be >= 1");
+  return dconv_dev::launch_unpack_kernel(src, c_i, c_o, h_f, w_f, c_ob, c_ib,
+                                         dst, as_stream(stream));
+}
+
+int dconv_cuda_pack_feature_map(const float* src, int n, int c, int h, int w,
+                                int c_b, int halo, float* dst, void* stream) {
+  if (!src || !dst) return set_error(DCONV_EPARAM, "NULL tensor pointer");
+  if (n < 1 || c < 1 || h < 1 || w < 1)
+    return set_error(DCONV_EINVAL_SHAPE, "BlockedFeatureMap: dims must be >= 1");
+  if (c_b < 1) return set_error(DCONV_EPARAM, "BlockedFeatureMap: block size must be >= 1");
+  if (halo < 0) return set_error(DCONV_EPARAM, "halo must be >= 0");
+  return dconv_dev::launch_pack_fm(src, n, c, h, w, c_b, halo, dst,
+                                   as_stream(stream));
+}
+
+int dconv_cuda_unpack_feature_map(const float* src, int n, int c, int h, int w,
+                                  int c_b, int halo, float* dst, void* stream) {
+  if (!src || !dst) return set_error(DCONV_EPARAM, "NULL tensor pointer");
+  if (n < 1 || c < 1 || h < 1 || w < 1)
+    return set_error(DCONV_EINVAL_SHAPE, "FeatureMap: dims must be >= 1");
+  if (c_b < 1) return set_error(DCONV_EPARAM, "BlockedFeatureMap: block size must be >= 1");
+  if (halo < 0) return set_error(DCONV_EPARAM, "halo must be >= 0");
+  return dconv_dev::launch_unpack_fm(src, n, c, h, w, c_b, halo, dst,
+                                     as_stream(stream));
+}
+
+int dconv_cuda_relu_blocked(float* x, int64_t count, void* stream) {
+  if (!x) return set_error(DCONV_EPARAM, "NULL tensor pointer");
+  if (count <= 0) return DCONV_OK;
+  return dconv_dev::launch_relu(x, count, as_stream(stream));
+}
+
+int dconv_cuda_add_blocked(const float* a, const float* b, float* out,
+                           int64_t count, int relu, void* stream) {
+  if (!a || !b || !out) return set_error(DCONV_EPARAM, "NULL tensor pointer");
+  if (count <= 0) return DCONV_OK;
+  return dconv_dev::launch_add(a, b, out, count, relu, as_stream(stream));
+}
+
+int dconv_cuda_maxpool2x2_blocked(const float* in, int n, int n_blocks, int h,
+                                  int w, int c_b, float* out,
+                                  int64_t out_img_stride,
+                                  int64_t out_blk_stride,
+                                  int64_t out_row_stride, void* stream) {
+  if (!in || !out) return set_error(DCONV_EPARAM, "NULL tensor pointer");
+  if (n < 1 || n_blocks < 1 || h < 2 || w < 2 || c_b < 1)
+    return set_error(DCONV_EINVAL_SHAPE, "maxpool2x2: bad dims");
+  const int64_t row = out_row_stride ? out_row_stride : (int64_t)(w / 2) * c_b;
+  const int64_t blk = out_blk_stride ? out_blk_stride : (int64_t)(h / 2) * row;
+  const int64_t img = out_img_stride ? out_img_stride : (int64_t)n_blocks * blk;
+  return dconv_dev::launch_maxpool2x2(in, n, n_blocks, h, w, c_b, out, img, blk,
+                                      row, as_stream(stream));
+}
+
+int dconv_cuda_zero(float* x, int64_t count, void* stream) {
+  if (!x) return set_error(DCONV_EPARAM, "NULL tensor pointer");
+  if (count <= 0) return DCONV_OK;
+  if (cudaMemsetAsync(x, 0, sizeof(float) * count, as_stream(stream)) != cudaSuccess)
+    return dconv_host::check_launch("cudaMemsetAsync");
+  return DCONV_OK;
+}
+
+int64_t dconv_cuda_launch_count(void) {
+  return g_launches.load(std::memory_order_relaxed);
+}
+
+double dconv_cuda_fp32_peak_probe(void* stream) {
+  return dconv_dev::fp32_peak_probe(as_stream(stream));
+}
+
+const char* dconv_cuda_strerror(int code) {
+  switch (code) {
+    case DCONV_OK: return "ok";
+    case DCONV_EINVAL_SHAPE: return "invalid shape";
+    case DCONV_ELAYOUT: return "layout error";
+    case DCONV_EPARAM: return "parameter error";
+    case DCONV_ECUDA: return "CUDA error";
+    case DCONV_ENCCL: return "NCCL error";
+    case DCONV_EUNSUPPORTED: return "unsupported configuration";
+    default: return "unknown error";
+  }
+}
+
+const char* dconv_cuda_last_error_detail(void) { return g_detail; }
+
+}  // extern "C"

@@ -1,0 +1,50 @@
+// conv_kernels.h -- internal launcher interfaces between the C-ABI layer
+// (abi.cu) and the kernels.  Not part of the public boundary.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dconv_dev {
+
+// Parameters of the FFMA direct-conv kernel (c_ib = c_ob = 8).  All strides
+// in floats.  Tiling / staging fields are filled in by the launcher.
+struct FfmaParams {
+  const float* in;
+  const float* w;
+  const float* skip;
+  float* out;
+  int n, h_i, w_i, h_o, w_o, h_f, w_f, s;
+  int ib_n;                 // input channel blocks (padded C_i / 8)
+  int jb_n;                 // output channel blocks in the weights
+  int jb_begin, jb_count;   // output blocks computed
+  int64_t in_img, in_blk, in_row;
+  int64_t out_img, out_blk, out_row;
+  int64_t sk_img, sk_blk, sk_row;
+  int epi;
+  // launcher-filled
+  int TH, TW, tiles_x, tiles_per_img;
+  int G, R, n_g, n_r, PH, PW;
+  int slab_floats, patch_floats, wstride_floats, stage_floats, NS;
+};
+
+int launch_conv_ffma(const FfmaParams& p, cudaStream_t stream);
+
+// Generic (any c_ib / c_ob) reference-order kernel and the first-layer reader.
+struct GenericParams {
+  const float* in;
+  const float* w;
+  const float* skip;
+  float* out;
+  int n, c_i, h_i, w_i, h_o, w_o, h_f, w_f, s, c_ib, c_ob;
+  int ib_n, jb_n, jb_begin, jb_count;
+  int64_t in_img, in_blk, in_row;    // for dense input: in_blk = H*W, in_row = W
+  int64_t out_img, out_blk, out_row;
+  int64_t sk_img, sk_blk, sk_row;
+  int epi;
+  int dense_input;                   // 1: first layer, input [N][C_i][H][W]
+};
+
+int launch_conv_generic(const GenericParams& p, cudaStream_t stream);
+int launch_conv_first_layer(const GenericParams& p, cudaStream_t stream);
+
+}  // namespace dconv_dev

@@ -1,0 +1,234 @@
+// layout.cu -- layout transforms and element-wise / pooling kernels in the
+// blocked layout.  All are HBM-bound; each thread owns one (or four, vector)
+// destination elements so stores are fully coalesced.
+//
+//   pack_kernel_dev   <- pack_kernel        tensor.cpp:85-95  (bit-exact)
+//   unpack_kernel_dev <- unpack_kernel      tensor.cpp:97-108
+//   pack_fm_dev       <- pack_feature_map   tensor.cpp:65-73  (+ optional halo)
+//   unpack_fm_dev     <- unpack_feature_map tensor.cpp:75-83
+//   relu / add        <- relu_blocked SPEC.md:326-334, skip layer PAPER.md:4-7
+//   maxpool2x2        <- subsampling layer PAPER.md:9-10
+#include "common.cuh"
+#include "layout_kernels.h"
+
+namespace dconv_dev {
+
+namespace {
+
+int grid_for(int64_t total, int per_thread = 1) {
+  int64_t blocks = (total / per_thread + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  if (blocks < 1) blocks = 1;
+  return (int)blocks;
+}
+
+#define GRID_STRIDE(e, total)                                            \
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (total); \
+       e += (int64_t)gridDim.x * blockDim.x)
+
+__global__ void pack_kernel_dev(const float* __restrict__ src, int c_i, int c_o,
+                                int h_f, int w_f, int c_ob, int c_ib,
+                                int ib_n, int64_t total,
+                                float* __restrict__ dst) {
+  GRID_STRIDE(e, total) {
+    int64_t t = e;
+    const int jj = (int)(t % c_ob); t /= c_ob;
+    const int ii = (int)(t % c_ib); t /= c_ib;
+    const int m = (int)(t % w_f); t /= w_f;
+    const int n = (int)(t % h_f); t /= h_f;
+    const int ib = (int)(t % ib_n); t /= ib_n;
+    const int jb = (int)t;
+    const int i = ib * c_ib + ii, j = jb * c_ob + jj;
+    dst[e] = (i < c_i && j < c_o)
+                 ? src[(((int64_t)i * c_o + j) * h_f + n) * w_f + m]
+                 : 0.0f;
+  }
+}
+
+__global__ void unpack_kernel_dev(const float* __restrict__ src, int c_i,
+                                  int c_o, int h_f, int w_f, int c_ob, int c_ib,
+                                  int ib_n, int64_t total,
+                                  float* __restrict__ dst) {
+  GRID_STRIDE(e, total) {
+    int64_t t = e;
+    const int m = (int)(t % w_f); t /= w_f;
+    const int n = (int)(t % h_f); t /= h_f;
+    const int j = (int)(t % c_o); t /= c_o;
+    const int i = (int)t;
+    dst[e] = src[(((((int64_t)(j / c_ob) * ib_n + i / c_ib) * h_f + n) * w_f +
+                   m) * c_ib + i % c_ib) * c_ob + j % c_ob];
+  }
+}
+
+__global__ void pack_fm_dev(const float* __restrict__ src, int c, int h, int w,
+                            int c_b, int halo, int nb, int64_t total,
+                            float* __restrict__ dst) {
+  const int hp = h + 2 * halo, wp = w + 2 * halo;
+  GRID_STRIDE(e, total) {
+    int64_t t = e;
+    const int cc = (int)(t % c_b); t /= c_b;
+    const int xp = (int)(t % wp); t /= wp;
+    const int yp = (int)(t % hp); t /= hp;
+    const int b = (int)(t % nb); t /= nb;
+    const int img = (int)t;
+    const int ch = b * c_b + cc, y = yp - halo, x = xp - halo;
+    dst[e] = (ch < c && y >= 0 && y < h && x >= 0 && x < w)
+                 ? src[(((int64_t)img * c + ch) * h + y) * w + x]
+                 : 0.0f;
+  }
+}
+
+__global__ void unpack_fm_dev(const float* __restrict__ src, int c, int h,
+                              int w, int c_b, int halo, int nb, int64_t total,
+                              float* __restrict__ dst) {
+  const int hp = h + 2 * halo, wp = w + 2 * halo;
+  GRID_STRIDE(e, total) {
+    int64_t t = e;
+    const int x = (int)(t % w); t /= w;
+    const int y = (int)(t % h); t /= h;
+    const int ch = (int)(t % c); t /= c;
+    const int img = (int)t;
+    dst[e] = src[((((int64_t)img * nb + ch / c_b) * hp + y + halo) * wp + x +
+                  halo) * c_b + ch % c_b];
+  }
+}
+
+__global__ void relu4_dev(float4* x, int64_t n4) {
+  GRID_STRIDE(e, n4) {
+    float4 v = x[e];
+    v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f);
+    v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
+    x[e] = v;
+  }
+}
+
+__global__ void relu1_dev(float* x, int64_t n) {
+  GRID_STRIDE(e, n) x[e] = fmaxf(x[e], 0.f);
+}
+
+__global__ void add4_dev(const float4* a, const float4* b, float4* o,
+                         int64_t n4, int relu) {
+  GRID_STRIDE(e, n4) {
+    const float4 u = a[e], v = b[e];
+    float4 r = make_float4(u.x + v.x, u.y + v.y, u.z + v.z, u.w + v.w);
+    if (relu) {
+      r.x = fmaxf(r.x, 0.f); r.y = fmaxf(r.y, 0.f);
+      r.z = fmaxf(r.z, 0.f); r.w = fmaxf(r.w, 0.f);
+    }
+    o[e] = r;
+  }
+}
+
+__global__ void add1_dev(const float* a, const float* b, float* o, int64_t n,
+                         int relu) {
+  GRID_STRIDE(e, n) {
+    const float r = a[e] + b[e];
+    o[e] = relu ? fmaxf(r, 0.f) : r;
+  }
+}
+
+// one thread per output element of [img][blk][ho][wo][c_b]
+__global__ void maxpool2x2_dev(const float* __restrict__ in, int n_blocks,
+                               int h, int w, int c_b, int64_t total,
+                               float* __restrict__ out, int64_t o_img,
+                               int64_t o_blk, int64_t o_row) {
+  const int ho = h / 2, wo = w / 2;
+  GRID_STRIDE(e, total) {
+    int64_t t = e;
+    const int cc = (int)(t % c_b); t /= c_b;
+    const int x = (int)(t % wo); t /= wo;
+    const int y = (int)(t % ho); t /= ho;
+    const int b = (int)(t % n_blocks); t /= n_blocks;
+    const int img = (int)t;
+    const float* p =
+        in + ((((int64_t)img * n_blocks + b) * h + 2 * y) * w + 2 * x) * c_b + cc;
+    float v = p[0];
+    v = fmaxf(v, p[c_b]);
+    v = fmaxf(v, p[(int64_t)w * c_b]);
+    v = fmaxf(v, p[(int64_t)w * c_b + c_b]);
+    out[(int64_t)img * o_img + (int64_t)b * o_blk + (int64_t)y * o_row +
+        (int64_t)x * c_b + cc] = v;
+  }
+}
+
+}  // namespace
+
+int launch_pack_kernel(const float* src, int c_i, int c_o, int h_f, int w_f,
+                       int c_ob, int c_ib, float* dst, cudaStream_t st) {
+  const int ib_n = (c_i + c_ib - 1) / c_ib, jb_n = (c_o + c_ob - 1) / c_ob;
+  const int64_t total = (int64_t)jb_n * ib_n * h_f * w_f * c_ib * c_ob;
+  pack_kernel_dev<<<grid_for(total), 256, 0, st>>>(src, c_i, c_o, h_f, w_f,
+                                                   c_ob, c_ib, ib_n, total, dst);
+  dconv_host::count_launch();
+  return dconv_host::check_launch("pack_kernel_dev");
+}
+
+int launch_unpack_kernel(const float* src, int c_i, int c_o, int h_f, int w_f,
+                         int c_ob, int c_ib, float* dst, cudaStream_t st) {
+  const int ib_n = (c_i + c_ib - 1) / c_ib;
+  const int64_t total = (int64_t)c_i * c_o * h_f * w_f;
+  unpack_kernel_dev<<<grid_for(total), 256, 0, st>>>(
+      src, c_i, c_o, h_f, w_f, c_ob, c_ib, ib_n, total, dst);
+  dconv_host::count_launch();
+  return dconv_host::check_launch("unpack_kernel_dev");
+}
+
+int launch_pack_fm(const float* src, int n, int c, int h, int w, int c_b,
+                   int halo, float* dst, cudaStream_t st) {
+  const int nb = (c + c_b - 1) / c_b;
+  const int64_t total =
+      (int64_t)n * nb * (h + 2 * halo) * (w + 2 * halo) * c_b;
+  pack_fm_dev<<<grid_for(total), 256, 0, st>>>(src, c, h, w, c_b, halo, nb,
+                                               total, dst);
+  dconv_host::count_launch();
+  return dconv_host::check_launch("pack_fm_dev");
+}
+
+int launch_unpack_fm(const float* src, int n, int c, int h, int w, int c_b,
+                     int halo, float* dst, cudaStream_t st) {
+  const int nb = (c + c_b - 1) / c_b;
+  const int64_t total = (int64_t)n * c * h * w;
+  unpack_fm_dev<<<grid_for(total), 256, 0, st>>>(src, c, h, w, c_b, halo, nb,
+                                                 total, dst);
+  dconv_host::count_launch();
+  return dconv_host::check_launch("unpack_fm_dev");
+}
+
+int launch_relu(float* x, int64_t count, cudaStream_t st) {
+  if (count % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+    relu4_dev<<<grid_for(count / 4), 256, 0, st>>>(
+        reinterpret_cast<float4*>(x), count / 4);
+  } else {
+    relu1_dev<<<grid_for(count), 256, 0, st>>>(x, count);
+  }
+  dconv_host::count_launch();
+  return dconv_host::check_launch("relu_dev");
+}
+
+int launch_add(const float* a, const float* b, float* o, int64_t count,
+               int relu, cudaStream_t st) {
+  const bool vec = count % 4 == 0 &&
+                   ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) |
+                     reinterpret_cast<uintptr_t>(o)) & 15) == 0;
+  if (vec)
+    add4_dev<<<grid_for(count / 4), 256, 0, st>>>(
+        reinterpret_cast<const float4*>(a), reinterpret_cast<const float4*>(b),
+        reinterpret_cast<float4*>(o), count / 4, relu);
+  else
+    add1_dev<<<grid_for(count), 256, 0, st>>>(a, b, o, count, relu);
+  dconv_host::count_launch();
+  return dconv_host::check_launch("add_dev");
+}
+
+int launch_maxpool2x2(const float* in, int n, int n_blocks, int h, int w,
+                      int c_b, float* out, int64_t o_img, int64_t o_blk,
+                      int64_t o_row, cudaStream_t st) {
+  const int64_t total = (int64_t)n * n_blocks * (h / 2) * (w / 2) * c_b;
+  maxpool2x2_dev<<<grid_for(total), 256, 0, st>>>(in, n_blocks, h, w, c_b,
+                                                  total, out, o_img, o_blk,
+                                                  o_row);
+  dconv_host::count_launch();
+  return dconv_host::check_launch("maxpool2x2_dev");
+}
+
+}  // namespace dconv_dev

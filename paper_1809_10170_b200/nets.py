@@ -1,0 +1,407 @@
+"""Layer catalogs of the BASELINE.json configs and the zero-reshape chain
+executor (``layer_chain``, widened with halo'd buffers,
+fused ReLU / skip-add epilogues and max-pool).
+
+Every activation lives in the blocked layout with c_b = 8 from the first
+layer's output to the network output: the only layout transform in a network
+is the first-layer *reader* (which consumes the dense image directly, no pack).
+"Pre-padded" inputs (BASELINE.json) are halo'd buffers: a producer writes its
+output into the interior of the consumer's buffer through the C-ABI's view
+strides, and the halo ring is zeroed once at allocation, outside any timing.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Tuple
+
+import torch
+
+from . import _abi
+from ._abi import check, lib, ptr, stream_ptr
+
+CB = 8  # channel block of every activation and weight in the networks
+
+
+@dataclass(frozen=True)
+class Layer:
+    """One conv layer: ConvShape fields (shape.hpp:29-45) + its role."""
+    name: str
+    c_i: int
+    c_o: int
+    h_i: int
+    w_i: int
+    h_f: int
+    w_f: int
+    s: int = 1
+    first: bool = False  # reads the dense network input (first-layer reader)
+
+    @property
+    def h_o(self) -> int:
+        return (self.h_i - self.h_f) // self.s + 1
+
+    @property
+    def w_o(self) -> int:
+        return (self.w_i - self.w_f) // self.s + 1
+
+    @property
+    def flops(self) -> int:  # conv_flops, reference.cpp:106-109 (one image)
+        return 2 * self.c_i * self.c_o * self.h_o * self.w_o * self.h_f * self.w_f
+
+    def in_bytes(self) -> int:
+        return 4 * self.c_i * self.h_i * self.w_i
+
+    def out_bytes(self) -> int:
+        return 4 * self.c_o * self.h_o * self.w_o
+
+    def w_bytes(self) -> int:
+        return 4 * self.c_i * self.c_o * self.h_f * self.w_f
+
+
+CFG1 = [Layer("cfg1", 64, 64, 58, 58, 3, 3, 1)]
+
+ALEXNET = [
+    Layer("conv1", 3, 96, 227, 227, 11, 11, 4, first=True),
+    Layer("conv2", 96, 256, 31, 31, 5, 5, 1),
+    Layer("conv3", 256, 384, 15, 15, 3, 3, 1),
+    Layer("conv4", 384, 384, 15, 15, 3, 3, 1),
+    Layer("conv5", 384, 256, 15, 15, 3, 3, 1),
+]
+
+VGG16 = [
+    Layer("conv1_1", 3, 64, 226, 226, 3, 3, 1, first=True),
+    Layer("conv1_2", 64, 64, 226, 226, 3, 3, 1),
+    Layer("conv2_1", 64, 128, 114, 114, 3, 3, 1),
+    Layer("conv2_2", 128, 128, 114, 114, 3, 3, 1),
+    Layer("conv3_1", 128, 256, 58, 58, 3, 3, 1),
+    Layer("conv3_2", 256, 256, 58, 58, 3, 3, 1),
+    Layer("conv3_3", 256, 256, 58, 58, 3, 3, 1),
+    Layer("conv4_1", 256, 512, 30, 30, 3, 3, 1),
+    Layer("conv4_2", 512, 512, 30, 30, 3, 3, 1),
+    Layer("conv4_3", 512, 512, 30, 30, 3, 3, 1),
+    Layer("conv5_1", 512, 512, 16, 16, 3, 3, 1),
+    Layer("conv5_2", 512, 512, 16, 16, 3, 3, 1),
+    Layer("conv5_3", 512, 512, 16, 16, 3, 3, 1),
+]
+# a 2x2/s2 max-pool follows these VGG layers (224->112->56->28->14)
+VGG16_POOL_AFTER = {"conv1_2", "conv2_2", "conv3_3", "conv4_3"}
+
+GOOGLENET = [
+    Layer("conv1_7x7_s2", 3, 64, 229, 229, 7, 7, 2, first=True),
+    Layer("inc3a_1x1", 192, 64, 28, 28, 1, 1, 1),
+    Layer("inc3a_3x3", 96, 128, 30, 30, 3, 3, 1),
+    Layer("inc3a_5x5", 16, 32, 32, 32, 5, 5, 1),
+    Layer("inc4a_1x1", 480, 192, 14, 14, 1, 1, 1),
+    Layer("inc4a_3x3", 112, 224, 16, 16, 3, 3, 1),
+]
+
+
+def resnet50_layers() -> List[Tuple[str, Layer]]:
+    """ResNet-50 v1.5-style topology (stride on the 3x3; projection shortcut
+    on the first block of each stage).  Stem input 229 instead of BASELINE's
+    230: (230 - 7) % 2 != 0 is rejected by ConvShape (shape.cpp:36)."""
+    out = [("stem", Layer("stem", 3, 64, 229, 229, 7, 7, 2, first=True))]
+    spatial, c_in = 56, 64
+    for stage, (mid, blocks) in enumerate(((64, 3), (128, 4), (256, 6), (512, 3))):
+        c_out = mid * 4
+        for b in range(blocks):
+            stride = 2 if (b == 0 and stage > 0) else 1
+            h_in = spatial
+            h_mid = h_in // stride
+            tag = f"s{stage + 1}b{b + 1}"
+            out.append((tag, Layer(f"{tag}_c1", c_in, mid, h_in, h_in, 1, 1, 1)))
+            if stride == 1:
+                out.append((tag, Layer(f"{tag}_c2", mid, mid, h_in + 2, h_in + 2, 3, 3, 1)))
+            else:
+                out.append((tag, Layer(f"{tag}_c2", mid, mid, h_in + 1, h_in + 1, 3, 3, 2)))
+            out.append((tag, Layer(f"{tag}_c3", mid, c_out, h_mid, h_mid, 1, 1, 1)))
+            if b == 0:
+                crop = h_in - 1 if stride == 2 else h_in
+                out.append((tag, Layer(f"{tag}_proj", c_in, c_out, crop, crop, 1, 1, stride)))
+            c_in = c_out
+            spatial = h_mid
+    return out
+
+
+CONFIGS: Dict[str, List[Layer]] = {
+    "cfg1": CFG1,
+    "alexnet": ALEXNET,
+    "vgg16": VGG16,
+    "googlenet": GOOGLENET,
+    "resnet50": [l for _, l in resnet50_layers()],
+}
+
+
+def network_flops(layers: List[Layer]) -> int:
+    return sum(l.flops for l in layers)
+
+
+# ---------------------------------------------------------------- execution
+def _desc(l: Layer, n: int, epilogue: int = 0) -> _abi.ConvDesc:
+    d = _abi.ConvDesc()
+    check(lib().dconv_conv_desc_init(ctypes.byref(d), n, l.c_i, l.c_o, l.h_i, l.w_i,
+                                     l.h_f, l.w_f, l.s, CB, CB))
+    d.epilogue = epilogue
+    return d
+
+
+def nblk(c: int) -> int:
+    return (c + CB - 1) // CB
+
+
+class Act:
+    """A blocked activation buffer [n][nblk][H+2h][W+2h][8] with a view of its
+    interior (offset and strides in floats)."""
+
+    def __init__(self, n: int, c: int, h: int, w: int, halo: int = 0,
+                 pad_hi_only: bool = False, device="cuda"):
+        self.n, self.c, self.h, self.w, self.halo = n, c, h, w, halo
+        # pad_hi_only: halo on top/left only (ResNet stride-2 "pad 1/0")
+        hp = h + (halo if pad_hi_only else 2 * halo)
+        wp = w + (halo if pad_hi_only else 2 * halo)
+        self.hp, self.wp = hp, wp
+        self.buf = torch.zeros((n, nblk(c), hp, wp, CB), dtype=torch.float32, device=device)
+        self.row = wp * CB
+        self.blk = hp * self.row
+        self.img = nblk(c) * self.blk
+        self.off = (halo * wp + halo) * CB
+
+    def base(self) -> int:
+        """Interior element (0, 0, 0): where a producer writes."""
+        return self.buf.data_ptr() + 4 * self.off
+
+    def full_view(self):
+        """(ptr, img, blk, row) of the whole halo'd buffer: what a consumer
+        conv reads (its h_i/w_i include the halo)."""
+        return (self.buf.data_ptr(), self.img, self.blk, self.row)
+
+    def interior(self) -> torch.Tensor:
+        return self.buf[:, :, self.halo:self.halo + self.h, self.halo:self.halo + self.w, :]
+
+
+def conv(l: Layer, n: int, x: "Act|torch.Tensor", w: torch.Tensor, out: Act,
+         epilogue: int = 0, skip: Optional[Act] = None, stream=None,
+         in_view: Optional[Tuple[int, int, int, int]] = None) -> None:
+    """Launch one conv layer through the C-ABI.  ``x`` is an Act (blocked) or,
+    for a first layer, the dense [n][c][h][w] network input.  ``in_view``
+    optionally overrides (ptr, img, blk, row) of the blocked input (crops)."""
+    d = _desc(l, n, epilogue)
+    d.out_img_stride, d.out_blk_stride, d.out_row_stride = out.img, out.blk, out.row
+    sp = 0
+    if skip is not None:
+        d.skip_img_stride, d.skip_blk_stride, d.skip_row_stride = skip.img, skip.blk, skip.row
+        sp = skip.base()
+    st = stream_ptr(stream)
+    if l.first:
+        check(lib().dconv_cuda_conv_first_layer(ctypes.byref(d), ptr(x), 0, ptr(w), sp,
+                                                out.base(), st))
+        return
+    if in_view is None:
+        in_view = x.full_view()
+    d.in_img_stride, d.in_blk_stride, d.in_row_stride = in_view[1:]
+    check(lib().dconv_cuda_conv_direct(ctypes.byref(d), in_view[0], ptr(w), sp,
+                                       out.base(), st))
+
+
+def maxpool_into(x: Act, out: Act, stream=None) -> None:
+    check(lib().dconv_cuda_maxpool2x2_blocked(x.base(), x.n, nblk(x.c), x.h, x.w, CB,
+                                              out.base(), out.img, out.blk, out.row,
+                                              stream_ptr(stream)))
+
+
+def pack_weights(dense: torch.Tensor, first: bool, stream=None) -> torch.Tensor:
+    """Dense [c_i][c_o][h_f][w_f] -> blocked (c_ob = 8; c_ib = 8, or c_i for
+    a first layer).  The one-time repack kernel (tensor.cpp:85-95)."""
+    ci, co, hf, wf = dense.shape
+    cib = ci if first else CB
+    out = torch.empty((nblk(co), (ci + cib - 1) // cib, hf, wf, cib, CB),
+                      dtype=torch.float32, device=dense.device)
+    check(lib().dconv_cuda_pack_kernel(ptr(dense.contiguous()), ci, co, hf, wf, CB, cib,
+                                       ptr(out), stream_ptr(stream)))
+    return out
+
+
+@dataclass
+class Step:
+    """One launch of a plan: a conv layer (kind 'conv' / 'first') or a
+    layout-preserving op ('pool')."""
+    fn: object
+    name: str
+    kind: str
+    flops: int = 0      # algorithmic FLOPs of this launch (conv_flops x n)
+    layer: Optional[Layer] = None
+
+
+@dataclass
+class Plan:
+    """A network instantiated on one device: weights, activations, and the
+    ordered launch list.  ``run()`` is one step (one pass over the batch)."""
+    name: str
+    n: int
+    layers: List[Layer]
+    weights: Dict[str, torch.Tensor] = field(default_factory=dict)
+    steps: List = field(default_factory=list)
+    input: Optional[torch.Tensor] = None   # dense network input (first layer)
+    output: Optional[Act] = None
+    per_layer_inputs: Dict[str, Act] = field(default_factory=dict)
+    outputs: Dict[str, Act] = field(default_factory=dict)
+
+    @property
+    def flops(self) -> int:
+        return self.n * network_flops(self.layers)
+
+    def run(self, stream=None) -> None:
+        for st in self.steps:
+            st.fn(stream)
+
+    def io_inputs(self) -> List[torch.Tensor]:
+        """Device tensors that are the step's inputs (network input, or every
+        layer's own input for the independent-layer configs)."""
+        ins = [self.input] if self.input is not None else []
+        return ins + [a.buf for a in self.per_layer_inputs.values()]
+
+    def io_outputs(self) -> List[torch.Tensor]:
+        if self.per_layer_inputs:
+            return [a.buf for a in self.outputs.values()]
+        return [self.output.buf]
+
+    def add_conv(self, l: Layer, fn) -> None:
+        self.steps.append(Step(fn, l.name, "first" if l.first else "conv",
+                               self.n * l.flops, l))
+
+    def add_op(self, name: str, fn) -> None:
+        self.steps.append(Step(fn, name, "pool"))
+
+
+def _fill(t: torch.Tensor, seed: int, stream_id: int, scale: float = 1.0) -> None:
+    """Seeded uniform[-1,1) on the device, same counter-based generator as
+    the CPU checker (oracle/oracle.c) so CPU and GPU inputs agree."""
+    from .synth import fill_uniform_
+    fill_uniform_(t, seed, stream_id, scale)
+
+
+def build_plan(config: str, n: int, seed: int = 1809, device="cuda",
+               dense_weights: Optional[Dict[str, torch.Tensor]] = None) -> Plan:
+    """Instantiates a BASELINE.json config on the current device."""
+    layers = CONFIGS[config]
+    p = Plan(config, n, list(layers))
+    for idx, l in enumerate(layers):
+        wd = dense_weights[l.name] if dense_weights else None
+        if wd is None:
+            wd = torch.empty((l.c_i, l.c_o, l.h_f, l.w_f), dtype=torch.float32, device=device)
+            scale = 1.0
+            if config == "resnet50":  # keep 53 unnormalised layers finite: sqrt(3/K)
+                scale = (3.0 / (l.c_i * l.h_f * l.w_f)) ** 0.5
+            _fill(wd, seed, 1000 + 2 * idx, scale)
+        p.weights[l.name] = pack_weights(wd, l.first)
+    if config in ("vgg16",):
+        _build_vgg(p, device, seed)
+    elif config == "resnet50":
+        _build_resnet(p, device, seed)
+    else:
+        _build_independent(p, device, seed)
+    return p
+
+
+def _build_independent(p: Plan, device, seed: int) -> None:
+    """AlexNet / GoogLeNet / cfg1: every layer on its own seeded input (the
+    configs give pre-padded per-layer input sizes)."""
+    for idx, l in enumerate(p.layers):
+        if l.first:
+            x = torch.empty((p.n, l.c_i, l.h_i, l.w_i), dtype=torch.float32, device=device)
+            _fill(x, seed, 2 * idx)
+            p.input = x
+        else:
+            x = Act(p.n, l.c_i, l.h_i, l.w_i, device=device)
+            _fill(x.buf, seed, 2 * idx)
+            _zero_pad_channels(x, l.c_i)
+            p.per_layer_inputs[l.name] = x
+        y = Act(p.n, l.c_o, l.h_o, l.w_o, device=device)
+        p.outputs[l.name] = y
+        w = p.weights[l.name]
+        p.add_conv(l, lambda st, l=l, x=x, w=w, y=y: conv(l, p.n, x, w, y, stream=st))
+    p.output = p.outputs[p.layers[-1].name]
+
+
+def _zero_pad_channels(a: Act, c: int) -> None:
+    if c % CB:
+        a.buf[:, -1, :, :, c % CB:] = 0.0
+
+
+def _build_vgg(p: Plan, device, seed: int) -> None:
+    """VGG-16: conv+ReLU chain; each conv writes into the interior of the next
+    conv's halo buffer (pad 1), pooling writes into the next halo buffer."""
+    layers = p.layers
+    x0 = torch.empty((p.n, 3, 226, 226), dtype=torch.float32, device=device)
+    _fill(x0, seed, 0)
+    # VGG's zero padding of the image: the 224x224 image sits in a 226 ring
+    x0[:, :, 0, :] = 0; x0[:, :, -1, :] = 0; x0[:, :, :, 0] = 0; x0[:, :, :, -1] = 0
+    p.input = x0
+    cur = x0
+    for i, l in enumerate(layers):
+        last = i == len(layers) - 1
+        pool = l.name in VGG16_POOL_AFTER
+        if last:
+            y = Act(p.n, l.c_o, l.h_o, l.w_o, device=device)
+        elif pool:
+            y = Act(p.n, l.c_o, l.h_o, l.w_o, device=device)
+        else:
+            y = Act(p.n, l.c_o, l.h_o, l.w_o, halo=1, device=device)
+        w = p.weights[l.name]
+        p.add_conv(l, lambda st, l=l, x=cur, w=w, y=y:
+                   conv(l, p.n, x, w, y, epilogue=_abi.EPI_RELU, stream=st))
+        p.outputs[l.name] = y
+        if pool:
+            z = Act(p.n, l.c_o, l.h_o // 2, l.w_o // 2, halo=1, device=device)
+            p.add_op(f"pool_{l.name}", lambda st, y=y, z=z: maxpool_into(y, z, st))
+            cur = z
+        else:
+            cur = y
+    p.output = cur
+
+
+def _build_resnet(p: Plan, device, seed: int) -> None:
+    """ResNet-50 chain: stem conv+ReLU -> 2x2 max-pool -> 16 bottlenecks with
+    the skip-add + ReLU fused into the third conv's epilogue."""
+    named = resnet50_layers()
+    stem = named[0][1]
+    x0 = torch.empty((p.n, 3, 229, 229), dtype=torch.float32, device=device)
+    _fill(x0, seed, 0)
+    p.input = x0
+    s_out = Act(p.n, 64, 112, 112, device=device)
+    w = p.weights["stem"]
+    p.add_conv(stem, lambda st: conv(stem, p.n, x0, w, s_out, epilogue=_abi.EPI_RELU, stream=st))
+    x = Act(p.n, 64, 56, 56, device=device)
+    p.add_op("pool_stem", lambda st: maxpool_into(s_out, x, st))
+    p.outputs["stem"] = s_out
+    blocks: Dict[str, List[Layer]] = {}
+    for tag, l in named[1:]:
+        blocks.setdefault(tag, []).append(l)
+    for tag, ls in blocks.items():
+        c1, c2, c3 = ls[0], ls[1], ls[2]
+        proj = ls[3] if len(ls) > 3 else None
+        if c2.s == 1:
+            mid1 = Act(p.n, c1.c_o, c1.h_o, c1.w_o, halo=1, device=device)
+        else:
+            mid1 = Act(p.n, c1.c_o, c1.h_o, c1.w_o, halo=1, pad_hi_only=True, device=device)
+        mid2 = Act(p.n, c2.c_o, c2.h_o, c2.w_o, device=device)
+        y = Act(p.n, c3.c_o, c3.h_o, c3.w_o, device=device)
+        p.add_conv(c1, lambda st, l=c1, x=x, m=mid1:
+                   conv(l, p.n, x, p.weights[l.name], m, epilogue=_abi.EPI_RELU, stream=st))
+        p.add_conv(c2, lambda st, l=c2, m=mid1, m2=mid2:
+                   conv(l, p.n, m, p.weights[l.name], m2, epilogue=_abi.EPI_RELU, stream=st))
+        if proj is not None:
+            sc = Act(p.n, proj.c_o, proj.h_o, proj.w_o, device=device)
+            # 1x1 s2 projection reads the 55x55 (or full) crop of x: a view
+            p.add_conv(proj, lambda st, l=proj, x=x, sc=sc:
+                       conv(l, p.n, x, p.weights[l.name], sc, stream=st,
+                            in_view=x.full_view()))
+            skip = sc
+        else:
+            skip = x
+        p.add_conv(c3, lambda st, l=c3, m2=mid2, y=y, sk=skip:
+                   conv(l, p.n, m2, p.weights[l.name], y,
+                        epilogue=_abi.EPI_ADD_RELU, skip=sk, stream=st))
+        p.outputs[tag] = y
+        x = y
+    p.output = x

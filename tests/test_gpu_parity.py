@@ -1,0 +1,310 @@
+"""GPU parity: every CUDA kernel of libdconv_b200.so, called through the
+C-ABI, against the CPU oracle (oracle/, pinned to the reference by
+tests/test_oracle.py) on identical seeded inputs.
+
+Tolerance (BASELINE.json north_star): fp32 direct conv
+|a - b| <= 1e-4 + 1e-5*|b| per element against conv_oracle64
+(reference.cpp:70-87); layout repacks, ReLU, skip-add and max-pool bit-exact.
+"""
+import zlib
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import pyoracle as po
+
+pytestmark = pytest.mark.gpu
+
+ATOL, RTOL = 1e-4, 1e-5
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1809_10170_b200._abi as abi
+    abi.lib()  # loud failure if the extension is missing
+    yield
+
+
+def dev(a: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t: torch.Tensor) -> np.ndarray:
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def assert_tol(got, want, what=""):
+    ok, nbad, err = po.within_tol(got, want, ATOL, RTOL)
+    assert ok, f"{what}: {nbad} elements out of tolerance, max abs err {err:.3g}"
+
+
+# ------------------------------------------------------------------ helpers
+from paper_1809_10170_b200 import dconv as D  # noqa: E402
+from paper_1809_10170_b200 import _abi, nets  # noqa: E402
+
+
+def run_conv(x, k, s, c_ib, c_ob, algo=_abi.ALGO_AUTO, relu=False, skip=None):
+    """dense numpy x [c][h][w], k [ci][co][hf][wf] -> blocked numpy output."""
+    ci, hi, wi = x.shape
+    _, co, hf, wf = k.shape
+    shape = D.ConvShape(ci, co, hi, wi, hf, wf, s)
+    xb = D.BlockedFeatureMap(ci, hi, wi, c_ib, data=dev(po.pack_feature_map(x, c_ib)[None]))
+    kb = D.BlockedKernel(ci, co, hf, wf, c_ob, c_ib, data=dev(po.pack_kernel(k, c_ob, c_ib)))
+    sk = None
+    if skip is not None:
+        sk = D.BlockedFeatureMap(co, shape.h_o, shape.w_o, c_ob, data=dev(skip[None]))
+    y = D.conv_direct(xb, kb, shape, D.BlockingParams(c_ob, 1, c_ib), relu=relu, skip=sk,
+                      algo=algo)
+    return host(y.data)[0]
+
+
+# ------------------------------------------------------------------ cases
+def test_cfg1_full_parity():
+    """BASELINE cfg1: 64->64 3x3 s1 58->56, b1, fp32, FFMA path."""
+    x = po.uniform((64, 58, 58), 1809, 0)
+    k = po.uniform((64, 64, 3, 3), 1809, 1)
+    got = run_conv(x, k, 1, 8, 8, algo=_abi.ALGO_FFMA)
+    want = po.pack_feature_map(po.conv_oracle64(x, k, 1), 8)
+    assert_tol(got, want, "cfg1")
+
+
+def test_golden_fixtures_generic_and_ffma():
+    """Reference-generated golden vectors (tests/golden) through both paths."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden.npz"))
+    names = sorted({k.split("/")[0] for k in g.files})
+    for n in names:
+        ci, co, hi, wi, hf, wf, s, cib, cob = g[f"{n}/geom"].tolist()
+        x, k = g[f"{n}/x"], g[f"{n}/k"]
+        got = run_conv(x, k, s, cib, cob, algo=_abi.ALGO_GENERIC)
+        assert_tol(got, g[f"{n}/y_oracle64_blocked"], f"{n}/generic")
+        got8 = run_conv(x, k, s, 8, 8, algo=_abi.ALGO_FFMA)
+        assert_tol(got8, po.pack_feature_map(g[f"{n}/y_oracle64"], 8), f"{n}/ffma")
+
+
+def test_spec_trivial_direct():
+    """1x1x1 [2]*[3] -> 6, both kernels."""
+    x = np.array([[[2.0]]], np.float32)
+    k = np.array([[[[3.0]]]], np.float32)
+    assert run_conv(x, k, 1, 1, 1, algo=_abi.ALGO_GENERIC).ravel()[0] == 6.0
+    y = run_conv(x, k, 1, 8, 8, algo=_abi.ALGO_FFMA).ravel()
+    assert y[0] == 6.0 and not y[1:].any()
+
+
+def test_acceptance1_random_shapes():
+    """SPEC.md:615 property suite (seeded, channels <= 64, spatial <= 32,
+    filters {1,3,5,7,11}, strides {1,2,4}) on the FFMA kernel."""
+    rng = np.random.default_rng(1809)
+    for t in range(120):
+        hf = int(rng.choice([1, 3, 5, 7, 11]))
+        wf = hf
+        s = int(rng.choice([1, 2, 4]))
+        ci, co = int(rng.integers(1, 65)), int(rng.integers(1, 65))
+        ho_max = (32 - hf) // s + 1
+        if ho_max < 1:
+            continue
+        ho, wo = int(rng.integers(1, ho_max + 1)), int(rng.integers(1, ho_max + 1))
+        hi, wi = (ho - 1) * s + hf, (wo - 1) * s + wf
+        x = po.uniform((ci, hi, wi), 2000 + t, 0)
+        k = po.uniform((ci, co, hf, wf), 2000 + t, 1)
+        want = po.pack_feature_map(po.conv_oracle64(x, k, s), 8)
+        assert_tol(run_conv(x, k, s, 8, 8, algo=_abi.ALGO_FFMA), want,
+                   f"case {t} ({ci},{co},{hi},{wi},{hf},{s})")
+
+
+def test_generic_any_block_sizes():
+    """Every (c_ob, c_ib) of the reference API has a CUDA path."""
+    rng = np.random.default_rng(5)
+    for t, (cob, cib) in enumerate([(1, 1), (4, 2), (8, 4), (3, 5), (16, 16), (32, 8), (6, 8)]):
+        ci, co = int(rng.integers(1, 20)), int(rng.integers(1, 20))
+        x = po.uniform((ci, 9, 11), 300 + t, 0)
+        k = po.uniform((ci, co, 3, 3), 300 + t, 1)
+        want = po.pack_feature_map(po.conv_oracle64(x, k, 2), cob)
+        assert_tol(run_conv(x, k, 2, cib, cob, algo=_abi.ALGO_GENERIC), want, f"{cob},{cib}")
+
+
+def test_edge_tiles_spec():
+    """w_o = 7 (ragged tiles), c_o = 6 (padded block)."""
+    x = po.uniform((5, 9, 9), 77, 0)
+    k = po.uniform((5, 6, 3, 3), 77, 1)
+    y = run_conv(x, k, 1, 8, 8, algo=_abi.ALGO_FFMA)
+    assert_tol(y, po.pack_feature_map(po.conv_oracle64(x, k, 1), 8), "edge")
+    assert not y[..., 6:].any(), "padded output channels must be exact 0"
+
+
+def test_fused_epilogues():
+    x = po.uniform((24, 12, 12), 88, 0)
+    k = po.uniform((24, 16, 3, 3), 88, 1)
+    ref = po.pack_feature_map(po.conv_oracle64(x, k, 1), 8)
+    skip = po.pack_feature_map(po.uniform((16, 10, 10), 88, 2), 8)
+    assert_tol(run_conv(x, k, 1, 8, 8, relu=True), np.maximum(ref, 0), "relu")
+    assert_tol(run_conv(x, k, 1, 8, 8, skip=skip), ref + skip, "add")
+    assert_tol(run_conv(x, k, 1, 8, 8, relu=True, skip=skip), np.maximum(ref + skip, 0),
+               "add_relu")
+    for algo in (_abi.ALGO_GENERIC,):
+        assert_tol(run_conv(x, k, 1, 8, 8, algo=algo, relu=True, skip=skip),
+                   np.maximum(ref + skip, 0), "generic add_relu")
+
+
+def test_determinism_bitwise():
+    """repeated runs are bitwise identical (no atomics)."""
+    x = po.uniform((64, 30, 30), 9, 0)
+    k = po.uniform((64, 128, 3, 3), 9, 1)
+    a = run_conv(x, k, 1, 8, 8)
+    b = run_conv(x, k, 1, 8, 8)
+    assert np.array_equal(a, b)
+
+
+# ------------------------------------------------------------------ layouts
+@pytest.mark.parametrize("cob,cib", [(1, 1), (4, 2), (8, 4), (8, 8), (3, 5), (8, 3), (32, 32)])
+def test_pack_kernel_bitexact(cob, cib):
+    k = po.uniform((13, 21, 3, 3), 50, cob * 7 + cib)
+    got = D.pack_kernel(dev(k), cob, cib)
+    assert np.array_equal(host(got.data), po.pack_kernel(k, cob, cib))
+    assert np.array_equal(host(D.unpack_kernel(got)), k)
+
+
+@pytest.mark.parametrize("cb", [1, 2, 3, 8, 16])
+def test_pack_feature_map_bitexact(cb):
+    x = po.uniform((2, 11, 7, 9), 60, cb)
+    got = D.pack_feature_map(dev(x), cb)
+    want = np.stack([po.pack_feature_map(x[i], cb) for i in range(2)])
+    assert np.array_equal(host(got.data), want)
+    assert np.array_equal(host(D.unpack_feature_map(got)), x)
+
+
+def test_pack_feature_map_halo():
+    import ctypes
+    x = po.uniform((1, 5, 4, 6), 61, 0)
+    out = torch.full((1, 1, 6, 8, 8), 7.0, device="cuda")
+    _abi.check(_abi.lib().dconv_cuda_pack_feature_map(_abi.ptr(dev(x)), 1, 5, 4, 6, 8, 1,
+                                                     _abi.ptr(out), _abi.stream_ptr()))
+    o = host(out)
+    want = np.zeros((1, 1, 6, 8, 8), np.float32)
+    want[0, :, 1:5, 1:7, :] = po.pack_feature_map(x[0], 8)
+    assert np.array_equal(o, want)
+
+
+def test_layout_counter_and_chain():
+    """chain of 1x1 weights 2.0 then 3.0 on 1.0 -> 6.0; no
+    layout transforms inside; c_ib/c_ob mismatch -> layout error."""
+    x = D.pack_feature_map(dev(np.ones((1, 1, 1), np.float32)), 8)
+    k1 = D.pack_kernel(dev(np.full((1, 1, 1, 1), 2.0, np.float32)), 8, 8)
+    k2 = D.pack_kernel(dev(np.full((1, 1, 1, 1), 3.0, np.float32)), 8, 8)
+    sh = D.ConvShape(1, 1, 1, 1, 1, 1, 1)
+    p = D.BlockingParams(8, 1, 8)
+    before = D.layout_transform_count()
+    y = D.layer_chain(x, [(k1, sh, p), (k2, sh, p)])
+    assert D.layout_transform_count() == before
+    assert host(y.data).ravel()[0] == 6.0
+    k3 = D.pack_kernel(dev(np.ones((1, 1, 1, 1), np.float32)), 4, 4)
+    with pytest.raises(ValueError, match="layout"):
+        D.layer_chain(x, [(k1, sh, p), (k3, sh, D.BlockingParams(4, 1, 4))])
+
+
+def test_shape_errors_match_reference():
+    with pytest.raises(ValueError, match="ConvShape"):
+        D.ConvShape(3, 64, 230, 230, 7, 7, 2)
+    with pytest.raises(ValueError, match="ConvShape"):
+        D.ConvShape(1, 1, 2, 2, 3, 3)
+
+
+# ------------------------------------------------------------ element-wise
+def test_relu_add_maxpool_bitexact():
+    a = po.uniform((3, 2, 6, 10, 8), 70, 0)
+    b = po.uniform((3, 2, 6, 10, 8), 70, 1)
+    ta, tb = dev(a), dev(b)
+    A = D.BlockedFeatureMap(16, 6, 10, 8, n=3, data=ta.clone())
+    B = D.BlockedFeatureMap(16, 6, 10, 8, n=3, data=tb)
+    assert np.array_equal(host(D.add_blocked(A, B).data), a + b)
+    assert np.array_equal(host(D.add_blocked(A, B, relu=True).data), np.maximum(a + b, 0))
+    assert np.array_equal(host(D.maxpool2x2_blocked(A).data),
+                          a.reshape(3, 2, 3, 2, 5, 2, 8).max(axis=(3, 5)))
+    D.relu_blocked(A)
+    assert np.array_equal(host(A.data), np.maximum(a, 0))
+    x = dev(np.array([-1.0, 0.0, 2.0], np.float32))
+    _abi.check(_abi.lib().dconv_cuda_relu_blocked(_abi.ptr(x), 3, _abi.stream_ptr()))
+    assert host(x).tolist() == [0.0, 0.0, 2.0]
+
+
+# ------------------------------------------------------- views and sharding
+def test_output_into_halo_and_crop_view():
+    """Producer writes into the interior of a halo'd consumer buffer; a
+    consumer reads a crop (ResNet stride-2 projection 55x55 of 56x56)."""
+    n = 2
+    x = po.uniform((n, 16, 12, 12), 90, 0)
+    k = po.uniform((16, 24, 1, 1), 90, 1)
+    a = nets.Act(n, 16, 12, 12)
+    a.buf.copy_(dev(np.stack([po.pack_feature_map(x[i], 8) for i in range(n)])))
+    l = nets.Layer("proj", 16, 24, 11, 11, 1, 1, 2)
+    y = nets.Act(n, 24, 6, 6, halo=1)
+    nets.conv(l, n, a, nets.pack_weights(dev(k), False), y)
+    got = host(y.buf)
+    for i in range(n):
+        want = po.pack_feature_map(po.conv_oracle64(x[i, :, :11, :11], k, 2), 8)
+        assert_tol(got[i, :, 1:7, 1:7, :], want, "crop->halo")
+    ring = got.copy()
+    ring[:, :, 1:7, 1:7, :] = 0
+    assert not ring.any(), "halo ring must stay zero"
+
+
+def test_co_block_sharding_ranges():
+    """C_o-block sharding: each rank computes a contiguous j' range into its
+    own slice buffer; the concatenation equals the full conv (bitwise)."""
+    import ctypes
+    x = po.uniform((32, 14, 14), 95, 0)
+    k = po.uniform((32, 64, 3, 3), 95, 1)
+    xb = dev(po.pack_feature_map(x, 8)[None])
+    kb = dev(po.pack_kernel(k, 8, 8))
+    full = run_conv(x, k, 1, 8, 8)
+    parts = []
+    for r in range(4):
+        d = D.make_desc(D.ConvShape(32, 64, 14, 14, 3, 3, 1), 1, 8, 8)
+        d.co_block_begin, d.co_block_count = 2 * r, 2
+        out = torch.empty((1, 2, 12, 12, 8), device="cuda")
+        _abi.check(_abi.lib().dconv_cuda_conv_direct(ctypes.byref(d), _abi.ptr(xb),
+                                                     _abi.ptr(kb), 0, _abi.ptr(out),
+                                                     _abi.stream_ptr()))
+        parts.append(host(out)[0])
+    assert np.array_equal(np.concatenate(parts, 0), full)
+
+
+# --------------------------------------------------- BASELINE config layers
+def _rows(h):
+    return sorted({0, 1, h // 2, h - 2, h - 1} & set(range(h)))
+
+
+ALL_LAYERS = [(cfg, l) for cfg in ("cfg1", "alexnet", "vgg16", "googlenet") for l in
+              nets.CONFIGS[cfg]] + [("resnet50", l) for l in {
+                  (l.c_i, l.c_o, l.h_i, l.h_f, l.s): l for l in nets.CONFIGS["resnet50"]}.values()]
+
+
+@pytest.mark.parametrize("cfg,layer", ALL_LAYERS, ids=[f"{c}-{l.name}" for c, l in ALL_LAYERS])
+def test_config_layer_parity(cfg, layer):
+    """Every distinct layer shape of BASELINE.json configs 1-5 at batch 2,
+    fp32, vs conv_oracle64 on sampled output rows (edges + middle) of both
+    images."""
+    l, n = layer, 2
+    sid = zlib.crc32(f"{cfg}/{l.name}".encode()) % 10_000
+    k = po.uniform((l.c_i, l.c_o, l.h_f, l.w_f), 4000 + sid, 1)
+    w = nets.pack_weights(dev(k), l.first)
+    assert np.array_equal(host(w), po.pack_kernel(k, 8, l.c_i if l.first else 8))
+    xs = [po.uniform((l.c_i, l.h_i, l.w_i), 4000 + sid, 10 + i) for i in range(n)]
+    y = nets.Act(n, l.c_o, l.h_o, l.w_o)
+    if l.first:
+        nets.conv(l, n, dev(np.stack(xs)), w, y)
+    else:
+        a = nets.Act(n, l.c_i, l.h_i, l.w_i)
+        a.buf.copy_(dev(np.stack([po.pack_feature_map(xx, 8) for xx in xs])))
+        nets.conv(l, n, a, w, y)
+    got = host(y.buf)
+    rows = _rows(l.h_o)
+    kb = po.pack_kernel(k, 8, 8)
+    for i in range(n):
+        xb = po.pack_feature_map(xs[i], 8)
+        for r in rows:
+            want = po.conv_oracle64_blocked(xb, kb, l.c_i, l.c_o, l.s, r, r + 1)
+            assert_tol(got[i, :, r], want[:, r], f"{cfg}/{l.name} img {i} row {r}")
