@@ -173,7 +173,11 @@ int dconv_cuda_conv_direct(const dconv_conv_desc* d, const float* in,
     p.out_img = r.out_img; p.out_blk = r.out_blk; p.out_row = r.out_row;
     p.sk_img = r.sk_img; p.sk_blk = r.sk_blk; p.sk_row = r.sk_row;
     p.epi = d->epilogue;
-    return dconv_dev::launch_conv_ffma(p, as_stream(stream));
+    rc = dconv_dev::launch_conv_ffma(p, as_stream(stream));
+    // AUTO: a configuration whose stage cannot be staged in shared memory
+    // (very large filters on tiny maps) runs on the generic kernel instead.
+    if (rc != DCONV_EUNSUPPORTED || d->algo != DCONV_ALGO_AUTO) return rc;
+    algo = DCONV_ALGO_GENERIC;
   }
   if (algo == DCONV_ALGO_GENERIC) {
     dconv_dev::GenericParams p{};
@@ -208,6 +212,14 @@ int dconv_cuda_conv_first_layer(const dconv_conv_desc* d, const float* in_dense,
   p.sk_img = r.sk_img; p.sk_blk = r.sk_blk; p.sk_row = r.sk_row;
   p.epi = d->epilogue;
   p.dense_input = 1;
+  const bool fast_ok = d->c_ob == 8 && aligned16(w) && aligned16(out) &&
+                       (!skip || aligned16(skip)) &&
+                       ((r.out_img | r.out_blk | r.out_row | r.sk_img | r.sk_blk |
+                         r.sk_row) & 3) == 0;
+  if (fast_ok && d->algo != DCONV_ALGO_GENERIC) {
+    rc = dconv_dev::launch_conv_first_fast(p, as_stream(stream));
+    if (rc != DCONV_EUNSUPPORTED) return rc;
+  }
   return dconv_dev::launch_conv_first_layer(p, as_stream(stream));
 }
 

@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int ib0 = g * p.G, Ge = min(p.G, p.ib_n - ib0);
       const int n0 = r * p.R, Re = min(p.R, p.h_f - n0);
       const int row0 = ty0 * p.s + n0;
-      const int rows = min((p.TH - 1) * p.s + Re, p.h_i - row0);
+      const int rows = min((p.THe - 1) * p.s + Re, p.h_i - row0);
       const uint32_t patch_bytes = (uint32_t)(Ge * rows * cols * kCB * 4);
       const uint32_t wbytes = (uint32_t)(Re * p.w_f * kCB * kCB * 4) * Ge;
       float* sp = smem + buf * p.stage_floats;
@@ -114,7 +114,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int k = 0; k < 8; ++k) {
     const int q = pg + PG * k;
     const int ty = q / p.TW, tx = q - (q / p.TW) * p.TW;
-    poff[k] = (ty * p.s * p.PW + tx * p.s) * kCB;
+    // pixels beyond the clamped patch never store; point them at offset 0
+    poff[k] = (ty < p.THe && tx < p.TWe) ? (ty * p.s * p.PW + tx * p.s) * kCB : 0;
   }
 
   // acc[k][c2] holds channels (2*c2, 2*c2+1) of pixel k as an fp32 pair so
@@ -239,7 +240,11 @@ int launch(FfmaParams p, cudaStream_t stream) {
   p.TW = t.TW;
   p.tiles_x = (p.w_o + p.TW - 1) / p.TW;
   p.tiles_per_img = (int)t.tiles;
-  p.PW = (p.TW - 1) * p.s + p.w_f;
+  // The patch only has to cover output pixels that exist: clamp the tile
+  // extents to the output before sizing it (pixels outside map to offset 0).
+  p.TWe = std::min(p.TW, p.w_o);
+  p.THe = std::min(p.TH, p.h_o);
+  p.PW = (p.TWe - 1) * p.s + p.w_f;
   p.slab_floats = p.h_f * p.w_f * kCB * kCB;
 
   // Stage decomposition (i'-groups x filter-row groups), sized for smem.
@@ -247,7 +252,7 @@ int launch(FfmaParams p, cudaStream_t stream) {
   const int full_taps_bytes = CG * p.h_f * p.w_f * kCB * kCB * 4;
   if (full_taps_bytes <= kWeightBudget) {
     p.R = p.h_f;
-    p.PH = (p.TH - 1) * p.s + p.R;
+    p.PH = (p.THe - 1) * p.s + p.R;
     const int patch1 = p.PH * p.PW * kCB * 4;
     p.G = std::max(1, std::min(kWeightBudget / full_taps_bytes,
                                kPatchBudget / std::max(1, patch1)));
@@ -256,7 +261,7 @@ int launch(FfmaParams p, cudaStream_t stream) {
     p.G = 1;
     p.R = std::max(1, kWeightBudget / (CG * p.w_f * kCB * kCB * 4));
     p.R = std::min(p.R, p.h_f);
-    p.PH = (p.TH - 1) * p.s + p.R;
+    p.PH = (p.THe - 1) * p.s + p.R;
   }
   p.n_g = (p.ib_n + p.G - 1) / p.G;
   p.n_r = (p.h_f + p.R - 1) / p.R;
@@ -269,7 +274,7 @@ int launch(FfmaParams p, cudaStream_t stream) {
   p.NS = std::min(kMaxStages, (kSmemBudget - 2 * kMaxStages * 8) / stage_bytes);
   const int S = p.n_g * p.n_r;
   p.NS = std::min(p.NS, std::max(2, S));
-  if (p.NS < 2)
+  if (p.NS < 2 || p.PH > 256 || p.PW > 256)
     return dconv_host::set_error(DCONV_EUNSUPPORTED,
                                  "conv_ffma: stage of %d bytes does not fit "
                                  "shared memory twice",

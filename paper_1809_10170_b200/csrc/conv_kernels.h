@@ -22,7 +22,7 @@ struct FfmaParams {
   int64_t sk_img, sk_blk, sk_row;
   int epi;
   // launcher-filled
-  int TH, TW, tiles_x, tiles_per_img;
+  int TH, TW, THe, TWe, tiles_x, tiles_per_img;
   int G, R, n_g, n_r, PH, PW;
   int slab_floats, patch_floats, wstride_floats, stage_floats, NS;
 };
@@ -46,5 +46,8 @@ struct GenericParams {
 
 int launch_conv_generic(const GenericParams& p, cudaStream_t stream);
 int launch_conv_first_layer(const GenericParams& p, cudaStream_t stream);
+// register-tiled first-layer reader (c_ob = 8); DCONV_EUNSUPPORTED if no
+// specialisation matches (the caller then uses launch_conv_first_layer).
+int launch_conv_first_fast(const GenericParams& p, cudaStream_t stream);
 
 }  // namespace dconv_dev
