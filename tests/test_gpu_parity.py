@@ -308,3 +308,22 @@ def test_config_layer_parity(cfg, layer):
         for r in rows:
             want = po.conv_oracle64_blocked(xb, kb, l.c_i, l.c_o, l.s, r, r + 1)
             assert_tol(got[i, :, r], want[:, r], f"{cfg}/{l.name} img {i} row {r}")
+
+
+@pytest.mark.parametrize("s,f,ci,co", [(1, 3, 3, 64), (2, 7, 3, 64), (4, 11, 3, 96), (1, 5, 3, 20),
+                                       (1, 1, 4, 8), (2, 3, 1, 64), (3, 3, 3, 16), (1, 3, 3, 72)])
+def test_first_layer_reader_variants(s, f, ci, co):
+    """Dense-input first layer (all specialisations + the generic fallback
+    for (s=3, f=3)) vs conv_oracle64, batch 2, ragged tiles, relu epilogue."""
+    n = 2
+    ho, wo = 13, 21
+    hi, wi = (ho - 1) * s + f, (wo - 1) * s + f
+    x = po.uniform((n, ci, hi, wi), 5000 + s * 100 + f, 0)
+    k = po.uniform((ci, co, f, f), 5000 + s * 100 + f, 1)
+    l = nets.Layer("first", ci, co, hi, wi, f, f, s, first=True)
+    y = nets.Act(n, co, ho, wo)
+    nets.conv(l, n, dev(x), nets.pack_weights(dev(k), True), y, epilogue=_abi.EPI_RELU)
+    got = host(y.buf)
+    for i in range(n):
+        want = np.maximum(po.pack_feature_map(po.conv_oracle64(x[i], k, s), 8), 0)
+        assert_tol(got[i], want, f"first s={s} f={f} img {i}")
