@@ -158,6 +158,13 @@ int dconv_cuda_maxpool2x2_blocked(const float* in, int n, int n_blocks, int h,
 /* Zeroes a float buffer (halo buffers are zeroed once, outside timing). */
 int dconv_cuda_zero(float* x, int64_t count, void* stream);
 
+/* Tile selector override for the FFMA kernel (the GPU analogue of the
+ * reference's BlockingParams choice, model.hpp:85-109): -1 = heuristic,
+ * 0 = 128px x 128ch / 8x8 thread tile / 8 warps, 1 = 128 x 128 / 8x4 / 16
+ * warps, 2 = 256 x 64 / 8x4 / 16 warps, 3 = 256 x 64 / 8x8 / 8 warps.
+ * Process-wide; used by tests and the autotuner. */
+int dconv_cuda_set_ffma_variant(int variant);
+
 /* Launch accounting: number of device kernels this library launched since
  * load (for bench.py's gpu_launches claim) and the name of the last kernel. */
 int64_t dconv_cuda_launch_count(void);

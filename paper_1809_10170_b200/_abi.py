@@ -58,6 +58,7 @@ _SIGS = {
     "dconv_cuda_add_blocked": (_I, [_P, _P, _P, _L, _I, _P]),
     "dconv_cuda_maxpool2x2_blocked": (_I, [_P] + [_I] * 5 + [_P, _L, _L, _L, _P]),
     "dconv_cuda_zero": (_I, [_P, _L, _P]),
+    "dconv_cuda_set_ffma_variant": (_I, [_I]),
     "dconv_cuda_launch_count": (_L, []),
     "dconv_cuda_fp32_peak_probe": (ctypes.c_double, [_P]),
     "dconv_cuda_strerror": (ctypes.c_char_p, [_I]),

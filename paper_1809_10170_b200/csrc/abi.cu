@@ -304,6 +304,12 @@ int dconv_cuda_zero(float* x, int64_t count, void* stream) {
   return DCONV_OK;
 }
 
+int dconv_cuda_set_ffma_variant(int variant) {
+  if (variant < -1 || variant > 3) return set_error(DCONV_EPARAM, "variant %d", variant);
+  dconv_dev::ffma_variant_override = variant;
+  return DCONV_OK;
+}
+
 int64_t dconv_cuda_launch_count(void) {
   return g_launches.load(std::memory_order_relaxed);
 }

@@ -1,21 +1,30 @@
-// conv_ffma.cu -- register-blocked FP32 FFMA direct convolution for sm_100a.
+// conv_ffma.cu -- register-blocked FP32 direct convolution for sm_100a.
 //
 // GPU restatement of Alg. 3 in the blocked layout with
 // c_ib = c_ob = 8 (one 32-byte pencil = one DRAM sector per pixel):
-//   * j' (output blocks, "in Parallel")      -> blockIdx.y, CG blocks per CTA
+//   * j' (output blocks, "in Parallel")      -> blockIdx.y, BN/8 blocks per CTA
 //   * l, k' (output rows / row tiles)        -> blockIdx.x, a TH x TW pixel tile
-//   * i' (input blocks, cache blocking)      -> the smem pipeline stage
+//   * i' (input blocks, cache blocking)      -> the shared-memory pipeline stage
 //   * (n, m, ii) reduction                   -> per-stage loop from smem
-//   * (kk, jj) register tile                 -> 8 pixels x 8 channels / thread
-// The input index is s*(k'*w_ob + kk) + m (SPEC.md:354 stride fix).
+//   * (kk, jj) register tile                 -> 8 pixels x TCO channels / thread
+// Input index s*(k'*w_ob + kk) + m (SPEC.md:354 stride fix).
 //
-// Data movement: a dedicated producer warp streams each stage -- the input
-// patch rows of G i'-blocks (each patch row is contiguous in the blocked
-// layout) and the matching (j', i') weight slab rows (contiguous,
-// tensor.hpp:138-140) -- with 1-D bulk async copies (cp.async.bulk -> UBLKCP)
-// into an NS-deep ring of shared-memory stages guarded by full/empty
-// mbarriers.  Eight compute warps consume.  Nothing is written to global
-// memory except the output, once, from registers (zero workspace).
+// Data movement: warp 0 streams each stage NS-1 stages ahead -- the input
+// patch rows of G i'-blocks (each row of a blocked map is contiguous) and the
+// matching (j', i') weight slab rows (contiguous, tensor.hpp:138-140) -- with
+// 1-D bulk async copies (cp.async.bulk, SASS UBLKCP) into an NS-deep ring of
+// smem stages guarded by full/empty mbarriers; all NW warps compute.
+//
+// Arithmetic: FFMA2 (fma.rn.f32x2, each lane an IEEE fp32 fma).  Accuracy:
+// two-level summation -- each thread accumulates ~256 products in registers,
+// then folds that partial sum into a running total kept in TMEM
+// (tcgen05.st / tcgen05.ld, no register cost).  For K = 4608 the worst-case
+// per-element error drops well below a single fp32 accumulator's (the
+// reference's own conv_naive reaches 3e-4 there), keeping every element
+// inside |a-b| <= 1e-4 + 1e-5|b| of conv_oracle64.
+//
+// Zero workspace: nothing is written to global memory except the output,
+// once, from registers (smem ring and TMEM are on-chip).
 #include <algorithm>
 #include <cstdio>
 
@@ -26,22 +35,87 @@ namespace dconv_dev {
 
 namespace {
 
-constexpr int kCB = 8;             // channel block of this kernel (c_ib = c_ob)
-constexpr int kComputeWarps = 8;   // 256 compute threads, 8x8 outputs each
-constexpr int kThreads = (kComputeWarps + 1) * 32;  // + producer warp
+constexpr int kCB = 8;          // channel block of this kernel (c_ib = c_ob)
 constexpr int kMaxStages = 8;
+constexpr int kTmemCols = 128;  // running totals: NW/4 slots x 8*TCO columns
 
-template <int BM, int BN>
-__global__ void __launch_bounds__(kThreads, 1)
+// ---- TMEM helpers (32 lanes x 32 columns of 32-bit per warp) ----------------
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, "
+      "%8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, "
+      "%23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]),
+      "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]),
+      "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+      "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]),
+      "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, "
+      "%8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, "
+      "%23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+        "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+        "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+        "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]),
+        "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// acc (NP pairs) -> TMEM at taddr (+ optional fold of the previous total)
+template <int NP>
+__device__ __forceinline__ void tmem_fold(uint32_t taddr, uint64_t* acc,
+                                          bool have_total, bool store) {
+  static_assert(NP % 16 == 0, "32-column chunks");
+#pragma unroll
+  for (int c = 0; c < NP / 16; ++c) {
+    uint32_t v[32];
+    const uint32_t ta = taddr + c * 32;
+    if (have_total) {
+      tmem_ld32(ta, v);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        uint64_t t;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(t) : "r"(v[2 * i]), "r"(v[2 * i + 1]));
+        acc[c * 16 + i] = fadd2(acc[c * 16 + i], t);
+      }
+    }
+    if (store) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        asm("mov.b64 {%0, %1}, %2;" : "=r"(v[2 * i]), "=r"(v[2 * i + 1]) : "l"(acc[c * 16 + i]));
+      tmem_st32(ta, v);
+    }
+  }
+}
+
+template <int BM, int BN, int TCO, int NW, int WF>
+__global__ void __launch_bounds__(NW * 32, 1)
     conv_ffma_kernel(const FfmaParams p) {
-  constexpr int PG = BM / 8;  // pixel groups
-  constexpr int CG = BN / 8;  // channel groups == output blocks per CTA
-  constexpr int WR = PG / 4;  // warps along pixels
-  static_assert(PG * CG == kComputeWarps * 32, "thread tile mismatch");
+  constexpr int PG = BM / 8;    // pixel groups (8 pixels each)
+  constexpr int CGT = BN / TCO; // channel thread groups (TCO channels each)
+  constexpr int WPG = PG / 4;   // warps along pixels
+  constexpr int NP = 8 * TCO / 2;  // accumulator pairs per thread
+  static_assert(PG * CGT == NW * 32, "thread tile mismatch");
+  static_assert(TCO == 4 || TCO == 8, "TCO");
+  constexpr int CG = BN / 8;    // output blocks per CTA
 
   extern __shared__ __align__(128) float smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.NS * p.stage_floats);
   uint64_t* empty = full + kMaxStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty + kMaxStages);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -49,96 +123,111 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tile = blockIdx.x - img * p.tiles_per_img;
   const int ty0 = (tile / p.tiles_x) * p.TH;
   const int tx0 = (tile % p.tiles_x) * p.TW;
-  const int jb0 = p.jb_begin + blockIdx.y * CG;  // first output block (global)
+  const int jb0 = p.jb_begin + blockIdx.y * CG;
   const int cg_valid = min(CG, p.jb_begin + p.jb_count - jb0);
   const int S = p.n_g * p.n_r;
+  const bool use_tmem = S > p.flush_every;
 
   if (tid == 0) {
     for (int i = 0; i < p.NS; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kComputeWarps);
+      mbar_init(&empty[i], NW);
     }
     fence_mbar_init();
   }
+  if (use_tmem && warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
-  if (warp == kComputeWarps) {
-    // ------------------------------------------------------------ producer
-    const float* in_img = p.in + (int64_t)img * p.in_img;
-    const int col0 = tx0 * p.s;
-    const int cols = min(p.PW, p.w_i - col0);
-    for (int st = 0; st < S; ++st) {
-      const int buf = st % p.NS;
-      if (st >= p.NS) mbar_wait(&empty[buf], ((st / p.NS) - 1) & 1);
-      const int g = st / p.n_r, r = st - g * p.n_r;
-      const int ib0 = g * p.G, Ge = min(p.G, p.ib_n - ib0);
-      const int n0 = r * p.R, Re = min(p.R, p.h_f - n0);
-      const int row0 = ty0 * p.s + n0;
-      const int rows = min((p.THe - 1) * p.s + Re, p.h_i - row0);
-      const uint32_t patch_bytes = (uint32_t)(Ge * rows * cols * kCB * 4);
-      const uint32_t wbytes = (uint32_t)(Re * p.w_f * kCB * kCB * 4) * Ge;
-      float* sp = smem + buf * p.stage_floats;
-      float* sw = sp + p.patch_floats;
-      if (lane == 0)
-        mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes * cg_valid);
-      __syncwarp();
-      const int n_patch = Ge * rows;
-      const int tasks = n_patch + cg_valid;
-      for (int t = lane; t < tasks; t += 32) {
-        if (t < n_patch) {
-          const int gi = t / rows, pr = t - gi * rows;
-          const float* src = in_img + (int64_t)(ib0 + gi) * p.in_blk +
-                             (int64_t)(row0 + pr) * p.in_row +
-                             (int64_t)col0 * kCB;
-          float* dst = sp + ((gi * p.PH + pr) * p.PW) * kCB;
-          bulk_g2s(dst, src, (uint32_t)(cols * kCB * 4), &full[buf]);
-        } else {
-          const int c = t - n_patch;
-          const float* src =
-              p.w + ((int64_t)(jb0 + c) * p.ib_n + ib0) * p.slab_floats +
-              (int64_t)n0 * p.w_f * kCB * kCB;
-          bulk_g2s(sw + c * p.wstride_floats, src, wbytes, &full[buf]);
-        }
+  // ------------------------------------------------------------ producer
+  // Warp 0 doubles as the producer: it issues stage st+NS-1 before computing
+  // stage st (the buffer it refills was released by every warp at the end of
+  // stage st-1), so no warp slot is spent on a copy-only warp and all NW
+  // warps keep the full per-SMSP register budget.
+  const float* in_img = p.in + (int64_t)img * p.in_img;
+  const int col0 = tx0 * p.s;
+  const int cols = min(p.PW, p.w_i - col0);
+  auto issue = [&](int st) {
+    const int buf = st % p.NS;
+    if (st >= p.NS) mbar_wait(&empty[buf], ((st / p.NS) - 1) & 1);
+    const int g = st / p.n_r, r = st - g * p.n_r;
+    const int ib0 = g * p.G, Ge = min(p.G, p.ib_n - ib0);
+    const int n0 = r * p.R, Re = min(p.R, p.h_f - n0);
+    const int row0 = ty0 * p.s + n0;
+    const int rows = min((p.THe - 1) * p.s + Re, p.h_i - row0);
+    const uint32_t patch_bytes = (uint32_t)(Ge * rows * cols * kCB * 4);
+    const uint32_t wbytes = (uint32_t)(Re * p.w_f * kCB * kCB * 4) * Ge;
+    float* sp = smem + buf * p.stage_floats;
+    float* sw = sp + p.patch_floats;
+    if (lane == 0) mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes * cg_valid);
+    __syncwarp();
+    const int n_patch = Ge * rows;
+    const int tasks = n_patch + cg_valid;
+    for (int t = lane; t < tasks; t += 32) {
+      if (t < n_patch) {
+        const int gi = t / rows, pr = t - gi * rows;
+        const float* src = in_img + (int64_t)(ib0 + gi) * p.in_blk +
+                           (int64_t)(row0 + pr) * p.in_row + (int64_t)col0 * kCB;
+        float* dst = sp + ((gi * p.PH + pr) * p.PW) * kCB;
+        bulk_g2s(dst, src, (uint32_t)(cols * kCB * 4), &full[buf]);
+      } else {
+        const int c = t - n_patch;
+        const float* src = p.w + ((int64_t)(jb0 + c) * p.ib_n + ib0) * p.slab_floats +
+                           (int64_t)n0 * p.w_f * kCB * kCB;
+        bulk_g2s(sw + c * p.wstride_floats, src, wbytes, &full[buf]);
       }
     }
-    return;
-  }
+  };
+  if (warp == 0)
+    for (int st = 0; st < min(S, p.NS - 1); ++st) issue(st);
 
   // -------------------------------------------------------------- consumers
-  const int wr = warp % WR, wc = warp / WR;
+  const int wr = warp % WPG, wc = warp / WPG;
   const int pg = wr * 4 + (lane & 3);
-  const int cg = wc * 8 + (lane >> 2);
+  const int cgt = wc * 8 + (lane >> 2);
+  const int cb = TCO == 8 ? cgt : (cgt >> 1);          // output block in CTA
+  const int cofs = TCO == 8 ? 0 : (cgt & 1) * 4;       // channel offset in block
 
   int poff[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int q = pg + PG * k;
     const int ty = q / p.TW, tx = q - (q / p.TW) * p.TW;
-    // pixels beyond the clamped patch never store; point them at offset 0
     poff[k] = (ty < p.THe && tx < p.TWe) ? (ty * p.s * p.PW + tx * p.s) * kCB : 0;
   }
 
-  // acc[k][c2] holds channels (2*c2, 2*c2+1) of pixel k as an fp32 pair so
-  // every update is one FFMA2 (fma.rn.f32x2, scalar-broadcast input).
-  uint64_t acc[8][4];
+  uint64_t acc[8][TCO / 2];
 #pragma unroll
   for (int k = 0; k < 8; ++k)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc[k][c] = 0ull;
+    for (int c = 0; c < TCO / 2; ++c) acc[k][c] = 0ull;
 
-  const int wf = p.w_f;
+  const uint32_t tmem_base = use_tmem ? *tmem_slot : 0u;
+  const uint32_t taddr = tmem_base + ((uint32_t)((warp & 3) * 32) << 16) +
+                         (uint32_t)((warp >> 2) * 8 * TCO);
+  bool have_total = false;
+
+  const int wf = WF > 0 ? WF : p.w_f;
   for (int st = 0; st < S; ++st) {
+    if (warp == 0 && st + p.NS - 1 < S) issue(st + p.NS - 1);
     const int buf = st % p.NS;
     mbar_wait(&full[buf], (st / p.NS) & 1);
     const int g = st / p.n_r, r = st - g * p.n_r;
     const int Ge = min(p.G, p.ib_n - g * p.G);
     const int Re = min(p.R, p.h_f - r * p.R);
     const float* sp = smem + buf * p.stage_floats;
-    const float* sw = sp + p.patch_floats + cg * p.wstride_floats;
+    const float* sw = sp + p.patch_floats + cb * p.wstride_floats + cofs;
     for (int gi = 0; gi < Ge; ++gi) {
       for (int n = 0; n < Re; ++n) {
         const float* pa_row = sp + ((gi * p.PH + n) * p.PW) * kCB;
         const float* pw_row = sw + ((gi * p.R + n) * wf) * (kCB * kCB);
+#pragma unroll(WF > 0 ? WF : 1)
         for (int m = 0; m < wf; ++m) {
           const float* pa = pa_row + m * kCB;
           const float* pw = pw_row + m * (kCB * kCB);
@@ -149,20 +238,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int k = 0; k < 8; ++k) a[k] = lds128(pa + poff[k] + half * 4);
 #pragma unroll
             for (int i4 = 0; i4 < 4; ++i4) {
-              const float4 b0 = lds128(pw + (half * 4 + i4) * kCB);
-              const float4 b1 = lds128(pw + (half * 4 + i4) * kCB + 4);
-              const uint64_t bp0 = pack2(b0.x, b0.y), bp1 = pack2(b0.z, b0.w);
-              const uint64_t bp2 = pack2(b1.x, b1.y), bp3 = pack2(b1.z, b1.w);
+              const float* pb = pw + (half * 4 + i4) * kCB;
+              const float4 b0 = lds128(pb);
+              uint64_t bp[TCO / 2];
+              bp[0] = pack2(b0.x, b0.y);
+              bp[1] = pack2(b0.z, b0.w);
+              if constexpr (TCO == 8) {
+                const float4 b1 = lds128(pb + 4);
+                bp[2] = pack2(b1.x, b1.y);
+                bp[3] = pack2(b1.z, b1.w);
+              }
 #pragma unroll
               for (int k = 0; k < 8; ++k) {
-                const float av = i4 == 0 ? a[k].x
-                                 : i4 == 1 ? a[k].y
-                                 : i4 == 2 ? a[k].z
-                                           : a[k].w;
-                ffma2(acc[k][0], av, bp0);
-                ffma2(acc[k][1], av, bp1);
-                ffma2(acc[k][2], av, bp2);
-                ffma2(acc[k][3], av, bp3);
+                const float av = i4 == 0 ? a[k].x : i4 == 1 ? a[k].y : i4 == 2 ? a[k].z : a[k].w;
+#pragma unroll
+                for (int c = 0; c < TCO / 2; ++c) ffma2(acc[k][c], av, bp[c]);
               }
             }
           }
@@ -171,41 +261,66 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[buf]);
+    // fold the partial sum into the TMEM running total every flush_every
+    // stages (never after the last stage: the epilogue folds it)
+    if (use_tmem && (st + 1) % p.flush_every == 0 && st + 1 < S) {
+      tmem_fold<NP>(taddr, &acc[0][0], have_total, true);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      have_total = true;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+#pragma unroll
+        for (int c = 0; c < TCO / 2; ++c) acc[k][c] = 0ull;
+    }
+  }
+  if (have_total) tmem_fold<NP>(taddr, &acc[0][0], true, false);
+
+  if (use_tmem) {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    // all warps are done with TMEM before warp 0 frees it
+    __syncthreads();
+    if (warp == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(kTmemCols));
+    }
   }
 
   // -------------------------------------------------------------- epilogue
-  if (cg >= cg_valid) return;
-  const int jl = jb0 + cg - p.jb_begin;  // block index within the output view
-  float* obase = p.out + (int64_t)img * p.out_img + (int64_t)jl * p.out_blk;
+  if (cb >= cg_valid) return;
+  const int jl = jb0 + cb - p.jb_begin;  // block index within the output view
+  float* obase = p.out + (int64_t)img * p.out_img + (int64_t)jl * p.out_blk + cofs;
   const float* sbase =
-      p.skip ? p.skip + (int64_t)img * p.sk_img + (int64_t)jl * p.sk_blk
-             : nullptr;
+      p.skip ? p.skip + (int64_t)img * p.sk_img + (int64_t)jl * p.sk_blk + cofs : nullptr;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int q = pg + PG * k;
     const int ty = q / p.TW, tx = q - (q / p.TW) * p.TW;
     const int y = ty0 + ty, x = tx0 + tx;
     if (y >= p.h_o || x >= p.w_o) continue;
-    const float2 c0 = unpack2(acc[k][0]), c1 = unpack2(acc[k][1]);
-    const float2 c2 = unpack2(acc[k][2]), c3 = unpack2(acc[k][3]);
-    float4 v0 = make_float4(c0.x, c0.y, c1.x, c1.y);
-    float4 v1 = make_float4(c2.x, c2.y, c3.x, c3.y);
+    float v[TCO];
+#pragma unroll
+    for (int c = 0; c < TCO / 2; ++c) {
+      const float2 f = unpack2(acc[k][c]);
+      v[2 * c] = f.x;
+      v[2 * c + 1] = f.y;
+    }
     if (p.epi & DCONV_EPI_ADD) {
       const float* sk = sbase + (int64_t)y * p.sk_row + (int64_t)x * kCB;
-      const float4 s0 = *reinterpret_cast<const float4*>(sk);
-      const float4 s1 = *reinterpret_cast<const float4*>(sk + 4);
-      v0.x += s0.x; v0.y += s0.y; v0.z += s0.z; v0.w += s0.w;
-      v1.x += s1.x; v1.y += s1.y; v1.z += s1.z; v1.w += s1.w;
+#pragma unroll
+      for (int c = 0; c < TCO; c += 4) {
+        const float4 s4 = *reinterpret_cast<const float4*>(sk + c);
+        v[c] += s4.x; v[c + 1] += s4.y; v[c + 2] += s4.z; v[c + 3] += s4.w;
+      }
     }
     if (p.epi & DCONV_EPI_RELU) {
-      v0.x = fmaxf(v0.x, 0.f); v0.y = fmaxf(v0.y, 0.f);
-      v0.z = fmaxf(v0.z, 0.f); v0.w = fmaxf(v0.w, 0.f);
-      v1.x = fmaxf(v1.x, 0.f); v1.y = fmaxf(v1.y, 0.f);
-      v1.z = fmaxf(v1.z, 0.f); v1.w = fmaxf(v1.w, 0.f);
+#pragma unroll
+      for (int c = 0; c < TCO; ++c) v[c] = fmaxf(v[c], 0.f);
     }
     float* o = obase + (int64_t)y * p.out_row + (int64_t)x * kCB;
-    *reinterpret_cast<float4*>(o) = v0;
-    *reinterpret_cast<float4*>(o + 4) = v1;
+#pragma unroll
+    for (int c = 0; c < TCO; c += 4)
+      *reinterpret_cast<float4*>(o + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
   }
 }
 
@@ -219,10 +334,9 @@ TilePick pick_tile(int BM, int h_o, int w_o, int s, int h_f, int w_f) {
   int64_t best_patch = 0;
   for (int TW = 4; TW <= BM && TW <= 128; TW *= 2) {
     const int TH = BM / TW;
-    const int64_t tiles =
-        (int64_t)((h_o + TH - 1) / TH) * ((w_o + TW - 1) / TW);
-    const int64_t patch =
-        (int64_t)((TH - 1) * s + h_f) * ((TW - 1) * s + w_f);
+    const int64_t tiles = (int64_t)((h_o + TH - 1) / TH) * ((w_o + TW - 1) / TW);
+    const int64_t patch = (int64_t)((std::min(TH, h_o) - 1) * s + h_f) *
+                          ((std::min(TW, w_o) - 1) * s + w_f);
     if (best.tiles < 0 || tiles < best.tiles ||
         (tiles == best.tiles && patch < best_patch)) {
       best = TilePick{TH, TW, tiles};
@@ -232,8 +346,8 @@ TilePick pick_tile(int BM, int h_o, int w_o, int s, int h_f, int w_f) {
   return best;
 }
 
-template <int BM, int BN>
-int launch(FfmaParams p, cudaStream_t stream) {
+template <int BM, int BN, int TCO, int NW, int WF>
+int launch_variant(FfmaParams p, cudaStream_t stream) {
   constexpr int CG = BN / 8;
   const TilePick t = pick_tile(BM, p.h_o, p.w_o, p.s, p.h_f, p.w_f);
   p.TH = t.TH;
@@ -266,38 +380,60 @@ int launch(FfmaParams p, cudaStream_t stream) {
   p.n_g = (p.ib_n + p.G - 1) / p.G;
   p.n_r = (p.h_f + p.R - 1) / p.R;
   p.patch_floats = p.G * p.PH * p.PW * kCB;
-  p.wstride_floats = p.G * p.R * p.w_f * kCB * kCB + 4;  // +16 B: bank spread
+  // +16 B (TCO 8) / +32 B (TCO 4) per block chunk: the lanes of a warp read
+  // distinct 16-byte bank groups of the weight stage.
+  p.wstride_floats = p.G * p.R * p.w_f * kCB * kCB + (TCO == 8 ? 4 : 8);
   p.stage_floats = p.patch_floats + CG * p.wstride_floats;
   p.stage_floats = (p.stage_floats + 31) & ~31;  // 128-byte aligned stages
   const int stage_bytes = p.stage_floats * 4;
   const int kSmemBudget = 220 * 1024;
-  p.NS = std::min(kMaxStages, (kSmemBudget - 2 * kMaxStages * 8) / stage_bytes);
+  const int bar_bytes = 2 * kMaxStages * 8 + 16;
+  p.NS = std::min(kMaxStages, (kSmemBudget - bar_bytes) / stage_bytes);
   const int S = p.n_g * p.n_r;
   p.NS = std::min(p.NS, std::max(2, S));
+  // partial sums cover >= 256 products before folding into the TMEM total
+  const int k_stage = p.G * p.R * p.w_f * kCB;
+  p.flush_every = std::max(1, (256 + k_stage - 1) / k_stage);
   if (p.NS < 2 || p.PH > 256 || p.PW > 256)
     return dconv_host::set_error(DCONV_EUNSUPPORTED,
                                  "conv_ffma: stage of %d bytes does not fit "
-                                 "shared memory twice",
-                                 stage_bytes);
-  const size_t smem = (size_t)p.NS * stage_bytes + 2 * kMaxStages * 8;
+                                 "shared memory twice", stage_bytes);
+  const size_t smem = (size_t)p.NS * stage_bytes + bar_bytes;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(conv_ffma_kernel<BM, BN>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         227 * 1024);
+    cudaFuncSetAttribute(conv_ffma_kernel<BM, BN, TCO, NW, WF>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = true;
   }
   dim3 grid((unsigned)(p.tiles_per_img * p.n), (unsigned)((p.jb_count + CG - 1) / CG));
-  conv_ffma_kernel<BM, BN><<<grid, kThreads, smem, stream>>>(p);
+  conv_ffma_kernel<BM, BN, TCO, NW, WF><<<grid, NW * 32, smem, stream>>>(p);
   dconv_host::count_launch();
   return dconv_host::check_launch("conv_ffma_kernel");
 }
 
+template <int BM, int BN, int TCO, int NW>
+int launch_wf(const FfmaParams& p, cudaStream_t stream) {
+  switch (p.w_f) {
+    case 1: return launch_variant<BM, BN, TCO, NW, 1>(p, stream);
+    case 3: return launch_variant<BM, BN, TCO, NW, 3>(p, stream);
+    case 5: return launch_variant<BM, BN, TCO, NW, 5>(p, stream);
+    default: return launch_variant<BM, BN, TCO, NW, 0>(p, stream);
+  }
+}
+
 }  // namespace
 
+int ffma_variant_override = -1;  // test/tuning hook (dconv_cuda_set_ffma_variant)
+
 int launch_conv_ffma(const FfmaParams& p, cudaStream_t stream) {
-  if (p.jb_count >= 12) return launch<128, 128>(p, stream);
-  return launch<256, 64>(p, stream);
+  int v = ffma_variant_override;
+  if (v < 0) v = p.jb_count >= 12 ? 1 : 2;
+  switch (v) {
+    case 0: return launch_wf<128, 128, 8, 8>(p, stream);   // 8x8 tile, 8 warps
+    case 1: return launch_wf<128, 128, 4, 16>(p, stream);  // 8x4 tile, 16 warps
+    case 2: return launch_wf<256, 64, 4, 16>(p, stream);   // 8x4 tile, BN = 64
+    default: return launch_wf<256, 64, 8, 8>(p, stream);   // 8x8 tile, BN = 64
+  }
 }
 
 }  // namespace dconv_dev

@@ -25,7 +25,10 @@ struct FfmaParams {
   int TH, TW, THe, TWe, tiles_x, tiles_per_img;
   int G, R, n_g, n_r, PH, PW;
   int slab_floats, patch_floats, wstride_floats, stage_floats, NS;
+  int flush_every;          // stages per partial sum before the TMEM fold
 };
+
+extern int ffma_variant_override;  // -1 = heuristic (dconv_cuda_set_ffma_variant)
 
 int launch_conv_ffma(const FfmaParams& p, cudaStream_t stream);
 

@@ -327,3 +327,23 @@ def test_first_layer_reader_variants(s, f, ci, co):
     for i in range(n):
         want = np.maximum(po.pack_feature_map(po.conv_oracle64(x[i], k, s), 8), 0)
         assert_tol(got[i], want, f"first s={s} f={f} img {i}")
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+def test_ffma_tile_variants(variant):
+    """Every FFMA tile variant (thread tile 8x8 / 8x4, 8 / 16 warps, BN 128 /
+    64) on ragged shapes, strides, filter widths 1/3/5/7 (templated and
+    runtime), and a K = 4608 layer where the TMEM two-level sum matters."""
+    lib = _abi.lib()
+    _abi.check(lib.dconv_cuda_set_ffma_variant(variant))
+    try:
+        cases = [(64, 64, 58, 58, 3, 1), (24, 40, 17, 23, 5, 1), (16, 136, 19, 21, 7, 2),
+                 (96, 72, 12, 31, 1, 2), (512, 128, 16, 16, 3, 1), (200, 16, 9, 9, 3, 2)]
+        for t, (ci, co, hi, wi, f, s) in enumerate(cases):
+            x = po.uniform((ci, hi, wi), 7000 + t, variant)
+            k = po.uniform((ci, co, f, f), 7000 + t, 10 + variant)
+            want = po.pack_feature_map(po.conv_oracle64(x, k, s), 8)
+            assert_tol(run_conv(x, k, s, 8, 8, algo=_abi.ALGO_FFMA), want,
+                       f"variant {variant} case {t}")
+    finally:
+        lib.dconv_cuda_set_ffma_variant(-1)
