@@ -338,7 +338,7 @@ def test_ffma_tile_variants(variant):
     _abi.check(lib.dconv_cuda_set_ffma_variant(variant))
     try:
         cases = [(64, 64, 58, 58, 3, 1), (24, 40, 17, 23, 5, 1), (16, 136, 19, 21, 7, 2),
-                 (96, 72, 12, 31, 1, 2), (512, 128, 16, 16, 3, 1), (200, 16, 9, 9, 3, 2)]
+                 (96, 72, 13, 31, 1, 2), (512, 128, 16, 16, 3, 1), (200, 16, 9, 9, 3, 2)]
         for t, (ci, co, hi, wi, f, s) in enumerate(cases):
             x = po.uniform((ci, hi, wi), 7000 + t, variant)
             k = po.uniform((ci, co, f, f), 7000 + t, 10 + variant)
