@@ -160,8 +160,8 @@ int dconv_cuda_zero(float* x, int64_t count, void* stream);
 
 /* Tile selector override for the FFMA kernel (the GPU analogue of the
  * reference's BlockingParams choice, model.hpp:85-109): -1 = heuristic,
- * 0 = 128px x 128ch / 8x8 thread tile / 8 warps, 1 = 128 x 128 / 8x4 / 16
- * warps, 2 = 256 x 64 / 8x4 / 16 warps, 3 = 256 x 64 / 8x8 / 8 warps.
+ * 0 = CTA tile 128 pixels x 128 channels, 1 = 256 pixels x 64 channels
+ * (8x8 register tile per thread in both).
  * Process-wide; used by tests and the autotuner. */
 int dconv_cuda_set_ffma_variant(int variant);
 

@@ -27,6 +27,7 @@
 // once, from registers (smem ring and TMEM are on-chip).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "conv_kernels.h"
@@ -37,6 +38,8 @@ namespace {
 
 constexpr int kCB = 8;          // channel block of this kernel (c_ib = c_ob)
 constexpr int kMaxStages = 8;
+constexpr int kComputeWarps = 8;  // 2 compute warpgroups, 8x8 outputs / thread
+constexpr int kThreads = (kComputeWarps + 4) * 32;  // + producer warpgroup
 constexpr int kTmemCols = 128;  // running totals: NW/4 slots x 8*TCO columns
 
 // ---- TMEM helpers (32 lanes x 32 columns of 32-bit per warp) ----------------
@@ -101,16 +104,17 @@ __device__ __forceinline__ void tmem_fold(uint32_t taddr, uint64_t* acc,
   }
 }
 
-template <int BM, int BN, int TCO, int NW, int WF>
-__global__ void __launch_bounds__(NW * 32, 1)
+template <int BM, int BN, int WF>
+__global__ void __launch_bounds__(kThreads, 1)
     conv_ffma_kernel(const FfmaParams p) {
-  constexpr int PG = BM / 8;    // pixel groups (8 pixels each)
-  constexpr int CGT = BN / TCO; // channel thread groups (TCO channels each)
-  constexpr int WPG = PG / 4;   // warps along pixels
+  constexpr int TCO = 8;         // channels per thread (one output block)
+  constexpr int NW = kComputeWarps;
+  constexpr int PG = BM / 8;     // pixel groups (8 pixels each)
+  constexpr int CGT = BN / TCO;  // channel thread groups == output blocks
+  constexpr int WPG = PG / 4;    // warps along pixels
   constexpr int NP = 8 * TCO / 2;  // accumulator pairs per thread
   static_assert(PG * CGT == NW * 32, "thread tile mismatch");
-  static_assert(TCO == 4 || TCO == 8, "TCO");
-  constexpr int CG = BN / 8;    // output blocks per CTA
+  constexpr int CG = BN / 8;     // output blocks per CTA tile
 
   extern __shared__ __align__(128) float smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.NS * p.stage_floats);
@@ -119,13 +123,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int img = blockIdx.x / p.tiles_per_img;
-  const int tile = blockIdx.x - img * p.tiles_per_img;
-  const int ty0 = (tile / p.tiles_x) * p.TH;
-  const int tx0 = (tile % p.tiles_x) * p.TW;
-  const int jb0 = p.jb_begin + blockIdx.y * CG;
-  const int cg_valid = min(CG, p.jb_begin + p.jb_count - jb0);
-  const int S = p.n_g * p.n_r;
+  const int S = p.n_g * p.n_r;                 // stages per work unit
+  const int co_groups = (p.jb_count + CG - 1) / CG;
+  const int n_units = p.tiles_per_img * p.n * co_groups;
   const bool use_tmem = S > p.flush_every;
 
   if (tid == 0) {
@@ -145,54 +145,74 @@ __global__ void __launch_bounds__(NW * 32, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
-  // ------------------------------------------------------------ producer
-  // Warp 0 doubles as the producer: it issues stage st+NS-1 before computing
-  // stage st (the buffer it refills was released by every warp at the end of
-  // stage st-1), so no warp slot is spent on a copy-only warp and all NW
-  // warps keep the full per-SMSP register budget.
-  const float* in_img = p.in + (int64_t)img * p.in_img;
-  const int col0 = tx0 * p.s;
-  const int cols = min(p.PW, p.w_i - col0);
-  auto issue = [&](int st) {
-    const int buf = st % p.NS;
-    if (st >= p.NS) mbar_wait(&empty[buf], ((st / p.NS) - 1) & 1);
-    const int g = st / p.n_r, r = st - g * p.n_r;
-    const int ib0 = g * p.G, Ge = min(p.G, p.ib_n - ib0);
-    const int n0 = r * p.R, Re = min(p.R, p.h_f - n0);
-    const int row0 = ty0 * p.s + n0;
-    const int rows = min((p.THe - 1) * p.s + Re, p.h_i - row0);
-    const uint32_t patch_bytes = (uint32_t)(Ge * rows * cols * kCB * 4);
-    const uint32_t wbytes = (uint32_t)(Re * p.w_f * kCB * kCB * 4) * Ge;
-    float* sp = smem + buf * p.stage_floats;
-    float* sw = sp + p.patch_floats;
-    if (lane == 0) mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes * cg_valid);
-    __syncwarp();
-    const int n_patch = Ge * rows;
-    const int tasks = n_patch + cg_valid;
-    for (int t = lane; t < tasks; t += 32) {
-      if (t < n_patch) {
-        const int gi = t / rows, pr = t - gi * rows;
-        const float* src = in_img + (int64_t)(ib0 + gi) * p.in_blk +
-                           (int64_t)(row0 + pr) * p.in_row + (int64_t)col0 * kCB;
-        float* dst = sp + ((gi * p.PH + pr) * p.PW) * kCB;
-        bulk_g2s(dst, src, (uint32_t)(cols * kCB * 4), &full[buf]);
-      } else {
-        const int c = t - n_patch;
-        const float* src = p.w + ((int64_t)(jb0 + c) * p.ib_n + ib0) * p.slab_floats +
-                           (int64_t)n0 * p.w_f * kCB * kCB;
-        bulk_g2s(sw + c * p.wstride_floats, src, wbytes, &full[buf]);
+  // unit u -> (co group fastest: concurrently running CTAs share the pixel
+  // tile's patch rows in L2, consecutive waves reuse the weight slabs)
+  auto decode = [&](int u, int& img, int& ty0, int& tx0, int& jb0, int& cg_valid) {
+    const int cgi = u % co_groups;
+    const int t = u / co_groups;
+    img = t / p.tiles_per_img;
+    const int tile = t - img * p.tiles_per_img;
+    ty0 = (tile / p.tiles_x) * p.TH;
+    tx0 = (tile % p.tiles_x) * p.TW;
+    jb0 = p.jb_begin + cgi * CG;
+    cg_valid = min(CG, p.jb_begin + p.jb_count - jb0);
+  };
+
+  if (warp >= NW) {
+    // ------------------------------------------------------------ producer
+    // One warpgroup, register budget handed to the compute warpgroups; its
+    // first warp streams every stage of every unit of this CTA through the
+    // NS-deep ring (prefetch runs across unit boundaries, so the epilogue of
+    // one tile overlaps the loads of the next).
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    if (warp != NW) return;
+    int gs = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      int img, ty0, tx0, jb0, cg_valid;
+      decode(u, img, ty0, tx0, jb0, cg_valid);
+      const float* in_img = p.in + (int64_t)img * p.in_img;
+      const int col0 = tx0 * p.s;
+      const int cols = min(p.PW, p.w_i - col0);
+      for (int st = 0; st < S; ++st, ++gs) {
+        const int buf = gs % p.NS;
+        if (gs >= p.NS) mbar_wait(&empty[buf], ((gs / p.NS) - 1) & 1);
+        const int g = st / p.n_r, r = st - g * p.n_r;
+        const int ib0 = g * p.G, Ge = min(p.G, p.ib_n - ib0);
+        const int n0 = r * p.R, Re = min(p.R, p.h_f - n0);
+        const int row0 = ty0 * p.s + n0;
+        const int rows = min((p.THe - 1) * p.s + Re, p.h_i - row0);
+        const uint32_t patch_bytes = (uint32_t)(Ge * rows * cols * kCB * 4);
+        const uint32_t wbytes = (uint32_t)(Re * p.w_f * kCB * kCB * 4) * Ge;
+        float* sp = smem + buf * p.stage_floats;
+        float* sw = sp + p.patch_floats;
+        if (lane == 0) mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes * cg_valid);
+        __syncwarp();
+        const int n_patch = Ge * rows;
+        const int tasks = n_patch + cg_valid;
+        for (int t = lane; t < tasks; t += 32) {
+          if (t < n_patch) {
+            const int gi = t / rows, pr = t - gi * rows;
+            const float* src = in_img + (int64_t)(ib0 + gi) * p.in_blk +
+                               (int64_t)(row0 + pr) * p.in_row + (int64_t)col0 * kCB;
+            float* dst = sp + ((gi * p.PH + pr) * p.PW) * kCB;
+            bulk_g2s(dst, src, (uint32_t)(cols * kCB * 4), &full[buf]);
+          } else {
+            const int c = t - n_patch;
+            const float* src = p.w + ((int64_t)(jb0 + c) * p.ib_n + ib0) * p.slab_floats +
+                               (int64_t)n0 * p.w_f * kCB * kCB;
+            bulk_g2s(sw + c * p.wstride_floats, src, wbytes, &full[buf]);
+          }
+        }
       }
     }
-  };
-  if (warp == 0)
-    for (int st = 0; st < min(S, p.NS - 1); ++st) issue(st);
+    return;
+  }
 
   // -------------------------------------------------------------- consumers
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
   const int wr = warp % WPG, wc = warp / WPG;
   const int pg = wr * 4 + (lane & 3);
-  const int cgt = wc * 8 + (lane >> 2);
-  const int cb = TCO == 8 ? cgt : (cgt >> 1);          // output block in CTA
-  const int cofs = TCO == 8 ? 0 : (cgt & 1) * 4;       // channel offset in block
+  const int cb = wc * 8 + (lane >> 2);  // output block within the CTA tile
 
   int poff[8];
 #pragma unroll
@@ -201,126 +221,128 @@ __global__ void __launch_bounds__(NW * 32, 1)
     const int ty = q / p.TW, tx = q - (q / p.TW) * p.TW;
     poff[k] = (ty < p.THe && tx < p.TWe) ? (ty * p.s * p.PW + tx * p.s) * kCB : 0;
   }
-
-  uint64_t acc[8][TCO / 2];
-#pragma unroll
-  for (int k = 0; k < 8; ++k)
-#pragma unroll
-    for (int c = 0; c < TCO / 2; ++c) acc[k][c] = 0ull;
-
   const uint32_t tmem_base = use_tmem ? *tmem_slot : 0u;
   const uint32_t taddr = tmem_base + ((uint32_t)((warp & 3) * 32) << 16) +
                          (uint32_t)((warp >> 2) * 8 * TCO);
-  bool have_total = false;
-
   const int wf = WF > 0 ? WF : p.w_f;
-  for (int st = 0; st < S; ++st) {
-    if (warp == 0 && st + p.NS - 1 < S) issue(st + p.NS - 1);
-    const int buf = st % p.NS;
-    mbar_wait(&full[buf], (st / p.NS) & 1);
-    const int g = st / p.n_r, r = st - g * p.n_r;
-    const int Ge = min(p.G, p.ib_n - g * p.G);
-    const int Re = min(p.R, p.h_f - r * p.R);
-    const float* sp = smem + buf * p.stage_floats;
-    const float* sw = sp + p.patch_floats + cb * p.wstride_floats + cofs;
-    for (int gi = 0; gi < Ge; ++gi) {
-      for (int n = 0; n < Re; ++n) {
-        const float* pa_row = sp + ((gi * p.PH + n) * p.PW) * kCB;
-        const float* pw_row = sw + ((gi * p.R + n) * wf) * (kCB * kCB);
+
+  int gs = 0;
+  for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    int img, ty0, tx0, jb0, cg_valid;
+    decode(u, img, ty0, tx0, jb0, cg_valid);
+    uint64_t acc[8][TCO / 2];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int c = 0; c < TCO / 2; ++c) acc[k][c] = 0ull;
+    bool have_total = false;
+
+    for (int st = 0; st < S; ++st, ++gs) {
+      const int buf = gs % p.NS;
+      mbar_wait(&full[buf], (gs / p.NS) & 1);
+      const int g = st / p.n_r, r = st - g * p.n_r;
+      const int Ge = min(p.G, p.ib_n - g * p.G);
+      const int Re = min(p.R, p.h_f - r * p.R);
+      const float* sp = smem + buf * p.stage_floats;
+      const float* sw = sp + p.patch_floats + cb * p.wstride_floats;
+      for (int gi = 0; gi < Ge; ++gi) {
+        for (int n = 0; n < Re; ++n) {
+          const float* pa_row = sp + ((gi * p.PH + n) * p.PW) * kCB;
+          const float* pw_row = sw + ((gi * p.R + n) * wf) * (kCB * kCB);
 #pragma unroll(WF > 0 ? WF : 1)
-        for (int m = 0; m < wf; ++m) {
-          const float* pa = pa_row + m * kCB;
-          const float* pw = pw_row + m * (kCB * kCB);
+          for (int m = 0; m < wf; ++m) {
+            const float* pa = pa_row + m * kCB;
+            const float* pw = pw_row + m * (kCB * kCB);
 #pragma unroll
-          for (int half = 0; half < 2; ++half) {
-            float4 a[8];
+            for (int half = 0; half < 2; ++half) {
+              float4 a[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) a[k] = lds128(pa + poff[k] + half * 4);
+              for (int k = 0; k < 8; ++k) a[k] = lds128(pa + poff[k] + half * 4);
 #pragma unroll
-            for (int i4 = 0; i4 < 4; ++i4) {
-              const float* pb = pw + (half * 4 + i4) * kCB;
-              const float4 b0 = lds128(pb);
-              uint64_t bp[TCO / 2];
-              bp[0] = pack2(b0.x, b0.y);
-              bp[1] = pack2(b0.z, b0.w);
-              if constexpr (TCO == 8) {
+              for (int i4 = 0; i4 < 4; ++i4) {
+                const float* pb = pw + (half * 4 + i4) * kCB;
+                const float4 b0 = lds128(pb);
                 const float4 b1 = lds128(pb + 4);
+                uint64_t bp[4];
+                bp[0] = pack2(b0.x, b0.y);
+                bp[1] = pack2(b0.z, b0.w);
                 bp[2] = pack2(b1.x, b1.y);
                 bp[3] = pack2(b1.z, b1.w);
-              }
 #pragma unroll
-              for (int k = 0; k < 8; ++k) {
-                const float av = i4 == 0 ? a[k].x : i4 == 1 ? a[k].y : i4 == 2 ? a[k].z : a[k].w;
+                for (int k = 0; k < 8; ++k) {
+                  const float av = i4 == 0 ? a[k].x : i4 == 1 ? a[k].y : i4 == 2 ? a[k].z : a[k].w;
 #pragma unroll
-                for (int c = 0; c < TCO / 2; ++c) ffma2(acc[k][c], av, bp[c]);
+                  for (int c = 0; c < 4; ++c) ffma2(acc[k][c], av, bp[c]);
+                }
               }
             }
           }
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[buf]);
+      // fold the partial sum into the TMEM running total every flush_every
+      // stages (never after the last stage: the epilogue folds it)
+      if (use_tmem && (st + 1) % p.flush_every == 0 && st + 1 < S) {
+        tmem_fold<NP>(taddr, &acc[0][0], have_total, true);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        have_total = true;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+          for (int c = 0; c < TCO / 2; ++c) acc[k][c] = 0ull;
+      }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[buf]);
-    // fold the partial sum into the TMEM running total every flush_every
-    // stages (never after the last stage: the epilogue folds it)
-    if (use_tmem && (st + 1) % p.flush_every == 0 && st + 1 < S) {
-      tmem_fold<NP>(taddr, &acc[0][0], have_total, true);
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      have_total = true;
+    if (have_total) tmem_fold<NP>(taddr, &acc[0][0], true, false);
+
+    // ------------------------------------------------------------ epilogue
+    if (cb < cg_valid) {
+      const int jl = jb0 + cb - p.jb_begin;  // block index within the output view
+      float* obase = p.out + (int64_t)img * p.out_img + (int64_t)jl * p.out_blk;
+      const float* sbase =
+          p.skip ? p.skip + (int64_t)img * p.sk_img + (int64_t)jl * p.sk_blk : nullptr;
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
+      for (int k = 0; k < 8; ++k) {
+        const int q = pg + PG * k;
+        const int ty = q / p.TW, tx = q - (q / p.TW) * p.TW;
+        const int y = ty0 + ty, x = tx0 + tx;
+        if (y >= p.h_o || x >= p.w_o) continue;
+        float v[TCO];
 #pragma unroll
-        for (int c = 0; c < TCO / 2; ++c) acc[k][c] = 0ull;
+        for (int c = 0; c < TCO / 2; ++c) {
+          const float2 f = unpack2(acc[k][c]);
+          v[2 * c] = f.x;
+          v[2 * c + 1] = f.y;
+        }
+        if (p.epi & DCONV_EPI_ADD) {
+          const float* sk = sbase + (int64_t)y * p.sk_row + (int64_t)x * kCB;
+#pragma unroll
+          for (int c = 0; c < TCO; c += 4) {
+            const float4 s4 = *reinterpret_cast<const float4*>(sk + c);
+            v[c] += s4.x; v[c + 1] += s4.y; v[c + 2] += s4.z; v[c + 3] += s4.w;
+          }
+        }
+        if (p.epi & DCONV_EPI_RELU) {
+#pragma unroll
+          for (int c = 0; c < TCO; ++c) v[c] = fmaxf(v[c], 0.f);
+        }
+        float* o = obase + (int64_t)y * p.out_row + (int64_t)x * kCB;
+#pragma unroll
+        for (int c = 0; c < TCO; c += 4)
+          *reinterpret_cast<float4*>(o + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+      }
     }
   }
-  if (have_total) tmem_fold<NP>(taddr, &acc[0][0], true, false);
 
   if (use_tmem) {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    // all warps are done with TMEM before warp 0 frees it
-    __syncthreads();
+    // every compute warp is done with TMEM before warp 0 frees it
+    asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
     if (warp == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                    "n"(kTmemCols));
     }
-  }
-
-  // -------------------------------------------------------------- epilogue
-  if (cb >= cg_valid) return;
-  const int jl = jb0 + cb - p.jb_begin;  // block index within the output view
-  float* obase = p.out + (int64_t)img * p.out_img + (int64_t)jl * p.out_blk + cofs;
-  const float* sbase =
-      p.skip ? p.skip + (int64_t)img * p.sk_img + (int64_t)jl * p.sk_blk + cofs : nullptr;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int q = pg + PG * k;
-    const int ty = q / p.TW, tx = q - (q / p.TW) * p.TW;
-    const int y = ty0 + ty, x = tx0 + tx;
-    if (y >= p.h_o || x >= p.w_o) continue;
-    float v[TCO];
-#pragma unroll
-    for (int c = 0; c < TCO / 2; ++c) {
-      const float2 f = unpack2(acc[k][c]);
-      v[2 * c] = f.x;
-      v[2 * c + 1] = f.y;
-    }
-    if (p.epi & DCONV_EPI_ADD) {
-      const float* sk = sbase + (int64_t)y * p.sk_row + (int64_t)x * kCB;
-#pragma unroll
-      for (int c = 0; c < TCO; c += 4) {
-        const float4 s4 = *reinterpret_cast<const float4*>(sk + c);
-        v[c] += s4.x; v[c + 1] += s4.y; v[c + 2] += s4.z; v[c + 3] += s4.w;
-      }
-    }
-    if (p.epi & DCONV_EPI_RELU) {
-#pragma unroll
-      for (int c = 0; c < TCO; ++c) v[c] = fmaxf(v[c], 0.f);
-    }
-    float* o = obase + (int64_t)y * p.out_row + (int64_t)x * kCB;
-#pragma unroll
-    for (int c = 0; c < TCO; c += 4)
-      *reinterpret_cast<float4*>(o + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
   }
 }
 
@@ -346,7 +368,7 @@ TilePick pick_tile(int BM, int h_o, int w_o, int s, int h_f, int w_f) {
   return best;
 }
 
-template <int BM, int BN, int TCO, int NW, int WF>
+template <int BM, int BN, int WF>
 int launch_variant(FfmaParams p, cudaStream_t stream) {
   constexpr int CG = BN / 8;
   const TilePick t = pick_tile(BM, p.h_o, p.w_o, p.s, p.h_f, p.w_f);
@@ -380,9 +402,9 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   p.n_g = (p.ib_n + p.G - 1) / p.G;
   p.n_r = (p.h_f + p.R - 1) / p.R;
   p.patch_floats = p.G * p.PH * p.PW * kCB;
-  // +16 B (TCO 8) / +32 B (TCO 4) per block chunk: the lanes of a warp read
-  // distinct 16-byte bank groups of the weight stage.
-  p.wstride_floats = p.G * p.R * p.w_f * kCB * kCB + (TCO == 8 ? 4 : 8);
+  // +16 B per block chunk: the 8 lanes of a warp that read different output
+  // blocks hit distinct 16-byte bank groups of the weight stage.
+  p.wstride_floats = p.G * p.R * p.w_f * kCB * kCB + 4;
   p.stage_floats = p.patch_floats + CG * p.wstride_floats;
   p.stage_floats = (p.stage_floats + 31) & ~31;  // 128-byte aligned stages
   const int stage_bytes = p.stage_floats * 4;
@@ -394,30 +416,37 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   // partial sums cover >= 256 products before folding into the TMEM total
   const int k_stage = p.G * p.R * p.w_f * kCB;
   p.flush_every = std::max(1, (256 + k_stage - 1) / k_stage);
+  if (const char* e = getenv("DCONV_FLUSH_EVERY")) p.flush_every = std::max(1, atoi(e));
   if (p.NS < 2 || p.PH > 256 || p.PW > 256)
     return dconv_host::set_error(DCONV_EUNSUPPORTED,
                                  "conv_ffma: stage of %d bytes does not fit "
                                  "shared memory twice", stage_bytes);
   const size_t smem = (size_t)p.NS * stage_bytes + bar_bytes;
   static bool attr_set = false;
+  static int sms = 0;
   if (!attr_set) {
-    cudaFuncSetAttribute(conv_ffma_kernel<BM, BN, TCO, NW, WF>,
+    cudaFuncSetAttribute(conv_ffma_kernel<BM, BN, WF>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     attr_set = true;
   }
-  dim3 grid((unsigned)(p.tiles_per_img * p.n), (unsigned)((p.jb_count + CG - 1) / CG));
-  conv_ffma_kernel<BM, BN, TCO, NW, WF><<<grid, NW * 32, smem, stream>>>(p);
+  // persistent: one CTA per SM walks the work units round-robin
+  const int64_t units = (int64_t)p.tiles_per_img * p.n * ((p.jb_count + CG - 1) / CG);
+  const int grid = (int)std::min<int64_t>(units, sms);
+  conv_ffma_kernel<BM, BN, WF><<<grid, kThreads, smem, stream>>>(p);
   dconv_host::count_launch();
   return dconv_host::check_launch("conv_ffma_kernel");
 }
 
-template <int BM, int BN, int TCO, int NW>
+template <int BM, int BN>
 int launch_wf(const FfmaParams& p, cudaStream_t stream) {
   switch (p.w_f) {
-    case 1: return launch_variant<BM, BN, TCO, NW, 1>(p, stream);
-    case 3: return launch_variant<BM, BN, TCO, NW, 3>(p, stream);
-    case 5: return launch_variant<BM, BN, TCO, NW, 5>(p, stream);
-    default: return launch_variant<BM, BN, TCO, NW, 0>(p, stream);
+    case 1: return launch_variant<BM, BN, 1>(p, stream);
+    case 3: return launch_variant<BM, BN, 3>(p, stream);
+    case 5: return launch_variant<BM, BN, 5>(p, stream);
+    default: return launch_variant<BM, BN, 0>(p, stream);
   }
 }
 
@@ -427,12 +456,10 @@ int ffma_variant_override = -1;  // test/tuning hook (dconv_cuda_set_ffma_varian
 
 int launch_conv_ffma(const FfmaParams& p, cudaStream_t stream) {
   int v = ffma_variant_override;
-  if (v < 0) v = p.jb_count >= 12 ? 1 : 2;
+  if (v < 0) v = p.jb_count >= 16 ? 0 : 1;
   switch (v) {
-    case 0: return launch_wf<128, 128, 8, 8>(p, stream);   // 8x8 tile, 8 warps
-    case 1: return launch_wf<128, 128, 4, 16>(p, stream);  // 8x4 tile, 16 warps
-    case 2: return launch_wf<256, 64, 4, 16>(p, stream);   // 8x4 tile, BN = 64
-    default: return launch_wf<256, 64, 8, 8>(p, stream);   // 8x8 tile, BN = 64
+    case 0: return launch_wf<128, 128>(p, stream);  // 128 px x 128 channels
+    default: return launch_wf<256, 64>(p, stream);  // 256 px x 64 channels
   }
 }
 

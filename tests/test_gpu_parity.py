@@ -329,11 +329,11 @@ def test_first_layer_reader_variants(s, f, ci, co):
         assert_tol(got[i], want, f"first s={s} f={f} img {i}")
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("variant", [0, 1])
 def test_ffma_tile_variants(variant):
-    """Every FFMA tile variant (thread tile 8x8 / 8x4, 8 / 16 warps, BN 128 /
-    64) on ragged shapes, strides, filter widths 1/3/5/7 (templated and
-    runtime), and a K = 4608 layer where the TMEM two-level sum matters."""
+    """Both FFMA CTA tiles (128 px x 128 ch, 256 px x 64 ch) on ragged shapes,
+    strides, filter widths 1/3/5/7 (templated and runtime), and a K = 4608
+    layer where the TMEM two-level sum matters."""
     lib = _abi.lib()
     _abi.check(lib.dconv_cuda_set_ffma_variant(variant))
     try:
