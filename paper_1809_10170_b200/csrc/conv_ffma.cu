@@ -3,7 +3,8 @@
 // GPU restatement of Alg. 3 in the blocked layout with
 // c_ib = c_ob = 8 (one 32-byte pencil = one DRAM sector per pixel):
 //   * j' (output blocks, "in Parallel")      -> blockIdx.y, BN/8 blocks per CTA
-//   * l, k' (output rows / row tiles)        -> blockIdx.x, a TH x TW pixel tile
+//   * l, k' (output rows / row tiles)        -> work unit: TH x TW pixel tile of
+//                                               the batch-stacked output
 //   * i' (input blocks, cache blocking)      -> the shared-memory pipeline stage
 //   * (n, m, ii) reduction                   -> per-stage loop from smem
 //   * (kk, jj) register tile                 -> 8 pixels x TCO channels / thread
@@ -104,6 +105,43 @@ __device__ __forceinline__ void tmem_fold(uint32_t taddr, uint64_t* acc,
   }
 }
 
+// Pixel tiles live on the batch-stacked "virtual image": image i occupies
+// virtual output rows [i*h_o, (i+1)*h_o).  A TH x TW tile starting at virtual
+// row vy0 therefore covers a run of row segments -- the tail of image img0,
+// then whole images, then the head of another -- so maps of any height
+// (56, 28, 14, 7, 13 ...) fill whole tiles.  In shared memory the patch rows
+// of the segments are stacked: segment 0 holds (cnt0-1)*s + R rows, every
+// later segment (h_o-1)*s + R rows.
+struct TileRows {
+  int vy0, img0, y0, cnt0, th;  // th: valid virtual rows of this tile
+};
+
+__device__ __forceinline__ TileRows tile_rows(const FfmaParams& p, int tile_y) {
+  TileRows t;
+  t.vy0 = tile_y * p.TH;
+  t.img0 = t.vy0 / p.h_o;
+  t.y0 = t.vy0 - t.img0 * p.h_o;
+  t.th = min(p.TH, p.n * p.h_o - t.vy0);
+  t.cnt0 = min(p.h_o - t.y0, t.th);
+  return t;
+}
+
+// tile row ty -> (image, output row, first patch row)
+__device__ __forceinline__ void tile_row(const FfmaParams& p, const TileRows& t, int ty,
+                                         int& img, int& y, int& prow) {
+  if (ty < t.cnt0) {
+    img = t.img0;
+    y = t.y0 + ty;
+    prow = ty * p.s;
+  } else {
+    const int d = ty - t.cnt0;
+    const int j = d / p.h_o;  // full segments before this one (segment j+1)
+    y = d - j * p.h_o;
+    img = t.img0 + 1 + j;
+    prow = (t.cnt0 - 1) * p.s + p.R + j * ((p.h_o - 1) * p.s + p.R) + y * p.s;
+  }
+}
+
 template <int BM, int BN, int WF>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_ffma_kernel(const FfmaParams p) {
@@ -125,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = tid >> 5, lane = tid & 31;
   const int S = p.n_g * p.n_r;                 // stages per work unit
   const int co_groups = (p.jb_count + CG - 1) / CG;
-  const int n_units = p.tiles_per_img * p.n * co_groups;
+  const int n_units = p.tiles_y * p.tiles_x * co_groups;
   const bool use_tmem = S > p.flush_every;
 
   if (tid == 0) {
@@ -147,13 +185,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // unit u -> (co group fastest: concurrently running CTAs share the pixel
   // tile's patch rows in L2, consecutive waves reuse the weight slabs)
-  auto decode = [&](int u, int& img, int& ty0, int& tx0, int& jb0, int& cg_valid) {
+  auto decode = [&](int u, TileRows& tr, int& tx0, int& jb0, int& cg_valid) {
     const int cgi = u % co_groups;
     const int t = u / co_groups;
-    img = t / p.tiles_per_img;
-    const int tile = t - img * p.tiles_per_img;
-    ty0 = (tile / p.tiles_x) * p.TH;
-    tx0 = (tile % p.tiles_x) * p.TW;
+    const int tile_y = t / p.tiles_x;
+    tr = tile_rows(p, tile_y);
+    tx0 = (t - tile_y * p.tiles_x) * p.TW;
     jb0 = p.jb_begin + cgi * CG;
     cg_valid = min(CG, p.jb_begin + p.jb_count - jb0);
   };
@@ -167,41 +204,54 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
     if (warp != NW) return;
     int gs = 0;
+    const int seg_rows_full = (p.h_o - 1) * p.s;  // + Re per full segment
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-      int img, ty0, tx0, jb0, cg_valid;
-      decode(u, img, ty0, tx0, jb0, cg_valid);
-      const float* in_img = p.in + (int64_t)img * p.in_img;
+      TileRows tr;
+      int tx0, jb0, cg_valid;
+      decode(u, tr, tx0, jb0, cg_valid);
       const int col0 = tx0 * p.s;
       const int cols = min(p.PW, p.w_i - col0);
+      const int n_seg = 1 + (tr.th - tr.cnt0 + p.h_o - 1) / p.h_o;
       for (int st = 0; st < S; ++st, ++gs) {
         const int buf = gs % p.NS;
         if (gs >= p.NS) mbar_wait(&empty[buf], ((gs / p.NS) - 1) & 1);
         const int g = st / p.n_r, r = st - g * p.n_r;
         const int ib0 = g * p.G, Ge = min(p.G, p.ib_n - ib0);
         const int n0 = r * p.R, Re = min(p.R, p.h_f - n0);
-        const int row0 = ty0 * p.s + n0;
-        const int rows = min((p.THe - 1) * p.s + Re, p.h_i - row0);
-        const uint32_t patch_bytes = (uint32_t)(Ge * rows * cols * kCB * 4);
+        // rows of each segment this stage: (cnt-1)*s + Re
+        const int rows_first = (tr.cnt0 - 1) * p.s + Re;
+        const int rest = tr.th - tr.cnt0;  // rows in later segments
+        const int n_full = rest / p.h_o, last_cnt = rest - n_full * p.h_o;
+        const int total_rows = rows_first + n_full * (seg_rows_full + Re) +
+                               (last_cnt ? (last_cnt - 1) * p.s + Re : 0);
+        const uint32_t patch_bytes = (uint32_t)(Ge * total_rows * cols * kCB * 4);
         const uint32_t wbytes = (uint32_t)(Re * p.w_f * kCB * kCB * 4) * Ge;
         float* sp = smem + buf * p.stage_floats;
         float* sw = sp + p.patch_floats;
         if (lane == 0) mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes * cg_valid);
         __syncwarp();
-        const int n_patch = Ge * rows;
-        const int tasks = n_patch + cg_valid;
-        for (int t = lane; t < tasks; t += 32) {
-          if (t < n_patch) {
-            const int gi = t / rows, pr = t - gi * rows;
-            const float* src = in_img + (int64_t)(ib0 + gi) * p.in_blk +
-                               (int64_t)(row0 + pr) * p.in_row + (int64_t)col0 * kCB;
-            float* dst = sp + ((gi * p.PH + pr) * p.PW) * kCB;
-            bulk_g2s(dst, src, (uint32_t)(cols * kCB * 4), &full[buf]);
+        for (int j = 0; j < n_seg; ++j) {
+          int img, y_start, rows, prow0;
+          if (j == 0) {
+            img = tr.img0; y_start = tr.y0; rows = rows_first; prow0 = 0;
           } else {
-            const int c = t - n_patch;
-            const float* src = p.w + ((int64_t)(jb0 + c) * p.ib_n + ib0) * p.slab_floats +
-                               (int64_t)n0 * p.w_f * kCB * kCB;
-            bulk_g2s(sw + c * p.wstride_floats, src, wbytes, &full[buf]);
+            const int cnt = min(p.h_o, rest - (j - 1) * p.h_o);
+            img = tr.img0 + j; y_start = 0; rows = (cnt - 1) * p.s + Re;
+            prow0 = (tr.cnt0 - 1) * p.s + p.R + (j - 1) * (seg_rows_full + p.R);
           }
+          const float* src0 = p.in + (int64_t)img * p.in_img +
+                              (int64_t)(y_start * p.s + n0) * p.in_row + (int64_t)col0 * kCB;
+          for (int t = lane; t < Ge * rows; t += 32) {
+            const int gi = t / rows, pr = t - gi * rows;
+            const float* src = src0 + (int64_t)(ib0 + gi) * p.in_blk + (int64_t)pr * p.in_row;
+            float* dst = sp + ((gi * p.PH + prow0 + pr) * p.PW) * kCB;
+            bulk_g2s(dst, src, (uint32_t)(cols * kCB * 4), &full[buf]);
+          }
+        }
+        for (int c = lane; c < cg_valid; c += 32) {
+          const float* src = p.w + ((int64_t)(jb0 + c) * p.ib_n + ib0) * p.slab_floats +
+                             (int64_t)n0 * p.w_f * kCB * kCB;
+          bulk_g2s(sw + c * p.wstride_floats, src, wbytes, &full[buf]);
         }
       }
     }
@@ -214,13 +264,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int pg = wr * 4 + (lane & 3);
   const int cb = wc * 8 + (lane >> 2);  // output block within the CTA tile
 
-  int poff[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int q = pg + PG * k;
-    const int ty = q / p.TW, tx = q - (q / p.TW) * p.TW;
-    poff[k] = (ty < p.THe && tx < p.TWe) ? (ty * p.s * p.PW + tx * p.s) * kCB : 0;
-  }
   const uint32_t tmem_base = use_tmem ? *tmem_slot : 0u;
   const uint32_t taddr = tmem_base + ((uint32_t)((warp & 3) * 32) << 16) +
                          (uint32_t)((warp >> 2) * 8 * TCO);
@@ -228,8 +271,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   int gs = 0;
   for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-    int img, ty0, tx0, jb0, cg_valid;
-    decode(u, img, ty0, tx0, jb0, cg_valid);
+    TileRows tr;
+    int tx0, jb0, cg_valid;
+    decode(u, tr, tx0, jb0, cg_valid);
+    // per-pixel patch offsets of this tile (pixels that do not exist read
+    // offset 0 and are never stored)
+    int poff[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int q = pg + PG * k;
+      const int ty = q / p.TW, tx = q - ty * p.TW;
+      int img, y, prow;
+      tile_row(p, tr, ty, img, y, prow);
+      poff[k] = (ty < tr.th && tx0 + tx < p.w_o) ? (prow * p.PW + tx * p.s) * kCB : 0;
+    }
     uint64_t acc[8][TCO / 2];
 #pragma unroll
     for (int k = 0; k < 8; ++k)
@@ -298,15 +353,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ epilogue
     if (cb < cg_valid) {
       const int jl = jb0 + cb - p.jb_begin;  // block index within the output view
-      float* obase = p.out + (int64_t)img * p.out_img + (int64_t)jl * p.out_blk;
-      const float* sbase =
-          p.skip ? p.skip + (int64_t)img * p.sk_img + (int64_t)jl * p.sk_blk : nullptr;
+      float* obase = p.out + (int64_t)jl * p.out_blk;
+      const float* sbase = p.skip ? p.skip + (int64_t)jl * p.sk_blk : nullptr;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int q = pg + PG * k;
-        const int ty = q / p.TW, tx = q - (q / p.TW) * p.TW;
-        const int y = ty0 + ty, x = tx0 + tx;
-        if (y >= p.h_o || x >= p.w_o) continue;
+        const int ty = q / p.TW, tx = q - ty * p.TW;
+        const int x = tx0 + tx;
+        if (ty >= tr.th || x >= p.w_o) continue;
+        int img, y, prow;
+        tile_row(p, tr, ty, img, y, prow);
         float v[TCO];
 #pragma unroll
         for (int c = 0; c < TCO / 2; ++c) {
@@ -315,7 +371,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           v[2 * c + 1] = f.y;
         }
         if (p.epi & DCONV_EPI_ADD) {
-          const float* sk = sbase + (int64_t)y * p.sk_row + (int64_t)x * kCB;
+          const float* sk = sbase + (int64_t)img * p.sk_img + (int64_t)y * p.sk_row +
+                            (int64_t)x * kCB;
 #pragma unroll
           for (int c = 0; c < TCO; c += 4) {
             const float4 s4 = *reinterpret_cast<const float4*>(sk + c);
@@ -326,7 +383,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int c = 0; c < TCO; ++c) v[c] = fmaxf(v[c], 0.f);
         }
-        float* o = obase + (int64_t)y * p.out_row + (int64_t)x * kCB;
+        float* o = obase + (int64_t)img * p.out_img + (int64_t)y * p.out_row +
+                   (int64_t)x * kCB;
 #pragma unroll
         for (int c = 0; c < TCO; c += 4)
           *reinterpret_cast<float4*>(o + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
@@ -346,40 +404,74 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-struct TilePick {
-  int TH, TW;
-  int64_t tiles;
-};
+// Rows of the stacked patch for a tile starting at output row y0 of an image
+// (segment layout of tile_row), with R filter rows per stage.
+int patch_rows(int y0, int th, int h_o, int s, int R) {
+  const int cnt0 = std::min(h_o - y0, th);
+  int rows = (cnt0 - 1) * s + R, rest = th - cnt0;
+  while (rest > 0) {
+    const int c = std::min(h_o, rest);
+    rows += (c - 1) * s + R;
+    rest -= c;
+  }
+  return rows;
+}
 
-TilePick pick_tile(int BM, int h_o, int w_o, int s, int h_f, int w_f) {
-  TilePick best{0, 0, -1};
+int max_patch_rows(const FfmaParams& p, int R) {
+  // every tile start residue that occurs (vy0 = tile_y * TH)
+  int best = 0;
+  const int vh = p.n * p.h_o;
+  for (int vy0 = 0, seen = 0; vy0 < vh && seen <= p.h_o; vy0 += p.TH, ++seen)
+    best = std::max(best, patch_rows(vy0 % p.h_o, std::min(p.TH, vh - vy0), p.h_o, p.s, R));
+  return best;
+}
+
+// Tile selector: pixel-tile width TW (powers of two, or the map width and its
+// halves/thirds), TH = BM / TW rows of the stacked batch.  Score = useful
+// pixels / launched pixels x SM-wave balance of the persistent schedule;
+// ties go to the smaller patch.
+void pick_tile(FfmaParams& p, int BM, int co_groups, int sms) {
+  int cand[16], nc = 0;
+  for (int tw = 4; tw <= 128 && tw <= BM; tw *= 2) cand[nc++] = tw;
+  for (int d = 1; d <= 4; ++d) {
+    const int tw = (p.w_o + d - 1) / d;
+    if (tw >= 2 && tw <= BM && tw <= 128) cand[nc++] = tw;
+  }
+  double best_score = -1;
   int64_t best_patch = 0;
-  for (int TW = 4; TW <= BM && TW <= 128; TW *= 2) {
-    const int TH = BM / TW;
-    const int64_t tiles = (int64_t)((h_o + TH - 1) / TH) * ((w_o + TW - 1) / TW);
-    const int64_t patch = (int64_t)((std::min(TH, h_o) - 1) * s + h_f) *
-                          ((std::min(TW, w_o) - 1) * s + w_f);
-    if (best.tiles < 0 || tiles < best.tiles ||
-        (tiles == best.tiles && patch < best_patch)) {
-      best = TilePick{TH, TW, tiles};
+  const int64_t vh = (int64_t)p.n * p.h_o;
+  for (int i = 0; i < nc; ++i) {
+    const int tw = cand[i], th = BM / tw;
+    const int64_t ty = (vh + th - 1) / th, tx = (p.w_o + tw - 1) / tw;
+    const int64_t units = ty * tx * co_groups;
+    const double pix = (double)vh * p.w_o / ((double)ty * tx * BM);
+    const double waves = (double)units / ((double)((units + sms - 1) / sms) * sms);
+    const double score = pix * waves;
+    const int64_t patch = (int64_t)((std::min<int64_t>(th, vh) - 1) * p.s + p.h_f) *
+                          ((std::min(tw, p.w_o) - 1) * p.s + p.w_f);
+    if (score > best_score + 1e-6 || (score > best_score - 1e-6 && patch < best_patch)) {
+      best_score = score;
       best_patch = patch;
+      p.TH = th;
+      p.TW = tw;
+      p.tiles_y = (int)ty;
+      p.tiles_x = (int)tx;
     }
   }
-  return best;
 }
 
 template <int BM, int BN, int WF>
 int launch_variant(FfmaParams p, cudaStream_t stream) {
   constexpr int CG = BN / 8;
-  const TilePick t = pick_tile(BM, p.h_o, p.w_o, p.s, p.h_f, p.w_f);
-  p.TH = t.TH;
-  p.TW = t.TW;
-  p.tiles_x = (p.w_o + p.TW - 1) / p.TW;
-  p.tiles_per_img = (int)t.tiles;
-  // The patch only has to cover output pixels that exist: clamp the tile
-  // extents to the output before sizing it (pixels outside map to offset 0).
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int co_groups = (p.jb_count + CG - 1) / CG;
+  pick_tile(p, BM, co_groups, sms);
   p.TWe = std::min(p.TW, p.w_o);
-  p.THe = std::min(p.TH, p.h_o);
   p.PW = (p.TWe - 1) * p.s + p.w_f;
   p.slab_floats = p.h_f * p.w_f * kCB * kCB;
 
@@ -388,7 +480,7 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   const int full_taps_bytes = CG * p.h_f * p.w_f * kCB * kCB * 4;
   if (full_taps_bytes <= kWeightBudget) {
     p.R = p.h_f;
-    p.PH = (p.THe - 1) * p.s + p.R;
+    p.PH = max_patch_rows(p, p.R);
     const int patch1 = p.PH * p.PW * kCB * 4;
     p.G = std::max(1, std::min(kWeightBudget / full_taps_bytes,
                                kPatchBudget / std::max(1, patch1)));
@@ -397,7 +489,7 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
     p.G = 1;
     p.R = std::max(1, kWeightBudget / (CG * p.w_f * kCB * kCB * 4));
     p.R = std::min(p.R, p.h_f);
-    p.PH = (p.THe - 1) * p.s + p.R;
+    p.PH = max_patch_rows(p, p.R);
   }
   p.n_g = (p.ib_n + p.G - 1) / p.G;
   p.n_r = (p.h_f + p.R - 1) / p.R;
@@ -417,23 +509,19 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   const int k_stage = p.G * p.R * p.w_f * kCB;
   p.flush_every = std::max(1, (256 + k_stage - 1) / k_stage);
   if (const char* e = getenv("DCONV_FLUSH_EVERY")) p.flush_every = std::max(1, atoi(e));
-  if (p.NS < 2 || p.PH > 256 || p.PW > 256)
+  if (p.NS < 2)
     return dconv_host::set_error(DCONV_EUNSUPPORTED,
                                  "conv_ffma: stage of %d bytes does not fit "
                                  "shared memory twice", stage_bytes);
   const size_t smem = (size_t)p.NS * stage_bytes + bar_bytes;
   static bool attr_set = false;
-  static int sms = 0;
   if (!attr_set) {
     cudaFuncSetAttribute(conv_ffma_kernel<BM, BN, WF>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     attr_set = true;
   }
   // persistent: one CTA per SM walks the work units round-robin
-  const int64_t units = (int64_t)p.tiles_per_img * p.n * ((p.jb_count + CG - 1) / CG);
+  const int64_t units = (int64_t)p.tiles_y * p.tiles_x * co_groups;
   const int grid = (int)std::min<int64_t>(units, sms);
   conv_ffma_kernel<BM, BN, WF><<<grid, kThreads, smem, stream>>>(p);
   dconv_host::count_launch();

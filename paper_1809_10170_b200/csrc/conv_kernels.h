@@ -22,7 +22,7 @@ struct FfmaParams {
   int64_t sk_img, sk_blk, sk_row;
   int epi;
   // launcher-filled
-  int TH, TW, THe, TWe, tiles_x, tiles_per_img;
+  int TH, TW, TWe, tiles_x, tiles_y;  // tiles over the batch-stacked output
   int G, R, n_g, n_r, PH, PW;
   int slab_floats, patch_floats, wstride_floats, stage_floats, NS;
   int flush_every;          // stages per partial sum before the TMEM fold

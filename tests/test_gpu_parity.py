@@ -347,3 +347,33 @@ def test_ffma_tile_variants(variant):
                        f"variant {variant} case {t}")
     finally:
         lib.dconv_cuda_set_ffma_variant(-1)
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_batched_stacked_tiles(variant):
+    """Pixel tiles over the batch-stacked output span several images (maps of
+    height 1..9 with tiles of up to 64 rows): every image checked."""
+    lib = _abi.lib()
+    _abi.check(lib.dconv_cuda_set_ffma_variant(variant))
+    try:
+        rng = np.random.default_rng(900 + variant)
+        for t in range(14):
+            n = int(rng.integers(2, 7))
+            f = int(rng.choice([1, 3, 5]))
+            s = int(rng.choice([1, 2]))
+            ho, wo = int(rng.integers(1, 10)), int(rng.integers(1, 16))
+            ci, co = int(rng.integers(1, 40)), int(rng.integers(1, 150))
+            hi, wi = (ho - 1) * s + f, (wo - 1) * s + f
+            x = po.uniform((n, ci, hi, wi), 950 + t, variant)
+            k = po.uniform((ci, co, f, f), 960 + t, variant)
+            l = nets.Layer("b", ci, co, hi, wi, f, f, s)
+            a = nets.Act(n, ci, hi, wi)
+            a.buf.copy_(dev(np.stack([po.pack_feature_map(x[i], 8) for i in range(n)])))
+            y = nets.Act(n, co, ho, wo)
+            nets.conv(l, n, a, nets.pack_weights(dev(k), False), y)
+            got = host(y.buf)
+            for i in range(n):
+                want = po.pack_feature_map(po.conv_oracle64(x[i], k, s), 8)
+                assert_tol(got[i], want, f"v{variant} case {t} img {i} ({n},{ci},{co},{hi},{wi},{f},{s})")
+    finally:
+        lib.dconv_cuda_set_ffma_variant(-1)
