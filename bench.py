@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=0, help="global batch (0 = config default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--shard", default="batch", choices=["batch", "co"],
+                    help="batch: image ranges per rank, no collective; co: batch-1 "
+                         "output-block sharding with an NCCL all-gather per layer")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="target CPU work for the cpu_baseline sample")
     return ap.parse_args()
@@ -179,13 +182,22 @@ def main_gpu(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lib = _abi.lib()
     batch = args.batch or DEFAULT_BATCH[args.config]
-    if batch % world:
-        raise SystemExit(f"global batch {batch} not divisible by {world} ranks")
-    n_local = batch // world  # batch sharding: contiguous image range per rank, no collective
+    co_shard = args.shard == "co"
+    if co_shard:
+        batch = args.batch or 1
+        if batch != 1:
+            raise SystemExit("--shard co is the batch-1 mode")
+        n_local = 1
+        args.no_graph = True  # NCCL collectives stay outside graph capture
+    else:
+        if batch % world:
+            raise SystemExit(f"global batch {batch} not divisible by {world} ranks")
+        n_local = batch // world  # batch sharding: contiguous image range per rank
 
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
-        plan = nets.build_plan(args.config, n_local, seed=1809 + rank)
+        plan = nets.build_plan(args.config, n_local, seed=1809 + (0 if co_shard else rank),
+                               shard=(rank, world, None) if co_shard else None)
     torch.cuda.synchronize()
     flops_local = plan.flops
 
@@ -235,10 +247,11 @@ def main_gpu(args):
     barrier()
     ms_total = max_over_ranks(e0.elapsed_time(e1))
     n_launch_steps = len(plan.steps)
-    gpu_launches = n_launch_steps * args.steps if graph is not None else \
-        lib.dconv_cuda_launch_count() - launches0
+    gpu_launches = sum(1 for s in plan.steps if s.kind != "gather") * args.steps \
+        if graph is not None else lib.dconv_cuda_launch_count() - launches0
     ms_step = ms_total / args.steps
-    value = flops_local * world / (ms_step * 1e-3) / 1e9
+    flops_job = flops_local * world  # equal shards in both modes
+    value = flops_job / (ms_step * 1e-3) / 1e9
 
     # ---- e2e: public API with host buffers, H2D + D2H inside the timed region
     ins = plan.io_inputs()
@@ -268,7 +281,7 @@ def main_gpu(args):
     e1.synchronize()
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / e2e_steps
-    e2e_value = flops_local * world / (e2e_ms * 1e-3) / 1e9
+    e2e_value = flops_job / (e2e_ms * 1e-3) / 1e9
 
     # ---- per-launch durations (CUDA events on the launching stream, eager)
     per = {s.name: [] for s in plan.steps}
@@ -330,14 +343,17 @@ def main_gpu(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded uniform[-1,1), counter-based generator)",
+        "mode": "C_o-block sharding + NCCL all-gather per layer" if co_shard else
+                "batch sharding, no collective",
         "config": {"workload": f"{args.config} chain" if args.config in ("vgg16", "resnet50")
                    else f"{args.config} layers", "global_batch": batch,
                    "per_rank_batch": n_local, "c_b": 8,
-                   "parallelism": f"batch-shard x{world}, no collective",
+                   "parallelism": (f"co-shard x{world}, all-gather" if co_shard
+                                   else f"batch-shard x{world}, no collective"),
                    "l2": "per-step working set > 126 MB L2 (activations streamed)"
                    if args.config in ("vgg16", "resnet50", "googlenet") else
                    "working set fits L2 (batch-1 config): warm-L2 numbers",
-                   "graph": graph is not None, "gflop_per_step": round(flops_local * world / 1e9, 3)},
+                   "graph": graph is not None, "gflop_per_step": round(flops_job / 1e9, 3)},
         "roofline": {"bound": "fp32", "achieved": round(achieved, 2), "peak": round(peak, 2),
                      "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if peak > 0 else None,
                      "traffic": traffic,

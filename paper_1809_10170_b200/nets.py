@@ -156,6 +156,7 @@ class Act:
     def __init__(self, n: int, c: int, h: int, w: int, halo: int = 0,
                  pad_hi_only: bool = False, device="cuda"):
         self.n, self.c, self.h, self.w, self.halo = n, c, h, w, halo
+        self.pad_hi_only = pad_hi_only
         # pad_hi_only: halo on top/left only (ResNet stride-2 "pad 1/0")
         hp = h + (halo if pad_hi_only else 2 * halo)
         wp = w + (halo if pad_hi_only else 2 * halo)
@@ -181,16 +182,24 @@ class Act:
 
 def conv(l: Layer, n: int, x: "Act|torch.Tensor", w: torch.Tensor, out: Act,
          epilogue: int = 0, skip: Optional[Act] = None, stream=None,
-         in_view: Optional[Tuple[int, int, int, int]] = None) -> None:
+         in_view: Optional[Tuple[int, int, int, int]] = None,
+         co_range: Optional[Tuple[int, int]] = None) -> None:
     """Launch one conv layer through the C-ABI.  ``x`` is an Act (blocked) or,
     for a first layer, the dense [n][c][h][w] network input.  ``in_view``
-    optionally overrides (ptr, img, blk, row) of the blocked input (crops)."""
+    optionally overrides (ptr, img, blk, row) of the blocked input (crops).
+    ``co_range`` = (first block, block count) computes only those output
+    blocks into ``out`` (a rank's C_o slice); ``skip`` is then read from the
+    same blocks of the full skip map."""
     d = _desc(l, n, epilogue)
     d.out_img_stride, d.out_blk_stride, d.out_row_stride = out.img, out.blk, out.row
+    b0 = 0
+    if co_range is not None:
+        b0, d.co_block_count = co_range
+        d.co_block_begin = b0
     sp = 0
     if skip is not None:
         d.skip_img_stride, d.skip_blk_stride, d.skip_row_stride = skip.img, skip.blk, skip.row
-        sp = skip.base()
+        sp = skip.base() + 4 * b0 * skip.blk
     st = stream_ptr(stream)
     if l.first:
         check(lib().dconv_cuda_conv_first_layer(ctypes.byref(d), ptr(x), 0, ptr(w), sp,
@@ -223,22 +232,28 @@ def pack_weights(dense: torch.Tensor, first: bool, stream=None) -> torch.Tensor:
 
 @dataclass
 class Step:
-    """One launch of a plan: a conv layer (kind 'conv' / 'first') or a
-    layout-preserving op ('pool')."""
+    """One launch of a plan: a conv layer (kind 'conv' / 'first'), a
+    layout-preserving op ('pool') or a collective ('gather')."""
     fn: object
     name: str
     kind: str
-    flops: int = 0      # algorithmic FLOPs of this launch (conv_flops x n)
+    flops: int = 0      # algorithmic FLOPs of this launch on this rank
     layer: Optional[Layer] = None
 
 
 @dataclass
 class Plan:
     """A network instantiated on one device: weights, activations, and the
-    ordered launch list.  ``run()`` is one step (one pass over the batch)."""
+    ordered launch list.  ``run()`` is one step (one pass over the batch).
+
+    ``shard`` = (rank, world, group) selects batch-1 output-block sharding:
+    every conv computes this rank's contiguous j' range into a local slice,
+    ReLU / skip-add / max-pool run on the slice, and an all-gather of the
+    slices rebuilds the full (halo'd) blocked map for the next layer."""
     name: str
     n: int
     layers: List[Layer]
+    shard: Optional[Tuple[int, int, object]] = None
     weights: Dict[str, torch.Tensor] = field(default_factory=dict)
     steps: List = field(default_factory=list)
     input: Optional[torch.Tensor] = None   # dense network input (first layer)
@@ -248,7 +263,8 @@ class Plan:
 
     @property
     def flops(self) -> int:
-        return self.n * network_flops(self.layers)
+        """Algorithmic FLOPs this rank executes per step."""
+        return sum(s.flops for s in self.steps)
 
     def run(self, stream=None) -> None:
         for st in self.steps:
@@ -265,12 +281,48 @@ class Plan:
             return [a.buf for a in self.outputs.values()]
         return [self.output.buf]
 
-    def add_conv(self, l: Layer, fn) -> None:
-        self.steps.append(Step(fn, l.name, "first" if l.first else "conv",
-                               self.n * l.flops, l))
+    # -- building blocks ----------------------------------------------------
+    def _local(self, full: Act, c: int) -> Act:
+        return Act(self.n, c, full.h, full.w, halo=full.halo, pad_hi_only=full.pad_hi_only,
+                   device=full.buf.device)
 
-    def add_op(self, name: str, fn) -> None:
-        self.steps.append(Step(fn, name, "pool"))
+    def _gather(self, name: str, full: Act, local: Act) -> None:
+        from .shard import all_gather_blocks
+        group = self.shard[2]
+        self.steps.append(Step(lambda st: all_gather_blocks(full.buf[0], local.buf[0], group),
+                               f"gather_{name}", "gather"))
+
+    def conv_into(self, l: Layer, x, y: Act, epilogue: int = 0, skip: Optional[Act] = None,
+                  gather: bool = True, in_view=None) -> Act:
+        """conv(l) into y (or into this rank's slice of y, then gathered).
+        Returns the Act holding this rank's result (y, or the slice)."""
+        w = self.weights[l.name]
+        kind = "first" if l.first else "conv"
+        if self.shard is None:
+            self.steps.append(Step(lambda st: conv(l, self.n, x, w, y, epilogue, skip, st, in_view),
+                                   l.name, kind, self.n * l.flops, l))
+            return y
+        from .shard import block_range
+        rank, world, _ = self.shard
+        if self.n != 1:
+            raise ValueError("C_o sharding is the batch-1 mode")
+        b0, cnt = block_range(nblk(l.c_o), world, rank)
+        ys = self._local(y, cnt * CB)
+        flops = l.flops * min(cnt * CB, l.c_o - b0 * CB) // l.c_o
+        self.steps.append(Step(lambda st: conv(l, self.n, x, w, ys, epilogue, skip, st, in_view,
+                                               (b0, cnt)), l.name, kind, flops, l))
+        if gather:
+            self._gather(l.name, y, ys)
+        return ys
+
+    def pool_into(self, name: str, src_local: Act, z: Act) -> None:
+        """2x2/s2 max-pool of this rank's result into z (gathered if sharded)."""
+        if self.shard is None:
+            self.steps.append(Step(lambda st: maxpool_into(src_local, z, st), name, "pool"))
+            return
+        zs = self._local(z, src_local.c)
+        self.steps.append(Step(lambda st: maxpool_into(src_local, zs, st), name, "pool"))
+        self._gather(name, z, zs)
 
 
 def _fill(t: torch.Tensor, seed: int, stream_id: int, scale: float = 1.0) -> None:
@@ -281,10 +333,12 @@ def _fill(t: torch.Tensor, seed: int, stream_id: int, scale: float = 1.0) -> Non
 
 
 def build_plan(config: str, n: int, seed: int = 1809, device="cuda",
-               dense_weights: Optional[Dict[str, torch.Tensor]] = None) -> Plan:
-    """Instantiates a BASELINE.json config on the current device."""
+               dense_weights: Optional[Dict[str, torch.Tensor]] = None,
+               shard: Optional[Tuple[int, int, object]] = None) -> Plan:
+    """Instantiates a BASELINE.json config on the current device.  ``shard``
+    = (rank, world, process group) for batch-1 C_o-block sharding."""
     layers = CONFIGS[config]
-    p = Plan(config, n, list(layers))
+    p = Plan(config, n, list(layers), shard=shard)
     for idx, l in enumerate(layers):
         wd = dense_weights[l.name] if dense_weights else None
         if wd is None:
@@ -318,8 +372,7 @@ def _build_independent(p: Plan, device, seed: int) -> None:
             p.per_layer_inputs[l.name] = x
         y = Act(p.n, l.c_o, l.h_o, l.w_o, device=device)
         p.outputs[l.name] = y
-        w = p.weights[l.name]
-        p.add_conv(l, lambda st, l=l, x=x, w=w, y=y: conv(l, p.n, x, w, y, stream=st))
+        p.conv_into(l, x, y)
     p.output = p.outputs[p.layers[-1].name]
 
 
@@ -341,19 +394,12 @@ def _build_vgg(p: Plan, device, seed: int) -> None:
     for i, l in enumerate(layers):
         last = i == len(layers) - 1
         pool = l.name in VGG16_POOL_AFTER
-        if last:
-            y = Act(p.n, l.c_o, l.h_o, l.w_o, device=device)
-        elif pool:
-            y = Act(p.n, l.c_o, l.h_o, l.w_o, device=device)
-        else:
-            y = Act(p.n, l.c_o, l.h_o, l.w_o, halo=1, device=device)
-        w = p.weights[l.name]
-        p.add_conv(l, lambda st, l=l, x=cur, w=w, y=y:
-                   conv(l, p.n, x, w, y, epilogue=_abi.EPI_RELU, stream=st))
+        y = Act(p.n, l.c_o, l.h_o, l.w_o, halo=0 if (last or pool) else 1, device=device)
         p.outputs[l.name] = y
+        mine = p.conv_into(l, cur, y, epilogue=_abi.EPI_RELU, gather=not pool)
         if pool:
             z = Act(p.n, l.c_o, l.h_o // 2, l.w_o // 2, halo=1, device=device)
-            p.add_op(f"pool_{l.name}", lambda st, y=y, z=z: maxpool_into(y, z, st))
+            p.pool_into(f"pool_{l.name}", mine, z)
             cur = z
         else:
             cur = y
@@ -369,39 +415,29 @@ def _build_resnet(p: Plan, device, seed: int) -> None:
     _fill(x0, seed, 0)
     p.input = x0
     s_out = Act(p.n, 64, 112, 112, device=device)
-    w = p.weights["stem"]
-    p.add_conv(stem, lambda st: conv(stem, p.n, x0, w, s_out, epilogue=_abi.EPI_RELU, stream=st))
-    x = Act(p.n, 64, 56, 56, device=device)
-    p.add_op("pool_stem", lambda st: maxpool_into(s_out, x, st))
     p.outputs["stem"] = s_out
+    mine = p.conv_into(stem, x0, s_out, epilogue=_abi.EPI_RELU, gather=False)
+    x = Act(p.n, 64, 56, 56, device=device)
+    p.pool_into("pool_stem", mine, x)
     blocks: Dict[str, List[Layer]] = {}
     for tag, l in named[1:]:
         blocks.setdefault(tag, []).append(l)
     for tag, ls in blocks.items():
         c1, c2, c3 = ls[0], ls[1], ls[2]
         proj = ls[3] if len(ls) > 3 else None
-        if c2.s == 1:
-            mid1 = Act(p.n, c1.c_o, c1.h_o, c1.w_o, halo=1, device=device)
-        else:
-            mid1 = Act(p.n, c1.c_o, c1.h_o, c1.w_o, halo=1, pad_hi_only=True, device=device)
+        mid1 = Act(p.n, c1.c_o, c1.h_o, c1.w_o, halo=1, pad_hi_only=(c2.s != 1), device=device)
         mid2 = Act(p.n, c2.c_o, c2.h_o, c2.w_o, device=device)
         y = Act(p.n, c3.c_o, c3.h_o, c3.w_o, device=device)
-        p.add_conv(c1, lambda st, l=c1, x=x, m=mid1:
-                   conv(l, p.n, x, p.weights[l.name], m, epilogue=_abi.EPI_RELU, stream=st))
-        p.add_conv(c2, lambda st, l=c2, m=mid1, m2=mid2:
-                   conv(l, p.n, m, p.weights[l.name], m2, epilogue=_abi.EPI_RELU, stream=st))
+        p.conv_into(c1, x, mid1, epilogue=_abi.EPI_RELU)
+        p.conv_into(c2, mid1, mid2, epilogue=_abi.EPI_RELU)
         if proj is not None:
             sc = Act(p.n, proj.c_o, proj.h_o, proj.w_o, device=device)
             # 1x1 s2 projection reads the 55x55 (or full) crop of x: a view
-            p.add_conv(proj, lambda st, l=proj, x=x, sc=sc:
-                       conv(l, p.n, x, p.weights[l.name], sc, stream=st,
-                            in_view=x.full_view()))
+            p.conv_into(proj, x, sc, in_view=x.full_view())
             skip = sc
         else:
             skip = x
-        p.add_conv(c3, lambda st, l=c3, m2=mid2, y=y, sk=skip:
-                   conv(l, p.n, m2, p.weights[l.name], y,
-                        epilogue=_abi.EPI_ADD_RELU, skip=sk, stream=st))
+        p.conv_into(c3, mid2, y, epilogue=_abi.EPI_ADD_RELU, skip=skip)
         p.outputs[tag] = y
         x = y
     p.output = x

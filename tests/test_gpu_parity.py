@@ -377,3 +377,79 @@ def test_batched_stacked_tiles(variant):
                 assert_tol(got[i], want, f"v{variant} case {t} img {i} ({n},{ci},{co},{hi},{wi},{f},{s})")
     finally:
         lib.dconv_cuda_set_ffma_variant(-1)
+
+
+# ------------------------------------------------ chains (wiring, teacher-forced)
+def _conv_io(plan):
+    """(layer, input Act/tensor, output Act, epilogue, skip) per conv, recorded
+    by re-wrapping nets.conv during a plan run."""
+    rec = []
+    orig = nets.conv
+
+    def spy(l, n, x, w, out, epilogue=0, skip=None, stream=None, in_view=None, co_range=None):
+        orig(l, n, x, w, out, epilogue, skip, stream, in_view, co_range)
+        torch.cuda.synchronize()
+        xin = x.clone() if isinstance(x, torch.Tensor) else x.buf.clone()
+        rec.append((l, xin, out.buf.clone(), out, epilogue, skip.buf.clone() if skip else None,
+                    skip, w))
+    nets.conv = spy
+    try:
+        plan.run()
+    finally:
+        nets.conv = orig
+    return rec
+
+
+@pytest.mark.parametrize("config", ["vgg16", "resnet50", "alexnet", "googlenet"])
+def test_chain_wiring_teacher_forced(config):
+    plan = nets.build_plan(config, 1)
+    rec = _conv_io(plan)
+    assert len(rec) == len(plan.layers)
+    for l, xin, yout, out, epi, skb, skip, w in rec:
+        xin = xin.cpu().numpy()[0]
+        got = yout.cpu().numpy()[0]
+        if l.first:
+            # dense input -> blocked c_b = 8 (zero channel padding is exact)
+            xb = po.pack_feature_map(np.ascontiguousarray(xin[:, :l.h_i, :l.w_i]), 8)
+        else:
+            xb = np.ascontiguousarray(xin[:, :l.h_i, :l.w_i, :])  # crop views (projections)
+        kd = po.unpack_kernel(w.cpu().numpy(), l.c_i, l.c_o) if not l.first else None
+        kb = po.pack_kernel(kd, 8, 8) if kd is not None else po.pack_kernel(
+            _first_dense(w.cpu().numpy(), l), 8, 8)
+        h = out.halo
+        for r in sorted({0, l.h_o // 2, l.h_o - 1}):
+            want = po.conv_oracle64_blocked(xb, kb, l.c_i, l.c_o, l.s, r, r + 1)[:, r]
+            if epi & _abi.EPI_ADD:
+                sk = skb.cpu().numpy()[0]
+                want = want + sk[:, skip.halo + r, skip.halo:skip.halo + l.w_o, :]
+            if epi & _abi.EPI_RELU:
+                want = np.maximum(want, 0)
+            g = got[:, h + r, h:h + l.w_o, :]
+            scale = max(1.0, float(np.abs(want).max()))
+            err = float(np.abs(g - want).max())
+            assert err <= 1e-5 * scale + 1e-4, f"{config}/{l.name} row {r}: err {err} scale {scale}"
+
+
+def _first_dense(wb, l):
+    """blocked first-layer weights (c_ib = c_i) -> dense [c_i][c_o][h_f][w_f]"""
+    return po.unpack_kernel(wb, l.c_i, l.c_o)
+
+
+def test_co_shard_plan_world1_matches_unsharded():
+    """The C_o-sharded plan (slices + all-gather via a real 1-rank NCCL group)
+    reproduces the unsharded plan bitwise on ResNet-50 b1."""
+    import os
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29517")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        a = nets.build_plan("resnet50", 1, seed=5)
+        b = nets.build_plan("resnet50", 1, seed=5, shard=(0, 1, None))
+        a.run()
+        b.run()
+        torch.cuda.synchronize()
+        assert any(s.kind == "gather" for s in b.steps)
+        assert torch.equal(a.output.buf, b.output.buf)
+    finally:
+        dist.destroy_process_group()
