@@ -178,11 +178,14 @@ def main_gpu(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    co_shard = args.shard == "co"
+    if world > 1 or co_shard:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", local))
     lib = _abi.lib()
     batch = args.batch or DEFAULT_BATCH[args.config]
-    co_shard = args.shard == "co"
     if co_shard:
         batch = args.batch or 1
         if batch != 1:
@@ -202,7 +205,7 @@ def main_gpu(args):
     flops_local = plan.flops
 
     def barrier():
-        if world > 1:
+        if dist.is_initialized():
             dist.barrier()
 
     def max_over_ranks(v: float) -> float:
@@ -324,7 +327,7 @@ def main_gpu(args):
             traffic = None
 
     if rank != 0:
-        if world > 1:
+        if dist.is_initialized():
             dist.barrier()
             dist.destroy_process_group()
         return
@@ -370,7 +373,7 @@ def main_gpu(args):
         "layers": layers,
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
 

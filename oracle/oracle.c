@@ -7,6 +7,10 @@
 
 #include <stdlib.h>
 #include <string.h>
+#if defined(__AVX2__) && defined(__FMA__)
+#include <immintrin.h>
+#define ORC_HAVE_AVX2 1
+#endif
 #ifdef _OPENMP
 #include <omp.h>
 #endif
@@ -190,9 +194,48 @@ void orc_conv_oracle64_blocked(const float* in, const float* k, int c_i,
 
 /* AVX2 register model (model.hpp:63-73 with n_vec=8, n_reg=16, 2 operand
  * registers reserved): (c_ob/8)*w_ob + 2 <= 16. */
-DEF_TILE(8, 14)
 DEF_TILE(16, 7)
 DEF_TILE(32, 3)
+
+#ifdef ORC_HAVE_AVX2
+/* The paper's micro-kernel for c_ob = 8 = one AVX2 vector: w_ob = 14 output
+ * columns x 8 channels held in 14 ymm accumulators; per (n, m, ii) one weight
+ * vector load (jj unit stride) and 14 broadcast-FMAs (kk).  Same (n, m, ii)
+ * accumulation order as the generic tile. */
+static void tile_8_14(const float* in, const float* w, float* out, int h_f,
+                      int w_f, int c_ib, int row_pitch, int col_stride) {
+  __m256 a0 = _mm256_loadu_ps(out + 0 * 8), a1 = _mm256_loadu_ps(out + 1 * 8);
+  __m256 a2 = _mm256_loadu_ps(out + 2 * 8), a3 = _mm256_loadu_ps(out + 3 * 8);
+  __m256 a4 = _mm256_loadu_ps(out + 4 * 8), a5 = _mm256_loadu_ps(out + 5 * 8);
+  __m256 a6 = _mm256_loadu_ps(out + 6 * 8), a7 = _mm256_loadu_ps(out + 7 * 8);
+  __m256 a8 = _mm256_loadu_ps(out + 8 * 8), a9 = _mm256_loadu_ps(out + 9 * 8);
+  __m256 a10 = _mm256_loadu_ps(out + 10 * 8), a11 = _mm256_loadu_ps(out + 11 * 8);
+  __m256 a12 = _mm256_loadu_ps(out + 12 * 8), a13 = _mm256_loadu_ps(out + 13 * 8);
+  const size_t cs = (size_t)col_stride;
+  for (int n = 0; n < h_f; ++n)
+    for (int m = 0; m < w_f; ++m) {
+      const float* ip = in + (size_t)n * row_pitch + (size_t)m * c_ib;
+      const float* wp = w + (size_t)(n * w_f + m) * c_ib * 8;
+      for (int ii = 0; ii < c_ib; ++ii, ++ip, wp += 8) {
+        const __m256 wv = _mm256_loadu_ps(wp);
+#define ORC_FMA(k) a##k = _mm256_fmadd_ps(_mm256_broadcast_ss(ip + (k) * cs), wv, a##k)
+        ORC_FMA(0); ORC_FMA(1); ORC_FMA(2); ORC_FMA(3); ORC_FMA(4); ORC_FMA(5);
+        ORC_FMA(6); ORC_FMA(7); ORC_FMA(8); ORC_FMA(9); ORC_FMA(10); ORC_FMA(11);
+        ORC_FMA(12); ORC_FMA(13);
+#undef ORC_FMA
+      }
+    }
+  _mm256_storeu_ps(out + 0 * 8, a0); _mm256_storeu_ps(out + 1 * 8, a1);
+  _mm256_storeu_ps(out + 2 * 8, a2); _mm256_storeu_ps(out + 3 * 8, a3);
+  _mm256_storeu_ps(out + 4 * 8, a4); _mm256_storeu_ps(out + 5 * 8, a5);
+  _mm256_storeu_ps(out + 6 * 8, a6); _mm256_storeu_ps(out + 7 * 8, a7);
+  _mm256_storeu_ps(out + 8 * 8, a8); _mm256_storeu_ps(out + 9 * 8, a9);
+  _mm256_storeu_ps(out + 10 * 8, a10); _mm256_storeu_ps(out + 11 * 8, a11);
+  _mm256_storeu_ps(out + 12 * 8, a12); _mm256_storeu_ps(out + 13 * 8, a13);
+}
+#else
+DEF_TILE(8, 14)
+#endif
 
 /* tile_kernel_generic (micro_kernel.hpp:48-51): runtime sizes, same order */
 static void tile_generic(const float* in, const float* w, float* out, int h_f,
@@ -236,24 +279,34 @@ static int conv_direct_impl(const float* in, const float* k, int n_img,
   const int row_pitch = w_i * c_ib;
   const int col_stride = s * c_ib;
   tile_fn full = literal ? NULL : find_tile(c_ob, w_ob);
-  const int units = n_img * jb_n;
 #ifdef _OPENMP
   if (threads <= 0) threads = omp_get_max_threads();
 #else
   threads = 1;
 #endif
-  /* j' in parallel; whole-block ownership so the
-   * result is bitwise independent of the thread count. */
+  /* j' in parallel, refined into row bands of the
+   * output block when there are fewer (image, j') pairs than threads, so
+   * narrow layers (C_o = 64 -> 8 blocks) still use every core.  Every output
+   * element is owned by exactly one unit and accumulated in the same order,
+   * so the result is bitwise independent of the thread count. */
+  int bands = 1;
+  while (n_img * jb_n * bands < 4 * threads && bands * 2 <= h_o) bands *= 2;
+  const int rows_per = (h_o + bands - 1) / bands;
+  const int units = n_img * jb_n * bands;
 #pragma omp parallel for schedule(dynamic, 1) num_threads(threads)
   for (int u = 0; u < units; ++u) {
-    const int img = u / jb_n, jb = u % jb_n;
+    const int band = u % bands, t = u / bands;
+    const int img = t / jb_n, jb = t % jb_n;
+    const int l0 = band * rows_per, l1 = (l0 + rows_per < h_o) ? l0 + rows_per : h_o;
+    if (l0 >= l1) continue;
     const float* inp = in + (size_t)img * in_img;
     float* ob = out + (size_t)img * out_img + (size_t)jb * out_blk;
-    memset(ob, 0, sizeof(float) * out_blk);
+    memset(ob + (size_t)l0 * w_o * c_ob, 0,
+           sizeof(float) * (size_t)(l1 - l0) * w_o * c_ob);
     for (int ib = 0; ib < ib_n; ++ib) {               /* i' */
       const float* w = k + ((size_t)jb * ib_n + ib) * slab;  /* tensor.hpp:138-140 */
       const float* inb = inp + (size_t)ib * h_i * w_i * c_ib;
-      for (int l = 0; l < h_o; ++l)                   /* l */
+      for (int l = l0; l < l1; ++l)                   /* l */
         for (int kb = 0; kb * w_ob < w_o; ++kb) {     /* k' */
           const int wob = (w_o - kb * w_ob) < w_ob ? (w_o - kb * w_ob) : w_ob;
           float* ot = ob + ((size_t)l * w_o + (size_t)kb * w_ob) * c_ob;
