@@ -155,22 +155,33 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int CG = BN / 8;     // output blocks per CTA tile
 
   extern __shared__ __align__(128) float smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.NS * p.stage_floats);
+  float* red = smem + p.NS * p.stage_floats;   // split-K partials [64][256]
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + p.red_floats);
   uint64_t* empty = full + kMaxStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty + kMaxStages);
+  uint64_t* ready = empty + kMaxStages;        // all ranks' partials written
+  uint64_t* done = ready + 1;                  // all ranks finished reading mine
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int S = p.n_g * p.n_r;                 // stages per work unit
   const int co_groups = (p.jb_count + CG - 1) / CG;
   const int n_units = p.tiles_y * p.tiles_x * co_groups;
-  const bool use_tmem = S > p.flush_every;
+  // Split-K over a thread-block cluster of ks CTAs: rank r runs stages
+  // [st0, st1) of every unit, the partial tiles are reduced through DSMEM.
+  const int ks = p.ksplit;
+  const int rank = blockIdx.x % ks;            // == %cluster_ctarank (1-D cluster)
+  const int cluster_id = blockIdx.x / ks, n_clusters = gridDim.x / ks;
+  const int st0 = rank * S / ks, st1 = (rank + 1) * S / ks;
+  const bool use_tmem = st1 - st0 > p.flush_every;
 
   if (tid == 0) {
     for (int i = 0; i < p.NS; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], NW);
     }
+    mbar_init(ready, NW * ks);
+    mbar_init(done, NW * ks);
     fence_mbar_init();
   }
   if (use_tmem && warp == 0) {
@@ -182,6 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (ks > 1) cluster_sync_all();  // every rank's barriers exist before remote arrives
 
   // unit u -> (co group fastest: concurrently running CTAs share the pixel
   // tile's patch rows in L2, consecutive waves reuse the weight slabs)
@@ -205,14 +217,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp != NW) return;
     int gs = 0;
     const int seg_rows_full = (p.h_o - 1) * p.s;  // + Re per full segment
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    for (int u = cluster_id; u < n_units; u += n_clusters) {
       TileRows tr;
       int tx0, jb0, cg_valid;
       decode(u, tr, tx0, jb0, cg_valid);
       const int col0 = tx0 * p.s;
       const int cols = min(p.PW, p.w_i - col0);
       const int n_seg = 1 + (tr.th - tr.cnt0 + p.h_o - 1) / p.h_o;
-      for (int st = 0; st < S; ++st, ++gs) {
+      for (int st = st0; st < st1; ++st, ++gs) {
         const int buf = gs % p.NS;
         if (gs >= p.NS) mbar_wait(&empty[buf], ((gs / p.NS) - 1) & 1);
         const int g = st / p.n_r, r = st - g * p.n_r;
@@ -269,8 +281,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                          (uint32_t)((warp >> 2) * 8 * TCO);
   const int wf = WF > 0 ? WF : p.w_f;
 
-  int gs = 0;
-  for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+  int gs = 0, unit_iter = 0;
+  for (int u = cluster_id; u < n_units; u += n_clusters, ++unit_iter) {
     TileRows tr;
     int tx0, jb0, cg_valid;
     decode(u, tr, tx0, jb0, cg_valid);
@@ -292,7 +304,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = 0; c < TCO / 2; ++c) acc[k][c] = 0ull;
     bool have_total = false;
 
-    for (int st = 0; st < S; ++st, ++gs) {
+    for (int st = st0; st < st1; ++st, ++gs) {
       const int buf = gs % p.NS;
       mbar_wait(&full[buf], (gs / p.NS) & 1);
       const int g = st / p.n_r, r = st - g * p.n_r;
@@ -338,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(&empty[buf]);
       // fold the partial sum into the TMEM running total every flush_every
       // stages (never after the last stage: the epilogue folds it)
-      if (use_tmem && (st + 1) % p.flush_every == 0 && st + 1 < S) {
+      if (use_tmem && (st - st0 + 1) % p.flush_every == 0 && st + 1 < st1) {
         tmem_fold<NP>(taddr, &acc[0][0], have_total, true);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         have_total = true;
@@ -351,25 +363,57 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (have_total) tmem_fold<NP>(taddr, &acc[0][0], true, false);
 
     // ------------------------------------------------------------ epilogue
+    // Split-K: every rank publishes its partial tile in its own smem, then
+    // rank r sums pixels [r*8/ks, (r+1)*8/ks) of every thread's 8x8 tile over
+    // ranks 0..ks-1 in that fixed order (deterministic, no global workspace).
+    int k_lo = 0, k_hi = 8;
+    if (ks > 1) {
+      if (unit_iter > 0) mbar_wait_cluster(done, (unit_iter - 1) & 1);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float2 f = unpack2(acc[k][c]);
+          red[(k * 8 + 2 * c) * (NW * 32) + tid] = f.x;
+          red[(k * 8 + 2 * c + 1) * (NW * 32) + tid] = f.y;
+        }
+      __syncwarp();
+      if (lane == 0)
+        for (int q = 0; q < ks; ++q) mbar_arrive_remote(ready, q);
+      mbar_wait_cluster(ready, unit_iter & 1);
+      k_lo = rank * 8 / ks;
+      k_hi = (rank + 1) * 8 / ks;
+    }
     if (cb < cg_valid) {
       const int jl = jb0 + cb - p.jb_begin;  // block index within the output view
       float* obase = p.out + (int64_t)jl * p.out_blk;
       const float* sbase = p.skip ? p.skip + (int64_t)jl * p.sk_blk : nullptr;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
+        if (k < k_lo || k >= k_hi) continue;
         const int q = pg + PG * k;
         const int ty = q / p.TW, tx = q - ty * p.TW;
         const int x = tx0 + tx;
-        if (ty >= tr.th || x >= p.w_o) continue;
+        const bool valid = ty < tr.th && x < p.w_o;
+        float v[TCO];
+        if (ks > 1) {
+#pragma unroll
+          for (int c = 0; c < TCO; ++c) {
+            float sum = 0.f;
+            for (int r = 0; r < ks; ++r) sum += ld_dsmem(&red[(k * 8 + c) * (NW * 32) + tid], r);
+            v[c] = sum;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < TCO / 2; ++c) {
+            const float2 f = unpack2(acc[k][c]);
+            v[2 * c] = f.x;
+            v[2 * c + 1] = f.y;
+          }
+        }
+        if (!valid) continue;
         int img, y, prow;
         tile_row(p, tr, ty, img, y, prow);
-        float v[TCO];
-#pragma unroll
-        for (int c = 0; c < TCO / 2; ++c) {
-          const float2 f = unpack2(acc[k][c]);
-          v[2 * c] = f.x;
-          v[2 * c + 1] = f.y;
-        }
         if (p.epi & DCONV_EPI_ADD) {
           const float* sk = sbase + (int64_t)img * p.sk_img + (int64_t)y * p.sk_row +
                             (int64_t)x * kCB;
@@ -390,7 +434,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           *reinterpret_cast<float4*>(o + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
       }
     }
+    if (ks > 1) {
+      __syncwarp();
+      if (lane == 0)
+        for (int q = 0; q < ks; ++q) mbar_arrive_remote(done, q);
+    }
   }
+  // no CTA may leave while a peer can still read its partials
+  if (ks > 1 && unit_iter > 0) mbar_wait_cluster(done, (unit_iter - 1) & 1);
 
   if (use_tmem) {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -500,11 +551,64 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   p.stage_floats = p.patch_floats + CG * p.wstride_floats;
   p.stage_floats = (p.stage_floats + 31) & ~31;  // 128-byte aligned stages
   const int stage_bytes = p.stage_floats * 4;
-  const int kSmemBudget = 220 * 1024;
-  const int bar_bytes = 2 * kMaxStages * 8 + 16;
-  p.NS = std::min(kMaxStages, (kSmemBudget - bar_bytes) / stage_bytes);
   const int S = p.n_g * p.n_r;
-  p.NS = std::min(p.NS, std::max(2, S));
+  const int kSmemBudget = 220 * 1024;
+  const int bar_bytes = (2 * kMaxStages + 2) * 8 + 16;
+  const int red_bytes = 8 * 8 * kComputeWarps * 32 * 4;  // 64 floats / thread
+
+  auto kernel = conv_ffma_kernel<BM, BN, WF>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_set = true;
+  }
+  // Split-K factor: the persistent schedule runs ceil(units / slots) rounds
+  // of ceil(S / ks) stages (+ a DSMEM reduction when ks > 1); pick the
+  // cheapest.  slots = co-resident clusters of ks CTAs (GPC-limited).
+  const int64_t units = (int64_t)p.tiles_y * p.tiles_x * co_groups;
+  int best_ks = 1;
+  double best_cost = 1e300;
+  static int slots_cache[9] = {0};
+  for (int ks = 1; ks <= 8; ks *= 2) {
+    if (ks > S) break;
+    if (ks > 1 && getenv("DCONV_NO_SPLITK")) break;
+    int slots = sms;
+    if (ks > 1) {
+      if (!slots_cache[ks]) {
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = ks;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(ks * 64);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = 200 * 1024;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess || n < 1) {
+          cudaGetLastError();
+          n = -1;
+        }
+        slots_cache[ks] = n;
+      }
+      slots = slots_cache[ks];
+      if (slots < 1) continue;
+    }
+    const double rounds = (double)((units + slots - 1) / slots);
+    const double cost = rounds * ((S + ks - 1) / ks + (ks > 1 ? 0.35 + 0.05 * ks : 0.0));
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best_ks = ks;
+    }
+  }
+  if (const char* e = getenv("DCONV_KSPLIT")) best_ks = std::max(1, std::min(atoi(e), std::min(8, S)));
+  p.ksplit = best_ks;
+  p.red_floats = p.ksplit > 1 ? red_bytes / 4 : 0;
+  const int ring_budget = kSmemBudget - bar_bytes - (p.ksplit > 1 ? red_bytes : 0);
+  p.NS = std::min(kMaxStages, ring_budget / stage_bytes);
+  p.NS = std::min(p.NS, std::max(2, (S + p.ksplit - 1) / p.ksplit));
   // partial sums cover >= 256 products before folding into the TMEM total
   const int k_stage = p.G * p.R * p.w_f * kCB;
   p.flush_every = std::max(1, (256 + k_stage - 1) / k_stage);
@@ -513,17 +617,30 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
     return dconv_host::set_error(DCONV_EUNSUPPORTED,
                                  "conv_ffma: stage of %d bytes does not fit "
                                  "shared memory twice", stage_bytes);
-  const size_t smem = (size_t)p.NS * stage_bytes + bar_bytes;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(conv_ffma_kernel<BM, BN, WF>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_set = true;
+  const size_t smem = (size_t)p.NS * stage_bytes + (p.ksplit > 1 ? red_bytes : 0) + bar_bytes;
+  // persistent: clusters of ksplit CTAs walk the work units round-robin
+  int slots = p.ksplit > 1 ? slots_cache[p.ksplit] : sms;
+  const int clusters = (int)std::min<int64_t>(units, std::max(1, slots));
+  if (p.ksplit == 1) {
+    kernel<<<clusters, kThreads, smem, stream>>>(p);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = p.ksplit;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(clusters * p.ksplit);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, p);
+    if (e != cudaSuccess)
+      return dconv_host::set_error(DCONV_ECUDA, "conv_ffma (cluster %d): %s", p.ksplit,
+                                   cudaGetErrorString(e));
   }
-  // persistent: one CTA per SM walks the work units round-robin
-  const int64_t units = (int64_t)p.tiles_y * p.tiles_x * co_groups;
-  const int grid = (int)std::min<int64_t>(units, sms);
-  conv_ffma_kernel<BM, BN, WF><<<grid, kThreads, smem, stream>>>(p);
   dconv_host::count_launch();
   return dconv_host::check_launch("conv_ffma_kernel");
 }

@@ -26,6 +26,8 @@ struct FfmaParams {
   int G, R, n_g, n_r, PH, PW;
   int slab_floats, patch_floats, wstride_floats, stage_floats, NS;
   int flush_every;          // stages per partial sum before the TMEM fold
+  int ksplit;               // CTAs per cluster sharing one unit's K range (1,2,4,8)
+  int red_floats;           // smem floats of the split-K partial buffer
 };
 
 extern int ffma_variant_override;  // -1 = heuristic (dconv_cuda_set_ffma_variant)

@@ -453,3 +453,35 @@ def test_co_shard_plan_world1_matches_unsharded():
         assert torch.equal(a.output.buf, b.output.buf)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ks", [2, 4, 8])
+def test_cluster_split_k(ks, monkeypatch):
+    """Split-K over a thread-block cluster with the DSMEM reduction, forced
+    to ks CTAs per unit: several units per cluster (barrier phases), ragged
+    stage splits, both CTA tiles; bitwise repeatable."""
+    monkeypatch.setenv("DCONV_KSPLIT", str(ks))
+    lib = _abi.lib()
+    try:
+        cases = [(64, 64, 58, 58, 3, 1, 1), (40, 136, 17, 23, 3, 1, 3), (96, 72, 13, 31, 1, 2, 2),
+                 (200, 24, 9, 9, 3, 2, 4), (24, 40, 17, 23, 5, 1, 2), (512, 128, 9, 9, 3, 1, 2)]
+        for variant in (0, 1):
+            _abi.check(lib.dconv_cuda_set_ffma_variant(variant))
+            for t, (ci, co, hi, wi, f, s, n) in enumerate(cases):
+                x = po.uniform((n, ci, hi, wi), 8000 + t, ks)
+                k = po.uniform((ci, co, f, f), 8100 + t, ks)
+                l = nets.Layer("k", ci, co, hi, wi, f, f, s)
+                a = nets.Act(n, ci, hi, wi)
+                a.buf.copy_(dev(np.stack([po.pack_feature_map(x[i], 8) for i in range(n)])))
+                wb = nets.pack_weights(dev(k), False)
+                y = nets.Act(n, co, l.h_o, l.w_o)
+                nets.conv(l, n, a, wb, y, epilogue=_abi.EPI_RELU)
+                got = host(y.buf)
+                y2 = nets.Act(n, co, l.h_o, l.w_o)
+                nets.conv(l, n, a, wb, y2, epilogue=_abi.EPI_RELU)
+                assert np.array_equal(got, host(y2.buf)), "split-K not bitwise repeatable"
+                for i in range(n):
+                    want = np.maximum(po.pack_feature_map(po.conv_oracle64(x[i], k, s), 8), 0)
+                    assert_tol(got[i], want, f"ks={ks} v{variant} case {t} img {i}")
+    finally:
+        lib.dconv_cuda_set_ffma_variant(-1)
