@@ -536,6 +536,10 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
     p.G = std::max(1, std::min(kWeightBudget / full_taps_bytes,
                                kPatchBudget / std::max(1, patch1)));
     p.G = std::min(p.G, p.ib_n);
+    // few work units (batch-1 layers): finer stages so split-K can spread
+    // one unit over up to 8 CTAs
+    const int64_t units0 = (int64_t)p.tiles_y * p.tiles_x * co_groups;
+    if (units0 * 2 < sms) p.G = 1;
   } else {
     p.G = 1;
     p.R = std::max(1, kWeightBudget / (CG * p.w_f * kCB * kCB * 4));
