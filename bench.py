@@ -318,11 +318,15 @@ def main_gpu(args):
         if "gflops" in rec:
             rec["frac_fp32_peak"] = round(rec["gflops"] / 1e3 / peak, 3)
 
-    traffic = None
+    traffic, traffic_note = None, None
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get(args.config)
+            t = json.load(open(tfile)).get(args.config)
+            if t:
+                traffic = t["dram_bytes"]
+                traffic_note = (f"{t['kernel']}: dram {t['dram_bytes']} B vs algorithmic "
+                                f"{t['algorithmic_bytes']} B per launch ({t['source']})")
         except Exception:
             traffic = None
 
@@ -359,7 +363,7 @@ def main_gpu(args):
                    "graph": graph is not None, "gflop_per_step": round(flops_job / 1e9, 3)},
         "roofline": {"bound": "fp32", "achieved": round(achieved, 2), "peak": round(peak, 2),
                      "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if peak > 0 else None,
-                     "traffic": traffic,
+                     "traffic": traffic, "traffic_note": traffic_note,
                      "kernel": "conv_ffma_kernel (all blocked conv launches of the step)",
                      "peak_source": "FFMA2 throughput probe measured live on this GPU "
                                     f"(nominal {NOMINAL_FP32_TFLOPS:.1f} at 1965 MHz)",
