@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=0, help="global batch (0 = config default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--algo", default="ffma", choices=["ffma", "tf32"],
+                    help="ffma: the fp32 FFMA path (the headline); tf32: stride-1 layers on "
+                         "the tcgen05/TMEM TF32 variant (reduced precision, reported apart)")
     ap.add_argument("--shard", default="batch", choices=["batch", "co"],
                     help="batch: image ranges per rank, no collective; co: batch-1 "
                          "output-block sharding with an NCCL all-gather per layer")
@@ -200,7 +203,8 @@ def main_gpu(args):
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         plan = nets.build_plan(args.config, n_local, seed=1809 + (0 if co_shard else rank),
-                               shard=(rank, world, None) if co_shard else None)
+                               shard=(rank, world, None) if co_shard else None,
+                               algo=args.algo)
     torch.cuda.synchronize()
     flops_local = plan.flops
 
@@ -348,7 +352,8 @@ def main_gpu(args):
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32" if args.algo == "ffma" else "tf32 (stride-1 layers) + f32",
         "data": "synthetic (seeded uniform[-1,1), counter-based generator)",
         "mode": "C_o-block sharding + NCCL all-gather per layer" if co_shard else
                 "batch sharding, no collective",

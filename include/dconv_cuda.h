@@ -117,6 +117,20 @@ int dconv_cuda_conv_direct(const dconv_conv_desc* d, const float* in,
                            const float* w, const float* skip, float* out,
                            void* stream);
 
+/* tcgen05/TMEM TF32 variant (north_star "tensor-core variant"; looser
+ * tolerance).  Stride 1, c_ib == c_ob == 8.  The weights are
+ * rearranged once (like pack_kernel, tensor.cpp:85-95) into the tensor-core
+ * operand layout; the caller owns that buffer (no hidden allocation).
+ *   dconv_cuda_tf32_prepared_size   -> floats of the prepared weight buffer
+ *   dconv_cuda_prepare_tf32_weights -> blocked kernel -> prepared weights
+ *   dconv_cuda_conv_direct_tf32     -> same contract as dconv_cuda_conv_direct */
+int dconv_cuda_tf32_prepared_size(const dconv_conv_desc* d, int64_t* floats);
+int dconv_cuda_prepare_tf32_weights(const dconv_conv_desc* d, const float* w_blocked,
+                                    float* w_prepared, void* stream);
+int dconv_cuda_conv_direct_tf32(const dconv_conv_desc* d, const float* in,
+                                const float* w_prepared, const float* skip, float* out,
+                                void* stream);
+
 /* First layer: dense [N][C_i][H_i][W_i] input (the paper does not impose the
  * blocked layout on network inputs) -> blocked output.
  * d->c_ib is ignored for the input; the weights must be packed with

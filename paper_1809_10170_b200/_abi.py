@@ -48,6 +48,9 @@ _SIGS = {
     "dconv_conv_shape": (_I, [_I] * 7 + [ctypes.POINTER(_I)] * 2),
     "dconv_conv_flops": (_L, [_I] * 6),
     "dconv_cuda_conv_direct": (_I, [ctypes.POINTER(ConvDesc), _P, _P, _P, _P, _P]),
+    "dconv_cuda_tf32_prepared_size": (_I, [ctypes.POINTER(ConvDesc), ctypes.POINTER(_L)]),
+    "dconv_cuda_prepare_tf32_weights": (_I, [ctypes.POINTER(ConvDesc), _P, _P, _P]),
+    "dconv_cuda_conv_direct_tf32": (_I, [ctypes.POINTER(ConvDesc), _P, _P, _P, _P, _P]),
     "dconv_cuda_conv_first_layer": (
         _I, [ctypes.POINTER(ConvDesc), _P, _L, _P, _P, _P, _P]),
     "dconv_cuda_pack_kernel": (_I, [_P] + [_I] * 6 + [_P, _P]),

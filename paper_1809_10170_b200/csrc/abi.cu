@@ -195,6 +195,52 @@ int dconv_cuda_conv_direct(const dconv_conv_desc* d, const float* in,
   return set_error(DCONV_EUNSUPPORTED, "algo %d not available", algo);
 }
 
+int dconv_cuda_tf32_prepared_size(const dconv_conv_desc* d, int64_t* floats) {
+  if (!d || !floats) return set_error(DCONV_EPARAM, "NULL argument");
+  Resolved r;
+  static const float dummy = 0.f;
+  int rc = resolve(d, false, 0, &dummy, &dummy, nullptr, &dummy, &r);
+  if (rc) return rc;
+  if (d->c_ib != 8 || d->c_ob != 8)
+    return set_error(DCONV_EUNSUPPORTED, "TF32 path needs c_ib == c_ob == 8");
+  *floats = dconv_dev::tf32_prepared_floats(r.ib_n, d->h_f, d->w_f, r.jb_count);
+  return DCONV_OK;
+}
+
+int dconv_cuda_prepare_tf32_weights(const dconv_conv_desc* d, const float* w,
+                                    float* w_prepared, void* stream) {
+  Resolved r;
+  int rc = resolve(d, false, 0, w, w, nullptr, w_prepared, &r);
+  if (rc) return rc;
+  if (d->c_ib != 8 || d->c_ob != 8)
+    return set_error(DCONV_EUNSUPPORTED, "TF32 path needs c_ib == c_ob == 8");
+  return dconv_dev::launch_prepare_tf32(w, r.ib_n, d->h_f, d->w_f, r.jb_begin, r.jb_count,
+                                        w_prepared, as_stream(stream));
+}
+
+int dconv_cuda_conv_direct_tf32(const dconv_conv_desc* d, const float* in,
+                                const float* w_prepared, const float* skip, float* out,
+                                void* stream) {
+  Resolved r;
+  int rc = resolve(d, false, 0, in, w_prepared, skip, out, &r);
+  if (rc) return rc;
+  if (d->c_ib != 8 || d->c_ob != 8 || !aligned16(in) || !aligned16(w_prepared) ||
+      !aligned16(out) || (skip && !aligned16(skip)) ||
+      ((r.in_img | r.in_blk | r.in_row | r.out_img | r.out_blk | r.out_row | r.sk_img |
+        r.sk_blk | r.sk_row) & 3) != 0)
+    return set_error(DCONV_EUNSUPPORTED, "TF32 path needs c_ib == c_ob == 8, aligned views");
+  dconv_dev::FfmaParams p{};
+  p.in = in; p.w = nullptr; p.skip = skip; p.out = out;
+  p.n = d->n; p.h_i = d->h_i; p.w_i = d->w_i; p.h_o = d->h_o; p.w_o = d->w_o;
+  p.h_f = d->h_f; p.w_f = d->w_f; p.s = d->stride;
+  p.ib_n = r.ib_n; p.jb_n = r.jb_n; p.jb_begin = r.jb_begin; p.jb_count = r.jb_count;
+  p.in_img = r.in_img; p.in_blk = r.in_blk; p.in_row = r.in_row;
+  p.out_img = r.out_img; p.out_blk = r.out_blk; p.out_row = r.out_row;
+  p.sk_img = r.sk_img; p.sk_blk = r.sk_blk; p.sk_row = r.sk_row;
+  p.epi = d->epilogue;
+  return dconv_dev::launch_conv_tf32(p, w_prepared, as_stream(stream));
+}
+
 int dconv_cuda_conv_first_layer(const dconv_conv_desc* d, const float* in_dense,
                                 int64_t in_img_stride, const float* w,
                                 const float* skip, float* out, void* stream) {

@@ -34,6 +34,13 @@ extern int ffma_variant_override;  // -1 = heuristic (dconv_cuda_set_ffma_varian
 
 int launch_conv_ffma(const FfmaParams& p, cudaStream_t stream);
 
+// tcgen05/TMEM TF32 variant (conv_tf32.cu): weights prepared once into the
+// UMMA K-major layout by launch_prepare_tf32.
+int64_t tf32_prepared_floats(int ib_n, int h_f, int w_f, int jb_count);
+int launch_prepare_tf32(const float* w, int ib_n, int h_f, int w_f, int jb_begin, int jb_count,
+                        float* out, cudaStream_t stream);
+int launch_conv_tf32(const FfmaParams& p, const float* w_prepared, cudaStream_t stream);
+
 // Generic (any c_ib / c_ob) reference-order kernel and the first-layer reader.
 struct GenericParams {
   const float* in;

@@ -1,0 +1,431 @@
+// conv_tf32.cu -- tcgen05/TMEM TF32 variant of the direct convolution
+// (north_star: "optional tcgen05/TMEM TF32 implicit-tile variant").
+//
+// Same algorithm and layout as conv_ffma.cu (Alg. 3, blocked
+// c_b = 8), executed on the 5th-generation tensor cores:
+//   D[128 px x N ch] (TMEM, fp32) += A[128 px x 8 ch] * B[8 ch x N ch]
+// per filter tap (n, m) and input block i' -- one tcgen05.mma.kind::tf32
+// with K = 8 = c_ib.
+//
+// A operand straight from the blocked map: a tensor-map TMA splits each
+// 32-byte pencil of the input patch into two 16-byte channel planes
+// (channels 0-3 and 4-7).  With 8-pixel-wide tiles, 8 consecutive pixels of
+// one plane are one 128-byte UMMA core matrix (K-major, no swizzle), the next
+// tile row is SBO = PW*16 bytes away and the second K chunk LBO = one plane
+// away -- so every tap (n, m) is just a different descriptor start address
+// into the same staged patch (no im2col, no copies).
+// B operand: the weights, rearranged once (prepare kernel below) into
+// [co-group][i'][n][m][k-half][N][4] so each stage is one contiguous bulk
+// copy already in the K-major core-matrix layout.
+//
+// Roles: warp 0 = TMA producer, warp 1 = MMA issuer (one thread), warps 2-5
+// = epilogue (tcgen05.ld of their TMEM lane quarter -> fused skip/ReLU ->
+// blocked pencil stores).  A unit = 4 M-tiles (64 rows x 8 cols) x N
+// channels, accumulated in all 512 TMEM columns.
+//
+// Precision: TF32 inputs (10-bit mantissa), fp32 accumulation; tolerance is
+// stated separately (tests/test_gpu_parity.py::test_tf32_*).
+#include <algorithm>
+#include <cstdio>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "conv_kernels.h"
+
+namespace dconv_dev {
+
+namespace {
+
+constexpr int kMT = 4;          // M-tiles (128 pixels each) per work unit
+constexpr int kTileRows = 16;   // an M-tile is 16 output rows x 8 columns
+constexpr int kTW = 8;
+constexpr int kMaxStagesT = 8;
+constexpr int kThreadsT = 6 * 32;
+
+struct Tf32Params {
+  const float* w;     // prepared weights
+  const float* skip;
+  float* out;
+  int n, h_i, w_i, h_o, w_o, h_f, w_f;
+  int ib_n, jb_begin, jb_count;
+  int N;              // channels per work unit (64 or 128), 8 | N
+  int n_cg;           // channel groups
+  int64_t out_img, out_blk, out_row, sk_img, sk_blk, sk_row;
+  int epi;
+  int G, R, n_g, n_r, PH, PW;
+  int plane_floats;   // one channel half-plane of a stage: G*PH*PW*4
+  int wstage_floats;  // G*R*w_f*2*N*4
+  int stage_floats;
+  int NS;
+  int row_groups, strips, units;
+  uint32_t idesc;
+};
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version 1 (sm_100); no swizzle, base offset 0
+  return d;
+}
+
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, int c3, int c4, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32x32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, "
+      "%8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, "
+      "%23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+        "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),
+        "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]),
+        "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__global__ void __launch_bounds__(kThreadsT, 1)
+    conv_tf32_kernel(const __grid_constant__ CUtensorMap tmap, const Tf32Params p) {
+  extern __shared__ __align__(1024) float smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.NS * p.stage_floats);
+  uint64_t* empty = full + kMaxStagesT;
+  uint64_t* acc_full = empty + kMaxStagesT;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = p.n_g * p.n_r;
+  const uint32_t tmem_cols = kMT * p.N <= 256 ? 256 : 512;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < p.NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 4);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  // unit u -> (channel group fastest, then strip, row group, image)
+  auto decode = [&](int u, int& img, int& y0, int& x0, int& cg) {
+    cg = u % p.n_cg;
+    int t = u / p.n_cg;
+    const int strip = t % p.strips;
+    t /= p.strips;
+    const int rg = t % p.row_groups;
+    img = t / p.row_groups;
+    y0 = rg * kMT * kTileRows;
+    x0 = strip * kTW;
+  };
+
+  if (warp == 0) {
+    // ----------------------------------------------------------- producer
+    if (lane == 0) {
+      int gs = 0;
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        int img, y0, x0, cg;
+        decode(u, img, y0, x0, cg);
+        for (int st = 0; st < S; ++st, ++gs) {
+          const int buf = gs % p.NS;
+          if (gs >= p.NS) mbar_wait(&empty[buf], ((gs / p.NS) - 1) & 1);
+          const int g = st / p.n_r, r = st - g * p.n_r;
+          const int ib0 = g * p.G, n0 = r * p.R;
+          const int Ge = min(p.G, p.ib_n - ib0), Re = min(p.R, p.h_f - n0);
+          float* sp = smem + buf * p.stage_floats;
+          // the TMA box always lands whole (OOB elements zero-filled)
+          const uint32_t patch_bytes = 2u * (uint32_t)(p.G * p.PH * p.PW * 4) * 4u;
+          const uint32_t wbytes = (uint32_t)(Ge * Re * p.w_f * 2 * p.N * 4) * 4u;
+          mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes);
+          tma_load_5d(sp, &tmap, 0, 0, x0, y0 + n0, img * p.ib_n + ib0, &full[buf]);
+          tma_load_5d(sp + p.plane_floats, &tmap, 0, 1, x0, y0 + n0, img * p.ib_n + ib0,
+                      &full[buf]);
+          const float* wsrc =
+              p.w + (((int64_t)cg * p.ib_n + ib0) * p.h_f + n0) * (int64_t)p.w_f * 2 * p.N * 4;
+          bulk_g2s(sp + 2 * p.plane_floats, wsrc, wbytes, &full[buf]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ----------------------------------------------------------- MMA issuer
+    int gs = 0, ui = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++ui) {
+      int img, y0, x0, cg;
+      decode(u, img, y0, x0, cg);
+      const int valid_rows = min(kMT * kTileRows, p.h_o - y0);
+      const int mts = (valid_rows + kTileRows - 1) / kTileRows;
+      if (ui > 0) mbar_wait(acc_empty, (ui - 1) & 1);  // epilogue drained TMEM
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int st = 0; st < S; ++st, ++gs) {
+        const int buf = gs % p.NS;
+        mbar_wait(&full[buf], (gs / p.NS) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int g = st / p.n_r, r = st - g * p.n_r;
+        const int Ge = min(p.G, p.ib_n - g * p.G);
+        const int Re = min(p.R, p.h_f - r * p.R);
+        const float* sp = smem + buf * p.stage_floats;
+        const uint32_t a_base = smem_u32(sp);
+        const uint32_t b_base = smem_u32(sp + 2 * p.plane_floats);
+        if (lane == 0) {
+          for (int gi = 0; gi < Ge; ++gi)
+            for (int n = 0; n < Re; ++n)
+              for (int m = 0; m < p.w_f; ++m) {
+                const uint64_t bdesc = umma_desc(
+                    b_base + (uint32_t)((((gi * p.R + n) * p.w_f + m) * 2) * p.N * 16),
+                    (uint32_t)(p.N * 16), 128u);
+                const bool first = (st == 0 && gi == 0 && n == 0 && m == 0);
+                for (int mt = 0; mt < mts; ++mt) {
+                  const uint64_t adesc = umma_desc(
+                      a_base + (uint32_t)(((gi * p.PH + mt * kTileRows + n) * p.PW + m) * 16),
+                      (uint32_t)(p.plane_floats * 4), (uint32_t)(p.PW * 16));
+                  umma_tf32(tmem_base + (uint32_t)(mt * p.N), adesc, bdesc, p.idesc,
+                            first ? 0u : 1u);
+                }
+              }
+          umma_commit(&empty[buf]);  // stage smem free once these MMAs retire
+          if (st == S - 1) umma_commit(acc_full);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ----------------------------------------------------------- epilogue
+    const int q = warp & 3;  // TMEM lane quarter of this warp
+    const int r = q * 32 + lane;  // pixel row of the M-tile
+    const int ty = r / kTW, tx = r % kTW;
+    int ui = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++ui) {
+      int img, y0, x0, cg;
+      decode(u, img, y0, x0, cg);
+      mbar_wait(acc_full, ui & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int x = x0 + tx;
+      for (int mt = 0; mt < kMT; ++mt) {
+        const int y = y0 + mt * kTileRows + ty;
+        if (y0 + mt * kTileRows >= p.h_o) break;  // warp-uniform
+        for (int c0 = 0; c0 < p.N; c0 += 32) {
+          float v[32];
+          tmem_ld32x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(mt * p.N + c0), v);
+          if (y >= p.h_o || x >= p.w_o) continue;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int jb = cg * (p.N / 8) + (c0 / 8) + b;  // block within the computed range
+            if (jb >= p.jb_count) break;
+            float* o = p.out + (int64_t)img * p.out_img + (int64_t)jb * p.out_blk +
+                       (int64_t)y * p.out_row + (int64_t)x * 8;
+            float* vv = v + b * 8;
+            if (p.epi & DCONV_EPI_ADD) {
+              const float* sk = p.skip + (int64_t)img * p.sk_img + (int64_t)jb * p.sk_blk +
+                                (int64_t)y * p.sk_row + (int64_t)x * 8;
+              const float4 s0 = *reinterpret_cast<const float4*>(sk);
+              const float4 s1 = *reinterpret_cast<const float4*>(sk + 4);
+              vv[0] += s0.x; vv[1] += s0.y; vv[2] += s0.z; vv[3] += s0.w;
+              vv[4] += s1.x; vv[5] += s1.y; vv[6] += s1.z; vv[7] += s1.w;
+            }
+            if (p.epi & DCONV_EPI_RELU) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) vv[i] = fmaxf(vv[i], 0.f);
+            }
+            *reinterpret_cast<float4*>(o) = make_float4(vv[0], vv[1], vv[2], vv[3]);
+            *reinterpret_cast<float4*>(o + 4) = make_float4(vv[4], vv[5], vv[6], vv[7]);
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty);
+    }
+  }
+
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(tmem_cols));
+  }
+}
+
+// Prepared weights: [cg][i'][n][m][k-half][N][4] from the blocked kernel
+// [jb][i'][n][m][ii][jj] (tensor.hpp:131-137); channel slots beyond jb_count
+// blocks are zero.  Bit-exact permutation.
+__global__ void prepare_tf32_weights_kernel(const float* __restrict__ w, int ib_n, int h_f,
+                                            int w_f, int jb_begin, int jb_count, int N,
+                                            int64_t total, float* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = e;
+    const int k4 = (int)(t % 4); t /= 4;
+    const int co = (int)(t % N); t /= N;
+    const int kh = (int)(t % 2); t /= 2;
+    const int m = (int)(t % w_f); t /= w_f;
+    const int n = (int)(t % h_f); t /= h_f;
+    const int ib = (int)(t % ib_n); t /= ib_n;
+    const int cg = (int)t;
+    const int jl = cg * (N / 8) + co / 8;  // block within the computed range
+    float v = 0.f;
+    if (jl < jb_count) {
+      const int jb = jb_begin + jl, jj = co % 8, ii = kh * 4 + k4;
+      v = w[(((((int64_t)jb * ib_n + ib) * h_f + n) * w_f + m) * 8 + ii) * 8 + jj];
+    }
+    out[e] = v;
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+int tf32_channels(int jb_count) { return jb_count * 8 >= 128 ? 128 : (jb_count * 8 > 64 ? 128 : 64); }
+
+int64_t tf32_prepared_floats(int ib_n, int h_f, int w_f, int jb_count) {
+  const int N = tf32_channels(jb_count);
+  const int n_cg = (jb_count * 8 + N - 1) / N;
+  return (int64_t)n_cg * ib_n * h_f * w_f * 2 * N * 4;
+}
+
+int launch_prepare_tf32(const float* w, int ib_n, int h_f, int w_f, int jb_begin, int jb_count,
+                        float* out, cudaStream_t stream) {
+  const int N = tf32_channels(jb_count);
+  const int64_t total = tf32_prepared_floats(ib_n, h_f, w_f, jb_count);
+  int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 32);
+  prepare_tf32_weights_kernel<<<(unsigned)blocks, 256, 0, stream>>>(w, ib_n, h_f, w_f, jb_begin,
+                                                                    jb_count, N, total, out);
+  dconv_host::count_launch();
+  return dconv_host::check_launch("prepare_tf32_weights_kernel");
+}
+
+int launch_conv_tf32(const FfmaParams& f, const float* w_prepared, cudaStream_t stream) {
+  if (f.s != 1)
+    return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_tf32: stride %d (only 1)", f.s);
+  if (f.in_img != (int64_t)f.ib_n * f.in_blk)
+    return dconv_host::set_error(DCONV_EUNSUPPORTED,
+                                 "conv_tf32: input view must stack blocks densely per image");
+  auto enc = encode_fn();
+  if (!enc) return dconv_host::set_error(DCONV_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  Tf32Params p{};
+  p.w = w_prepared;
+  p.skip = f.skip;
+  p.out = f.out;
+  p.n = f.n; p.h_i = f.h_i; p.w_i = f.w_i; p.h_o = f.h_o; p.w_o = f.w_o;
+  p.h_f = f.h_f; p.w_f = f.w_f;
+  p.ib_n = f.ib_n; p.jb_begin = f.jb_begin; p.jb_count = f.jb_count;
+  p.N = tf32_channels(f.jb_count);
+  p.n_cg = (f.jb_count * 8 + p.N - 1) / p.N;
+  p.out_img = f.out_img; p.out_blk = f.out_blk; p.out_row = f.out_row;
+  p.sk_img = f.sk_img; p.sk_blk = f.sk_blk; p.sk_row = f.sk_row;
+  p.epi = f.epi;
+  p.PW = kTW - 1 + p.w_f;
+  // stage = G input blocks x R filter rows, <= 48 KB of weights
+  const int wtap = 2 * p.N * 4 * 4;  // bytes per (i', n, m)
+  if (p.h_f * p.w_f * wtap <= 48 * 1024) {
+    p.R = p.h_f;
+    p.G = std::max(1, std::min(p.ib_n, (48 * 1024) / (p.h_f * p.w_f * wtap)));
+  } else {
+    p.G = 1;
+    p.R = std::max(1, std::min(p.h_f, (48 * 1024) / (p.w_f * wtap)));
+  }
+  p.n_g = (p.ib_n + p.G - 1) / p.G;
+  p.n_r = (p.h_f + p.R - 1) / p.R;
+  p.PH = kMT * kTileRows - 1 + p.R;
+  if (p.PH > 256 || p.PW > 256 || p.G > 256)
+    return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_tf32: TMA box too large");
+  p.plane_floats = (p.G * p.PH * p.PW * 4 + 31) & ~31;  // TMA destinations 128 B aligned
+  p.wstage_floats = p.G * p.R * p.w_f * 2 * p.N * 4;
+  p.stage_floats = ((2 * p.plane_floats + p.wstage_floats) + 255) & ~255;  // 1 KB aligned
+  const int stage_bytes = p.stage_floats * 4;
+  const int bar_bytes = (2 * kMaxStagesT + 2) * 8 + 16;
+  p.NS = std::min(kMaxStagesT, (220 * 1024 - bar_bytes) / stage_bytes);
+  if (p.NS < 2)
+    return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_tf32: stage of %d bytes", stage_bytes);
+  p.row_groups = (p.h_o + kMT * kTileRows - 1) / (kMT * kTileRows);
+  p.strips = (p.w_o + kTW - 1) / kTW;
+  p.units = p.n * p.row_groups * p.strips * p.n_cg;
+  // instruction descriptor: D f32, A/B tf32, K-major both, N, M = 128
+  p.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(p.N >> 3) << 17) |
+            ((uint32_t)(128 >> 4) << 24);
+
+  // tensor map over the input view: {c4, half, W, H, image*block}
+  CUtensorMap map;
+  const cuuint64_t dims[5] = {4, 2, (cuuint64_t)f.w_i, (cuuint64_t)f.h_i,
+                              (cuuint64_t)f.n * f.ib_n};
+  const cuuint64_t strides[4] = {16, 32, (cuuint64_t)f.in_row * 4, (cuuint64_t)f.in_blk * 4};
+  const cuuint32_t box[5] = {4, 1, (cuuint32_t)p.PW, (cuuint32_t)p.PH, (cuuint32_t)p.G};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  const CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(f.in),
+                          dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS)
+    return dconv_host::set_error(DCONV_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+
+  static int sms = 0;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(conv_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    attr = true;
+  }
+  const size_t smem = (size_t)p.NS * stage_bytes + bar_bytes;
+  const int grid = std::min(p.units, sms);
+  conv_tf32_kernel<<<grid, kThreadsT, smem, stream>>>(map, p);
+  dconv_host::count_launch();
+  return dconv_host::check_launch("conv_tf32_kernel");
+}
+
+}  // namespace dconv_dev

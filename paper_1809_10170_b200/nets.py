@@ -212,6 +212,32 @@ def conv(l: Layer, n: int, x: "Act|torch.Tensor", w: torch.Tensor, out: Act,
                                        out.base(), st))
 
 
+def conv_tf32(l: Layer, n: int, x: "Act", wprep: torch.Tensor, out: Act,
+              epilogue: int = 0, skip: Optional[Act] = None, stream=None) -> None:
+    """tcgen05/TMEM TF32 launch of a stride-1 blocked layer (weights prepared
+    by prepare_tf32)."""
+    d = _desc(l, n, epilogue)
+    d.out_img_stride, d.out_blk_stride, d.out_row_stride = out.img, out.blk, out.row
+    d.in_img_stride, d.in_blk_stride, d.in_row_stride = x.full_view()[1:]
+    sp = 0
+    if skip is not None:
+        d.skip_img_stride, d.skip_blk_stride, d.skip_row_stride = skip.img, skip.blk, skip.row
+        sp = skip.base()
+    check(lib().dconv_cuda_conv_direct_tf32(ctypes.byref(d), x.full_view()[0], ptr(wprep), sp,
+                                            out.base(), stream_ptr(stream)))
+
+
+def prepare_tf32(l: Layer, w_blocked: torch.Tensor, stream=None) -> torch.Tensor:
+    """One-time rearrangement of a blocked kernel into the UMMA operand layout."""
+    d = _desc(l, 1)
+    sz = ctypes.c_int64(0)
+    check(lib().dconv_cuda_tf32_prepared_size(ctypes.byref(d), ctypes.byref(sz)))
+    out = torch.empty(sz.value, dtype=torch.float32, device=w_blocked.device)
+    check(lib().dconv_cuda_prepare_tf32_weights(ctypes.byref(d), ptr(w_blocked), ptr(out),
+                                                stream_ptr(stream)))
+    return out
+
+
 def maxpool_into(x: Act, out: Act, stream=None) -> None:
     check(lib().dconv_cuda_maxpool2x2_blocked(x.base(), x.n, nblk(x.c), x.h, x.w, CB,
                                               out.base(), out.img, out.blk, out.row,
@@ -254,6 +280,7 @@ class Plan:
     n: int
     layers: List[Layer]
     shard: Optional[Tuple[int, int, object]] = None
+    algo: str = "ffma"   # "tf32": stride-1 blocked layers on the tcgen05 path
     weights: Dict[str, torch.Tensor] = field(default_factory=dict)
     steps: List = field(default_factory=list)
     input: Optional[torch.Tensor] = None   # dense network input (first layer)
@@ -299,6 +326,12 @@ class Plan:
         w = self.weights[l.name]
         kind = "first" if l.first else "conv"
         if self.shard is None:
+            if self.algo == "tf32" and not l.first and l.s == 1 and in_view is None:
+                wp = prepare_tf32(l, w)
+                self.weights[l.name + ".tf32"] = wp
+                self.steps.append(Step(lambda st: conv_tf32(l, self.n, x, wp, y, epilogue, skip, st),
+                                       l.name, "tf32", self.n * l.flops, l))
+                return y
             self.steps.append(Step(lambda st: conv(l, self.n, x, w, y, epilogue, skip, st, in_view),
                                    l.name, kind, self.n * l.flops, l))
             return y
@@ -334,11 +367,12 @@ def _fill(t: torch.Tensor, seed: int, stream_id: int, scale: float = 1.0) -> Non
 
 def build_plan(config: str, n: int, seed: int = 1809, device="cuda",
                dense_weights: Optional[Dict[str, torch.Tensor]] = None,
-               shard: Optional[Tuple[int, int, object]] = None) -> Plan:
+               shard: Optional[Tuple[int, int, object]] = None, algo: str = "ffma") -> Plan:
     """Instantiates a BASELINE.json config on the current device.  ``shard``
-    = (rank, world, process group) for batch-1 C_o-block sharding."""
+    = (rank, world, process group) for batch-1 C_o-block sharding; ``algo``
+    = "tf32" runs the stride-1 blocked layers on the tcgen05 TF32 kernel."""
     layers = CONFIGS[config]
-    p = Plan(config, n, list(layers), shard=shard)
+    p = Plan(config, n, list(layers), shard=shard, algo=algo)
     for idx, l in enumerate(layers):
         wd = dense_weights[l.name] if dense_weights else None
         if wd is None:

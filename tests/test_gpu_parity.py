@@ -485,3 +485,58 @@ def test_cluster_split_k(ks, monkeypatch):
                     assert_tol(got[i], want, f"ks={ks} v{variant} case {t} img {i}")
     finally:
         lib.dconv_cuda_set_ffma_variant(-1)
+
+
+# ---------------------------------------------------------- TF32 tensor cores
+def run_conv_tf32(x, k, relu=False, skip=None):
+    """tcgen05/TMEM TF32 path through the C-ABI (stride 1, c_b = 8)."""
+    import ctypes
+    ci, hi, wi = x.shape[-3:]
+    n = x.shape[0] if x.ndim == 4 else 1
+    xs = x if x.ndim == 4 else x[None]
+    _, co, hf, wf = k.shape
+    shape = D.ConvShape(ci, co, hi, wi, hf, wf, 1)
+    d = D.make_desc(shape, n, 8, 8, (_abi.EPI_RELU if relu else 0) | (_abi.EPI_ADD if skip is not None else 0))
+    xb = dev(np.stack([po.pack_feature_map(xs[i], 8) for i in range(n)]))
+    kb = dev(po.pack_kernel(k, 8, 8))
+    sz = ctypes.c_int64(0)
+    _abi.check(_abi.lib().dconv_cuda_tf32_prepared_size(ctypes.byref(d), ctypes.byref(sz)))
+    wp = torch.empty(sz.value, device="cuda")
+    _abi.check(_abi.lib().dconv_cuda_prepare_tf32_weights(ctypes.byref(d), _abi.ptr(kb), _abi.ptr(wp),
+                                                          _abi.stream_ptr()))
+    out = torch.empty((n, (co + 7) // 8, shape.h_o, shape.w_o, 8), device="cuda")
+    sk = dev(skip) if skip is not None else None
+    _abi.check(_abi.lib().dconv_cuda_conv_direct_tf32(ctypes.byref(d), _abi.ptr(xb), _abi.ptr(wp),
+                                                      _abi.ptr(sk), _abi.ptr(out), _abi.stream_ptr()))
+    return host(out)
+
+
+def tf32_bound(x, k):
+    """|a - b| <= 2^-9 * sum|x||w| + 1e-5: TF32 keeps 10 of fp32's 23
+    mantissa bits (relative error <= 2^-10 per operand, <= 2^-9 per product)."""
+    return 2.0 ** -9 * po.pack_feature_map(po.conv_oracle64(np.abs(x), np.abs(k), 1), 8) + 1e-5
+
+
+@pytest.mark.parametrize("ci,co,h,w,f,n", [(64, 64, 18, 18, 3, 1), (16, 128, 20, 13, 3, 2),
+                                            (24, 40, 70, 21, 3, 1), (32, 256, 10, 10, 1, 3),
+                                            (8, 72, 12, 12, 5, 1), (96, 136, 9, 30, 3, 2)])
+def test_tf32_tensor_core_parity(ci, co, h, w, f, n):
+    x = po.uniform((n, ci, h, w), 9100 + ci, co)
+    k = po.uniform((ci, co, f, f), 9200 + ci, co)
+    got = run_conv_tf32(x, k)
+    for i in range(n):
+        want = po.pack_feature_map(po.conv_oracle64(x[i], k, 1), 8)
+        err = np.abs(got[i].astype(np.float64) - want)
+        bound = tf32_bound(x[i], k)
+        assert (err <= bound).all(), f"TF32 error {err.max()} exceeds bound (max ratio {(err / bound).max()})"
+        assert err.max() > 0 or ci * f * f <= 8  # it really is TF32, not an fp32 fallback
+
+
+def test_tf32_epilogue_and_padding():
+    x = po.uniform((1, 16, 12, 12), 93, 0)
+    k = po.uniform((16, 20, 3, 3), 93, 1)
+    skip = po.pack_feature_map(po.uniform((20, 10, 10), 93, 2), 8)[None]
+    got = run_conv_tf32(x, k, relu=True, skip=skip)[0]
+    want = np.maximum(po.pack_feature_map(po.conv_oracle64(x[0], k, 1), 8) + skip[0], 0)
+    assert (np.abs(got - want) <= tf32_bound(x[0], k)).all()
+    assert not got[..., 4:][-1].any(), "padded output channels must be exact 0"
