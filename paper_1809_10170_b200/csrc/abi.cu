@@ -199,7 +199,9 @@ int dconv_cuda_tf32_prepared_size(const dconv_conv_desc* d, int64_t* floats) {
   if (!d || !floats) return set_error(DCONV_EPARAM, "NULL argument");
   Resolved r;
   static const float dummy = 0.f;
-  int rc = resolve(d, false, 0, &dummy, &dummy, nullptr, &dummy, &r);
+  dconv_conv_desc geom = *d;  // geometry only: the epilogue is irrelevant here
+  geom.epilogue = DCONV_EPI_NONE;
+  int rc = resolve(&geom, false, 0, &dummy, &dummy, nullptr, &dummy, &r);
   if (rc) return rc;
   if (d->c_ib != 8 || d->c_ob != 8)
     return set_error(DCONV_EUNSUPPORTED, "TF32 path needs c_ib == c_ob == 8");
@@ -210,7 +212,9 @@ int dconv_cuda_tf32_prepared_size(const dconv_conv_desc* d, int64_t* floats) {
 int dconv_cuda_prepare_tf32_weights(const dconv_conv_desc* d, const float* w,
                                     float* w_prepared, void* stream) {
   Resolved r;
-  int rc = resolve(d, false, 0, w, w, nullptr, w_prepared, &r);
+  dconv_conv_desc geom = *d;
+  geom.epilogue = DCONV_EPI_NONE;
+  int rc = resolve(&geom, false, 0, w, w, nullptr, w_prepared, &r);
   if (rc) return rc;
   if (d->c_ib != 8 || d->c_ob != 8)
     return set_error(DCONV_EUNSUPPORTED, "TF32 path needs c_ib == c_ob == 8");
