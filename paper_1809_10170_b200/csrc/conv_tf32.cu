@@ -370,9 +370,11 @@ int launch_conv_tf32(const FfmaParams& f, const float* w_prepared, cudaStream_t 
   p.PW = kTW - 1 + p.w_f;
   // stage = G input blocks x R filter rows, <= 48 KB of weights
   const int wtap = 2 * p.N * 4 * 4;  // bytes per (i', n, m)
+  const int patch_blk_bytes = 2 * (kMT * kTileRows - 1 + p.h_f) * p.PW * 16;  // both planes
   if (p.h_f * p.w_f * wtap <= 48 * 1024) {
     p.R = p.h_f;
-    p.G = std::max(1, std::min(p.ib_n, (48 * 1024) / (p.h_f * p.w_f * wtap)));
+    p.G = std::max(1, std::min({p.ib_n, (48 * 1024) / (p.h_f * p.w_f * wtap),
+                                (40 * 1024) / patch_blk_bytes}));
   } else {
     p.G = 1;
     p.R = std::max(1, std::min(p.h_f, (48 * 1024) / (p.w_f * wtap)));
