@@ -170,6 +170,30 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def tf32_gemm_peak(stream) -> float:
+    """TF32 tensor-core roofline denominator: cuBLAS TF32 GEMM (8192^3),
+    best of 5, CUDA events (same convention as MEASURED_PEAKS.json's bf16)."""
+    import torch
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        with torch.cuda.stream(stream):
+            a = torch.randn(8192, 8192, device="cuda")
+            b = torch.randn(8192, 8192, device="cuda")
+            best = 0.0
+            for _ in range(6):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                torch.matmul(a, b)
+                e1.record(stream)
+                e1.synchronize()
+                best = max(best, 2 * 8192 ** 3 / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+        del a, b
+        return best
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
 # ------------------------------------------------------------------ GPU arm
 def main_gpu(args):
     import torch
@@ -316,7 +340,15 @@ def main_gpu(args):
             ffma_ms += ms
         else:
             other_ms += ms
-    peak = float(lib.dconv_cuda_fp32_peak_probe(stream.cuda_stream))
+    if args.algo == "tf32":
+        # tensor-core roofline: the tcgen05 launches against a cuBLAS TF32 GEMM
+        # (8192^3, torch.matmul with TF32 allowed) measured live on this GPU
+        ffma_flops = sum(s.flops for s in plan.steps if s.kind == "tf32")
+        ffma_ms = sum(statistics.median(per[s.name]) for s in plan.steps if s.kind == "tf32")
+        other_ms = sum(statistics.median(per[s.name]) for s in plan.steps if s.kind != "tf32")
+        peak = tf32_gemm_peak(stream)
+    else:
+        peak = float(lib.dconv_cuda_fp32_peak_probe(stream.cuda_stream))
     achieved = ffma_flops / (ffma_ms * 1e-3) / 1e12 if ffma_ms else 0.0
     for rec in layers:
         if "gflops" in rec:
@@ -366,12 +398,17 @@ def main_gpu(args):
                    if args.config in ("vgg16", "resnet50", "googlenet") else
                    "working set fits L2 (batch-1 config): warm-L2 numbers",
                    "graph": graph is not None, "gflop_per_step": round(flops_job / 1e9, 3)},
-        "roofline": {"bound": "fp32", "achieved": round(achieved, 2), "peak": round(peak, 2),
+        "roofline": {"bound": "fp32" if args.algo == "ffma" else "tensor",
+                     "achieved": round(achieved, 2), "peak": round(peak, 2),
                      "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if peak > 0 else None,
                      "traffic": traffic, "traffic_note": traffic_note,
-                     "kernel": "conv_ffma_kernel (all blocked conv launches of the step)",
-                     "peak_source": "FFMA2 throughput probe measured live on this GPU "
-                                    f"(nominal {NOMINAL_FP32_TFLOPS:.1f} at 1965 MHz)",
+                     "kernel": ("conv_ffma_kernel (all blocked conv launches of the step)"
+                                if args.algo == "ffma" else
+                                "conv_tf32_kernel (all stride-1 blocked conv launches)"),
+                     "peak_source": ("FFMA2 throughput probe measured live on this GPU "
+                                     f"(nominal {NOMINAL_FP32_TFLOPS:.1f} at 1965 MHz)"
+                                     if args.algo == "ffma" else
+                                     "cuBLAS TF32 GEMM 8192^3 measured live (nominal 1100 dense)"),
                      "share_of_step": round(ffma_ms / (ffma_ms + other_ms), 4)
                      if ffma_ms + other_ms else None},
         "cpu_baseline": cpu,
