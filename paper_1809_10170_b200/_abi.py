@@ -12,7 +12,7 @@ import os
 from typing import Optional
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdconv_b200.so")
+LIB_PATH = os.environ.get("DCONV_LIB") or os.path.join(_HERE, "libdconv_b200.so")  # override: A/B builds
 
 # error codes (dconv_cuda.h)
 OK, EINVAL_SHAPE, ELAYOUT, EPARAM, ECUDA, ENCCL, EUNSUPPORTED = range(7)

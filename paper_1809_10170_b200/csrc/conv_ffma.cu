@@ -335,12 +335,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 bp[1] = pack2(b0.z, b0.w);
                 bp[2] = pack2(b1.x, b1.y);
                 bp[3] = pack2(b1.z, b1.w);
+#ifndef DCONV_C_OUTER
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                   const float av = i4 == 0 ? a[k].x : i4 == 1 ? a[k].y : i4 == 2 ? a[k].z : a[k].w;
 #pragma unroll
                   for (int c = 0; c < 4; ++c) ffma2(acc[k][c], av, bp[c]);
                 }
+#else
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                  for (int k = 0; k < 8; ++k) {
+                    const float av = i4 == 0 ? a[k].x : i4 == 1 ? a[k].y : i4 == 2 ? a[k].z : a[k].w;
+                    ffma2(acc[k][c], av, bp[c]);
+                  }
+#endif
               }
             }
           }

@@ -24,4 +24,4 @@ for _ in range(10):
 b.record()
 b.synchronize()
 ms = a.elapsed_time(b) / 10
-print(f"layer {ci}->{co} {hi}x{wi} f{f} s{s} n{n}: {ms*1e3:.1f} us, {n*l.flops/ms/1e9:.1f} GFLOP/s")
+print(f"layer {ci}->{co} {hi}x{wi} f{f} s{s} n{n}: {ms*1e3:.1f} us, {n*l.flops/ms/1e9:.1f} TFLOP/s")
