@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = tid >> 5, lane = tid & 31;
   const int S = p.n_g * p.n_r;                 // stages per work unit
   const int co_groups = (p.jb_count + CG - 1) / CG;
-  const int n_units = p.tiles_y * p.tiles_x * co_groups;
+  const int n_units = p.unit_count;             // this launch's units: [unit_begin, +count)
   // Split-K over a thread-block cluster of ks CTAs: rank r runs stages
   // [st0, st1) of every unit, the partial tiles are reduced through DSMEM.
   const int ks = p.ksplit;
@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // unit u -> (co group fastest: concurrently running CTAs share the pixel
   // tile's patch rows in L2, consecutive waves reuse the weight slabs)
   auto decode = [&](int u, TileRows& tr, int& tx0, int& jb0, int& cg_valid) {
+    u += p.unit_begin;
     const int cgi = u % co_groups;
     const int t = u / co_groups;
     const int tile_y = t / p.tiles_x;
@@ -335,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 bp[1] = pack2(b0.z, b0.w);
                 bp[2] = pack2(b1.x, b1.y);
                 bp[3] = pack2(b1.z, b1.w);
-#ifndef DCONV_C_OUTER
+#ifdef DCONV_K_OUTER
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                   const float av = i4 == 0 ? a[k].x : i4 == 1 ? a[k].y : i4 == 2 ? a[k].z : a[k].w;
@@ -521,22 +522,14 @@ void pick_tile(FfmaParams& p, int BM, int co_groups, int sms) {
   }
 }
 
-template <int BM, int BN, int WF>
-int launch_variant(FfmaParams p, cudaStream_t stream) {
+// Stage geometry for split factor ks: G input blocks x R filter rows per
+// stage under a 40 KB weight / 32 KB patch budget (G = 1 when `fine`: few
+// units, or split-K whose 64 KB partial buffer shares smem with the ring),
+// NS ring depth, TMEM fold interval.  Returns the dynamic smem bytes, or 0 if
+// two stages do not fit.
+template <int BN>
+size_t configure(FfmaParams& p, int ks, bool fine) {
   constexpr int CG = BN / 8;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  const int co_groups = (p.jb_count + CG - 1) / CG;
-  pick_tile(p, BM, co_groups, sms);
-  p.TWe = std::min(p.TW, p.w_o);
-  p.PW = (p.TWe - 1) * p.s + p.w_f;
-  p.slab_floats = p.h_f * p.w_f * kCB * kCB;
-
-  // Stage decomposition (i'-groups x filter-row groups), sized for smem.
   const int kWeightBudget = 40 * 1024, kPatchBudget = 32 * 1024;
   const int full_taps_bytes = CG * p.h_f * p.w_f * kCB * kCB * 4;
   if (full_taps_bytes <= kWeightBudget) {
@@ -546,10 +539,7 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
     p.G = std::max(1, std::min(kWeightBudget / full_taps_bytes,
                                kPatchBudget / std::max(1, patch1)));
     p.G = std::min(p.G, p.ib_n);
-    // few work units (batch-1 layers): finer stages so split-K can spread
-    // one unit over up to 8 CTAs
-    const int64_t units0 = (int64_t)p.tiles_y * p.tiles_x * co_groups;
-    if (units0 * 2 < sms) p.G = 1;
+    if (fine || ks > 1) p.G = 1;
   } else {
     p.G = 1;
     p.R = std::max(1, kWeightBudget / (CG * p.w_f * kCB * kCB * 4));
@@ -562,79 +552,56 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   // +16 B per block chunk: the 8 lanes of a warp that read different output
   // blocks hit distinct 16-byte bank groups of the weight stage.
   p.wstride_floats = p.G * p.R * p.w_f * kCB * kCB + 4;
-  p.stage_floats = p.patch_floats + CG * p.wstride_floats;
-  p.stage_floats = (p.stage_floats + 31) & ~31;  // 128-byte aligned stages
-  const int stage_bytes = p.stage_floats * 4;
+  p.stage_floats = (p.patch_floats + CG * p.wstride_floats + 31) & ~31;  // 128 B aligned
   const int S = p.n_g * p.n_r;
   const int kSmemBudget = 220 * 1024;
   const int bar_bytes = (2 * kMaxStages + 2) * 8 + 16;
   const int red_bytes = 8 * 8 * kComputeWarps * 32 * 4;  // 64 floats / thread
-
-  auto kernel = conv_ffma_kernel<BM, BN, WF>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_set = true;
-  }
-  // Split-K factor: the persistent schedule runs ceil(units / slots) rounds
-  // of ceil(S / ks) stages (+ a DSMEM reduction when ks > 1); pick the
-  // cheapest.  slots = co-resident clusters of ks CTAs (GPC-limited).
-  const int64_t units = (int64_t)p.tiles_y * p.tiles_x * co_groups;
-  int best_ks = 1;
-  double best_cost = 1e300;
-  static int slots_cache[9] = {0};
-  for (int ks = 1; ks <= 8; ks *= 2) {
-    if (ks > S) break;
-    if (ks > 1 && getenv("DCONV_NO_SPLITK")) break;
-    int slots = sms;
-    if (ks > 1) {
-      if (!slots_cache[ks]) {
-        cudaLaunchConfig_t cfg{};
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = ks;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.gridDim = dim3(ks * 64);
-        cfg.blockDim = dim3(kThreads);
-        cfg.dynamicSmemBytes = 200 * 1024;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess || n < 1) {
-          cudaGetLastError();
-          n = -1;
-        }
-        slots_cache[ks] = n;
-      }
-      slots = slots_cache[ks];
-      if (slots < 1) continue;
-    }
-    const double rounds = (double)((units + slots - 1) / slots);
-    const double cost = rounds * ((S + ks - 1) / ks + (ks > 1 ? 0.35 + 0.05 * ks : 0.0));
-    if (cost < best_cost - 1e-9) {
-      best_cost = cost;
-      best_ks = ks;
-    }
-  }
-  if (const char* e = getenv("DCONV_KSPLIT")) best_ks = std::max(1, std::min(atoi(e), std::min(8, S)));
-  p.ksplit = best_ks;
-  p.red_floats = p.ksplit > 1 ? red_bytes / 4 : 0;
-  const int ring_budget = kSmemBudget - bar_bytes - (p.ksplit > 1 ? red_bytes : 0);
-  p.NS = std::min(kMaxStages, ring_budget / stage_bytes);
-  p.NS = std::min(p.NS, std::max(2, (S + p.ksplit - 1) / p.ksplit));
+  p.ksplit = ks;
+  p.red_floats = ks > 1 ? red_bytes / 4 : 0;
+  const int ring_budget = kSmemBudget - bar_bytes - (ks > 1 ? red_bytes : 0);
+  p.NS = std::min(kMaxStages, ring_budget / (p.stage_floats * 4));
+  p.NS = std::min(p.NS, std::max(2, (S + ks - 1) / ks));
   // partial sums cover >= 256 products before folding into the TMEM total
   const int k_stage = p.G * p.R * p.w_f * kCB;
   p.flush_every = std::max(1, (256 + k_stage - 1) / k_stage);
   if (const char* e = getenv("DCONV_FLUSH_EVERY")) p.flush_every = std::max(1, atoi(e));
-  if (p.NS < 2)
-    return dconv_host::set_error(DCONV_EUNSUPPORTED,
-                                 "conv_ffma: stage of %d bytes does not fit "
-                                 "shared memory twice", stage_bytes);
-  const size_t smem = (size_t)p.NS * stage_bytes + (p.ksplit > 1 ? red_bytes : 0) + bar_bytes;
-  // persistent: clusters of ksplit CTAs walk the work units round-robin
-  int slots = p.ksplit > 1 ? slots_cache[p.ksplit] : sms;
-  const int clusters = (int)std::min<int64_t>(units, std::max(1, slots));
+  if (p.NS < 2) return 0;
+  return (size_t)p.NS * p.stage_floats * 4 + (ks > 1 ? red_bytes : 0) + bar_bytes;
+}
+
+// co-resident clusters of ks CTAs at ~200 KB smem (GPC-limited); cached
+template <class K>
+int cluster_slots(K kernel, int ks, int sms) {
+  static int cache[9] = {0};
+  if (ks == 1) return sms;
+  if (!cache[ks]) {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = ks;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(ks * 64);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 200 * 1024;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess || n < 1) {
+      cudaGetLastError();
+      n = -1;
+    }
+    cache[ks] = n;
+  }
+  return cache[ks];
+}
+
+template <class K>
+int launch_units(K kernel, FfmaParams p, size_t smem, int unit_begin, int unit_count,
+                 int clusters, cudaStream_t stream) {
+  p.unit_begin = unit_begin;
+  p.unit_count = unit_count;
   if (p.ksplit == 1) {
     kernel<<<clusters, kThreads, smem, stream>>>(p);
   } else {
@@ -657,6 +624,87 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   }
   dconv_host::count_launch();
   return dconv_host::check_launch("conv_ffma_kernel");
+}
+
+template <int BM, int BN, int WF>
+int launch_variant(FfmaParams p, cudaStream_t stream) {
+  constexpr int CG = BN / 8;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int co_groups = (p.jb_count + CG - 1) / CG;
+  pick_tile(p, BM, co_groups, sms);
+  p.TWe = std::min(p.TW, p.w_o);
+  p.PW = (p.TWe - 1) * p.s + p.w_f;
+  p.slab_floats = p.h_f * p.w_f * kCB * kCB;
+  const int units = p.tiles_y * p.tiles_x * co_groups;
+  const bool fine = (int64_t)units * 2 < sms;  // batch-1 layers: split-K over fine stages
+
+  auto kernel = conv_ffma_kernel<BM, BN, WF>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_set = true;
+  }
+  FfmaParams q = p;
+  if (!configure<BN>(q, 1, fine))
+    return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_ffma: stage does not fit smem twice");
+  const int S = q.n_g * q.n_r;
+  const bool no_split = getenv("DCONV_NO_SPLITK") != nullptr;
+
+  // (1) few units (batch 1): one split-K launch.  The persistent schedule
+  // runs ceil(units / slots) rounds of ceil(S / ks) stages (+ a DSMEM
+  // reduction); pick the cheapest ks.
+  int best_ks = 1;
+  double best_cost = (double)((units + sms - 1) / sms) * S;
+  for (int ks = 2; ks <= 8 && ks <= S && !no_split; ks *= 2) {
+    const int slots = cluster_slots(kernel, ks, sms);
+    if (slots < 1) continue;
+    const double cost = (double)((units + slots - 1) / slots) *
+                        ((S + ks - 1) / ks + 0.35 + 0.05 * ks);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best_ks = ks;
+    }
+  }
+  if (const char* e = getenv("DCONV_KSPLIT")) best_ks = std::max(1, std::min(atoi(e), std::min(8, S)));
+  if (best_ks > 1) {
+    FfmaParams r = p;
+    const size_t smem = configure<BN>(r, best_ks, true);
+    if (!smem) return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_ffma: split stage");
+    const int clusters = std::min(units, std::max(1, cluster_slots(kernel, best_ks, sms)));
+    return launch_units(kernel, r, smem, 0, units, clusters, stream);
+  }
+
+  // (2) many units: full waves without splitting; a ragged last wave (< 75%
+  // of the SMs) runs as a second launch whose units are split over clusters,
+  // so the SMs that would idle help finish the tail.
+  const int main_units = units / sms * sms, tail = units - main_units;
+  int tail_ks = 1;
+  if (main_units > 0 && tail > 0 && tail * 4 < sms * 3 && !no_split &&
+      !getenv("DCONV_NO_TAILSPLIT")) {
+    for (int ks = 8; ks >= 2; ks /= 2) {
+      FfmaParams t = p;
+      if (!configure<BN>(t, ks, true)) continue;
+      if (ks > t.n_g * t.n_r) continue;
+      const int slots = cluster_slots(kernel, ks, sms);
+      if (slots >= tail) {
+        tail_ks = ks;
+        break;
+      }
+    }
+  }
+  const size_t smem_main = configure<BN>(q, 1, fine);
+  if (tail_ks == 1)
+    return launch_units(kernel, q, smem_main, 0, units, std::min(units, sms), stream);
+  int rc = launch_units(kernel, q, smem_main, 0, main_units, sms, stream);
+  if (rc) return rc;
+  FfmaParams t = p;
+  const size_t smem_tail = configure<BN>(t, tail_ks, true);
+  return launch_units(kernel, t, smem_tail, main_units, tail, tail, stream);
 }
 
 template <int BM, int BN>

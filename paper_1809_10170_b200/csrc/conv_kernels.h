@@ -28,6 +28,7 @@ struct FfmaParams {
   int flush_every;          // stages per partial sum before the TMEM fold
   int ksplit;               // CTAs per cluster sharing one unit's K range (1,2,4,8)
   int red_floats;           // smem floats of the split-K partial buffer
+  int unit_begin, unit_count;  // work units of this launch
 };
 
 extern int ffma_variant_override;  // -1 = heuristic (dconv_cuda_set_ffma_variant)

@@ -540,3 +540,24 @@ def test_tf32_epilogue_and_padding():
     want = np.maximum(po.pack_feature_map(po.conv_oracle64(x[0], k, 1), 8) + skip[0], 0)
     assert (np.abs(got - want) <= tf32_bound(x[0], k)).all()
     assert not got[..., 4:][-1].any(), "padded output channels must be exact 0"
+
+
+def test_tail_split_launch():
+    """Unit counts just above a wave (196 units on 148 SMs): the full wave runs
+    unsplit, the ragged tail as a second, split-K launch (the first unit
+    ranges of each launch and the seam between them are checked)."""
+    n, ci, co, hi = 16, 64, 64, 58
+    x = po.uniform((n, ci, hi, hi), 9300, 0)
+    k = po.uniform((ci, co, 3, 3), 9300, 1)
+    l = nets.Layer("tail", ci, co, hi, hi, 3, 3, 1)
+    a = nets.Act(n, ci, hi, hi)
+    a.buf.copy_(dev(np.stack([po.pack_feature_map(x[i], 8) for i in range(n)])))
+    y = nets.Act(n, co, l.h_o, l.w_o)
+    nets.conv(l, n, a, nets.pack_weights(dev(k), False), y)
+    got = host(y.buf)
+    kb = po.pack_kernel(k, 8, 8)
+    for i in (0, 11, 12, 15):  # main-wave images and tail images
+        xb = po.pack_feature_map(x[i], 8)
+        for r in (0, 27, 55):
+            want = po.conv_oracle64_blocked(xb, kb, ci, co, 1, r, r + 1)
+            assert_tol(got[i, :, r], want[:, r], f"img {i} row {r}")
