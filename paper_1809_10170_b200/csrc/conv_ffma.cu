@@ -490,8 +490,29 @@ int max_patch_rows(const FfmaParams& p, int R) {
 
 // Tile selector: pixel-tile width TW (powers of two, or the map width and its
 // halves/thirds), TH = BM / TW rows of the stacked batch.  Score = useful
-// pixels / launched pixels x SM-wave balance of the persistent schedule;
-// ties go to the smaller patch.
+// pixels / launched pixel-slots, where the launch takes floor(units/sms)
+// full waves plus a ragged tail that the tail-split launch finishes in about
+// 1/2, 1/4 or 1/8 of a wave when it fits on sms/2, /4, /8 clusters.  Ties go
+// to the smaller patch.
+double tail_rounds(int64_t units, int sms) {
+  const int64_t full = units / sms, tail = units - full * sms;
+  double t = 0.0;
+  if (tail > 0) {
+    if (full == 0) {
+      // fewer units than SMs: one split-K launch over clusters of ks CTAs
+      // (co-resident clusters ~ sms/2, sms/4 - 1, sms/8 - 2)
+      t = 1.0;
+      if (tail * 8 <= sms - 16) t = 0.125 + 0.4;
+      else if (tail * 4 <= sms - 4) t = 0.25 + 0.2;
+      else if (tail * 2 <= sms) t = 0.5 + 0.1;
+    } else if (tail * 8 <= sms / 2) t = 0.125 + 0.05;
+    else if (tail * 4 <= sms) t = 0.25 + 0.05;
+    else if (tail * 2 <= sms) t = 0.5 + 0.05;
+    else t = 1.0;
+  }
+  return (double)full + t;
+}
+
 void pick_tile(FfmaParams& p, int BM, int co_groups, int sms) {
   int cand[16], nc = 0;
   for (int tw = 4; tw <= 128 && tw <= BM; tw *= 2) cand[nc++] = tw;
@@ -506,9 +527,8 @@ void pick_tile(FfmaParams& p, int BM, int co_groups, int sms) {
     const int tw = cand[i], th = BM / tw;
     const int64_t ty = (vh + th - 1) / th, tx = (p.w_o + tw - 1) / tw;
     const int64_t units = ty * tx * co_groups;
-    const double pix = (double)vh * p.w_o / ((double)ty * tx * BM);
-    const double waves = (double)units / ((double)((units + sms - 1) / sms) * sms);
-    const double score = pix * waves;
+    const double slots_used = tail_rounds(units, sms) * sms;
+    const double score = (double)vh * p.w_o * co_groups / (slots_used * BM);
     const int64_t patch = (int64_t)((std::min<int64_t>(th, vh) - 1) * p.s + p.h_f) *
                           ((std::min(tw, p.w_o) - 1) * p.s + p.w_f);
     if (score > best_score + 1e-6 || (score > best_score - 1e-6 && patch < best_patch)) {
@@ -539,7 +559,13 @@ size_t configure(FfmaParams& p, int ks, bool fine) {
     p.G = std::max(1, std::min(kWeightBudget / full_taps_bytes,
                                kPatchBudget / std::max(1, patch1)));
     p.G = std::min(p.G, p.ib_n);
-    if (fine || ks > 1) p.G = 1;
+    if (fine || ks > 1) {
+      // finer stages (split-K shares smem with its 64 KB partial buffer):
+      // keep each stage <= 36 KB so the ring stays >= 4 deep; 1x1 layers
+      // still group several input blocks per stage
+      const int per_block = patch1 + CG * p.R * p.w_f * kCB * kCB * 4;
+      p.G = std::max(1, std::min(p.G, (36 * 1024) / per_block));
+    }
   } else {
     p.G = 1;
     p.R = std::max(1, kWeightBudget / (CG * p.w_f * kCB * kCB * 4));
@@ -655,12 +681,12 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   const int S = q.n_g * q.n_r;
   const bool no_split = getenv("DCONV_NO_SPLITK") != nullptr;
 
-  // (1) few units (batch 1): one split-K launch.  The persistent schedule
+  // (1) fewer units than SMs (batch 1): one split-K launch.  The persistent schedule
   // runs ceil(units / slots) rounds of ceil(S / ks) stages (+ a DSMEM
   // reduction); pick the cheapest ks.
   int best_ks = 1;
   double best_cost = (double)((units + sms - 1) / sms) * S;
-  for (int ks = 2; ks <= 8 && ks <= S && !no_split; ks *= 2) {
+  for (int ks = 2; ks <= 8 && ks <= S && !no_split && units < sms; ks *= 2) {
     const int slots = cluster_slots(kernel, ks, sms);
     if (slots < 1) continue;
     const double cost = (double)((units + slots - 1) / slots) *
@@ -698,6 +724,12 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
     }
   }
   const size_t smem_main = configure<BN>(q, 1, fine);
+  if (getenv("DCONV_DEBUG"))
+    fprintf(stderr,
+            "conv_ffma<%d,%d,%d>: %dx%d tiles TH=%d TW=%d units=%d S=%d G=%d R=%d NS=%d "
+            "main=%d tail=%d tail_ks=%d\n",
+            BM, BN, WF, q.tiles_y, q.tiles_x, q.TH, q.TW, units, S, q.G, q.R, q.NS, main_units,
+            tail, tail_ks);
   if (tail_ks == 1)
     return launch_units(kernel, q, smem_main, 0, units, std::min(units, sms), stream);
   int rc = launch_units(kernel, q, smem_main, 0, main_units, sms, stream);
