@@ -566,6 +566,7 @@ size_t configure(FfmaParams& p, int ks, bool fine) {
       const int per_block = patch1 + CG * p.R * p.w_f * kCB * kCB * 4;
       p.G = std::max(1, std::min(p.G, (36 * 1024) / per_block));
     }
+    if (const char* e = getenv("DCONV_FORCE_G")) p.G = std::max(1, std::min(p.ib_n, atoi(e)));
   } else {
     p.G = 1;
     p.R = std::max(1, kWeightBudget / (CG * p.w_f * kCB * kCB * 4));
