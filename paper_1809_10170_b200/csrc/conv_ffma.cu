@@ -313,19 +313,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int Re = min(p.R, p.h_f - r * p.R);
       const float* sp = smem + buf * p.stage_floats;
       const float* sw = sp + p.patch_floats + cb * p.wstride_floats;
+      // per-pixel patch pointers once per stage; rows and taps then add a
+      // warp-uniform offset (measured +1%; swapping the channel-half order
+      // between warpgroups to de-phase their LDS bubbles measured -2.5%).
+      const float* pk[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) pk[k] = sp + poff[k];
       for (int gi = 0; gi < Ge; ++gi) {
         for (int n = 0; n < Re; ++n) {
-          const float* pa_row = sp + ((gi * p.PH + n) * p.PW) * kCB;
+          const int row_off = ((gi * p.PH + n) * p.PW) * kCB;
           const float* pw_row = sw + ((gi * p.R + n) * wf) * (kCB * kCB);
 #pragma unroll(WF > 0 ? WF : 1)
           for (int m = 0; m < wf; ++m) {
-            const float* pa = pa_row + m * kCB;
             const float* pw = pw_row + m * (kCB * kCB);
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {
+            for (int h = 0; h < 2; ++h) {
+              const int half = h;
               float4 a[8];
 #pragma unroll
-              for (int k = 0; k < 8; ++k) a[k] = lds128(pa + poff[k] + half * 4);
+              for (int k = 0; k < 8; ++k) a[k] = lds128(pk[k] + row_off + m * kCB + half * 4);
 #pragma unroll
               for (int i4 = 0; i4 < 4; ++i4) {
                 const float* pb = pw + (half * 4 + i4) * kCB;
@@ -336,14 +342,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 bp[1] = pack2(b0.z, b0.w);
                 bp[2] = pack2(b1.x, b1.y);
                 bp[3] = pack2(b1.z, b1.w);
-#ifdef DCONV_K_OUTER
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                  const float av = i4 == 0 ? a[k].x : i4 == 1 ? a[k].y : i4 == 2 ? a[k].z : a[k].w;
-#pragma unroll
-                  for (int c = 0; c < 4; ++c) ffma2(acc[k][c], av, bp[c]);
-                }
-#else
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
 #pragma unroll
@@ -351,7 +349,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float av = i4 == 0 ? a[k].x : i4 == 1 ? a[k].y : i4 == 2 ? a[k].z : a[k].w;
                     ffma2(acc[k][c], av, bp[c]);
                   }
-#endif
               }
             }
           }
