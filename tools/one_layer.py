@@ -1,5 +1,5 @@
 """Runs one conv layer a few times (for ncu / compute-sanitizer captures).
-usage: python tools/one_layer.py CI CO HI WI F S N [reps]"""
+usage: python tools/one_layer.py CI CO HI WI F S N [reps] [ffma|tf32]"""
 import sys
 
 import torch
@@ -9,19 +9,25 @@ from paper_1809_10170_b200 import nets  # noqa: E402
 
 ci, co, hi, wi, f, s, n = (int(v) for v in sys.argv[1:8])
 reps = int(sys.argv[8]) if len(sys.argv) > 8 else 3
+algo = sys.argv[9] if len(sys.argv) > 9 else "ffma"
 l = nets.Layer("one", ci, co, hi, wi, f, f, s)
 x = nets.Act(n, ci, hi, wi)
 x.buf.uniform_(-1, 1)
 w = nets.pack_weights(torch.empty((ci, co, f, f), device="cuda").uniform_(-1, 1), False)
 y = nets.Act(n, co, l.h_o, l.w_o)
+if algo == "tf32":
+    wp = nets.prepare_tf32(l, w)
+    run = lambda: nets.conv_tf32(l, n, x, wp, y)  # noqa: E731
+else:
+    run = lambda: nets.conv(l, n, x, w, y)  # noqa: E731
 for _ in range(reps):
-    nets.conv(l, n, x, w, y)
+    run()
 torch.cuda.synchronize()
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 a.record()
 for _ in range(10):
-    nets.conv(l, n, x, w, y)
+    run()
 b.record()
 b.synchronize()
 ms = a.elapsed_time(b) / 10
-print(f"layer {ci}->{co} {hi}x{wi} f{f} s{s} n{n}: {ms*1e3:.1f} us, {n*l.flops/ms/1e9:.1f} TFLOP/s")
+print(f"{algo} layer {ci}->{co} {hi}x{wi} f{f} s{s} n{n}: {ms*1e3:.1f} us, {n*l.flops/ms/1e9:.1f} TFLOP/s")
