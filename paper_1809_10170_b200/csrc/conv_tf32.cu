@@ -20,8 +20,8 @@
 //
 // Roles: warp 0 = TMA producer, warp 1 = MMA issuer (one thread), warps 2-5
 // = epilogue (tcgen05.ld of their TMEM lane quarter -> fused skip/ReLU ->
-// blocked pencil stores).  A unit = 4 M-tiles (64 rows x 8 cols) x N
-// channels, accumulated in all 512 TMEM columns.
+// blocked pencil stores).  A unit = MT <= 4 M-tiles (16*MT rows x 8 cols)
+// x N channels, accumulated in up to 512 TMEM columns.
 //
 // Precision: TF32 inputs (10-bit mantissa), fp32 accumulation; tolerance is
 // stated separately (tests/test_gpu_parity.py::test_tf32_*).
@@ -37,7 +37,7 @@ namespace dconv_dev {
 
 namespace {
 
-constexpr int kMT = 4;          // M-tiles (128 pixels each) per work unit
+constexpr int kMaxMT = 4;       // M-tiles (128 pixels each) per work unit, at most
 constexpr int kTileRows = 16;   // an M-tile is 16 output rows x 8 columns
 constexpr int kTW = 8;
 constexpr int kMaxStagesT = 8;
@@ -59,6 +59,7 @@ struct Tf32Params {
   int stage_floats;
   int NS;
   int row_groups, strips, units;
+  int MT;             // M-tiles per unit (1..4)
   uint32_t idesc;
 };
 
@@ -126,7 +127,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = p.n_g * p.n_r;
-  const uint32_t tmem_cols = kMT * p.N <= 256 ? 256 : 512;
+  const uint32_t tmem_cols = kMaxMT * p.N <= 256 ? 256 : 512;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < p.NS; ++i) {
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
     t /= p.strips;
     const int rg = t % p.row_groups;
     img = t / p.row_groups;
-    y0 = rg * kMT * kTileRows;
+    y0 = rg * p.MT * kTileRows;
     x0 = strip * kTW;
   };
 
@@ -193,7 +194,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
     for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++ui) {
       int img, y0, x0, cg;
       decode(u, img, y0, x0, cg);
-      const int valid_rows = min(kMT * kTileRows, p.h_o - y0);
+      const int valid_rows = min(p.MT * kTileRows, p.h_o - y0);
       const int mts = (valid_rows + kTileRows - 1) / kTileRows;
       if (ui > 0) mbar_wait(acc_empty, (ui - 1) & 1);  // epilogue drained TMEM
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       mbar_wait(acc_full, ui & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int x = x0 + tx;
-      for (int mt = 0; mt < kMT; ++mt) {
+      for (int mt = 0; mt < p.MT; ++mt) {
         const int y = y0 + mt * kTileRows + ty;
         if (y0 + mt * kTileRows >= p.h_o) break;  // warp-uniform
         for (int c0 = 0; c0 < p.N; c0 += 32) {
@@ -370,7 +371,33 @@ int launch_conv_tf32(const FfmaParams& f, const float* w_prepared, cudaStream_t 
   p.PW = kTW - 1 + p.w_f;
   // stage = G input blocks x R filter rows, <= 48 KB of weights
   const int wtap = 2 * p.N * 4 * 4;  // bytes per (i', n, m)
-  const int patch_blk_bytes = 2 * (kMT * kTileRows - 1 + p.h_f) * p.PW * 16;  // both planes
+  // M-tiles per unit: more tiles share each weight stage (less L2/smem
+  // traffic per MAC); fewer give more units.  Score = useful rows x SM-wave
+  // balance (a ragged last wave costs a full round here), ties -> larger MT.
+  {
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int strips = (p.w_o + kTW - 1) / kTW;
+    double best = -1;
+    for (int mt = kMaxMT; mt >= 1; --mt) {
+      const int rg = (p.h_o + mt * kTileRows - 1) / (mt * kTileRows);
+      const int64_t units = (int64_t)p.n * rg * strips * p.n_cg;
+      const double rows_eff = (double)p.h_o / (rg * mt * kTileRows);
+      const double waves = (double)units / ((double)((units + sms - 1) / sms) * sms);
+      const double traffic = 1.0 - 0.06 * (kMaxMT - mt);  // weight reuse across M-tiles
+      const double score = rows_eff * waves * traffic;
+      if (score > best + 1e-6) {
+        best = score;
+        p.MT = mt;
+      }
+    }
+    if (const char* e = getenv("DCONV_TF32_MT")) p.MT = std::max(1, std::min(kMaxMT, atoi(e)));
+  }
+  const int patch_blk_bytes = 2 * (p.MT * kTileRows - 1 + p.h_f) * p.PW * 16;  // both planes
   if (p.h_f * p.w_f * wtap <= 48 * 1024) {
     p.R = p.h_f;
     p.G = std::max(1, std::min({p.ib_n, (48 * 1024) / (p.h_f * p.w_f * wtap),
@@ -381,7 +408,7 @@ int launch_conv_tf32(const FfmaParams& f, const float* w_prepared, cudaStream_t 
   }
   p.n_g = (p.ib_n + p.G - 1) / p.G;
   p.n_r = (p.h_f + p.R - 1) / p.R;
-  p.PH = kMT * kTileRows - 1 + p.R;
+  p.PH = p.MT * kTileRows - 1 + p.R;
   if (p.PH > 256 || p.PW > 256 || p.G > 256)
     return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_tf32: TMA box too large");
   p.plane_floats = (p.G * p.PH * p.PW * 4 + 31) & ~31;  // TMA destinations 128 B aligned
@@ -392,7 +419,7 @@ int launch_conv_tf32(const FfmaParams& f, const float* w_prepared, cudaStream_t 
   p.NS = std::min(kMaxStagesT, (220 * 1024 - bar_bytes) / stage_bytes);
   if (p.NS < 2)
     return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_tf32: stage of %d bytes", stage_bytes);
-  p.row_groups = (p.h_o + kMT * kTileRows - 1) / (kMT * kTileRows);
+  p.row_groups = (p.h_o + p.MT * kTileRows - 1) / (p.MT * kTileRows);
   p.strips = (p.w_o + kTW - 1) / kTW;
   p.units = p.n * p.row_groups * p.strips * p.n_cg;
   // instruction descriptor: D f32, A/B tf32, K-major both, N, M = 128
