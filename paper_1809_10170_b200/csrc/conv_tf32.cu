@@ -373,7 +373,8 @@ int launch_conv_tf32(const FfmaParams& f, const float* w_prepared, cudaStream_t 
   const int wtap = 2 * p.N * 4 * 4;  // bytes per (i', n, m)
   // M-tiles per unit: more tiles share each weight stage (less L2/smem
   // traffic per MAC); fewer give more units.  Score = useful rows x SM-wave
-  // balance (a ragged last wave costs a full round here), ties -> larger MT.
+  // balance (a ragged last wave costs a full round) / load-bound cost; ties
+  // go to the larger MT.
   {
     static int sms = 0;
     if (!sms) {
@@ -388,8 +389,10 @@ int launch_conv_tf32(const FfmaParams& f, const float* w_prepared, cudaStream_t 
       const int64_t units = (int64_t)p.n * rg * strips * p.n_cg;
       const double rows_eff = (double)p.h_o / (rg * mt * kTileRows);
       const double waves = (double)units / ((double)((units + sms - 1) / sms) * sms);
-      const double traffic = 1.0 - 0.06 * (kMaxMT - mt);  // weight reuse across M-tiles
-      const double score = rows_eff * waves * traffic;
+      // a stage's loads take about as long as 2.5 M-tiles of MMAs, so units
+      // with fewer M-tiles turn load-bound: time per pixel ~ max(mt, 2.5)/mt
+      const double cost = std::max((double)mt, 2.5) / mt;
+      const double score = rows_eff * waves / cost;
       if (score > best + 1e-6) {
         best = score;
         p.MT = mt;
