@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--batch", type=int, default=0, help="global batch (0 = config default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-tune", action="store_true",
+                    help="skip the per-layer CTA-tile autotune at plan build")
     ap.add_argument("--algo", default="ffma", choices=["ffma", "tf32"],
                     help="ffma: the fp32 FFMA path (the headline); tf32: stride-1 layers on "
                          "the tcgen05/TMEM TF32 variant (reduced precision, reported apart)")
@@ -243,7 +245,8 @@ def main_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- warm-up (eager), then capture one step as a CUDA graph
+    # ---- per-layer tile autotune (plan build, untimed), warm-up, graph capture
+    tiles = {} if args.no_tune or args.algo != "ffma" else plan.autotune(stream)
     for _ in range(args.warmup):
         plan.run(stream)
     stream.synchronize()
@@ -397,7 +400,9 @@ def main_gpu(args):
                    "l2": "per-step working set > 126 MB L2 (activations streamed)"
                    if args.config in ("vgg16", "resnet50", "googlenet") else
                    "working set fits L2 (batch-1 config): warm-L2 numbers",
-                   "graph": graph is not None, "gflop_per_step": round(flops_job / 1e9, 3)},
+                   "graph": graph is not None, "gflop_per_step": round(flops_job / 1e9, 3),
+                   "tiles": {k: ["", "128x128", "256x64", "192x128/12w", "384x64/12w"][v]
+                             for k, v in tiles.items()}},
         "roofline": {"bound": "fp32" if args.algo == "ffma" else "tensor",
                      "achieved": round(achieved, 2), "peak": round(peak, 2),
                      "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if peak > 0 else None,

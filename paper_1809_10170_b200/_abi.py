@@ -30,7 +30,8 @@ class ConvDesc(ctypes.Structure):
             "out_img_stride", "out_blk_stride", "out_row_stride",
             "skip_img_stride", "skip_blk_stride", "skip_row_stride")] + [
         ("epilogue", ctypes.c_int), ("algo", ctypes.c_int),
-        ("co_block_begin", ctypes.c_int), ("co_block_count", ctypes.c_int)]
+        ("co_block_begin", ctypes.c_int), ("co_block_count", ctypes.c_int),
+        ("tile_variant", ctypes.c_int)]
 
 
 class DconvError(RuntimeError):

@@ -173,6 +173,7 @@ int dconv_cuda_conv_direct(const dconv_conv_desc* d, const float* in,
     p.out_img = r.out_img; p.out_blk = r.out_blk; p.out_row = r.out_row;
     p.sk_img = r.sk_img; p.sk_blk = r.sk_blk; p.sk_row = r.sk_row;
     p.epi = d->epilogue;
+    p.variant = d->tile_variant > 0 ? d->tile_variant - 1 : -1;
     rc = dconv_dev::launch_conv_ffma(p, as_stream(stream));
     // AUTO: a configuration whose stage cannot be staged in shared memory
     // (very large filters on tiny maps) runs on the generic kernel instead.
@@ -355,7 +356,7 @@ int dconv_cuda_zero(float* x, int64_t count, void* stream) {
 }
 
 int dconv_cuda_set_ffma_variant(int variant) {
-  if (variant < -1 || variant > 1) return set_error(DCONV_EPARAM, "variant %d", variant);
+  if (variant < -1 || variant > 3) return set_error(DCONV_EPARAM, "variant %d", variant);
   dconv_dev::ffma_variant_override = variant;
   return DCONV_OK;
 }

@@ -39,9 +39,8 @@ namespace {
 
 constexpr int kCB = 8;          // channel block of this kernel (c_ib = c_ob)
 constexpr int kMaxStages = 8;
-constexpr int kComputeWarps = 8;  // 2 compute warpgroups, 8x8 outputs / thread
+constexpr int kComputeWarps = 8;  // default: 2 compute warpgroups, 8x8 outputs / thread
 constexpr int kThreads = (kComputeWarps + 4) * 32;  // + producer warpgroup
-constexpr int kTmemCols = 128;  // running totals: NW/4 slots x 8*TCO columns
 
 // ---- TMEM helpers (32 lanes x 32 columns of 32-bit per warp) ----------------
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
@@ -142,11 +141,14 @@ __device__ __forceinline__ void tile_row(const FfmaParams& p, const TileRows& t,
   }
 }
 
-template <int BM, int BN, int WF>
-__global__ void __launch_bounds__(kThreads, 1)
+// NW compute warps (8: 232 registers each; 12: 152 registers, 3 warps per
+// SMSP for latency hiding, activations loaded 2 channels at a time).
+template <int BM, int BN, int WF, int NW>
+__global__ void __launch_bounds__((NW + 4) * 32, 1)
     conv_ffma_kernel(const FfmaParams p) {
   constexpr int TCO = 8;         // channels per thread (one output block)
-  constexpr int NW = kComputeWarps;
+  constexpr int AV = NW == 8 ? 4 : 2;  // activation channels per LDS
+  constexpr int kTmemCols = NW <= 8 ? 128 : 256;  // NW/4 slots x 64 columns
   constexpr int PG = BM / 8;     // pixel groups (8 pixels each)
   constexpr int CGT = BN / TCO;  // channel thread groups == output blocks
   constexpr int WPG = PG / 4;    // warps along pixels
@@ -272,7 +274,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   // -------------------------------------------------------------- consumers
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+  if constexpr (NW == 8) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 152;");
+  }
   const int wr = warp % WPG, wc = warp / WPG;
   const int pg = wr * 4 + (lane & 3);
   const int cb = wc * 8 + (lane >> 2);  // output block within the CTA tile
@@ -327,14 +333,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int m = 0; m < wf; ++m) {
             const float* pw = pw_row + m * (kCB * kCB);
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < 8 / AV; ++h) {
               const int half = h;
-              float4 a[8];
+              float a[8][AV];
 #pragma unroll
-              for (int k = 0; k < 8; ++k) a[k] = lds128(pk[k] + row_off + m * kCB + half * 4);
+              for (int k = 0; k < 8; ++k) {
+                if constexpr (AV == 4) {
+                  const float4 t = lds128(pk[k] + row_off + m * kCB + half * 4);
+                  a[k][0] = t.x; a[k][1] = t.y; a[k][2] = t.z; a[k][3] = t.w;
+                } else {
+                  const float2 t = *reinterpret_cast<const float2*>(pk[k] + row_off + m * kCB + half * 2);
+                  a[k][0] = t.x; a[k][1] = t.y;
+                }
+              }
 #pragma unroll
-              for (int i4 = 0; i4 < 4; ++i4) {
-                const float* pb = pw + (half * 4 + i4) * kCB;
+              for (int i4 = 0; i4 < AV; ++i4) {
+                const float* pb = pw + (half * AV + i4) * kCB;
                 const float4 b0 = lds128(pb);
                 const float4 b1 = lds128(pb + 4);
                 uint64_t bp[4];
@@ -345,10 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
 #pragma unroll
-                  for (int k = 0; k < 8; ++k) {
-                    const float av = i4 == 0 ? a[k].x : i4 == 1 ? a[k].y : i4 == 2 ? a[k].z : a[k].w;
-                    ffma2(acc[k][c], av, bp[c]);
-                  }
+                  for (int k = 0; k < 8; ++k) ffma2(acc[k][c], a[k][i4], bp[c]);
               }
             }
           }
@@ -544,7 +555,7 @@ void pick_tile(FfmaParams& p, int BM, int co_groups, int sms) {
 // units, or split-K whose 64 KB partial buffer shares smem with the ring),
 // NS ring depth, TMEM fold interval.  Returns the dynamic smem bytes, or 0 if
 // two stages do not fit.
-template <int BN>
+template <int BN, int NW>
 size_t configure(FfmaParams& p, int ks, bool fine) {
   constexpr int CG = BN / 8;
   const int kWeightBudget = 40 * 1024, kPatchBudget = 32 * 1024;
@@ -580,7 +591,7 @@ size_t configure(FfmaParams& p, int ks, bool fine) {
   const int S = p.n_g * p.n_r;
   const int kSmemBudget = 220 * 1024;
   const int bar_bytes = (2 * kMaxStages + 2) * 8 + 16;
-  const int red_bytes = 8 * 8 * kComputeWarps * 32 * 4;  // 64 floats / thread
+  const int red_bytes = 8 * 8 * NW * 32 * 4;  // 64 floats / thread
   p.ksplit = ks;
   p.red_floats = ks > 1 ? red_bytes / 4 : 0;
   const int ring_budget = kSmemBudget - bar_bytes - (ks > 1 ? red_bytes : 0);
@@ -596,7 +607,7 @@ size_t configure(FfmaParams& p, int ks, bool fine) {
 
 // co-resident clusters of ks CTAs at ~200 KB smem (GPC-limited); cached
 template <class K>
-int cluster_slots(K kernel, int ks, int sms) {
+int cluster_slots(K kernel, int ks, int sms, int threads) {
   static int cache[9] = {0};
   if (ks == 1) return sms;
   if (!cache[ks]) {
@@ -607,7 +618,7 @@ int cluster_slots(K kernel, int ks, int sms) {
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3(ks * 64);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = 200 * 1024;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
@@ -622,12 +633,12 @@ int cluster_slots(K kernel, int ks, int sms) {
 }
 
 template <class K>
-int launch_units(K kernel, FfmaParams p, size_t smem, int unit_begin, int unit_count,
-                 int clusters, cudaStream_t stream) {
+int launch_units(K kernel, int threads, FfmaParams p, size_t smem, int unit_begin,
+                 int unit_count, int clusters, cudaStream_t stream) {
   p.unit_begin = unit_begin;
   p.unit_count = unit_count;
   if (p.ksplit == 1) {
-    kernel<<<clusters, kThreads, smem, stream>>>(p);
+    kernel<<<clusters, threads, smem, stream>>>(p);
   } else {
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute attr[1];
@@ -636,7 +647,7 @@ int launch_units(K kernel, FfmaParams p, size_t smem, int unit_begin, int unit_c
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3(clusters * p.ksplit);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cfg.attrs = attr;
@@ -650,8 +661,9 @@ int launch_units(K kernel, FfmaParams p, size_t smem, int unit_begin, int unit_c
   return dconv_host::check_launch("conv_ffma_kernel");
 }
 
-template <int BM, int BN, int WF>
+template <int BM, int BN, int WF, int NW>
 int launch_variant(FfmaParams p, cudaStream_t stream) {
+  constexpr int threads = (NW + 4) * 32;
   constexpr int CG = BN / 8;
   static int sms = 0;
   if (!sms) {
@@ -667,17 +679,19 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   const int units = p.tiles_y * p.tiles_x * co_groups;
   const bool fine = (int64_t)units * 2 < sms;  // batch-1 layers: split-K over fine stages
 
-  auto kernel = conv_ffma_kernel<BM, BN, WF>;
+  auto kernel = conv_ffma_kernel<BM, BN, WF, NW>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = true;
   }
   FfmaParams q = p;
-  if (!configure<BN>(q, 1, fine))
+  if (!configure<BN, NW>(q, 1, fine))
     return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_ffma: stage does not fit smem twice");
   const int S = q.n_g * q.n_r;
-  const bool no_split = getenv("DCONV_NO_SPLITK") != nullptr;
+  // the 12-warp variant's partial buffer (96 KB) leaves no room for a ring:
+  // it never splits K
+  const bool no_split = getenv("DCONV_NO_SPLITK") != nullptr || NW != 8;
 
   // (1) fewer units than SMs (batch 1): one split-K launch.  The persistent schedule
   // runs ceil(units / slots) rounds of ceil(S / ks) stages (+ a DSMEM
@@ -685,7 +699,7 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   int best_ks = 1;
   double best_cost = (double)((units + sms - 1) / sms) * S;
   for (int ks = 2; ks <= 8 && ks <= S && !no_split && units < sms; ks *= 2) {
-    const int slots = cluster_slots(kernel, ks, sms);
+    const int slots = cluster_slots(kernel, ks, sms, threads);
     if (slots < 1) continue;
     const double cost = (double)((units + slots - 1) / slots) *
                         ((S + ks - 1) / ks + 0.35 + 0.05 * ks);
@@ -697,10 +711,10 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   if (const char* e = getenv("DCONV_KSPLIT")) best_ks = std::max(1, std::min(atoi(e), std::min(8, S)));
   if (best_ks > 1) {
     FfmaParams r = p;
-    const size_t smem = configure<BN>(r, best_ks, true);
+    const size_t smem = configure<BN, NW>(r, best_ks, true);
     if (!smem) return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_ffma: split stage");
-    const int clusters = std::min(units, std::max(1, cluster_slots(kernel, best_ks, sms)));
-    return launch_units(kernel, r, smem, 0, units, clusters, stream);
+    const int clusters = std::min(units, std::max(1, cluster_slots(kernel, best_ks, sms, threads)));
+    return launch_units(kernel, threads, r, smem, 0, units, clusters, stream);
   }
 
   // (2) many units: full waves without splitting; a ragged last wave (< 75%
@@ -712,16 +726,16 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
       !getenv("DCONV_NO_TAILSPLIT")) {
     for (int ks = 8; ks >= 2; ks /= 2) {
       FfmaParams t = p;
-      if (!configure<BN>(t, ks, true)) continue;
+      if (!configure<BN, NW>(t, ks, true)) continue;
       if (ks > t.n_g * t.n_r) continue;
-      const int slots = cluster_slots(kernel, ks, sms);
+      const int slots = cluster_slots(kernel, ks, sms, threads);
       if (slots >= tail) {
         tail_ks = ks;
         break;
       }
     }
   }
-  const size_t smem_main = configure<BN>(q, 1, fine);
+  const size_t smem_main = configure<BN, NW>(q, 1, fine);
   if (getenv("DCONV_DEBUG"))
     fprintf(stderr,
             "conv_ffma<%d,%d,%d>: %dx%d tiles TH=%d TW=%d units=%d S=%d G=%d R=%d NS=%d "
@@ -729,21 +743,21 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
             BM, BN, WF, q.tiles_y, q.tiles_x, q.TH, q.TW, units, S, q.G, q.R, q.NS, main_units,
             tail, tail_ks);
   if (tail_ks == 1)
-    return launch_units(kernel, q, smem_main, 0, units, std::min(units, sms), stream);
-  int rc = launch_units(kernel, q, smem_main, 0, main_units, sms, stream);
+    return launch_units(kernel, threads, q, smem_main, 0, units, std::min(units, sms), stream);
+  int rc = launch_units(kernel, threads, q, smem_main, 0, main_units, sms, stream);
   if (rc) return rc;
   FfmaParams t = p;
-  const size_t smem_tail = configure<BN>(t, tail_ks, true);
-  return launch_units(kernel, t, smem_tail, main_units, tail, tail, stream);
+  const size_t smem_tail = configure<BN, NW>(t, tail_ks, true);
+  return launch_units(kernel, threads, t, smem_tail, main_units, tail, tail, stream);
 }
 
-template <int BM, int BN>
+template <int BM, int BN, int NW = 8>
 int launch_wf(const FfmaParams& p, cudaStream_t stream) {
   switch (p.w_f) {
-    case 1: return launch_variant<BM, BN, 1>(p, stream);
-    case 3: return launch_variant<BM, BN, 3>(p, stream);
-    case 5: return launch_variant<BM, BN, 5>(p, stream);
-    default: return launch_variant<BM, BN, 0>(p, stream);
+    case 1: return launch_variant<BM, BN, 1, NW>(p, stream);
+    case 3: return launch_variant<BM, BN, 3, NW>(p, stream);
+    case 5: return launch_variant<BM, BN, 5, NW>(p, stream);
+    default: return launch_variant<BM, BN, 0, NW>(p, stream);
   }
 }
 
@@ -752,11 +766,16 @@ int launch_wf(const FfmaParams& p, cudaStream_t stream) {
 int ffma_variant_override = -1;  // test/tuning hook (dconv_cuda_set_ffma_variant)
 
 int launch_conv_ffma(const FfmaParams& p, cudaStream_t stream) {
-  int v = ffma_variant_override;
-  if (v < 0) v = p.jb_count >= 16 ? 0 : 1;
+  int v = p.variant >= 0 ? p.variant : ffma_variant_override;
+  // measured (tools/sweep_variants.py): 256 px x 64 ch wins on every 3x3 /
+  // 5x5 layer of the configs; 1x1 layers with >= 128 output channels
+  // (little reuse per staged pixel) prefer 128 px x 128 ch
+  if (v < 0) v = (p.h_f * p.w_f == 1 && p.jb_count >= 16) ? 0 : 1;
   switch (v) {
     case 0: return launch_wf<128, 128>(p, stream);  // 128 px x 128 channels
-    default: return launch_wf<256, 64>(p, stream);  // 256 px x 64 channels
+    case 1: return launch_wf<256, 64>(p, stream);   // 256 px x 64 channels
+    case 2: return launch_wf<192, 128, 12>(p, stream);  // 12 compute warps
+    default: return launch_wf<384, 64, 12>(p, stream);  // 12 compute warps
   }
 }
 

@@ -29,6 +29,7 @@ struct FfmaParams {
   int ksplit;               // CTAs per cluster sharing one unit's K range (1,2,4,8)
   int red_floats;           // smem floats of the split-K partial buffer
   int unit_begin, unit_count;  // work units of this launch
+  int variant;                 // requested CTA tile (-1 = selector)
 };
 
 extern int ffma_variant_override;  // -1 = heuristic (dconv_cuda_set_ffma_variant)

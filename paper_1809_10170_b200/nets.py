@@ -183,7 +183,7 @@ class Act:
 def conv(l: Layer, n: int, x: "Act|torch.Tensor", w: torch.Tensor, out: Act,
          epilogue: int = 0, skip: Optional[Act] = None, stream=None,
          in_view: Optional[Tuple[int, int, int, int]] = None,
-         co_range: Optional[Tuple[int, int]] = None) -> None:
+         co_range: Optional[Tuple[int, int]] = None, tile_variant: int = 0) -> None:
     """Launch one conv layer through the C-ABI.  ``x`` is an Act (blocked) or,
     for a first layer, the dense [n][c][h][w] network input.  ``in_view``
     optionally overrides (ptr, img, blk, row) of the blocked input (crops).
@@ -191,6 +191,7 @@ def conv(l: Layer, n: int, x: "Act|torch.Tensor", w: torch.Tensor, out: Act,
     blocks into ``out`` (a rank's C_o slice); ``skip`` is then read from the
     same blocks of the full skip map."""
     d = _desc(l, n, epilogue)
+    d.tile_variant = tile_variant
     d.out_img_stride, d.out_blk_stride, d.out_row_stride = out.img, out.blk, out.row
     b0 = 0
     if co_range is not None:
@@ -282,6 +283,7 @@ class Plan:
     shard: Optional[Tuple[int, int, object]] = None
     algo: str = "ffma"   # "tf32": stride-1 blocked layers on the tcgen05 path
     weights: Dict[str, torch.Tensor] = field(default_factory=dict)
+    tiles: Dict[str, int] = field(default_factory=dict)  # autotuned FFMA CTA tile per layer
     steps: List = field(default_factory=list)
     input: Optional[torch.Tensor] = None   # dense network input (first layer)
     output: Optional[Act] = None
@@ -296,6 +298,35 @@ class Plan:
     def run(self, stream=None) -> None:
         for st in self.steps:
             st.fn(stream)
+
+    def autotune(self, stream=None, variants=(1, 2), reps: int = 3) -> Dict[str, int]:
+        """Times every FFMA conv step with each CTA tile (desc.tile_variant)
+        on the plan's own buffers and keeps the fastest -- the GPU analogue of
+        the reference's autotune (model.hpp:103-109), run
+        once at plan build, outside any timed region."""
+        import statistics
+        s = stream or torch.cuda.current_stream()
+        for st in self.steps:
+            if st.kind != "conv":
+                continue
+            best, best_ms = 0, None
+            for v in variants:
+                self.tiles[st.name] = v
+                ts = []
+                for r in range(reps + 1):
+                    a = torch.cuda.Event(enable_timing=True)
+                    b = torch.cuda.Event(enable_timing=True)
+                    a.record(s)
+                    st.fn(s)
+                    b.record(s)
+                    b.synchronize()
+                    if r:
+                        ts.append(a.elapsed_time(b))
+                ms = statistics.median(ts)
+                if best_ms is None or ms < best_ms:
+                    best, best_ms = v, ms
+            self.tiles[st.name] = best
+        return dict(self.tiles)
 
     def io_inputs(self) -> List[torch.Tensor]:
         """Device tensors that are the step's inputs (network input, or every
@@ -332,7 +363,8 @@ class Plan:
                 self.steps.append(Step(lambda st: conv_tf32(l, self.n, x, wp, y, epilogue, skip, st),
                                        l.name, "tf32", self.n * l.flops, l))
                 return y
-            self.steps.append(Step(lambda st: conv(l, self.n, x, w, y, epilogue, skip, st, in_view),
+            self.steps.append(Step(lambda st: conv(l, self.n, x, w, y, epilogue, skip, st, in_view,
+                                                   tile_variant=self.tiles.get(l.name, 0)),
                                    l.name, kind, self.n * l.flops, l))
             return y
         from .shard import block_range
@@ -343,7 +375,8 @@ class Plan:
         ys = self._local(y, cnt * CB)
         flops = l.flops * min(cnt * CB, l.c_o - b0 * CB) // l.c_o
         self.steps.append(Step(lambda st: conv(l, self.n, x, w, ys, epilogue, skip, st, in_view,
-                                               (b0, cnt)), l.name, kind, flops, l))
+                                               (b0, cnt), tile_variant=self.tiles.get(l.name, 0)),
+                               l.name, kind, flops, l))
         if gather:
             self._gather(l.name, y, ys)
         return ys
