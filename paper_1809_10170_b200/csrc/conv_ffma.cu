@@ -143,16 +143,17 @@ __device__ __forceinline__ void tile_row(const FfmaParams& p, const TileRows& t,
 
 // NW compute warps (8: 232 registers each; 12: 152 registers, 3 warps per
 // SMSP for latency hiding, activations loaded 2 channels at a time).
-template <int BM, int BN, int WF, int NW>
+template <int BM, int BN, int WF, int NW, int TPX>
 __global__ void __launch_bounds__((NW + 4) * 32, 1)
     conv_ffma_kernel(const FfmaParams p) {
   constexpr int TCO = 8;         // channels per thread (one output block)
   constexpr int AV = NW == 8 ? 4 : 2;  // activation channels per LDS
-  constexpr int kTmemCols = NW <= 8 ? 128 : 256;  // NW/4 slots x 64 columns
-  constexpr int PG = BM / 8;     // pixel groups (8 pixels each)
+  // TMEM running totals: NW/4 warp slots x TPX*8 columns
+  constexpr int kTmemCols = (NW / 4) * TPX * 8 <= 128 ? 128 : ((NW / 4) * TPX * 8 <= 256 ? 256 : 512);
+  constexpr int PG = BM / TPX;   // pixel groups (TPX pixels each)
   constexpr int CGT = BN / TCO;  // channel thread groups == output blocks
   constexpr int WPG = PG / 4;    // warps along pixels
-  constexpr int NP = 8 * TCO / 2;  // accumulator pairs per thread
+  constexpr int NP = TPX * TCO / 2;  // accumulator pairs per thread
   static_assert(PG * CGT == NW * 32, "thread tile mismatch");
   constexpr int CG = BN / 8;     // output blocks per CTA tile
 
@@ -285,7 +286,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
 
   const uint32_t tmem_base = use_tmem ? *tmem_slot : 0u;
   const uint32_t taddr = tmem_base + ((uint32_t)((warp & 3) * 32) << 16) +
-                         (uint32_t)((warp >> 2) * 8 * TCO);
+                         (uint32_t)((warp >> 2) * TPX * TCO);
   const int wf = WF > 0 ? WF : p.w_f;
 
   int gs = 0, unit_iter = 0;
@@ -295,18 +296,18 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
     decode(u, tr, tx0, jb0, cg_valid);
     // per-pixel patch offsets of this tile (pixels that do not exist read
     // offset 0 and are never stored)
-    int poff[8];
+    int poff[TPX];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < TPX; ++k) {
       const int q = pg + PG * k;
       const int ty = q / p.TW, tx = q - ty * p.TW;
       int img, y, prow;
       tile_row(p, tr, ty, img, y, prow);
       poff[k] = (ty < tr.th && tx0 + tx < p.w_o) ? (prow * p.PW + tx * p.s) * kCB : 0;
     }
-    uint64_t acc[8][TCO / 2];
+    uint64_t acc[TPX][TCO / 2];
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
+    for (int k = 0; k < TPX; ++k)
 #pragma unroll
       for (int c = 0; c < TCO / 2; ++c) acc[k][c] = 0ull;
     bool have_total = false;
@@ -322,9 +323,9 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
       // per-pixel patch pointers once per stage; rows and taps then add a
       // warp-uniform offset (measured +1%; swapping the channel-half order
       // between warpgroups to de-phase their LDS bubbles measured -2.5%).
-      const float* pk[8];
+      const float* pk[TPX];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) pk[k] = sp + poff[k];
+      for (int k = 0; k < TPX; ++k) pk[k] = sp + poff[k];
       for (int gi = 0; gi < Ge; ++gi) {
         for (int n = 0; n < Re; ++n) {
           const int row_off = ((gi * p.PH + n) * p.PW) * kCB;
@@ -335,9 +336,9 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
 #pragma unroll
             for (int h = 0; h < 8 / AV; ++h) {
               const int half = h;
-              float a[8][AV];
+              float a[TPX][AV];
 #pragma unroll
-              for (int k = 0; k < 8; ++k) {
+              for (int k = 0; k < TPX; ++k) {
                 if constexpr (AV == 4) {
                   const float4 t = lds128(pk[k] + row_off + m * kCB + half * 4);
                   a[k][0] = t.x; a[k][1] = t.y; a[k][2] = t.z; a[k][3] = t.w;
@@ -359,7 +360,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
 #pragma unroll
-                  for (int k = 0; k < 8; ++k) ffma2(acc[k][c], a[k][i4], bp[c]);
+                  for (int k = 0; k < TPX; ++k) ffma2(acc[k][c], a[k][i4], bp[c]);
               }
             }
           }
@@ -374,7 +375,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         have_total = true;
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
+        for (int k = 0; k < TPX; ++k)
 #pragma unroll
           for (int c = 0; c < TCO / 2; ++c) acc[k][c] = 0ull;
       }
@@ -385,11 +386,11 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
     // Split-K: every rank publishes its partial tile in its own smem, then
     // rank r sums pixels [r*8/ks, (r+1)*8/ks) of every thread's 8x8 tile over
     // ranks 0..ks-1 in that fixed order (deterministic, no global workspace).
-    int k_lo = 0, k_hi = 8;
+    int k_lo = 0, k_hi = TPX;
     if (ks > 1) {
       if (unit_iter > 0) mbar_wait_cluster(done, (unit_iter - 1) & 1);
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
+      for (int k = 0; k < TPX; ++k)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const float2 f = unpack2(acc[k][c]);
@@ -400,15 +401,15 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
       if (lane == 0)
         for (int q = 0; q < ks; ++q) mbar_arrive_remote(ready, q);
       mbar_wait_cluster(ready, unit_iter & 1);
-      k_lo = rank * 8 / ks;
-      k_hi = (rank + 1) * 8 / ks;
+      k_lo = rank * TPX / ks;
+      k_hi = (rank + 1) * TPX / ks;
     }
     if (cb < cg_valid) {
       const int jl = jb0 + cb - p.jb_begin;  // block index within the output view
       float* obase = p.out + (int64_t)jl * p.out_blk;
       const float* sbase = p.skip ? p.skip + (int64_t)jl * p.sk_blk : nullptr;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < TPX; ++k) {
         if (k < k_lo || k >= k_hi) continue;
         const int q = pg + PG * k;
         const int ty = q / p.TW, tx = q - ty * p.TW;
@@ -555,7 +556,7 @@ void pick_tile(FfmaParams& p, int BM, int co_groups, int sms) {
 // units, or split-K whose 64 KB partial buffer shares smem with the ring),
 // NS ring depth, TMEM fold interval.  Returns the dynamic smem bytes, or 0 if
 // two stages do not fit.
-template <int BN, int NW>
+template <int BN, int NW, int TPX>
 size_t configure(FfmaParams& p, int ks, bool fine) {
   constexpr int CG = BN / 8;
   const int kWeightBudget = 40 * 1024, kPatchBudget = 32 * 1024;
@@ -591,7 +592,7 @@ size_t configure(FfmaParams& p, int ks, bool fine) {
   const int S = p.n_g * p.n_r;
   const int kSmemBudget = 220 * 1024;
   const int bar_bytes = (2 * kMaxStages + 2) * 8 + 16;
-  const int red_bytes = 8 * 8 * NW * 32 * 4;  // 64 floats / thread
+  const int red_bytes = TPX * 8 * NW * 32 * 4;  // TPX*8 floats / thread
   p.ksplit = ks;
   p.red_floats = ks > 1 ? red_bytes / 4 : 0;
   const int ring_budget = kSmemBudget - bar_bytes - (ks > 1 ? red_bytes : 0);
@@ -661,7 +662,7 @@ int launch_units(K kernel, int threads, FfmaParams p, size_t smem, int unit_begi
   return dconv_host::check_launch("conv_ffma_kernel");
 }
 
-template <int BM, int BN, int WF, int NW>
+template <int BM, int BN, int WF, int NW, int TPX>
 int launch_variant(FfmaParams p, cudaStream_t stream) {
   constexpr int threads = (NW + 4) * 32;
   constexpr int CG = BN / 8;
@@ -679,19 +680,19 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   const int units = p.tiles_y * p.tiles_x * co_groups;
   const bool fine = (int64_t)units * 2 < sms;  // batch-1 layers: split-K over fine stages
 
-  auto kernel = conv_ffma_kernel<BM, BN, WF, NW>;
+  auto kernel = conv_ffma_kernel<BM, BN, WF, NW, TPX>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = true;
   }
   FfmaParams q = p;
-  if (!configure<BN, NW>(q, 1, fine))
+  if (!configure<BN, NW, TPX>(q, 1, fine))
     return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_ffma: stage does not fit smem twice");
   const int S = q.n_g * q.n_r;
   // the 12-warp variant's partial buffer (96 KB) leaves no room for a ring:
   // it never splits K
-  const bool no_split = getenv("DCONV_NO_SPLITK") != nullptr || NW != 8;
+  const bool no_split = getenv("DCONV_NO_SPLITK") != nullptr || NW != 8 || TPX != 8;
 
   // (1) fewer units than SMs (batch 1): one split-K launch.  The persistent schedule
   // runs ceil(units / slots) rounds of ceil(S / ks) stages (+ a DSMEM
@@ -711,7 +712,7 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   if (const char* e = getenv("DCONV_KSPLIT")) best_ks = std::max(1, std::min(atoi(e), std::min(8, S)));
   if (best_ks > 1) {
     FfmaParams r = p;
-    const size_t smem = configure<BN, NW>(r, best_ks, true);
+    const size_t smem = configure<BN, NW, TPX>(r, best_ks, true);
     if (!smem) return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_ffma: split stage");
     const int clusters = std::min(units, std::max(1, cluster_slots(kernel, best_ks, sms, threads)));
     return launch_units(kernel, threads, r, smem, 0, units, clusters, stream);
@@ -726,7 +727,7 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
       !getenv("DCONV_NO_TAILSPLIT")) {
     for (int ks = 8; ks >= 2; ks /= 2) {
       FfmaParams t = p;
-      if (!configure<BN, NW>(t, ks, true)) continue;
+      if (!configure<BN, NW, TPX>(t, ks, true)) continue;
       if (ks > t.n_g * t.n_r) continue;
       const int slots = cluster_slots(kernel, ks, sms, threads);
       if (slots >= tail) {
@@ -735,7 +736,7 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
       }
     }
   }
-  const size_t smem_main = configure<BN, NW>(q, 1, fine);
+  const size_t smem_main = configure<BN, NW, TPX>(q, 1, fine);
   if (getenv("DCONV_DEBUG"))
     fprintf(stderr,
             "conv_ffma<%d,%d,%d>: %dx%d tiles TH=%d TW=%d units=%d S=%d G=%d R=%d NS=%d "
@@ -747,17 +748,17 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   int rc = launch_units(kernel, threads, q, smem_main, 0, main_units, sms, stream);
   if (rc) return rc;
   FfmaParams t = p;
-  const size_t smem_tail = configure<BN, NW>(t, tail_ks, true);
+  const size_t smem_tail = configure<BN, NW, TPX>(t, tail_ks, true);
   return launch_units(kernel, threads, t, smem_tail, main_units, tail, tail, stream);
 }
 
-template <int BM, int BN, int NW = 8>
+template <int BM, int BN, int NW = 8, int TPX = 8>
 int launch_wf(const FfmaParams& p, cudaStream_t stream) {
   switch (p.w_f) {
-    case 1: return launch_variant<BM, BN, 1, NW>(p, stream);
-    case 3: return launch_variant<BM, BN, 3, NW>(p, stream);
-    case 5: return launch_variant<BM, BN, 5, NW>(p, stream);
-    default: return launch_variant<BM, BN, 0, NW>(p, stream);
+    case 1: return launch_variant<BM, BN, 1, NW, TPX>(p, stream);
+    case 3: return launch_variant<BM, BN, 3, NW, TPX>(p, stream);
+    case 5: return launch_variant<BM, BN, 5, NW, TPX>(p, stream);
+    default: return launch_variant<BM, BN, 0, NW, TPX>(p, stream);
   }
 }
 
@@ -775,7 +776,9 @@ int launch_conv_ffma(const FfmaParams& p, cudaStream_t stream) {
     case 0: return launch_wf<128, 128>(p, stream);  // 128 px x 128 channels
     case 1: return launch_wf<256, 64>(p, stream);   // 256 px x 64 channels
     case 2: return launch_wf<192, 128, 12>(p, stream);  // 12 compute warps
-    default: return launch_wf<384, 64, 12>(p, stream);  // 12 compute warps
+    case 3: return launch_wf<384, 64, 12>(p, stream);   // 12 compute warps
+    case 4: return launch_wf<512, 64, 8, 16>(p, stream);  // 16 px x 8 ch / thread
+    default: return launch_wf<256, 128, 8, 16>(p, stream);  // 16 px x 8 ch / thread
   }
 }
 
