@@ -773,12 +773,12 @@ int launch_conv_ffma(const FfmaParams& p, cudaStream_t stream) {
   // (little reuse per staged pixel) prefer 128 px x 128 ch
   if (v < 0) v = (p.h_f * p.w_f == 1 && p.jb_count >= 16) ? 0 : 1;
   switch (v) {
+    // Measured on B200 and not instantiated (tools/variant_run.sh): 12
+    // compute warps with 2-channel activation loads (<192,128,12>,
+    // <384,64,12>) -6..-12%; 16 px x 8 ch per thread (<512,64,8,16>,
+    // <256,128,8,16>, spills at 229 registers) -13%.
     case 0: return launch_wf<128, 128>(p, stream);  // 128 px x 128 channels
-    case 1: return launch_wf<256, 64>(p, stream);   // 256 px x 64 channels
-    case 2: return launch_wf<192, 128, 12>(p, stream);  // 12 compute warps
-    case 3: return launch_wf<384, 64, 12>(p, stream);   // 12 compute warps
-    case 4: return launch_wf<512, 64, 8, 16>(p, stream);  // 16 px x 8 ch / thread
-    default: return launch_wf<256, 128, 8, 16>(p, stream);  // 16 px x 8 ch / thread
+    default: return launch_wf<256, 64>(p, stream);  // 256 px x 64 channels
   }
 }
 
