@@ -143,13 +143,23 @@ __device__ __forceinline__ void tile_row(const FfmaParams& p, const TileRows& t,
 
 // NW compute warps (8: 232 registers each; 12: 152 registers, 3 warps per
 // SMSP for latency hiding, activations loaded 2 channels at a time).
-template <int BM, int BN, int WF, int NW, int TPX>
+// Weight chunk of output block c inside a stage: TCO = 8 pads each chunk by
+// 16 B, TCO = 16 (a thread reads blocks 2t and 2t+1) skews every block pair by
+// 16 B -- either way the 8 lanes of a warp that read different blocks hit
+// distinct 16-byte bank groups.
+template <int TCO>
+__host__ __device__ __forceinline__ int wchunk(int c, int wstride) {
+  return TCO == 16 ? c * wstride + (c >> 1) * 4 : c * wstride;
+}
+
+template <int BM, int BN, int WF, int NW, int TPX, int TCO>
 __global__ void __launch_bounds__((NW + 4) * 32, 1)
     conv_ffma_kernel(const FfmaParams p) {
-  constexpr int TCO = 8;         // channels per thread (one output block)
+  // TCO: channels per thread (1 or 2 output blocks)
+  constexpr int NBLK = TCO / 8;
   constexpr int AV = NW == 8 ? 4 : 2;  // activation channels per LDS
-  // TMEM running totals: NW/4 warp slots x TPX*8 columns
-  constexpr int kTmemCols = (NW / 4) * TPX * 8 <= 128 ? 128 : ((NW / 4) * TPX * 8 <= 256 ? 256 : 512);
+  // TMEM running totals: NW/4 warp slots x TPX*TCO columns
+  constexpr int kTmemCols = (NW / 4) * TPX * TCO <= 128 ? 128 : ((NW / 4) * TPX * TCO <= 256 ? 256 : 512);
   constexpr int PG = BM / TPX;   // pixel groups (TPX pixels each)
   constexpr int CGT = BN / TCO;  // channel thread groups == output blocks
   constexpr int WPG = PG / 4;    // warps along pixels
@@ -267,7 +277,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
         for (int c = lane; c < cg_valid; c += 32) {
           const float* src = p.w + ((int64_t)(jb0 + c) * p.ib_n + ib0) * p.slab_floats +
                              (int64_t)n0 * p.w_f * kCB * kCB;
-          bulk_g2s(sw + c * p.wstride_floats, src, wbytes, &full[buf]);
+          bulk_g2s(sw + wchunk<TCO>(c, p.wstride_floats), src, wbytes, &full[buf]);
         }
       }
     }
@@ -282,7 +292,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
   }
   const int wr = warp % WPG, wc = warp / WPG;
   const int pg = wr * 4 + (lane & 3);
-  const int cb = wc * 8 + (lane >> 2);  // output block within the CTA tile
+  const int cb = (wc * 8 + (lane >> 2)) * NBLK;  // first output block within the CTA tile
 
   const uint32_t tmem_base = use_tmem ? *tmem_slot : 0u;
   const uint32_t taddr = tmem_base + ((uint32_t)((warp & 3) * 32) << 16) +
@@ -319,7 +329,8 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
       const int Ge = min(p.G, p.ib_n - g * p.G);
       const int Re = min(p.R, p.h_f - r * p.R);
       const float* sp = smem + buf * p.stage_floats;
-      const float* sw = sp + p.patch_floats + cb * p.wstride_floats;
+      const float* sw = sp + p.patch_floats + wchunk<TCO>(cb, p.wstride_floats);
+      const int sw2 = NBLK > 1 ? wchunk<TCO>(cb + 1, p.wstride_floats) - wchunk<TCO>(cb, p.wstride_floats) : 0;
       // per-pixel patch pointers once per stage; rows and taps then add a
       // warp-uniform offset (measured +1%; swapping the channel-half order
       // between warpgroups to de-phase their LDS bubbles measured -2.5%).
@@ -349,18 +360,21 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
               }
 #pragma unroll
               for (int i4 = 0; i4 < AV; ++i4) {
-                const float* pb = pw + (half * AV + i4) * kCB;
-                const float4 b0 = lds128(pb);
-                const float4 b1 = lds128(pb + 4);
-                uint64_t bp[4];
-                bp[0] = pack2(b0.x, b0.y);
-                bp[1] = pack2(b0.z, b0.w);
-                bp[2] = pack2(b1.x, b1.y);
-                bp[3] = pack2(b1.z, b1.w);
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
+                for (int bb = 0; bb < NBLK; ++bb) {
+                  const float* pb = pw + bb * sw2 + (half * AV + i4) * kCB;
+                  const float4 b0 = lds128(pb);
+                  const float4 b1 = lds128(pb + 4);
+                  uint64_t bp[4];
+                  bp[0] = pack2(b0.x, b0.y);
+                  bp[1] = pack2(b0.z, b0.w);
+                  bp[2] = pack2(b1.x, b1.y);
+                  bp[3] = pack2(b1.z, b1.w);
 #pragma unroll
-                  for (int k = 0; k < TPX; ++k) ffma2(acc[k][c], a[k][i4], bp[c]);
+                  for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int k = 0; k < TPX; ++k) ffma2(acc[k][bb * 4 + c], a[k][i4], bp[c]);
+                }
               }
             }
           }
@@ -387,7 +401,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
     // rank r sums pixels [r*8/ks, (r+1)*8/ks) of every thread's 8x8 tile over
     // ranks 0..ks-1 in that fixed order (deterministic, no global workspace).
     int k_lo = 0, k_hi = TPX;
-    if (ks > 1) {
+    if (TCO == 8 && ks > 1) {
       if (unit_iter > 0) mbar_wait_cluster(done, (unit_iter - 1) & 1);
 #pragma unroll
       for (int k = 0; k < TPX; ++k)
@@ -404,8 +418,10 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
       k_lo = rank * TPX / ks;
       k_hi = (rank + 1) * TPX / ks;
     }
-    if (cb < cg_valid) {
-      const int jl = jb0 + cb - p.jb_begin;  // block index within the output view
+#pragma unroll
+    for (int bb = 0; bb < NBLK; ++bb) {
+      if (cb + bb >= cg_valid) continue;
+      const int jl = jb0 + cb + bb - p.jb_begin;  // block index within the output view
       float* obase = p.out + (int64_t)jl * p.out_blk;
       const float* sbase = p.skip ? p.skip + (int64_t)jl * p.sk_blk : nullptr;
 #pragma unroll
@@ -415,18 +431,18 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
         const int ty = q / p.TW, tx = q - ty * p.TW;
         const int x = tx0 + tx;
         const bool valid = ty < tr.th && x < p.w_o;
-        float v[TCO];
-        if (ks > 1) {
+        float v[8];
+        if (TCO == 8 && ks > 1) {
 #pragma unroll
-          for (int c = 0; c < TCO; ++c) {
+          for (int c = 0; c < 8; ++c) {
             float sum = 0.f;
             for (int r = 0; r < ks; ++r) sum += ld_dsmem(&red[(k * 8 + c) * (NW * 32) + tid], r);
             v[c] = sum;
           }
         } else {
 #pragma unroll
-          for (int c = 0; c < TCO / 2; ++c) {
-            const float2 f = unpack2(acc[k][c]);
+          for (int c = 0; c < 4; ++c) {
+            const float2 f = unpack2(acc[k][bb * 4 + c]);
             v[2 * c] = f.x;
             v[2 * c + 1] = f.y;
           }
@@ -438,23 +454,23 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
           const float* sk = sbase + (int64_t)img * p.sk_img + (int64_t)y * p.sk_row +
                             (int64_t)x * kCB;
 #pragma unroll
-          for (int c = 0; c < TCO; c += 4) {
+          for (int c = 0; c < 8; c += 4) {
             const float4 s4 = *reinterpret_cast<const float4*>(sk + c);
             v[c] += s4.x; v[c + 1] += s4.y; v[c + 2] += s4.z; v[c + 3] += s4.w;
           }
         }
         if (p.epi & DCONV_EPI_RELU) {
 #pragma unroll
-          for (int c = 0; c < TCO; ++c) v[c] = fmaxf(v[c], 0.f);
+          for (int c = 0; c < 8; ++c) v[c] = fmaxf(v[c], 0.f);
         }
         float* o = obase + (int64_t)img * p.out_img + (int64_t)y * p.out_row +
                    (int64_t)x * kCB;
 #pragma unroll
-        for (int c = 0; c < TCO; c += 4)
+        for (int c = 0; c < 8; c += 4)
           *reinterpret_cast<float4*>(o + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
       }
     }
-    if (ks > 1) {
+    if (TCO == 8 && ks > 1) {
       __syncwarp();
       if (lane == 0)
         for (int q = 0; q < ks; ++q) mbar_arrive_remote(done, q);
@@ -556,7 +572,7 @@ void pick_tile(FfmaParams& p, int BM, int co_groups, int sms) {
 // units, or split-K whose 64 KB partial buffer shares smem with the ring),
 // NS ring depth, TMEM fold interval.  Returns the dynamic smem bytes, or 0 if
 // two stages do not fit.
-template <int BN, int NW, int TPX>
+template <int BN, int NW, int TPX, int TCO>
 size_t configure(FfmaParams& p, int ks, bool fine) {
   constexpr int CG = BN / 8;
   const int kWeightBudget = 40 * 1024, kPatchBudget = 32 * 1024;
@@ -587,12 +603,12 @@ size_t configure(FfmaParams& p, int ks, bool fine) {
   p.patch_floats = p.G * p.PH * p.PW * kCB;
   // +16 B per block chunk: the 8 lanes of a warp that read different output
   // blocks hit distinct 16-byte bank groups of the weight stage.
-  p.wstride_floats = p.G * p.R * p.w_f * kCB * kCB + 4;
-  p.stage_floats = (p.patch_floats + CG * p.wstride_floats + 31) & ~31;  // 128 B aligned
+  p.wstride_floats = p.G * p.R * p.w_f * kCB * kCB + (TCO == 8 ? 4 : 0);
+  p.stage_floats = (p.patch_floats + wchunk<TCO>(CG, p.wstride_floats) + 31) & ~31;  // 128 B aligned
   const int S = p.n_g * p.n_r;
   const int kSmemBudget = 220 * 1024;
   const int bar_bytes = (2 * kMaxStages + 2) * 8 + 16;
-  const int red_bytes = TPX * 8 * NW * 32 * 4;  // TPX*8 floats / thread
+  const int red_bytes = TPX * TCO * NW * 32 * 4;  // TPX*TCO floats / thread
   p.ksplit = ks;
   p.red_floats = ks > 1 ? red_bytes / 4 : 0;
   const int ring_budget = kSmemBudget - bar_bytes - (ks > 1 ? red_bytes : 0);
@@ -662,7 +678,7 @@ int launch_units(K kernel, int threads, FfmaParams p, size_t smem, int unit_begi
   return dconv_host::check_launch("conv_ffma_kernel");
 }
 
-template <int BM, int BN, int WF, int NW, int TPX>
+template <int BM, int BN, int WF, int NW, int TPX, int TCO>
 int launch_variant(FfmaParams p, cudaStream_t stream) {
   constexpr int threads = (NW + 4) * 32;
   constexpr int CG = BN / 8;
@@ -680,19 +696,19 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   const int units = p.tiles_y * p.tiles_x * co_groups;
   const bool fine = (int64_t)units * 2 < sms;  // batch-1 layers: split-K over fine stages
 
-  auto kernel = conv_ffma_kernel<BM, BN, WF, NW, TPX>;
+  auto kernel = conv_ffma_kernel<BM, BN, WF, NW, TPX, TCO>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = true;
   }
   FfmaParams q = p;
-  if (!configure<BN, NW, TPX>(q, 1, fine))
+  if (!configure<BN, NW, TPX, TCO>(q, 1, fine))
     return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_ffma: stage does not fit smem twice");
   const int S = q.n_g * q.n_r;
   // the 12-warp variant's partial buffer (96 KB) leaves no room for a ring:
   // it never splits K
-  const bool no_split = getenv("DCONV_NO_SPLITK") != nullptr || NW != 8 || TPX != 8;
+  const bool no_split = getenv("DCONV_NO_SPLITK") != nullptr || NW != 8 || TPX != 8 || TCO != 8;
 
   // (1) fewer units than SMs (batch 1): one split-K launch.  The persistent schedule
   // runs ceil(units / slots) rounds of ceil(S / ks) stages (+ a DSMEM
@@ -712,7 +728,7 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   if (const char* e = getenv("DCONV_KSPLIT")) best_ks = std::max(1, std::min(atoi(e), std::min(8, S)));
   if (best_ks > 1) {
     FfmaParams r = p;
-    const size_t smem = configure<BN, NW, TPX>(r, best_ks, true);
+    const size_t smem = configure<BN, NW, TPX, TCO>(r, best_ks, true);
     if (!smem) return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_ffma: split stage");
     const int clusters = std::min(units, std::max(1, cluster_slots(kernel, best_ks, sms, threads)));
     return launch_units(kernel, threads, r, smem, 0, units, clusters, stream);
@@ -727,7 +743,7 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
       !getenv("DCONV_NO_TAILSPLIT")) {
     for (int ks = 8; ks >= 2; ks /= 2) {
       FfmaParams t = p;
-      if (!configure<BN, NW, TPX>(t, ks, true)) continue;
+      if (!configure<BN, NW, TPX, TCO>(t, ks, true)) continue;
       if (ks > t.n_g * t.n_r) continue;
       const int slots = cluster_slots(kernel, ks, sms, threads);
       if (slots >= tail) {
@@ -736,7 +752,7 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
       }
     }
   }
-  const size_t smem_main = configure<BN, NW, TPX>(q, 1, fine);
+  const size_t smem_main = configure<BN, NW, TPX, TCO>(q, 1, fine);
   if (getenv("DCONV_DEBUG"))
     fprintf(stderr,
             "conv_ffma<%d,%d,%d>: %dx%d tiles TH=%d TW=%d units=%d S=%d G=%d R=%d NS=%d "
@@ -748,17 +764,17 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   int rc = launch_units(kernel, threads, q, smem_main, 0, main_units, sms, stream);
   if (rc) return rc;
   FfmaParams t = p;
-  const size_t smem_tail = configure<BN, NW, TPX>(t, tail_ks, true);
+  const size_t smem_tail = configure<BN, NW, TPX, TCO>(t, tail_ks, true);
   return launch_units(kernel, threads, t, smem_tail, main_units, tail, tail, stream);
 }
 
-template <int BM, int BN, int NW = 8, int TPX = 8>
+template <int BM, int BN, int NW = 8, int TPX = 8, int TCO = 8>
 int launch_wf(const FfmaParams& p, cudaStream_t stream) {
   switch (p.w_f) {
-    case 1: return launch_variant<BM, BN, 1, NW, TPX>(p, stream);
-    case 3: return launch_variant<BM, BN, 3, NW, TPX>(p, stream);
-    case 5: return launch_variant<BM, BN, 5, NW, TPX>(p, stream);
-    default: return launch_variant<BM, BN, 0, NW, TPX>(p, stream);
+    case 1: return launch_variant<BM, BN, 1, NW, TPX, TCO>(p, stream);
+    case 3: return launch_variant<BM, BN, 3, NW, TPX, TCO>(p, stream);
+    case 5: return launch_variant<BM, BN, 5, NW, TPX, TCO>(p, stream);
+    default: return launch_variant<BM, BN, 0, NW, TPX, TCO>(p, stream);
   }
 }
 
@@ -776,7 +792,10 @@ int launch_conv_ffma(const FfmaParams& p, cudaStream_t stream) {
     // Measured on B200 and not instantiated (tools/variant_run.sh): 12
     // compute warps with 2-channel activation loads (<192,128,12>,
     // <384,64,12>) -6..-12%; 16 px x 8 ch per thread (<512,64,8,16>,
-    // <256,128,8,16>, spills at 229 registers) -13%.
+    // <256,128,8,16>, spills at 229 registers) -13%; 8 px x 16 ch per thread
+    // (<256,128,8,8,16>, 25% fewer LDS per FFMA2) +-0% at 128 ch, -6% at
+    // 256/512 ch.  tools/ffma2_pattern.cu: this operand pattern tops out at
+    // ~59 TFLOP/s with any warp count (83% of the FFMA2 probe).
     case 0: return launch_wf<128, 128>(p, stream);  // 128 px x 128 channels
     default: return launch_wf<256, 64>(p, stream);  // 256 px x 64 channels
   }
