@@ -517,8 +517,11 @@ int max_patch_rows(const FfmaParams& p, int R) {
 // halves/thirds), TH = BM / TW rows of the stacked batch.  Score = useful
 // pixels / launched pixel-slots, where the launch takes floor(units/sms)
 // full waves plus a ragged tail that the tail-split launch finishes in about
-// 1/2, 1/4 or 1/8 of a wave when it fits on sms/2, /4, /8 clusters.  Ties go
-// to the smaller patch.
+// 1/2, 1/4 or 1/8 of a wave when it fits on sms/2, /4, /8 clusters -- divided
+// by how far the producer's bulk copies (one per patch row and input block,
+// ~kCopyCycles each, measured) outrun the unit's FFMA2 time: narrow tiles of
+// 1x1 layers are copy-bound (TW = 4 on a 56-wide map ran at 16 TFLOP/s).
+// Ties go to the smaller patch.
 double tail_rounds(int64_t units, int sms) {
   const int64_t full = units / sms, tail = units - full * sms;
   double t = 0.0;
@@ -538,7 +541,10 @@ double tail_rounds(int64_t units, int sms) {
   return (double)full + t;
 }
 
-void pick_tile(FfmaParams& p, int BM, int co_groups, int sms) {
+constexpr double kCopyCycles = 50.0;   // per bulk copy (row of one input block)
+constexpr double kFfmaPerCycle = 102.0;  // FMA / cycle / SM sustained (80% of 128)
+
+void pick_tile(FfmaParams& p, int BM, int BN, int co_groups, int sms) {
   int cand[16], nc = 0;
   for (int tw = 4; tw <= 128 && tw <= BM; tw *= 2) cand[nc++] = tw;
   for (int d = 1; d <= 4; ++d) {
@@ -548,12 +554,20 @@ void pick_tile(FfmaParams& p, int BM, int co_groups, int sms) {
   double best_score = -1;
   int64_t best_patch = 0;
   const int64_t vh = (int64_t)p.n * p.h_o;
+  FfmaParams q = p;
   for (int i = 0; i < nc; ++i) {
     const int tw = cand[i], th = BM / tw;
     const int64_t ty = (vh + th - 1) / th, tx = (p.w_o + tw - 1) / tw;
     const int64_t units = ty * tx * co_groups;
     const double slots_used = tail_rounds(units, sms) * sms;
-    const double score = (double)vh * p.w_o * co_groups / (slots_used * BM);
+    q.TH = th;
+    q.TW = tw;
+    const double rows = max_patch_rows(q, p.h_f);
+    // producer copies per input block vs FFMA2 cycles per input block
+    const double copy_ratio = kCopyCycles * rows /
+                              ((double)BM * BN * kCB * p.h_f * p.w_f / kFfmaPerCycle);
+    const double score = (double)vh * p.w_o * co_groups / (slots_used * BM) /
+                         std::max(1.0, copy_ratio);
     const int64_t patch = (int64_t)((std::min<int64_t>(th, vh) - 1) * p.s + p.h_f) *
                           ((std::min(tw, p.w_o) - 1) * p.s + p.w_f);
     if (score > best_score + 1e-6 || (score > best_score - 1e-6 && patch < best_patch)) {
@@ -613,7 +627,8 @@ size_t configure(FfmaParams& p, int ks, bool fine) {
   p.red_floats = ks > 1 ? red_bytes / 4 : 0;
   const int ring_budget = kSmemBudget - bar_bytes - (ks > 1 ? red_bytes : 0);
   p.NS = std::min(kMaxStages, ring_budget / (p.stage_floats * 4));
-  p.NS = std::min(p.NS, std::max(2, (S + ks - 1) / ks));
+  // the ring spans unit boundaries (the producer prefetches the next unit), so
+  // its depth is set by shared memory alone, not by the stages per unit
   // partial sums cover >= 256 products before folding into the TMEM total
   const int k_stage = p.G * p.R * p.w_f * kCB;
   p.flush_every = std::max(1, (256 + k_stage - 1) / k_stage);
@@ -689,7 +704,7 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int co_groups = (p.jb_count + CG - 1) / CG;
-  pick_tile(p, BM, co_groups, sms);
+  pick_tile(p, BM, BN, co_groups, sms);
   p.TWe = std::min(p.TW, p.w_o);
   p.PW = (p.TWe - 1) * p.s + p.w_f;
   p.slab_floats = p.h_f * p.w_f * kCB * kCB;
