@@ -100,6 +100,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src,
       : "memory");
 }
 
+// Warm L2 with [src, src + bytes) (bytes a multiple of 16); no completion.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // fp32 pair helpers: acc.{lo,hi} += a * b.{lo,hi} as one FFMA2 (RN per lane,
 // bitwise identical to two fmaf).  ptxas folds the {a, a} pair into the
 // FFMA2 scalar-broadcast operand form, so no MOV is emitted.

@@ -115,10 +115,15 @@ struct TileRows {
   int vy0, img0, y0, cnt0, th;  // th: valid virtual rows of this tile
 };
 
+// v / h_o for 0 <= v < n * h_o (multiply-high by a host-computed reciprocal)
+__device__ __forceinline__ int div_ho(const FfmaParams& p, int v) {
+  return p.h_o_magic ? (int)__umulhi((unsigned)v, p.h_o_magic) : v / p.h_o;
+}
+
 __device__ __forceinline__ TileRows tile_rows(const FfmaParams& p, int tile_y) {
   TileRows t;
   t.vy0 = tile_y * p.TH;
-  t.img0 = t.vy0 / p.h_o;
+  t.img0 = div_ho(p, t.vy0);
   t.y0 = t.vy0 - t.img0 * p.h_o;
   t.th = min(p.TH, p.n * p.h_o - t.vy0);
   t.cnt0 = min(p.h_o - t.y0, t.th);
@@ -134,7 +139,7 @@ __device__ __forceinline__ void tile_row(const FfmaParams& p, const TileRows& t,
     prow = ty * p.s;
   } else {
     const int d = ty - t.cnt0;
-    const int j = d / p.h_o;  // full segments before this one (segment j+1)
+    const int j = div_ho(p, d);  // full segments before this one (segment j+1)
     y = d - j * p.h_o;
     img = t.img0 + 1 + j;
     prow = (t.cnt0 - 1) * p.s + p.R + j * ((p.h_o - 1) * p.s + p.R) + y * p.s;
@@ -238,6 +243,20 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
       const int col0 = tx0 * p.s;
       const int cols = min(p.PW, p.w_i - col0);
       const int n_seg = 1 + (tr.th - tr.cnt0 + p.h_o - 1) / p.h_o;
+      if ((p.epi & DCONV_EPI_ADD) && rank == 0 && p.skip_prefetch) {
+        // the epilogue reads this unit's skip tile once: pull it into L2 now,
+        // a unit ahead of the read, so the ADD epilogue does not wait on HBM
+        const uint32_t row_bytes = (uint32_t)(min(p.TW, p.w_o - tx0) * kCB * 4);
+        for (int t = lane; t < cg_valid * tr.th; t += 32) {
+          const int c = t / tr.th, ty = t - c * tr.th;
+          int img, y, prow;
+          tile_row(p, tr, ty, img, y, prow);
+          bulk_prefetch_l2(p.skip + (int64_t)(jb0 + c - p.jb_begin) * p.sk_blk +
+                               (int64_t)img * p.sk_img + (int64_t)y * p.sk_row +
+                               (int64_t)tx0 * kCB,
+                           row_bytes);
+        }
+      }
       for (int st = st0; st < st1; ++st, ++gs) {
         const int buf = gs % p.NS;
         if (gs >= p.NS) mbar_wait(&empty[buf], ((gs / p.NS) - 1) & 1);
@@ -310,7 +329,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
 #pragma unroll
     for (int k = 0; k < TPX; ++k) {
       const int q = pg + PG * k;
-      const int ty = q / p.TW, tx = q - ty * p.TW;
+      const int ty = (int)__umulhi((unsigned)q, p.tw_magic), tx = q - ty * p.TW;
       int img, y, prow;
       tile_row(p, tr, ty, img, y, prow);
       poff[k] = (ty < tr.th && tx0 + tx < p.w_o) ? (prow * p.PW + tx * p.s) * kCB : 0;
@@ -337,46 +356,54 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
       const float* pk[TPX];
 #pragma unroll
       for (int k = 0; k < TPX; ++k) pk[k] = sp + poff[k];
-      for (int gi = 0; gi < Ge; ++gi) {
-        for (int n = 0; n < Re; ++n) {
-          const int row_off = ((gi * p.PH + n) * p.PW) * kCB;
-          const float* pw_row = sw + ((gi * p.R + n) * wf) * (kCB * kCB);
-#pragma unroll(WF > 0 ? WF : 1)
-          for (int m = 0; m < wf; ++m) {
-            const float* pw = pw_row + m * (kCB * kCB);
+      // one filter tap of one input block: 8 channels x (8 px x TCO ch)
+      auto tap = [&](const float* pw, int aoff) {
 #pragma unroll
-            for (int h = 0; h < 8 / AV; ++h) {
-              const int half = h;
-              float a[TPX][AV];
+        for (int half = 0; half < 8 / AV; ++half) {
+          float a[TPX][AV];
 #pragma unroll
-              for (int k = 0; k < TPX; ++k) {
-                if constexpr (AV == 4) {
-                  const float4 t = lds128(pk[k] + row_off + m * kCB + half * 4);
-                  a[k][0] = t.x; a[k][1] = t.y; a[k][2] = t.z; a[k][3] = t.w;
-                } else {
-                  const float2 t = *reinterpret_cast<const float2*>(pk[k] + row_off + m * kCB + half * 2);
-                  a[k][0] = t.x; a[k][1] = t.y;
-                }
-              }
-#pragma unroll
-              for (int i4 = 0; i4 < AV; ++i4) {
-#pragma unroll
-                for (int bb = 0; bb < NBLK; ++bb) {
-                  const float* pb = pw + bb * sw2 + (half * AV + i4) * kCB;
-                  const float4 b0 = lds128(pb);
-                  const float4 b1 = lds128(pb + 4);
-                  uint64_t bp[4];
-                  bp[0] = pack2(b0.x, b0.y);
-                  bp[1] = pack2(b0.z, b0.w);
-                  bp[2] = pack2(b1.x, b1.y);
-                  bp[3] = pack2(b1.z, b1.w);
-#pragma unroll
-                  for (int c = 0; c < 4; ++c)
-#pragma unroll
-                    for (int k = 0; k < TPX; ++k) ffma2(acc[k][bb * 4 + c], a[k][i4], bp[c]);
-                }
-              }
+          for (int k = 0; k < TPX; ++k) {
+            if constexpr (AV == 4) {
+              const float4 t = lds128(pk[k] + aoff + half * 4);
+              a[k][0] = t.x; a[k][1] = t.y; a[k][2] = t.z; a[k][3] = t.w;
+            } else {
+              const float2 t = *reinterpret_cast<const float2*>(pk[k] + aoff + half * 2);
+              a[k][0] = t.x; a[k][1] = t.y;
             }
+          }
+#pragma unroll
+          for (int i4 = 0; i4 < AV; ++i4) {
+#pragma unroll
+            for (int bb = 0; bb < NBLK; ++bb) {
+              const float* pb = pw + bb * sw2 + (half * AV + i4) * kCB;
+              const float4 b0 = lds128(pb);
+              const float4 b1 = lds128(pb + 4);
+              uint64_t bp[4];
+              bp[0] = pack2(b0.x, b0.y);
+              bp[1] = pack2(b0.z, b0.w);
+              bp[2] = pack2(b1.x, b1.y);
+              bp[3] = pack2(b1.z, b1.w);
+#pragma unroll
+              for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int k = 0; k < TPX; ++k) ffma2(acc[k][bb * 4 + c], a[k][i4], bp[c]);
+            }
+          }
+        }
+      };
+      if (WF == 1 && Re == 1) {
+        // 1x1 filters: a stage is Ge input blocks of one tap each; unrolled
+        // so the accumulators stay put across blocks (no register rotation)
+        const int gstride = p.PH * p.PW * kCB, wgstride = p.R * kCB * kCB;
+#pragma unroll 4
+        for (int gi = 0; gi < Ge; ++gi) tap(sw + gi * wgstride, gi * gstride);
+      } else {
+        for (int gi = 0; gi < Ge; ++gi) {
+          for (int n = 0; n < Re; ++n) {
+            const int row_off = ((gi * p.PH + n) * p.PW) * kCB;
+            const float* pw_row = sw + ((gi * p.R + n) * wf) * (kCB * kCB);
+#pragma unroll(WF > 0 ? WF : 1)
+            for (int m = 0; m < wf; ++m) tap(pw_row + m * (kCB * kCB), row_off + m * kCB);
           }
         }
       }
@@ -428,7 +455,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
       for (int k = 0; k < TPX; ++k) {
         if (k < k_lo || k >= k_hi) continue;
         const int q = pg + PG * k;
-        const int ty = q / p.TW, tx = q - ty * p.TW;
+        const int ty = (int)__umulhi((unsigned)q, p.tw_magic), tx = q - ty * p.TW;
         const int x = tx0 + tx;
         const bool valid = ty < tr.th && x < p.w_o;
         float v[8];
@@ -706,6 +733,8 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   const int co_groups = (p.jb_count + CG - 1) / CG;
   pick_tile(p, BM, BN, co_groups, sms);
   p.TWe = std::min(p.TW, p.w_o);
+  // q / TW for q < BM by multiply-high (exact: BM * TW < 2^32)
+  p.tw_magic = (unsigned)(((uint64_t(1) << 32) + p.TW - 1) / p.TW);
   p.PW = (p.TWe - 1) * p.s + p.w_f;
   p.slab_floats = p.h_f * p.w_f * kCB * kCB;
   const int units = p.tiles_y * p.tiles_x * co_groups;
@@ -797,7 +826,13 @@ int launch_wf(const FfmaParams& p, cudaStream_t stream) {
 
 int ffma_variant_override = -1;  // test/tuning hook (dconv_cuda_set_ffma_variant)
 
-int launch_conv_ffma(const FfmaParams& p, cudaStream_t stream) {
+int launch_conv_ffma(const FfmaParams& p0, cudaStream_t stream) {
+  FfmaParams p = p0;
+  p.h_o_magic = (int64_t)p.n * p.h_o * p.h_o < (int64_t(1) << 32)
+                    ? (unsigned)(((uint64_t(1) << 32) + p.h_o - 1) / p.h_o)
+                    : 0u;
+  static const bool no_skip_prefetch = getenv("DCONV_NO_SKIP_PREFETCH") != nullptr;
+  p.skip_prefetch = (p.epi & DCONV_EPI_ADD) && !no_skip_prefetch;
   int v = p.variant >= 0 ? p.variant : ffma_variant_override;
   // measured (tools/sweep_variants.py): 256 px x 64 ch wins on every 3x3 /
   // 5x5 layer of the configs; 1x1 layers with >= 128 output channels

@@ -30,6 +30,9 @@ struct FfmaParams {
   int red_floats;           // smem floats of the split-K partial buffer
   int unit_begin, unit_count;  // work units of this launch
   int variant;                 // requested CTA tile (-1 = selector)
+  int skip_prefetch;           // ADD epilogue: L2-prefetch the skip tile a unit ahead
+  unsigned tw_magic;           // ceil(2^32 / TW)
+  unsigned h_o_magic;          // ceil(2^32 / h_o) when n * h_o^2 < 2^32, else 0
 };
 
 extern int ffma_variant_override;  // -1 = heuristic (dconv_cuda_set_ffma_variant)
