@@ -136,13 +136,13 @@ __device__ __forceinline__ void tile_row(const FfmaParams& p, const TileRows& t,
   if (ty < t.cnt0) {
     img = t.img0;
     y = t.y0 + ty;
-    prow = ty * p.s;
+    prow = ty * p.sy;
   } else {
     const int d = ty - t.cnt0;
     const int j = div_ho(p, d);  // full segments before this one (segment j+1)
     y = d - j * p.h_o;
     img = t.img0 + 1 + j;
-    prow = (t.cnt0 - 1) * p.s + p.R + j * ((p.h_o - 1) * p.s + p.R) + y * p.s;
+    prow = (t.cnt0 - 1) * p.sy + p.R + j * ((p.h_o - 1) * p.sy + p.R) + y * p.sy;
   }
 }
 
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
     if (warp != NW) return;
     int gs = 0;
-    const int seg_rows_full = (p.h_o - 1) * p.s;  // + Re per full segment
+    const int seg_rows_full = (p.h_o - 1) * p.sy;  // + Re per full segment
     for (int u = cluster_id; u < n_units; u += n_clusters) {
       TileRows tr;
       int tx0, jb0, cg_valid;
@@ -264,11 +264,11 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
         const int ib0 = g * p.G, Ge = min(p.G, p.ib_n - ib0);
         const int n0 = r * p.R, Re = min(p.R, p.h_f - n0);
         // rows of each segment this stage: (cnt-1)*s + Re
-        const int rows_first = (tr.cnt0 - 1) * p.s + Re;
+        const int rows_first = (tr.cnt0 - 1) * p.sy + Re;
         const int rest = tr.th - tr.cnt0;  // rows in later segments
         const int n_full = rest / p.h_o, last_cnt = rest - n_full * p.h_o;
         const int total_rows = rows_first + n_full * (seg_rows_full + Re) +
-                               (last_cnt ? (last_cnt - 1) * p.s + Re : 0);
+                               (last_cnt ? (last_cnt - 1) * p.sy + Re : 0);
         const uint32_t patch_bytes = (uint32_t)(Ge * total_rows * cols * kCB * 4);
         const uint32_t wbytes = (uint32_t)(Re * p.w_f * kCB * kCB * 4) * Ge;
         float* sp = smem + buf * p.stage_floats;
@@ -281,11 +281,11 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
             img = tr.img0; y_start = tr.y0; rows = rows_first; prow0 = 0;
           } else {
             const int cnt = min(p.h_o, rest - (j - 1) * p.h_o);
-            img = tr.img0 + j; y_start = 0; rows = (cnt - 1) * p.s + Re;
-            prow0 = (tr.cnt0 - 1) * p.s + p.R + (j - 1) * (seg_rows_full + p.R);
+            img = tr.img0 + j; y_start = 0; rows = (cnt - 1) * p.sy + Re;
+            prow0 = (tr.cnt0 - 1) * p.sy + p.R + (j - 1) * (seg_rows_full + p.R);
           }
           const float* src0 = p.in + (int64_t)img * p.in_img +
-                              (int64_t)(y_start * p.s + n0) * p.in_row + (int64_t)col0 * kCB;
+                              (int64_t)(y_start * p.sy + n0) * p.in_row + (int64_t)col0 * kCB;
           for (int t = lane; t < Ge * rows; t += 32) {
             const int gi = t / rows, pr = t - gi * rows;
             const float* src = src0 + (int64_t)(ib0 + gi) * p.in_blk + (int64_t)pr * p.in_row;
@@ -536,7 +536,7 @@ int max_patch_rows(const FfmaParams& p, int R) {
   int best = 0;
   const int vh = p.n * p.h_o;
   for (int vy0 = 0, seen = 0; vy0 < vh && seen <= p.h_o; vy0 += p.TH, ++seen)
-    best = std::max(best, patch_rows(vy0 % p.h_o, std::min(p.TH, vh - vy0), p.h_o, p.s, R));
+    best = std::max(best, patch_rows(vy0 % p.h_o, std::min(p.TH, vh - vy0), p.h_o, p.sy, R));
   return best;
 }
 
@@ -595,7 +595,7 @@ void pick_tile(FfmaParams& p, int BM, int BN, int co_groups, int sms) {
                               ((double)BM * BN * kCB * p.h_f * p.w_f / kFfmaPerCycle);
     const double score = (double)vh * p.w_o * co_groups / (slots_used * BM) /
                          std::max(1.0, copy_ratio);
-    const int64_t patch = (int64_t)((std::min<int64_t>(th, vh) - 1) * p.s + p.h_f) *
+    const int64_t patch = (int64_t)((std::min<int64_t>(th, vh) - 1) * p.sy + p.h_f) *
                           ((std::min(tw, p.w_o) - 1) * p.s + p.w_f);
     if (score > best_score + 1e-6 || (score > best_score - 1e-6 && patch < best_patch)) {
       best_score = score;
@@ -828,6 +828,15 @@ int ffma_variant_override = -1;  // test/tuning hook (dconv_cuda_set_ffma_varian
 
 int launch_conv_ffma(const FfmaParams& p0, cudaStream_t stream) {
   FfmaParams p = p0;
+  // 1x1 stride-s layers read only every s-th input row: view the input with
+  // an s-times row pitch so the patch stages just those rows (column
+  // stride stays s)
+  p.sy = p.s;
+  if (p.h_f == 1 && p.s > 1) {
+    p.in_row *= p.s;
+    p.h_i = p.h_o;
+    p.sy = 1;
+  }
   p.h_o_magic = (int64_t)p.n * p.h_o * p.h_o < (int64_t(1) << 32)
                     ? (unsigned)(((uint64_t(1) << 32) + p.h_o - 1) / p.h_o)
                     : 0u;

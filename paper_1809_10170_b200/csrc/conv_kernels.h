@@ -31,6 +31,7 @@ struct FfmaParams {
   int unit_begin, unit_count;  // work units of this launch
   int variant;                 // requested CTA tile (-1 = selector)
   int skip_prefetch;           // ADD epilogue: L2-prefetch the skip tile a unit ahead
+  int sy;                      // row stride of the staged patch (s, or 1 for 1x1 re-viewed)
   unsigned tw_magic;           // ceil(2^32 / TW)
   unsigned h_o_magic;          // ceil(2^32 / h_o) when n * h_o^2 < 2^32, else 0
 };
