@@ -785,7 +785,8 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   int tail_ks = 1;
   if (main_units > 0 && tail > 0 && tail * 4 < sms * 3 && !no_split &&
       !getenv("DCONV_NO_TAILSPLIT")) {
-    for (int ks = 8; ks >= 2; ks /= 2) {
+    static const bool pow2_only = getenv("DCONV_TAIL_POW2") != nullptr;
+    for (int ks = 8; ks >= 2; ks = pow2_only ? ks / 2 : ks - 1) {
       FfmaParams t = p;
       if (!configure<BN, NW, TPX, TCO>(t, ks, true)) continue;
       if (ks > t.n_g * t.n_r) continue;
@@ -797,6 +798,9 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
     }
   }
   const size_t smem_main = configure<BN, NW, TPX, TCO>(q, 1, fine);
+  if (getenv("DCONV_DEBUG") && tail_ks > 1)
+    for (int ks = 2; ks <= 8; ++ks)
+      fprintf(stderr, "  cluster_slots(%d) = %d\n", ks, cluster_slots(kernel, ks, sms, threads));
   if (getenv("DCONV_DEBUG"))
     fprintf(stderr,
             "conv_ffma<%d,%d,%d>: %dx%d tiles TH=%d TW=%d units=%d S=%d G=%d R=%d NS=%d "

@@ -456,7 +456,7 @@ def test_co_shard_plan_world1_matches_unsharded():
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("ks", [2, 4, 8])
+@pytest.mark.parametrize("ks", [2, 3, 4, 6, 8])
 def test_cluster_split_k(ks, monkeypatch):
     """Split-K over a thread-block cluster with the DSMEM reduction, forced
     to ks CTAs per unit: several units per cluster (barrier phases), ragged
