@@ -32,6 +32,9 @@
  *   dconv_cuda_maxpool2x2_blocked <- subsampling, PAPER.md:9-10 (no reference code)
  *   dconv_conv_shape            <- ConvShape::ConvShape shape.cpp:30-40
  *   dconv_conv_flops            <- conv_flops         reference.cpp:106-109
+ *   dconv_file_*                <- tensor file format (serialize.cpp
+ *                                  is absent from the snapshot) and the CLI's
+ *                                  `pack` subcommand
  */
 #ifndef DCONV_CUDA_H
 #define DCONV_CUDA_H
@@ -52,7 +55,10 @@ enum {
   DCONV_EPARAM = 3,        /* bad parameter (null pointer, bad epilogue...) */
   DCONV_ECUDA = 4,         /* a CUDA runtime call failed */
   DCONV_ENCCL = 5,         /* reserved for the multi-GPU layer */
-  DCONV_EUNSUPPORTED = 6   /* no kernel for this configuration */
+  DCONV_EUNSUPPORTED = 6,  /* no kernel for this configuration */
+  DCONV_EFORMAT = 7,       /* malformed tensor file (parse error) */
+  DCONV_EBLOCKED = 8,      /* "already blocked": packing a packed file */
+  DCONV_EIO = 9            /* file open / read / write failed */
 };
 
 /* Fused epilogue applied to the fp32 accumulator before the single store. */
@@ -187,6 +193,36 @@ int64_t dconv_cuda_launch_count(void);
 /* Peak FP32 FFMA throughput probe (TFLOP/s) measured with CUDA events on the
  * current device: the roofline denominator for the FFMA kernel. */
 double dconv_cuda_fp32_peak_probe(void* stream);
+
+/* ---- Tensor files --------------------------------
+ * Flat little-endian file: 7 int32 header words, then the fp32 payload.
+ *   feature map: {C,   H,   W,   c_b  (0 = dense CHW),  0,   0,    0}
+ *   kernel:      {C_i, H_f, W_f, c_ob (0 = dense),      C_o, c_ib, 1}
+ * Payload: dense CHW / [C_i][C_o][H_f][W_f], or the blocked layout with its
+ * zero-padded channel slots.  (serialize.cpp is absent from the reference
+ * snapshot; this is the header the SPEC describes, word order fixed here.) */
+typedef struct dconv_file_header {
+  int32_t c, h, w, c_b, c_o, c_ib, kind;
+} dconv_file_header;
+enum { DCONV_FILE_FEATURE_MAP = 0, DCONV_FILE_KERNEL = 1 };
+
+/* Payload length in floats implied by a header (-1 if the header is invalid). */
+int64_t dconv_file_payload_floats(const dconv_file_header* h);
+/* Host-side I/O.  read_header validates the header and the file length. */
+int dconv_file_read_header(const char* path, dconv_file_header* h);
+int dconv_file_read_payload(const char* path, float* host_dst, int64_t floats);
+int dconv_file_write(const char* path, const dconv_file_header* h,
+                     const float* host_src, int64_t floats);
+/* The CLI `pack` step: dense kernel file -> blocked kernel file, repacked on
+ * the GPU (dconv_cuda_pack_kernel).  DCONV_EBLOCKED if the input is already
+ * blocked. */
+int dconv_pack_kernel_file(const char* in_path, int c_ob, int c_ib,
+                           const char* out_path);
+/* Weight ingest: a kernel file (dense or already blocked with the same
+ * c_ob/c_ib) into device memory in the blocked layout `d_dst`
+ * (dconv_cuda_pack_kernel's size).  Dense files are repacked on the GPU. */
+int dconv_cuda_load_kernel_file(const char* path, int c_ob, int c_ib,
+                                float* d_dst, void* stream);
 
 const char* dconv_cuda_strerror(int code);
 const char* dconv_cuda_last_error_detail(void);

@@ -15,7 +15,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DCONV_LIB") or os.path.join(_HERE, "libdconv_b200.so")  # override: A/B builds
 
 # error codes (dconv_cuda.h)
-OK, EINVAL_SHAPE, ELAYOUT, EPARAM, ECUDA, ENCCL, EUNSUPPORTED = range(7)
+OK, EINVAL_SHAPE, ELAYOUT, EPARAM, ECUDA, ENCCL, EUNSUPPORTED, EFORMAT, EBLOCKED, EIO = range(10)
+FILE_FEATURE_MAP, FILE_KERNEL = 0, 1
 EPI_NONE, EPI_RELU, EPI_ADD, EPI_ADD_RELU = range(4)
 ALGO_AUTO, ALGO_FFMA, ALGO_GENERIC, ALGO_TF32 = range(4)
 
@@ -32,6 +33,12 @@ class ConvDesc(ctypes.Structure):
         ("epilogue", ctypes.c_int), ("algo", ctypes.c_int),
         ("co_block_begin", ctypes.c_int), ("co_block_count", ctypes.c_int),
         ("tile_variant", ctypes.c_int)]
+
+
+class FileHeader(ctypes.Structure):
+    """Mirror of ``dconv_file_header`` (7 int32 words)."""
+
+    _fields_ = [(n, ctypes.c_int32) for n in ("c", "h", "w", "c_b", "c_o", "c_ib", "kind")]
 
 
 class DconvError(RuntimeError):
@@ -65,6 +72,12 @@ _SIGS = {
     "dconv_cuda_set_ffma_variant": (_I, [_I]),
     "dconv_cuda_launch_count": (_L, []),
     "dconv_cuda_fp32_peak_probe": (ctypes.c_double, [_P]),
+    "dconv_file_payload_floats": (_L, [ctypes.POINTER(FileHeader)]),
+    "dconv_file_read_header": (_I, [ctypes.c_char_p, ctypes.POINTER(FileHeader)]),
+    "dconv_file_read_payload": (_I, [ctypes.c_char_p, _P, _L]),
+    "dconv_file_write": (_I, [ctypes.c_char_p, ctypes.POINTER(FileHeader), _P, _L]),
+    "dconv_pack_kernel_file": (_I, [ctypes.c_char_p, _I, _I, ctypes.c_char_p]),
+    "dconv_cuda_load_kernel_file": (_I, [ctypes.c_char_p, _I, _I, _P, _P]),
     "dconv_cuda_strerror": (ctypes.c_char_p, [_I]),
     "dconv_cuda_last_error_detail": (ctypes.c_char_p, []),
 }
@@ -92,14 +105,15 @@ def lib() -> ctypes.CDLL:
 def check(rc: int) -> None:
     """Map a C-ABI return code to the reference's exception types.
 
-    EINVAL_SHAPE / ELAYOUT / EPARAM -> ValueError (std::invalid_argument in
-    the reference: shape.cpp:26, tensor.cpp:29, reference.cpp:28);
-    ECUDA / ENCCL / EUNSUPPORTED -> DconvError (std::runtime_error)."""
+    EINVAL_SHAPE / ELAYOUT / EPARAM / EFORMAT / EBLOCKED -> ValueError
+    (std::invalid_argument in the reference: shape.cpp:26, tensor.cpp:29,
+    reference.cpp:28; "parse error" / "already blocked", SPEC.md:583-587);
+    ECUDA / ENCCL / EUNSUPPORTED / EIO -> DconvError (std::runtime_error)."""
     if rc == OK:
         return
     l = lib()
     msg = f"{l.dconv_cuda_strerror(rc).decode()}: {l.dconv_cuda_last_error_detail().decode()}"
-    if rc in (EINVAL_SHAPE, ELAYOUT, EPARAM):
+    if rc in (EINVAL_SHAPE, ELAYOUT, EPARAM, EFORMAT, EBLOCKED):
         raise ValueError(msg)
     raise DconvError(msg)
 

@@ -378,6 +378,9 @@ const char* dconv_cuda_strerror(int code) {
     case DCONV_ECUDA: return "CUDA error";
     case DCONV_ENCCL: return "NCCL error";
     case DCONV_EUNSUPPORTED: return "unsupported configuration";
+    case DCONV_EFORMAT: return "parse error";
+    case DCONV_EBLOCKED: return "already blocked";
+    case DCONV_EIO: return "I/O error";
     default: return "unknown error";
   }
 }

@@ -294,3 +294,74 @@ def layer_chain(inp: BlockedFeatureMap, layers: Sequence, stream=None) -> Blocke
         x = conv_direct(x, kernel, shape, params, relu=relu, stream=stream)
     assert layout_transform_count() == before, "layout transform inside chain"
     return x
+
+
+# ---------------------------------------------------------------- tensor files
+# SPEC.md:129 (7-int header + little-endian fp32 payload) and the CLI `pack`
+# step SPEC.md:580-587; the header word order is documented in dconv_cuda.h.
+def _host_f32(t) -> "np.ndarray":
+    import numpy as np
+    if isinstance(t, torch.Tensor):
+        t = t.detach().cpu().numpy()
+    return np.ascontiguousarray(t, dtype=np.float32)
+
+
+def read_header(path: str) -> _abi.FileHeader:
+    h = _abi.FileHeader()
+    check(lib().dconv_file_read_header(path.encode(), h))
+    return h
+
+
+def _write(path: str, hdr: Tuple[int, ...], payload) -> None:
+    a = _host_f32(payload)
+    h = _abi.FileHeader(*hdr)
+    check(lib().dconv_file_write(path.encode(), h, a.ctypes.data, a.size))
+
+
+def save_feature_map(path: str, dense) -> None:
+    """Dense [c][h][w] map -> file (c_b = 0)."""
+    c, hh, w = dense.shape
+    _write(path, (c, hh, w, 0, 0, 0, _abi.FILE_FEATURE_MAP), dense)
+
+
+def save_blocked_feature_map(path: str, x: BlockedFeatureMap) -> None:
+    if x.n != 1:
+        raise ValueError("tensor files hold one image (SPEC.md:132)")
+    _write(path, (x.channels, x.height, x.width, x.c_b, 0, 0, _abi.FILE_FEATURE_MAP), x.data)
+
+
+def save_kernel(path: str, dense) -> None:
+    """Dense KernelTensor [c_i][c_o][h_f][w_f] -> file (c_ob = c_ib = 0)."""
+    ci, co, hf, wf = dense.shape
+    _write(path, (ci, hf, wf, 0, co, 0, _abi.FILE_KERNEL), dense)
+
+
+def save_blocked_kernel(path: str, k: BlockedKernel) -> None:
+    _write(path, (k.c_i, k.h_f, k.w_f, k.c_ob, k.c_o, k.c_ib, _abi.FILE_KERNEL), k.data)
+
+
+def read_payload(path: str) -> Tuple[_abi.FileHeader, "np.ndarray"]:
+    """Header and raw fp32 payload of a tensor file (host memory)."""
+    import numpy as np
+    h = read_header(path)
+    out = np.empty(lib().dconv_file_payload_floats(h), dtype=np.float32)
+    check(lib().dconv_file_read_payload(path.encode(), out.ctypes.data, out.size))
+    return h, out
+
+
+def load_kernel_file(path: str, c_ob: int, c_ib: int, stream=None) -> BlockedKernel:
+    """Weight ingest: a dense or already-blocked kernel file -> device
+    BlockedKernel (dense files are repacked on the GPU)."""
+    h = read_header(path)
+    if h.kind != _abi.FILE_KERNEL:
+        raise ValueError(f"parse error: '{path}' is not a kernel file")
+    k = BlockedKernel(h.c, h.c_o, h.h, h.w, c_ob, c_ib)
+    check(lib().dconv_cuda_load_kernel_file(path.encode(), c_ob, c_ib, ptr(k.data),
+                                            stream_ptr(stream)))
+    return k
+
+
+def pack_kernel_file(in_path: str, c_ob: int, c_ib: int, out_path: str) -> None:
+    """The CLI `pack` subcommand: dense kernel file ->
+    blocked kernel file; a blocked input raises ValueError("already blocked")."""
+    check(lib().dconv_pack_kernel_file(in_path.encode(), c_ob, c_ib, out_path.encode()))

@@ -6,9 +6,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 #include "dconv/direct.hpp"
+#include "dconv/serialize.hpp"
 
 using namespace dconv;
 
@@ -145,6 +147,28 @@ int main() {
     EXPECT(y.data[0] == 6.0f);
     layers[1].params = BlockingParams{4, 1, 4};
     EXPECT(throws_invalid([&] { layer_chain(in, layers); }));
+  }
+
+  // tensor files + the CLI pack step
+  {
+    unsigned st = 7u;
+    KernelTensor k(5, 11, 3, 3);
+    for (auto& v : k.data) v = frand(st);
+    const std::string dense = "/tmp/dconv_dropin_k.bin", blk = "/tmp/dconv_dropin_kb.bin",
+                      back = "/tmp/dconv_dropin_kd.bin";
+    save(dense, k);
+    pack_kernel_file(dense, 8, 8, blk);
+    const BlockedKernel kb = load_blocked_kernel(blk);
+    EXPECT(kb.data == pack_kernel(k, 8, 8).data);          // GPU repack == pack_kernel
+    save(back, unpack_kernel(kb));
+    EXPECT(load_kernel(back).data == k.data);               // roundtrip: identical payload
+    EXPECT(throws_invalid([&] { pack_kernel_file(blk, 8, 8, "/tmp/dconv_dropin_x.bin"); }));
+    KernelTensor one(1, 1, 1, 1);                           // 1-weight kernel file
+    one.data = {0.5f};
+    save(dense, one);
+    pack_kernel_file(dense, 8, 8, blk);
+    const BlockedKernel ob = load_blocked_kernel(blk);
+    EXPECT(ob.data.size() == 64 && ob.data[0] == 0.5f);
   }
 
   if (failures) {
