@@ -55,6 +55,10 @@ def parse():
     ap.add_argument("--shard", default="batch", choices=["batch", "co"],
                     help="batch: image ranges per rank, no collective; co: batch-1 "
                          "output-block sharding with an NCCL all-gather per layer")
+    ap.add_argument("--gather", default="nccl", choices=["nccl", "peer"],
+                    help="--shard co exchange: nccl all-gather of slices, or peer = each "
+                         "conv/pool epilogue stores into every rank's map over NVLink "
+                         "(symmetric memory) + a device barrier")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="target CPU work for the cpu_baseline sample")
     return ap.parse_args()
@@ -230,7 +234,7 @@ def main_gpu(args):
     with torch.cuda.stream(stream):
         plan = nets.build_plan(args.config, n_local, seed=1809 + (0 if co_shard else rank),
                                shard=(rank, world, None) if co_shard else None,
-                               algo=args.algo)
+                               algo=args.algo, gather_mode=args.gather)
     torch.cuda.synchronize()
     flops_local = plan.flops
 
@@ -281,7 +285,7 @@ def main_gpu(args):
     barrier()
     ms_total = max_over_ranks(e0.elapsed_time(e1))
     n_launch_steps = len(plan.steps)
-    gpu_launches = sum(1 for s in plan.steps if s.kind != "gather") * args.steps \
+    gpu_launches = sum(1 for s in plan.steps if s.kind not in ("gather", "barrier")) * args.steps \
         if graph is not None else lib.dconv_cuda_launch_count() - launches0
     ms_step = ms_total / args.steps
     flops_job = flops_local * world  # equal shards in both modes
@@ -390,12 +394,15 @@ def main_gpu(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32" if args.algo == "ffma" else "tf32 (stride-1 layers) + f32",
         "data": "synthetic (seeded uniform[-1,1), counter-based generator)",
-        "mode": "C_o-block sharding + NCCL all-gather per layer" if co_shard else
+        "mode": ("C_o-block sharding + " + ("fused peer-store gather (symmetric memory, "
+                                            "NVLink) + device barrier per layer"
+                                            if args.gather == "peer" else
+                                            "NCCL all-gather per layer")) if co_shard else
                 "batch sharding, no collective",
         "config": {"workload": f"{args.config} chain" if args.config in ("vgg16", "resnet50")
                    else f"{args.config} layers", "global_batch": batch,
                    "per_rank_batch": n_local, "c_b": 8,
-                   "parallelism": (f"co-shard x{world}, all-gather" if co_shard
+                   "parallelism": (f"co-shard x{world}, {args.gather} gather" if co_shard
                                    else f"batch-shard x{world}, no collective"),
                    "l2": "per-step working set > 126 MB L2 (activations streamed)"
                    if args.config in ("vgg16", "resnet50", "googlenet") else

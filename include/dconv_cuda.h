@@ -147,6 +147,22 @@ int dconv_cuda_conv_first_layer(const dconv_conv_desc* d, const float* in_dense,
                                 int64_t in_img_stride, const float* w,
                                 const float* skip, float* out, void* stream);
 
+/* Fused gather for C_o sharding: identical to
+ * dconv_cuda_conv_direct / _conv_first_layer, and every output pencil this
+ * rank computes is also stored, at the same offset, into each of
+ * `n_peers` (<= 7) peer copies of the output map -- device pointers that are
+ * P2P-mapped over NVLink (e.g. torch symmetric memory), addressed exactly
+ * like `out`.  After a barrier every rank holds the full map, with no
+ * separate all-gather.  FFMA / register-tiled first-layer kernels only. */
+int dconv_cuda_conv_direct_peers(const dconv_conv_desc* d, const float* in,
+                                 const float* w, const float* skip, float* out,
+                                 float* const* peer_outs, int n_peers, void* stream);
+int dconv_cuda_conv_first_layer_peers(const dconv_conv_desc* d, const float* in_dense,
+                                      int64_t in_img_stride, const float* w,
+                                      const float* skip, float* out,
+                                      float* const* peer_outs, int n_peers,
+                                      void* stream);
+
 /* pack_kernel: dense [C_i][C_o][H_f][W_f] -> blocked.  Bit-exact permutation,
  * padded slots written 0.  `dst` holds round_up(C_o,c_ob)*round_up(C_i,c_ib)*H_f*W_f. */
 int dconv_cuda_pack_kernel(const float* src, int c_i, int c_o, int h_f, int w_f,

@@ -61,6 +61,10 @@ _SIGS = {
     "dconv_cuda_conv_direct_tf32": (_I, [ctypes.POINTER(ConvDesc), _P, _P, _P, _P, _P]),
     "dconv_cuda_conv_first_layer": (
         _I, [ctypes.POINTER(ConvDesc), _P, _L, _P, _P, _P, _P]),
+    "dconv_cuda_conv_direct_peers": (
+        _I, [ctypes.POINTER(ConvDesc), _P, _P, _P, _P, ctypes.POINTER(_P), _I, _P]),
+    "dconv_cuda_conv_first_layer_peers": (
+        _I, [ctypes.POINTER(ConvDesc), _P, _L, _P, _P, _P, ctypes.POINTER(_P), _I, _P]),
     "dconv_cuda_pack_kernel": (_I, [_P] + [_I] * 6 + [_P, _P]),
     "dconv_cuda_unpack_kernel": (_I, [_P] + [_I] * 6 + [_P, _P]),
     "dconv_cuda_pack_feature_map": (_I, [_P] + [_I] * 6 + [_P, _P]),

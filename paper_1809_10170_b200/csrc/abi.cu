@@ -146,9 +146,21 @@ int resolve(const dconv_conv_desc* d, bool dense_input, int64_t dense_img,
 
 extern "C" {
 
-int dconv_cuda_conv_direct(const dconv_conv_desc* d, const float* in,
-                           const float* w, const float* skip, float* out,
-                           void* stream) {
+namespace {
+int check_peers(float* const* peers, int n_peers) {
+  if (n_peers < 0 || n_peers > dconv_dev::kMaxPeers)
+    return set_error(DCONV_EPARAM, "n_peers %d outside [0, %d]", n_peers, dconv_dev::kMaxPeers);
+  if (n_peers && !peers) return set_error(DCONV_EPARAM, "NULL peer list");
+  for (int i = 0; i < n_peers; ++i)
+    if (!peers[i] || !aligned16(peers[i]))
+      return set_error(DCONV_EPARAM, "peer output %d is NULL or not 16-byte aligned", i);
+  return DCONV_OK;
+}
+
+int conv_direct_impl(const dconv_conv_desc* d, const float* in, const float* w,
+                     const float* skip, float* out, float* const* peers, int n_peers,
+                     void* stream) {
+  if (int rc = check_peers(peers, n_peers)) return rc;
   Resolved r;
   int rc = resolve(d, false, 0, in, w, skip, out, &r);
   if (rc) return rc;
@@ -174,12 +186,16 @@ int dconv_cuda_conv_direct(const dconv_conv_desc* d, const float* in,
     p.sk_img = r.sk_img; p.sk_blk = r.sk_blk; p.sk_row = r.sk_row;
     p.epi = d->epilogue;
     p.variant = d->tile_variant > 0 ? d->tile_variant - 1 : -1;
+    p.n_peers = n_peers;
+    for (int i = 0; i < n_peers; ++i) p.peer_out[i] = peers[i];
     rc = dconv_dev::launch_conv_ffma(p, as_stream(stream));
     // AUTO: a configuration whose stage cannot be staged in shared memory
     // (very large filters on tiny maps) runs on the generic kernel instead.
     if (rc != DCONV_EUNSUPPORTED || d->algo != DCONV_ALGO_AUTO) return rc;
     algo = DCONV_ALGO_GENERIC;
   }
+  if (algo == DCONV_ALGO_GENERIC && n_peers)
+    return set_error(DCONV_EUNSUPPORTED, "fused peer gather needs the FFMA kernel (c_b = 8)");
   if (algo == DCONV_ALGO_GENERIC) {
     dconv_dev::GenericParams p{};
     p.in = in; p.w = w; p.skip = skip; p.out = out;
@@ -194,6 +210,18 @@ int dconv_cuda_conv_direct(const dconv_conv_desc* d, const float* in,
     return dconv_dev::launch_conv_generic(p, as_stream(stream));
   }
   return set_error(DCONV_EUNSUPPORTED, "algo %d not available", algo);
+}
+}  // namespace
+
+int dconv_cuda_conv_direct(const dconv_conv_desc* d, const float* in, const float* w,
+                           const float* skip, float* out, void* stream) {
+  return conv_direct_impl(d, in, w, skip, out, nullptr, 0, stream);
+}
+
+int dconv_cuda_conv_direct_peers(const dconv_conv_desc* d, const float* in, const float* w,
+                                 const float* skip, float* out, float* const* peer_outs,
+                                 int n_peers, void* stream) {
+  return conv_direct_impl(d, in, w, skip, out, peer_outs, n_peers, stream);
 }
 
 int dconv_cuda_tf32_prepared_size(const dconv_conv_desc* d, int64_t* floats) {
@@ -246,9 +274,11 @@ int dconv_cuda_conv_direct_tf32(const dconv_conv_desc* d, const float* in,
   return dconv_dev::launch_conv_tf32(p, w_prepared, as_stream(stream));
 }
 
-int dconv_cuda_conv_first_layer(const dconv_conv_desc* d, const float* in_dense,
-                                int64_t in_img_stride, const float* w,
-                                const float* skip, float* out, void* stream) {
+namespace {
+int conv_first_impl(const dconv_conv_desc* d, const float* in_dense, int64_t in_img_stride,
+                    const float* w, const float* skip, float* out, float* const* peers,
+                    int n_peers, void* stream) {
+  if (int rc = check_peers(peers, n_peers)) return rc;
   Resolved r;
   int rc = resolve(d, true, in_img_stride, in_dense, w, skip, out, &r);
   if (rc) return rc;
@@ -263,6 +293,8 @@ int dconv_cuda_conv_first_layer(const dconv_conv_desc* d, const float* in_dense,
   p.sk_img = r.sk_img; p.sk_blk = r.sk_blk; p.sk_row = r.sk_row;
   p.epi = d->epilogue;
   p.dense_input = 1;
+  p.n_peers = n_peers;
+  for (int i = 0; i < n_peers; ++i) p.peer_out[i] = peers[i];
   const bool fast_ok = d->c_ob == 8 && aligned16(w) && aligned16(out) &&
                        (!skip || aligned16(skip)) &&
                        ((r.out_img | r.out_blk | r.out_row | r.sk_img | r.sk_blk |
@@ -271,7 +303,23 @@ int dconv_cuda_conv_first_layer(const dconv_conv_desc* d, const float* in_dense,
     rc = dconv_dev::launch_conv_first_fast(p, as_stream(stream));
     if (rc != DCONV_EUNSUPPORTED) return rc;
   }
+  if (n_peers)
+    return set_error(DCONV_EUNSUPPORTED, "fused peer gather needs the register-tiled first-layer reader");
   return dconv_dev::launch_conv_first_layer(p, as_stream(stream));
+}
+}  // namespace
+
+int dconv_cuda_conv_first_layer(const dconv_conv_desc* d, const float* in_dense,
+                                int64_t in_img_stride, const float* w, const float* skip,
+                                float* out, void* stream) {
+  return conv_first_impl(d, in_dense, in_img_stride, w, skip, out, nullptr, 0, stream);
+}
+
+int dconv_cuda_conv_first_layer_peers(const dconv_conv_desc* d, const float* in_dense,
+                                      int64_t in_img_stride, const float* w,
+                                      const float* skip, float* out, float* const* peer_outs,
+                                      int n_peers, void* stream) {
+  return conv_first_impl(d, in_dense, in_img_stride, w, skip, out, peer_outs, n_peers, stream);
 }
 
 int dconv_cuda_pack_kernel(const float* src, int c_i, int c_o, int h_f, int w_f,

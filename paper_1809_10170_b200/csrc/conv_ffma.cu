@@ -495,6 +495,13 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
 #pragma unroll
         for (int c = 0; c < 8; c += 4)
           *reinterpret_cast<float4*>(o + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+        // fused C_o-shard gather: the same pencil into every peer's map
+        for (int q = 0; q < p.n_peers; ++q) {
+          float* po = p.peer_out[q] + (o - p.out);
+#pragma unroll
+          for (int c = 0; c < 8; c += 4)
+            *reinterpret_cast<float4*>(po + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+        }
       }
     }
     if (TCO == 8 && ks > 1) {

@@ -143,6 +143,11 @@ __global__ void __launch_bounds__(256)
     }
     *reinterpret_cast<float4*>(obase + x * 8) = v0;
     *reinterpret_cast<float4*>(obase + x * 8 + 4) = v1;
+    for (int q = 0; q < p.n_peers; ++q) {  // fused C_o-shard gather
+      float* po = p.peer_out[q] + (obase - p.out) + x * 8;
+      *reinterpret_cast<float4*>(po) = v0;
+      *reinterpret_cast<float4*>(po + 4) = v1;
+    }
   }
 }
 

@@ -8,6 +8,8 @@ namespace dconv_dev {
 
 // Parameters of the FFMA direct-conv kernel (c_ib = c_ob = 8).  All strides
 // in floats.  Tiling / staging fields are filled in by the launcher.
+constexpr int kMaxPeers = 7;  // fused C_o-shard gather: up to 8 GPUs
+
 struct FfmaParams {
   const float* in;
   const float* w;
@@ -34,6 +36,10 @@ struct FfmaParams {
   int sy;                      // row stride of the staged patch (s, or 1 for 1x1 re-viewed)
   unsigned tw_magic;           // ceil(2^32 / TW)
   unsigned h_o_magic;          // ceil(2^32 / h_o) when n * h_o^2 < 2^32, else 0
+  // fused gather: every output store is repeated at the same offset from
+  // each peer's copy of the output map (P2P-mapped over NVLink)
+  int n_peers;
+  float* peer_out[kMaxPeers];
 };
 
 extern int ffma_variant_override;  // -1 = heuristic (dconv_cuda_set_ffma_variant)
@@ -60,6 +66,8 @@ struct GenericParams {
   int64_t sk_img, sk_blk, sk_row;
   int epi;
   int dense_input;                   // 1: first layer, input [N][C_i][H][W]
+  int n_peers;                       // fused gather (first-layer reader only)
+  float* peer_out[kMaxPeers];
 };
 
 int launch_conv_generic(const GenericParams& p, cudaStream_t stream);

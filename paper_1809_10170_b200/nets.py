@@ -179,17 +179,28 @@ class Act:
     def interior(self) -> torch.Tensor:
         return self.buf[:, :, self.halo:self.halo + self.h, self.halo:self.halo + self.w, :]
 
+    def block_view(self, b0: int) -> "Act":
+        """The same map seen from output block b0 on (a rank's C_o slice
+        inside the full buffer): base() moves, strides stay."""
+        import copy
+        v = copy.copy(self)
+        v.off = self.off + b0 * self.blk
+        return v
+
 
 def conv(l: Layer, n: int, x: "Act|torch.Tensor", w: torch.Tensor, out: Act,
          epilogue: int = 0, skip: Optional[Act] = None, stream=None,
          in_view: Optional[Tuple[int, int, int, int]] = None,
-         co_range: Optional[Tuple[int, int]] = None, tile_variant: int = 0) -> None:
+         co_range: Optional[Tuple[int, int]] = None, tile_variant: int = 0,
+         peers: Optional[List[int]] = None) -> None:
     """Launch one conv layer through the C-ABI.  ``x`` is an Act (blocked) or,
     for a first layer, the dense [n][c][h][w] network input.  ``in_view``
     optionally overrides (ptr, img, blk, row) of the blocked input (crops).
     ``co_range`` = (first block, block count) computes only those output
     blocks into ``out`` (a rank's C_o slice); ``skip`` is then read from the
-    same blocks of the full skip map."""
+    same blocks of the full skip map.  ``peers``: device addresses (P2P-mapped
+    peer copies of ``out``) that receive the same stores -- the fused
+    C_o-shard gather."""
     d = _desc(l, n, epilogue)
     d.tile_variant = tile_variant
     d.out_img_stride, d.out_blk_stride, d.out_row_stride = out.img, out.blk, out.row
@@ -202,15 +213,25 @@ def conv(l: Layer, n: int, x: "Act|torch.Tensor", w: torch.Tensor, out: Act,
         d.skip_img_stride, d.skip_blk_stride, d.skip_row_stride = skip.img, skip.blk, skip.row
         sp = skip.base() + 4 * b0 * skip.blk
     st = stream_ptr(stream)
+    pl = (ctypes.c_void_p * max(1, len(peers or [])))(*(peers or []))
+    np_ = len(peers or [])
     if l.first:
-        check(lib().dconv_cuda_conv_first_layer(ctypes.byref(d), ptr(x), 0, ptr(w), sp,
-                                                out.base(), st))
+        if np_:
+            check(lib().dconv_cuda_conv_first_layer_peers(ctypes.byref(d), ptr(x), 0, ptr(w), sp,
+                                                          out.base(), pl, np_, st))
+        else:
+            check(lib().dconv_cuda_conv_first_layer(ctypes.byref(d), ptr(x), 0, ptr(w), sp,
+                                                    out.base(), st))
         return
     if in_view is None:
         in_view = x.full_view()
     d.in_img_stride, d.in_blk_stride, d.in_row_stride = in_view[1:]
-    check(lib().dconv_cuda_conv_direct(ctypes.byref(d), in_view[0], ptr(w), sp,
-                                       out.base(), st))
+    if np_:
+        check(lib().dconv_cuda_conv_direct_peers(ctypes.byref(d), in_view[0], ptr(w), sp,
+                                                 out.base(), pl, np_, st))
+    else:
+        check(lib().dconv_cuda_conv_direct(ctypes.byref(d), in_view[0], ptr(w), sp,
+                                           out.base(), st))
 
 
 def conv_tf32(l: Layer, n: int, x: "Act", wprep: torch.Tensor, out: Act,
@@ -239,10 +260,12 @@ def prepare_tf32(l: Layer, w_blocked: torch.Tensor, stream=None) -> torch.Tensor
     return out
 
 
-def maxpool_into(x: Act, out: Act, stream=None) -> None:
+def maxpool_into(x: Act, out: Act, stream=None, out_ptr: Optional[int] = None) -> None:
+    """2x2/s2 max-pool of x into the view ``out`` (``out_ptr`` overrides its
+    base address: a peer's copy of the same view)."""
     check(lib().dconv_cuda_maxpool2x2_blocked(x.base(), x.n, nblk(x.c), x.h, x.w, CB,
-                                              out.base(), out.img, out.blk, out.row,
-                                              stream_ptr(stream)))
+                                              out.base() if out_ptr is None else out_ptr,
+                                              out.img, out.blk, out.row, stream_ptr(stream)))
 
 
 def pack_weights(dense: torch.Tensor, first: bool, stream=None) -> torch.Tensor:
@@ -282,6 +305,10 @@ class Plan:
     layers: List[Layer]
     shard: Optional[Tuple[int, int, object]] = None
     algo: str = "ffma"   # "tf32": stride-1 blocked layers on the tcgen05 path
+    # C_o-shard exchange: "nccl" = slice + all-gather; "peer" = the conv/pool
+    # epilogue stores into every rank's full map (symmetric memory over
+    # NVLink) followed by a device barrier -- no collective on the data path
+    gather_mode: str = "nccl"
     weights: Dict[str, torch.Tensor] = field(default_factory=dict)
     tiles: Dict[str, int] = field(default_factory=dict)  # autotuned FFMA CTA tile per layer
     steps: List = field(default_factory=list)
@@ -344,6 +371,31 @@ class Plan:
         return Act(self.n, c, full.h, full.w, halo=full.halo, pad_hi_only=full.pad_hi_only,
                    device=full.buf.device)
 
+    def _adopt_symmetric(self, full: Act) -> None:
+        """Move ``full`` into symmetric memory (one allocation per rank,
+        P2P-mapped) and record the peers' addresses of the same map."""
+        if getattr(full, "symm", None) is not None:
+            return
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        rank, world, group = self.shard
+        group = group or dist.group.WORLD
+        t = symm_mem.empty(tuple(full.buf.shape), dtype=torch.float32, device=full.buf.device)
+        t.zero_()  # halo ring and padded channels are zeros on every rank
+        h = symm_mem.rendezvous(t, group)
+        off = t.data_ptr() - h.buffer_ptrs[rank]
+        full.buf = t
+        full.symm = h
+        full.peer_bases = [h.buffer_ptrs[r] + off for r in range(world) if r != rank]
+
+    def _peer_ptrs(self, full: Act, b0: int) -> List[int]:
+        """Peers' addresses of block b0's interior origin in ``full``."""
+        return [b + 4 * (full.off + b0 * full.blk) for b in full.peer_bases]
+
+    def _barrier(self, name: str, full: Act) -> None:
+        h = full.symm
+        self.steps.append(Step(lambda st: h.barrier(channel=0), f"barrier_{name}", "barrier"))
+
     def _gather(self, name: str, full: Act, local: Act) -> None:
         from .shard import all_gather_blocks
         group = self.shard[2]
@@ -372,8 +424,20 @@ class Plan:
         if self.n != 1:
             raise ValueError("C_o sharding is the batch-1 mode")
         b0, cnt = block_range(nblk(l.c_o), world, rank)
-        ys = self._local(y, cnt * CB)
         flops = l.flops * min(cnt * CB, l.c_o - b0 * CB) // l.c_o
+        if self.gather_mode == "peer" and gather:
+            # fused gather: this rank's blocks go straight into every rank's
+            # full map (local store + NVLink peer stores), then one barrier
+            self._adopt_symmetric(y)
+            yv, peers = y.block_view(b0), self._peer_ptrs(y, b0)
+            self.steps.append(Step(lambda st: conv(l, self.n, x, w, yv, epilogue, skip, st,
+                                                   in_view, (b0, cnt),
+                                                   tile_variant=self.tiles.get(l.name, 0),
+                                                   peers=peers),
+                                   l.name, kind, flops, l))
+            self._barrier(l.name, y)
+            return yv
+        ys = self._local(y, cnt * CB)
         self.steps.append(Step(lambda st: conv(l, self.n, x, w, ys, epilogue, skip, st, in_view,
                                                (b0, cnt), tile_variant=self.tiles.get(l.name, 0)),
                                l.name, kind, flops, l))
@@ -385,6 +449,21 @@ class Plan:
         """2x2/s2 max-pool of this rank's result into z (gathered if sharded)."""
         if self.shard is None:
             self.steps.append(Step(lambda st: maxpool_into(src_local, z, st), name, "pool"))
+            return
+        if self.gather_mode == "peer":
+            # pool this rank's slice into every rank's z (local + peers)
+            from .shard import block_range
+            rank, world, _ = self.shard
+            b0, _cnt = block_range(nblk(z.c), world, rank)
+            self._adopt_symmetric(z)
+            zv, peers = z.block_view(b0), self._peer_ptrs(z, b0)
+
+            def pool_all(st, src=src_local, zv=zv, peers=peers):
+                maxpool_into(src, zv, st)
+                for pp in peers:
+                    maxpool_into(src, zv, st, out_ptr=pp)
+            self.steps.append(Step(pool_all, name, "pool"))
+            self._barrier(name, z)
             return
         zs = self._local(z, src_local.c)
         self.steps.append(Step(lambda st: maxpool_into(src_local, zs, st), name, "pool"))
@@ -400,12 +479,17 @@ def _fill(t: torch.Tensor, seed: int, stream_id: int, scale: float = 1.0) -> Non
 
 def build_plan(config: str, n: int, seed: int = 1809, device="cuda",
                dense_weights: Optional[Dict[str, torch.Tensor]] = None,
-               shard: Optional[Tuple[int, int, object]] = None, algo: str = "ffma") -> Plan:
+               shard: Optional[Tuple[int, int, object]] = None, algo: str = "ffma",
+               gather_mode: str = "nccl") -> Plan:
     """Instantiates a BASELINE.json config on the current device.  ``shard``
-    = (rank, world, process group) for batch-1 C_o-block sharding; ``algo``
-    = "tf32" runs the stride-1 blocked layers on the tcgen05 TF32 kernel."""
+    = (rank, world, process group) for batch-1 C_o-block sharding, with the
+    exchange ``gather_mode`` "nccl" (all-gather) or "peer" (fused peer stores
+    + barrier); ``algo`` = "tf32" runs the stride-1 blocked layers on the
+    tcgen05 TF32 kernel."""
+    if gather_mode not in ("nccl", "peer"):
+        raise ValueError(f"gather_mode {gather_mode!r}")
     layers = CONFIGS[config]
-    p = Plan(config, n, list(layers), shard=shard, algo=algo)
+    p = Plan(config, n, list(layers), shard=shard, algo=algo, gather_mode=gather_mode)
     for idx, l in enumerate(layers):
         wd = dense_weights[l.name] if dense_weights else None
         if wd is None:

@@ -456,6 +456,82 @@ def test_co_shard_plan_world1_matches_unsharded():
         dist.destroy_process_group()
 
 
+def test_peer_store_epilogue_writes_every_copy():
+    """The fused C_o-shard gather kernel path: a rank's output blocks are
+    stored into its own map and, at the same offsets, into every peer copy
+    (here local buffers stand in for the P2P-mapped peers); blocks owned by
+    other ranks are left untouched in all copies.  FFMA and first-layer
+    reader, ReLU and ADD_RELU epilogues."""
+    import ctypes
+    lib = _abi.lib()
+    # blocked 3x3 layer: rank 1 of 2 computes output blocks [2, 4) of 4
+    ci, co, h = 16, 32, 12
+    x = po.uniform((ci, h, h), 9500, 0)
+    k = po.uniform((ci, co, 3, 3), 9500, 1)
+    skip = po.pack_feature_map(po.uniform((co, h - 2, h - 2), 9500, 2), 8)
+    l = nets.Layer("pe", ci, co, h, h, 3, 3, 1)
+    a = nets.Act(1, ci, h, h)
+    a.buf.copy_(dev(po.pack_feature_map(x, 8)[None]))
+    sk = nets.Act(1, co, h - 2, h - 2)
+    sk.buf.copy_(dev(skip[None]))
+    copies = [nets.Act(1, co, h - 2, h - 2, halo=1) for _ in range(3)]
+    for c in copies:
+        c.buf.fill_(7.0)
+    b0, cnt = 2, 2
+    peers = [c.base() + 4 * b0 * c.blk for c in copies[1:]]
+    nets.conv(l, 1, a, nets.pack_weights(dev(k), False), copies[0].block_view(b0),
+              _abi.EPI_ADD_RELU, sk, co_range=(b0, cnt), peers=peers)
+    want = np.maximum(po.pack_feature_map(po.conv_oracle64(x, k, 1), 8) + skip, 0)
+    ref = host(copies[0].buf)
+    for c in copies:
+        got = host(c.buf)
+        assert np.array_equal(got, ref), "peer copy differs from the local store"
+        assert_tol(got[0, b0:b0 + cnt, 1:-1, 1:-1], want[b0:b0 + cnt], "peer-store conv")
+        assert (got[0, :b0] == 7.0).all() and (got[0, :, 0] == 7.0).all()
+    # first-layer reader with peers
+    xf = po.uniform((3, 23, 23), 9501, 0)
+    kf = po.uniform((3, 64, 7, 7), 9501, 1)
+    lf = nets.Layer("pf", 3, 64, 23, 23, 7, 7, 2, True)
+    outs = [nets.Act(1, 64, lf.h_o, lf.w_o) for _ in range(2)]
+    nets.conv(lf, 1, dev(xf[None]), nets.pack_weights(dev(kf), True), outs[0].block_view(4),
+              _abi.EPI_RELU, co_range=(4, 4), peers=[outs[1].base() + 4 * 4 * outs[1].blk])
+    wantf = np.maximum(po.pack_feature_map(po.conv_oracle64(xf, kf, 2), 8), 0)
+    g0, g1 = host(outs[0].buf), host(outs[1].buf)
+    assert np.array_equal(g0, g1)
+    assert_tol(g0[0, 4:], wantf[4:], "peer-store first layer")
+    assert not g0[0, :4].any()
+    # argument checks
+    d = nets._desc(l, 1)
+    bad = (ctypes.c_void_p * 8)(*([peers[0]] * 8))
+    with pytest.raises(ValueError, match="n_peers"):
+        _abi.check(lib.dconv_cuda_conv_direct_peers(ctypes.byref(d), a.base(), 0, 0,
+                                                    copies[0].base(), bad, 8, 0))
+
+
+def test_co_shard_peer_gather_plan_world1():
+    """The symmetric-memory ("peer") C_o-shard plan on a 1-rank NCCL group:
+    symmetric buffers, block views, device barriers -- bitwise equal to the
+    unsharded plan on ResNet-50 b1 and VGG-16 b1."""
+    import os
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29519")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        for cfg in ("resnet50", "vgg16"):
+            a = nets.build_plan(cfg, 1, seed=6)
+            b = nets.build_plan(cfg, 1, seed=6, shard=(0, 1, None), gather_mode="peer")
+            assert any(s.kind == "barrier" for s in b.steps)
+            assert not any(s.kind == "gather" for s in b.steps)
+            for _ in range(2):  # repeated steps reuse the symmetric buffers
+                a.run()
+                b.run()
+            torch.cuda.synchronize()
+            assert torch.equal(a.output.buf, b.output.buf), cfg
+    finally:
+        dist.destroy_process_group()
+
+
 @pytest.mark.parametrize("ks", [2, 3, 4, 6, 8])
 def test_cluster_split_k(ks, monkeypatch):
     """Split-K over a thread-block cluster with the DSMEM reduction, forced
