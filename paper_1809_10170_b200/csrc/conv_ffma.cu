@@ -427,8 +427,49 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
     // Split-K: every rank publishes its partial tile in its own smem, then
     // rank r sums pixels [r*8/ks, (r+1)*8/ks) of every thread's 8x8 tile over
     // ranks 0..ks-1 in that fixed order (deterministic, no global workspace).
-    int k_lo = 0, k_hi = TPX;
+    // pixel k of this thread, output block jl of the view: skip-add, ReLU,
+    // one pencil store (+ the same pencil into every peer's map)
+    auto emit = [&](int k, int jl, float (&v)[8]) {
+      const int q = pg + PG * k;
+      const int ty = (int)__umulhi((unsigned)q, p.tw_magic), tx = q - ty * p.TW;
+      const int x = tx0 + tx;
+      if (ty >= tr.th || x >= p.w_o) return;
+      int img, y, prow;
+      tile_row(p, tr, ty, img, y, prow);
+      if (p.epi & DCONV_EPI_ADD) {
+        const float* sk = p.skip + (int64_t)jl * p.sk_blk + (int64_t)img * p.sk_img +
+                          (int64_t)y * p.sk_row + (int64_t)x * kCB;
+#pragma unroll
+        for (int c = 0; c < 8; c += 4) {
+          const float4 s4 = *reinterpret_cast<const float4*>(sk + c);
+          v[c] += s4.x; v[c + 1] += s4.y; v[c + 2] += s4.z; v[c + 3] += s4.w;
+        }
+      }
+      if (p.epi & DCONV_EPI_RELU) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) v[c] = fmaxf(v[c], 0.f);
+      }
+      float* o = p.out + (int64_t)jl * p.out_blk + (int64_t)img * p.out_img +
+                 (int64_t)y * p.out_row + (int64_t)x * kCB;
+#pragma unroll
+      for (int c = 0; c < 8; c += 4)
+        *reinterpret_cast<float4*>(o + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+      // fused C_o-shard gather: the same pencil into every peer's map
+      for (int pi = 0; pi < p.n_peers; ++pi) {
+        float* po = p.peer_out[pi] + (o - p.out);
+#pragma unroll
+        for (int c = 0; c < 8; c += 4)
+          *reinterpret_cast<float4*>(po + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+      }
+    };
+
     if (TCO == 8 && ks > 1) {
+      // Split-K: every rank publishes its partial tile in its own smem, then
+      // rank r sums pixels [r*8/ks, (r+1)*8/ks) of every thread's 8x8 tile
+      // over ranks 0..ks-1 in that fixed order (deterministic, no global
+      // workspace).  Rolled loops: this path runs once per unit, and a
+      // compact body avoids the instruction-cache misses that dominate
+      // batch-1 layers.
       if (unit_iter > 0) mbar_wait_cluster(done, (unit_iter - 1) & 1);
 #pragma unroll
       for (int k = 0; k < TPX; ++k)
@@ -442,72 +483,38 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
       if (lane == 0)
         for (int q = 0; q < ks; ++q) mbar_arrive_remote(ready, q);
       mbar_wait_cluster(ready, unit_iter & 1);
-      k_lo = rank * TPX / ks;
-      k_hi = (rank + 1) * TPX / ks;
-    }
+      if (cb < cg_valid) {
+        const int jl = jb0 + cb - p.jb_begin;
+#pragma unroll 1
+        for (int k = rank * TPX / ks; k < (rank + 1) * TPX / ks; ++k) {
+          float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+          for (int r = 0; r < ks; ++r)
 #pragma unroll
-    for (int bb = 0; bb < NBLK; ++bb) {
-      if (cb + bb >= cg_valid) continue;
-      const int jl = jb0 + cb + bb - p.jb_begin;  // block index within the output view
-      float* obase = p.out + (int64_t)jl * p.out_blk;
-      const float* sbase = p.skip ? p.skip + (int64_t)jl * p.sk_blk : nullptr;
+            for (int c = 0; c < 8; ++c) v[c] += ld_dsmem(&red[(k * 8 + c) * (NW * 32) + tid], r);
+          emit(k, jl, v);
+        }
+      }
+      __syncwarp();
+      if (lane == 0)
+        for (int q = 0; q < ks; ++q) mbar_arrive_remote(done, q);
+    } else {
 #pragma unroll
-      for (int k = 0; k < TPX; ++k) {
-        if (k < k_lo || k >= k_hi) continue;
-        const int q = pg + PG * k;
-        const int ty = (int)__umulhi((unsigned)q, p.tw_magic), tx = q - ty * p.TW;
-        const int x = tx0 + tx;
-        const bool valid = ty < tr.th && x < p.w_o;
-        float v[8];
-        if (TCO == 8 && ks > 1) {
+      for (int bb = 0; bb < NBLK; ++bb) {
+        if (cb + bb >= cg_valid) continue;
+        const int jl = jb0 + cb + bb - p.jb_begin;  // block index within the output view
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            float sum = 0.f;
-            for (int r = 0; r < ks; ++r) sum += ld_dsmem(&red[(k * 8 + c) * (NW * 32) + tid], r);
-            v[c] = sum;
-          }
-        } else {
+        for (int k = 0; k < TPX; ++k) {
+          float v[8];
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             const float2 f = unpack2(acc[k][bb * 4 + c]);
             v[2 * c] = f.x;
             v[2 * c + 1] = f.y;
           }
-        }
-        if (!valid) continue;
-        int img, y, prow;
-        tile_row(p, tr, ty, img, y, prow);
-        if (p.epi & DCONV_EPI_ADD) {
-          const float* sk = sbase + (int64_t)img * p.sk_img + (int64_t)y * p.sk_row +
-                            (int64_t)x * kCB;
-#pragma unroll
-          for (int c = 0; c < 8; c += 4) {
-            const float4 s4 = *reinterpret_cast<const float4*>(sk + c);
-            v[c] += s4.x; v[c + 1] += s4.y; v[c + 2] += s4.z; v[c + 3] += s4.w;
-          }
-        }
-        if (p.epi & DCONV_EPI_RELU) {
-#pragma unroll
-          for (int c = 0; c < 8; ++c) v[c] = fmaxf(v[c], 0.f);
-        }
-        float* o = obase + (int64_t)img * p.out_img + (int64_t)y * p.out_row +
-                   (int64_t)x * kCB;
-#pragma unroll
-        for (int c = 0; c < 8; c += 4)
-          *reinterpret_cast<float4*>(o + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
-        // fused C_o-shard gather: the same pencil into every peer's map
-        for (int q = 0; q < p.n_peers; ++q) {
-          float* po = p.peer_out[q] + (o - p.out);
-#pragma unroll
-          for (int c = 0; c < 8; c += 4)
-            *reinterpret_cast<float4*>(po + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+          emit(k, jl, v);
         }
       }
-    }
-    if (TCO == 8 && ks > 1) {
-      __syncwarp();
-      if (lane == 0)
-        for (int q = 0; q < ks; ++q) mbar_arrive_remote(done, q);
     }
   }
   // no CTA may leave while a peer can still read its partials
