@@ -39,6 +39,7 @@ namespace {
 
 constexpr int kCB = 8;          // channel block of this kernel (c_ib = c_ob)
 constexpr int kMaxStages = 8;
+constexpr int kMaxKs = 16;      // split-K cluster size (> 8 is the non-portable opt-in)
 constexpr int kComputeWarps = 8;  // default: 2 compute warpgroups, 8x8 outputs / thread
 constexpr int kThreads = (kComputeWarps + 4) * 32;  // + producer warpgroup
 
@@ -198,8 +199,8 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], NW);
     }
-    mbar_init(ready, NW * ks);
-    mbar_init(done, NW * ks);
+    mbar_init(ready, ks);  // one arrive per rank (thread 0, after a named barrier)
+    mbar_init(done, ks);
     fence_mbar_init();
   }
   if (use_tmem && warp == 0) {
@@ -479,25 +480,32 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
           red[(k * 8 + 2 * c) * (NW * 32) + tid] = f.x;
           red[(k * 8 + 2 * c + 1) * (NW * 32) + tid] = f.y;
         }
-      __syncwarp();
-      if (lane == 0)
-        for (int q = 0; q < ks; ++q) mbar_arrive_remote(ready, q);
+      // all compute warps' partials are in smem: one fence, ks relaxed arrives
+      asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+      if (tid == 0) {
+        fence_cluster();
+        for (int q = 0; q < ks; ++q) mbar_arrive_remote_relaxed(ready, q);
+      }
       mbar_wait_cluster(ready, unit_iter & 1);
       if (cb < cg_valid) {
         const int jl = jb0 + cb - p.jb_begin;
 #pragma unroll 1
         for (int k = rank * TPX / ks; k < (rank + 1) * TPX / ks; ++k) {
           float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
+          // ranks in order 0..ks-1 (fixed summation order); 4 ranks' loads in flight
+#pragma unroll 4
           for (int r = 0; r < ks; ++r)
 #pragma unroll
             for (int c = 0; c < 8; ++c) v[c] += ld_dsmem(&red[(k * 8 + c) * (NW * 32) + tid], r);
           emit(k, jl, v);
         }
       }
-      __syncwarp();
-      if (lane == 0)
-        for (int q = 0; q < ks; ++q) mbar_arrive_remote(done, q);
+      // every compute warp has consumed the peers' partials
+      asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+      if (tid == 0) {
+        fence_cluster();
+        for (int q = 0; q < ks; ++q) mbar_arrive_remote_relaxed(done, q);
+      }
     } else {
 #pragma unroll
       for (int bb = 0; bb < NBLK; ++bb) {
@@ -582,10 +590,43 @@ double tail_rounds(int64_t units, int sms) {
   return (double)full + t;
 }
 
-constexpr double kCopyCycles = 50.0;   // per bulk copy (row of one input block)
+constexpr double kCopyCycles = 50.0;     // per bulk copy (row of one input block)
 constexpr double kFfmaPerCycle = 102.0;  // FMA / cycle / SM sustained (80% of 128)
+constexpr double kUnitOverhead = 1500.0; // per-unit prologue + epilogue, cycles
+constexpr double kLaunchFill = 2500.0;   // first stage in flight, cycles
 
-void pick_tile(FfmaParams& p, int BM, int BN, int co_groups, int sms) {
+// One unit's FFMA2 cycles (BM x BN outputs x the whole reduction) + overhead.
+double unit_cycles(const FfmaParams& p, int BM, int BN) {
+  return (double)BM * BN * p.ib_n * kCB * p.h_f * p.w_f / kFfmaPerCycle + kUnitOverhead;
+}
+
+// Few units (< SMs): every unit's K range split over a cluster of ks CTAs,
+// ceil(units / slots[ks]) rounds of (unit / ks + DSMEM reduction).
+double split_cycles(int64_t units, int ks, int slots, double unit) {
+  const double rounds = (double)((units + slots - 1) / slots);
+  const double red = ks > 1 ? 1500.0 + 300.0 * ks : 0.0;
+  return rounds * (unit / ks + red) + kLaunchFill;
+}
+
+// Cheapest split factor for `units` (< SMs) given the co-resident cluster
+// counts slots[ks] (slots[1] = SMs); ks <= max_ks (stages to split).
+int best_split(int64_t units, const int* slots, int max_ks, double unit, double* cycles) {
+  int best = 1;
+  double best_c = split_cycles(units, 1, slots[1], unit);
+  for (int ks = 2; ks <= kMaxKs && ks <= max_ks; ++ks) {
+    if (slots[ks] < 1) continue;
+    const double c = split_cycles(units, ks, slots[ks], unit);
+    if (c < best_c - 1e-9) {
+      best_c = c;
+      best = ks;
+    }
+  }
+  if (cycles) *cycles = best_c;
+  return best;
+}
+
+void pick_tile(FfmaParams& p, int BM, int BN, int co_groups, int sms, const int* slots,
+               bool allow_split) {
   int cand[16], nc = 0;
   for (int tw = 4; tw <= 128 && tw <= BM; tw *= 2) cand[nc++] = tw;
   for (int d = 1; d <= 4; ++d) {
@@ -595,23 +636,28 @@ void pick_tile(FfmaParams& p, int BM, int BN, int co_groups, int sms) {
   double best_score = -1;
   int64_t best_patch = 0;
   const int64_t vh = (int64_t)p.n * p.h_o;
+  const double unit = unit_cycles(p, BM, BN);
   FfmaParams q = p;
   for (int i = 0; i < nc; ++i) {
     const int tw = cand[i], th = BM / tw;
     const int64_t ty = (vh + th - 1) / th, tx = (p.w_o + tw - 1) / tw;
     const int64_t units = ty * tx * co_groups;
-    const double slots_used = tail_rounds(units, sms) * sms;
+    double cycles;
+    if (units < sms && allow_split)
+      best_split(units, slots, p.ib_n, unit, &cycles);
+    else
+      cycles = tail_rounds(units, sms) * unit + kLaunchFill;
     q.TH = th;
     q.TW = tw;
     const double rows = max_patch_rows(q, p.h_f);
     // producer copies per input block vs FFMA2 cycles per input block
     const double copy_ratio = kCopyCycles * rows /
                               ((double)BM * BN * kCB * p.h_f * p.w_f / kFfmaPerCycle);
-    const double score = (double)vh * p.w_o * co_groups / (slots_used * BM) /
-                         std::max(1.0, copy_ratio);
+    const double score = 1.0 / (cycles * std::max(1.0, copy_ratio));
     const int64_t patch = (int64_t)((std::min<int64_t>(th, vh) - 1) * p.sy + p.h_f) *
                           ((std::min(tw, p.w_o) - 1) * p.s + p.w_f);
-    if (score > best_score + 1e-6 || (score > best_score - 1e-6 && patch < best_patch)) {
+    if (score > best_score * (1 + 1e-9) ||
+        (score > best_score * (1 - 1e-9) && patch < best_patch)) {
       best_score = score;
       best_patch = patch;
       p.TH = th;
@@ -681,7 +727,7 @@ size_t configure(FfmaParams& p, int ks, bool fine) {
 // co-resident clusters of ks CTAs at ~200 KB smem (GPC-limited); cached
 template <class K>
 int cluster_slots(K kernel, int ks, int sms, int threads) {
-  static int cache[9] = {0};
+  static int cache[kMaxKs + 1] = {0};
   if (ks == 1) return sms;
   if (!cache[ks]) {
     cudaLaunchConfig_t cfg{};
@@ -745,7 +791,20 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int co_groups = (p.jb_count + CG - 1) / CG;
-  pick_tile(p, BM, BN, co_groups, sms);
+  auto kernel = conv_ffma_kernel<BM, BN, WF, NW, TPX, TCO>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr_set = true;
+  }
+  // only the 8-warp 8x8-per-thread tile has the DSMEM split-K reduction
+  const bool no_split = getenv("DCONV_NO_SPLITK") != nullptr || NW != 8 || TPX != 8 || TCO != 8;
+  int slots[kMaxKs + 1] = {0};
+  slots[1] = sms;
+  if (!no_split)
+    for (int ks = 2; ks <= kMaxKs; ++ks) slots[ks] = cluster_slots(kernel, ks, sms, threads);
+  pick_tile(p, BM, BN, co_groups, sms, slots, !no_split);
   p.TWe = std::min(p.TW, p.w_o);
   // q / TW for q < BM by multiply-high (exact: BM * TW < 2^32)
   p.tw_magic = (unsigned)(((uint64_t(1) << 32) + p.TW - 1) / p.TW);
@@ -754,41 +813,28 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   const int units = p.tiles_y * p.tiles_x * co_groups;
   const bool fine = (int64_t)units * 2 < sms;  // batch-1 layers: split-K over fine stages
 
-  auto kernel = conv_ffma_kernel<BM, BN, WF, NW, TPX, TCO>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_set = true;
-  }
   FfmaParams q = p;
   if (!configure<BN, NW, TPX, TCO>(q, 1, fine))
     return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_ffma: stage does not fit smem twice");
   const int S = q.n_g * q.n_r;
-  // the 12-warp variant's partial buffer (96 KB) leaves no room for a ring:
-  // it never splits K
-  const bool no_split = getenv("DCONV_NO_SPLITK") != nullptr || NW != 8 || TPX != 8 || TCO != 8;
 
-  // (1) fewer units than SMs (batch 1): one split-K launch.  The persistent schedule
-  // runs ceil(units / slots) rounds of ceil(S / ks) stages (+ a DSMEM
-  // reduction); pick the cheapest ks.
+  // (1) fewer units than SMs (batch 1): one split-K launch with the cheapest
+  // cluster size (the same cycle model as the tile selector).
   int best_ks = 1;
-  double best_cost = (double)((units + sms - 1) / sms) * S;
-  for (int ks = 2; ks <= 8 && ks <= S && !no_split && units < sms; ks *= 2) {
-    const int slots = cluster_slots(kernel, ks, sms, threads);
-    if (slots < 1) continue;
-    const double cost = (double)((units + slots - 1) / slots) *
-                        ((S + ks - 1) / ks + 0.35 + 0.05 * ks);
-    if (cost < best_cost - 1e-9) {
-      best_cost = cost;
-      best_ks = ks;
-    }
+  if (units < sms && !no_split) {
+    FfmaParams t = p;
+    if (configure<BN, NW, TPX, TCO>(t, 2, true))
+      best_ks = best_split(units, slots, t.n_g * t.n_r, unit_cycles(p, BM, BN), nullptr);
   }
-  if (const char* e = getenv("DCONV_KSPLIT")) best_ks = std::max(1, std::min(atoi(e), std::min(8, S)));
+  if (const char* e = getenv("DCONV_KSPLIT")) best_ks = std::max(1, std::min(atoi(e), std::min(kMaxKs, S)));
   if (best_ks > 1) {
     FfmaParams r = p;
     const size_t smem = configure<BN, NW, TPX, TCO>(r, best_ks, true);
     if (!smem) return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_ffma: split stage");
     const int clusters = std::min(units, std::max(1, cluster_slots(kernel, best_ks, sms, threads)));
+    if (getenv("DCONV_DEBUG"))
+      fprintf(stderr, "conv_ffma<%d,%d,%d>: split TH=%d TW=%d units=%d ks=%d clusters=%d S=%d\n",
+              BM, BN, WF, r.TH, r.TW, units, best_ks, clusters, r.n_g * r.n_r);
     return launch_units(kernel, threads, r, smem, 0, units, clusters, stream);
   }
 
@@ -800,7 +846,7 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   if (main_units > 0 && tail > 0 && tail * 4 < sms * 3 && !no_split &&
       !getenv("DCONV_NO_TAILSPLIT")) {
     static const bool pow2_only = getenv("DCONV_TAIL_POW2") != nullptr;
-    for (int ks = 8; ks >= 2; ks = pow2_only ? ks / 2 : ks - 1) {
+    for (int ks = kMaxKs; ks >= 2; ks = pow2_only ? ks / 2 : ks - 1) {
       FfmaParams t = p;
       if (!configure<BN, NW, TPX, TCO>(t, ks, true)) continue;
       if (ks > t.n_g * t.n_r) continue;
@@ -813,7 +859,7 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   }
   const size_t smem_main = configure<BN, NW, TPX, TCO>(q, 1, fine);
   if (getenv("DCONV_DEBUG") && tail_ks > 1)
-    for (int ks = 2; ks <= 8; ++ks)
+    for (int ks = 2; ks <= kMaxKs; ++ks)
       fprintf(stderr, "  cluster_slots(%d) = %d\n", ks, cluster_slots(kernel, ks, sms, threads));
   if (getenv("DCONV_DEBUG"))
     fprintf(stderr,

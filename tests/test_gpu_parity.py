@@ -532,7 +532,7 @@ def test_co_shard_peer_gather_plan_world1():
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("ks", [2, 3, 4, 6, 8])
+@pytest.mark.parametrize("ks", [2, 3, 4, 6, 8, 12, 16])
 def test_cluster_split_k(ks, monkeypatch):
     """Split-K over a thread-block cluster with the DSMEM reduction, forced
     to ks CTAs per unit: several units per cluster (barrier phases), ragged
