@@ -6,11 +6,13 @@
 //
 // CTA: 256 threads = 32 pixel groups x 8 output blocks (64 channels).  A
 // pixel group is 8 consecutive output pixels of one row; each thread keeps an
-// 8-pixel x 8-channel accumulator tile (FFMA2 pairs).  The CTA stages its
-// input patch (all C_i planes, zero-filled outside the image) and the weights
-// of its 8 output blocks in shared memory once, then for every (c, n) loads a
-// register row segment of 7*S + WF input values and reuses it across the WF
-// filter columns (s*(k'*w_ob + kk) + m indexing).
+// 8-pixel x 8-channel accumulator tile (FFMA2 pairs).  The CTA stages the
+// weights of its 8 output blocks in shared memory once and then walks its
+// pixel tiles persistently: while it computes tile i from one patch buffer
+// (all C_i planes, zero-filled outside the image), cp.async fills the other
+// with tile i+1.  For every (c, n) a thread loads a register row segment of
+// 7*S + WF input values and reuses it across the WF filter columns
+// (s*(k'*w_ob + kk) + m indexing).
 #include <algorithm>
 
 #include "common.cuh"
@@ -30,23 +32,21 @@ struct FirstTile {
 };
 
 template <int S, int WF>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 2)
     conv_first_kernel(const GenericParams p, const FirstTile t) {
   extern __shared__ __align__(16) float smem[];
   const int taps_c = p.h_f * WF * p.c_i;  // (n, m, c) rows of the weight tile
   float* sw = smem;                                   // [taps_c][2][kCG][4]
-  float* sp = smem + taps_c * kCG * 8;                // [c_i][PH][PWs]
+  const int patch_floats = (p.c_i * t.PH * t.PWs + 3) & ~3;
+  float* sp0 = smem + taps_c * kCG * 8;               // 2 x [c_i][PH][PWs]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tiles_img = t.tiles_x * t.tiles_y;
-  const int img = blockIdx.x / tiles_img;
-  const int tile = blockIdx.x - img * tiles_img;
-  const int y0 = (tile / t.tiles_x) * t.TH;
-  const int x0 = (tile % t.tiles_x) * t.CX * 8;
+  const int n_tiles = tiles_img * p.n;
   const int jb0 = p.jb_begin + blockIdx.y * kCG;
   const int cg_valid = min(kCG, p.jb_begin + p.jb_count - jb0);
 
-  // ---- stage weights: global [jb][n][m][c][8] -> smem [(n,m,c)][half][cb][4]
+  // ---- stage weights once: global [jb][n][m][c][8] -> smem [(n,m,c)][half][cb][4]
   for (int e = tid; e < taps_c * kCG * 2; e += 256) {
     const int half = e & 1;
     const int cb = (e >> 1) % kCG;
@@ -57,96 +57,115 @@ __global__ void __launch_bounds__(256)
                                            half * 4);
     *reinterpret_cast<float4*>(sw + ((row * 2 + half) * kCG + cb) * 4) = v;
   }
-  // ---- stage the input patch (zero outside the image)
-  const float* in = p.in + (int64_t)img * p.in_img;
-  const int iy0 = y0 * S, ix0 = x0 * S;
-  const int patch = p.c_i * t.PH * t.PW;
-  for (int e = tid; e < patch; e += 256) {
-    const int col = e % t.PW;
-    const int rc = e / t.PW;
-    const int row = rc % t.PH, c = rc / t.PH;
-    const int gy = iy0 + row, gx = ix0 + col;
-    float v = 0.f;
-    if (gy < p.h_i && gx < p.w_i)
-      v = in[(int64_t)c * p.in_blk + (int64_t)gy * p.in_row + gx];
-    sp[(c * t.PH + row) * t.PWs + col] = v;
-  }
-  __syncthreads();
+  // ---- async patch staging (zero outside the image)
+  auto stage = [&](int tile, float* sp) {
+    const int img = tile / tiles_img, tt = tile - img * tiles_img;
+    const int iy0 = (tt / t.tiles_x) * t.TH * S, ix0 = (tt % t.tiles_x) * t.CX * 8 * S;
+    const float* in = p.in + (int64_t)img * p.in_img;
+    const int patch = p.c_i * t.PH * t.PW;
+    for (int e = tid; e < patch; e += 256) {
+      const int col = e % t.PW;
+      const int rc = e / t.PW;
+      const int row = rc % t.PH, c = rc / t.PH;
+      const int gy = iy0 + row, gx = ix0 + col;
+      const bool ok = gy < p.h_i && gx < p.w_i;
+      cp_async4(sp + (c * t.PH + row) * t.PWs + col,
+                ok ? in + (int64_t)c * p.in_blk + (int64_t)gy * p.in_row + gx : p.in, ok);
+    }
+    cp_async_commit();
+  };
 
-  // ---- compute: pixel group pg = (row r, column group cx); block cb
   const int pg = (lane & 3) + 4 * warp;
   const int cb = lane >> 2;
   const int r = pg % t.TH, cx = pg / t.TH;
   const bool active = cx < t.CX;
-  uint64_t acc[8][4];
-#pragma unroll
-  for (int j = 0; j < 8; ++j)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[j][q] = 0ull;
 
-  if (active) {
-    constexpr int L = 7 * S + WF;  // input columns feeding 8 pixels x WF taps
-    for (int c = 0; c < p.c_i; ++c) {
-      for (int n = 0; n < p.h_f; ++n) {
-        const float* row = sp + (c * t.PH + r * S + n) * t.PWs + cx * 8 * S;
-        float seg[L];
+  int buf = 0;
+  if ((int)blockIdx.x < n_tiles) stage(blockIdx.x, sp0);
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, buf ^= 1) {
+    const int next = tile + gridDim.x;
+    if (next < n_tiles) {
+      stage(next, sp0 + (buf ^ 1) * patch_floats);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();  // this tile's patch (and, first time, the weights) visible
+    const float* sp = sp0 + buf * patch_floats;
+    const int img = tile / tiles_img, tt = tile - img * tiles_img;
+    const int y0 = (tt / t.tiles_x) * t.TH, x0 = (tt % t.tiles_x) * t.CX * 8;
+
+    // ---- compute: pixel group pg = (row r, column group cx); block cb
+    uint64_t acc[8][4];
 #pragma unroll
-        for (int i = 0; i < L; ++i) seg[i] = row[i];
-        const float* wrow = sw + ((n * WF) * p.c_i + c) * (2 * kCG * 4) + cb * 4;
+    for (int j = 0; j < 8; ++j)
 #pragma unroll
-        for (int m = 0; m < WF; ++m) {
-          const float* wp = wrow + m * p.c_i * (2 * kCG * 4);
-          const float4 b0 = lds128(wp);
-          const float4 b1 = lds128(wp + kCG * 4);
-          const uint64_t bp0 = pack2(b0.x, b0.y), bp1 = pack2(b0.z, b0.w);
-          const uint64_t bp2 = pack2(b1.x, b1.y), bp3 = pack2(b1.z, b1.w);
+      for (int q = 0; q < 4; ++q) acc[j][q] = 0ull;
+    if (active) {
+      constexpr int L = 7 * S + WF;  // input columns feeding 8 pixels x WF taps
+      for (int c = 0; c < p.c_i; ++c) {
+        for (int n = 0; n < p.h_f; ++n) {
+          const float* row = sp + (c * t.PH + r * S + n) * t.PWs + cx * 8 * S;
+          float seg[L];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float a = seg[j * S + m];
-            ffma2(acc[j][0], a, bp0);
-            ffma2(acc[j][1], a, bp1);
-            ffma2(acc[j][2], a, bp2);
-            ffma2(acc[j][3], a, bp3);
+          for (int i = 0; i < L; ++i) seg[i] = row[i];
+          const float* wrow = sw + ((n * WF) * p.c_i + c) * (2 * kCG * 4) + cb * 4;
+#pragma unroll
+          for (int m = 0; m < WF; ++m) {
+            const float* wp = wrow + m * p.c_i * (2 * kCG * 4);
+            const float4 b0 = lds128(wp);
+            const float4 b1 = lds128(wp + kCG * 4);
+            const uint64_t bp0 = pack2(b0.x, b0.y), bp1 = pack2(b0.z, b0.w);
+            const uint64_t bp2 = pack2(b1.x, b1.y), bp3 = pack2(b1.z, b1.w);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float a = seg[j * S + m];
+              ffma2(acc[j][0], a, bp0);
+              ffma2(acc[j][1], a, bp1);
+              ffma2(acc[j][2], a, bp2);
+              ffma2(acc[j][3], a, bp3);
+            }
           }
         }
       }
     }
-  }
-  if (!active || cb >= cg_valid) return;
-  const int y = y0 + r;
-  if (y >= p.h_o) return;
-  const int jl = jb0 + cb - p.jb_begin;
-  float* obase = p.out + (int64_t)img * p.out_img + (int64_t)jl * p.out_blk +
-                 (int64_t)y * p.out_row;
-  const float* sbase = p.skip ? p.skip + (int64_t)img * p.sk_img + (int64_t)jl * p.sk_blk +
-                                    (int64_t)y * p.sk_row
-                              : nullptr;
+    __syncthreads();  // everyone is done with this buffer before it is refilled
+
+    const int y = y0 + r;
+    if (!active || cb >= cg_valid || y >= p.h_o) continue;
+    const int jl = jb0 + cb - p.jb_begin;
+    float* obase = p.out + (int64_t)img * p.out_img + (int64_t)jl * p.out_blk +
+                   (int64_t)y * p.out_row;
+    const float* sbase = p.skip ? p.skip + (int64_t)img * p.sk_img + (int64_t)jl * p.sk_blk +
+                                      (int64_t)y * p.sk_row
+                                : nullptr;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const int x = x0 + cx * 8 + j;
-    if (x >= p.w_o) break;
-    const float2 c0 = unpack2(acc[j][0]), c1 = unpack2(acc[j][1]);
-    const float2 c2 = unpack2(acc[j][2]), c3 = unpack2(acc[j][3]);
-    float4 v0 = make_float4(c0.x, c0.y, c1.x, c1.y);
-    float4 v1 = make_float4(c2.x, c2.y, c3.x, c3.y);
-    if (p.epi & DCONV_EPI_ADD) {
-      const float4 s0 = *reinterpret_cast<const float4*>(sbase + x * 8);
-      const float4 s1 = *reinterpret_cast<const float4*>(sbase + x * 8 + 4);
-      v0.x += s0.x; v0.y += s0.y; v0.z += s0.z; v0.w += s0.w;
-      v1.x += s1.x; v1.y += s1.y; v1.z += s1.z; v1.w += s1.w;
-    }
-    if (p.epi & DCONV_EPI_RELU) {
-      v0.x = fmaxf(v0.x, 0.f); v0.y = fmaxf(v0.y, 0.f);
-      v0.z = fmaxf(v0.z, 0.f); v0.w = fmaxf(v0.w, 0.f);
-      v1.x = fmaxf(v1.x, 0.f); v1.y = fmaxf(v1.y, 0.f);
-      v1.z = fmaxf(v1.z, 0.f); v1.w = fmaxf(v1.w, 0.f);
-    }
-    *reinterpret_cast<float4*>(obase + x * 8) = v0;
-    *reinterpret_cast<float4*>(obase + x * 8 + 4) = v1;
-    for (int q = 0; q < p.n_peers; ++q) {  // fused C_o-shard gather
-      float* po = p.peer_out[q] + (obase - p.out) + x * 8;
-      *reinterpret_cast<float4*>(po) = v0;
-      *reinterpret_cast<float4*>(po + 4) = v1;
+    for (int j = 0; j < 8; ++j) {
+      const int x = x0 + cx * 8 + j;
+      if (x >= p.w_o) break;
+      const float2 c0 = unpack2(acc[j][0]), c1 = unpack2(acc[j][1]);
+      const float2 c2 = unpack2(acc[j][2]), c3 = unpack2(acc[j][3]);
+      float4 v0 = make_float4(c0.x, c0.y, c1.x, c1.y);
+      float4 v1 = make_float4(c2.x, c2.y, c3.x, c3.y);
+      if (p.epi & DCONV_EPI_ADD) {
+        const float4 s0 = *reinterpret_cast<const float4*>(sbase + x * 8);
+        const float4 s1 = *reinterpret_cast<const float4*>(sbase + x * 8 + 4);
+        v0.x += s0.x; v0.y += s0.y; v0.z += s0.z; v0.w += s0.w;
+        v1.x += s1.x; v1.y += s1.y; v1.z += s1.z; v1.w += s1.w;
+      }
+      if (p.epi & DCONV_EPI_RELU) {
+        v0.x = fmaxf(v0.x, 0.f); v0.y = fmaxf(v0.y, 0.f);
+        v0.z = fmaxf(v0.z, 0.f); v0.w = fmaxf(v0.w, 0.f);
+        v1.x = fmaxf(v1.x, 0.f); v1.y = fmaxf(v1.y, 0.f);
+        v1.z = fmaxf(v1.z, 0.f); v1.w = fmaxf(v1.w, 0.f);
+      }
+      *reinterpret_cast<float4*>(obase + x * 8) = v0;
+      *reinterpret_cast<float4*>(obase + x * 8 + 4) = v1;
+      for (int q = 0; q < p.n_peers; ++q) {  // fused C_o-shard gather
+        float* po = p.peer_out[q] + (obase - p.out) + x * 8;
+        *reinterpret_cast<float4*>(po) = v0;
+        *reinterpret_cast<float4*>(po + 4) = v1;
+      }
     }
   }
 }
@@ -165,7 +184,7 @@ FirstTile pick_first_tile(const GenericParams& p, size_t w_bytes, size_t budget)
     const int pw = (cx * 8 - 1) * p.s + p.w_f;
     const int pws = pw | 1;  // odd row stride: rows of a warp hit distinct banks
     const size_t patch = (size_t)p.c_i * ph * pws * 4;
-    if (w_bytes + patch > budget) continue;
+    if (w_bytes + 2 * patch > budget) continue;  // double-buffered
     const double eff = (double)p.h_o * p.w_o / ((double)tx * ty * kPGN * 8);
     if (eff > best_eff + 1e-9 || (eff > best_eff - 1e-9 && patch < best_patch)) {
       best = FirstTile{cx, th, tx, ty, ph, pw, pws};
@@ -179,18 +198,33 @@ FirstTile pick_first_tile(const GenericParams& p, size_t w_bytes, size_t budget)
 template <int S, int WF>
 int launch_first(const GenericParams& p, cudaStream_t stream) {
   const size_t w_bytes = (size_t)p.h_f * WF * p.c_i * kCG * 8 * 4;
-  const size_t budget = 200 * 1024;
+  const size_t budget = 220 * 1024;
   const FirstTile t = pick_first_tile(p, w_bytes, budget);
   if (t.CX == 0) return DCONV_EUNSUPPORTED;
-  const size_t smem = w_bytes + (size_t)p.c_i * t.PH * t.PWs * 4;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(conv_first_kernel<S, WF>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
+  const size_t patch = (((size_t)p.c_i * t.PH * t.PWs + 3) & ~size_t(3)) * 4;
+  const size_t smem = w_bytes + 2 * patch;  // weights + double-buffered patch
+  auto kernel = conv_first_kernel<S, WF>;
+  static int per_sm = 0, sms = 0;
+  if (!per_sm) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    per_sm = -1;
   }
-  dim3 grid((unsigned)(t.tiles_x * t.tiles_y * p.n), (unsigned)((p.jb_count + kCG - 1) / kCG));
-  conv_first_kernel<S, WF><<<grid, 256, smem, stream>>>(p, t);
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, smem) != cudaSuccess ||
+      occ < 1) {
+    cudaGetLastError();
+    return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_first: %zu B smem per CTA", smem);
+  }
+  const int co_groups = (p.jb_count + kCG - 1) / kCG;
+  const int n_tiles = t.tiles_x * t.tiles_y * p.n;
+  // persistent: enough CTAs to fill every SM's resident slots, split over
+  // the output-block groups
+  const int slots = std::max(1, sms * occ / co_groups);
+  dim3 grid((unsigned)std::min(n_tiles, slots), (unsigned)co_groups);
+  kernel<<<grid, 256, smem, stream>>>(p, t);
   dconv_host::count_launch();
   return dconv_host::check_launch("conv_first_kernel");
 }

@@ -1,5 +1,6 @@
 """Runs one conv layer a few times (for ncu / compute-sanitizer captures).
-usage: python tools/one_layer.py CI CO HI WI F S N [reps] [ffma|tf32]"""
+usage: python tools/one_layer.py CI CO HI WI F S N [reps] [ffma|tf32|first]
+(first: the first-layer reader on a dense [N][CI][HI][WI] input)"""
 import sys
 
 import torch
@@ -10,10 +11,13 @@ from paper_1809_10170_b200 import nets  # noqa: E402
 ci, co, hi, wi, f, s, n = (int(v) for v in sys.argv[1:8])
 reps = int(sys.argv[8]) if len(sys.argv) > 8 else 3
 algo = sys.argv[9] if len(sys.argv) > 9 else "ffma"
-l = nets.Layer("one", ci, co, hi, wi, f, f, s)
-x = nets.Act(n, ci, hi, wi)
-x.buf.uniform_(-1, 1)
-w = nets.pack_weights(torch.empty((ci, co, f, f), device="cuda").uniform_(-1, 1), False)
+l = nets.Layer("one", ci, co, hi, wi, f, f, s, algo == "first")
+if algo == "first":
+    x = torch.empty((n, ci, hi, wi), device="cuda").uniform_(-1, 1)
+else:
+    x = nets.Act(n, ci, hi, wi)
+    x.buf.uniform_(-1, 1)
+w = nets.pack_weights(torch.empty((ci, co, f, f), device="cuda").uniform_(-1, 1), l.first)
 y = nets.Act(n, co, l.h_o, l.w_o)
 if algo == "tf32":
     wp = nets.prepare_tf32(l, w)
