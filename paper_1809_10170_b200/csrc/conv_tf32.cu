@@ -27,6 +27,8 @@
 // stated separately (tests/test_gpu_parity.py::test_tf32_*).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <vector>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -61,6 +63,8 @@ struct Tf32Params {
   int row_groups, strips, units;
   int MT;             // M-tiles per unit (1..4)
   uint32_t idesc;
+  unsigned long long* dbg;  // DCONV_TF32_PROFILE: per-CTA wait cycles (else null)
+  int noload;               // DCONV_TF32_NOLOAD (timing experiment only): skip refills
 };
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -88,6 +92,28 @@ __device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t a, uint64_t 
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Issued by one elected lane of a converged warp (elect.sync); the
+// descriptors come in as 32-bit halves so the loop arithmetic stays 32-bit.
+__device__ __forceinline__ void umma_tf32_elect(uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi,
+                                                uint32_t b_lo, uint32_t b_hi, uint32_t idesc,
+                                                uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred e, p;\n.reg .b64 ad, bd;\n"
+      "mov.b64 ad, {%1, %2};\nmov.b64 bd, {%3, %4};\n"
+      "setp.ne.b32 p, %6, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ad, bd, %5, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+          smem_u32(bar))
       : "memory");
 }
 
@@ -170,7 +196,11 @@ __global__ void __launch_bounds__(kThreadsT, 1)
         decode(u, img, y0, x0, cg);
         for (int st = 0; st < S; ++st, ++gs) {
           const int buf = gs % p.NS;
-          if (gs >= p.NS) mbar_wait(&empty[buf], ((gs / p.NS) - 1) & 1);
+          if (gs >= p.NS) {
+            const long long t0 = p.dbg ? clock64() : 0;
+            mbar_wait_backoff(&empty[buf], ((gs / p.NS) - 1) & 1, 64);
+            if (p.dbg) p.dbg[blockIdx.x * 4 + 0] += clock64() - t0;
+          }
           const int g = st / p.n_r, r = st - g * p.n_r;
           const int ib0 = g * p.G, n0 = r * p.R;
           const int Ge = min(p.G, p.ib_n - ib0), Re = min(p.R, p.h_f - n0);
@@ -178,6 +208,10 @@ __global__ void __launch_bounds__(kThreadsT, 1)
           // the TMA box always lands whole (OOB elements zero-filled)
           const uint32_t patch_bytes = 2u * (uint32_t)(p.G * p.PH * p.PW * 4) * 4u;
           const uint32_t wbytes = (uint32_t)(Ge * Re * p.w_f * 2 * p.N * 4) * 4u;
+          if (p.noload && gs >= p.NS) {
+            mbar_arrive(&full[buf]);
+            continue;
+          }
           mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes);
           tma_load_5d(sp, &tmap, 0, 0, x0, y0 + n0, img * p.ib_n + ib0, &full[buf]);
           tma_load_5d(sp + p.plane_floats, &tmap, 0, 1, x0, y0 + n0, img * p.ib_n + ib0,
@@ -196,11 +230,19 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       decode(u, img, y0, x0, cg);
       const int valid_rows = min(p.MT * kTileRows, p.h_o - y0);
       const int mts = (valid_rows + kTileRows - 1) / kTileRows;
-      if (ui > 0) mbar_wait(acc_empty, (ui - 1) & 1);  // epilogue drained TMEM
+      if (ui > 0) {
+        const long long t0 = p.dbg ? clock64() : 0;
+        mbar_wait(acc_empty, (ui - 1) & 1);  // epilogue drained TMEM
+        if (p.dbg && lane == 0) p.dbg[blockIdx.x * 4 + 2] += clock64() - t0;
+      }
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       for (int st = 0; st < S; ++st, ++gs) {
         const int buf = gs % p.NS;
-        mbar_wait(&full[buf], (gs / p.NS) & 1);
+        {
+          const long long t0 = p.dbg ? clock64() : 0;
+          mbar_wait(&full[buf], (gs / p.NS) & 1);
+          if (p.dbg && lane == 0) p.dbg[blockIdx.x * 4 + 1] += clock64() - t0;
+        }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int g = st / p.n_r, r = st - g * p.n_r;
         const int Ge = min(p.G, p.ib_n - g * p.G);
@@ -208,25 +250,33 @@ __global__ void __launch_bounds__(kThreadsT, 1)
         const float* sp = smem + buf * p.stage_floats;
         const uint32_t a_base = smem_u32(sp);
         const uint32_t b_base = smem_u32(sp + 2 * p.plane_floats);
-        if (lane == 0) {
-          for (int gi = 0; gi < Ge; ++gi)
-            for (int n = 0; n < Re; ++n)
-              for (int m = 0; m < p.w_f; ++m) {
-                const uint64_t bdesc = umma_desc(
-                    b_base + (uint32_t)((((gi * p.R + n) * p.w_f + m) * 2) * p.N * 16),
-                    (uint32_t)(p.N * 16), 128u);
-                const bool first = (st == 0 && gi == 0 && n == 0 && m == 0);
-                for (int mt = 0; mt < mts; ++mt) {
-                  const uint64_t adesc = umma_desc(
-                      a_base + (uint32_t)(((gi * p.PH + mt * kTileRows + n) * p.PW + m) * 16),
-                      (uint32_t)(p.plane_floats * 4), (uint32_t)(p.PW * 16));
-                  umma_tf32(tmem_base + (uint32_t)(mt * p.N), adesc, bdesc, p.idesc,
-                            first ? 0u : 1u);
-                }
-              }
-          umma_commit(&empty[buf]);  // stage smem free once these MMAs retire
-          if (st == S - 1) umma_commit(acc_full);
-        }
+        // The whole warp walks the taps (every value is warp-uniform, so it
+        // stays in the uniform datapath); one elected lane issues each MMA.
+        // A descriptor's low word (start >> 4 | LBO >> 4 << 16) advances by
+        // the byte offset >> 4 (smem < 256 KB: no carry), the high word
+        // (SBO, version) is fixed -- a 32-bit add per MMA.
+        const uint32_t a_lo0 = ((a_base >> 4) & 0x3FFFu) | (((uint32_t)(p.plane_floats * 4) >> 4) << 16);
+        const uint32_t a_hi = ((uint32_t)(p.PW * 16) >> 4) | (1u << 14);
+        const uint32_t b_lo0 = ((b_base >> 4) & 0x3FFFu) | (((uint32_t)(p.N * 16) >> 4) << 16);
+        const uint32_t b_hi = (128u >> 4) | (1u << 14);
+        const uint32_t a_mt = (uint32_t)(kTileRows * p.PW);  // next M-tile (16 B units)
+        const uint32_t b_tap = (uint32_t)(2 * p.N);          // next (n, m) tap
+        uint32_t accum = st == 0 ? 0u : 1u;
+        for (int gi = 0; gi < Ge; ++gi)
+          for (int n = 0; n < Re; ++n) {
+            const uint32_t arow = a_lo0 + (uint32_t)((gi * p.PH + n) * p.PW);
+            const uint32_t brow = b_lo0 + (uint32_t)((gi * p.R + n) * p.w_f) * b_tap;
+            for (int m = 0; m < p.w_f; ++m) {
+              const uint32_t blo = brow + (uint32_t)m * b_tap;
+              uint32_t alo = arow + (uint32_t)m;
+              for (int mt = 0; mt < mts; ++mt, alo += a_mt)
+                umma_tf32_elect(tmem_base + (uint32_t)(mt * p.N), alo, a_hi, blo, b_hi, p.idesc,
+                                accum);
+              accum = 1u;
+            }
+          }
+        umma_commit_elect(&empty[buf]);  // stage smem free once these MMAs retire
+        if (st == S - 1) umma_commit_elect(acc_full);
         __syncwarp();
       }
     }
@@ -239,7 +289,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
     for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++ui) {
       int img, y0, x0, cg;
       decode(u, img, y0, x0, cg);
-      mbar_wait(acc_full, ui & 1);
+      mbar_wait_backoff(acc_full, ui & 1, 256);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int x = x0 + tx;
       for (int mt = 0; mt < p.MT; ++mt) {
@@ -279,6 +329,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
     }
   }
 
+  if (p.dbg && threadIdx.x == 32) p.dbg[blockIdx.x * 4 + 3] = (unsigned long long)clock64();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) {
@@ -455,6 +506,28 @@ int launch_conv_tf32(const FfmaParams& f, const float* w_prepared, cudaStream_t 
   }
   const size_t smem = (size_t)p.NS * stage_bytes + bar_bytes;
   const int grid = std::min(p.units, sms);
+  static const bool prof = getenv("DCONV_TF32_PROFILE") != nullptr;
+  p.noload = getenv("DCONV_TF32_NOLOAD") != nullptr;
+  if (prof) {  // debugging aid: where do the roles wait?  (not for timed runs)
+    cudaMalloc(&p.dbg, (size_t)grid * 4 * 8);
+    cudaMemsetAsync(p.dbg, 0, (size_t)grid * 4 * 8, stream);
+    long long start = 0;
+    conv_tf32_kernel<<<grid, kThreadsT, smem, stream>>>(map, p);
+    std::vector<unsigned long long> h((size_t)grid * 4);
+    cudaMemcpy(h.data(), p.dbg, h.size() * 8, cudaMemcpyDeviceToHost);
+    double w_empty = 0, w_full = 0, w_acc = 0;
+    for (int b = 0; b < grid; ++b) {
+      w_empty += h[b * 4]; w_full += h[b * 4 + 1]; w_acc += h[b * 4 + 2];
+    }
+    (void)start;
+    fprintf(stderr,
+            "conv_tf32 N=%d MT=%d G=%d R=%d NS=%d stage=%d B units=%d S=%d: per CTA avg wait "
+            "cycles producer(empty)=%.0f mma(full)=%.0f mma(acc_empty)=%.0f\n",
+            p.N, p.MT, p.G, p.R, p.NS, stage_bytes, p.units, p.n_g * p.n_r, w_empty / grid,
+            w_full / grid, w_acc / grid);
+    cudaFree(p.dbg);
+    p.dbg = nullptr;
+  }
   conv_tf32_kernel<<<grid, kThreadsT, smem, stream>>>(map, p);
   dconv_host::count_launch();
   return dconv_host::check_launch("conv_tf32_kernel");
