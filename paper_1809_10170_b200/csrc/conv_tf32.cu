@@ -142,6 +142,9 @@ __device__ __forceinline__ void tmem_ld32x32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// WF_T / MT_T: filter width and M-tiles per unit as compile-time constants
+// (0 = runtime), so the per-stage MMA walk unrolls into straight-line issue.
+template <int WF_T, int MT_T>
 __global__ void __launch_bounds__(kThreadsT, 1)
     conv_tf32_kernel(const __grid_constant__ CUtensorMap tmap, const Tf32Params p) {
   extern __shared__ __align__(1024) float smem[];
@@ -262,11 +265,32 @@ __global__ void __launch_bounds__(kThreadsT, 1)
         const uint32_t a_mt = (uint32_t)(kTileRows * p.PW);  // next M-tile (16 B units)
         const uint32_t b_tap = (uint32_t)(2 * p.N);          // next (n, m) tap
         uint32_t accum = st == 0 ? 0u : 1u;
+        const int wf = WF_T > 0 ? WF_T : p.w_f;
         for (int gi = 0; gi < Ge; ++gi)
           for (int n = 0; n < Re; ++n) {
             const uint32_t arow = a_lo0 + (uint32_t)((gi * p.PH + n) * p.PW);
-            const uint32_t brow = b_lo0 + (uint32_t)((gi * p.R + n) * p.w_f) * b_tap;
-            for (int m = 0; m < p.w_f; ++m) {
+            const uint32_t brow = b_lo0 + (uint32_t)((gi * p.R + n) * wf) * b_tap;
+            if (MT_T > 0 && mts == MT_T) {
+#pragma unroll
+              for (int m = 0; m < (WF_T > 0 ? WF_T : 1); ++m) {
+#pragma unroll
+                for (int mt = 0; mt < MT_T; ++mt)
+                  umma_tf32_elect(tmem_base + (uint32_t)(mt * p.N),
+                                  arow + (uint32_t)m + (uint32_t)mt * a_mt, a_hi,
+                                  brow + (uint32_t)m * b_tap, b_hi, p.idesc, accum);
+                accum = 1u;
+              }
+              if (WF_T > 0) continue;
+              for (int m = 1; m < wf; ++m) {
+#pragma unroll
+                for (int mt = 0; mt < MT_T; ++mt)
+                  umma_tf32_elect(tmem_base + (uint32_t)(mt * p.N),
+                                  arow + (uint32_t)m + (uint32_t)mt * a_mt, a_hi,
+                                  brow + (uint32_t)m * b_tap, b_hi, p.idesc, 1u);
+              }
+              continue;
+            }
+            for (int m = 0; m < wf; ++m) {
               const uint32_t blo = brow + (uint32_t)m * b_tap;
               uint32_t alo = arow + (uint32_t)m;
               for (int mt = 0; mt < mts; ++mt, alo += a_mt)
@@ -379,6 +403,17 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 }  // namespace
+
+using Tf32Kernel = void (*)(const CUtensorMap, const Tf32Params);
+Tf32Kernel pick_tf32_kernel(const Tf32Params& p) {
+  static const Tf32Kernel k3[4] = {conv_tf32_kernel<3, 1>, conv_tf32_kernel<3, 2>,
+                                   conv_tf32_kernel<3, 3>, conv_tf32_kernel<3, 4>};
+  static const Tf32Kernel k1[4] = {conv_tf32_kernel<1, 1>, conv_tf32_kernel<1, 2>,
+                                   conv_tf32_kernel<1, 3>, conv_tf32_kernel<1, 4>};
+  if (p.w_f == 3) return k3[p.MT - 1];
+  if (p.w_f == 1) return k1[p.MT - 1];
+  return conv_tf32_kernel<0, 0>;
+}
 
 int tf32_channels(int jb_count) { return jb_count * 8 >= 128 ? 128 : (jb_count * 8 > 64 ? 128 : 64); }
 
@@ -497,8 +532,10 @@ int launch_conv_tf32(const FfmaParams& f, const float* w_prepared, cudaStream_t 
   static int sms = 0;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(conv_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         227 * 1024);
+    for (auto k : {conv_tf32_kernel<0, 0>, conv_tf32_kernel<3, 1>, conv_tf32_kernel<3, 2>,
+                   conv_tf32_kernel<3, 3>, conv_tf32_kernel<3, 4>, conv_tf32_kernel<1, 1>,
+                   conv_tf32_kernel<1, 2>, conv_tf32_kernel<1, 3>, conv_tf32_kernel<1, 4>})
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -512,7 +549,7 @@ int launch_conv_tf32(const FfmaParams& f, const float* w_prepared, cudaStream_t 
     cudaMalloc(&p.dbg, (size_t)grid * 4 * 8);
     cudaMemsetAsync(p.dbg, 0, (size_t)grid * 4 * 8, stream);
     long long start = 0;
-    conv_tf32_kernel<<<grid, kThreadsT, smem, stream>>>(map, p);
+    pick_tf32_kernel(p)<<<grid, kThreadsT, smem, stream>>>(map, p);
     std::vector<unsigned long long> h((size_t)grid * 4);
     cudaMemcpy(h.data(), p.dbg, h.size() * 8, cudaMemcpyDeviceToHost);
     double w_empty = 0, w_full = 0, w_acc = 0;
@@ -528,7 +565,7 @@ int launch_conv_tf32(const FfmaParams& f, const float* w_prepared, cudaStream_t 
     cudaFree(p.dbg);
     p.dbg = nullptr;
   }
-  conv_tf32_kernel<<<grid, kThreadsT, smem, stream>>>(map, p);
+  pick_tf32_kernel(p)<<<grid, kThreadsT, smem, stream>>>(map, p);
   dconv_host::count_launch();
   return dconv_host::check_launch("conv_tf32_kernel");
 }
