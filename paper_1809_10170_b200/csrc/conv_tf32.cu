@@ -156,6 +156,8 @@ __global__ void __launch_bounds__(kThreadsT, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = p.n_g * p.n_r;
+  long long prof[6] = {0, 0, 0, 0, 0, 0};  // DCONV_TF32_PROFILE only
+  const long long prof_t0 = p.dbg ? clock64() : 0;
   const uint32_t tmem_cols = kMaxMT * p.N <= 256 ? 256 : 512;
 
   if (threadIdx.x == 0) {
@@ -193,18 +195,21 @@ __global__ void __launch_bounds__(kThreadsT, 1)
   if (warp == 0) {
     // ----------------------------------------------------------- producer
     if (lane == 0) {
-      int gs = 0;
+      // ring slot and phase advance incrementally (no per-stage division)
+      int gs = 0, buf = 0;
+      uint32_t phase = 0;
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
         int img, y0, x0, cg;
         decode(u, img, y0, x0, cg);
+        int g = 0, r = 0;
         for (int st = 0; st < S; ++st, ++gs) {
-          const int buf = gs % p.NS;
+          if (st > 0 && ++r == p.n_r) { r = 0; ++g; }
+          if (gs > 0 && ++buf == p.NS) { buf = 0; phase ^= 1u; }
           if (gs >= p.NS) {
             const long long t0 = p.dbg ? clock64() : 0;
-            mbar_wait_backoff(&empty[buf], ((gs / p.NS) - 1) & 1, 64);
-            if (p.dbg) p.dbg[blockIdx.x * 4 + 0] += clock64() - t0;
+            mbar_wait_backoff(&empty[buf], phase ^ 1u, 64);
+            if (p.dbg) prof[0] += clock64() - t0;
           }
-          const int g = st / p.n_r, r = st - g * p.n_r;
           const int ib0 = g * p.G, n0 = r * p.R;
           const int Ge = min(p.G, p.ib_n - ib0), Re = min(p.R, p.h_f - n0);
           float* sp = smem + buf * p.stage_floats;
@@ -227,7 +232,8 @@ __global__ void __launch_bounds__(kThreadsT, 1)
     }
   } else if (warp == 1) {
     // ----------------------------------------------------------- MMA issuer
-    int gs = 0, ui = 0;
+    int gs = 0, ui = 0, buf = 0;
+    uint32_t phase = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++ui) {
       int img, y0, x0, cg;
       decode(u, img, y0, x0, cg);
@@ -236,18 +242,20 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       if (ui > 0) {
         const long long t0 = p.dbg ? clock64() : 0;
         mbar_wait(acc_empty, (ui - 1) & 1);  // epilogue drained TMEM
-        if (p.dbg && lane == 0) p.dbg[blockIdx.x * 4 + 2] += clock64() - t0;
+        if (p.dbg) prof[2] += clock64() - t0;
       }
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      int g = 0, r = 0;
       for (int st = 0; st < S; ++st, ++gs) {
-        const int buf = gs % p.NS;
+        if (st > 0 && ++r == p.n_r) { r = 0; ++g; }
+        if (gs > 0 && ++buf == p.NS) { buf = 0; phase ^= 1u; }
         {
           const long long t0 = p.dbg ? clock64() : 0;
-          mbar_wait(&full[buf], (gs / p.NS) & 1);
-          if (p.dbg && lane == 0) p.dbg[blockIdx.x * 4 + 1] += clock64() - t0;
+          mbar_wait(&full[buf], phase);
+          if (p.dbg) prof[1] += clock64() - t0;
         }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int g = st / p.n_r, r = st - g * p.n_r;
+        const long long t_issue = p.dbg ? clock64() : 0;
         const int Ge = min(p.G, p.ib_n - g * p.G);
         const int Re = min(p.R, p.h_f - r * p.R);
         const float* sp = smem + buf * p.stage_floats;
@@ -299,9 +307,11 @@ __global__ void __launch_bounds__(kThreadsT, 1)
               accum = 1u;
             }
           }
+        if (p.dbg) prof[4] += clock64() - t_issue;
         umma_commit_elect(&empty[buf]);  // stage smem free once these MMAs retire
         if (st == S - 1) umma_commit_elect(acc_full);
         __syncwarp();
+        if (p.dbg) prof[5] += clock64() - t_issue;
       }
     }
   } else {
@@ -353,7 +363,12 @@ __global__ void __launch_bounds__(kThreadsT, 1)
     }
   }
 
-  if (p.dbg && threadIdx.x == 32) p.dbg[blockIdx.x * 4 + 3] = (unsigned long long)clock64();
+  if (p.dbg) {  // per-role cycle sums, kept in registers during the loop
+    if (threadIdx.x == 0) p.dbg[blockIdx.x * 8 + 0] = prof[0];
+    if (threadIdx.x == 32)
+      for (int i = 1; i < 6; ++i) p.dbg[blockIdx.x * 8 + i] = prof[i];
+    if (threadIdx.x == 32) p.dbg[blockIdx.x * 8 + 6] = clock64() - prof_t0;
+  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) {
@@ -415,7 +430,13 @@ Tf32Kernel pick_tf32_kernel(const Tf32Params& p) {
   return conv_tf32_kernel<0, 0>;
 }
 
-int tf32_channels(int jb_count) { return jb_count * 8 >= 128 ? 128 : (jb_count * 8 > 64 ? 128 : 64); }
+// Channels per unit: an M=128 MMA costs ~71 cycles for any N <= 128 and ~128
+// cycles at N = 256 (tools/umma_tf32_rate.cu), so wide layers use N = 256.
+int tf32_channels(int jb_count) {
+  static const int force = getenv("DCONV_TF32_N") ? atoi(getenv("DCONV_TF32_N")) : 0;
+  if (force == 64 || force == 128 || force == 256) return force;
+  return jb_count * 8 >= 256 ? 256 : (jb_count * 8 > 64 ? 128 : 64);
+}
 
 int64_t tf32_prepared_floats(int ib_n, int h_f, int w_f, int jb_count) {
   const int N = tf32_channels(jb_count);
@@ -469,22 +490,29 @@ int launch_conv_tf32(const FfmaParams& f, const float* w_prepared, cudaStream_t 
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
     const int strips = (p.w_o + kTW - 1) / kTW;
+    // time = rounds x per-unit cycles; a unit streams ib_n input blocks, each
+    // max(MMA time, load time): 9*MT MMAs of ~78 cycles (N <= 128) against its
+    // patch + weight bytes at ~40 B/cycle/SM when every SM loads (L2 bound),
+    // plus ~3000 cycles of fill and epilogue per unit.
     double best = -1;
     for (int mt = kMaxMT; mt >= 1; --mt) {
+      if (mt * p.N > 512) continue;  // accumulators: MT x N TMEM columns
       const int rg = (p.h_o + mt * kTileRows - 1) / (mt * kTileRows);
       const int64_t units = (int64_t)p.n * rg * strips * p.n_cg;
-      const double rows_eff = (double)p.h_o / (rg * mt * kTileRows);
-      const double waves = (double)units / ((double)((units + sms - 1) / sms) * sms);
-      // a stage's loads take about as long as 2.5 M-tiles of MMAs, so units
-      // with fewer M-tiles turn load-bound: time per pixel ~ max(mt, 2.5)/mt
-      const double cost = std::max((double)mt, 2.5) / mt;
-      const double score = rows_eff * waves / cost;
-      if (score > best + 1e-6) {
+      const double taps = (double)p.h_f * p.w_f;
+      const double mma = taps * mt * (p.N > 128 ? 128.0 : 78.0);
+      const double bytes = (double)(mt * kTileRows - 1 + p.h_f) * (kTW - 1 + p.w_f) * 32.0 +
+                           taps * p.N * 32.0;
+      const double unit = p.ib_n * std::max(mma, bytes / 40.0) + 3000.0;
+      const double rounds = (double)((units + sms - 1) / sms);
+      const double score = 1.0 / (rounds * unit);
+      if (score > best * (1 + 1e-9)) {
         best = score;
         p.MT = mt;
       }
     }
-    if (const char* e = getenv("DCONV_TF32_MT")) p.MT = std::max(1, std::min(kMaxMT, atoi(e)));
+    if (const char* e = getenv("DCONV_TF32_MT"))
+      p.MT = std::max(1, std::min(std::min(kMaxMT, 512 / p.N), atoi(e)));
   }
   const int patch_blk_bytes = 2 * (p.MT * kTileRows - 1 + p.h_f) * p.PW * 16;  // both planes
   if (p.h_f * p.w_f * wtap <= 48 * 1024) {
@@ -546,22 +574,24 @@ int launch_conv_tf32(const FfmaParams& f, const float* w_prepared, cudaStream_t 
   static const bool prof = getenv("DCONV_TF32_PROFILE") != nullptr;
   p.noload = getenv("DCONV_TF32_NOLOAD") != nullptr;
   if (prof) {  // debugging aid: where do the roles wait?  (not for timed runs)
-    cudaMalloc(&p.dbg, (size_t)grid * 4 * 8);
-    cudaMemsetAsync(p.dbg, 0, (size_t)grid * 4 * 8, stream);
+    cudaMalloc(&p.dbg, (size_t)grid * 8 * 8);
+    cudaMemsetAsync(p.dbg, 0, (size_t)grid * 8 * 8, stream);
     long long start = 0;
     pick_tf32_kernel(p)<<<grid, kThreadsT, smem, stream>>>(map, p);
-    std::vector<unsigned long long> h((size_t)grid * 4);
+    std::vector<unsigned long long> h((size_t)grid * 8);
     cudaMemcpy(h.data(), p.dbg, h.size() * 8, cudaMemcpyDeviceToHost);
-    double w_empty = 0, w_full = 0, w_acc = 0;
+    double w_empty = 0, w_full = 0, w_acc = 0, issue = 0, issue_commit = 0, total = 0;
     for (int b = 0; b < grid; ++b) {
-      w_empty += h[b * 4]; w_full += h[b * 4 + 1]; w_acc += h[b * 4 + 2];
+      w_empty += h[b * 8]; w_full += h[b * 8 + 1]; w_acc += h[b * 8 + 2];
+      issue += h[b * 8 + 4]; issue_commit += h[b * 8 + 5]; total += h[b * 8 + 6];
     }
     (void)start;
     fprintf(stderr,
             "conv_tf32 N=%d MT=%d G=%d R=%d NS=%d stage=%d B units=%d S=%d: per CTA avg wait "
-            "cycles producer(empty)=%.0f mma(full)=%.0f mma(acc_empty)=%.0f\n",
+            "cycles producer(empty)=%.0f mma(full)=%.0f mma(acc_empty)=%.0f issue=%.0f "
+            "issue+commit=%.0f total=%.0f\n",
             p.N, p.MT, p.G, p.R, p.NS, stage_bytes, p.units, p.n_g * p.n_r, w_empty / grid,
-            w_full / grid, w_acc / grid);
+            w_full / grid, w_acc / grid, issue / grid, issue_commit / grid, total / grid);
     cudaFree(p.dbg);
     p.dbg = nullptr;
   }

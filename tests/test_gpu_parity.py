@@ -596,7 +596,8 @@ def tf32_bound(x, k):
 
 @pytest.mark.parametrize("ci,co,h,w,f,n", [(64, 64, 18, 18, 3, 1), (16, 128, 20, 13, 3, 2),
                                             (24, 40, 70, 21, 3, 1), (32, 256, 10, 10, 1, 3),
-                                            (8, 72, 12, 12, 5, 1), (96, 136, 9, 30, 3, 2)])
+                                            (8, 72, 12, 12, 5, 1), (96, 136, 9, 30, 3, 2),
+                                            (40, 264, 20, 11, 3, 2), (24, 512, 35, 9, 3, 1)])
 def test_tf32_tensor_core_parity(ci, co, h, w, f, n):
     x = po.uniform((n, ci, h, w), 9100 + ci, co)
     k = po.uniform((ci, co, f, f), 9200 + ci, co)
