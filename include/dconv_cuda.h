@@ -66,7 +66,10 @@ enum {
   DCONV_EPI_NONE = 0,
   DCONV_EPI_RELU = 1,      /* relu_blocked fused */
   DCONV_EPI_ADD = 2,       /* + skip (same blocked geometry as the output) */
-  DCONV_EPI_ADD_RELU = 3   /* relu(conv + skip): ResNet block tail */
+  DCONV_EPI_ADD_RELU = 3,  /* relu(conv + skip): ResNet block tail */
+  DCONV_EPI_MAXPOOL = 4    /* flag: 2x2/s2 max-pool fused after the above; the
+                              output view is the pooled map (h_o/2 x w_o/2,
+                              h_o and w_o even).  TF32 path only. */
 };
 
 /* Kernel selection. */

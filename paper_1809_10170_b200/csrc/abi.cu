@@ -107,8 +107,13 @@ int resolve(const dconv_conv_desc* d, bool dense_input, int64_t dense_img,
     return set_error(DCONV_EINVAL_SHAPE, "desc h_o/w_o inconsistent with ConvShape");
   if (d->c_ib < 1 || d->c_ob < 1)
     return set_error(DCONV_EPARAM, "block sizes must be >= 1");
-  if (d->epilogue < 0 || d->epilogue > 3)
+  if (d->epilogue < 0 || d->epilogue > 7)
     return set_error(DCONV_EPARAM, "unknown epilogue %d", d->epilogue);
+  const bool pool = (d->epilogue & DCONV_EPI_MAXPOOL) != 0;
+  if (pool && ((d->h_o | d->w_o) & 1))
+    return set_error(DCONV_EINVAL_SHAPE, "fused 2x2 max-pool needs an even output (%d x %d)",
+                     d->h_o, d->w_o);
+  const int ph = pool ? d->h_o / 2 : d->h_o, pw = pool ? d->w_o / 2 : d->w_o;
   if ((d->epilogue & DCONV_EPI_ADD) && !skip)
     return set_error(DCONV_EPARAM, "ADD epilogue needs a skip tensor");
   const int c_ib = dense_input ? d->c_i : d->c_ib;
@@ -131,13 +136,13 @@ int resolve(const dconv_conv_desc* d, bool dense_input, int64_t dense_img,
         r->in_blk < (int64_t)d->h_i * r->in_row)
       return set_error(DCONV_ELAYOUT, "input view strides smaller than the map");
   }
-  r->out_row = d->out_row_stride ? d->out_row_stride : (int64_t)d->w_o * d->c_ob;
-  r->out_blk = d->out_blk_stride ? d->out_blk_stride : (int64_t)d->h_o * r->out_row;
+  r->out_row = d->out_row_stride ? d->out_row_stride : (int64_t)pw * d->c_ob;
+  r->out_blk = d->out_blk_stride ? d->out_blk_stride : (int64_t)ph * r->out_row;
   r->out_img = d->out_img_stride ? d->out_img_stride : (int64_t)r->jb_count * r->out_blk;
   r->sk_row = d->skip_row_stride ? d->skip_row_stride : (int64_t)d->w_o * d->c_ob;
   r->sk_blk = d->skip_blk_stride ? d->skip_blk_stride : (int64_t)d->h_o * r->sk_row;
   r->sk_img = d->skip_img_stride ? d->skip_img_stride : (int64_t)r->jb_count * r->sk_blk;
-  if (r->out_row < (int64_t)d->w_o * d->c_ob || r->out_blk < (int64_t)d->h_o * r->out_row)
+  if (r->out_row < (int64_t)pw * d->c_ob || r->out_blk < (int64_t)ph * r->out_row)
     return set_error(DCONV_ELAYOUT, "output view strides smaller than the map");
   return DCONV_OK;
 }
@@ -161,6 +166,8 @@ int conv_direct_impl(const dconv_conv_desc* d, const float* in, const float* w,
                      const float* skip, float* out, float* const* peers, int n_peers,
                      void* stream) {
   if (int rc = check_peers(peers, n_peers)) return rc;
+  if (d && (d->epilogue & DCONV_EPI_MAXPOOL))
+    return set_error(DCONV_EUNSUPPORTED, "fused max-pool epilogue: TF32 path only");
   Resolved r;
   int rc = resolve(d, false, 0, in, w, skip, out, &r);
   if (rc) return rc;
@@ -279,6 +286,8 @@ int conv_first_impl(const dconv_conv_desc* d, const float* in_dense, int64_t in_
                     const float* w, const float* skip, float* out, float* const* peers,
                     int n_peers, void* stream) {
   if (int rc = check_peers(peers, n_peers)) return rc;
+  if (d && (d->epilogue & DCONV_EPI_MAXPOOL))
+    return set_error(DCONV_EUNSUPPORTED, "fused max-pool epilogue: TF32 path only");
   Resolved r;
   int rc = resolve(d, true, in_img_stride, in_dense, w, skip, out, &r);
   if (rc) return rc;

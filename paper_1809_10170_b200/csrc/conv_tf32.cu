@@ -326,13 +326,48 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       mbar_wait_backoff(acc_full, ui & 1, 256);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int x = x0 + tx;
+      const bool pool = (p.epi & DCONV_EPI_MAXPOOL) != 0;
       for (int mt = 0; mt < p.MT; ++mt) {
         const int y = y0 + mt * kTileRows + ty;
         if (y0 + mt * kTileRows >= p.h_o) break;  // warp-uniform
+        const bool valid = y < p.h_o && x < p.w_o;
         for (int c0 = 0; c0 < p.N; c0 += 32) {
           float v[32];
           tmem_ld32x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(mt * p.N + c0), v);
-          if (y >= p.h_o || x >= p.w_o) continue;
+          if (pool) {
+            // 2x2 window = lanes {l, l^1, l^8, l^9} (8-px tile rows, even
+            // origins, even h_o/w_o: a window is all valid or all invalid)
+            if (valid && (p.epi & DCONV_EPI_ADD)) {
+#pragma unroll
+              for (int b = 0; b < 4; ++b) {
+                const int jb = cg * (p.N / 8) + (c0 / 8) + b;
+                if (jb >= p.jb_count) break;
+                const float* sk = p.skip + (int64_t)img * p.sk_img + (int64_t)jb * p.sk_blk +
+                                  (int64_t)y * p.sk_row + (int64_t)x * 8;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[b * 8 + i] += sk[i];
+              }
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              v[i] = fmaxf(v[i], __shfl_xor_sync(0xffffffffu, v[i], 1));
+              v[i] = fmaxf(v[i], __shfl_xor_sync(0xffffffffu, v[i], 8));
+              if (p.epi & DCONV_EPI_RELU) v[i] = fmaxf(v[i], 0.f);
+            }
+            if (!valid || (tx & 1) || (ty & 1)) continue;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const int jb = cg * (p.N / 8) + (c0 / 8) + b;
+              if (jb >= p.jb_count) break;
+              float* o = p.out + (int64_t)img * p.out_img + (int64_t)jb * p.out_blk +
+                         (int64_t)(y >> 1) * p.out_row + (int64_t)(x >> 1) * 8;
+              const float* vv = v + b * 8;
+              *reinterpret_cast<float4*>(o) = make_float4(vv[0], vv[1], vv[2], vv[3]);
+              *reinterpret_cast<float4*>(o + 4) = make_float4(vv[4], vv[5], vv[6], vv[7]);
+            }
+            continue;
+          }
+          if (!valid) continue;
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
             const int jb = cg * (p.N / 8) + (c0 / 8) + b;  // block within the computed range

@@ -545,6 +545,15 @@ def _build_vgg(p: Plan, device, seed: int) -> None:
     for i, l in enumerate(layers):
         last = i == len(layers) - 1
         pool = l.name in VGG16_POOL_AFTER
+        if pool and p.algo == "tf32" and p.shard is None and not l.first:
+            # TF32 path: conv + ReLU + 2x2 max-pool in one kernel, straight
+            # into the next layer's halo buffer (the full-resolution map is
+            # never written)
+            z = Act(p.n, l.c_o, l.h_o // 2, l.w_o // 2, halo=1, device=device)
+            p.outputs[l.name] = z
+            p.conv_into(l, cur, z, epilogue=_abi.EPI_RELU | _abi.EPI_MAXPOOL)
+            cur = z
+            continue
         y = Act(p.n, l.c_o, l.h_o, l.w_o, halo=0 if (last or pool) else 1, device=device)
         p.outputs[l.name] = y
         mine = p.conv_into(l, cur, y, epilogue=_abi.EPI_RELU, gather=not pool)

@@ -610,6 +610,34 @@ def test_tf32_tensor_core_parity(ci, co, h, w, f, n):
         assert err.max() > 0 or ci * f * f <= 8  # it really is TF32, not an fp32 fallback
 
 
+@pytest.mark.parametrize("ci,co,h,w,n", [(16, 64, 34, 26, 2), (24, 264, 18, 18, 1), (8, 40, 66, 10, 3)])
+def test_tf32_fused_maxpool_epilogue(ci, co, h, w, n):
+    """conv + ReLU + 2x2/s2 max-pool in the TF32 epilogue (the VGG pooled
+    layers on the TF32 path) equals the TF32 conv followed by the separate
+    bit-exact pool kernel, bit for bit, written into a halo'd view."""
+    l = nets.Layer("p", ci, co, h, w, 3, 3, 1)
+    x = po.uniform((n, ci, h, w), 9700 + ci, co)
+    k = po.uniform((ci, co, 3, 3), 9701 + ci, co)
+    a = nets.Act(n, ci, h, w)
+    a.buf.copy_(dev(np.stack([po.pack_feature_map(x[i], 8) for i in range(n)])))
+    wp = nets.prepare_tf32(l, nets.pack_weights(dev(k), False))
+    y = nets.Act(n, co, l.h_o, l.w_o)
+    nets.conv_tf32(l, n, a, wp, y, _abi.EPI_RELU)
+    ref = nets.Act(n, co, l.h_o // 2, l.w_o // 2, halo=1)
+    nets.maxpool_into(y, ref)
+    z = nets.Act(n, co, l.h_o // 2, l.w_o // 2, halo=1)
+    nets.conv_tf32(l, n, a, wp, z, _abi.EPI_RELU | _abi.EPI_MAXPOOL)
+    assert torch.equal(z.buf, ref.buf)
+    # FFMA / odd outputs: refused, not silently wrong
+    with pytest.raises(_abi.DconvError):
+        nets.conv(l, n, a, nets.pack_weights(dev(k), False), z, _abi.EPI_RELU | _abi.EPI_MAXPOOL)
+    lo = nets.Layer("o", ci, co, h + 1, w, 3, 3, 1)
+    ao = nets.Act(n, ci, h + 1, w)
+    with pytest.raises(ValueError, match="even"):
+        nets.conv_tf32(lo, n, ao, nets.prepare_tf32(lo, nets.pack_weights(dev(k), False)), z,
+                       _abi.EPI_MAXPOOL)
+
+
 def test_tf32_epilogue_and_padding():
     x = po.uniform((1, 16, 12, 12), 93, 0)
     k = po.uniform((16, 20, 3, 3), 93, 1)
