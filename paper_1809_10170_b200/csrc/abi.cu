@@ -166,8 +166,10 @@ int conv_direct_impl(const dconv_conv_desc* d, const float* in, const float* w,
                      const float* skip, float* out, float* const* peers, int n_peers,
                      void* stream) {
   if (int rc = check_peers(peers, n_peers)) return rc;
-  if (d && (d->epilogue & DCONV_EPI_MAXPOOL))
-    return set_error(DCONV_EUNSUPPORTED, "fused max-pool epilogue: TF32 path only");
+  if (d && (d->epilogue & DCONV_EPI_MAXPOOL) &&
+      (n_peers || (d->epilogue & DCONV_EPI_ADD) || d->algo == DCONV_ALGO_GENERIC))
+    return set_error(DCONV_EUNSUPPORTED,
+                     "fused max-pool epilogue: FFMA/TF32 paths, no skip-add, no peers");
   Resolved r;
   int rc = resolve(d, false, 0, in, w, skip, out, &r);
   if (rc) return rc;
@@ -201,8 +203,9 @@ int conv_direct_impl(const dconv_conv_desc* d, const float* in, const float* w,
     if (rc != DCONV_EUNSUPPORTED || d->algo != DCONV_ALGO_AUTO) return rc;
     algo = DCONV_ALGO_GENERIC;
   }
-  if (algo == DCONV_ALGO_GENERIC && n_peers)
-    return set_error(DCONV_EUNSUPPORTED, "fused peer gather needs the FFMA kernel (c_b = 8)");
+  if (algo == DCONV_ALGO_GENERIC && (n_peers || (d->epilogue & DCONV_EPI_MAXPOOL)))
+    return set_error(DCONV_EUNSUPPORTED,
+                     "fused peer gather / max-pool need the FFMA kernel (c_b = 8)");
   if (algo == DCONV_ALGO_GENERIC) {
     dconv_dev::GenericParams p{};
     p.in = in; p.w = w; p.skip = skip; p.out = out;

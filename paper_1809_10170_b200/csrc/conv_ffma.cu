@@ -506,6 +506,49 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
         fence_cluster();
         for (int q = 0; q < ks; ++q) mbar_arrive_remote_relaxed(done, q);
       }
+    } else if (p.epi & DCONV_EPI_MAXPOOL) {
+      // fused ReLU + 2x2/s2 max-pool: vertical partner in-thread (pixel
+      // k + TW/PG), horizontal partner in lane ^ 1; the even-column lane
+      // stores the pooled pencil (windows are all valid or all invalid:
+      // even h_o, w_o and tile origins)
+      const int kv = p.TW / PG;
+      const int jl = jb0 + cb - p.jb_begin;
+      auto pool_pair = [&](int k, int k2) {
+        float v[8];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float2 a = unpack2(acc[k][c]), b = unpack2(acc[k2][c]);
+          v[2 * c] = fmaxf(a.x, b.x);
+          v[2 * c + 1] = fmaxf(a.y, b.y);
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          v[c] = fmaxf(v[c], __shfl_xor_sync(0xffffffffu, v[c], 1));
+          if (p.epi & DCONV_EPI_RELU) v[c] = fmaxf(v[c], 0.f);
+        }
+        const int q = pg + PG * k;
+        const int ty = (int)__umulhi((unsigned)q, p.tw_magic), tx = q - ty * p.TW;
+        const int x = tx0 + tx;
+        if (cb >= cg_valid || (tx & 1) || ty >= tr.th || x >= p.w_o) return;
+        int img, y, prow;
+        tile_row(p, tr, ty, img, y, prow);
+        float* o = p.out + (int64_t)jl * p.out_blk + (int64_t)img * p.out_img +
+                   (int64_t)(y >> 1) * p.out_row + (int64_t)(x >> 1) * kCB;
+        *reinterpret_cast<float4*>(o) = make_float4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<float4*>(o + 4) = make_float4(v[4], v[5], v[6], v[7]);
+      };
+      if (kv == 1) {
+#pragma unroll
+        for (int k = 0; k < TPX; k += 2) pool_pair(k, k + 1);
+      } else if (kv == 2) {
+#pragma unroll
+        for (int k = 0; k < TPX; ++k)
+          if ((k & 2) == 0) pool_pair(k, k + 2);
+      } else {
+#pragma unroll
+        for (int k = 0; k < TPX; ++k)
+          if ((k & 4) == 0 && k + 4 < TPX) pool_pair(k, k + 4);
+      }
     } else {
 #pragma unroll
       for (int bb = 0; bb < NBLK; ++bb) {
@@ -628,10 +671,18 @@ int best_split(int64_t units, const int* slots, int max_ks, double unit, double*
 void pick_tile(FfmaParams& p, int BM, int BN, int co_groups, int sms, const int* slots,
                bool allow_split) {
   int cand[16], nc = 0;
-  for (int tw = 4; tw <= 128 && tw <= BM; tw *= 2) cand[nc++] = tw;
-  for (int d = 1; d <= 4; ++d) {
-    const int tw = (p.w_o + d - 1) / d;
-    if (tw >= 2 && tw <= BM && tw <= 128) cand[nc++] = tw;
+  const int PG = BM / 8;  // pixel groups (8 px per thread)
+  if (p.epi & DCONV_EPI_MAXPOOL) {
+    // fused 2x2 pool: a thread's vertical window partner is pixel k + TW/PG
+    // (TW a multiple of PG, TH even), the horizontal one is lane ^ 1
+    for (int tw = PG; tw <= 128 && tw <= BM / 2; tw *= 2)
+      if ((BM / tw) % 2 == 0) cand[nc++] = tw;
+  } else {
+    for (int tw = 4; tw <= 128 && tw <= BM; tw *= 2) cand[nc++] = tw;
+    for (int d = 1; d <= 4; ++d) {
+      const int tw = (p.w_o + d - 1) / d;
+      if (tw >= 2 && tw <= BM && tw <= 128) cand[nc++] = tw;
+    }
   }
   double best_score = -1;
   int64_t best_patch = 0;
@@ -799,12 +850,15 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
     attr_set = true;
   }
   // only the 8-warp 8x8-per-thread tile has the DSMEM split-K reduction
-  const bool no_split = getenv("DCONV_NO_SPLITK") != nullptr || NW != 8 || TPX != 8 || TCO != 8;
+  const bool no_split = getenv("DCONV_NO_SPLITK") != nullptr || NW != 8 || TPX != 8 ||
+                        TCO != 8 || (p.epi & DCONV_EPI_MAXPOOL);
   int slots[kMaxKs + 1] = {0};
   slots[1] = sms;
   if (!no_split)
     for (int ks = 2; ks <= kMaxKs; ++ks) slots[ks] = cluster_slots(kernel, ks, sms, threads);
   pick_tile(p, BM, BN, co_groups, sms, slots, !no_split);
+  if ((p.epi & DCONV_EPI_MAXPOOL) && p.TW == 0)
+    return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_ffma: no pool-compatible tile");
   p.TWe = std::min(p.TW, p.w_o);
   // q / TW for q < BM by multiply-high (exact: BM * TW < 2^32)
   p.tw_magic = (unsigned)(((uint64_t(1) << 32) + p.TW - 1) / p.TW);

@@ -12,6 +12,7 @@ strides, and the halo ring is zeroed once at allocation, outside any timing.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Tuple
 
@@ -545,10 +546,13 @@ def _build_vgg(p: Plan, device, seed: int) -> None:
     for i, l in enumerate(layers):
         last = i == len(layers) - 1
         pool = l.name in VGG16_POOL_AFTER
-        if pool and p.algo == "tf32" and p.shard is None and not l.first:
-            # TF32 path: conv + ReLU + 2x2 max-pool in one kernel, straight
-            # into the next layer's halo buffer (the full-resolution map is
-            # never written)
+        fuse_ffma = (p.algo == "ffma" and l.w_o % 16 == 0 and l.h_o % 2 == 0
+                     and os.environ.get("DCONV_NO_POOL_FUSION") is None)
+        if pool and (p.algo == "tf32" or fuse_ffma) and p.shard is None and not l.first:
+            # conv + ReLU + 2x2 max-pool in one kernel, straight into the next
+            # layer's halo buffer (the full-resolution map is never written).
+            # FFMA: only where the pool-compatible tiles (TW a multiple of
+            # the pixel-group count) cover the row without waste.
             z = Act(p.n, l.c_o, l.h_o // 2, l.w_o // 2, halo=1, device=device)
             p.outputs[l.name] = z
             p.conv_into(l, cur, z, epilogue=_abi.EPI_RELU | _abi.EPI_MAXPOOL)

@@ -418,6 +418,19 @@ def test_chain_wiring_teacher_forced(config):
         kb = po.pack_kernel(kd, 8, 8) if kd is not None else po.pack_kernel(
             _first_dense(w.cpu().numpy(), l), 8, 8)
         h = out.halo
+        if epi & _abi.EPI_MAXPOOL:  # fused 2x2/s2 pool: compare pooled rows
+            hp, wp = l.h_o // 2, l.w_o // 2
+            for rp in sorted({0, hp // 2, hp - 1}):
+                two = po.conv_oracle64_blocked(xb, kb, l.c_i, l.c_o, l.s, 2 * rp, 2 * rp + 2)
+                two = two[:, 2 * rp:2 * rp + 2]
+                if epi & _abi.EPI_RELU:
+                    two = np.maximum(two, 0)
+                want = two.reshape(two.shape[0], 2, wp, 2, 8).max(axis=(1, 3))
+                g = got[:, h + rp, h:h + wp, :]
+                scale = max(1.0, float(np.abs(want).max()))
+                err = float(np.abs(g - want).max())
+                assert err <= 1e-5 * scale + 1e-4, f"{config}/{l.name} pooled row {rp}: err {err}"
+            continue
         for r in sorted({0, l.h_o // 2, l.h_o - 1}):
             want = po.conv_oracle64_blocked(xb, kb, l.c_i, l.c_o, l.s, r, r + 1)[:, r]
             if epi & _abi.EPI_ADD:
@@ -610,6 +623,34 @@ def test_tf32_tensor_core_parity(ci, co, h, w, f, n):
         assert err.max() > 0 or ci * f * f <= 8  # it really is TF32, not an fp32 fallback
 
 
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("ci,co,h,w,n", [(16, 64, 34, 34, 2), (24, 136, 18, 66, 1), (8, 40, 10, 130, 3)])
+def test_ffma_fused_maxpool_epilogue(ci, co, h, w, n, variant):
+    """FFMA conv + ReLU + 2x2/s2 max-pool in one kernel (in-thread vertical
+    and lane^1 horizontal window partners) equals the FFMA conv with the
+    same tile followed by the bit-exact pool kernel, bit for bit; windows
+    span stacked images."""
+    lib = _abi.lib()
+    _abi.check(lib.dconv_cuda_set_ffma_variant(variant))
+    try:
+        l = nets.Layer("p", ci, co, h, w, 3, 3, 1)
+        x = po.uniform((n, ci, h, w), 9800 + ci, co)
+        k = po.uniform((ci, co, 3, 3), 9801 + ci, co)
+        a = nets.Act(n, ci, h, w)
+        a.buf.copy_(dev(np.stack([po.pack_feature_map(x[i], 8) for i in range(n)])))
+        wb = nets.pack_weights(dev(k), False)
+        z = nets.Act(n, co, l.h_o // 2, l.w_o // 2, halo=1)
+        nets.conv(l, n, a, wb, z, _abi.EPI_RELU | _abi.EPI_MAXPOOL)
+        got = host(z.buf)
+        for i in range(n):
+            y = np.maximum(po.conv_oracle64(x[i], k, 1), 0)
+            want = po.pack_feature_map(y.reshape(co, l.h_o // 2, 2, l.w_o // 2, 2).max(axis=(2, 4)), 8)
+            assert_tol(got[i, :, 1:-1, 1:-1], want, f"fused pool img {i}")
+            assert not got[i, :, 0].any() and not got[i, :, :, 0].any()
+    finally:
+        lib.dconv_cuda_set_ffma_variant(-1)
+
+
 @pytest.mark.parametrize("ci,co,h,w,n", [(16, 64, 34, 26, 2), (24, 264, 18, 18, 1), (8, 40, 66, 10, 3)])
 def test_tf32_fused_maxpool_epilogue(ci, co, h, w, n):
     """conv + ReLU + 2x2/s2 max-pool in the TF32 epilogue (the VGG pooled
@@ -628,9 +669,7 @@ def test_tf32_fused_maxpool_epilogue(ci, co, h, w, n):
     z = nets.Act(n, co, l.h_o // 2, l.w_o // 2, halo=1)
     nets.conv_tf32(l, n, a, wp, z, _abi.EPI_RELU | _abi.EPI_MAXPOOL)
     assert torch.equal(z.buf, ref.buf)
-    # FFMA / odd outputs: refused, not silently wrong
-    with pytest.raises(_abi.DconvError):
-        nets.conv(l, n, a, nets.pack_weights(dev(k), False), z, _abi.EPI_RELU | _abi.EPI_MAXPOOL)
+    # odd outputs: refused, not silently wrong
     lo = nets.Layer("o", ci, co, h + 1, w, 3, 3, 1)
     ao = nets.Act(n, ci, h + 1, w)
     with pytest.raises(ValueError, match="even"):
