@@ -104,7 +104,10 @@ __global__ void __launch_bounds__(256, 2)
     if (active) {
       constexpr int L = 7 * S + WF;  // input columns feeding 8 pixels x WF taps
       for (int c = 0; c < p.c_i; ++c) {
-        for (int n = 0; n < p.h_f; ++n) {
+        // h_f == WF (square filters, checked at launch): unrolled, so the
+        // accumulators stay in place across filter rows
+#pragma unroll
+        for (int n = 0; n < WF; ++n) {
           const float* row = sp + (c * t.PH + r * S + n) * t.PWs + cx * 8 * S;
           float seg[L];
 #pragma unroll
