@@ -43,7 +43,8 @@ constexpr int kMaxMT = 4;       // M-tiles (128 pixels each) per work unit, at m
 constexpr int kTileRows = 16;   // an M-tile is 16 output rows x 8 columns
 constexpr int kTW = 8;
 constexpr int kMaxStagesT = 8;
-constexpr int kThreadsT = 6 * 32;
+constexpr int kEpiWarps = 8;   // 2 per TMEM lane quarter, each half of the columns
+constexpr int kThreadsT = (2 + kEpiWarps) * 32;
 
 struct Tf32Params {
   const float* w;     // prepared weights
@@ -150,23 +151,29 @@ __global__ void __launch_bounds__(kThreadsT, 1)
   extern __shared__ __align__(1024) float smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.NS * p.stage_floats);
   uint64_t* empty = full + kMaxStagesT;
-  uint64_t* acc_full = empty + kMaxStagesT;
-  uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  // accumulators: nacc = 2 TMEM sets (MT*N <= 256) so the MMAs of unit u+1
+  // overlap the epilogue of unit u, else 1
+  uint64_t* acc_full = empty + kMaxStagesT;   // [2]
+  uint64_t* acc_empty = acc_full + 2;         // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = p.n_g * p.n_r;
   long long prof[6] = {0, 0, 0, 0, 0, 0};  // DCONV_TF32_PROFILE only
   const long long prof_t0 = p.dbg ? clock64() : 0;
-  const uint32_t tmem_cols = kMaxMT * p.N <= 256 ? 256 : 512;
+  const uint32_t tmem_cols = 512;
+  const int nacc = p.MT * p.N <= 256 ? 2 : 1;
+  const uint32_t acc_cols = (uint32_t)(p.MT * p.N);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < p.NS; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    mbar_init(acc_full, 1);
-    mbar_init(acc_empty, 4);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], kEpiWarps);
+    }
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -239,9 +246,11 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       decode(u, img, y0, x0, cg);
       const int valid_rows = min(p.MT * kTileRows, p.h_o - y0);
       const int mts = (valid_rows + kTileRows - 1) / kTileRows;
-      if (ui > 0) {
+      const int ab = nacc == 2 ? (ui & 1) : 0, au = nacc == 2 ? (ui >> 1) : ui;
+      const uint32_t acc_base = tmem_base + (uint32_t)ab * acc_cols;
+      if (au > 0) {
         const long long t0 = p.dbg ? clock64() : 0;
-        mbar_wait(acc_empty, (ui - 1) & 1);  // epilogue drained TMEM
+        mbar_wait(&acc_empty[ab], (au - 1) & 1);  // epilogue drained this TMEM set
         if (p.dbg) prof[2] += clock64() - t0;
       }
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -283,7 +292,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
               for (int m = 0; m < (WF_T > 0 ? WF_T : 1); ++m) {
 #pragma unroll
                 for (int mt = 0; mt < MT_T; ++mt)
-                  umma_tf32_elect(tmem_base + (uint32_t)(mt * p.N),
+                  umma_tf32_elect(acc_base + (uint32_t)(mt * p.N),
                                   arow + (uint32_t)m + (uint32_t)mt * a_mt, a_hi,
                                   brow + (uint32_t)m * b_tap, b_hi, p.idesc, accum);
                 accum = 1u;
@@ -292,7 +301,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
               for (int m = 1; m < wf; ++m) {
 #pragma unroll
                 for (int mt = 0; mt < MT_T; ++mt)
-                  umma_tf32_elect(tmem_base + (uint32_t)(mt * p.N),
+                  umma_tf32_elect(acc_base + (uint32_t)(mt * p.N),
                                   arow + (uint32_t)m + (uint32_t)mt * a_mt, a_hi,
                                   brow + (uint32_t)m * b_tap, b_hi, p.idesc, 1u);
               }
@@ -302,14 +311,14 @@ __global__ void __launch_bounds__(kThreadsT, 1)
               const uint32_t blo = brow + (uint32_t)m * b_tap;
               uint32_t alo = arow + (uint32_t)m;
               for (int mt = 0; mt < mts; ++mt, alo += a_mt)
-                umma_tf32_elect(tmem_base + (uint32_t)(mt * p.N), alo, a_hi, blo, b_hi, p.idesc,
+                umma_tf32_elect(acc_base + (uint32_t)(mt * p.N), alo, a_hi, blo, b_hi, p.idesc,
                                 accum);
               accum = 1u;
             }
           }
         if (p.dbg) prof[4] += clock64() - t_issue;
         umma_commit_elect(&empty[buf]);  // stage smem free once these MMAs retire
-        if (st == S - 1) umma_commit_elect(acc_full);
+        if (st == S - 1) umma_commit_elect(&acc_full[ab]);
         __syncwarp();
         if (p.dbg) prof[5] += clock64() - t_issue;
       }
@@ -317,13 +326,16 @@ __global__ void __launch_bounds__(kThreadsT, 1)
   } else {
     // ----------------------------------------------------------- epilogue
     const int q = warp & 3;  // TMEM lane quarter of this warp
+    const int ch = (warp - 2) / 4;  // which half of the N columns
     const int r = q * 32 + lane;  // pixel row of the M-tile
     const int ty = r / kTW, tx = r % kTW;
     int ui = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++ui) {
       int img, y0, x0, cg;
       decode(u, img, y0, x0, cg);
-      mbar_wait_backoff(acc_full, ui & 1, 256);
+      const int ab = nacc == 2 ? (ui & 1) : 0, au = nacc == 2 ? (ui >> 1) : ui;
+      const uint32_t acc_base = tmem_base + (uint32_t)ab * acc_cols;
+      mbar_wait_backoff(&acc_full[ab], au & 1, 256);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int x = x0 + tx;
       const bool pool = (p.epi & DCONV_EPI_MAXPOOL) != 0;
@@ -331,9 +343,10 @@ __global__ void __launch_bounds__(kThreadsT, 1)
         const int y = y0 + mt * kTileRows + ty;
         if (y0 + mt * kTileRows >= p.h_o) break;  // warp-uniform
         const bool valid = y < p.h_o && x < p.w_o;
-        for (int c0 = 0; c0 < p.N; c0 += 32) {
+        const int half_n = p.N / 2;  // >= 32
+        for (int c0 = ch * half_n; c0 < (ch + 1) * half_n; c0 += 32) {
           float v[32];
-          tmem_ld32x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(mt * p.N + c0), v);
+          tmem_ld32x32(acc_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(mt * p.N + c0), v);
           if (pool) {
             // 2x2 window = lanes {l, l^1, l^8, l^9} (8-px tile rows, even
             // origins, even h_o/w_o: a window is all valid or all invalid)
@@ -394,7 +407,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(acc_empty);
+      if (lane == 0) mbar_arrive(&acc_empty[ab]);
     }
   }
 
@@ -538,7 +551,8 @@ int launch_conv_tf32(const FfmaParams& f, const float* w_prepared, cudaStream_t 
       const double mma = taps * mt * (p.N > 128 ? 128.0 : 78.0);
       const double bytes = (double)(mt * kTileRows - 1 + p.h_f) * (kTW - 1 + p.w_f) * 32.0 +
                            taps * p.N * 32.0;
-      const double unit = p.ib_n * std::max(mma, bytes / 40.0) + 3000.0;
+      // double-buffered accumulators (MT*N <= 256) hide most of the epilogue
+      const double unit = p.ib_n * std::max(mma, bytes / 40.0) + (mt * p.N <= 256 ? 800.0 : 3000.0);
       const double rounds = (double)((units + sms - 1) / sms);
       const double score = 1.0 / (rounds * unit);
       if (score > best * (1 + 1e-9)) {
@@ -567,7 +581,7 @@ int launch_conv_tf32(const FfmaParams& f, const float* w_prepared, cudaStream_t 
   p.wstage_floats = p.G * p.R * p.w_f * 2 * p.N * 4;
   p.stage_floats = ((2 * p.plane_floats + p.wstage_floats) + 255) & ~255;  // 1 KB aligned
   const int stage_bytes = p.stage_floats * 4;
-  const int bar_bytes = (2 * kMaxStagesT + 2) * 8 + 16;
+  const int bar_bytes = (2 * kMaxStagesT + 4) * 8 + 16;
   p.NS = std::min(kMaxStagesT, (220 * 1024 - bar_bytes) / stage_bytes);
   if (p.NS < 2)
     return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_tf32: stage of %d bytes", stage_bytes);

@@ -1,8 +1,11 @@
 """Summarise bench.py's per-layer list by layer role (tools; reads a bench log)."""
 import json
+import signal
 import re
 import sys
 from collections import defaultdict
+
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)
 
 d = None
 for line in open(sys.argv[1]):
