@@ -503,7 +503,18 @@ int launch_prepare_tf32(const float* w, int ib_n, int h_f, int w_f, int jb_begin
   return dconv_host::check_launch("prepare_tf32_weights_kernel");
 }
 
-int launch_conv_tf32(const FfmaParams& f, const float* w_prepared, cudaStream_t stream) {
+int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t stream) {
+  FfmaParams f = f0;
+  // a 1x1 stride-s conv is a 1x1 stride-1 conv over the subsampled view
+  // (every s-th pixel of every s-th row): only the tensor map's strides change
+  int64_t px_floats = 8;
+  if (f.s > 1 && f.h_f == 1 && f.w_f == 1) {
+    px_floats = 8 * (int64_t)f.s;
+    f.in_row *= f.s;
+    f.h_i = f.h_o;
+    f.w_i = f.w_o;
+    f.s = 1;
+  }
   if (f.s != 1)
     return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_tf32: stride %d (only 1)", f.s);
   if (f.in_img != (int64_t)f.ib_n * f.in_blk)
@@ -596,7 +607,8 @@ int launch_conv_tf32(const FfmaParams& f, const float* w_prepared, cudaStream_t 
   CUtensorMap map;
   const cuuint64_t dims[5] = {4, 2, (cuuint64_t)f.w_i, (cuuint64_t)f.h_i,
                               (cuuint64_t)f.n * f.ib_n};
-  const cuuint64_t strides[4] = {16, 32, (cuuint64_t)f.in_row * 4, (cuuint64_t)f.in_blk * 4};
+  const cuuint64_t strides[4] = {16, (cuuint64_t)px_floats * 4, (cuuint64_t)f.in_row * 4,
+                                 (cuuint64_t)f.in_blk * 4};
   const cuuint32_t box[5] = {4, 1, (cuuint32_t)p.PW, (cuuint32_t)p.PH, (cuuint32_t)p.G};
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   const CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(f.in),

@@ -236,17 +236,20 @@ def conv(l: Layer, n: int, x: "Act|torch.Tensor", w: torch.Tensor, out: Act,
 
 
 def conv_tf32(l: Layer, n: int, x: "Act", wprep: torch.Tensor, out: Act,
-              epilogue: int = 0, skip: Optional[Act] = None, stream=None) -> None:
-    """tcgen05/TMEM TF32 launch of a stride-1 blocked layer (weights prepared
-    by prepare_tf32)."""
+              epilogue: int = 0, skip: Optional[Act] = None, stream=None,
+              in_view: Optional[Tuple[int, int, int, int]] = None) -> None:
+    """tcgen05/TMEM TF32 launch of a blocked layer (stride 1, or a 1x1 of any
+    stride; weights prepared by prepare_tf32)."""
     d = _desc(l, n, epilogue)
     d.out_img_stride, d.out_blk_stride, d.out_row_stride = out.img, out.blk, out.row
-    d.in_img_stride, d.in_blk_stride, d.in_row_stride = x.full_view()[1:]
+    if in_view is None:
+        in_view = x.full_view()
+    d.in_img_stride, d.in_blk_stride, d.in_row_stride = in_view[1:]
     sp = 0
     if skip is not None:
         d.skip_img_stride, d.skip_blk_stride, d.skip_row_stride = skip.img, skip.blk, skip.row
         sp = skip.base()
-    check(lib().dconv_cuda_conv_direct_tf32(ctypes.byref(d), x.full_view()[0], ptr(wprep), sp,
+    check(lib().dconv_cuda_conv_direct_tf32(ctypes.byref(d), in_view[0], ptr(wprep), sp,
                                             out.base(), stream_ptr(stream)))
 
 
@@ -410,10 +413,11 @@ class Plan:
         w = self.weights[l.name]
         kind = "first" if l.first else "conv"
         if self.shard is None:
-            if self.algo == "tf32" and not l.first and l.s == 1 and in_view is None:
+            if self.algo == "tf32" and not l.first and (l.s == 1 or (l.h_f == 1 and l.w_f == 1)):
                 wp = prepare_tf32(l, w)
                 self.weights[l.name + ".tf32"] = wp
-                self.steps.append(Step(lambda st: conv_tf32(l, self.n, x, wp, y, epilogue, skip, st),
+                self.steps.append(Step(lambda st: conv_tf32(l, self.n, x, wp, y, epilogue, skip, st,
+                                                            in_view),
                                        l.name, "tf32", self.n * l.flops, l))
                 return y
             self.steps.append(Step(lambda st: conv(l, self.n, x, w, y, epilogue, skip, st, in_view,

@@ -677,6 +677,31 @@ def test_tf32_fused_maxpool_epilogue(ci, co, h, w, n):
                        _abi.EPI_MAXPOOL)
 
 
+@pytest.mark.parametrize("ci,co,hb,s", [(32, 64, 56, 2), (40, 136, 27, 2), (16, 24, 13, 3)])
+def test_tf32_strided_1x1_on_crop_view(ci, co, hb, s):
+    """1x1 stride-s convs (ResNet projections) on the TF32 path: a stride-1
+    1x1 over the tensor map's subsampled view, here of a crop view (h_i =
+    hb - 1 rows/cols of an hb x hb buffer, like the 55x55 crop of 56x56)."""
+    n = 2
+    hi = hb - 1 if (hb - 2) % s == 0 else hb
+    x = po.uniform((n, ci, hb, hb), 9900 + ci, s)
+    k = po.uniform((ci, co, 1, 1), 9901 + ci, s)
+    a = nets.Act(n, ci, hb, hb)
+    a.buf.copy_(dev(np.stack([po.pack_feature_map(x[i], 8) for i in range(n)])))
+    l = nets.Layer("pr", ci, co, hi, hi, 1, 1, s)
+    y = nets.Act(n, co, l.h_o, l.w_o)
+    wp = nets.prepare_tf32(l, nets.pack_weights(dev(k), False))
+    nets.conv_tf32(l, n, a, wp, y, in_view=a.full_view())
+    got = host(y.buf)
+    for i in range(n):
+        xc = np.ascontiguousarray(x[i][:, :hi, :hi])
+        want = po.pack_feature_map(po.conv_oracle64(xc, k, s), 8)
+        err = np.abs(got[i].astype(np.float64) - want)
+        bound = 2.0 ** -9 * po.pack_feature_map(po.conv_oracle64(np.abs(xc), np.abs(k), s), 8) + 1e-5
+        assert (err <= bound).all(), f"max err {err.max()}"
+        assert err.max() > 0  # really the TF32 path
+
+
 def test_tf32_epilogue_and_padding():
     x = po.uniform((1, 16, 12, 12), 93, 0)
     k = po.uniform((16, 20, 3, 3), 93, 1)
