@@ -381,6 +381,27 @@ __global__ void __launch_bounds__(kThreadsT, 1)
             continue;
           }
           if (!valid) continue;
+          if (p.epi & DCONV_EPI_ADD) {
+            // all of the chunk's skip pencils in flight before any store
+            // (read-only path: the loads do not wait behind the stores)
+            float4 s4[8];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const int jb = min(cg * (p.N / 8) + (c0 / 8) + b, p.jb_count - 1);
+              const float4* sk = reinterpret_cast<const float4*>(
+                  p.skip + (int64_t)img * p.sk_img + (int64_t)jb * p.sk_blk +
+                  (int64_t)y * p.sk_row + (int64_t)x * 8);
+              s4[2 * b] = __ldg(sk);
+              s4[2 * b + 1] = __ldg(sk + 1);
+            }
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              float* vv = v + b * 8;
+              vv[0] += s4[2 * b].x; vv[1] += s4[2 * b].y; vv[2] += s4[2 * b].z; vv[3] += s4[2 * b].w;
+              vv[4] += s4[2 * b + 1].x; vv[5] += s4[2 * b + 1].y;
+              vv[6] += s4[2 * b + 1].z; vv[7] += s4[2 * b + 1].w;
+            }
+          }
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
             const int jb = cg * (p.N / 8) + (c0 / 8) + b;  // block within the computed range
@@ -388,14 +409,6 @@ __global__ void __launch_bounds__(kThreadsT, 1)
             float* o = p.out + (int64_t)img * p.out_img + (int64_t)jb * p.out_blk +
                        (int64_t)y * p.out_row + (int64_t)x * 8;
             float* vv = v + b * 8;
-            if (p.epi & DCONV_EPI_ADD) {
-              const float* sk = p.skip + (int64_t)img * p.sk_img + (int64_t)jb * p.sk_blk +
-                                (int64_t)y * p.sk_row + (int64_t)x * 8;
-              const float4 s0 = *reinterpret_cast<const float4*>(sk);
-              const float4 s1 = *reinterpret_cast<const float4*>(sk + 4);
-              vv[0] += s0.x; vv[1] += s0.y; vv[2] += s0.z; vv[3] += s0.w;
-              vv[4] += s1.x; vv[5] += s1.y; vv[6] += s1.z; vv[7] += s1.w;
-            }
             if (p.epi & DCONV_EPI_RELU) {
 #pragma unroll
               for (int i = 0; i < 8; ++i) vv[i] = fmaxf(vv[i], 0.f);
