@@ -65,7 +65,6 @@ struct Tf32Params {
   int MT;             // M-tiles per unit (1..4)
   uint32_t idesc;
   unsigned long long* dbg;  // DCONV_TF32_PROFILE: per-CTA wait cycles (else null)
-  int noload;               // DCONV_TF32_NOLOAD (timing experiment only): skip refills
 };
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -223,10 +222,6 @@ __global__ void __launch_bounds__(kThreadsT, 1)
           // the TMA box always lands whole (OOB elements zero-filled)
           const uint32_t patch_bytes = 2u * (uint32_t)(p.G * p.PH * p.PW * 4) * 4u;
           const uint32_t wbytes = (uint32_t)(Ge * Re * p.w_f * 2 * p.N * 4) * 4u;
-          if (p.noload && gs >= p.NS) {
-            mbar_arrive(&full[buf]);
-            continue;
-          }
           mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes);
           tma_load_5d(sp, &tmap, 0, 0, x0, y0 + n0, img * p.ib_n + ib0, &full[buf]);
           tma_load_5d(sp + p.plane_floats, &tmap, 0, 1, x0, y0 + n0, img * p.ib_n + ib0,
@@ -646,7 +641,6 @@ int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t
   const size_t smem = (size_t)p.NS * stage_bytes + bar_bytes;
   const int grid = std::min(p.units, sms);
   static const bool prof = getenv("DCONV_TF32_PROFILE") != nullptr;
-  p.noload = getenv("DCONV_TF32_NOLOAD") != nullptr;
   if (prof) {  // debugging aid: where do the roles wait?  (not for timed runs)
     cudaMalloc(&p.dbg, (size_t)grid * 8 * 8);
     cudaMemsetAsync(p.dbg, 0, (size_t)grid * 8 * 8, stream);

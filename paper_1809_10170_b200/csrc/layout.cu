@@ -78,6 +78,30 @@ __global__ void pack_fm_dev(const float* __restrict__ src, int c, int h, int w,
   }
 }
 
+// c_b = 8: one thread per output pencil (8 channel reads, each coalesced
+// across x; two float4 stores), 32-bit index math per pencil.
+__global__ void pack_fm8_dev(const float* __restrict__ src, int c, int h, int w, int halo,
+                             int nb, int64_t pencils, float* __restrict__ dst) {
+  const int hp = h + 2 * halo, wp = w + 2 * halo;
+  GRID_STRIDE(e, pencils) {
+    int64_t t = e;
+    const int xp = (int)(t % wp); t /= wp;
+    const int yp = (int)(t % hp); t /= hp;
+    const int b = (int)(t % nb);
+    const int img = (int)(t / nb);
+    const int y = yp - halo, x = xp - halo;
+    float v[8];
+    const bool in = y >= 0 && y < h && x >= 0 && x < w;
+    const float* s = src + (((int64_t)img * c + b * 8) * h + y) * w + x;
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc)
+      v[cc] = (in && b * 8 + cc < c) ? __ldg(s + (int64_t)cc * h * w) : 0.0f;
+    float4* d = reinterpret_cast<float4*>(dst + e * 8);
+    d[0] = make_float4(v[0], v[1], v[2], v[3]);
+    d[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+}
+
 __global__ void unpack_fm_dev(const float* __restrict__ src, int c, int h,
                               int w, int c_b, int halo, int nb, int64_t total,
                               float* __restrict__ dst) {
@@ -178,6 +202,11 @@ int launch_pack_fm(const float* src, int n, int c, int h, int w, int c_b,
   const int nb = (c + c_b - 1) / c_b;
   const int64_t total =
       (int64_t)n * nb * (h + 2 * halo) * (w + 2 * halo) * c_b;
+  if (c_b == 8 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    pack_fm8_dev<<<grid_for(total / 8), 256, 0, st>>>(src, c, h, w, halo, nb, total / 8, dst);
+    dconv_host::count_launch();
+    return dconv_host::check_launch("pack_fm8_dev");
+  }
   pack_fm_dev<<<grid_for(total), 256, 0, st>>>(src, c, h, w, c_b, halo, nb,
                                                total, dst);
   dconv_host::count_launch();

@@ -413,6 +413,27 @@ class Plan:
         w = self.weights[l.name]
         kind = "first" if l.first else "conv"
         if self.shard is None:
+            if self.algo == "tf32" and l.first and l.s == 1 and in_view is None:
+                # TF32 path, stride-1 first layer (VGG conv1_1): zero-pad the
+                # image to one 8-channel block (a pack kernel, SPEC.md:121's
+                # first-layer choice) and run it as a blocked tcgen05 layer;
+                # FLOPs are still counted with the real C_i
+                lb = Layer(l.name, l.c_i, l.c_o, l.h_i, l.w_i, l.h_f, l.w_f, l.s, False)
+                dense = torch.empty((l.c_i, l.c_o, l.h_f, l.w_f), dtype=torch.float32,
+                                    device=w.device)
+                check(lib().dconv_cuda_unpack_kernel(ptr(w), l.c_i, l.c_o, l.h_f, l.w_f, CB, l.c_i,
+                                                     ptr(dense), stream_ptr(None)))
+                wp = prepare_tf32(lb, pack_weights(dense, False))
+                self.weights[l.name + ".tf32"] = wp
+                xb = Act(self.n, l.c_i, l.h_i, l.w_i, device=w.device)
+                n = self.n
+                self.steps.append(Step(
+                    lambda st: check(lib().dconv_cuda_pack_feature_map(
+                        ptr(x), n, l.c_i, l.h_i, l.w_i, CB, 0, ptr(xb.buf), stream_ptr(st))),
+                    f"pack_{l.name}", "pack"))
+                self.steps.append(Step(lambda st: conv_tf32(lb, n, xb, wp, y, epilogue, skip, st),
+                                       l.name, "tf32", n * l.flops, l))
+                return y
             if self.algo == "tf32" and not l.first and (l.s == 1 or (l.h_f == 1 and l.w_f == 1)):
                 wp = prepare_tf32(l, w)
                 self.weights[l.name + ".tf32"] = wp

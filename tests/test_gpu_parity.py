@@ -748,3 +748,21 @@ def test_autotuned_plan_matches_default_tiles():
         x, y = host(a.outputs[name].buf), host(b.outputs[name].buf)
         scale = max(1.0, float(np.abs(x).max()))
         assert float(np.abs(x - y).max()) <= 1e-5 * scale + 1e-4, name
+
+
+def test_tf32_first_layer_packs_and_matches_ffma_plan():
+    """TF32 plans run VGG's stride-1 first layer as pack (8-channel block,
+    zero-padded) + tcgen05 conv; its output equals the FFMA first-layer
+    reader's within the TF32 bound."""
+    a = nets.build_plan("vgg16", 1, seed=13)
+    b = nets.build_plan("vgg16", 1, seed=13, algo="tf32")
+    assert [s.kind for s in b.steps[:2]] == ["pack", "tf32"]
+    a.run()
+    b.run()
+    torch.cuda.synchronize()
+    ya, yb = host(a.outputs["conv1_1"].buf), host(b.outputs["conv1_1"].buf)
+    l = nets.VGG16[0]
+    x = host(a.input)[0]
+    k = po.unpack_kernel(host(a.weights[l.name]), l.c_i, l.c_o)
+    bound = 2.0 ** -9 * po.pack_feature_map(po.conv_oracle64(np.abs(x), np.abs(k), 1), 8) + 1e-5
+    assert (np.abs(ya[0, :, 1:-1, 1:-1] - yb[0, :, 1:-1, 1:-1]) <= 2 * bound).all()
