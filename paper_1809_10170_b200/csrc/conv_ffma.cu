@@ -72,6 +72,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
       : "memory");
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, "
+      "%8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+        "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+        "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
 __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   uint64_t r;
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
@@ -102,6 +113,32 @@ __device__ __forceinline__ void tmem_fold(uint32_t taddr, uint64_t* acc,
         asm("mov.b64 {%0, %1}, %2;" : "=r"(v[2 * i]), "=r"(v[2 * i + 1]) : "l"(acc[c * 16 + i]));
       tmem_st32(ta, v);
     }
+  }
+}
+
+// final = (running total) + acc -> TMEM result columns t_res, handed to the
+// epilogue warpgroup
+template <int NP>
+__device__ __forceinline__ void tmem_finalize(uint32_t t_tot, uint32_t t_res, const uint64_t* acc,
+                                              bool have_total) {
+#pragma unroll
+  for (int c = 0; c < NP / 16; ++c) {
+    uint32_t v[32];
+    if (have_total) {
+      tmem_ld32(t_tot + c * 32, v);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        uint64_t t;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(t) : "r"(v[2 * i]), "r"(v[2 * i + 1]));
+        t = fadd2(acc[c * 16 + i], t);
+        asm("mov.b64 {%0, %1}, %2;" : "=r"(v[2 * i]), "=r"(v[2 * i + 1]) : "l"(t));
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        asm("mov.b64 {%0, %1}, %2;" : "=r"(v[2 * i]), "=r"(v[2 * i + 1]) : "l"(acc[c * 16 + i]));
+    }
+    tmem_st32(t_res + c * 32, v);
   }
 }
 
@@ -158,8 +195,12 @@ __host__ __device__ __forceinline__ int wchunk(int c, int wstride) {
   return TCO == 16 ? c * wstride + (c >> 1) * 4 : c * wstride;
 }
 
+// Roles: NW compute warps (two warpgroups), a producer warpgroup (one active
+// warp) and an epilogue warpgroup: when p.epi_wg, the compute warps hand each
+// finished tile to the epilogue warps through TMEM and go straight on to the
+// next unit, so skip-add / ReLU / stores overlap the next tile's FFMA2s.
 template <int BM, int BN, int WF, int NW, int TPX, int TCO>
-__global__ void __launch_bounds__((NW + 4) * 32, 1)
+__global__ void __launch_bounds__((NW + 8) * 32, 1)
     conv_ffma_kernel(const FfmaParams p) {
   // TCO: channels per thread (1 or 2 output blocks)
   constexpr int NBLK = TCO / 8;
@@ -179,7 +220,9 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
   uint64_t* empty = full + kMaxStages;
   uint64_t* ready = empty + kMaxStages;        // all ranks' partials written
   uint64_t* done = ready + 1;                  // all ranks finished reading mine
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* res_full = done + 1;               // [2] tile results in TMEM
+  uint64_t* res_empty = res_full + 2;          // [2] epilogue drained them
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_empty + 2);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -201,12 +244,20 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
     }
     mbar_init(ready, ks);  // one arrive per rank (thread 0, after a named barrier)
     mbar_init(done, ks);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&res_full[i], NW);
+      mbar_init(&res_empty[i], 4);
+    }
     fence_mbar_init();
   }
-  if (use_tmem && warp == 0) {
+  // TMEM: running totals [0, 128) + (epilogue hand-off) 2 result buffers
+  constexpr int kResCols = (NW / 4) * TPX * TCO;
+  const bool tmem_on = use_tmem || p.epi_wg;
+  const uint32_t tmem_cols = p.epi_wg ? 512u : (uint32_t)kTmemCols;
+  if (tmem_on && warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "n"(kTmemCols));
+                 "r"(tmem_cols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -227,14 +278,107 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
     cg_valid = min(CG, p.jb_begin + p.jb_count - jb0);
   };
 
+  if (warp >= NW + 4) {
+    // ------------------------------------------------------------ epilogue WG
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+    if constexpr (NW == 8 && TCO == 8) {
+      if (p.epi_wg) {
+        const uint32_t tmem_base = *tmem_slot;
+        const int qd = warp & 3;  // TMEM lane quarter = compute warps qd, qd + 4
+        int unit_iter = 0;
+        for (int u = cluster_id; u < n_units; u += n_clusters, ++unit_iter) {
+          TileRows tr;
+          int tx0, jb0, cg_valid;
+          decode(u, tr, tx0, jb0, cg_valid);
+          const int rb = unit_iter & 1;
+          mbar_wait(&res_full[rb], (unit_iter >> 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+          for (int half = 0; half < 2; ++half) {
+            const int cw = qd + 4 * half;  // the compute warp whose tile this lane holds
+            const int pg = (cw % WPG) * 4 + (lane & 3);
+            const int cb = (cw / WPG) * 8 + (lane >> 2);
+            const int jl = jb0 + cb - p.jb_begin;
+            const uint32_t tr_addr = tmem_base + ((uint32_t)(qd * 32) << 16) +
+                                     (uint32_t)(kResCols * (1 + rb) + half * TPX * TCO);
+#pragma unroll 1
+            for (int kc = 0; kc < TPX / 2; ++kc) {
+              uint32_t v[16];
+              tmem_ld16(tr_addr + kc * 16, v);
+              if (cb >= cg_valid) continue;
+              // 2 pixels x 8 channels: skip pencils first (all in flight)
+              float4 sk4[4];
+              int64_t ooff[2];
+              bool ok[2];
+#pragma unroll
+              for (int kk = 0; kk < 2; ++kk) {
+                const int k = kc * 2 + kk;
+                const int q = pg + PG * k;
+                const int ty = (int)__umulhi((unsigned)q, p.tw_magic), tx = q - ty * p.TW;
+                const int x = tx0 + tx;
+                ok[kk] = ty < tr.th && x < p.w_o;
+                int img = 0, y = 0, prow;
+                if (ok[kk]) tile_row(p, tr, ty, img, y, prow);
+                ooff[kk] = (int64_t)jl * p.out_blk + (int64_t)img * p.out_img +
+                           (int64_t)y * p.out_row + (int64_t)x * kCB;
+                if ((p.epi & DCONV_EPI_ADD) && ok[kk]) {
+                  const float4* sk = reinterpret_cast<const float4*>(
+                      p.skip + (int64_t)jl * p.sk_blk + (int64_t)img * p.sk_img +
+                      (int64_t)y * p.sk_row + (int64_t)x * kCB);
+                  sk4[2 * kk] = __ldg(sk);
+                  sk4[2 * kk + 1] = __ldg(sk + 1);
+                }
+              }
+#pragma unroll
+              for (int kk = 0; kk < 2; ++kk) {
+                if (!ok[kk]) continue;
+                float o[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) o[c] = __uint_as_float(v[kk * 8 + c]);
+                if (p.epi & DCONV_EPI_ADD) {
+                  o[0] += sk4[2 * kk].x; o[1] += sk4[2 * kk].y;
+                  o[2] += sk4[2 * kk].z; o[3] += sk4[2 * kk].w;
+                  o[4] += sk4[2 * kk + 1].x; o[5] += sk4[2 * kk + 1].y;
+                  o[6] += sk4[2 * kk + 1].z; o[7] += sk4[2 * kk + 1].w;
+                }
+                if (p.epi & DCONV_EPI_RELU) {
+#pragma unroll
+                  for (int c = 0; c < 8; ++c) o[c] = fmaxf(o[c], 0.f);
+                }
+                float* dst = p.out + ooff[kk];
+                *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+                *reinterpret_cast<float4*>(dst + 4) = make_float4(o[4], o[5], o[6], o[7]);
+                for (int pi = 0; pi < p.n_peers; ++pi) {
+                  float* pd = p.peer_out[pi] + ooff[kk];
+                  *reinterpret_cast<float4*>(pd) = make_float4(o[0], o[1], o[2], o[3]);
+                  *reinterpret_cast<float4*>(pd + 4) = make_float4(o[4], o[5], o[6], o[7]);
+                }
+              }
+            }
+          }
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&res_empty[rb]);
+        }
+      }
+    }
+    // TMEM is freed only after every compute and epilogue warp is done
+    if (tmem_on) asm volatile("bar.sync 2, %0;" ::"n"((NW + 4) * 32) : "memory");
+    return;
+  }
   if (warp >= NW) {
     // ------------------------------------------------------------ producer
     // One warpgroup, register budget handed to the compute warpgroups; its
-    // first warp streams every stage of every unit of this CTA through the
-    // NS-deep ring (prefetch runs across unit boundaries, so the epilogue of
-    // one tile overlaps the loads of the next).
+    // warps stream every stage of every unit of this CTA through the NS-deep
+    // ring (prefetch runs across unit boundaries, so the epilogue of one tile
+    // overlaps the loads of the next).  A bulk copy takes uniform operands,
+    // so a warp issues its lanes' copies one after another: the stage's
+    // copies are spread over kProdWarps warps to issue them in parallel
+    // (1x1 layers need ~130 row copies per unit).
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
-    if (warp != NW) return;
+    constexpr int kProdWarps = 4;
+    const int pw = warp - NW;
+    const int pt = pw * 32 + lane;  // producer thread index
     int gs = 0;
     const int seg_rows_full = (p.h_o - 1) * p.sy;  // + Re per full segment
     for (int u = cluster_id; u < n_units; u += n_clusters) {
@@ -248,7 +392,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
         // the epilogue reads this unit's skip tile once: pull it into L2 now,
         // a unit ahead of the read, so the ADD epilogue does not wait on HBM
         const uint32_t row_bytes = (uint32_t)(min(p.TW, p.w_o - tx0) * kCB * 4);
-        for (int t = lane; t < cg_valid * tr.th; t += 32) {
+        for (int t = pt; t < cg_valid * tr.th; t += 32 * kProdWarps) {
           const int c = t / tr.th, ty = t - c * tr.th;
           int img, y, prow;
           tile_row(p, tr, ty, img, y, prow);
@@ -274,7 +418,9 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
         const uint32_t wbytes = (uint32_t)(Re * p.w_f * kCB * kCB * 4) * Ge;
         float* sp = smem + buf * p.stage_floats;
         float* sw = sp + p.patch_floats;
-        if (lane == 0) mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes * cg_valid);
+        // one expect_tx per stage; copies of other warps may complete before
+        // it (the transaction count is allowed to run ahead within a phase)
+        if (pt == 0) mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes * cg_valid);
         __syncwarp();
         for (int j = 0; j < n_seg; ++j) {
           int img, y_start, rows, prow0;
@@ -287,14 +433,14 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
           }
           const float* src0 = p.in + (int64_t)img * p.in_img +
                               (int64_t)(y_start * p.sy + n0) * p.in_row + (int64_t)col0 * kCB;
-          for (int t = lane; t < Ge * rows; t += 32) {
+          for (int t = pt; t < Ge * rows; t += 32 * kProdWarps) {
             const int gi = t / rows, pr = t - gi * rows;
             const float* src = src0 + (int64_t)(ib0 + gi) * p.in_blk + (int64_t)pr * p.in_row;
             float* dst = sp + ((gi * p.PH + prow0 + pr) * p.PW) * kCB;
             bulk_g2s(dst, src, (uint32_t)(cols * kCB * 4), &full[buf]);
           }
         }
-        for (int c = lane; c < cg_valid; c += 32) {
+        for (int c = pt; c < cg_valid; c += 32 * kProdWarps) {
           const float* src = p.w + ((int64_t)(jb0 + c) * p.ib_n + ib0) * p.slab_floats +
                              (int64_t)n0 * p.w_f * kCB * kCB;
           bulk_g2s(sw + wchunk<TCO>(c, p.wstride_floats), src, wbytes, &full[buf]);
@@ -306,7 +452,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
 
   // -------------------------------------------------------------- consumers
   if constexpr (NW == 8) {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 152;");
   }
@@ -314,7 +460,7 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
   const int pg = wr * 4 + (lane & 3);
   const int cb = (wc * 8 + (lane >> 2)) * NBLK;  // first output block within the CTA tile
 
-  const uint32_t tmem_base = use_tmem ? *tmem_slot : 0u;
+  const uint32_t tmem_base = tmem_on ? *tmem_slot : 0u;
   const uint32_t taddr = tmem_base + ((uint32_t)((warp & 3) * 32) << 16) +
                          (uint32_t)((warp >> 2) * TPX * TCO);
   const int wf = WF > 0 ? WF : p.w_f;
@@ -421,6 +567,19 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
 #pragma unroll
           for (int c = 0; c < TCO / 2; ++c) acc[k][c] = 0ull;
       }
+    }
+    if (p.epi_wg) {
+      // hand the finished tile to the epilogue warpgroup (TMEM result buffer
+      // unit_iter & 1) and go on with the next unit
+      const int rb = unit_iter & 1;
+      if (unit_iter >= 2) mbar_wait(&res_empty[rb], ((unit_iter >> 1) - 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      tmem_finalize<NP>(taddr, taddr + (uint32_t)(kResCols * (1 + rb)), &acc[0][0], have_total);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&res_full[rb]);
+      continue;
     }
     if (have_total) tmem_fold<NP>(taddr, &acc[0][0], true, false);
 
@@ -571,14 +730,14 @@ __global__ void __launch_bounds__((NW + 4) * 32, 1)
   // no CTA may leave while a peer can still read its partials
   if (ks > 1 && unit_iter > 0) mbar_wait_cluster(done, (unit_iter - 1) & 1);
 
-  if (use_tmem) {
+  if (tmem_on) {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    // every compute warp is done with TMEM before warp 0 frees it
-    asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+    // every compute and epilogue warp is done with TMEM before warp 0 frees it
+    asm volatile("bar.sync 2, %0;" ::"n"((NW + 4) * 32) : "memory");
     if (warp == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                   "n"(kTmemCols));
+                   "r"(tmem_cols));
     }
   }
 }
@@ -707,6 +866,8 @@ void pick_tile(FfmaParams& p, int BM, int BN, int co_groups, int sms, const int*
     const double score = 1.0 / (cycles * std::max(1.0, copy_ratio));
     const int64_t patch = (int64_t)((std::min<int64_t>(th, vh) - 1) * p.sy + p.h_f) *
                           ((std::min(tw, p.w_o) - 1) * p.s + p.w_f);
+    static const int force_tw = getenv("DCONV_FORCE_TW") ? atoi(getenv("DCONV_FORCE_TW")) : 0;
+    if (force_tw && tw != force_tw) continue;  // tuning experiments only
     if (score > best_score * (1 + 1e-9) ||
         (score > best_score * (1 - 1e-9) && patch < best_patch)) {
       best_score = score;
@@ -759,7 +920,7 @@ size_t configure(FfmaParams& p, int ks, bool fine) {
   p.stage_floats = (p.patch_floats + wchunk<TCO>(CG, p.wstride_floats) + 31) & ~31;  // 128 B aligned
   const int S = p.n_g * p.n_r;
   const int kSmemBudget = 220 * 1024;
-  const int bar_bytes = (2 * kMaxStages + 2) * 8 + 16;
+  const int bar_bytes = (2 * kMaxStages + 6) * 8 + 16;
   const int red_bytes = TPX * TCO * NW * 32 * 4;  // TPX*TCO floats / thread
   p.ksplit = ks;
   p.red_floats = ks > 1 ? red_bytes / 4 : 0;
@@ -807,6 +968,14 @@ int launch_units(K kernel, int threads, FfmaParams p, size_t smem, int unit_begi
                  int unit_count, int clusters, cudaStream_t stream) {
   p.unit_begin = unit_begin;
   p.unit_count = unit_count;
+  // epilogue warpgroup hand-off for whole-K units (split-K reduces in the
+  // compute warps; the fused pool pairs pixels across lanes there)
+  static const bool no_epi_wg = getenv("DCONV_NO_EPI_WG") != nullptr;
+  p.epi_wg = (p.ksplit == 1 && !(p.epi & DCONV_EPI_MAXPOOL) && !no_epi_wg) ? 1 : 0;
+  // the epilogue warpgroup hides the skip reads behind the next tile; a
+  // producer L2 prefetch would cost a bulk op per 256-B skip row and make
+  // the single producer warp the bottleneck (measured on 1x1 layers)
+  if (p.epi_wg) p.skip_prefetch = 0;
   if (p.ksplit == 1) {
     kernel<<<clusters, threads, smem, stream>>>(p);
   } else {
@@ -833,7 +1002,7 @@ int launch_units(K kernel, int threads, FfmaParams p, size_t smem, int unit_begi
 
 template <int BM, int BN, int WF, int NW, int TPX, int TCO>
 int launch_variant(FfmaParams p, cudaStream_t stream) {
-  constexpr int threads = (NW + 4) * 32;
+  constexpr int threads = (NW + 8) * 32;
   constexpr int CG = BN / 8;
   static int sms = 0;
   if (!sms) {

@@ -40,6 +40,7 @@ struct FfmaParams {
   // each peer's copy of the output map (P2P-mapped over NVLink)
   int n_peers;
   float* peer_out[kMaxPeers];
+  int epi_wg;                  // 1: compute warps hand tiles to the epilogue warpgroup
 };
 
 extern int ffma_variant_override;  // -1 = heuristic (dconv_cuda_set_ffma_variant)

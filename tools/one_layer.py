@@ -1,5 +1,5 @@
 """Runs one conv layer a few times (for ncu / compute-sanitizer captures).
-usage: python tools/one_layer.py CI CO HI WI F S N [reps] [ffma|tf32|first]
+usage: python tools/one_layer.py CI CO HI WI F S N [reps] [ffma|tf32|first|ffma_add|tf32_add]
 (first: the first-layer reader on a dense [N][CI][HI][WI] input)"""
 import sys
 
@@ -19,11 +19,18 @@ else:
     x.buf.uniform_(-1, 1)
 w = nets.pack_weights(torch.empty((ci, co, f, f), device="cuda").uniform_(-1, 1), l.first)
 y = nets.Act(n, co, l.h_o, l.w_o)
+sk = None
+epi = 0
+if algo.endswith("_add"):  # ResNet block tail: relu(conv + skip)
+    sk = nets.Act(n, co, l.h_o, l.w_o)
+    sk.buf.uniform_(-1, 1)
+    epi = 3
+    algo = algo[:-4]
 if algo == "tf32":
     wp = nets.prepare_tf32(l, w)
-    run = lambda: nets.conv_tf32(l, n, x, wp, y)  # noqa: E731
+    run = lambda: nets.conv_tf32(l, n, x, wp, y, epi, sk)  # noqa: E731
 else:
-    run = lambda: nets.conv(l, n, x, w, y)  # noqa: E731
+    run = lambda: nets.conv(l, n, x, w, y, epi, sk)  # noqa: E731
 for _ in range(reps):
     run()
 torch.cuda.synchronize()
