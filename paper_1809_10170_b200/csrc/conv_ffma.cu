@@ -280,7 +280,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
 
   if (warp >= NW + 4) {
     // ------------------------------------------------------------ epilogue WG
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;");
     if constexpr (NW == 8 && TCO == 8) {
       if (p.epi_wg) {
         const uint32_t tmem_base = *tmem_slot;
@@ -301,27 +301,27 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
             const int jl = jb0 + cb - p.jb_begin;
             const uint32_t tr_addr = tmem_base + ((uint32_t)(qd * 32) << 16) +
                                      (uint32_t)(kResCols * (1 + rb) + half * TPX * TCO);
+            // 4 pixels at a time: their output offsets and skip pencils first
+            // (8 loads in flight per thread), then the TMEM chunks are read
+            // and stored.  Every lane runs the tcgen05.ld (warp-collective);
+            // blocks past cg_valid only skip their stores.
+            const bool blk_ok = cb < cg_valid;
 #pragma unroll 1
-            for (int kc = 0; kc < TPX / 2; ++kc) {
-              uint32_t v[16];
-              tmem_ld16(tr_addr + kc * 16, v);
-              if (cb >= cg_valid) continue;
-              // 2 pixels x 8 channels: skip pencils first (all in flight)
-              float4 sk4[4];
-              int64_t ooff[2];
-              bool ok[2];
+            for (int k4 = 0; k4 < TPX; k4 += 4) {
+              int64_t ooff[4];
+              float4 sk4[8];
 #pragma unroll
-              for (int kk = 0; kk < 2; ++kk) {
-                const int k = kc * 2 + kk;
-                const int q = pg + PG * k;
+              for (int kk = 0; kk < 4; ++kk) {
+                const int q = pg + PG * (k4 + kk);
                 const int ty = (int)__umulhi((unsigned)q, p.tw_magic), tx = q - ty * p.TW;
                 const int x = tx0 + tx;
-                ok[kk] = ty < tr.th && x < p.w_o;
+                const bool ok = blk_ok && ty < tr.th && x < p.w_o;
                 int img = 0, y = 0, prow;
-                if (ok[kk]) tile_row(p, tr, ty, img, y, prow);
-                ooff[kk] = (int64_t)jl * p.out_blk + (int64_t)img * p.out_img +
-                           (int64_t)y * p.out_row + (int64_t)x * kCB;
-                if ((p.epi & DCONV_EPI_ADD) && ok[kk]) {
+                if (ok) tile_row(p, tr, ty, img, y, prow);
+                ooff[kk] = ok ? (int64_t)jl * p.out_blk + (int64_t)img * p.out_img +
+                                    (int64_t)y * p.out_row + (int64_t)x * kCB
+                              : -1;
+                if ((p.epi & DCONV_EPI_ADD) && ok) {
                   const float4* sk = reinterpret_cast<const float4*>(
                       p.skip + (int64_t)jl * p.sk_blk + (int64_t)img * p.sk_img +
                       (int64_t)y * p.sk_row + (int64_t)x * kCB);
@@ -330,28 +330,34 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
                 }
               }
 #pragma unroll
-              for (int kk = 0; kk < 2; ++kk) {
-                if (!ok[kk]) continue;
-                float o[8];
+              for (int kc = 0; kc < 2; ++kc) {
+                uint32_t v[16];
+                tmem_ld16(tr_addr + (k4 * 8 + kc * 16), v);
 #pragma unroll
-                for (int c = 0; c < 8; ++c) o[c] = __uint_as_float(v[kk * 8 + c]);
-                if (p.epi & DCONV_EPI_ADD) {
-                  o[0] += sk4[2 * kk].x; o[1] += sk4[2 * kk].y;
-                  o[2] += sk4[2 * kk].z; o[3] += sk4[2 * kk].w;
-                  o[4] += sk4[2 * kk + 1].x; o[5] += sk4[2 * kk + 1].y;
-                  o[6] += sk4[2 * kk + 1].z; o[7] += sk4[2 * kk + 1].w;
-                }
-                if (p.epi & DCONV_EPI_RELU) {
+                for (int kj = 0; kj < 2; ++kj) {
+                  const int kk = kc * 2 + kj;
+                  if (ooff[kk] < 0) continue;
+                  float o[8];
 #pragma unroll
-                  for (int c = 0; c < 8; ++c) o[c] = fmaxf(o[c], 0.f);
-                }
-                float* dst = p.out + ooff[kk];
-                *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
-                *reinterpret_cast<float4*>(dst + 4) = make_float4(o[4], o[5], o[6], o[7]);
-                for (int pi = 0; pi < p.n_peers; ++pi) {
-                  float* pd = p.peer_out[pi] + ooff[kk];
-                  *reinterpret_cast<float4*>(pd) = make_float4(o[0], o[1], o[2], o[3]);
-                  *reinterpret_cast<float4*>(pd + 4) = make_float4(o[4], o[5], o[6], o[7]);
+                  for (int c = 0; c < 8; ++c) o[c] = __uint_as_float(v[kj * 8 + c]);
+                  if (p.epi & DCONV_EPI_ADD) {
+                    o[0] += sk4[2 * kk].x; o[1] += sk4[2 * kk].y;
+                    o[2] += sk4[2 * kk].z; o[3] += sk4[2 * kk].w;
+                    o[4] += sk4[2 * kk + 1].x; o[5] += sk4[2 * kk + 1].y;
+                    o[6] += sk4[2 * kk + 1].z; o[7] += sk4[2 * kk + 1].w;
+                  }
+                  if (p.epi & DCONV_EPI_RELU) {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) o[c] = fmaxf(o[c], 0.f);
+                  }
+                  float* dst = p.out + ooff[kk];
+                  *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+                  *reinterpret_cast<float4*>(dst + 4) = make_float4(o[4], o[5], o[6], o[7]);
+                  for (int pi = 0; pi < p.n_peers; ++pi) {
+                    float* pd = p.peer_out[pi] + ooff[kk];
+                    *reinterpret_cast<float4*>(pd) = make_float4(o[0], o[1], o[2], o[3]);
+                    *reinterpret_cast<float4*>(pd + 4) = make_float4(o[4], o[5], o[6], o[7]);
+                  }
                 }
               }
             }
@@ -375,7 +381,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
     // so a warp issues its lanes' copies one after another: the stage's
     // copies are spread over kProdWarps warps to issue them in parallel
     // (1x1 layers need ~130 row copies per unit).
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 32;");
     constexpr int kProdWarps = 4;
     const int pw = warp - NW;
     const int pt = pw * 32 + lane;  // producer thread index
@@ -452,7 +458,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
 
   // -------------------------------------------------------------- consumers
   if constexpr (NW == 8) {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 192;");
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 152;");
   }
