@@ -354,8 +354,12 @@ def main_gpu(args):
         ffma_ms = sum(statistics.median(per[s.name]) for s in plan.steps if s.kind == "tf32")
         other_ms = sum(statistics.median(per[s.name]) for s in plan.steps if s.kind != "tf32")
         peak = tf32_gemm_peak(stream)
+        pattern = None
     else:
         peak = float(lib.dconv_cuda_fp32_peak_probe(stream.cuda_stream))
+        # the kernel's own FFMA2 operand pattern without memory traffic: the
+        # practical ceiling of its instruction mix (reported beside the peak)
+        pattern = float(lib.dconv_cuda_ffma2_pattern_probe(stream.cuda_stream))
     achieved = ffma_flops / (ffma_ms * 1e-3) / 1e12 if ffma_ms else 0.0
     for rec in layers:
         if "gflops" in rec:
@@ -422,7 +426,13 @@ def main_gpu(args):
                                      if args.algo == "ffma" else
                                      "cuBLAS TF32 GEMM 8192^3 measured live (nominal 1100 dense)"),
                      "share_of_step": round(ffma_ms / (ffma_ms + other_ms), 4)
-                     if ffma_ms + other_ms else None},
+                     if ffma_ms + other_ms else None,
+                     **({"pattern_ceiling": round(pattern, 2),
+                         "frac_of_pattern_ceiling": round(achieved / pattern, 4),
+                         "pattern_note": "FFMA2 broadcast-scalar x pair from LDS.128, 8 px x 8 ch "
+                                         "per thread, no memory traffic "
+                                         "(dconv_cuda_ffma2_pattern_probe)"}
+                        if pattern else {})},
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_value, 1), "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 4)},

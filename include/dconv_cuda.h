@@ -213,6 +213,10 @@ int64_t dconv_cuda_launch_count(void);
 /* Peak FP32 FFMA throughput probe (TFLOP/s) measured with CUDA events on the
  * current device: the roofline denominator for the FFMA kernel. */
 double dconv_cuda_fp32_peak_probe(void* stream);
+/* The conv kernel's FFMA2 operand pattern (broadcast scalar x pair, LDS.128
+ * operands, 8 px x 8 ch per thread) with no memory traffic: its practical
+ * ceiling, reported beside the peak (tools/ffma2_pattern.cu). */
+double dconv_cuda_ffma2_pattern_probe(void* stream);
 
 /* ---- Tensor files --------------------------------
  * Flat little-endian file: 7 int32 header words, then the fp32 payload.

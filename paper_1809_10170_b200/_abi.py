@@ -77,6 +77,7 @@ _SIGS = {
     "dconv_cuda_set_ffma_variant": (_I, [_I]),
     "dconv_cuda_launch_count": (_L, []),
     "dconv_cuda_fp32_peak_probe": (ctypes.c_double, [_P]),
+    "dconv_cuda_ffma2_pattern_probe": (ctypes.c_double, [_P]),
     "dconv_file_payload_floats": (_L, [ctypes.POINTER(FileHeader)]),
     "dconv_file_read_header": (_I, [ctypes.c_char_p, ctypes.POINTER(FileHeader)]),
     "dconv_file_read_payload": (_I, [ctypes.c_char_p, _P, _L]),

@@ -429,6 +429,10 @@ double dconv_cuda_fp32_peak_probe(void* stream) {
   return dconv_dev::fp32_peak_probe(as_stream(stream));
 }
 
+double dconv_cuda_ffma2_pattern_probe(void* stream) {
+  return dconv_dev::ffma2_pattern_probe(as_stream(stream));
+}
+
 const char* dconv_cuda_strerror(int code) {
   switch (code) {
     case DCONV_OK: return "ok";

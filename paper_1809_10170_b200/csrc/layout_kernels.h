@@ -19,4 +19,5 @@ int launch_maxpool2x2(const float* in, int n, int n_blocks, int h, int w,
                       int c_b, float* out, int64_t o_img, int64_t o_blk,
                       int64_t o_row, cudaStream_t st);
 double fp32_peak_probe(cudaStream_t st);
+double ffma2_pattern_probe(cudaStream_t st);
 }  // namespace dconv_dev
