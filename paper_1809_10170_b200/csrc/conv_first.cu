@@ -26,12 +26,14 @@ constexpr int kCG = 8;     // output blocks per CTA
 constexpr int kPGN = 32;   // pixel groups per CTA
 
 struct FirstTile {
-  int CX, TH;              // column groups (8 px each) x rows per CTA
+  int CX, TH;              // column groups (PX px each) x rows per CTA
   int tiles_x, tiles_y;
   int PH, PW, PWs;         // patch rows, cols, padded row stride (floats)
 };
 
-template <int S, int WF>
+// PX: output pixels per thread (8; 2 for batch-1 maps, where 256-pixel
+// tiles would leave most SMs idle)
+template <int S, int WF, int PX>
 __global__ void __launch_bounds__(256, 2)
     conv_first_kernel(const GenericParams p, const FirstTile t) {
   extern __shared__ __align__(16) float smem[];
@@ -60,7 +62,7 @@ __global__ void __launch_bounds__(256, 2)
   // ---- async patch staging (zero outside the image)
   auto stage = [&](int tile, float* sp) {
     const int img = tile / tiles_img, tt = tile - img * tiles_img;
-    const int iy0 = (tt / t.tiles_x) * t.TH * S, ix0 = (tt % t.tiles_x) * t.CX * 8 * S;
+    const int iy0 = (tt / t.tiles_x) * t.TH * S, ix0 = (tt % t.tiles_x) * t.CX * PX * S;
     const float* in = p.in + (int64_t)img * p.in_img;
     const int patch = p.c_i * t.PH * t.PW;
     for (int e = tid; e < patch; e += 256) {
@@ -93,22 +95,22 @@ __global__ void __launch_bounds__(256, 2)
     __syncthreads();  // this tile's patch (and, first time, the weights) visible
     const float* sp = sp0 + buf * patch_floats;
     const int img = tile / tiles_img, tt = tile - img * tiles_img;
-    const int y0 = (tt / t.tiles_x) * t.TH, x0 = (tt % t.tiles_x) * t.CX * 8;
+    const int y0 = (tt / t.tiles_x) * t.TH, x0 = (tt % t.tiles_x) * t.CX * PX;
 
     // ---- compute: pixel group pg = (row r, column group cx); block cb
-    uint64_t acc[8][4];
+    uint64_t acc[PX][4];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
+    for (int j = 0; j < PX; ++j)
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[j][q] = 0ull;
     if (active) {
-      constexpr int L = 7 * S + WF;  // input columns feeding 8 pixels x WF taps
+      constexpr int L = (PX - 1) * S + WF;  // input columns feeding PX pixels x WF taps
       for (int c = 0; c < p.c_i; ++c) {
         // h_f == WF (square filters, checked at launch): unrolled, so the
         // accumulators stay in place across filter rows
 #pragma unroll
         for (int n = 0; n < WF; ++n) {
-          const float* row = sp + (c * t.PH + r * S + n) * t.PWs + cx * 8 * S;
+          const float* row = sp + (c * t.PH + r * S + n) * t.PWs + cx * PX * S;
           float seg[L];
 #pragma unroll
           for (int i = 0; i < L; ++i) seg[i] = row[i];
@@ -121,7 +123,7 @@ __global__ void __launch_bounds__(256, 2)
             const uint64_t bp0 = pack2(b0.x, b0.y), bp1 = pack2(b0.z, b0.w);
             const uint64_t bp2 = pack2(b1.x, b1.y), bp3 = pack2(b1.z, b1.w);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < PX; ++j) {
               const float a = seg[j * S + m];
               ffma2(acc[j][0], a, bp0);
               ffma2(acc[j][1], a, bp1);
@@ -143,8 +145,8 @@ __global__ void __launch_bounds__(256, 2)
                                       (int64_t)y * p.sk_row
                                 : nullptr;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int x = x0 + cx * 8 + j;
+    for (int j = 0; j < PX; ++j) {
+      const int x = x0 + cx * PX + j;
       if (x >= p.w_o) break;
       const float2 c0 = unpack2(acc[j][0]), c1 = unpack2(acc[j][1]);
       const float2 c2 = unpack2(acc[j][2]), c3 = unpack2(acc[j][3]);
@@ -173,22 +175,22 @@ __global__ void __launch_bounds__(256, 2)
   }
 }
 
-FirstTile pick_first_tile(const GenericParams& p, size_t w_bytes, size_t budget) {
+FirstTile pick_first_tile(const GenericParams& p, size_t w_bytes, size_t budget, int PX) {
   FirstTile best{};
   double best_eff = -1;
   size_t best_patch = 0;
-  const int max_cx = std::min(kPGN, (p.w_o + 7) / 8);
+  const int max_cx = std::min(kPGN, (p.w_o + PX - 1) / PX);
   for (int cx = 1; cx <= max_cx; ++cx) {
     const int th = std::min(kPGN / cx, p.h_o);
     if (th < 1) continue;
-    const int tx = (p.w_o + cx * 8 - 1) / (cx * 8);
+    const int tx = (p.w_o + cx * PX - 1) / (cx * PX);
     const int ty = (p.h_o + th - 1) / th;
     const int ph = (th - 1) * p.s + p.h_f;
-    const int pw = (cx * 8 - 1) * p.s + p.w_f;
+    const int pw = (cx * PX - 1) * p.s + p.w_f;
     const int pws = pw | 1;  // odd row stride: rows of a warp hit distinct banks
     const size_t patch = (size_t)p.c_i * ph * pws * 4;
     if (w_bytes + 2 * patch > budget) continue;  // double-buffered
-    const double eff = (double)p.h_o * p.w_o / ((double)tx * ty * kPGN * 8);
+    const double eff = (double)p.h_o * p.w_o / ((double)tx * ty * kPGN * PX);
     if (eff > best_eff + 1e-9 || (eff > best_eff - 1e-9 && patch < best_patch)) {
       best = FirstTile{cx, th, tx, ty, ph, pw, pws};
       best_eff = eff;
@@ -198,15 +200,13 @@ FirstTile pick_first_tile(const GenericParams& p, size_t w_bytes, size_t budget)
   return best;
 }
 
-template <int S, int WF>
-int launch_first(const GenericParams& p, cudaStream_t stream) {
+template <int S, int WF, int PX>
+int launch_first_px(const GenericParams& p, const FirstTile& t, cudaStream_t stream) {
   const size_t w_bytes = (size_t)p.h_f * WF * p.c_i * kCG * 8 * 4;
-  const size_t budget = 220 * 1024;
-  const FirstTile t = pick_first_tile(p, w_bytes, budget);
   if (t.CX == 0) return DCONV_EUNSUPPORTED;
   const size_t patch = (((size_t)p.c_i * t.PH * t.PWs + 3) & ~size_t(3)) * 4;
   const size_t smem = w_bytes + 2 * patch;  // weights + double-buffered patch
-  auto kernel = conv_first_kernel<S, WF>;
+  auto kernel = conv_first_kernel<S, WF, PX>;
   static int per_sm = 0, sms = 0;
   if (!per_sm) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -230,6 +230,27 @@ int launch_first(const GenericParams& p, cudaStream_t stream) {
   kernel<<<grid, 256, smem, stream>>>(p, t);
   dconv_host::count_launch();
   return dconv_host::check_launch("conv_first_kernel");
+}
+
+template <int S, int WF>
+int launch_first(const GenericParams& p, cudaStream_t stream) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const size_t w_bytes = (size_t)p.h_f * WF * p.c_i * kCG * 8 * 4;
+  const size_t budget = 220 * 1024;
+  const int co_groups = (p.jb_count + kCG - 1) / kCG;
+  // 8 pixels per thread unless that leaves SMs idle (batch-1 maps): then 2
+  const FirstTile t8 = pick_first_tile(p, w_bytes, budget, 8);
+  if (t8.CX == 0) return DCONV_EUNSUPPORTED;
+  if ((int64_t)t8.tiles_x * t8.tiles_y * p.n * co_groups >= sms)
+    return launch_first_px<S, WF, 8>(p, t8, stream);
+  const FirstTile t2 = pick_first_tile(p, w_bytes, budget, 2);
+  if (t2.CX == 0) return launch_first_px<S, WF, 8>(p, t8, stream);
+  return launch_first_px<S, WF, 2>(p, t2, stream);
 }
 
 }  // namespace
