@@ -76,6 +76,13 @@ __device__ __forceinline__ float ld_dsmem(const float* local_equiv, uint32_t ran
                : "memory");
   return v;
 }
+// 16-byte store into CTA `rank`'s shared memory (same offset as local_equiv)
+__device__ __forceinline__ void st_dsmem4(float* local_equiv, uint32_t rank, float4 v) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                   mapa(smem_u32(local_equiv), rank)),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
                    : "memory");

@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "conv_kernels.h"
@@ -226,6 +227,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  const long long t_start = p.dbg ? clock64() : 0;
   const int S = p.n_g * p.n_r;                 // stages per work unit
   const int co_groups = (p.jb_count + CG - 1) / CG;
   const int n_units = p.unit_count;             // this launch's units: [unit_begin, +count)
@@ -467,6 +469,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
   const int cb = (wc * 8 + (lane >> 2)) * NBLK;  // first output block within the CTA tile
 
   const uint32_t tmem_base = tmem_on ? *tmem_slot : 0u;
+  if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 1] = clock64() - t_start;  // setup done
   const uint32_t taddr = tmem_base + ((uint32_t)((warp & 3) * 32) << 16) +
                          (uint32_t)((warp >> 2) * TPX * TCO);
   const int wf = WF > 0 ? WF : p.w_f;
@@ -497,6 +500,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
     for (int st = st0; st < st1; ++st, ++gs) {
       const int buf = gs % p.NS;
       mbar_wait(&full[buf], (gs / p.NS) & 1);
+      if (p.dbg && tid == 0 && gs == 0) p.dbg[blockIdx.x * 8 + 2] = clock64() - t_start;
       const int g = st / p.n_r, r = st - g * p.n_r;
       const int Ge = min(p.G, p.ib_n - g * p.G);
       const int Re = min(p.R, p.h_f - r * p.R);
@@ -574,6 +578,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
           for (int c = 0; c < TCO / 2; ++c) acc[k][c] = 0ull;
       }
     }
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 3] = clock64() - t_start;  // loop end
     if (p.epi_wg) {
       // hand the finished tile to the epilogue warpgroup (TMEM result buffer
       // unit_iter & 1) and go on with the next unit
@@ -630,46 +635,81 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
     };
 
     if (TCO == 8 && ks > 1) {
-      // Split-K: every rank publishes its partial tile in its own smem, then
-      // rank r sums pixels [r*8/ks, (r+1)*8/ks) of every thread's 8x8 tile
-      // over ranks 0..ks-1 in that fixed order (deterministic, no global
-      // workspace).  Rolled loops: this path runs once per unit, and a
-      // compact body avoids the instruction-cache misses that dominate
-      // batch-1 layers.
+      // Split-K, push model: a thread's tile is 16 items (pixel k, channel
+      // half); item i belongs to rank owner(i) (ranks own contiguous item
+      // ranges [i*ks/16 ...]).  Every rank stores its partial of item i
+      // straight into the owner's smem slot [source rank][slot] (remote
+      // st.shared::cluster, fire-and-forget), then each owner sums its slots
+      // locally in rank order 0..ks-1: deterministic, no global workspace,
+      // and no remote-load latency on the critical path.
+      constexpr int kItems = 2 * TPX;
+      const int ipo = (kItems + ks - 1) / ks;  // items per owner, at most
+      const bool last_unit = u + n_clusters >= n_units;  // cluster-uniform
+      // owners must have read the previous unit before we overwrite
       if (unit_iter > 0) mbar_wait_cluster(done, (unit_iter - 1) & 1);
 #pragma unroll
-      for (int k = 0; k < TPX; ++k)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const float2 f = unpack2(acc[k][c]);
-          red[(k * 8 + 2 * c) * (NW * 32) + tid] = f.x;
-          red[(k * 8 + 2 * c + 1) * (NW * 32) + tid] = f.y;
-        }
-      // all compute warps' partials are in smem: one fence, ks relaxed arrives
+      for (int i = 0; i < kItems; ++i) {
+        const int k = i >> 1, hf = i & 1;
+        const int owner = ((i + 1) * ks + kItems - 1) / kItems - 1;
+        const int slot = i - owner * kItems / ks;
+        const float2 a = unpack2(acc[k][2 * hf]), b = unpack2(acc[k][2 * hf + 1]);
+        st_dsmem4(red + ((rank * ipo + slot) * (NW * 32) + tid) * 4, owner,
+                  make_float4(a.x, a.y, b.x, b.y));
+      }
+      // every compute warp's stores issued: one fence, ks relaxed arrives
       asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+      if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 4] = clock64() - t_start;  // published
       if (tid == 0) {
         fence_cluster();
         for (int q = 0; q < ks; ++q) mbar_arrive_remote_relaxed(ready, q);
       }
       mbar_wait_cluster(ready, unit_iter & 1);
+      if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 5] = clock64() - t_start;  // all ready
       if (cb < cg_valid) {
         const int jl = jb0 + cb - p.jb_begin;
+        const int i_lo = rank * kItems / ks, i_hi = (rank + 1) * kItems / ks;
 #pragma unroll 1
-        for (int k = rank * TPX / ks; k < (rank + 1) * TPX / ks; ++k) {
-          float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-          // ranks in order 0..ks-1 (fixed summation order); 4 ranks' loads in flight
+        for (int i = i_lo; i < i_hi; ++i) {
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          const float* rp = red + ((i - i_lo) * (NW * 32) + tid) * 4;
 #pragma unroll 4
-          for (int r = 0; r < ks; ++r)
-#pragma unroll
-            for (int c = 0; c < 8; ++c) v[c] += ld_dsmem(&red[(k * 8 + c) * (NW * 32) + tid], r);
-          emit(k, jl, v);
+          for (int src = 0; src < ks; ++src) {
+            const float4 t = lds128(rp + src * ipo * (NW * 32) * 4);
+            v.x += t.x; v.y += t.y; v.z += t.z; v.w += t.w;
+          }
+          // pixel i/2, channels (i&1)*4 .. +3
+          const int k = i >> 1, hf = i & 1;
+          const int q = pg + PG * k;
+          const int ty = (int)__umulhi((unsigned)q, p.tw_magic), tx = q - ty * p.TW;
+          const int x = tx0 + tx;
+          if (ty >= tr.th || x >= p.w_o) continue;
+          int img, y, prow;
+          tile_row(p, tr, ty, img, y, prow);
+          if (p.epi & DCONV_EPI_ADD) {
+            const float4 s4 = __ldg(reinterpret_cast<const float4*>(
+                p.skip + (int64_t)jl * p.sk_blk + (int64_t)img * p.sk_img + (int64_t)y * p.sk_row +
+                (int64_t)x * kCB + hf * 4));
+            v.x += s4.x; v.y += s4.y; v.z += s4.z; v.w += s4.w;
+          }
+          if (p.epi & DCONV_EPI_RELU) {
+            v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f);
+            v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
+          }
+          const int64_t off = (int64_t)jl * p.out_blk + (int64_t)img * p.out_img +
+                              (int64_t)y * p.out_row + (int64_t)x * kCB + hf * 4;
+          *reinterpret_cast<float4*>(p.out + off) = v;
+          for (int pi = 0; pi < p.n_peers; ++pi)
+            *reinterpret_cast<float4*>(p.peer_out[pi] + off) = v;
         }
       }
-      // every compute warp has consumed the peers' partials
-      asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
-      if (tid == 0) {
-        fence_cluster();
-        for (int q = 0; q < ks; ++q) mbar_arrive_remote_relaxed(done, q);
+      if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 6] = clock64() - t_start;  // reduced
+      if (!last_unit) {
+        // every compute warp has read its slots: the ranks may publish again
+        asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+        if (tid == 0) {
+          fence_cluster();
+          for (int q = 0; q < ks; ++q) mbar_arrive_remote_relaxed(done, q);
+        }
       }
     } else if (p.epi & DCONV_EPI_MAXPOOL) {
       // fused ReLU + 2x2/s2 max-pool: vertical partner in-thread (pixel
@@ -733,8 +773,10 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
       }
     }
   }
-  // no CTA may leave while a peer can still read its partials
-  if (ks > 1 && unit_iter > 0) mbar_wait_cluster(done, (unit_iter - 1) & 1);
+  // (push model: every remote access to this CTA's smem -- the peers'
+  // partial stores and arrives -- completes before its last `ready` wait, so
+  // no exit barrier is needed)
+  if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 7] = clock64() - t_start;  // exit
 
   if (tmem_on) {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -927,7 +969,8 @@ size_t configure(FfmaParams& p, int ks, bool fine) {
   const int S = p.n_g * p.n_r;
   const int kSmemBudget = 220 * 1024;
   const int bar_bytes = (2 * kMaxStages + 6) * 8 + 16;
-  const int red_bytes = TPX * TCO * NW * 32 * 4;  // TPX*TCO floats / thread
+  // split-K slots: ks sources x ceil(16 / ks) items x 4 floats per thread
+  const int red_bytes = ks * ((2 * TPX + ks - 1) / ks) * NW * 32 * 16;
   p.ksplit = ks;
   p.red_floats = ks > 1 ? red_bytes / 4 : 0;
   const int ring_budget = kSmemBudget - bar_bytes - (ks > 1 ? red_bytes : 0);
@@ -982,6 +1025,40 @@ int launch_units(K kernel, int threads, FfmaParams p, size_t smem, int unit_begi
   // producer L2 prefetch would cost a bulk op per 256-B skip row and make
   // the single producer warp the bottleneck (measured on 1x1 layers)
   if (p.epi_wg) p.skip_prefetch = 0;
+  static const bool prof = getenv("DCONV_FFMA_PROFILE") != nullptr;
+  if (prof) {  // debugging aid: per-CTA phase clocks of one extra launch
+    const int grid = p.ksplit == 1 ? clusters : clusters * p.ksplit;
+    cudaMalloc(&p.dbg, (size_t)grid * 8 * 8);
+    cudaMemset(p.dbg, 0, (size_t)grid * 8 * 8);
+    if (p.ksplit == 1) {
+      kernel<<<clusters, threads, smem, stream>>>(p);
+    } else {
+      cudaLaunchConfig_t cfg{};
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = p.ksplit;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(threads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = stream;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, kernel, p);
+    }
+    std::vector<long long> h((size_t)grid * 8);
+    cudaMemcpy(h.data(), p.dbg, h.size() * 8, cudaMemcpyDeviceToHost);
+    double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int b = 0; b < grid; ++b)
+      for (int i = 1; i < 8; ++i) a[i] += h[b * 8 + i];
+    fprintf(stderr, "conv_ffma profile: grid=%d ks=%d avg cycles: setup=%.0f first_data=%.0f "
+            "loop_end=%.0f published=%.0f all_ready=%.0f reduced=%.0f exit=%.0f\n", grid,
+            p.ksplit, a[1] / grid, a[2] / grid, a[3] / grid, a[4] / grid, a[5] / grid,
+            a[6] / grid, a[7] / grid);
+    cudaFree(p.dbg);
+    p.dbg = nullptr;
+  }
   if (p.ksplit == 1) {
     kernel<<<clusters, threads, smem, stream>>>(p);
   } else {

@@ -41,6 +41,7 @@ struct FfmaParams {
   int n_peers;
   float* peer_out[kMaxPeers];
   int epi_wg;                  // 1: compute warps hand tiles to the epilogue warpgroup
+  long long* dbg;              // DCONV_FFMA_PROFILE: per-CTA phase clocks (else null)
 };
 
 extern int ffma_variant_override;  // -1 = heuristic (dconv_cuda_set_ffma_variant)
