@@ -265,7 +265,10 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (ks > 1) cluster_sync_all();  // every rank's barriers exist before remote arrives
+  // every rank's barriers and smem must exist before the first remote access:
+  // arrive now, wait only right before the first publish (the ranks' setup
+  // and main loops overlap the barrier instead of waiting on it)
+  if (ks > 1) cluster_arrive_release();
 
   // unit u -> (co group fastest: concurrently running CTAs share the pixel
   // tile's patch rows in L2, consecutive waves reuse the weight slabs)
@@ -646,6 +649,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
       const int ipo = (kItems + ks - 1) / ks;  // items per owner, at most
       const bool last_unit = u + n_clusters >= n_units;  // cluster-uniform
       // owners must have read the previous unit before we overwrite
+      if (unit_iter == 0) cluster_wait_acquire();
       if (unit_iter > 0) mbar_wait_cluster(done, (unit_iter - 1) & 1);
 #pragma unroll
       for (int i = 0; i < kItems; ++i) {
