@@ -12,7 +12,7 @@ O=gpurun_out/round
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/nvidia_smi.txt 2>&1
 
-python bench.py > $O/bench_vgg16_ffma.log 2>&1
+T0=$SECONDS; python bench.py > $O/bench_vgg16_ffma.log 2>&1; echo "bench default wall $((SECONDS - T0)) s" > $O/bench_default_wall.txt
 for c in resnet50 googlenet alexnet cfg1; do
   python bench.py --config $c --no-cpu-baseline > $O/bench_${c}_ffma.log 2>&1
 done
