@@ -184,6 +184,14 @@ int dconv_cuda_pack_feature_map(const float* src, int n, int c, int h, int w,
 int dconv_cuda_unpack_feature_map(const float* src, int n, int c, int h, int w,
                                   int c_b, int halo, float* dst, void* stream);
 
+/* Space-to-depth repack of a dense image batch [n][c][h][w] into the blocked
+ * layout [n][ceil(c*f*f/8)][ceil(h/f)][ceil(w/f)][8]: channel (dy*f + dx)*c + ch
+ * of the result is pixel (f*y + dy, f*x + dx) of channel ch (zero outside).
+ * A stride-f first layer becomes a stride-1 blocked layer over it (the TF32
+ * path's stems); not part of the reference API. */
+int dconv_cuda_pack_space_to_depth(const float* src, int n, int c, int h, int w, int f,
+                                   float* dst, void* stream);
+
 /* Element-wise / pooling kernels in the blocked layout (count in floats). */
 int dconv_cuda_relu_blocked(float* x, int64_t count, void* stream);
 int dconv_cuda_add_blocked(const float* a, const float* b, float* out,

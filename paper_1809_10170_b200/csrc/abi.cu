@@ -357,6 +357,16 @@ int dconv_cuda_unpack_kernel(const float* src, int c_i, int c_o, int h_f,
                                          dst, as_stream(stream));
 }
 
+int dconv_cuda_pack_space_to_depth(const float* src, int n, int c, int h, int w, int f,
+                                   float* dst, void* stream) {
+  if (!src || !dst) return set_error(DCONV_EPARAM, "NULL tensor pointer");
+  if (n < 1 || c < 1 || h < 1 || w < 1 || f < 1)
+    return set_error(DCONV_EINVAL_SHAPE, "space-to-depth: dims must be >= 1");
+  if (reinterpret_cast<uintptr_t>(dst) & 15)
+    return set_error(DCONV_EPARAM, "space-to-depth: destination must be 16-byte aligned");
+  return dconv_dev::launch_pack_s2d(src, n, c, h, w, f, dst, as_stream(stream));
+}
+
 int dconv_cuda_pack_feature_map(const float* src, int n, int c, int h, int w,
                                 int c_b, int halo, float* dst, void* stream) {
   if (!src || !dst) return set_error(DCONV_EPARAM, "NULL tensor pointer");

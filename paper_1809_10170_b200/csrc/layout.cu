@@ -102,6 +102,36 @@ __global__ void pack_fm8_dev(const float* __restrict__ src, int c, int h, int w,
   }
 }
 
+// Space-to-depth + block packing of a dense image batch: output channel
+// cs = (dy*f + dx)*c + ch of the s2d map is input (ch, s*ys + dy, s*xs + dx);
+// [n][ceil(c*f*f/8)][hs][ws][8], zero outside the image and in pad channels.
+__global__ void pack_s2d8_dev(const float* __restrict__ src, int c, int h, int w, int f,
+                              int hs, int ws, int nb, int64_t pencils, float* __restrict__ dst) {
+  const int cs_n = c * f * f;
+  GRID_STRIDE(e, pencils) {
+    int64_t t = e;
+    const int xs = (int)(t % ws); t /= ws;
+    const int ys = (int)(t % hs); t /= hs;
+    const int b = (int)(t % nb);
+    const int img = (int)(t / nb);
+    float v[8];
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) {
+      const int cs = b * 8 + cc;
+      float x = 0.0f;
+      if (cs < cs_n) {
+        const int ch = cs % c, d = cs / c, dy = d / f, dx = d % f;
+        const int y = ys * f + dy, xx = xs * f + dx;
+        if (y < h && xx < w) x = __ldg(src + (((int64_t)img * c + ch) * h + y) * w + xx);
+      }
+      v[cc] = x;
+    }
+    float4* d4 = reinterpret_cast<float4*>(dst + e * 8);
+    d4[0] = make_float4(v[0], v[1], v[2], v[3]);
+    d4[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+}
+
 __global__ void unpack_fm_dev(const float* __restrict__ src, int c, int h,
                               int w, int c_b, int halo, int nb, int64_t total,
                               float* __restrict__ dst) {
@@ -211,6 +241,16 @@ int launch_pack_fm(const float* src, int n, int c, int h, int w, int c_b,
                                                total, dst);
   dconv_host::count_launch();
   return dconv_host::check_launch("pack_fm_dev");
+}
+
+int launch_pack_s2d(const float* src, int n, int c, int h, int w, int f, float* dst,
+                    cudaStream_t st) {
+  const int hs = (h + f - 1) / f, ws = (w + f - 1) / f;
+  const int nb = (c * f * f + 7) / 8;
+  const int64_t pencils = (int64_t)n * nb * hs * ws;
+  pack_s2d8_dev<<<grid_for(pencils), 256, 0, st>>>(src, c, h, w, f, hs, ws, nb, pencils, dst);
+  dconv_host::count_launch();
+  return dconv_host::check_launch("pack_s2d8_dev");
 }
 
 int launch_unpack_fm(const float* src, int n, int c, int h, int w, int c_b,

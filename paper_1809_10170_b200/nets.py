@@ -413,6 +413,8 @@ class Plan:
         w = self.weights[l.name]
         kind = "first" if l.first else "conv"
         if self.shard is None:
+            if self.algo == "tf32" and l.first and l.s > 1 and in_view is None:
+                return self._tf32_s2d_first(l, x, y, epilogue, skip)
             if self.algo == "tf32" and l.first and l.s == 1 and in_view is None:
                 # TF32 path, stride-1 first layer (VGG conv1_1): zero-pad the
                 # image to one 8-channel block (a pack kernel, SPEC.md:121's
@@ -470,6 +472,39 @@ class Plan:
         if gather:
             self._gather(l.name, y, ys)
         return ys
+
+    def _tf32_s2d_first(self, l: Layer, x, y: Act, epilogue: int, skip) -> Act:
+        """TF32 path, stride-f first layer (GoogLeNet/ResNet 7x7/s2, AlexNet
+        11x11/s4): space-to-depth turns it into a stride-1 conv with f*f*C_i
+        channels and a ceil(h_f/f) x ceil(w_f/f) filter (exact: the extra taps
+        and channels are zero weights), run on the tcgen05 kernel.  FLOPs are
+        counted with the original layer."""
+        f = l.s
+        cs = l.c_i * f * f
+        hs, ws = -(-l.h_i // f), -(-l.w_i // f)
+        hf, wf = -(-l.h_f // f), -(-l.w_f // f)
+        lb = Layer(l.name, cs, l.c_o, hs, ws, hf, wf, 1, False)
+        assert (lb.h_o, lb.w_o) == (l.h_o, l.w_o)
+        w = self.weights[l.name]
+        dense = torch.empty((l.c_i, l.c_o, l.h_f, l.w_f), dtype=torch.float32, device=w.device)
+        check(lib().dconv_cuda_unpack_kernel(ptr(w), l.c_i, l.c_o, l.h_f, l.w_f, CB, l.c_i,
+                                             ptr(dense), stream_ptr(None)))
+        # w_s2d[(dy*f + dx)*C_i + c][o][n'][m'] = w[c][o][f*n' + dy][f*m' + dx]
+        wpad = torch.zeros((l.c_i, l.c_o, hf * f, wf * f), dtype=torch.float32, device=w.device)
+        wpad[:, :, :l.h_f, :l.w_f] = dense
+        ws2d = (wpad.view(l.c_i, l.c_o, hf, f, wf, f).permute(3, 5, 0, 1, 2, 4)
+                .reshape(cs, l.c_o, hf, wf).contiguous())
+        wp = prepare_tf32(lb, pack_weights(ws2d, False))
+        self.weights[l.name + ".tf32"] = wp
+        xb = Act(self.n, cs, hs, ws, device=w.device)
+        n = self.n
+        self.steps.append(Step(
+            lambda st: check(lib().dconv_cuda_pack_space_to_depth(
+                ptr(x), n, l.c_i, l.h_i, l.w_i, f, ptr(xb.buf), stream_ptr(st))),
+            f"pack_{l.name}", "pack"))
+        self.steps.append(Step(lambda st: conv_tf32(lb, n, xb, wp, y, epilogue, skip, st),
+                               l.name, "tf32", n * l.flops, l))
+        return y
 
     def pool_into(self, name: str, src_local: Act, z: Act) -> None:
         """2x2/s2 max-pool of this rank's result into z (gathered if sharded)."""

@@ -766,3 +766,23 @@ def test_tf32_first_layer_packs_and_matches_ffma_plan():
     k = po.unpack_kernel(host(a.weights[l.name]), l.c_i, l.c_o)
     bound = 2.0 ** -9 * po.pack_feature_map(po.conv_oracle64(np.abs(x), np.abs(k), 1), 8) + 1e-5
     assert (np.abs(ya[0, :, 1:-1, 1:-1] - yb[0, :, 1:-1, 1:-1]) <= 2 * bound).all()
+
+
+@pytest.mark.parametrize("config,name", [("googlenet", "conv1_7x7_s2"), ("alexnet", "conv1")])
+def test_tf32_space_to_depth_stem_matches_reader(config, name):
+    """TF32 plans run strided stems as space-to-depth repack + stride-1
+    tcgen05 conv; the result equals the fp32 first-layer reader within the
+    TF32 bound (the s2d weights are an exact rearrangement, extra taps zero)."""
+    a = nets.build_plan(config, 1, seed=17)
+    b = nets.build_plan(config, 1, seed=17, algo="tf32")
+    assert any(s.kind == "pack" and s.name == f"pack_{name}" for s in b.steps)
+    a.run()
+    b.run()
+    torch.cuda.synchronize()
+    l = [x for x in a.layers if x.name == name][0]
+    ya, yb = host(a.outputs[name].buf), host(b.outputs[name].buf)
+    x = host(a.input)[0]
+    k = po.unpack_kernel(host(a.weights[name]), l.c_i, l.c_o)
+    bound = 2.0 ** -9 * po.pack_feature_map(po.conv_oracle64(np.abs(x), np.abs(k), l.s), 8) + 1e-5
+    assert (np.abs(ya[0] - yb[0]) <= 2 * bound).all()
+    assert np.abs(ya[0] - yb[0]).max() > 0  # the tcgen05 path really ran
