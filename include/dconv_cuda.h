@@ -192,6 +192,12 @@ int dconv_cuda_unpack_feature_map(const float* src, int n, int c, int h, int w,
 int dconv_cuda_pack_space_to_depth(const float* src, int n, int c, int h, int w, int f,
                                    float* dst, void* stream);
 
+/* The same for a blocked (c_b = 8) map view with strides in floats: a stride-f
+ * blocked layer becomes a stride-1 layer over the result (TF32 path). */
+int dconv_cuda_space_to_depth_blocked(const float* src, int64_t in_img_stride,
+                                      int64_t in_blk_stride, int64_t in_row_stride, int n, int c,
+                                      int h, int w, int f, float* dst, void* stream);
+
 /* Element-wise / pooling kernels in the blocked layout (count in floats). */
 int dconv_cuda_relu_blocked(float* x, int64_t count, void* stream);
 int dconv_cuda_add_blocked(const float* a, const float* b, float* out,

@@ -70,6 +70,7 @@ _SIGS = {
     "dconv_cuda_unpack_kernel": (_I, [_P] + [_I] * 6 + [_P, _P]),
     "dconv_cuda_pack_feature_map": (_I, [_P] + [_I] * 6 + [_P, _P]),
     "dconv_cuda_pack_space_to_depth": (_I, [_P] + [_I] * 5 + [_P, _P]),
+    "dconv_cuda_space_to_depth_blocked": (_I, [_P, _L, _L, _L] + [_I] * 5 + [_P, _P]),
     "dconv_cuda_unpack_feature_map": (_I, [_P] + [_I] * 6 + [_P, _P]),
     "dconv_cuda_relu_blocked": (_I, [_P, _L, _P]),
     "dconv_cuda_add_blocked": (_I, [_P, _P, _P, _L, _I, _P]),

@@ -367,6 +367,21 @@ int dconv_cuda_pack_space_to_depth(const float* src, int n, int c, int h, int w,
   return dconv_dev::launch_pack_s2d(src, n, c, h, w, f, dst, as_stream(stream));
 }
 
+int dconv_cuda_space_to_depth_blocked(const float* src, int64_t in_img_stride,
+                                      int64_t in_blk_stride, int64_t in_row_stride, int n, int c,
+                                      int h, int w, int f, float* dst, void* stream) {
+  if (!src || !dst) return set_error(DCONV_EPARAM, "NULL tensor pointer");
+  if (n < 1 || c < 1 || h < 1 || w < 1 || f < 1)
+    return set_error(DCONV_EINVAL_SHAPE, "space-to-depth: dims must be >= 1");
+  if (in_row_stride < (int64_t)w * 8 || in_blk_stride < (int64_t)h * in_row_stride ||
+      in_img_stride < (int64_t)((c + 7) / 8) * in_blk_stride)
+    return set_error(DCONV_ELAYOUT, "space-to-depth: input view strides smaller than the map");
+  if (reinterpret_cast<uintptr_t>(dst) & 15)
+    return set_error(DCONV_EPARAM, "space-to-depth: destination must be 16-byte aligned");
+  return dconv_dev::launch_s2d_blocked(src, in_img_stride, in_blk_stride, in_row_stride, n, c, h,
+                                       w, f, dst, as_stream(stream));
+}
+
 int dconv_cuda_pack_feature_map(const float* src, int n, int c, int h, int w,
                                 int c_b, int halo, float* dst, void* stream) {
   if (!src || !dst) return set_error(DCONV_EPARAM, "NULL tensor pointer");

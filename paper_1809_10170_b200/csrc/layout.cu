@@ -132,6 +132,52 @@ __global__ void pack_s2d8_dev(const float* __restrict__ src, int c, int h, int w
   }
 }
 
+// Space-to-depth of a blocked map view (c_b = 8 in and out): output channel
+// cs = (dy*f + dx)*c + ch at (ys, xs) is input channel ch at (f*ys+dy, f*xs+dx).
+__global__ void s2d_blocked8_dev(const float* __restrict__ src, int64_t in_img, int64_t in_blk,
+                                 int64_t in_row, int c, int h, int w, int f, int hs, int ws,
+                                 int nb, int64_t pencils, float* __restrict__ dst) {
+  const int cs_n = c * f * f;
+  GRID_STRIDE(e, pencils) {
+    int64_t t = e;
+    const int xs = (int)(t % ws); t /= ws;
+    const int ys = (int)(t % hs); t /= hs;
+    const int b = (int)(t % nb);
+    const int img = (int)(t / nb);
+    float4* d4 = reinterpret_cast<float4*>(dst + e * 8);
+    if ((c & 7) == 0) {
+      // C a multiple of 8: an output pencil is one whole input pencil
+      const int d = (b * 8) / c, ch0 = b * 8 - d * c, dy = d / f, dx = d % f;
+      const int y = ys * f + dy, xx = xs * f + dx;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), q = a;
+      if (y < h && xx < w) {
+        const float4* sp = reinterpret_cast<const float4*>(
+            src + img * in_img + (ch0 >> 3) * in_blk + y * in_row + (int64_t)xx * 8);
+        a = __ldg(sp);
+        q = __ldg(sp + 1);
+      }
+      d4[0] = a;
+      d4[1] = q;
+      continue;
+    }
+    float v[8];
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) {
+      const int cs = b * 8 + cc;
+      float x = 0.0f;
+      if (cs < cs_n) {
+        const int ch = cs % c, d = cs / c, dy = d / f, dx = d % f;
+        const int y = ys * f + dy, xx = xs * f + dx;
+        if (y < h && xx < w)
+          x = __ldg(src + img * in_img + (ch >> 3) * in_blk + y * in_row + (int64_t)xx * 8 + (ch & 7));
+      }
+      v[cc] = x;
+    }
+    d4[0] = make_float4(v[0], v[1], v[2], v[3]);
+    d4[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+}
+
 __global__ void unpack_fm_dev(const float* __restrict__ src, int c, int h,
                               int w, int c_b, int halo, int nb, int64_t total,
                               float* __restrict__ dst) {
@@ -251,6 +297,17 @@ int launch_pack_s2d(const float* src, int n, int c, int h, int w, int f, float* 
   pack_s2d8_dev<<<grid_for(pencils), 256, 0, st>>>(src, c, h, w, f, hs, ws, nb, pencils, dst);
   dconv_host::count_launch();
   return dconv_host::check_launch("pack_s2d8_dev");
+}
+
+int launch_s2d_blocked(const float* src, int64_t in_img, int64_t in_blk, int64_t in_row, int n,
+                       int c, int h, int w, int f, float* dst, cudaStream_t st) {
+  const int hs = (h + f - 1) / f, ws = (w + f - 1) / f;
+  const int nb = (c * f * f + 7) / 8;
+  const int64_t pencils = (int64_t)n * nb * hs * ws;
+  s2d_blocked8_dev<<<grid_for(pencils), 256, 0, st>>>(src, in_img, in_blk, in_row, c, h, w, f, hs,
+                                                      ws, nb, pencils, dst);
+  dconv_host::count_launch();
+  return dconv_host::check_launch("s2d_blocked8_dev");
 }
 
 int launch_unpack_fm(const float* src, int n, int c, int h, int w, int c_b,

@@ -10,6 +10,8 @@ int launch_unpack_kernel(const float* src, int c_i, int c_o, int h_f, int w_f,
                          int c_ob, int c_ib, float* dst, cudaStream_t st);
 int launch_pack_s2d(const float* src, int n, int c, int h, int w, int f, float* dst,
                     cudaStream_t st);
+int launch_s2d_blocked(const float* src, int64_t in_img, int64_t in_blk, int64_t in_row, int n,
+                       int c, int h, int w, int f, float* dst, cudaStream_t st);
 int launch_pack_fm(const float* src, int n, int c, int h, int w, int c_b,
                    int halo, float* dst, cudaStream_t st);
 int launch_unpack_fm(const float* src, int n, int c, int h, int w, int c_b,

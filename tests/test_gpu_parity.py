@@ -786,3 +786,42 @@ def test_tf32_space_to_depth_stem_matches_reader(config, name):
     bound = 2.0 ** -9 * po.pack_feature_map(po.conv_oracle64(np.abs(x), np.abs(k), l.s), 8) + 1e-5
     assert (np.abs(ya[0] - yb[0]) <= 2 * bound).all()
     assert np.abs(ya[0] - yb[0]).max() > 0  # the tcgen05 path really ran
+
+
+def test_tf32_space_to_depth_strided_blocked_layers():
+    """ResNet-50's 3x3/s2 convs on the TF32 path (blocked space-to-depth of
+    the top/left-padded input + stride-1 tcgen05 conv): each equals the FFMA
+    plan's layer output within the TF32 bound (teacher-forced: same input)."""
+    b = nets.build_plan("resnet50", 1, seed=19, algo="tf32")
+    assert sum(1 for s in b.steps if s.name.startswith("s2d_")) == 3
+    rec = {}
+    orig = nets.conv_tf32
+
+    def spy(l, n, x, wp, out, epilogue=0, skip=None, stream=None, in_view=None):
+        orig(l, n, x, wp, out, epilogue, skip, stream, in_view)
+        torch.cuda.synchronize()
+        rec[l.name] = (l, x.buf.clone(), out.buf.clone(), out, epilogue)
+    nets.conv_tf32 = spy
+    try:
+        b.run()
+    finally:
+        nets.conv_tf32 = orig
+    for name in ("s2b1_c2", "s3b1_c2", "s4b1_c2"):
+        lb, xs2d, yout, out, epi = rec[name]
+        lo = [l for _, l in nets.resnet50_layers() if l.name == name][0]
+        # undo the space-to-depth on the host: xs2d[(dy*2+dx)*C + c] at (ys, xs)
+        xs = host(xs2d)[0]
+        c, f = lo.c_i, lo.s
+        blk = xs.transpose(0, 3, 1, 2).reshape(-1, xs.shape[1], xs.shape[2])[:c * f * f]
+        x = np.zeros((c, blk.shape[1] * f, blk.shape[2] * f), np.float32)
+        for dy in range(f):
+            for dx in range(f):
+                x[:, dy::f, dx::f] = blk[(dy * f + dx) * c:(dy * f + dx + 1) * c]
+        x = x[:, :lo.h_i, :lo.w_i]
+        k = po.unpack_kernel(host(b.weights[name]), lo.c_i, lo.c_o)
+        want = po.pack_feature_map(po.conv_oracle64(x, k, f), 8)
+        if epi & _abi.EPI_RELU:
+            want = np.maximum(want, 0)
+        got = host(yout)[0][:, out.halo:out.halo + lo.h_o, out.halo:out.halo + lo.w_o]
+        bound = 2.0 ** -9 * po.pack_feature_map(po.conv_oracle64(np.abs(x), np.abs(k), f), 8) + 1e-5
+        assert (np.abs(got - want) <= bound).all(), name
