@@ -251,6 +251,34 @@ __global__ void maxpool2x2_dev(const float* __restrict__ in, int n_blocks,
   }
 }
 
+// c_b = 8: one thread per output pencil, 16-byte loads/stores (the pool is
+// HBM-bound: 4 input pencils read, one written)
+__device__ __forceinline__ float4 max4(float4 a, float4 b) {
+  return make_float4(fmaxf(a.x, b.x), fmaxf(a.y, b.y), fmaxf(a.z, b.z), fmaxf(a.w, b.w));
+}
+__global__ void maxpool2x2_8_dev(const float* __restrict__ in, int n_blocks, int h, int w,
+                                 int64_t pencils, float* __restrict__ out, int64_t o_img,
+                                 int64_t o_blk, int64_t o_row) {
+  const int ho = h / 2, wo = w / 2;
+  GRID_STRIDE(e, pencils) {
+    int64_t t = e;
+    const int x = (int)(t % wo); t /= wo;
+    const int y = (int)(t % ho); t /= ho;
+    const int b = (int)(t % n_blocks);
+    const int img = (int)(t / n_blocks);
+    const float4* p = reinterpret_cast<const float4*>(
+        in + ((((int64_t)img * n_blocks + b) * h + 2 * y) * w + 2 * x) * 8);
+    const int64_t r4 = (int64_t)w * 2;  // one input row in float4 units
+    const float4 a = max4(max4(__ldg(p), __ldg(p + 2)), max4(__ldg(p + r4), __ldg(p + r4 + 2)));
+    const float4 c = max4(max4(__ldg(p + 1), __ldg(p + 3)),
+                          max4(__ldg(p + r4 + 1), __ldg(p + r4 + 3)));
+    float4* o = reinterpret_cast<float4*>(out + (int64_t)img * o_img + (int64_t)b * o_blk +
+                                          (int64_t)y * o_row + (int64_t)x * 8);
+    o[0] = a;
+    o[1] = c;
+  }
+}
+
 }  // namespace
 
 int launch_pack_kernel(const float* src, int c_i, int c_o, int h_f, int w_f,
@@ -350,6 +378,13 @@ int launch_maxpool2x2(const float* in, int n, int n_blocks, int h, int w,
                       int c_b, float* out, int64_t o_img, int64_t o_blk,
                       int64_t o_row, cudaStream_t st) {
   const int64_t total = (int64_t)n * n_blocks * (h / 2) * (w / 2) * c_b;
+  if (c_b == 8 && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0 &&
+      ((o_img | o_blk | o_row) & 3) == 0) {
+    maxpool2x2_8_dev<<<grid_for(total / 8), 256, 0, st>>>(in, n_blocks, h, w, total / 8, out,
+                                                          o_img, o_blk, o_row);
+    dconv_host::count_launch();
+    return dconv_host::check_launch("maxpool2x2_8_dev");
+  }
   maxpool2x2_dev<<<grid_for(total), 256, 0, st>>>(in, n_blocks, h, w, c_b,
                                                   total, out, o_img, o_blk,
                                                   o_row);

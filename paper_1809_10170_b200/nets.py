@@ -674,11 +674,16 @@ def _build_resnet(p: Plan, device, seed: int) -> None:
     x0 = torch.empty((p.n, 3, 229, 229), dtype=torch.float32, device=device)
     _fill(x0, seed, 0)
     p.input = x0
-    s_out = Act(p.n, 64, 112, 112, device=device)
-    p.outputs["stem"] = s_out
-    mine = p.conv_into(stem, x0, s_out, epilogue=_abi.EPI_RELU, gather=False)
     x = Act(p.n, 64, 56, 56, device=device)
-    p.pool_into("pool_stem", mine, x)
+    if p.algo == "tf32" and p.shard is None:
+        # tcgen05 stem (space-to-depth) with ReLU + 2x2 max-pool in its epilogue
+        p.outputs["stem"] = x
+        p.conv_into(stem, x0, x, epilogue=_abi.EPI_RELU | _abi.EPI_MAXPOOL)
+    else:
+        s_out = Act(p.n, 64, 112, 112, device=device)
+        p.outputs["stem"] = s_out
+        mine = p.conv_into(stem, x0, s_out, epilogue=_abi.EPI_RELU, gather=False)
+        p.pool_into("pool_stem", mine, x)
     blocks: Dict[str, List[Layer]] = {}
     for tag, l in named[1:]:
         blocks.setdefault(tag, []).append(l)
