@@ -22,6 +22,11 @@ bool aligned16(const void* p) {
 }  // namespace
 
 namespace dconv_host {
+bool pdl_enabled() {
+  static const bool on = getenv("DCONV_NO_PDL") == nullptr;
+  return on;
+}
+
 int set_error(int code, const char* fmt, ...) {
   va_list ap;
   va_start(ap, fmt);

@@ -156,6 +156,16 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// Programmatic dependent launch: a kernel launched with the
+// programmatic-stream-serialization attribute may start while the previous
+// kernel in the stream is still running; it must pdl_wait() before touching
+// data that kernel produces.  pdl_launch_dependents() lets the next kernel
+// start launching (it still waits for this grid in its own pdl_wait).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Warm L2 with [src, src + bytes) (bytes a multiple of 16); no completion.
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
@@ -188,6 +198,7 @@ __device__ __forceinline__ float4 lds128(const float* p) {
 
 // Host-side helpers shared by the launchers (defined in abi.cu).
 namespace dconv_host {
+bool pdl_enabled();  // DCONV_NO_PDL unset
 int set_error(int code, const char* fmt, ...);
 int check_launch(const char* kernel);
 void count_launch();

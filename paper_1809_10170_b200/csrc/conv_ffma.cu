@@ -265,6 +265,10 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // setup above overlaps the previous kernel's tail (programmatic dependent
+  // launch); its output is read only from here on
+  pdl_wait();
+  pdl_launch_dependents();
   // every rank's barriers and smem must exist before the first remote access:
   // arrive now, wait only right before the first publish (the ranks' setup
   // and main loops overlap the barrier instead of waiting on it)
@@ -1063,21 +1067,28 @@ int launch_units(K kernel, int threads, FfmaParams p, size_t smem, int unit_begi
     cudaFree(p.dbg);
     p.dbg = nullptr;
   }
-  if (p.ksplit == 1) {
-    kernel<<<clusters, threads, smem, stream>>>(p);
-  } else {
+  {
     cudaLaunchConfig_t cfg{};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = p.ksplit;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (p.ksplit > 1) {
+      attr[na].id = cudaLaunchAttributeClusterDimension;
+      attr[na].val.clusterDim.x = p.ksplit;
+      attr[na].val.clusterDim.y = 1;
+      attr[na].val.clusterDim.z = 1;
+      ++na;
+    }
+    if (dconv_host::pdl_enabled()) {
+      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[na].val.programmaticStreamSerializationAllowed = 1;
+      ++na;
+    }
     cfg.gridDim = dim3(clusters * p.ksplit);
     cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, p);
     if (e != cudaSuccess)
       return dconv_host::set_error(DCONV_ECUDA, "conv_ffma (cluster %d): %s", p.ksplit,

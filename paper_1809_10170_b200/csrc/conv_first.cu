@@ -48,6 +48,8 @@ __global__ void __launch_bounds__(256, 2)
   const int jb0 = p.jb_begin + blockIdx.y * kCG;
   const int cg_valid = min(kCG, p.jb_begin + p.jb_count - jb0);
 
+  pdl_wait();  // programmatic dependent launch: input readable from here on
+  pdl_launch_dependents();
   // ---- stage weights once: global [jb][n][m][c][8] -> smem [(n,m,c)][half][cb][4]
   for (int e = tid; e < taps_c * kCG * 2; e += 256) {
     const int half = e & 1;
@@ -227,7 +229,19 @@ int launch_first_px(const GenericParams& p, const FirstTile& t, cudaStream_t str
   // the output-block groups
   const int slots = std::max(1, sms * occ / co_groups);
   dim3 grid((unsigned)std::min(n_tiles, slots), (unsigned)co_groups);
-  kernel<<<grid, 256, smem, stream>>>(p, t);
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = dconv_host::pdl_enabled() ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, p, t);
+  if (e != cudaSuccess)
+    return dconv_host::set_error(DCONV_ECUDA, "conv_first: %s", cudaGetErrorString(e));
   dconv_host::count_launch();
   return dconv_host::check_launch("conv_first_kernel");
 }

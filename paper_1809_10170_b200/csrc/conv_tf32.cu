@@ -185,6 +185,8 @@ __global__ void __launch_bounds__(kThreadsT, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // programmatic dependent launch: input readable from here on
+  pdl_launch_dependents();
 
   // unit u -> (channel group fastest, then strip, row group, image)
   auto decode = [&](int u, int& img, int& y0, int& x0, int& cg) {
@@ -663,7 +665,21 @@ int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t
     cudaFree(p.dbg);
     p.dbg = nullptr;
   }
-  pick_tf32_kernel(p)<<<grid, kThreadsT, smem, stream>>>(map, p);
+  {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreadsT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = dconv_host::pdl_enabled() ? 1 : 0;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, pick_tf32_kernel(p), map, p);
+    if (e != cudaSuccess)
+      return dconv_host::set_error(DCONV_ECUDA, "conv_tf32: %s", cudaGetErrorString(e));
+  }
   dconv_host::count_launch();
   return dconv_host::check_launch("conv_tf32_kernel");
 }
