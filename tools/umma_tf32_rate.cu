@@ -21,7 +21,7 @@ __device__ __forceinline__ uint64_t desc(uint32_t saddr, uint32_t lbo, uint32_t 
 // MODE 1: the conv kernel's descriptor walk -- A from a [plane][PH][PW][4]
 // patch (LBO = plane bytes, SBO = PW*16), taps (n, m) shift the A start by
 // (n*PW + m)*16 B, MT = 4 M-tiles at 16*PW*16 B; B walks 9 taps of 2*N*16 B.
-template <int N, int NACC, int MODE = 0>
+template <int N, int NACC, int MODE = 0, int M = 128>
 __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long* out, int a_stride, int commit_every) {
   extern __shared__ __align__(1024) float smem[];
   __shared__ uint64_t bar, bar2;
@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long* o
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tslot;
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
-                         ((uint32_t)(128 >> 4) << 24);
+                         ((uint32_t)(M >> 4) << 24);
   long long t0 = 0, t1 = 0;
   if (threadIdx.x == 0) {
     const uint32_t a0 = smem_u32(A), b0 = smem_u32(B);
@@ -94,27 +94,27 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long* o
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-template <int N, int NACC, int MODE = 0>
+template <int N, int NACC, int MODE = 0, int M = 128>
 void run(int sms, int a_stride, int commit_every = 0) {
   unsigned long long* d;
   cudaMalloc(&d, sms * 8);
   const int iters = 20000;
   const size_t smem = (12 * 1024 + 4 * N * 4) * 4 + 1024;
-  cudaFuncSetAttribute(probe<N, NACC, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  probe<N, NACC, MODE><<<sms, 128, smem>>>(iters, d, a_stride, commit_every);
+  cudaFuncSetAttribute(probe<N, NACC, MODE, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  probe<N, NACC, MODE, M><<<sms, 128, smem>>>(iters, d, a_stride, commit_every);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  probe<N, NACC, MODE><<<sms, 128, smem>>>(iters, d, a_stride, commit_every);
+  probe<N, NACC, MODE, M><<<sms, 128, smem>>>(iters, d, a_stride, commit_every);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms;
   cudaEventElapsedTime(&ms, e0, e1);
   unsigned long long h = 0;
   cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-  const double flops = 2.0 * 128 * N * 8 * iters * sms;
-  printf("commit/%d mode %d N=%3d acc-sets=%d a_step/PW=%3d: %.1f cycles/MMA, %.0f TFLOP/s  (%s)\n", commit_every, MODE, N, NACC, a_stride,
+  const double flops = 2.0 * M * N * 8 * iters * sms;
+  printf("M=%d commit/%d mode %d N=%3d acc-sets=%d a_step/PW=%3d: %.1f cycles/MMA, %.0f TFLOP/s  (%s)\n", M, commit_every, MODE, N, NACC, a_stride,
          (double)h / iters, flops / ms / 1e9, cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
@@ -132,7 +132,8 @@ int main() {
   run<128, 4, 1>(sms, 8);   // PW = 8 (SBO 128)
   run<128, 4, 1>(sms, 16);  // PW = 16 (SBO 256)
   run<64, 4, 1>(sms, 10);
-  run<128, 4, 1>(sms, 10, 36);
-  run<128, 4, 1>(sms, 10, 4);
+  run<64, 1, 0, 64>(sms, 0);
+  run<128, 1, 0, 64>(sms, 0);
+  run<256, 1, 0, 64>(sms, 0);
   return 0;
 }
