@@ -41,6 +41,24 @@ namespace {
 constexpr int kCB = 8;          // channel block of this kernel (c_ib = c_ob)
 constexpr int kMaxStages = 8;
 constexpr int kMaxKs = 16;      // split-K cluster size (> 8 is the non-portable opt-in)
+
+// Tuning / debugging overrides, read once per process.
+struct Knobs {
+  int force_g = 0, flush_every = 0, ksplit = 0;
+  bool no_splitk = false, no_tailsplit = false, debug = false;
+  Knobs() {
+    if (const char* e = getenv("DCONV_FORCE_G")) force_g = atoi(e);
+    if (const char* e = getenv("DCONV_FLUSH_EVERY")) flush_every = atoi(e);
+    if (const char* e = getenv("DCONV_KSPLIT")) ksplit = atoi(e);
+    no_splitk = getenv("DCONV_NO_SPLITK") != nullptr;
+    no_tailsplit = getenv("DCONV_NO_TAILSPLIT") != nullptr;
+    debug = getenv("DCONV_DEBUG") != nullptr;
+  }
+};
+const Knobs& knobs() {
+  static const Knobs k;
+  return k;
+}
 constexpr int kComputeWarps = 8;  // default: 2 compute warpgroups, 8x8 outputs / thread
 constexpr int kThreads = (kComputeWarps + 4) * 32;  // + producer warpgroup
 
@@ -960,7 +978,7 @@ size_t configure(FfmaParams& p, int ks, bool fine) {
       const int per_block = patch1 + CG * p.R * p.w_f * kCB * kCB * 4;
       p.G = std::max(1, std::min(p.G, (36 * 1024) / per_block));
     }
-    if (const char* e = getenv("DCONV_FORCE_G")) p.G = std::max(1, std::min(p.ib_n, atoi(e)));
+    if (knobs().force_g) p.G = std::max(1, std::min(p.ib_n, knobs().force_g));
   } else {
     p.G = 1;
     p.R = std::max(1, kWeightBudget / (CG * p.w_f * kCB * kCB * 4));
@@ -988,7 +1006,7 @@ size_t configure(FfmaParams& p, int ks, bool fine) {
   // partial sums cover >= 256 products before folding into the TMEM total
   const int k_stage = p.G * p.R * p.w_f * kCB;
   p.flush_every = std::max(1, (256 + k_stage - 1) / k_stage);
-  if (const char* e = getenv("DCONV_FLUSH_EVERY")) p.flush_every = std::max(1, atoi(e));
+  if (knobs().flush_every) p.flush_every = std::max(1, knobs().flush_every);
   if (p.NS < 2) return 0;
   return (size_t)p.NS * p.stage_floats * 4 + (ks > 1 ? red_bytes : 0) + bar_bytes;
 }
@@ -1117,7 +1135,7 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
     attr_set = true;
   }
   // only the 8-warp 8x8-per-thread tile has the DSMEM split-K reduction
-  const bool no_split = getenv("DCONV_NO_SPLITK") != nullptr || NW != 8 || TPX != 8 ||
+  const bool no_split = knobs().no_splitk || NW != 8 || TPX != 8 ||
                         TCO != 8 || (p.epi & DCONV_EPI_MAXPOOL);
   int slots[kMaxKs + 1] = {0};
   slots[1] = sms;
@@ -1147,13 +1165,13 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
     if (configure<BN, NW, TPX, TCO>(t, 2, true))
       best_ks = best_split(units, slots, t.n_g * t.n_r, unit_cycles(p, BM, BN), nullptr);
   }
-  if (const char* e = getenv("DCONV_KSPLIT")) best_ks = std::max(1, std::min(atoi(e), std::min(kMaxKs, S)));
+  if (knobs().ksplit) best_ks = std::max(1, std::min(knobs().ksplit, std::min(kMaxKs, S)));
   if (best_ks > 1) {
     FfmaParams r = p;
     const size_t smem = configure<BN, NW, TPX, TCO>(r, best_ks, true);
     if (!smem) return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_ffma: split stage");
     const int clusters = std::min(units, std::max(1, cluster_slots(kernel, best_ks, sms, threads)));
-    if (getenv("DCONV_DEBUG"))
+    if (knobs().debug)
       fprintf(stderr, "conv_ffma<%d,%d,%d>: split TH=%d TW=%d units=%d ks=%d clusters=%d S=%d\n",
               BM, BN, WF, r.TH, r.TW, units, best_ks, clusters, r.n_g * r.n_r);
     return launch_units(kernel, threads, r, smem, 0, units, clusters, stream);
@@ -1165,7 +1183,7 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   const int main_units = units / sms * sms, tail = units - main_units;
   int tail_ks = 1;
   if (main_units > 0 && tail > 0 && tail * 4 < sms * 3 && !no_split &&
-      !getenv("DCONV_NO_TAILSPLIT")) {
+      !knobs().no_tailsplit) {
     static const bool pow2_only = getenv("DCONV_TAIL_POW2") != nullptr;
     for (int ks = kMaxKs; ks >= 2; ks = pow2_only ? ks / 2 : ks - 1) {
       FfmaParams t = p;
@@ -1179,10 +1197,10 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
     }
   }
   const size_t smem_main = configure<BN, NW, TPX, TCO>(q, 1, fine);
-  if (getenv("DCONV_DEBUG") && tail_ks > 1)
+  if (knobs().debug && tail_ks > 1)
     for (int ks = 2; ks <= kMaxKs; ++ks)
       fprintf(stderr, "  cluster_slots(%d) = %d\n", ks, cluster_slots(kernel, ks, sms, threads));
-  if (getenv("DCONV_DEBUG"))
+  if (knobs().debug)
     fprintf(stderr,
             "conv_ffma<%d,%d,%d>: %dx%d tiles TH=%d TW=%d units=%d S=%d G=%d R=%d NS=%d "
             "main=%d tail=%d tail_ks=%d\n",

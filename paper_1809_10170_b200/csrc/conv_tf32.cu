@@ -581,7 +581,8 @@ int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t
         p.MT = mt;
       }
     }
-    if (const char* e = getenv("DCONV_TF32_MT"))
+    static const char* force_mt = getenv("DCONV_TF32_MT");
+    if (const char* e = force_mt)
       p.MT = std::max(1, std::min(std::min(kMaxMT, 512 / p.N), atoi(e)));
   }
   const int patch_blk_bytes = 2 * (p.MT * kTileRows - 1 + p.h_f) * p.PW * 16;  // both planes
