@@ -642,8 +642,11 @@ def _build_vgg(p: Plan, device, seed: int) -> None:
     for i, l in enumerate(layers):
         last = i == len(layers) - 1
         pool = l.name in VGG16_POOL_AFTER
+        # FFMA: the fused pool epilogue (conv_ffma EPI_MAXPOOL) ties the
+        # separate pencil pool kernel on VGG b32 (54.28 vs 54.29 TFLOP/s) and
+        # loses with the untuned tile choice, so it is opt-in
         fuse_ffma = (p.algo == "ffma" and l.w_o % 16 == 0 and l.h_o % 2 == 0
-                     and os.environ.get("DCONV_NO_POOL_FUSION") is None)
+                     and os.environ.get("DCONV_POOL_FUSION") is not None)
         if pool and (p.algo == "tf32" or fuse_ffma) and p.shard is None and not l.first:
             # conv + ReLU + 2x2 max-pool in one kernel, straight into the next
             # layer's halo buffer (the full-resolution map is never written).
