@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-tune", action="store_true",
                     help="skip the per-layer CTA-tile autotune at plan build")
-    ap.add_argument("--algo", default="ffma", choices=["ffma", "tf32"],
+    ap.add_argument("--algo", default="ffma", choices=["ffma", "tf32", "tf32x3"],
                     help="ffma: the fp32 FFMA path (the headline); tf32: stride-1 layers on "
                          "the tcgen05/TMEM TF32 variant (reduced precision, reported apart)")
     ap.add_argument("--shard", default="batch", choices=["batch", "co"],
@@ -347,7 +347,7 @@ def main_gpu(args):
             ffma_ms += ms
         else:
             other_ms += ms
-    if args.algo == "tf32":
+    if args.algo in ("tf32", "tf32x3"):
         # tensor-core roofline: the tcgen05 launches against a cuBLAS TF32 GEMM
         # (8192^3, torch.matmul with TF32 allowed) measured live on this GPU
         ffma_flops = sum(s.flops for s in plan.steps if s.kind == "tf32")
@@ -355,6 +355,11 @@ def main_gpu(args):
         other_ms = sum(statistics.median(per[s.name]) for s in plan.steps if s.kind != "tf32")
         peak = tf32_gemm_peak(stream)
         pattern = None
+        if args.algo == "tf32x3":
+            # split-TF32 issues three TF32 MMAs per product: the tensor pipe
+            # does 3x the algorithmic FLOPs (reported as such against the
+            # TF32 peak; fp32-equivalent rate = achieved / 3)
+            ffma_flops *= 3
     else:
         peak = float(lib.dconv_cuda_fp32_peak_probe(stream.cuda_stream))
         # the kernel's own FFMA2 operand pattern without memory traffic: the
@@ -396,7 +401,8 @@ def main_gpu(args):
         "metric": METRIC, "value": round(value, 1), "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f32" if args.algo == "ffma" else "tf32 (stride-1 layers) + f32",
+        "dtype": {"ffma": "f32", "tf32": "tf32 (stride-1 layers) + f32",
+                  "tf32x3": "f32 (split-TF32 x3 on tcgen05, fp32 tolerance) + f32"}[args.algo],
         "data": "synthetic (seeded uniform[-1,1), counter-based generator)",
         "mode": ("C_o-block sharding + " + ("fused peer-store gather (symmetric memory, "
                                             "NVLink) + device barrier per layer"
@@ -420,7 +426,10 @@ def main_gpu(args):
                      "traffic": traffic, "traffic_note": traffic_note,
                      "kernel": ("conv_ffma_kernel (all blocked conv launches of the step)"
                                 if args.algo == "ffma" else
-                                "conv_tf32_kernel (all stride-1 blocked conv launches)"),
+                                "conv_tf32_kernel (all stride-1 blocked conv launches)"
+                                if args.algo == "tf32" else
+                                "conv_tf32x3_kernel (all tensor-core launches; achieved counts "
+                                "the 3 TF32 MMAs per product, fp32-equivalent = achieved / 3)"),
                      "peak_source": ("FFMA2 throughput probe measured live on this GPU "
                                      f"(nominal {NOMINAL_FP32_TFLOPS:.1f} at 1965 MHz)"
                                      if args.algo == "ffma" else

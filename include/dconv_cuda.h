@@ -78,7 +78,8 @@ enum {
   DCONV_ALGO_AUTO = 0,     /* fast FFMA path when c_ib == c_ob == 8, else generic */
   DCONV_ALGO_FFMA = 1,     /* register-blocked FFMA kernel (c_ib == c_ob == 8) */
   DCONV_ALGO_GENERIC = 2,  /* any (c_ib, c_ob); slow reference-order kernel */
-  DCONV_ALGO_TF32 = 3      /* tcgen05/TMEM TF32 variant (looser tolerance) */
+  DCONV_ALGO_TF32 = 3,     /* tcgen05/TMEM TF32 variant (looser tolerance) */
+  DCONV_ALGO_TF32X3 = 4    /* split-TF32 tensor-core variant, fp32 tolerance */
 };
 
 /* One convolution layer over a batch of blocked feature maps.
@@ -142,6 +143,21 @@ int dconv_cuda_prepare_tf32_weights(const dconv_conv_desc* d, const float* w_blo
 int dconv_cuda_conv_direct_tf32(const dconv_conv_desc* d, const float* in,
                                 const float* w_prepared, const float* skip, float* out,
                                 void* stream);
+
+/* Split-TF32 tensor-core variant with the fp32 tolerance of the FFMA path
+ * (|a-b| <= 1e-4 + 1e-5|b| against conv_oracle64, reference.cpp:70-87):
+ * x = x_hi + x_lo, w = w_hi + w_lo, three TF32 MMAs per tap
+ * (x_hi*w_lo + x_lo*w_hi + x_hi*w_hi) with the reduction summed in chunks
+ * of ~288 products (TMEM chunk accumulators, fp32 register totals).  Same
+ * geometry limits and contract as the TF32 calls; the activation split
+ * happens in shared memory (no workspace); the prepared weights hold hi and
+ * lo halves (2x the TF32 buffer). */
+int dconv_cuda_tf32x3_prepared_size(const dconv_conv_desc* d, int64_t* floats);
+int dconv_cuda_prepare_tf32x3_weights(const dconv_conv_desc* d, const float* w_blocked,
+                                      float* w_prepared, void* stream);
+int dconv_cuda_conv_direct_tf32x3(const dconv_conv_desc* d, const float* in,
+                                  const float* w_prepared, const float* skip, float* out,
+                                  void* stream);
 
 /* First layer: dense [N][C_i][H_i][W_i] input (the paper does not impose the
  * blocked layout on network inputs) -> blocked output.

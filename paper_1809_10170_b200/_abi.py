@@ -60,6 +60,9 @@ _SIGS = {
     "dconv_cuda_tf32_prepared_size": (_I, [ctypes.POINTER(ConvDesc), ctypes.POINTER(_L)]),
     "dconv_cuda_prepare_tf32_weights": (_I, [ctypes.POINTER(ConvDesc), _P, _P, _P]),
     "dconv_cuda_conv_direct_tf32": (_I, [ctypes.POINTER(ConvDesc), _P, _P, _P, _P, _P]),
+    "dconv_cuda_tf32x3_prepared_size": (_I, [ctypes.POINTER(ConvDesc), ctypes.POINTER(_L)]),
+    "dconv_cuda_prepare_tf32x3_weights": (_I, [ctypes.POINTER(ConvDesc), _P, _P, _P]),
+    "dconv_cuda_conv_direct_tf32x3": (_I, [ctypes.POINTER(ConvDesc), _P, _P, _P, _P, _P]),
     "dconv_cuda_conv_first_layer": (
         _I, [ctypes.POINTER(ConvDesc), _P, _L, _P, _P, _P, _P]),
     "dconv_cuda_conv_direct_peers": (

@@ -239,7 +239,8 @@ int dconv_cuda_conv_direct_peers(const dconv_conv_desc* d, const float* in, cons
   return conv_direct_impl(d, in, w, skip, out, peer_outs, n_peers, stream);
 }
 
-int dconv_cuda_tf32_prepared_size(const dconv_conv_desc* d, int64_t* floats) {
+namespace {
+int tf32_prepared_size_impl(const dconv_conv_desc* d, int64_t* floats, bool x3) {
   if (!d || !floats) return set_error(DCONV_EPARAM, "NULL argument");
   Resolved r;
   static const float dummy = 0.f;
@@ -249,26 +250,29 @@ int dconv_cuda_tf32_prepared_size(const dconv_conv_desc* d, int64_t* floats) {
   if (rc) return rc;
   if (d->c_ib != 8 || d->c_ob != 8)
     return set_error(DCONV_EUNSUPPORTED, "TF32 path needs c_ib == c_ob == 8");
-  *floats = dconv_dev::tf32_prepared_floats(r.ib_n, d->h_f, d->w_f, r.jb_count);
+  *floats = x3 ? dconv_dev::tf32x3_prepared_floats(r.ib_n, d->h_f, d->w_f, r.jb_count)
+               : dconv_dev::tf32_prepared_floats(r.ib_n, d->h_f, d->w_f, r.jb_count);
   return DCONV_OK;
 }
 
-int dconv_cuda_prepare_tf32_weights(const dconv_conv_desc* d, const float* w,
-                                    float* w_prepared, void* stream) {
+int prepare_tf32_impl(const dconv_conv_desc* d, const float* w, float* w_prepared, void* stream,
+                      bool x3) {
   Resolved r;
+  if (!d) return set_error(DCONV_EPARAM, "NULL argument");
   dconv_conv_desc geom = *d;
   geom.epilogue = DCONV_EPI_NONE;
   int rc = resolve(&geom, false, 0, w, w, nullptr, w_prepared, &r);
   if (rc) return rc;
   if (d->c_ib != 8 || d->c_ob != 8)
     return set_error(DCONV_EUNSUPPORTED, "TF32 path needs c_ib == c_ob == 8");
-  return dconv_dev::launch_prepare_tf32(w, r.ib_n, d->h_f, d->w_f, r.jb_begin, r.jb_count,
-                                        w_prepared, as_stream(stream));
+  return x3 ? dconv_dev::launch_prepare_tf32x3(w, r.ib_n, d->h_f, d->w_f, r.jb_begin, r.jb_count,
+                                               w_prepared, as_stream(stream))
+            : dconv_dev::launch_prepare_tf32(w, r.ib_n, d->h_f, d->w_f, r.jb_begin, r.jb_count,
+                                             w_prepared, as_stream(stream));
 }
 
-int dconv_cuda_conv_direct_tf32(const dconv_conv_desc* d, const float* in,
-                                const float* w_prepared, const float* skip, float* out,
-                                void* stream) {
+int conv_tf32_impl(const dconv_conv_desc* d, const float* in, const float* w_prepared,
+                   const float* skip, float* out, void* stream, bool x3) {
   Resolved r;
   int rc = resolve(d, false, 0, in, w_prepared, skip, out, &r);
   if (rc) return rc;
@@ -286,7 +290,34 @@ int dconv_cuda_conv_direct_tf32(const dconv_conv_desc* d, const float* in,
   p.out_img = r.out_img; p.out_blk = r.out_blk; p.out_row = r.out_row;
   p.sk_img = r.sk_img; p.sk_blk = r.sk_blk; p.sk_row = r.sk_row;
   p.epi = d->epilogue;
-  return dconv_dev::launch_conv_tf32(p, w_prepared, as_stream(stream));
+  return x3 ? dconv_dev::launch_conv_tf32x3(p, w_prepared, as_stream(stream))
+            : dconv_dev::launch_conv_tf32(p, w_prepared, as_stream(stream));
+}
+}  // namespace
+
+int dconv_cuda_tf32_prepared_size(const dconv_conv_desc* d, int64_t* floats) {
+  return tf32_prepared_size_impl(d, floats, false);
+}
+int dconv_cuda_prepare_tf32_weights(const dconv_conv_desc* d, const float* w,
+                                    float* w_prepared, void* stream) {
+  return prepare_tf32_impl(d, w, w_prepared, stream, false);
+}
+int dconv_cuda_conv_direct_tf32(const dconv_conv_desc* d, const float* in,
+                                const float* w_prepared, const float* skip, float* out,
+                                void* stream) {
+  return conv_tf32_impl(d, in, w_prepared, skip, out, stream, false);
+}
+int dconv_cuda_tf32x3_prepared_size(const dconv_conv_desc* d, int64_t* floats) {
+  return tf32_prepared_size_impl(d, floats, true);
+}
+int dconv_cuda_prepare_tf32x3_weights(const dconv_conv_desc* d, const float* w,
+                                      float* w_prepared, void* stream) {
+  return prepare_tf32_impl(d, w, w_prepared, stream, true);
+}
+int dconv_cuda_conv_direct_tf32x3(const dconv_conv_desc* d, const float* in,
+                                  const float* w_prepared, const float* skip, float* out,
+                                  void* stream) {
+  return conv_tf32_impl(d, in, w_prepared, skip, out, stream, true);
 }
 
 namespace {

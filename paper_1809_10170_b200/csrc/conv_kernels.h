@@ -55,6 +55,13 @@ int launch_prepare_tf32(const float* w, int ib_n, int h_f, int w_f, int jb_begin
                         float* out, cudaStream_t stream);
 int launch_conv_tf32(const FfmaParams& p, const float* w_prepared, cudaStream_t stream);
 
+// split-TF32 variant (conv_tf32x3.cu): fp32 tolerance on the tensor cores;
+// weights prepared once into hi/lo operand pairs.
+int64_t tf32x3_prepared_floats(int ib_n, int h_f, int w_f, int jb_count);
+int launch_prepare_tf32x3(const float* w, int ib_n, int h_f, int w_f, int jb_begin, int jb_count,
+                          float* out, cudaStream_t stream);
+int launch_conv_tf32x3(const FfmaParams& p, const float* w_prepared, cudaStream_t stream);
+
 // Generic (any c_ib / c_ob) reference-order kernel and the first-layer reader.
 struct GenericParams {
   const float* in;

@@ -29,118 +29,15 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
-#include "common.cuh"
-#include "conv_kernels.h"
+#include "tf32_common.cuh"
 
 namespace dconv_dev {
 
 namespace {
 
-constexpr int kMaxMT = 4;       // M-tiles (128 pixels each) per work unit, at most
-constexpr int kTileRows = 16;   // an M-tile is 16 output rows x 8 columns
-constexpr int kTW = 8;
-constexpr int kMaxStagesT = 8;
+using namespace tf32;
 constexpr int kEpiWarps = 8;   // 2 per TMEM lane quarter, each half of the columns
 constexpr int kThreadsT = (2 + kEpiWarps) * 32;
-
-struct Tf32Params {
-  const float* w;     // prepared weights
-  const float* skip;
-  float* out;
-  int n, h_i, w_i, h_o, w_o, h_f, w_f;
-  int ib_n, jb_begin, jb_count;
-  int N;              // channels per work unit (64 or 128), 8 | N
-  int n_cg;           // channel groups
-  int64_t out_img, out_blk, out_row, sk_img, sk_blk, sk_row;
-  int epi;
-  int G, R, n_g, n_r, PH, PW;
-  int plane_floats;   // one channel half-plane of a stage: G*PH*PW*4
-  int wstage_floats;  // G*R*w_f*2*N*4
-  int stage_floats;
-  int NS;
-  int row_groups, strips, units;
-  int MT;             // M-tiles per unit (1..4)
-  uint32_t idesc;
-  unsigned long long* dbg;  // DCONV_TF32_PROFILE: per-CTA wait cycles (else null)
-};
-
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1 << 46;  // descriptor version 1 (sm_100); no swizzle, base offset 0
-  return d;
-}
-
-__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, int c0, int c1,
-                                            int c2, int c3, int c4, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
-      "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
-                                          uint32_t accumulate) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
-// Issued by one elected lane of a converged warp (elect.sync); the
-// descriptors come in as 32-bit halves so the loop arithmetic stays 32-bit.
-__device__ __forceinline__ void umma_tf32_elect(uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi,
-                                                uint32_t b_lo, uint32_t b_hi, uint32_t idesc,
-                                                uint32_t accumulate) {
-  asm volatile(
-      "{\n.reg .pred e, p;\n.reg .b64 ad, bd;\n"
-      "mov.b64 ad, {%1, %2};\nmov.b64 bd, {%3, %4};\n"
-      "setp.ne.b32 p, %6, 0;\n"
-      "elect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ad, bd, %5, p;\n}\n" ::"r"(d_tmem),
-      "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
-  asm volatile(
-      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
-          smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld32x32(uint32_t taddr, float (&v)[32]) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, "
-      "%8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, "
-      "%23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
-        "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),
-        "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
-        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]),
-        "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr)
-      : "memory");
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
 
 // WF_T / MT_T: filter width and M-tiles per unit as compile-time constants
 // (0 = runtime), so the per-stage MMA walk unrolls into straight-line issue.
@@ -188,16 +85,8 @@ __global__ void __launch_bounds__(kThreadsT, 1)
   pdl_wait();  // programmatic dependent launch: input readable from here on
   pdl_launch_dependents();
 
-  // unit u -> (channel group fastest, then strip, row group, image)
   auto decode = [&](int u, int& img, int& y0, int& x0, int& cg) {
-    cg = u % p.n_cg;
-    int t = u / p.n_cg;
-    const int strip = t % p.strips;
-    t /= p.strips;
-    const int rg = t % p.row_groups;
-    img = t / p.row_groups;
-    y0 = rg * p.MT * kTileRows;
-    x0 = strip * kTW;
+    decode_unit(p, u, img, y0, x0, cg);
   };
 
   if (warp == 0) {
@@ -335,7 +224,6 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       mbar_wait_backoff(&acc_full[ab], au & 1, 256);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int x = x0 + tx;
-      const bool pool = (p.epi & DCONV_EPI_MAXPOOL) != 0;
       for (int mt = 0; mt < p.MT; ++mt) {
         const int y = y0 + mt * kTileRows + ty;
         if (y0 + mt * kTileRows >= p.h_o) break;  // warp-uniform
@@ -344,75 +232,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
         for (int c0 = ch * half_n; c0 < (ch + 1) * half_n; c0 += 32) {
           float v[32];
           tmem_ld32x32(acc_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(mt * p.N + c0), v);
-          if (pool) {
-            // 2x2 window = lanes {l, l^1, l^8, l^9} (8-px tile rows, even
-            // origins, even h_o/w_o: a window is all valid or all invalid)
-            if (valid && (p.epi & DCONV_EPI_ADD)) {
-#pragma unroll
-              for (int b = 0; b < 4; ++b) {
-                const int jb = cg * (p.N / 8) + (c0 / 8) + b;
-                if (jb >= p.jb_count) break;
-                const float* sk = p.skip + (int64_t)img * p.sk_img + (int64_t)jb * p.sk_blk +
-                                  (int64_t)y * p.sk_row + (int64_t)x * 8;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) v[b * 8 + i] += sk[i];
-              }
-            }
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              v[i] = fmaxf(v[i], __shfl_xor_sync(0xffffffffu, v[i], 1));
-              v[i] = fmaxf(v[i], __shfl_xor_sync(0xffffffffu, v[i], 8));
-              if (p.epi & DCONV_EPI_RELU) v[i] = fmaxf(v[i], 0.f);
-            }
-            if (!valid || (tx & 1) || (ty & 1)) continue;
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-              const int jb = cg * (p.N / 8) + (c0 / 8) + b;
-              if (jb >= p.jb_count) break;
-              float* o = p.out + (int64_t)img * p.out_img + (int64_t)jb * p.out_blk +
-                         (int64_t)(y >> 1) * p.out_row + (int64_t)(x >> 1) * 8;
-              const float* vv = v + b * 8;
-              *reinterpret_cast<float4*>(o) = make_float4(vv[0], vv[1], vv[2], vv[3]);
-              *reinterpret_cast<float4*>(o + 4) = make_float4(vv[4], vv[5], vv[6], vv[7]);
-            }
-            continue;
-          }
-          if (!valid) continue;
-          if (p.epi & DCONV_EPI_ADD) {
-            // all of the chunk's skip pencils in flight before any store
-            // (read-only path: the loads do not wait behind the stores)
-            float4 s4[8];
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-              const int jb = min(cg * (p.N / 8) + (c0 / 8) + b, p.jb_count - 1);
-              const float4* sk = reinterpret_cast<const float4*>(
-                  p.skip + (int64_t)img * p.sk_img + (int64_t)jb * p.sk_blk +
-                  (int64_t)y * p.sk_row + (int64_t)x * 8);
-              s4[2 * b] = __ldg(sk);
-              s4[2 * b + 1] = __ldg(sk + 1);
-            }
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-              float* vv = v + b * 8;
-              vv[0] += s4[2 * b].x; vv[1] += s4[2 * b].y; vv[2] += s4[2 * b].z; vv[3] += s4[2 * b].w;
-              vv[4] += s4[2 * b + 1].x; vv[5] += s4[2 * b + 1].y;
-              vv[6] += s4[2 * b + 1].z; vv[7] += s4[2 * b + 1].w;
-            }
-          }
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const int jb = cg * (p.N / 8) + (c0 / 8) + b;  // block within the computed range
-            if (jb >= p.jb_count) break;
-            float* o = p.out + (int64_t)img * p.out_img + (int64_t)jb * p.out_blk +
-                       (int64_t)y * p.out_row + (int64_t)x * 8;
-            float* vv = v + b * 8;
-            if (p.epi & DCONV_EPI_RELU) {
-#pragma unroll
-              for (int i = 0; i < 8; ++i) vv[i] = fmaxf(vv[i], 0.f);
-            }
-            *reinterpret_cast<float4*>(o) = make_float4(vv[0], vv[1], vv[2], vv[3]);
-            *reinterpret_cast<float4*>(o + 4) = make_float4(vv[4], vv[5], vv[6], vv[7]);
-          }
+          emit32(p, v, img, y, x, valid, tx, ty, cg, c0);
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -462,19 +282,6 @@ __global__ void prepare_tf32_weights_kernel(const float* __restrict__ w, int ib_
   }
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
-
 }  // namespace
 
 using Tf32Kernel = void (*)(const CUtensorMap, const Tf32Params);
@@ -515,36 +322,13 @@ int launch_prepare_tf32(const float* w, int ib_n, int h_f, int w_f, int jb_begin
 
 int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t stream) {
   FfmaParams f = f0;
-  // a 1x1 stride-s conv is a 1x1 stride-1 conv over the subsampled view
-  // (every s-th pixel of every s-th row): only the tensor map's strides change
   int64_t px_floats = 8;
-  if (f.s > 1 && f.h_f == 1 && f.w_f == 1) {
-    px_floats = 8 * (int64_t)f.s;
-    f.in_row *= f.s;
-    f.h_i = f.h_o;
-    f.w_i = f.w_o;
-    f.s = 1;
-  }
-  if (f.s != 1)
-    return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_tf32: stride %d (only 1)", f.s);
-  if (f.in_img != (int64_t)f.ib_n * f.in_blk)
-    return dconv_host::set_error(DCONV_EUNSUPPORTED,
-                                 "conv_tf32: input view must stack blocks densely per image");
-  auto enc = encode_fn();
-  if (!enc) return dconv_host::set_error(DCONV_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  if (int rc = prepare_view(f, px_floats, "conv_tf32")) return rc;
   Tf32Params p{};
   p.w = w_prepared;
-  p.skip = f.skip;
-  p.out = f.out;
-  p.n = f.n; p.h_i = f.h_i; p.w_i = f.w_i; p.h_o = f.h_o; p.w_o = f.w_o;
-  p.h_f = f.h_f; p.w_f = f.w_f;
-  p.ib_n = f.ib_n; p.jb_begin = f.jb_begin; p.jb_count = f.jb_count;
+  copy_geometry(p, f);
   p.N = tf32_channels(f.jb_count);
   p.n_cg = (f.jb_count * 8 + p.N - 1) / p.N;
-  p.out_img = f.out_img; p.out_blk = f.out_blk; p.out_row = f.out_row;
-  p.sk_img = f.sk_img; p.sk_blk = f.sk_blk; p.sk_row = f.sk_row;
-  p.epi = f.epi;
-  p.PW = kTW - 1 + p.w_f;
   // stage = G input blocks x R filter rows, <= 48 KB of weights
   const int wtap = 2 * p.N * 4 * 4;  // bytes per (i', n, m)
   // M-tiles per unit: more tiles share each weight stage (less L2/smem
@@ -611,23 +395,11 @@ int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t
   p.strips = (p.w_o + kTW - 1) / kTW;
   p.units = p.n * p.row_groups * p.strips * p.n_cg;
   // instruction descriptor: D f32, A/B tf32, K-major both, N, M = 128
-  p.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(p.N >> 3) << 17) |
-            ((uint32_t)(128 >> 4) << 24);
+  p.idesc = tf32_idesc(p.N);
 
   // tensor map over the input view: {c4, half, W, H, image*block}
   CUtensorMap map;
-  const cuuint64_t dims[5] = {4, 2, (cuuint64_t)f.w_i, (cuuint64_t)f.h_i,
-                              (cuuint64_t)f.n * f.ib_n};
-  const cuuint64_t strides[4] = {16, (cuuint64_t)px_floats * 4, (cuuint64_t)f.in_row * 4,
-                                 (cuuint64_t)f.in_blk * 4};
-  const cuuint32_t box[5] = {4, 1, (cuuint32_t)p.PW, (cuuint32_t)p.PH, (cuuint32_t)p.G};
-  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  const CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(f.in),
-                          dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS)
-    return dconv_host::set_error(DCONV_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+  if (int rc = encode_input_map(&map, f, px_floats, p.PW, p.PH, p.G)) return rc;
 
   static int sms = 0;
   static bool attr = false;

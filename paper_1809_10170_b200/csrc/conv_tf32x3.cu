@@ -1,0 +1,505 @@
+// conv_tf32x3.cu -- split-TF32 ("3xTF32") tcgen05 direct convolution that
+// meets the fp32 tolerance of the FFMA path (|a-b| <= 1e-4 + 1e-5|b| against
+// conv_oracle64, reference.cpp:70-87).
+//
+// Same algorithm, layout and tiling as conv_tf32.cu (Alg. 3, PAPER.md:326-363,
+// blocked c_b = 8; one tcgen05.mma.kind::tf32 per filter tap and input block),
+// with every operand split into a TF32 head and an fp32 remainder:
+//   x = x_hi + x_lo, x_hi = x with the low 13 mantissa bits cleared,
+//   conv(x, w) ~= T(x_hi, w_hi) + T(x_hi, w_lo) + T(x_lo, w_hi)
+// (the dropped x_lo*w_lo term is ~2^-22 of a product).
+//   * Weights: hi and lo are prepared once (bit-exact split of the blocked
+//     kernel, like pack_kernel tensor.cpp:85-95) and streamed by bulk copy.
+//   * Activations: TMA stages the raw fp32 patch; two "split" warps clear
+//     the low bits in place and write the remainders into a second pair of
+//     planes of the same stage -- on chip, so no workspace is added.
+//   * Accumulation: the tensor core adds into its fp32 accumulator with an
+//     error that grows with the accumulator's magnitude (K = 4608 in one
+//     accumulator fails the fp32 bar: profiles/r1_tf32x3_accuracy.txt).  The
+//     reduction is therefore cut into chunks of ~288 products: the MMAs of a
+//     chunk go to one of two TMEM accumulator sets while the epilogue warps
+//     add the previous chunk into fp32 register totals (IEEE adds), the same
+//     two-level summation the FFMA kernel does with its TMEM fold
+//     (profiles/r1_tf32x3_chunk.txt: chunk K vs accuracy).
+//
+// Roles (12 warps): warp 0 TMA producer, warp 1 MMA issuer (elect.sync),
+// warps 2-3 operand split, warps 4-11 epilogue (chunk drain into registers,
+// then fused skip/ReLU/pool and blocked pencil stores).
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "tf32_common.cuh"
+
+namespace dconv_dev {
+
+int tf32_channels(int jb_count);  // conv_tf32.cu
+
+namespace {
+
+using namespace tf32;
+constexpr int kSplitWarps = 2;
+constexpr int kEpiWarpsX = 8;
+constexpr int kThreadsX = (4 + kEpiWarpsX) * 32;
+constexpr uint32_t kHiMask = 0xFFFFE000u;  // TF32: sign, exponent, 10 mantissa bits
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, "
+      "%8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+        "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),
+        "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float4 hi4(float4 v) {
+  return make_float4(__uint_as_float(__float_as_uint(v.x) & kHiMask),
+                     __uint_as_float(__float_as_uint(v.y) & kHiMask),
+                     __uint_as_float(__float_as_uint(v.z) & kHiMask),
+                     __uint_as_float(__float_as_uint(v.w) & kHiMask));
+}
+
+// COLS = MT * N / 2: accumulator columns each epilogue thread totals in
+// registers (two epilogue warps per TMEM lane quarter, each half of N).
+template <int WF_T, int MT_T, int COLS>
+__global__ void __launch_bounds__(kThreadsX, 1)
+    conv_tf32x3_kernel(const __grid_constant__ CUtensorMap tmap, const Tf32Params p) {
+  extern __shared__ __align__(1024) float smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.NS * p.stage_floats);
+  uint64_t* split = full + kMaxStagesT;       // stage split into hi / lo planes
+  uint64_t* empty = split + kMaxStagesT;
+  uint64_t* chunk_full = empty + kMaxStagesT;  // [2] chunk accumulator sets
+  uint64_t* chunk_empty = chunk_full + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(chunk_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = p.n_g * p.n_r;
+  const int n_chunks = (S + p.chunk_st - 1) / p.chunk_st;
+  constexpr uint32_t kSetCols = 256;  // chunk set c & 1 at column (c & 1) * 256
+  const uint32_t tmem_cols = 512;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < p.NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&split[i], kSplitWarps);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&chunk_full[i], 1);
+      mbar_init(&chunk_empty[i], kEpiWarpsX);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // programmatic dependent launch: input readable from here on
+  pdl_launch_dependents();
+
+  // register split per warpgroup (one setmaxnreg per warpgroup, dominating
+  // its roles' code): WG0 = producer, MMA issuer, split warps; WG1-2 = epilogue
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+  if (warp == 0) {
+    // ----------------------------------------------------------- producer
+    if (lane == 0) {
+      int gs = 0, buf = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        int img, y0, x0, cg;
+        decode_unit(p, u, img, y0, x0, cg);
+        int g = 0, r = 0;
+        for (int st = 0; st < S; ++st, ++gs) {
+          if (st > 0 && ++r == p.n_r) { r = 0; ++g; }
+          if (gs > 0 && ++buf == p.NS) { buf = 0; phase ^= 1u; }
+          if (gs >= p.NS) mbar_wait_backoff(&empty[buf], phase ^ 1u, 64);
+          const int ib0 = g * p.G, n0 = r * p.R;
+          const int Ge = min(p.G, p.ib_n - ib0), Re = min(p.R, p.h_f - n0);
+          float* sp = smem + buf * p.stage_floats;
+          // the TMA box always lands whole (OOB elements zero-filled)
+          const uint32_t patch_bytes = 2u * (uint32_t)(p.G * p.PH * p.PW * 4) * 4u;
+          const uint32_t wbytes = (uint32_t)(Ge * Re * p.w_f * 4 * p.N * 4) * 4u;
+          mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes);
+          tma_load_5d(sp, &tmap, 0, 0, x0, y0 + n0, img * p.ib_n + ib0, &full[buf]);
+          tma_load_5d(sp + p.plane_floats, &tmap, 0, 1, x0, y0 + n0, img * p.ib_n + ib0,
+                      &full[buf]);
+          const float* wsrc =
+              p.w + (((int64_t)cg * p.ib_n + ib0) * p.h_f + n0) * (int64_t)p.w_f * 4 * p.N * 4;
+          bulk_g2s(sp + 4 * p.plane_floats, wsrc, wbytes, &full[buf]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ----------------------------------------------------------- MMA issuer
+    int gs = 0, buf = 0, cs = 0;
+    uint32_t phase = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      int img, y0, x0, cg;
+      decode_unit(p, u, img, y0, x0, cg);
+      const int valid_rows = min(p.MT * kTileRows, p.h_o - y0);
+      const int mts = (valid_rows + kTileRows - 1) / kTileRows;
+      int g = 0, r = 0, ci = 0;
+      uint32_t acc_base = 0, accum = 0;
+      for (int st = 0; st < S; ++st, ++gs) {
+        if (st > 0 && ++r == p.n_r) { r = 0; ++g; }
+        if (gs > 0 && ++buf == p.NS) { buf = 0; phase ^= 1u; }
+        if (ci == 0) {
+          // new chunk: its accumulator set must have been drained
+          const int set = cs & 1;
+          if (cs >= 2) mbar_wait(&chunk_empty[set], ((cs >> 1) - 1) & 1);
+          acc_base = tmem_base + (uint32_t)set * kSetCols;
+          accum = 0u;
+        }
+        mbar_wait(&split[buf], phase);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int Ge = min(p.G, p.ib_n - g * p.G);
+        const int Re = min(p.R, p.h_f - r * p.R);
+        const float* sp = smem + buf * p.stage_floats;
+        const uint32_t a_base = smem_u32(sp);
+        const uint32_t b_base = smem_u32(sp + 4 * p.plane_floats);
+        // descriptor low words (start >> 4 | LBO >> 4 << 16) advance by 32-bit
+        // adds (see conv_tf32.cu); lo planes / lo weights at fixed offsets
+        const uint32_t a_lo0 = ((a_base >> 4) & 0x3FFFu) | (((uint32_t)(p.plane_floats * 4) >> 4) << 16);
+        const uint32_t a_hi = ((uint32_t)(p.PW * 16) >> 4) | (1u << 14);
+        const uint32_t b_lo0 = ((b_base >> 4) & 0x3FFFu) | (((uint32_t)(p.N * 16) >> 4) << 16);
+        const uint32_t b_hi = (128u >> 4) | (1u << 14);
+        const uint32_t a_mt = (uint32_t)(kTileRows * p.PW);  // next M-tile (16 B units)
+        const uint32_t b_tap = (uint32_t)(4 * p.N);          // next (n, m) tap: hi + lo
+        const uint32_t a_rem = (uint32_t)(p.plane_floats / 2);  // lo planes (16 B units)
+        const uint32_t b_rem = (uint32_t)(2 * p.N);             // lo weights of a tap
+        const int wf = WF_T > 0 ? WF_T : p.w_f;
+        constexpr int kMtLoop = MT_T > 0 ? MT_T : kMaxMT;
+        for (int gi = 0; gi < Ge; ++gi)
+          for (int n = 0; n < Re; ++n) {
+            const uint32_t arow = a_lo0 + (uint32_t)((gi * p.PH + n) * p.PW);
+            const uint32_t brow = b_lo0 + (uint32_t)((gi * p.R + n) * wf) * b_tap;
+#pragma unroll
+            for (int m = 0; m < (WF_T > 0 ? WF_T : 1); ++m) {
+#pragma unroll
+              for (int mt = 0; mt < kMtLoop; ++mt) {
+                if (mt >= mts) break;
+                const uint32_t d = acc_base + (uint32_t)(mt * p.N);
+                const uint32_t a = arow + (uint32_t)m + (uint32_t)mt * a_mt;
+                const uint32_t b = brow + (uint32_t)m * b_tap;
+                // small terms first, the head product last
+                umma_tf32_elect(d, a, a_hi, b + b_rem, b_hi, p.idesc, accum);
+                umma_tf32_elect(d, a + a_rem, a_hi, b, b_hi, p.idesc, 1u);
+                umma_tf32_elect(d, a, a_hi, b, b_hi, p.idesc, 1u);
+              }
+              accum = 1u;
+            }
+            if (WF_T > 0) continue;
+            for (int m = 1; m < wf; ++m) {
+              for (int mt = 0; mt < mts; ++mt) {
+                const uint32_t d = acc_base + (uint32_t)(mt * p.N);
+                const uint32_t a = arow + (uint32_t)m + (uint32_t)mt * a_mt;
+                const uint32_t b = brow + (uint32_t)m * b_tap;
+                umma_tf32_elect(d, a, a_hi, b + b_rem, b_hi, p.idesc, 1u);
+                umma_tf32_elect(d, a + a_rem, a_hi, b, b_hi, p.idesc, 1u);
+                umma_tf32_elect(d, a, a_hi, b, b_hi, p.idesc, 1u);
+              }
+            }
+          }
+        umma_commit_elect(&empty[buf]);  // stage smem free once these MMAs retire
+        if (++ci == p.chunk_st || st == S - 1) {
+          umma_commit_elect(&chunk_full[cs & 1]);
+          ci = 0;
+          ++cs;
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ----------------------------------------------------------- operand split
+    // x -> x_hi (in place) and x_lo = x - x_hi (second plane pair)
+    const int t = threadIdx.x - 64;
+    int gs = 0, buf = 0;
+    uint32_t phase = 0;
+    const int n4 = p.plane_floats / 2;  // float4s in the two hi planes
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      for (int st = 0; st < S; ++st, ++gs) {
+        if (gs > 0 && ++buf == p.NS) { buf = 0; phase ^= 1u; }
+        mbar_wait(&full[buf], phase);
+        float4* hi = reinterpret_cast<float4*>(smem + buf * p.stage_floats);
+        float4* lo = hi + n4;
+#pragma unroll 4
+        for (int i = t; i < n4; i += kSplitWarps * 32) {
+          const float4 v = hi[i];
+          const float4 h = hi4(v);
+          hi[i] = h;
+          lo[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+        }
+        fence_proxy_async_smem();  // generic-proxy writes -> tcgen05.mma operands
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&split[buf]);
+      }
+    }
+  }
+  } else {
+    // ----------------------------------------------------------- epilogue
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+    const int q = warp & 3;         // TMEM lane quarter of this warp
+    const int ch = (warp - 4) / 4;  // which half of the N columns
+    const int r = q * 32 + lane;    // pixel row of the M-tile
+    const int ty = r / kTW, tx = r % kTW;
+    const int cpm = p.N / 64;       // 32-column chunks per M-tile per thread
+    const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
+    int cs = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      int img, y0, x0, cg;
+      decode_unit(p, u, img, y0, x0, cg);
+      const int valid_rows = min(p.MT * kTileRows, p.h_o - y0);
+      const int mts = (valid_rows + kTileRows - 1) / kTileRows;
+      float tot[COLS];
+      for (int c = 0; c < n_chunks; ++c, ++cs) {
+        const int set = cs & 1;
+        mbar_wait_backoff(&chunk_full[set], (cs >> 1) & 1, 32);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < COLS / 32; ++j) {
+          const int mt = j / cpm;
+          const int c0 = ch * (p.N / 2) + (j - mt * cpm) * 32;
+          if (mt < mts) {  // warp-uniform
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              float v[16];
+              tmem_ld16(lane_base + (uint32_t)set * kSetCols + (uint32_t)(mt * p.N + c0 + h * 16), v);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                float& t = tot[j * 32 + h * 16 + i];
+                t = c == 0 ? v[i] : t + v[i];
+              }
+            }
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&chunk_empty[set]);
+      }
+      const int x = x0 + tx;
+#pragma unroll
+      for (int j = 0; j < COLS / 32; ++j) {
+        const int mt = j / cpm;
+        const int c0 = ch * (p.N / 2) + (j - mt * cpm) * 32;
+        if (mt < mts) {
+          const int y = y0 + mt * kTileRows + ty;
+          const bool valid = y < p.h_o && x < p.w_o;
+          emit32(p, *reinterpret_cast<float(*)[32]>(&tot[j * 32]), img, y, x, valid, tx, ty, cg,
+                 c0);
+        }
+      }
+    }
+  }
+
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(tmem_cols));
+  }
+}
+
+// Prepared weights: [cg][i'][n][m][hi/lo][k-half][N][4] from the blocked
+// kernel [jb][i'][n][m][ii][jj] (tensor.hpp:131-137): w_hi = w with the low
+// 13 mantissa bits cleared, w_lo = w - w_hi (exact).  Channel slots beyond
+// jb_count blocks are zero.
+__global__ void prepare_tf32x3_weights_kernel(const float* __restrict__ w, int ib_n, int h_f,
+                                              int w_f, int jb_begin, int jb_count, int N,
+                                              int64_t total, float* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = e;
+    const int k4 = (int)(t % 4); t /= 4;
+    const int co = (int)(t % N); t /= N;
+    const int kh = (int)(t % 2); t /= 2;
+    const int hl = (int)(t % 2); t /= 2;
+    const int m = (int)(t % w_f); t /= w_f;
+    const int n = (int)(t % h_f); t /= h_f;
+    const int ib = (int)(t % ib_n); t /= ib_n;
+    const int cg = (int)t;
+    const int jl = cg * (N / 8) + co / 8;
+    float v = 0.f;
+    if (jl < jb_count) {
+      const int jb = jb_begin + jl, jj = co % 8, ii = kh * 4 + k4;
+      v = w[(((((int64_t)jb * ib_n + ib) * h_f + n) * w_f + m) * 8 + ii) * 8 + jj];
+    }
+    const float h = __uint_as_float(__float_as_uint(v) & kHiMask);
+    out[e] = hl ? v - h : h;
+  }
+}
+
+using X3Kernel = void (*)(const CUtensorMap, const Tf32Params);
+
+// (WF, MT, COLS) instantiations: WF in {3, 1, generic}, MT * N in {128, 256}
+template <int WF>
+X3Kernel pick_wf(int MT, int cols) {
+  if (MT == 1) return cols == 64 ? conv_tf32x3_kernel<WF, 1, 64> : conv_tf32x3_kernel<WF, 1, 128>;
+  if (MT == 2) return cols == 64 ? conv_tf32x3_kernel<WF, 2, 64> : conv_tf32x3_kernel<WF, 2, 128>;
+  return conv_tf32x3_kernel<WF, 4, 128>;
+}
+X3Kernel pick_x3_kernel(const Tf32Params& p) {
+  const int cols = p.MT * p.N / 2;
+  if (p.w_f == 3) return pick_wf<3>(p.MT, cols);
+  if (p.w_f == 1) return pick_wf<1>(p.MT, cols);
+  return pick_wf<0>(p.MT, cols);
+}
+
+void set_x3_attrs() {
+  static bool done = false;
+  if (done) return;
+  for (X3Kernel k : {pick_wf<3>(1, 64), pick_wf<3>(1, 128), pick_wf<3>(2, 64), pick_wf<3>(2, 128),
+                     pick_wf<3>(4, 128), pick_wf<1>(1, 64), pick_wf<1>(1, 128), pick_wf<1>(2, 64),
+                     pick_wf<1>(2, 128), pick_wf<1>(4, 128), pick_wf<0>(1, 64), pick_wf<0>(1, 128),
+                     pick_wf<0>(2, 64), pick_wf<0>(2, 128), pick_wf<0>(4, 128)})
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  done = true;
+}
+
+}  // namespace
+
+int64_t tf32x3_prepared_floats(int ib_n, int h_f, int w_f, int jb_count) {
+  const int N = tf32_channels(jb_count);
+  const int n_cg = (jb_count * 8 + N - 1) / N;
+  return (int64_t)n_cg * ib_n * h_f * w_f * 4 * N * 4;
+}
+
+int launch_prepare_tf32x3(const float* w, int ib_n, int h_f, int w_f, int jb_begin, int jb_count,
+                          float* out, cudaStream_t stream) {
+  const int N = tf32_channels(jb_count);
+  const int64_t total = tf32x3_prepared_floats(ib_n, h_f, w_f, jb_count);
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 32);
+  prepare_tf32x3_weights_kernel<<<(unsigned)blocks, 256, 0, stream>>>(w, ib_n, h_f, w_f, jb_begin,
+                                                                      jb_count, N, total, out);
+  dconv_host::count_launch();
+  return dconv_host::check_launch("prepare_tf32x3_weights_kernel");
+}
+
+int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream_t stream) {
+  FfmaParams f = f0;
+  int64_t px_floats = 8;
+  if (int rc = prepare_view(f, px_floats, "conv_tf32x3")) return rc;
+  Tf32Params p{};
+  p.w = w_prepared;
+  copy_geometry(p, f);
+  p.N = tf32_channels(f.jb_count);
+  p.n_cg = (f.jb_count * 8 + p.N - 1) / p.N;
+  const int sms = sm_count();
+  const int wtap = 4 * p.N * 4 * 4;  // bytes per (i', n, m): hi + lo
+  // M-tiles per unit (MT * N in {128, 256}: two chunk sets fit TMEM, the
+  // totals fit the epilogue registers).  Cost per input block = max(3 MMAs
+  // per tap and M-tile, shared-memory traffic at ~120 B/cycle: the MMAs read
+  // A + B from smem, the TMA writes patch + hi/lo weights, the split warps
+  // read and rewrite the patch) + per-unit fill / epilogue.
+  {
+    double best = -1;
+    for (int mt = kMaxMT; mt >= 1; --mt) {
+      const int cols = mt * p.N / 2;
+      if (cols != 64 && cols != 128) continue;
+      const int rg = (p.h_o + mt * kTileRows - 1) / (mt * kTileRows);
+      const int64_t units = (int64_t)p.n * rg * ((p.w_o + kTW - 1) / kTW) * p.n_cg;
+      const double taps = (double)p.h_f * p.w_f;
+      const double mma_cyc = p.N > 128 ? 128.0 : 71.0;
+      const double mma = taps * mt * 3 * mma_cyc;
+      const double patch = (double)(mt * kTileRows - 1 + p.h_f) * (kTW - 1 + p.w_f) * 32.0;
+      const double smem_bytes = taps * mt * 3 * (4096.0 + p.N * 32.0) + taps * wtap + patch * 4;
+      const double unit = p.ib_n * std::max(mma, smem_bytes / 120.0) + 1500.0;
+      const double rounds = (double)((units + sms - 1) / sms);
+      const double score = 1.0 / (rounds * unit);
+      if (score > best * (1 + 1e-9)) {
+        best = score;
+        p.MT = mt;
+      }
+    }
+    if (best < 0) return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_tf32x3: N = %d", p.N);
+    static const char* force_mt = getenv("DCONV_TF32_MT");
+    if (force_mt) {
+      const int mt = atoi(force_mt);
+      if (mt >= 1 && mt <= kMaxMT && (mt * p.N == 128 || mt * p.N == 256)) p.MT = mt;
+    }
+  }
+  // stage = G input blocks x R filter rows: <= 72 KB of hi/lo weights,
+  // <= 40 KB of patch (hi + lo planes); at least two stages in 220 KB --
+  // else fewer filter rows per stage, then fewer M-tiles
+  const int bar_bytes = (3 * kMaxStagesT + 4) * 8 + 16;
+  int stage_bytes = 0;
+  for (int r_cap = p.h_f;; ) {
+    const int patch_blk_bytes = 4 * (p.MT * kTileRows - 1 + std::min(p.h_f, r_cap)) * p.PW * 16;
+    if (p.h_f * p.w_f * wtap <= 72 * 1024 && r_cap == p.h_f) {
+      p.R = p.h_f;
+      p.G = std::max(1, std::min({p.ib_n, (72 * 1024) / (p.h_f * p.w_f * wtap),
+                                  (40 * 1024) / patch_blk_bytes}));
+    } else {
+      p.G = 1;
+      p.R = std::max(1, std::min(r_cap, (72 * 1024) / (p.w_f * wtap)));
+    }
+    p.PH = p.MT * kTileRows - 1 + p.R;
+    p.plane_floats = (p.G * p.PH * p.PW * 4 + 31) & ~31;  // 128 B aligned planes
+    p.wstage_floats = p.G * p.R * p.w_f * 4 * p.N * 4;
+    p.stage_floats = ((4 * p.plane_floats + p.wstage_floats) + 255) & ~255;  // 1 KB aligned
+    stage_bytes = p.stage_floats * 4;
+    p.NS = std::min(kMaxStagesT, (220 * 1024 - bar_bytes) / stage_bytes);
+    if (p.NS >= 2) break;
+    if (p.R > 1) {
+      r_cap = p.R - 1;
+    } else if (p.MT > 1 && (p.MT / 2) * p.N >= 128) {
+      p.MT /= 2;
+      r_cap = p.h_f;
+    } else {
+      return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_tf32x3: stage of %d bytes",
+                                   stage_bytes);
+    }
+  }
+  p.n_g = (p.ib_n + p.G - 1) / p.G;
+  p.n_r = (p.h_f + p.R - 1) / p.R;
+  if (p.PH > 256 || p.PW > 256 || p.G > 256)
+    return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_tf32x3: TMA box too large");
+  // accumulator chunk: ~288 products (DCONV_X3_CHUNK_K), whole stages
+  static const int chunk_k = getenv("DCONV_X3_CHUNK_K") ? atoi(getenv("DCONV_X3_CHUNK_K")) : 288;
+  const int k_stage = p.G * p.R * p.w_f * 8;
+  p.chunk_st = std::max(1, chunk_k / k_stage);
+  p.row_groups = (p.h_o + p.MT * kTileRows - 1) / (p.MT * kTileRows);
+  p.strips = (p.w_o + kTW - 1) / kTW;
+  p.units = p.n * p.row_groups * p.strips * p.n_cg;
+  p.idesc = tf32_idesc(p.N);
+
+  CUtensorMap map;
+  if (int rc = encode_input_map(&map, f, px_floats, p.PW, p.PH, p.G)) return rc;
+  set_x3_attrs();
+  const size_t smem = (size_t)p.NS * stage_bytes + bar_bytes;
+  const int grid = std::min(p.units, sms);
+  static const bool dbg = getenv("DCONV_DEBUG") != nullptr;
+  if (dbg)
+    fprintf(stderr, "conv_tf32x3 N=%d MT=%d G=%d R=%d NS=%d stage=%d B chunk_st=%d units=%d\n",
+            p.N, p.MT, p.G, p.R, p.NS, stage_bytes, p.chunk_st, p.units);
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreadsX);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = dconv_host::pdl_enabled() ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, pick_x3_kernel(p), map, p);
+  if (e != cudaSuccess)
+    return dconv_host::set_error(DCONV_ECUDA, "conv_tf32x3: %s", cudaGetErrorString(e));
+  dconv_host::count_launch();
+  return dconv_host::check_launch("conv_tf32x3_kernel");
+}
+
+}  // namespace dconv_dev

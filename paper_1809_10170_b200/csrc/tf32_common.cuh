@@ -1,0 +1,262 @@
+// tf32_common.cuh -- tcgen05 / TMA helpers and the blocked-pencil epilogue
+// shared by the TF32 tensor-core kernels (conv_tf32.cu: one TF32 pass;
+// conv_tf32x3.cu: split-TF32, fp32 tolerance).
+#pragma once
+#include <algorithm>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "conv_kernels.h"
+
+namespace dconv_dev {
+namespace tf32 {
+
+constexpr int kMaxMT = 4;       // M-tiles (128 pixels each) per work unit, at most
+constexpr int kTileRows = 16;   // an M-tile is 16 output rows x 8 columns
+constexpr int kTW = 8;
+constexpr int kMaxStagesT = 8;
+
+struct Tf32Params {
+  const float* w;     // prepared weights
+  const float* skip;
+  float* out;
+  int n, h_i, w_i, h_o, w_o, h_f, w_f;
+  int ib_n, jb_begin, jb_count;
+  int N;              // channels per work unit (64, 128 or 256), 8 | N
+  int n_cg;           // channel groups
+  int64_t out_img, out_blk, out_row, sk_img, sk_blk, sk_row;
+  int epi;
+  int G, R, n_g, n_r, PH, PW;
+  int plane_floats;   // one channel half-plane of a stage: G*PH*PW*4
+  int wstage_floats;  // G*R*w_f*2*N*4 (x2 for split-TF32: hi and lo)
+  int stage_floats;
+  int NS;
+  int row_groups, strips, units;
+  int MT;             // M-tiles per unit (1..4)
+  int chunk_st;       // split-TF32: stages per TMEM accumulator chunk
+  uint32_t idesc;
+  unsigned long long* dbg;  // DCONV_TF32_PROFILE: per-CTA wait cycles (else null)
+};
+
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, int c3, int c4, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Issued by one elected lane of a converged warp (elect.sync); the
+// descriptors come in as 32-bit halves so the loop arithmetic stays 32-bit.
+__device__ __forceinline__ void umma_tf32_elect(uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi,
+                                                uint32_t b_lo, uint32_t b_hi, uint32_t idesc,
+                                                uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred e, p;\n.reg .b64 ad, bd;\n"
+      "mov.b64 ad, {%1, %2};\nmov.b64 bd, {%3, %4};\n"
+      "setp.ne.b32 p, %6, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ad, bd, %5, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32x32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, "
+      "%8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, "
+      "%23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+        "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),
+        "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]),
+        "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// unit u -> (channel group fastest, then strip, row group, image)
+__device__ __forceinline__ void decode_unit(const Tf32Params& p, int u, int& img, int& y0, int& x0,
+                                            int& cg) {
+  cg = u % p.n_cg;
+  int t = u / p.n_cg;
+  const int strip = t % p.strips;
+  t /= p.strips;
+  const int rg = t % p.row_groups;
+  img = t / p.row_groups;
+  y0 = rg * p.MT * kTileRows;
+  x0 = strip * kTW;
+}
+
+// Epilogue for 32 accumulator columns (4 output blocks starting at channel c0
+// of channel group cg) of pixel (img, y, x): fused skip-add / ReLU / 2x2
+// max-pool, then blocked pencil stores.  Every lane of the warp must call it
+// (the pool exchanges values across lanes); `valid` masks the stores.
+__device__ __forceinline__ void emit32(const Tf32Params& p, float (&v)[32], int img, int y, int x,
+                                       bool valid, int tx, int ty, int cg, int c0) {
+  if (p.epi & DCONV_EPI_MAXPOOL) {
+    // 2x2 window = lanes {l, l^1, l^8, l^9} (8-px tile rows, even
+    // origins, even h_o/w_o: a window is all valid or all invalid)
+    if (valid && (p.epi & DCONV_EPI_ADD)) {
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int jb = cg * (p.N / 8) + (c0 / 8) + b;
+        if (jb >= p.jb_count) break;
+        const float* sk = p.skip + (int64_t)img * p.sk_img + (int64_t)jb * p.sk_blk +
+                          (int64_t)y * p.sk_row + (int64_t)x * 8;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[b * 8 + i] += sk[i];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      v[i] = fmaxf(v[i], __shfl_xor_sync(0xffffffffu, v[i], 1));
+      v[i] = fmaxf(v[i], __shfl_xor_sync(0xffffffffu, v[i], 8));
+      if (p.epi & DCONV_EPI_RELU) v[i] = fmaxf(v[i], 0.f);
+    }
+    if (!valid || (tx & 1) || (ty & 1)) return;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int jb = cg * (p.N / 8) + (c0 / 8) + b;
+      if (jb >= p.jb_count) break;
+      float* o = p.out + (int64_t)img * p.out_img + (int64_t)jb * p.out_blk +
+                 (int64_t)(y >> 1) * p.out_row + (int64_t)(x >> 1) * 8;
+      const float* vv = v + b * 8;
+      *reinterpret_cast<float4*>(o) = make_float4(vv[0], vv[1], vv[2], vv[3]);
+      *reinterpret_cast<float4*>(o + 4) = make_float4(vv[4], vv[5], vv[6], vv[7]);
+    }
+    return;
+  }
+  if (!valid) return;
+  if (p.epi & DCONV_EPI_ADD) {
+    // all of the chunk's skip pencils in flight before any store
+    // (read-only path: the loads do not wait behind the stores)
+    float4 s4[8];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int jb = min(cg * (p.N / 8) + (c0 / 8) + b, p.jb_count - 1);
+      const float4* sk = reinterpret_cast<const float4*>(
+          p.skip + (int64_t)img * p.sk_img + (int64_t)jb * p.sk_blk + (int64_t)y * p.sk_row +
+          (int64_t)x * 8);
+      s4[2 * b] = __ldg(sk);
+      s4[2 * b + 1] = __ldg(sk + 1);
+    }
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      float* vv = v + b * 8;
+      vv[0] += s4[2 * b].x; vv[1] += s4[2 * b].y; vv[2] += s4[2 * b].z; vv[3] += s4[2 * b].w;
+      vv[4] += s4[2 * b + 1].x; vv[5] += s4[2 * b + 1].y;
+      vv[6] += s4[2 * b + 1].z; vv[7] += s4[2 * b + 1].w;
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const int jb = cg * (p.N / 8) + (c0 / 8) + b;  // block within the computed range
+    if (jb >= p.jb_count) break;
+    float* o = p.out + (int64_t)img * p.out_img + (int64_t)jb * p.out_blk +
+               (int64_t)y * p.out_row + (int64_t)x * 8;
+    float* vv = v + b * 8;
+    if (p.epi & DCONV_EPI_RELU) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) vv[i] = fmaxf(vv[i], 0.f);
+    }
+    *reinterpret_cast<float4*>(o) = make_float4(vv[0], vv[1], vv[2], vv[3]);
+    *reinterpret_cast<float4*>(o + 4) = make_float4(vv[4], vv[5], vv[6], vv[7]);
+  }
+}
+
+inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// Host side shared by both launchers: a 1x1 stride-s layer becomes a stride-1
+// 1x1 layer over the subsampled view; checks; the 5-D tensor map over the
+// input view {c4, half, W, H, image*block} with a PW x PH x G box.
+inline int prepare_view(FfmaParams& f, int64_t& px_floats, const char* who) {
+  px_floats = 8;
+  if (f.s > 1 && f.h_f == 1 && f.w_f == 1) {
+    px_floats = 8 * (int64_t)f.s;
+    f.in_row *= f.s;
+    f.h_i = f.h_o;
+    f.w_i = f.w_o;
+    f.s = 1;
+  }
+  if (f.s != 1) return dconv_host::set_error(DCONV_EUNSUPPORTED, "%s: stride %d (only 1)", who, f.s);
+  if (f.in_img != (int64_t)f.ib_n * f.in_blk)
+    return dconv_host::set_error(DCONV_EUNSUPPORTED,
+                                 "%s: input view must stack blocks densely per image", who);
+  if (!encode_fn()) return dconv_host::set_error(DCONV_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  return DCONV_OK;
+}
+
+inline int encode_input_map(CUtensorMap* map, const FfmaParams& f, int64_t px_floats, int PW,
+                            int PH, int G) {
+  const cuuint64_t dims[5] = {4, 2, (cuuint64_t)f.w_i, (cuuint64_t)f.h_i,
+                              (cuuint64_t)f.n * f.ib_n};
+  const cuuint64_t strides[4] = {16, (cuuint64_t)px_floats * 4, (cuuint64_t)f.in_row * 4,
+                                 (cuuint64_t)f.in_blk * 4};
+  const cuuint32_t box[5] = {4, 1, (cuuint32_t)PW, (cuuint32_t)PH, (cuuint32_t)G};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  const CUresult cr = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(f.in),
+                                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS)
+    return dconv_host::set_error(DCONV_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+  return DCONV_OK;
+}
+
+inline void copy_geometry(Tf32Params& p, const FfmaParams& f) {
+  p.skip = f.skip;
+  p.out = f.out;
+  p.n = f.n; p.h_i = f.h_i; p.w_i = f.w_i; p.h_o = f.h_o; p.w_o = f.w_o;
+  p.h_f = f.h_f; p.w_f = f.w_f;
+  p.ib_n = f.ib_n; p.jb_begin = f.jb_begin; p.jb_count = f.jb_count;
+  p.out_img = f.out_img; p.out_blk = f.out_blk; p.out_row = f.out_row;
+  p.sk_img = f.sk_img; p.sk_blk = f.sk_blk; p.sk_row = f.sk_row;
+  p.epi = f.epi;
+  p.PW = kTW - 1 + p.w_f;
+}
+
+// instruction descriptor: D f32, A/B tf32, K-major both, N, M = 128
+inline uint32_t tf32_idesc(int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(128 >> 4) << 24);
+}
+
+inline int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
+}  // namespace tf32
+}  // namespace dconv_dev

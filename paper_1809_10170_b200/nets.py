@@ -237,9 +237,10 @@ def conv(l: Layer, n: int, x: "Act|torch.Tensor", w: torch.Tensor, out: Act,
 
 def conv_tf32(l: Layer, n: int, x: "Act", wprep: torch.Tensor, out: Act,
               epilogue: int = 0, skip: Optional[Act] = None, stream=None,
-              in_view: Optional[Tuple[int, int, int, int]] = None) -> None:
+              in_view: Optional[Tuple[int, int, int, int]] = None, x3: bool = False) -> None:
     """tcgen05/TMEM TF32 launch of a blocked layer (stride 1, or a 1x1 of any
-    stride; weights prepared by prepare_tf32)."""
+    stride; weights prepared by prepare_tf32).  ``x3``: the split-TF32 kernel
+    (fp32 tolerance; weights prepared with ``x3=True``)."""
     d = _desc(l, n, epilogue)
     d.out_img_stride, d.out_blk_stride, d.out_row_stride = out.img, out.blk, out.row
     if in_view is None:
@@ -249,18 +250,21 @@ def conv_tf32(l: Layer, n: int, x: "Act", wprep: torch.Tensor, out: Act,
     if skip is not None:
         d.skip_img_stride, d.skip_blk_stride, d.skip_row_stride = skip.img, skip.blk, skip.row
         sp = skip.base()
-    check(lib().dconv_cuda_conv_direct_tf32(ctypes.byref(d), in_view[0], ptr(wprep), sp,
-                                            out.base(), stream_ptr(stream)))
+    fn = lib().dconv_cuda_conv_direct_tf32x3 if x3 else lib().dconv_cuda_conv_direct_tf32
+    check(fn(ctypes.byref(d), in_view[0], ptr(wprep), sp, out.base(), stream_ptr(stream)))
 
 
-def prepare_tf32(l: Layer, w_blocked: torch.Tensor, stream=None) -> torch.Tensor:
-    """One-time rearrangement of a blocked kernel into the UMMA operand layout."""
+def prepare_tf32(l: Layer, w_blocked: torch.Tensor, stream=None, x3: bool = False) -> torch.Tensor:
+    """One-time rearrangement of a blocked kernel into the UMMA operand layout
+    (``x3``: hi/lo operand pairs for the split-TF32 kernel)."""
     d = _desc(l, 1)
     sz = ctypes.c_int64(0)
-    check(lib().dconv_cuda_tf32_prepared_size(ctypes.byref(d), ctypes.byref(sz)))
+    L = lib()
+    size_fn = L.dconv_cuda_tf32x3_prepared_size if x3 else L.dconv_cuda_tf32_prepared_size
+    prep_fn = L.dconv_cuda_prepare_tf32x3_weights if x3 else L.dconv_cuda_prepare_tf32_weights
+    check(size_fn(ctypes.byref(d), ctypes.byref(sz)))
     out = torch.empty(sz.value, dtype=torch.float32, device=w_blocked.device)
-    check(lib().dconv_cuda_prepare_tf32_weights(ctypes.byref(d), ptr(w_blocked), ptr(out),
-                                                stream_ptr(stream)))
+    check(prep_fn(ctypes.byref(d), ptr(w_blocked), ptr(out), stream_ptr(stream)))
     return out
 
 
@@ -295,6 +299,11 @@ class Step:
     layer: Optional[Layer] = None
 
 
+# tensor-core plans: "tf32" (one TF32 pass, looser tolerance) and "tf32x3"
+# (split-TF32, the fp32 tolerance of the FFMA path)
+TC_ALGOS = ("tf32", "tf32x3")
+
+
 @dataclass
 class Plan:
     """A network instantiated on one device: weights, activations, and the
@@ -308,7 +317,7 @@ class Plan:
     n: int
     layers: List[Layer]
     shard: Optional[Tuple[int, int, object]] = None
-    algo: str = "ffma"   # "tf32": stride-1 blocked layers on the tcgen05 path
+    algo: str = "ffma"   # "tf32" / "tf32x3": blocked layers on the tcgen05 path
     # C_o-shard exchange: "nccl" = slice + all-gather; "peer" = the conv/pool
     # epilogue stores into every rank's full map (symmetric memory over
     # NVLink) followed by a device barrier -- no collective on the data path
@@ -318,6 +327,10 @@ class Plan:
     steps: List = field(default_factory=list)
     input: Optional[torch.Tensor] = None   # dense network input (first layer)
     output: Optional[Act] = None
+
+    @property
+    def x3(self) -> bool:
+        return self.algo == "tf32x3"
     per_layer_inputs: Dict[str, Act] = field(default_factory=dict)
     outputs: Dict[str, Act] = field(default_factory=dict)
 
@@ -413,9 +426,9 @@ class Plan:
         w = self.weights[l.name]
         kind = "first" if l.first else "conv"
         if self.shard is None:
-            if self.algo == "tf32" and l.first and l.s > 1 and in_view is None:
+            if self.algo in TC_ALGOS and l.first and l.s > 1 and in_view is None:
                 return self._tf32_s2d_first(l, x, y, epilogue, skip)
-            if self.algo == "tf32" and l.first and l.s == 1 and in_view is None:
+            if self.algo in TC_ALGOS and l.first and l.s == 1 and in_view is None:
                 # TF32 path, stride-1 first layer (VGG conv1_1): zero-pad the
                 # image to one 8-channel block (a pack kernel, SPEC.md:121's
                 # first-layer choice) and run it as a blocked tcgen05 layer;
@@ -425,7 +438,7 @@ class Plan:
                                     device=w.device)
                 check(lib().dconv_cuda_unpack_kernel(ptr(w), l.c_i, l.c_o, l.h_f, l.w_f, CB, l.c_i,
                                                      ptr(dense), stream_ptr(None)))
-                wp = prepare_tf32(lb, pack_weights(dense, False))
+                wp = prepare_tf32(lb, pack_weights(dense, False), x3=self.x3)
                 self.weights[l.name + ".tf32"] = wp
                 xb = Act(self.n, l.c_i, l.h_i, l.w_i, device=w.device)
                 n = self.n
@@ -433,17 +446,18 @@ class Plan:
                     lambda st: check(lib().dconv_cuda_pack_feature_map(
                         ptr(x), n, l.c_i, l.h_i, l.w_i, CB, 0, ptr(xb.buf), stream_ptr(st))),
                     f"pack_{l.name}", "pack"))
-                self.steps.append(Step(lambda st: conv_tf32(lb, n, xb, wp, y, epilogue, skip, st),
+                self.steps.append(Step(lambda st: conv_tf32(lb, n, xb, wp, y, epilogue, skip, st,
+                                                            x3=self.x3),
                                        l.name, "tf32", n * l.flops, l))
                 return y
-            if (self.algo == "tf32" and not l.first and l.s > 1 and l.h_f > 1
+            if (self.algo in TC_ALGOS and not l.first and l.s > 1 and l.h_f > 1
                     and os.environ.get("DCONV_NO_S2D") is None):
                 return self._tf32_s2d_blocked(l, x, y, epilogue, skip, in_view)
-            if self.algo == "tf32" and not l.first and (l.s == 1 or (l.h_f == 1 and l.w_f == 1)):
-                wp = prepare_tf32(l, w)
+            if self.algo in TC_ALGOS and not l.first and (l.s == 1 or (l.h_f == 1 and l.w_f == 1)):
+                wp = prepare_tf32(l, w, x3=self.x3)
                 self.weights[l.name + ".tf32"] = wp
                 self.steps.append(Step(lambda st: conv_tf32(l, self.n, x, wp, y, epilogue, skip, st,
-                                                            in_view),
+                                                            in_view, x3=self.x3),
                                        l.name, "tf32", self.n * l.flops, l))
                 return y
             self.steps.append(Step(lambda st: conv(l, self.n, x, w, y, epilogue, skip, st, in_view,
@@ -497,7 +511,7 @@ class Plan:
         wpad[:, :, :l.h_f, :l.w_f] = dense
         ws2d = (wpad.view(l.c_i, l.c_o, hf, f, wf, f).permute(3, 5, 0, 1, 2, 4)
                 .reshape(cs, l.c_o, hf, wf).contiguous())
-        wp = prepare_tf32(lb, pack_weights(ws2d, False))
+        wp = prepare_tf32(lb, pack_weights(ws2d, False), x3=self.x3)
         self.weights[l.name + ".tf32"] = wp
         xb = Act(self.n, cs, hs, ws, device=w.device)
         n = self.n
@@ -505,7 +519,8 @@ class Plan:
             lambda st: check(lib().dconv_cuda_pack_space_to_depth(
                 ptr(x), n, l.c_i, l.h_i, l.w_i, f, ptr(xb.buf), stream_ptr(st))),
             f"pack_{l.name}", "pack"))
-        self.steps.append(Step(lambda st: conv_tf32(lb, n, xb, wp, y, epilogue, skip, st),
+        self.steps.append(Step(lambda st: conv_tf32(lb, n, xb, wp, y, epilogue, skip, st,
+                                                    x3=self.x3),
                                l.name, "tf32", n * l.flops, l))
         return y
 
@@ -528,7 +543,7 @@ class Plan:
         wpad[:, :, :l.h_f, :l.w_f] = dense
         ws2d = (wpad.view(l.c_i, l.c_o, hf, f, wf, f).permute(3, 5, 0, 1, 2, 4)
                 .reshape(cs, l.c_o, hf, wf).contiguous())
-        wp = prepare_tf32(lb, pack_weights(ws2d, False))
+        wp = prepare_tf32(lb, pack_weights(ws2d, False), x3=self.x3)
         self.weights[l.name + ".tf32"] = wp
         xb = Act(self.n, cs, hs, ws, device=w.device)
         n = self.n
@@ -538,7 +553,8 @@ class Plan:
                 view[0], view[1], view[2], view[3], n, l.c_i, l.h_i, l.w_i, f, ptr(xb.buf),
                 stream_ptr(st))),
             f"s2d_{l.name}", "pack"))
-        self.steps.append(Step(lambda st: conv_tf32(lb, n, xb, wp, y, epilogue, skip, st),
+        self.steps.append(Step(lambda st: conv_tf32(lb, n, xb, wp, y, epilogue, skip, st,
+                                                    x3=self.x3),
                                l.name, "tf32", n * l.flops, l))
         return y
 
@@ -647,7 +663,7 @@ def _build_vgg(p: Plan, device, seed: int) -> None:
         # loses with the untuned tile choice, so it is opt-in
         fuse_ffma = (p.algo == "ffma" and l.w_o % 16 == 0 and l.h_o % 2 == 0
                      and os.environ.get("DCONV_POOL_FUSION") is not None)
-        if pool and (p.algo == "tf32" or fuse_ffma) and p.shard is None and not l.first:
+        if pool and (p.algo in TC_ALGOS or fuse_ffma) and p.shard is None and not l.first:
             # conv + ReLU + 2x2 max-pool in one kernel, straight into the next
             # layer's halo buffer (the full-resolution map is never written).
             # FFMA: only where the pool-compatible tiles (TW a multiple of
@@ -678,7 +694,7 @@ def _build_resnet(p: Plan, device, seed: int) -> None:
     _fill(x0, seed, 0)
     p.input = x0
     x = Act(p.n, 64, 56, 56, device=device)
-    if p.algo == "tf32" and p.shard is None:
+    if p.algo in TC_ALGOS and p.shard is None:
         # tcgen05 stem (space-to-depth) with ReLU + 2x2 max-pool in its epilogue
         p.outputs["stem"] = x
         p.conv_into(stem, x0, x, epilogue=_abi.EPI_RELU | _abi.EPI_MAXPOOL)

@@ -578,8 +578,9 @@ def test_cluster_split_k(ks, monkeypatch):
 
 
 # ---------------------------------------------------------- TF32 tensor cores
-def run_conv_tf32(x, k, relu=False, skip=None):
-    """tcgen05/TMEM TF32 path through the C-ABI (stride 1, c_b = 8)."""
+def run_conv_tf32(x, k, relu=False, skip=None, x3=False):
+    """tcgen05/TMEM TF32 path through the C-ABI (stride 1, c_b = 8); ``x3``:
+    the split-TF32 entry points."""
     import ctypes
     ci, hi, wi = x.shape[-3:]
     n = x.shape[0] if x.ndim == 4 else 1
@@ -590,14 +591,17 @@ def run_conv_tf32(x, k, relu=False, skip=None):
     xb = dev(np.stack([po.pack_feature_map(xs[i], 8) for i in range(n)]))
     kb = dev(po.pack_kernel(k, 8, 8))
     sz = ctypes.c_int64(0)
-    _abi.check(_abi.lib().dconv_cuda_tf32_prepared_size(ctypes.byref(d), ctypes.byref(sz)))
+    L = _abi.lib()
+    sfx = "tf32x3" if x3 else "tf32"
+    _abi.check(getattr(L, f"dconv_cuda_{sfx}_prepared_size")(ctypes.byref(d), ctypes.byref(sz)))
     wp = torch.empty(sz.value, device="cuda")
-    _abi.check(_abi.lib().dconv_cuda_prepare_tf32_weights(ctypes.byref(d), _abi.ptr(kb), _abi.ptr(wp),
-                                                          _abi.stream_ptr()))
+    _abi.check(getattr(L, f"dconv_cuda_prepare_{sfx}_weights")(ctypes.byref(d), _abi.ptr(kb),
+                                                               _abi.ptr(wp), _abi.stream_ptr()))
     out = torch.empty((n, (co + 7) // 8, shape.h_o, shape.w_o, 8), device="cuda")
     sk = dev(skip) if skip is not None else None
-    _abi.check(_abi.lib().dconv_cuda_conv_direct_tf32(ctypes.byref(d), _abi.ptr(xb), _abi.ptr(wp),
-                                                      _abi.ptr(sk), _abi.ptr(out), _abi.stream_ptr()))
+    _abi.check(getattr(L, f"dconv_cuda_conv_direct_{sfx}")(ctypes.byref(d), _abi.ptr(xb), _abi.ptr(wp),
+                                                           _abi.ptr(sk), _abi.ptr(out),
+                                                           _abi.stream_ptr()))
     return host(out)
 
 
@@ -621,6 +625,62 @@ def test_tf32_tensor_core_parity(ci, co, h, w, f, n):
         bound = tf32_bound(x[i], k)
         assert (err <= bound).all(), f"TF32 error {err.max()} exceeds bound (max ratio {(err / bound).max()})"
         assert err.max() > 0 or ci * f * f <= 8  # it really is TF32, not an fp32 fallback
+
+
+# ---------------------------------------------- split-TF32 (fp32 tolerance)
+@pytest.mark.parametrize("ci,co,h,w,f,n", [(64, 64, 18, 18, 3, 1), (16, 128, 20, 13, 3, 2),
+                                            (24, 40, 70, 21, 3, 1), (32, 256, 10, 10, 1, 3),
+                                            (8, 72, 12, 12, 5, 1), (96, 136, 9, 30, 3, 2),
+                                            (40, 264, 20, 11, 3, 2), (24, 512, 35, 9, 3, 1),
+                                            (512, 512, 9, 9, 3, 2), (256, 256, 16, 16, 3, 2),
+                                            (1024, 256, 14, 14, 1, 2), (64, 64, 58, 58, 3, 1)])
+def test_tf32x3_meets_fp32_tolerance(ci, co, h, w, f, n):
+    """The split-TF32 tensor-core kernel against the fp64 oracle with the
+    fp32 FFMA tolerance |a-b| <= 1e-4 + 1e-5|b| (north_star), up to
+    K = C_i*H_f*W_f = 4608 (the chunked two-level summation)."""
+    x = po.uniform((n, ci, h, w), 9100 + ci, co)
+    k = po.uniform((ci, co, f, f), 9200 + ci, co)
+    got = run_conv_tf32(x, k, x3=True)
+    one = run_conv_tf32(x[:1], k) if ci * f * f > 8 else None
+    for i in range(n):
+        want = po.pack_feature_map(po.conv_oracle64(x[i], k, 1), 8)
+        assert_tol(got[i], want, f"tf32x3 img {i}")
+    if one is not None:  # the single-pass TF32 kernel does not meet it: x3 is doing work
+        want = po.pack_feature_map(po.conv_oracle64(x[0], k, 1), 8)
+        assert not po.within_tol(one[0], want, ATOL, RTOL)[0]
+
+
+def test_tf32x3_epilogue_and_padding():
+    x = po.uniform((2, 40, 12, 12), 95, 0)
+    k = po.uniform((40, 20, 3, 3), 95, 1)
+    skip = np.stack([po.pack_feature_map(po.uniform((20, 10, 10), 95, 2 + i), 8) for i in range(2)])
+    got = run_conv_tf32(x, k, relu=True, skip=skip, x3=True)
+    for i in range(2):
+        want = np.maximum(po.pack_feature_map(po.conv_oracle64(x[i], k, 1), 8) + skip[i], 0)
+        assert_tol(got[i], want, f"tf32x3 relu+skip img {i}")
+        assert not got[i][-1][..., 4:].any(), "padded output channels must be exact 0"
+
+
+@pytest.mark.parametrize("ci,co,h,w,n", [(16, 64, 34, 26, 2), (24, 264, 18, 18, 1)])
+def test_tf32x3_fused_maxpool_epilogue(ci, co, h, w, n):
+    """split-TF32 conv + ReLU + 2x2 max-pool in one kernel == the same conv
+    followed by the bit-exact pool kernel, bit for bit."""
+    l = nets.Layer("p", ci, co, h, w, 3, 3, 1)
+    x = po.uniform((n, ci, h, w), 9750 + ci, co)
+    k = po.uniform((ci, co, 3, 3), 9751 + ci, co)
+    a = nets.Act(n, ci, h, w)
+    a.buf.copy_(dev(np.stack([po.pack_feature_map(x[i], 8) for i in range(n)])))
+    wp = nets.prepare_tf32(l, nets.pack_weights(dev(k), False), x3=True)
+    y = nets.Act(n, co, l.h_o, l.w_o)
+    nets.conv_tf32(l, n, a, wp, y, _abi.EPI_RELU, x3=True)
+    ref = nets.Act(n, co, l.h_o // 2, l.w_o // 2, halo=1)
+    nets.maxpool_into(y, ref)
+    z = nets.Act(n, co, l.h_o // 2, l.w_o // 2, halo=1)
+    nets.conv_tf32(l, n, a, wp, z, _abi.EPI_RELU | _abi.EPI_MAXPOOL, x3=True)
+    assert torch.equal(z.buf, ref.buf)
+    for i in range(n):
+        assert_tol(host(y.buf)[i], np.maximum(po.pack_feature_map(po.conv_oracle64(x[i], k, 1), 8), 0),
+                   f"tf32x3 img {i}")
 
 
 @pytest.mark.parametrize("variant", [0, 1])
@@ -797,8 +857,8 @@ def test_tf32_space_to_depth_strided_blocked_layers():
     rec = {}
     orig = nets.conv_tf32
 
-    def spy(l, n, x, wp, out, epilogue=0, skip=None, stream=None, in_view=None):
-        orig(l, n, x, wp, out, epilogue, skip, stream, in_view)
+    def spy(l, n, x, wp, out, epilogue=0, skip=None, stream=None, in_view=None, **kw):
+        orig(l, n, x, wp, out, epilogue, skip, stream, in_view, **kw)
         torch.cuda.synchronize()
         rec[l.name] = (l, x.buf.clone(), out.buf.clone(), out, epilogue)
     nets.conv_tf32 = spy
