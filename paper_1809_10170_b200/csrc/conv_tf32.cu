@@ -394,6 +394,7 @@ int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t
   p.row_groups = (p.h_o + p.MT * kTileRows - 1) / (p.MT * kTileRows);
   p.strips = (p.w_o + kTW - 1) / kTW;
   p.units = p.n * p.row_groups * p.strips * p.n_cg;
+  p.stack = 1;
   // instruction descriptor: D f32, A/B tf32, K-major both, N, M = 128
   p.idesc = tf32_idesc(p.N);
 

@@ -132,10 +132,25 @@ __global__ void __launch_bounds__(kThreadsX, 1)
           // the TMA box always lands whole (OOB elements zero-filled)
           const uint32_t patch_bytes = 2u * (uint32_t)(p.G * p.PH * p.PW * 4) * 4u;
           const uint32_t wbytes = (uint32_t)(Ge * Re * p.w_f * 4 * p.N * 4) * 4u;
-          mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes);
-          tma_load_5d(sp, &tmap, 0, 0, x0, y0 + n0, img * p.ib_n + ib0, &full[buf]);
-          tma_load_5d(sp + p.plane_floats, &tmap, 0, 1, x0, y0 + n0, img * p.ib_n + ib0,
-                      &full[buf]);
+          if (p.stack > 1) {
+            // one box per (image slot, input block): slot k of block g lands
+            // at patch row k * SP of that block's rows
+            const int slots = min(p.stack, p.n - img);
+            const uint32_t box = (uint32_t)(p.SP * p.PW * 4) * 4u;
+            mbar_arrive_expect_tx(&full[buf], 2u * box * (uint32_t)(slots * Ge) + wbytes);
+            for (int k = 0; k < slots; ++k)
+              for (int gi = 0; gi < Ge; ++gi) {
+                float* dst = sp + (gi * p.PH + k * p.SP) * p.PW * 4;
+                const int c4 = (img + k) * p.ib_n + ib0 + gi;
+                tma_load_5d(dst, &tmap, 0, 0, x0, n0, c4, &full[buf]);
+                tma_load_5d(dst + p.plane_floats, &tmap, 0, 1, x0, n0, c4, &full[buf]);
+              }
+          } else {
+            mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes);
+            tma_load_5d(sp, &tmap, 0, 0, x0, y0 + n0, img * p.ib_n + ib0, &full[buf]);
+            tma_load_5d(sp + p.plane_floats, &tmap, 0, 1, x0, y0 + n0, img * p.ib_n + ib0,
+                        &full[buf]);
+          }
           const float* wsrc =
               p.w + (((int64_t)cg * p.ib_n + ib0) * p.h_f + n0) * (int64_t)p.w_f * 4 * p.N * 4;
           bulk_g2s(sp + 4 * p.plane_floats, wsrc, wbytes, &full[buf]);
@@ -149,7 +164,7 @@ __global__ void __launch_bounds__(kThreadsX, 1)
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       int img, y0, x0, cg;
       decode_unit(p, u, img, y0, x0, cg);
-      const int valid_rows = min(p.MT * kTileRows, p.h_o - y0);
+      const int valid_rows = p.stack > 1 ? p.MT * kTileRows : min(p.MT * kTileRows, p.h_o - y0);
       const int mts = (valid_rows + kTileRows - 1) / kTileRows;
       int g = 0, r = 0, ci = 0;
       uint32_t acc_base = 0, accum = 0;
@@ -224,7 +239,10 @@ __global__ void __launch_bounds__(kThreadsX, 1)
     }
   } else {
     // ----------------------------------------------------------- operand split
-    // x -> x_hi (in place) and x_lo = x - x_hi (second plane pair)
+    // x_lo = x - x_hi into the second plane pair.  x_hi is the raw patch:
+    // kind::tf32 reads only the top 19 bits of an fp32 operand (truncation;
+    // a rounding tensor core would make x_hi + x_lo != x and fail the fp32
+    // tolerance tests by orders of magnitude, tests/test_gpu_parity.py).
     const int t = threadIdx.x - 64;
     int gs = 0, buf = 0;
     uint32_t phase = 0;
@@ -233,13 +251,12 @@ __global__ void __launch_bounds__(kThreadsX, 1)
       for (int st = 0; st < S; ++st, ++gs) {
         if (gs > 0 && ++buf == p.NS) { buf = 0; phase ^= 1u; }
         mbar_wait(&full[buf], phase);
-        float4* hi = reinterpret_cast<float4*>(smem + buf * p.stage_floats);
-        float4* lo = hi + n4;
+        const float4* hi = reinterpret_cast<const float4*>(smem + buf * p.stage_floats);
+        float4* lo = reinterpret_cast<float4*>(smem + buf * p.stage_floats) + n4;
 #pragma unroll 4
         for (int i = t; i < n4; i += kSplitWarps * 32) {
           const float4 v = hi[i];
           const float4 h = hi4(v);
-          hi[i] = h;
           lo[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
         }
         fence_proxy_async_smem();  // generic-proxy writes -> tcgen05.mma operands
@@ -261,7 +278,7 @@ __global__ void __launch_bounds__(kThreadsX, 1)
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       int img, y0, x0, cg;
       decode_unit(p, u, img, y0, x0, cg);
-      const int valid_rows = min(p.MT * kTileRows, p.h_o - y0);
+      const int valid_rows = p.stack > 1 ? p.MT * kTileRows : min(p.MT * kTileRows, p.h_o - y0);
       const int mts = (valid_rows + kTileRows - 1) / kTileRows;
       float tot[COLS];
       for (int c = 0; c < n_chunks; ++c, ++cs) {
@@ -295,10 +312,11 @@ __global__ void __launch_bounds__(kThreadsX, 1)
         const int mt = j / cpm;
         const int c0 = ch * (p.N / 2) + (j - mt * cpm) * 32;
         if (mt < mts) {
-          const int y = y0 + mt * kTileRows + ty;
-          const bool valid = y < p.h_o && x < p.w_o;
-          emit32(p, *reinterpret_cast<float(*)[32]>(&tot[j * 32]), img, y, x, valid, tx, ty, cg,
-                 c0);
+          int im, y;
+          bool ok;
+          tile_row_pixel(p, img, y0, mt * kTileRows + ty, im, y, ok);
+          emit32(p, *reinterpret_cast<float(*)[32]>(&tot[j * 32]), im, y, x, ok && x < p.w_o, tx,
+                 ty, cg, c0);
         }
       }
     }
@@ -399,24 +417,46 @@ int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream
   p.n_cg = (f.jb_count * 8 + p.N - 1) / p.N;
   const int sms = sm_count();
   const int wtap = 4 * p.N * 4 * 4;  // bytes per (i', n, m): hi + lo
+  // Filter rows per stage when the whole filter's hi/lo weights of one
+  // input block fit the 72 KB weight budget: all of them, else as many as fit.
+  auto rows_for = [&](int r_cap) {
+    return p.h_f * p.w_f * wtap <= 72 * 1024 && r_cap == p.h_f
+               ? p.h_f
+               : std::max(1, std::min(r_cap, (72 * 1024) / (p.w_f * wtap)));
+  };
+  // Image slots per unit: small maps (h_o = 7) stack images along the tile
+  // rows, slot k at patch row k * SP (SP = h_o + R - 1), instead of leaving
+  // most of a 16-row M-tile empty.  Not with the fused pool (its windows
+  // pair tile rows).
+  auto stack_for = [&](int mt, int R) {
+    const int sp = p.h_o + R - 1;
+    if ((p.epi & DCONV_EPI_MAXPOOL) || p.h_o + sp > mt * kTileRows) return 1;
+    static const bool no_stack = getenv("DCONV_NO_STACK") != nullptr;
+    return no_stack ? 1 : std::min(p.n, (mt * kTileRows - p.h_o) / sp + 1);
+  };
   // M-tiles per unit (MT * N in {128, 256}: two chunk sets fit TMEM, the
   // totals fit the epilogue registers).  Cost per input block = max(3 MMAs
-  // per tap and M-tile, shared-memory traffic at ~120 B/cycle: the MMAs read
-  // A + B from smem, the TMA writes patch + hi/lo weights, the split warps
-  // read and rewrite the patch) + per-unit fill / epilogue.
+  // per tap and M-tile; shared-memory traffic at ~120 B/cycle (MMA operand
+  // reads, TMA writes, the split's read + write); L2 -> SM loads at ~40
+  // B/cycle (patch + hi/lo weights)) + per-unit fill / epilogue; rounds of
+  // units over the SMs.
   {
     double best = -1;
     for (int mt = kMaxMT; mt >= 1; --mt) {
       const int cols = mt * p.N / 2;
       if (cols != 64 && cols != 128) continue;
-      const int rg = (p.h_o + mt * kTileRows - 1) / (mt * kTileRows);
-      const int64_t units = (int64_t)p.n * rg * ((p.w_o + kTW - 1) / kTW) * p.n_cg;
+      const int st = stack_for(mt, rows_for(p.h_f));
+      const int rg = st > 1 ? 1 : (p.h_o + mt * kTileRows - 1) / (mt * kTileRows);
+      const int64_t units =
+          (int64_t)((p.n + st - 1) / st) * rg * ((p.w_o + kTW - 1) / kTW) * p.n_cg;
       const double taps = (double)p.h_f * p.w_f;
       const double mma_cyc = p.N > 128 ? 128.0 : 71.0;
       const double mma = taps * mt * 3 * mma_cyc;
       const double patch = (double)(mt * kTileRows - 1 + p.h_f) * (kTW - 1 + p.w_f) * 32.0;
-      const double smem_bytes = taps * mt * 3 * (4096.0 + p.N * 32.0) + taps * wtap + patch * 4;
-      const double unit = p.ib_n * std::max(mma, smem_bytes / 120.0) + 1500.0;
+      const double smem_bytes = taps * mt * 3 * (4096.0 + p.N * 32.0) + taps * wtap + patch * 3;
+      const double l2_bytes = taps * wtap + patch;
+      const double unit =
+          p.ib_n * std::max({mma, smem_bytes / 120.0, l2_bytes / 40.0}) + 1500.0;
       const double rounds = (double)((units + sms - 1) / sms);
       const double score = 1.0 / (rounds * unit);
       if (score > best * (1 + 1e-9)) {
@@ -437,16 +477,27 @@ int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream
   const int bar_bytes = (3 * kMaxStagesT + 4) * 8 + 16;
   int stage_bytes = 0;
   for (int r_cap = p.h_f;; ) {
-    const int patch_blk_bytes = 4 * (p.MT * kTileRows - 1 + std::min(p.h_f, r_cap)) * p.PW * 16;
-    if (p.h_f * p.w_f * wtap <= 72 * 1024 && r_cap == p.h_f) {
-      p.R = p.h_f;
-      p.G = std::max(1, std::min({p.ib_n, (72 * 1024) / (p.h_f * p.w_f * wtap),
-                                  (40 * 1024) / patch_blk_bytes}));
-    } else {
-      p.G = 1;
-      p.R = std::max(1, std::min(r_cap, (72 * 1024) / (p.w_f * wtap)));
+    p.R = rows_for(r_cap);
+    p.stack = stack_for(p.MT, p.R);
+    p.SP = p.h_o + p.R - 1;
+    p.PW = kTW - 1 + p.w_f;
+    if (p.stack > 1) {
+      // every slot's TMA destination (row k*SP of a block) 128-byte aligned:
+      // widen the smem row pitch (= box width; the extra columns are
+      // out-of-bounds zero fill or unused pixels) so SP*PW % 8 == 0
+      int pw = p.PW;
+      while ((p.SP * pw) % 8) ++pw;
+      if (pw <= 16) p.PW = pw; else p.stack = 1;
     }
-    p.PH = p.MT * kTileRows - 1 + p.R;
+    // patch rows per input block (stacked: every slot's rows; rows read by
+    // never-stored tile rows stay inside the block; blocks 128-B aligned)
+    p.PH = std::max(p.MT * kTileRows - 1 + p.R, p.stack > 1 ? p.stack * p.SP : 0);
+    if (p.stack > 1)
+      while ((p.PH * p.PW) % 8) ++p.PH;
+    const int patch_blk_bytes = 4 * p.PH * p.PW * 16;
+    p.G = p.R == p.h_f ? std::max(1, std::min({p.ib_n, (72 * 1024) / (p.h_f * p.w_f * wtap),
+                                               (40 * 1024) / patch_blk_bytes}))
+                       : 1;
     p.plane_floats = (p.G * p.PH * p.PW * 4 + 31) & ~31;  // 128 B aligned planes
     p.wstage_floats = p.G * p.R * p.w_f * 4 * p.N * 4;
     p.stage_floats = ((4 * p.plane_floats + p.wstage_floats) + 255) & ~255;  // 1 KB aligned
@@ -471,20 +522,24 @@ int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream
   static const int chunk_k = getenv("DCONV_X3_CHUNK_K") ? atoi(getenv("DCONV_X3_CHUNK_K")) : 288;
   const int k_stage = p.G * p.R * p.w_f * 8;
   p.chunk_st = std::max(1, chunk_k / k_stage);
-  p.row_groups = (p.h_o + p.MT * kTileRows - 1) / (p.MT * kTileRows);
+  p.row_groups = p.stack > 1 ? 1 : (p.h_o + p.MT * kTileRows - 1) / (p.MT * kTileRows);
   p.strips = (p.w_o + kTW - 1) / kTW;
-  p.units = p.n * p.row_groups * p.strips * p.n_cg;
+  p.units = (p.n + p.stack - 1) / p.stack * p.row_groups * p.strips * p.n_cg;
   p.idesc = tf32_idesc(p.N);
 
   CUtensorMap map;
-  if (int rc = encode_input_map(&map, f, px_floats, p.PW, p.PH, p.G)) return rc;
+  // stacked: one box per (image slot, block), SP rows; else PH rows x G blocks
+  if (int rc = p.stack > 1 ? encode_input_map(&map, f, px_floats, p.PW, p.SP, 1)
+                           : encode_input_map(&map, f, px_floats, p.PW, p.PH, p.G))
+    return rc;
   set_x3_attrs();
   const size_t smem = (size_t)p.NS * stage_bytes + bar_bytes;
   const int grid = std::min(p.units, sms);
   static const bool dbg = getenv("DCONV_DEBUG") != nullptr;
   if (dbg)
-    fprintf(stderr, "conv_tf32x3 N=%d MT=%d G=%d R=%d NS=%d stage=%d B chunk_st=%d units=%d\n",
-            p.N, p.MT, p.G, p.R, p.NS, stage_bytes, p.chunk_st, p.units);
+    fprintf(stderr,
+            "conv_tf32x3 N=%d MT=%d G=%d R=%d NS=%d stage=%d B chunk_st=%d stack=%d units=%d\n",
+            p.N, p.MT, p.G, p.R, p.NS, stage_bytes, p.chunk_st, p.stack, p.units);
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

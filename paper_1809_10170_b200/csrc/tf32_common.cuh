@@ -35,6 +35,8 @@ struct Tf32Params {
   int row_groups, strips, units;
   int MT;             // M-tiles per unit (1..4)
   int chunk_st;       // split-TF32: stages per TMEM accumulator chunk
+  int stack;          // images stacked along the tile rows (small maps), 1 = off
+  int SP;             // stacked mode: patch rows per image slot (h_o + R - 1)
   uint32_t idesc;
   unsigned long long* dbg;  // DCONV_TF32_PROFILE: per-CTA wait cycles (else null)
 };
@@ -90,7 +92,8 @@ __device__ __forceinline__ void tmem_ld32x32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// unit u -> (channel group fastest, then strip, row group, image)
+// unit u -> (channel group fastest, then strip, row group, image (group));
+// with p.stack > 1 a unit holds images img .. img + stack - 1 (one row group)
 __device__ __forceinline__ void decode_unit(const Tf32Params& p, int u, int& img, int& y0, int& x0,
                                             int& cg) {
   cg = u % p.n_cg;
@@ -98,9 +101,26 @@ __device__ __forceinline__ void decode_unit(const Tf32Params& p, int u, int& img
   const int strip = t % p.strips;
   t /= p.strips;
   const int rg = t % p.row_groups;
-  img = t / p.row_groups;
+  img = (t / p.row_groups) * p.stack;
   y0 = rg * p.MT * kTileRows;
   x0 = strip * kTW;
+}
+
+// Tile row j (0 .. MT*16-1) of a unit -> (image, output row).  Stacked
+// images: slot k = j / SP holds image img + k, output row j - k*SP (rows
+// h_o .. SP-1 of a slot mix two images' patch rows and are never stored).
+__device__ __forceinline__ void tile_row_pixel(const Tf32Params& p, int img, int y0, int j,
+                                               int& im, int& y, bool& ok) {
+  if (p.stack > 1) {
+    const int k = j / p.SP;
+    im = img + k;
+    y = j - k * p.SP;
+    ok = k < p.stack && y < p.h_o && im < p.n;
+  } else {
+    im = img;
+    y = y0 + j;
+    ok = y < p.h_o;
+  }
 }
 
 // Epilogue for 32 accumulator columns (4 output blocks starting at channel c0

@@ -633,7 +633,9 @@ def test_tf32_tensor_core_parity(ci, co, h, w, f, n):
                                             (8, 72, 12, 12, 5, 1), (96, 136, 9, 30, 3, 2),
                                             (40, 264, 20, 11, 3, 2), (24, 512, 35, 9, 3, 1),
                                             (512, 512, 9, 9, 3, 2), (256, 256, 16, 16, 3, 2),
-                                            (1024, 256, 14, 14, 1, 2), (64, 64, 58, 58, 3, 1)])
+                                            (1024, 256, 14, 14, 1, 2), (64, 64, 58, 58, 3, 1),
+                                            (64, 128, 9, 9, 3, 3), (96, 256, 7, 7, 1, 5),
+                                            (40, 72, 6, 11, 1, 4)])
 def test_tf32x3_meets_fp32_tolerance(ci, co, h, w, f, n):
     """The split-TF32 tensor-core kernel against the fp64 oracle with the
     fp32 FFMA tolerance |a-b| <= 1e-4 + 1e-5|b| (north_star), up to
@@ -650,12 +652,16 @@ def test_tf32x3_meets_fp32_tolerance(ci, co, h, w, f, n):
         assert not po.within_tol(one[0], want, ATOL, RTOL)[0]
 
 
-def test_tf32x3_epilogue_and_padding():
-    x = po.uniform((2, 40, 12, 12), 95, 0)
+@pytest.mark.parametrize("n,h", [(2, 12), (3, 9)])
+def test_tf32x3_epilogue_and_padding(n, h):
+    """ReLU + skip epilogue and zero padded channels; h = 9 (7x7 output)
+    runs with two images stacked per M-tile (the last unit half empty)."""
+    x = po.uniform((n, 40, h, h), 95, 0)
     k = po.uniform((40, 20, 3, 3), 95, 1)
-    skip = np.stack([po.pack_feature_map(po.uniform((20, 10, 10), 95, 2 + i), 8) for i in range(2)])
+    skip = np.stack([po.pack_feature_map(po.uniform((20, h - 2, h - 2), 95, 2 + i), 8)
+                     for i in range(n)])
     got = run_conv_tf32(x, k, relu=True, skip=skip, x3=True)
-    for i in range(2):
+    for i in range(n):
         want = np.maximum(po.pack_feature_map(po.conv_oracle64(x[i], k, 1), 8) + skip[i], 0)
         assert_tol(got[i], want, f"tf32x3 relu+skip img {i}")
         assert not got[i][-1][..., 4:].any(), "padded output channels must be exact 0"

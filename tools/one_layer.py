@@ -1,5 +1,5 @@
 """Runs one conv layer a few times (for ncu / compute-sanitizer captures).
-usage: python tools/one_layer.py CI CO HI WI F S N [reps] [ffma|tf32|first|ffma_add|tf32_add]
+usage: python tools/one_layer.py CI CO HI WI F S N [reps] [ffma|tf32|tf32x3|first|ffma_add|tf32_add|tf32x3_add]
 (first: the first-layer reader on a dense [N][CI][HI][WI] input)"""
 import sys
 
@@ -26,9 +26,10 @@ if algo.endswith("_add"):  # ResNet block tail: relu(conv + skip)
     sk.buf.uniform_(-1, 1)
     epi = 3
     algo = algo[:-4]
-if algo == "tf32":
-    wp = nets.prepare_tf32(l, w)
-    run = lambda: nets.conv_tf32(l, n, x, wp, y, epi, sk)  # noqa: E731
+if algo in ("tf32", "tf32x3"):
+    x3 = algo == "tf32x3"
+    wp = nets.prepare_tf32(l, w, x3=x3)
+    run = lambda: nets.conv_tf32(l, n, x, wp, y, epi, sk, x3=x3)  # noqa: E731
 else:
     run = lambda: nets.conv(l, n, x, w, y, epi, sk)  # noqa: E731
 for _ in range(reps):
