@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "tf32_common.cuh"
 
@@ -42,6 +43,9 @@ constexpr int kSplitWarps = 2;
 constexpr int kEpiWarpsX = 8;
 constexpr int kThreadsX = (4 + kEpiWarpsX) * 32;
 constexpr uint32_t kHiMask = 0xFFFFE000u;  // TF32: sign, exponent, 10 mantissa bits
+// Role wait-cycle instrumentation (DCONV_TF32_PROFILE), compiled in only when
+// set here: it costs registers in the 56-register producer/MMA/split group.
+constexpr bool kProf = false;
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
@@ -106,6 +110,9 @@ __global__ void __launch_bounds__(kThreadsX, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
+  // DCONV_TF32_PROFILE: per-role wait cycles (lane 0 of warps 0, 1, 2)
+  long long prof = 0, prof2 = 0;
+  const long long prof_t0 = kProf && p.dbg ? clock64() : 0;
   pdl_wait();  // programmatic dependent launch: input readable from here on
   pdl_launch_dependents();
 
@@ -125,7 +132,11 @@ __global__ void __launch_bounds__(kThreadsX, 1)
         for (int st = 0; st < S; ++st, ++gs) {
           if (st > 0 && ++r == p.n_r) { r = 0; ++g; }
           if (gs > 0 && ++buf == p.NS) { buf = 0; phase ^= 1u; }
-          if (gs >= p.NS) mbar_wait_backoff(&empty[buf], phase ^ 1u, 64);
+          if (gs >= p.NS) {
+            const long long t0 = kProf && p.dbg ? clock64() : 0;
+            mbar_wait_backoff(&empty[buf], phase ^ 1u, 64);
+            if (kProf && p.dbg) prof += clock64() - t0;
+          }
           const int ib0 = g * p.G, n0 = r * p.R;
           const int Ge = min(p.G, p.ib_n - ib0), Re = min(p.R, p.h_f - n0);
           float* sp = smem + buf * p.stage_floats;
@@ -174,11 +185,19 @@ __global__ void __launch_bounds__(kThreadsX, 1)
         if (ci == 0) {
           // new chunk: its accumulator set must have been drained
           const int set = cs & 1;
-          if (cs >= 2) mbar_wait(&chunk_empty[set], ((cs >> 1) - 1) & 1);
+          if (cs >= 2) {
+            const long long t0 = kProf && p.dbg ? clock64() : 0;
+            mbar_wait(&chunk_empty[set], ((cs >> 1) - 1) & 1);
+            if (kProf && p.dbg) prof2 += clock64() - t0;
+          }
           acc_base = tmem_base + (uint32_t)set * kSetCols;
           accum = 0u;
         }
-        mbar_wait(&split[buf], phase);
+        {
+          const long long t0 = kProf && p.dbg ? clock64() : 0;
+          mbar_wait(&split[buf], phase);
+          if (kProf && p.dbg) prof += clock64() - t0;
+        }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int Ge = min(p.G, p.ib_n - g * p.G);
         const int Re = min(p.R, p.h_f - r * p.R);
@@ -250,7 +269,9 @@ __global__ void __launch_bounds__(kThreadsX, 1)
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       for (int st = 0; st < S; ++st, ++gs) {
         if (gs > 0 && ++buf == p.NS) { buf = 0; phase ^= 1u; }
+        const long long t0 = kProf && p.dbg ? clock64() : 0;
         mbar_wait(&full[buf], phase);
+        if (kProf && p.dbg) prof += clock64() - t0;
         const float4* hi = reinterpret_cast<const float4*>(smem + buf * p.stage_floats);
         float4* lo = reinterpret_cast<float4*>(smem + buf * p.stage_floats) + n4;
 #pragma unroll 4
@@ -322,6 +343,11 @@ __global__ void __launch_bounds__(kThreadsX, 1)
     }
   }
 
+  if (kProf && p.dbg && lane == 0 && warp <= 2) {
+    p.dbg[blockIdx.x * 8 + warp] = prof;
+    if (warp == 1) p.dbg[blockIdx.x * 8 + 4] = prof2;
+    if (warp == 1) p.dbg[blockIdx.x * 8 + 5] = clock64() - prof_t0;
+  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) {
@@ -540,6 +566,23 @@ int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream
     fprintf(stderr,
             "conv_tf32x3 N=%d MT=%d G=%d R=%d NS=%d stage=%d B chunk_st=%d stack=%d units=%d\n",
             p.N, p.MT, p.G, p.R, p.NS, stage_bytes, p.chunk_st, p.stack, p.units);
+  static const bool prof = kProf && getenv("DCONV_TF32_PROFILE") != nullptr;
+  if (prof) {  // debugging aid: where do the roles wait?  (not for timed runs)
+    cudaMalloc(&p.dbg, (size_t)grid * 8 * 8);
+    cudaMemsetAsync(p.dbg, 0, (size_t)grid * 8 * 8, stream);
+    pick_x3_kernel(p)<<<grid, kThreadsX, smem, stream>>>(map, p);
+    std::vector<unsigned long long> h((size_t)grid * 8);
+    cudaMemcpy(h.data(), p.dbg, h.size() * 8, cudaMemcpyDeviceToHost);
+    double a[6] = {0, 0, 0, 0, 0, 0};
+    for (int b = 0; b < grid; ++b)
+      for (int i = 0; i < 6; ++i) a[i] += (double)h[b * 8 + i] / grid;
+    fprintf(stderr,
+            "conv_tf32x3 profile: avg cycles producer(empty)=%.0f mma(split)=%.0f "
+            "mma(chunk_empty)=%.0f split(full)=%.0f total=%.0f\n",
+            a[0], a[1], a[4], a[2], a[5]);
+    cudaFree(p.dbg);
+    p.dbg = nullptr;
+  }
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
