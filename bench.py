@@ -374,7 +374,8 @@ def main_gpu(args):
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tfile):
         try:
-            t = json.load(open(tfile)).get(args.config)
+            key = args.config if args.algo == "ffma" else f"{args.config}_{args.algo}"
+            t = json.load(open(tfile)).get(key)
             if t:
                 traffic = t["dram_bytes"]
                 traffic_note = (f"{t['kernel']}: dram {t['dram_bytes']} B vs algorithmic "

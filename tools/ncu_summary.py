@@ -26,6 +26,10 @@ METRICS = [
     "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
     "sm__cycles_active.avg", "sm__cycles_elapsed.avg",
     "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed",
 ]
 
 
@@ -49,16 +53,17 @@ def launches(src_csv: str):
     return out
 
 
-def step_summary(ls):
+def step_summary(ls, first="conv_first"):
     """The last complete step: launches between the last two first-layer
     launches (the final one belongs to the e2e/event passes)."""
-    idx = [i for i, (n, _, _) in enumerate(ls) if n.startswith("conv_first")]
+    idx = [i for i, (n, _, _) in enumerate(ls) if n.startswith(first)]
     a, b = idx[-3], idx[-2]
     step = ls[a:b]
     tot = sum(t for _, t, _ in step)
     agg = defaultdict(lambda: [0, 0.0])
     for n, t, _ in step:
-        k = "conv_ffma_kernel" if n.startswith("conv_ffma") else n
+        k = next((p for p in ("conv_ffma_kernel", "conv_tf32x3_kernel", "conv_tf32_kernel")
+                  if n.startswith(p)), n)
         agg[k][0] += 1
         agg[k][1] += t
     return {
@@ -106,6 +111,21 @@ def main():
         if os.path.exists(p):
             full[name] = full_metrics(p)
     json.dump(full, open(os.path.join(dst, f"{tag}_ncu_full_conv_ffma.json"), "w"), indent=1)
+    x3 = {}
+    for name, rep in (("vgg16_conv4_2_b32", "full_x3_conv4_2.ncu-rep"),
+                      ("resnet50_1x1_1024_256_b256", "full_x3_r50_1x1.ncu-rep")):
+        p = os.path.join(src, rep)
+        if os.path.exists(p):
+            x3[name] = full_metrics(p)
+    if x3:
+        json.dump(x3, open(os.path.join(dst, f"{tag}_ncu_full_conv_tf32x3.json"), "w"), indent=1)
+    xl = os.path.join(src, "launches_vgg16_tf32x3.csv")
+    if os.path.exists(xl):
+        sx = step_summary(launches(xl), first="pack")
+        sx["source"] = summ["source"].replace("--no-cpu-baseline", "--no-cpu-baseline --algo tf32x3")
+        json.dump(sx, open(os.path.join(dst, f"{tag}_ncu_launches_vgg16_b32_tf32x3.json"), "w"),
+                  indent=1)
+        print(json.dumps(sx["share_by_kernel"], indent=1))
     print(json.dumps(summ["share_by_kernel"], indent=1))
     for k, v in full.items():
         print(k, {m: v.get(m) for m in ("gpu__time_duration.sum", "dram__bytes_read.sum",
