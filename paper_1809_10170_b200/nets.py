@@ -426,9 +426,10 @@ class Plan:
         w = self.weights[l.name]
         kind = "first" if l.first else "conv"
         if self.shard is None:
-            if self.algo in TC_ALGOS and l.first and l.s > 1 and in_view is None:
+            tc = self.algo in TC_ALGOS and not (self.x3 and self._few_units(l, epilogue))
+            if tc and l.first and l.s > 1 and in_view is None:
                 return self._tf32_s2d_first(l, x, y, epilogue, skip)
-            if self.algo in TC_ALGOS and l.first and l.s == 1 and in_view is None:
+            if tc and l.first and l.s == 1 and in_view is None:
                 # TF32 path, stride-1 first layer (VGG conv1_1): zero-pad the
                 # image to one 8-channel block (a pack kernel, SPEC.md:121's
                 # first-layer choice) and run it as a blocked tcgen05 layer;
@@ -450,10 +451,10 @@ class Plan:
                                                             x3=self.x3),
                                        l.name, "tf32", n * l.flops, l))
                 return y
-            if (self.algo in TC_ALGOS and not l.first and l.s > 1 and l.h_f > 1
+            if (tc and not l.first and l.s > 1 and l.h_f > 1
                     and os.environ.get("DCONV_NO_S2D") is None):
                 return self._tf32_s2d_blocked(l, x, y, epilogue, skip, in_view)
-            if self.algo in TC_ALGOS and not l.first and (l.s == 1 or (l.h_f == 1 and l.w_f == 1)):
+            if tc and not l.first and (l.s == 1 or (l.h_f == 1 and l.w_f == 1)):
                 wp = prepare_tf32(l, w, x3=self.x3)
                 self.weights[l.name + ".tf32"] = wp
                 self.steps.append(Step(lambda st: conv_tf32(l, self.n, x, wp, y, epilogue, skip, st,
@@ -489,6 +490,17 @@ class Plan:
         if gather:
             self._gather(l.name, y, ys)
         return ys
+
+    def _few_units(self, l: Layer, epilogue: int) -> bool:
+        """Split-TF32 plans run a layer on the FFMA kernel (same fp32
+        tolerance) when it has fewer tensor-core work units (128-pixel
+        M-tiles x 128-channel groups) than SMs: batch-1 layers, where the FFMA
+        kernel's split-K over a cluster keeps every SM busy and the split-TF32
+        kernel (no split-K) would leave most of them idle."""
+        if epilogue & _abi.EPI_MAXPOOL:
+            return False
+        units = self.n * -(-l.h_o // 16) * -(-l.w_o // 8) * -(-l.c_o // 128)
+        return units < 148
 
     def _tf32_s2d_first(self, l: Layer, x, y: Act, epilogue: int, skip) -> Act:
         """TF32 path, stride-f first layer (GoogLeNet/ResNet 7x7/s2, AlexNet

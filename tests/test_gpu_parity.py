@@ -930,9 +930,15 @@ def test_full_size_plans_sampled_parity(config, n):
     finally:
         nets.conv = orig
     assert len(rec) == len(plan.layers)
-    for l, xin, yout, out, epi, skb, skip, w in rec:
-        kd = po.unpack_kernel(host(w), l.c_i, l.c_o)
-        kb = po.pack_kernel(kd, 8, 8)
+    _check_sampled(config, [(l, xin, yout, out, epi, skb, skip,
+                             po.pack_kernel(po.unpack_kernel(host(w), l.c_i, l.c_o), 8, 8))
+                            for l, xin, yout, out, epi, skb, skip, w in rec], imgs, check)
+
+
+def _check_sampled(config, rec, imgs, check):
+    """Sampled rows of every recorded launch (input, output, epilogue of the
+    first / middle / last image) against the fp64 oracle on the same input."""
+    for l, xin, yout, out, epi, skb, skip, kb in rec:
         for j in range(len(imgs)):
             x = xin[j].numpy()
             xb = (po.pack_feature_map(np.ascontiguousarray(x[:, :l.h_i, :l.w_i]), 8) if l.first
@@ -955,3 +961,51 @@ def test_full_size_plans_sampled_parity(config, n):
                 if epi & _abi.EPI_RELU:
                     want = np.maximum(want, 0)
                 check(got[:, h + r, h:h + l.w_o, :], want, f"{config}/{l.name} img {imgs[j]} row {r}")
+
+
+@pytest.mark.parametrize("config,n", [("vgg16", 32), ("resnet50", 256), ("googlenet", 64)])
+def test_tf32x3_full_size_plans_sampled_parity(config, n):
+    """The split-TF32 bench workloads at full batch: every tensor-core launch
+    (space-to-depth stems and strided layers, fused pools, skip-add
+    epilogues, image-stacked 7x7 tiles) checked on sampled rows of the
+    first / middle / last image against the fp64 oracle with the same fp32
+    bound as the FFMA plans (per element for independent layers, per layer
+    normwise for the deep chains)."""
+    normwise = config in ("vgg16", "resnet50")
+
+    def check(g, want, what):
+        if not normwise:
+            assert_tol(g, want, what)
+            return
+        scale = max(1.0, float(np.abs(want).max()))
+        err = float(np.abs(g - want).max())
+        assert err <= 1e-5 * scale + 1e-4, f"{what}: err {err} scale {scale}"
+    prepared = {}
+    orig_prep, orig_conv = nets.prepare_tf32, nets.conv_tf32
+
+    def prep_spy(l, w_blocked, stream=None, x3=False):
+        wp = orig_prep(l, w_blocked, stream, x3)
+        prepared[wp.data_ptr()] = host(w_blocked).copy()
+        return wp
+    nets.prepare_tf32 = prep_spy
+    try:
+        plan = nets.build_plan(config, n, seed=29, algo="tf32x3")
+    finally:
+        nets.prepare_tf32 = orig_prep
+    imgs = sorted({0, n // 2, n - 1})
+    rec = []
+
+    def spy(l, nn, x, wp, out, epilogue=0, skip=None, stream=None, in_view=None, x3=False):
+        assert x3
+        orig_conv(l, nn, x, wp, out, epilogue, skip, stream, in_view, x3=x3)
+        torch.cuda.synchronize()
+        kb = po.pack_kernel(po.unpack_kernel(prepared[wp.data_ptr()], l.c_i, l.c_o), 8, 8)
+        rec.append((l, x.buf[imgs].cpu(), out.buf[imgs].cpu(), out, epilogue,
+                    skip.buf[imgs].cpu() if skip is not None else None, skip, kb))
+    nets.conv_tf32 = spy
+    try:
+        plan.run()
+    finally:
+        nets.conv_tf32 = orig_conv
+    assert len(rec) == sum(1 for st in plan.steps if st.kind == "tf32") > 0
+    _check_sampled(config, rec, imgs, check)
