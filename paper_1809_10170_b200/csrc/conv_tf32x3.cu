@@ -274,11 +274,21 @@ __global__ void __launch_bounds__(kThreadsX, 1)
         if (kProf && p.dbg) prof += clock64() - t0;
         const float4* hi = reinterpret_cast<const float4*>(smem + buf * p.stage_floats);
         float4* lo = reinterpret_cast<float4*>(smem + buf * p.stage_floats) + n4;
-#pragma unroll 4
-        for (int i = t; i < n4; i += kSplitWarps * 32) {
-          const float4 v = hi[i];
-          const float4 h = hi4(v);
-          lo[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+        // batches of 8 loads in flight before any store (the stores could
+        // alias later loads for the compiler, which would serialise them)
+        constexpr int kStep = kSplitWarps * 32;
+        for (int i0 = t; i0 < n4; i0 += 8 * kStep) {
+          float4 v[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (i0 + k * kStep < n4) v[k] = hi[i0 + k * kStep];
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (i0 + k * kStep < n4) {
+              const float4 h = hi4(v[k]);
+              lo[i0 + k * kStep] = make_float4(v[k].x - h.x, v[k].y - h.y, v[k].z - h.z,
+                                               v[k].w - h.w);
+            }
         }
         fence_proxy_async_smem();  // generic-proxy writes -> tcgen05.mma operands
         __syncwarp();
