@@ -113,10 +113,25 @@ __global__ void __launch_bounds__(kThreadsT, 1)
           // the TMA box always lands whole (OOB elements zero-filled)
           const uint32_t patch_bytes = 2u * (uint32_t)(p.G * p.PH * p.PW * 4) * 4u;
           const uint32_t wbytes = (uint32_t)(Ge * Re * p.w_f * 2 * p.N * 4) * 4u;
-          mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes);
-          tma_load_5d(sp, &tmap, 0, 0, x0, y0 + n0, img * p.ib_n + ib0, &full[buf]);
-          tma_load_5d(sp + p.plane_floats, &tmap, 0, 1, x0, y0 + n0, img * p.ib_n + ib0,
-                      &full[buf]);
+          if (p.stack > 1) {
+            // image-stacked tile: one box per (image slot, input block) at
+            // patch row k * SP of that block (see conv_tf32x3.cu)
+            const int slots = min(p.stack, p.n - img);
+            const uint32_t box = (uint32_t)(p.SP * p.PW * 4) * 4u;
+            mbar_arrive_expect_tx(&full[buf], 2u * box * (uint32_t)(slots * Ge) + wbytes);
+            for (int k = 0; k < slots; ++k)
+              for (int gi = 0; gi < Ge; ++gi) {
+                float* dst = sp + (gi * p.PH + k * p.SP) * p.PW * 4;
+                const int c4 = (img + k) * p.ib_n + ib0 + gi;
+                tma_load_5d(dst, &tmap, 0, 0, x0, n0, c4, &full[buf]);
+                tma_load_5d(dst + p.plane_floats, &tmap, 0, 1, x0, n0, c4, &full[buf]);
+              }
+          } else {
+            mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes);
+            tma_load_5d(sp, &tmap, 0, 0, x0, y0 + n0, img * p.ib_n + ib0, &full[buf]);
+            tma_load_5d(sp + p.plane_floats, &tmap, 0, 1, x0, y0 + n0, img * p.ib_n + ib0,
+                        &full[buf]);
+          }
           const float* wsrc =
               p.w + (((int64_t)cg * p.ib_n + ib0) * p.h_f + n0) * (int64_t)p.w_f * 2 * p.N * 4;
           bulk_g2s(sp + 2 * p.plane_floats, wsrc, wbytes, &full[buf]);
@@ -130,7 +145,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
     for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++ui) {
       int img, y0, x0, cg;
       decode(u, img, y0, x0, cg);
-      const int valid_rows = min(p.MT * kTileRows, p.h_o - y0);
+      const int valid_rows = p.stack > 1 ? p.MT * kTileRows : min(p.MT * kTileRows, p.h_o - y0);
       const int mts = (valid_rows + kTileRows - 1) / kTileRows;
       const int ab = nacc == 2 ? (ui & 1) : 0, au = nacc == 2 ? (ui >> 1) : ui;
       const uint32_t acc_base = tmem_base + (uint32_t)ab * acc_cols;
@@ -225,14 +240,16 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int x = x0 + tx;
       for (int mt = 0; mt < p.MT; ++mt) {
-        const int y = y0 + mt * kTileRows + ty;
-        if (y0 + mt * kTileRows >= p.h_o) break;  // warp-uniform
-        const bool valid = y < p.h_o && x < p.w_o;
+        if (p.stack == 1 && y0 + mt * kTileRows >= p.h_o) break;  // warp-uniform
+        int im, y;
+        bool ok;
+        tile_row_pixel(p, img, y0, mt * kTileRows + ty, im, y, ok);
+        const bool valid = ok && x < p.w_o;
         const int half_n = p.N / 2;  // >= 32
         for (int c0 = ch * half_n; c0 < (ch + 1) * half_n; c0 += 32) {
           float v[32];
           tmem_ld32x32(acc_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(mt * p.N + c0), v);
-          emit32(p, v, img, y, x, valid, tx, ty, cg, c0);
+          emit32(p, v, im, y, x, valid, tx, ty, cg, c0);
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -350,8 +367,13 @@ int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t
     double best = -1;
     for (int mt = kMaxMT; mt >= 1; --mt) {
       if (mt * p.N > 512) continue;  // accumulators: MT x N TMEM columns
-      const int rg = (p.h_o + mt * kTileRows - 1) / (mt * kTileRows);
-      const int64_t units = (int64_t)p.n * rg * strips * p.n_cg;
+      // small maps stack images along the tile rows (below)
+      const int sp = p.h_o + p.h_f - 1;
+      const int st = !(p.epi & DCONV_EPI_MAXPOOL) && p.h_o + sp <= mt * kTileRows
+                         ? std::min(p.n, (mt * kTileRows - p.h_o) / sp + 1)
+                         : 1;
+      const int rg = st > 1 ? 1 : (p.h_o + mt * kTileRows - 1) / (mt * kTileRows);
+      const int64_t units = (int64_t)((p.n + st - 1) / st) * rg * strips * p.n_cg;
       const double taps = (double)p.h_f * p.w_f;
       const double mma = taps * mt * (p.N > 128 ? 128.0 : 78.0);
       const double bytes = (double)(mt * kTileRows - 1 + p.h_f) * (kTW - 1 + p.w_f) * 32.0 +
@@ -369,18 +391,32 @@ int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t
     if (const char* e = force_mt)
       p.MT = std::max(1, std::min(std::min(kMaxMT, 512 / p.N), atoi(e)));
   }
-  const int patch_blk_bytes = 2 * (p.MT * kTileRows - 1 + p.h_f) * p.PW * 16;  // both planes
-  if (p.h_f * p.w_f * wtap <= 48 * 1024) {
-    p.R = p.h_f;
-    p.G = std::max(1, std::min({p.ib_n, (48 * 1024) / (p.h_f * p.w_f * wtap),
-                                (40 * 1024) / patch_blk_bytes}));
-  } else {
-    p.G = 1;
-    p.R = std::max(1, std::min(p.h_f, (48 * 1024) / (p.w_f * wtap)));
+  // filter rows per stage, then image stacking for small maps (h_o = 7:
+  // slot k of a unit holds image img + k at tile row k * SP; not with the
+  // fused pool), then the input blocks per stage
+  p.R = p.h_f * p.w_f * wtap <= 48 * 1024
+            ? p.h_f
+            : std::max(1, std::min(p.h_f, (48 * 1024) / (p.w_f * wtap)));
+  p.SP = p.h_o + p.R - 1;
+  p.stack = 1;
+  static const bool no_stack = getenv("DCONV_NO_STACK") != nullptr;
+  if (!no_stack && !(p.epi & DCONV_EPI_MAXPOOL) && p.h_o + p.SP <= p.MT * kTileRows) {
+    int pw = p.PW;
+    while ((p.SP * pw) % 8) ++pw;  // 128-B aligned slot boxes
+    if (pw <= 16) {
+      p.PW = pw;
+      p.stack = std::min(p.n, (p.MT * kTileRows - p.h_o) / p.SP + 1);
+    }
   }
+  p.PH = std::max(p.MT * kTileRows - 1 + p.R, p.stack > 1 ? p.stack * p.SP : 0);
+  if (p.stack > 1)
+    while ((p.PH * p.PW) % 8) ++p.PH;
+  const int patch_blk_bytes = 2 * p.PH * p.PW * 16;  // both planes
+  p.G = p.R == p.h_f ? std::max(1, std::min({p.ib_n, (48 * 1024) / (p.h_f * p.w_f * wtap),
+                                             (40 * 1024) / patch_blk_bytes}))
+                     : 1;
   p.n_g = (p.ib_n + p.G - 1) / p.G;
   p.n_r = (p.h_f + p.R - 1) / p.R;
-  p.PH = p.MT * kTileRows - 1 + p.R;
   if (p.PH > 256 || p.PW > 256 || p.G > 256)
     return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_tf32: TMA box too large");
   p.plane_floats = (p.G * p.PH * p.PW * 4 + 31) & ~31;  // TMA destinations 128 B aligned
@@ -391,16 +427,17 @@ int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t
   p.NS = std::min(kMaxStagesT, (220 * 1024 - bar_bytes) / stage_bytes);
   if (p.NS < 2)
     return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_tf32: stage of %d bytes", stage_bytes);
-  p.row_groups = (p.h_o + p.MT * kTileRows - 1) / (p.MT * kTileRows);
+  p.row_groups = p.stack > 1 ? 1 : (p.h_o + p.MT * kTileRows - 1) / (p.MT * kTileRows);
   p.strips = (p.w_o + kTW - 1) / kTW;
-  p.units = p.n * p.row_groups * p.strips * p.n_cg;
-  p.stack = 1;
+  p.units = (p.n + p.stack - 1) / p.stack * p.row_groups * p.strips * p.n_cg;
   // instruction descriptor: D f32, A/B tf32, K-major both, N, M = 128
   p.idesc = tf32_idesc(p.N);
 
   // tensor map over the input view: {c4, half, W, H, image*block}
   CUtensorMap map;
-  if (int rc = encode_input_map(&map, f, px_floats, p.PW, p.PH, p.G)) return rc;
+  if (int rc = p.stack > 1 ? encode_input_map(&map, f, px_floats, p.PW, p.SP, 1)
+                           : encode_input_map(&map, f, px_floats, p.PW, p.PH, p.G))
+    return rc;
 
   static int sms = 0;
   static bool attr = false;
