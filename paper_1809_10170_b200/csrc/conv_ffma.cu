@@ -962,7 +962,11 @@ void pick_tile(FfmaParams& p, int BM, int BN, int co_groups, int sms, const int*
 template <int BN, int NW, int TPX, int TCO>
 size_t configure(FfmaParams& p, int ks, bool fine) {
   constexpr int CG = BN / 8;
-  const int kWeightBudget = 40 * 1024, kPatchBudget = 32 * 1024;
+  // patch budget: 1x1 layers stage twice the input blocks per stage (their
+  // stages are short: one tap per block; ResNet-50 256->64 at 56x56 +17%)
+  static const int patch_kb = getenv("DCONV_PATCH_BUDGET") ? atoi(getenv("DCONV_PATCH_BUDGET")) : 0;
+  const int kWeightBudget = 40 * 1024;
+  const int kPatchBudget = (patch_kb ? patch_kb : (p.h_f * p.w_f == 1 ? 64 : 32)) * 1024;
   const int full_taps_bytes = CG * p.h_f * p.w_f * kCB * kCB * 4;
   if (full_taps_bytes <= kWeightBudget) {
     p.R = p.h_f;
