@@ -70,3 +70,28 @@ def test_product_package_never_imports_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"(import\s+oracle|from\s+oracle|liboracle|pyoracle|"
                                      r"libdconv_ref|\borc_[a-z])", txt), f
+
+
+def test_split_tf32_host_side():
+    """Split-TF32 entry points on the host: the prepared buffer holds hi and
+    lo halves (exactly twice the TF32 one), NULL arguments are refused
+    before any launch, and the plan builder routes batch-1 layers with fewer
+    tensor-core units than SMs to the FFMA kernel (same fp32 tolerance)."""
+    from paper_1809_10170_b200 import _abi, nets
+    lib = _abi.lib()
+    for shp in [(64, 64, 58, 58, 3), (256, 1024, 14, 14, 1), (24, 40, 9, 9, 5)]:
+        ci, co, h, w, f = shp
+        d = _abi.ConvDesc()
+        assert lib.dconv_conv_desc_init(ctypes.byref(d), 1, ci, co, h, w, f, f, 1, 8, 8) == 0
+        a, b = ctypes.c_int64(0), ctypes.c_int64(0)
+        assert lib.dconv_cuda_tf32_prepared_size(ctypes.byref(d), ctypes.byref(a)) == 0
+        assert lib.dconv_cuda_tf32x3_prepared_size(ctypes.byref(d), ctypes.byref(b)) == 0
+        assert b.value == 2 * a.value > 0
+        assert lib.dconv_cuda_conv_direct_tf32x3(ctypes.byref(d), 0, 0, 0, 0, 0) == _abi.EPARAM
+    assert lib.dconv_cuda_tf32x3_prepared_size(None, None) == _abi.EPARAM
+    p = nets.Plan("t", 1, [], algo="tf32x3")
+    assert p.x3 and "tf32x3" in nets.TC_ALGOS
+    assert p._few_units(nets.Layer("c", 64, 64, 58, 58, 3, 3, 1), 0)       # cfg1 b1: 28 units
+    assert not p._few_units(nets.Layer("c", 64, 64, 58, 58, 3, 3, 1), _abi.EPI_MAXPOOL)
+    assert not nets.Plan("t", 32, [], algo="tf32x3")._few_units(
+        nets.Layer("c", 64, 64, 58, 58, 3, 3, 1), 0)

@@ -768,14 +768,19 @@ def test_tf32_strided_1x1_on_crop_view(ci, co, hb, s):
         assert err.max() > 0  # really the TF32 path
 
 
-def test_tf32_epilogue_and_padding():
-    x = po.uniform((1, 16, 12, 12), 93, 0)
+@pytest.mark.parametrize("n,h", [(1, 12), (3, 9)])
+def test_tf32_epilogue_and_padding(n, h):
+    """ReLU + skip epilogue and zero padded channels; h = 9 (7x7 output)
+    stacks two images per M-tile (the last unit half empty)."""
+    x = po.uniform((n, 16, h, h), 93, 0)
     k = po.uniform((16, 20, 3, 3), 93, 1)
-    skip = po.pack_feature_map(po.uniform((20, 10, 10), 93, 2), 8)[None]
-    got = run_conv_tf32(x, k, relu=True, skip=skip)[0]
-    want = np.maximum(po.pack_feature_map(po.conv_oracle64(x[0], k, 1), 8) + skip[0], 0)
-    assert (np.abs(got - want) <= tf32_bound(x[0], k)).all()
-    assert not got[..., 4:][-1].any(), "padded output channels must be exact 0"
+    skip = np.stack([po.pack_feature_map(po.uniform((20, h - 2, h - 2), 93, 2 + i), 8)
+                     for i in range(n)])
+    got = run_conv_tf32(x, k, relu=True, skip=skip)
+    for i in range(n):
+        want = np.maximum(po.pack_feature_map(po.conv_oracle64(x[i], k, 1), 8) + skip[i], 0)
+        assert (np.abs(got[i] - want) <= tf32_bound(x[i], k)).all()
+        assert not got[i][-1][..., 4:].any(), "padded output channels must be exact 0"
 
 
 def test_tail_split_launch():
