@@ -83,5 +83,31 @@ void conv_direct(const DeviceFeatureMap& in, const DeviceKernel& kernel,
                  const ConvShape& shape, DeviceFeatureMap& out, int epilogue = 0,
                  const DeviceFeatureMap* skip = nullptr, void* stream = nullptr);
 
+/// Tensor-core variants of conv_direct (c_ib = c_ob = 8, stride 1 or a 1x1
+/// of any stride): kTf32 = one TF32 pass (looser tolerance); kSplitTf32 =
+/// three TF32 passes with chunked fp32 summation, the fp32 tolerance of the
+/// FFMA path.  The weights are rearranged once into the operand layout.
+enum class TensorCoreMode { kTf32 = 0, kSplitTf32 = 1 };
+
+class DevicePreparedKernel {
+ public:
+  DevicePreparedKernel(const DeviceKernel& k, const ConvShape& shape, TensorCoreMode mode,
+                       void* stream = nullptr);
+  ~DevicePreparedKernel();
+  DevicePreparedKernel(const DevicePreparedKernel&) = delete;
+  DevicePreparedKernel& operator=(const DevicePreparedKernel&) = delete;
+  const float* data() const { return ptr_; }
+  ConvShape shape;
+  TensorCoreMode mode;
+
+ private:
+  float* ptr_ = nullptr;
+};
+
+/// conv_direct on the tensor cores into a preallocated output (asynchronous).
+void conv_direct(const DeviceFeatureMap& in, const DevicePreparedKernel& kernel,
+                 DeviceFeatureMap& out, int epilogue = 0,
+                 const DeviceFeatureMap* skip = nullptr, void* stream = nullptr);
+
 }  // namespace cuda
 }  // namespace dconv

@@ -296,5 +296,44 @@ void conv_direct(const DeviceFeatureMap& in, const DeviceKernel& k, const ConvSh
                                out.data(), stream));
 }
 
+DevicePreparedKernel::DevicePreparedKernel(const DeviceKernel& k, const ConvShape& s,
+                                           TensorCoreMode m, void* stream)
+    : shape(s), mode(m) {
+  if (k.c_ib != 8 || k.c_ob != 8)
+    throw std::invalid_argument("conv_direct: layout error (tensor-core path needs c_b = 8)");
+  if (k.c_i != s.c_i || k.c_o != s.c_o || k.h_f != s.h_f || k.w_f != s.w_f)
+    throw std::invalid_argument("conv: kernel dims do not match shape");
+  const dconv_conv_desc d = make_desc(s, 1, 8, 8, DCONV_EPI_NONE);
+  const bool x3 = m == TensorCoreMode::kSplitTf32;
+  int64_t floats = 0;
+  check(x3 ? dconv_cuda_tf32x3_prepared_size(&d, &floats)
+           : dconv_cuda_tf32_prepared_size(&d, &floats));
+  cuda_check(cudaMalloc(&ptr_, std::size_t(floats) * sizeof(float)), "cudaMalloc");
+  check(x3 ? dconv_cuda_prepare_tf32x3_weights(&d, k.data(), ptr_, stream)
+           : dconv_cuda_prepare_tf32_weights(&d, k.data(), ptr_, stream));
+  cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "sync");
+}
+
+DevicePreparedKernel::~DevicePreparedKernel() {
+  if (ptr_) cudaFree(ptr_);
+}
+
+void conv_direct(const DeviceFeatureMap& in, const DevicePreparedKernel& k,
+                 DeviceFeatureMap& out, int epilogue, const DeviceFeatureMap* skip,
+                 void* stream) {
+  const ConvShape& s = k.shape;
+  if (in.c_b != 8 || out.c_b != 8)
+    throw std::invalid_argument("conv_direct: layout error (tensor-core path needs c_b = 8)");
+  if (in.channels != s.c_i || in.height != s.h_i || in.width != s.w_i || in.n != out.n)
+    throw std::invalid_argument("conv: input dims do not match shape");
+  if (out.channels != s.c_o || out.height != s.h_o || out.width != s.w_o)
+    throw std::invalid_argument("conv: output dims do not match shape");
+  const dconv_conv_desc d = make_desc(s, in.n, 8, 8, epilogue);
+  const float* sk = skip ? skip->data() : nullptr;
+  check(k.mode == TensorCoreMode::kSplitTf32
+            ? dconv_cuda_conv_direct_tf32x3(&d, in.data(), k.data(), sk, out.data(), stream)
+            : dconv_cuda_conv_direct_tf32(&d, in.data(), k.data(), sk, out.data(), stream));
+}
+
 }  // namespace cuda
 }  // namespace dconv

@@ -114,6 +114,26 @@ int main() {
       for (int yy = 0; yy < s.h_o; ++yy)
         for (int xx = 0; xx < s.w_o; ++xx) EXPECT(y.at(ch, yy, xx) == 0.0f);
   }
+  // tensor-core variants through the device API: split-TF32 meets the same
+  // fp32 tolerance as conv_direct (K = 4608 here); one TF32 pass does not
+  {
+    ConvShape s(512, 40, 9, 9, 3, 3, 1);
+    FeatureMap x(s.c_i, s.h_i, s.w_i);
+    KernelTensor k(s.c_i, s.c_o, 3, 3);
+    unsigned st = 4608u;
+    for (float& v : x.data) v = frand(st);
+    for (float& v : k.data) v = frand(st);
+    cuda::DeviceFeatureMap dx(1, s.c_i, s.h_i, s.w_i, 8), dy(1, s.c_o, s.h_o, s.w_o, 8);
+    dx.upload(pack_feature_map(x, 8));
+    cuda::DeviceKernel dk(pack_kernel(k, 8, 8));
+    const FeatureMap want = oracle(x, k, s);
+    cuda::DevicePreparedKernel x3(dk, s, cuda::TensorCoreMode::kSplitTf32);
+    cuda::conv_direct(dx, x3, dy);
+    EXPECT(close_all(unpack_feature_map(dy.download()), want));
+    cuda::DevicePreparedKernel t1(dk, s, cuda::TensorCoreMode::kTf32);
+    cuda::conv_direct(dx, t1, dy);
+    EXPECT(!close_all(unpack_feature_map(dy.download()), want));
+  }
   // layout error
   EXPECT(throws_invalid([] {
     BlockedFeatureMap x(4, 3, 3, 2);
