@@ -148,7 +148,7 @@ int dconv_cuda_conv_direct_tf32(const dconv_conv_desc* d, const float* in,
  * (|a-b| <= 1e-4 + 1e-5|b| against conv_oracle64, reference.cpp:70-87):
  * x = x_hi + x_lo, w = w_hi + w_lo, three TF32 MMAs per tap
  * (x_hi*w_lo + x_lo*w_hi + x_hi*w_hi) with the reduction summed in chunks
- * of ~288 products (TMEM chunk accumulators, fp32 register totals).  Same
+ * of ~144 products (TMEM chunk accumulators, fp32 register totals).  Same
  * geometry limits and contract as the TF32 calls; the activation split
  * happens in shared memory (no workspace); the prepared weights hold hi and
  * lo halves (2x the TF32 buffer). */

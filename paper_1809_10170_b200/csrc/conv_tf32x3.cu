@@ -16,11 +16,11 @@
 //   * Accumulation: the tensor core adds into its fp32 accumulator with an
 //     error that grows with the accumulator's magnitude (K = 4608 in one
 //     accumulator fails the fp32 bar: profiles/r1_tf32x3_accuracy.txt).  The
-//     reduction is therefore cut into chunks of ~288 products: the MMAs of a
+//     reduction is therefore cut into chunks of ~144 products: the MMAs of a
 //     chunk go to one of two TMEM accumulator sets while the epilogue warps
 //     add the previous chunk into fp32 register totals (IEEE adds), the same
 //     two-level summation the FFMA kernel does with its TMEM fold
-//     (profiles/r1_tf32x3_chunk.txt: chunk K vs accuracy).
+//     (profiles/r1_tf32x3_kernel_accuracy.txt: chunk K vs accuracy).
 //
 // Roles (12 warps): warp 0 TMA producer, warp 1 MMA issuer (elect.sync),
 // warps 2-3 operand split, warps 4-11 epilogue (chunk drain into registers,
@@ -554,8 +554,10 @@ int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream
   p.n_r = (p.h_f + p.R - 1) / p.R;
   if (p.PH > 256 || p.PW > 256 || p.G > 256)
     return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_tf32x3: TMA box too large");
-  // accumulator chunk: ~288 products (DCONV_X3_CHUNK_K), whole stages
-  static const int chunk_k = getenv("DCONV_X3_CHUNK_K") ? atoi(getenv("DCONV_X3_CHUNK_K")) : 288;
+  // accumulator chunk: ~144 products (DCONV_X3_CHUNK_K), whole stages
+  // (profiles/r1_tf32x3_kernel_accuracy.txt: worst element at 0.52 of the
+  // fp32 tolerance at K = 4608; 288 reaches 0.90, 576 fails)
+  static const int chunk_k = getenv("DCONV_X3_CHUNK_K") ? atoi(getenv("DCONV_X3_CHUNK_K")) : 144;
   const int k_stage = p.G * p.R * p.w_f * 8;
   p.chunk_st = std::max(1, chunk_k / k_stage);
   p.row_groups = p.stack > 1 ? 1 : (p.h_o + p.MT * kTileRows - 1) / (p.MT * kTileRows);
