@@ -647,6 +647,10 @@ def test_tf32x3_meets_fp32_tolerance(ci, co, h, w, f, n):
     for i in range(n):
         want = po.pack_feature_map(po.conv_oracle64(x[i], k, 1), 8)
         assert_tol(got[i], want, f"tf32x3 img {i}")
+        # and with a margin: the chunked sum keeps the worst element at
+        # <= 0.52 of the bound (profiles/r1_tf32x3_kernel_accuracy.txt)
+        ok, nbad, err = po.within_tol(got[i], want, 0.75 * ATOL, 0.75 * RTOL)
+        assert ok, f"tf32x3 img {i}: {nbad} elements beyond 0.75 of the tolerance ({err:.3g})"
     if one is not None:  # the single-pass TF32 kernel does not meet it: x3 is doing work
         want = po.pack_feature_map(po.conv_oracle64(x[0], k, 1), 8)
         assert not po.within_tol(one[0], want, ATOL, RTOL)[0]
