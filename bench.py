@@ -347,7 +347,10 @@ def main_gpu(args):
             ffma_ms += ms
         else:
             other_ms += ms
-    if args.algo in ("tf32", "tf32x3"):
+    # the roofline follows the kernel that ran: a split-TF32 plan whose layers
+    # all fell back to the FFMA kernel (batch 1, few units) reports FFMA's
+    roof_algo = args.algo if any(s.kind == "tf32" for s in plan.steps) else "ffma"
+    if roof_algo in ("tf32", "tf32x3"):
         # tensor-core roofline: the tcgen05 launches against a cuBLAS TF32 GEMM
         # (8192^3, torch.matmul with TF32 allowed) measured live on this GPU
         ffma_flops = sum(s.flops for s in plan.steps if s.kind == "tf32")
@@ -355,7 +358,7 @@ def main_gpu(args):
         other_ms = sum(statistics.median(per[s.name]) for s in plan.steps if s.kind != "tf32")
         peak = tf32_gemm_peak(stream)
         pattern = None
-        if args.algo == "tf32x3":
+        if roof_algo == "tf32x3":
             # split-TF32 issues three TF32 MMAs per product: the tensor pipe
             # does 3x the algorithmic FLOPs (reported as such against the
             # TF32 peak; fp32-equivalent rate = achieved / 3)
@@ -374,7 +377,7 @@ def main_gpu(args):
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tfile):
         try:
-            key = args.config if args.algo == "ffma" else f"{args.config}_{args.algo}"
+            key = args.config if roof_algo == "ffma" else f"{args.config}_{roof_algo}"
             t = json.load(open(tfile)).get(key)
             if t:
                 traffic = t["dram_bytes"]
@@ -421,19 +424,19 @@ def main_gpu(args):
                    "graph": graph is not None, "gflop_per_step": round(flops_job / 1e9, 3),
                    "tiles": {k: ["", "128x128", "256x64"][v]
                              for k, v in tiles.items()}},
-        "roofline": {"bound": "fp32" if args.algo == "ffma" else "tensor",
+        "roofline": {"bound": "fp32" if roof_algo == "ffma" else "tensor",
                      "achieved": round(achieved, 2), "peak": round(peak, 2),
                      "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if peak > 0 else None,
                      "traffic": traffic, "traffic_note": traffic_note,
                      "kernel": ("conv_ffma_kernel (all blocked conv launches of the step)"
-                                if args.algo == "ffma" else
+                                if roof_algo == "ffma" else
                                 "conv_tf32_kernel (all stride-1 blocked conv launches)"
-                                if args.algo == "tf32" else
+                                if roof_algo == "tf32" else
                                 "conv_tf32x3_kernel (all tensor-core launches; achieved counts "
                                 "the 3 TF32 MMAs per product, fp32-equivalent = achieved / 3)"),
                      "peak_source": ("FFMA2 throughput probe measured live on this GPU "
                                      f"(nominal {NOMINAL_FP32_TFLOPS:.1f} at 1965 MHz)"
-                                     if args.algo == "ffma" else
+                                     if roof_algo == "ffma" else
                                      "cuBLAS TF32 GEMM 8192^3 measured live (nominal 1100 dense)"),
                      "share_of_step": round(ffma_ms / (ffma_ms + other_ms), 4)
                      if ffma_ms + other_ms else None,
