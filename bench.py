@@ -422,7 +422,7 @@ def main_gpu(args):
                    if args.config in ("vgg16", "resnet50", "googlenet") else
                    "working set fits L2 (batch-1 config): warm-L2 numbers",
                    "graph": graph is not None, "gflop_per_step": round(flops_job / 1e9, 3),
-                   "tiles": {k: ["", "128x128", "256x64"][v]
+                   "tiles": {k: ["", "128x128", "256x64", "128x64"][v]
                              for k, v in tiles.items()}},
         "roofline": {"bound": "fp32" if roof_algo == "ffma" else "tensor",
                      "achieved": round(achieved, 2), "peak": round(peak, 2),

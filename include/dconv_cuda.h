@@ -103,7 +103,8 @@ typedef struct dconv_conv_desc {
   int co_block_begin;      /* first output block j' computed (C_o sharding) */
   int co_block_count;      /* number of output blocks computed; 0 = all */
   int tile_variant;        /* FFMA CTA tile: 0 = selector, 1 = 128 px x 128 ch,
-                              2 = 256 px x 64 ch; see Plan.autotune in nets.py */
+                              2 = 256 px x 64 ch, 3 = 128 px x 64 ch;
+                              see Plan.autotune in nets.py */
 } dconv_conv_desc;
 
 /* Fills `d` for a dense layer and validates it like ConvShape's constructor.
@@ -232,8 +233,8 @@ int dconv_cuda_zero(float* x, int64_t count, void* stream);
 
 /* Tile selector override for the FFMA kernel (the GPU analogue of the
  * reference's BlockingParams choice, model.hpp:85-109): -1 = heuristic,
- * 0 = CTA tile 128 pixels x 128 channels, 1 = 256 pixels x 64 channels.
- * Process-wide; a descriptor's tile_variant (if non-zero) takes precedence. */
+ * 0 = CTA tile 128 pixels x 128 channels, 1 = 256 pixels x 64 channels,
+ * 2 = 128 pixels x 64 channels (batch-1 layers).  Process-wide; a descriptor's tile_variant (if non-zero) takes precedence. */
 int dconv_cuda_set_ffma_variant(int variant);
 
 /* Launch accounting: number of device kernels this library launched since

@@ -477,7 +477,7 @@ int dconv_cuda_zero(float* x, int64_t count, void* stream) {
 }
 
 int dconv_cuda_set_ffma_variant(int variant) {
-  if (variant < -1 || variant > 1) return set_error(DCONV_EPARAM, "variant %d", variant);
+  if (variant < -1 || variant > 2) return set_error(DCONV_EPARAM, "variant %d", variant);
   dconv_dev::ffma_variant_override = variant;
   return DCONV_OK;
 }

@@ -1138,8 +1138,8 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr_set = true;
   }
-  // only the 8-warp 8x8-per-thread tile has the DSMEM split-K reduction
-  const bool no_split = knobs().no_splitk || NW != 8 || TPX != 8 ||
+  // the DSMEM split-K reduction: 8 warps, 8 channels x 4 or 8 pixels/thread
+  const bool no_split = knobs().no_splitk || NW != 8 || (TPX != 8 && TPX != 4) ||
                         TCO != 8 || (p.epi & DCONV_EPI_MAXPOOL);
   int slots[kMaxKs + 1] = {0};
   slots[1] = sms;
@@ -1263,6 +1263,11 @@ int launch_conv_ffma(const FfmaParams& p0, cudaStream_t stream) {
     // 256/512 ch.  tools/ffma2_pattern.cu: this operand pattern tops out at
     // ~59 TFLOP/s with any warp count (83% of the FFMA2 probe).
     case 0: return launch_wf<128, 128>(p, stream);  // 128 px x 128 channels
+    case 2:  // 128 px x 64 channels, 4 px x 8 ch per thread: twice the units
+             // of the 256 x 64 tile for batch-1 layers (less split-K)
+      if (p.epi & DCONV_EPI_MAXPOOL)
+        return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_ffma: 128x64 tile has no fused pool");
+      return launch_wf<128, 64, 8, 4, 8>(p, stream);
     default: return launch_wf<256, 64>(p, stream);  // 256 px x 64 channels
   }
 }

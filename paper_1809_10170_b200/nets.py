@@ -343,7 +343,7 @@ class Plan:
         for st in self.steps:
             st.fn(stream)
 
-    def autotune(self, stream=None, variants=(1, 2), reps: int = 3) -> Dict[str, int]:
+    def autotune(self, stream=None, variants=(1, 2, 3), reps: int = 3) -> Dict[str, int]:
         """Times every FFMA conv step with each CTA tile (desc.tile_variant)
         on the plan's own buffers and keeps the fastest -- the GPU analogue of
         the reference's autotune (model.hpp:103-109), run

@@ -329,9 +329,9 @@ def test_first_layer_reader_variants(s, f, ci, co):
         assert_tol(got[i], want, f"first s={s} f={f} img {i}")
 
 
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1, 2])
 def test_ffma_tile_variants(variant):
-    """Both FFMA CTA tiles (128 px x 128 ch, 256 px x 64 ch) on ragged shapes,
+    """The FFMA CTA tiles (128 px x 128 ch, 256 px x 64 ch, 128 px x 64 ch) on ragged shapes,
     strides, filter widths 1/3/5/7 (templated and runtime), and a K = 4608
     layer where the TMEM two-level sum matters."""
     lib = _abi.lib()
@@ -349,7 +349,7 @@ def test_ffma_tile_variants(variant):
         lib.dconv_cuda_set_ffma_variant(-1)
 
 
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1, 2])
 def test_batched_stacked_tiles(variant):
     """Pixel tiles over the batch-stacked output span several images (maps of
     height 1..9 with tiles of up to 64 rows): every image checked."""
@@ -549,13 +549,13 @@ def test_co_shard_peer_gather_plan_world1():
 def test_cluster_split_k(ks, monkeypatch):
     """Split-K over a thread-block cluster with the DSMEM reduction, forced
     to ks CTAs per unit: several units per cluster (barrier phases), ragged
-    stage splits, both CTA tiles; bitwise repeatable."""
+    stage splits, every CTA tile; bitwise repeatable."""
     monkeypatch.setenv("DCONV_KSPLIT", str(ks))
     lib = _abi.lib()
     try:
         cases = [(64, 64, 58, 58, 3, 1, 1), (40, 136, 17, 23, 3, 1, 3), (96, 72, 13, 31, 1, 2, 2),
                  (200, 24, 9, 9, 3, 2, 4), (24, 40, 17, 23, 5, 1, 2), (512, 128, 9, 9, 3, 1, 2)]
-        for variant in (0, 1):
+        for variant in (0, 1, 2):
             _abi.check(lib.dconv_cuda_set_ffma_variant(variant))
             for t, (ci, co, hi, wi, f, s, n) in enumerate(cases):
                 x = po.uniform((n, ci, hi, wi), 8000 + t, ks)
