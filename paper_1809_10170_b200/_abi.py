@@ -19,7 +19,7 @@ OK, EINVAL_SHAPE, ELAYOUT, EPARAM, ECUDA, ENCCL, EUNSUPPORTED, EFORMAT, EBLOCKED
 FILE_FEATURE_MAP, FILE_KERNEL = 0, 1
 EPI_NONE, EPI_RELU, EPI_ADD, EPI_ADD_RELU = range(4)
 EPI_MAXPOOL = 4  # flag: fused 2x2/s2 max-pool (TF32 path)
-ALGO_AUTO, ALGO_FFMA, ALGO_GENERIC, ALGO_TF32 = range(4)
+ALGO_AUTO, ALGO_FFMA, ALGO_GENERIC, ALGO_TF32, ALGO_TF32X3 = range(5)
 
 
 class ConvDesc(ctypes.Structure):

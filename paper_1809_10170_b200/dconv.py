@@ -244,6 +244,59 @@ def conv_direct(inp: BlockedFeatureMap, kernel: BlockedKernel, shape: ConvShape,
     return out
 
 
+class PreparedKernel:
+    """A blocked kernel rearranged once into the tensor-core operand layout
+    (the C++ ``dconv::cuda::DevicePreparedKernel``): ``split=True`` holds the
+    hi/lo halves of the split-TF32 kernel (the fp32 tolerance of
+    ``conv_direct``), ``split=False`` the single-pass TF32 layout."""
+
+    def __init__(self, kernel: BlockedKernel, shape: ConvShape, split: bool = True,
+                 stream=None):
+        import ctypes
+        if kernel.c_ob != 8 or kernel.c_ib != 8:
+            raise ValueError("conv_direct: layout error (tensor-core path needs c_b = 8)")
+        if (kernel.c_i, kernel.c_o, kernel.h_f, kernel.w_f) != (
+                shape.c_i, shape.c_o, shape.h_f, shape.w_f):
+            raise ValueError("conv: kernel dims do not match shape")
+        self.shape, self.split = shape, split
+        d = make_desc(shape, 1, 8, 8)
+        sz = ctypes.c_int64(0)
+        L = lib()
+        size_fn = L.dconv_cuda_tf32x3_prepared_size if split else L.dconv_cuda_tf32_prepared_size
+        prep_fn = L.dconv_cuda_prepare_tf32x3_weights if split else L.dconv_cuda_prepare_tf32_weights
+        check(size_fn(ctypes.byref(d), ctypes.byref(sz)))
+        self.data = torch.empty(sz.value, dtype=torch.float32, device=kernel.data.device)
+        check(prep_fn(ctypes.byref(d), ptr(kernel.data), ptr(self.data), stream_ptr(stream)))
+
+
+def conv_direct_tc(inp: BlockedFeatureMap, kernel: PreparedKernel, *, relu: bool = False,
+                   skip: Optional[BlockedFeatureMap] = None,
+                   out: Optional[BlockedFeatureMap] = None, stream=None) -> BlockedFeatureMap:
+    """conv_direct on the tcgen05 tensor cores (c_b = 8; stride 1, or a 1x1 of
+    any stride): the split-TF32 kernel for a ``PreparedKernel(split=True)``
+    (fp32 tolerance), else one TF32 pass (looser tolerance)."""
+    import ctypes
+    shape = kernel.shape
+    if inp.c_b != 8:
+        raise ValueError("conv_direct: layout error (tensor-core path needs c_b = 8)")
+    if (inp.channels, inp.height, inp.width) != (shape.c_i, shape.h_i, shape.w_i):
+        raise ValueError("conv: input dims do not match shape")
+    epi = (_abi.EPI_RELU if relu else 0) | (_abi.EPI_ADD if skip is not None else 0)
+    d = make_desc(shape, inp.n, 8, 8, epi,
+                  _abi.ALGO_TF32X3 if kernel.split else _abi.ALGO_TF32)
+    if out is None:
+        out = BlockedFeatureMap(shape.c_o, shape.h_o, shape.w_o, 8, n=inp.n,
+                                device=inp.data.device,
+                                data=torch.empty((inp.n, round_up(shape.c_o, 8) // 8,
+                                                  shape.h_o, shape.w_o, 8),
+                                                 dtype=torch.float32, device=inp.data.device))
+    L = lib()
+    fn = L.dconv_cuda_conv_direct_tf32x3 if kernel.split else L.dconv_cuda_conv_direct_tf32
+    check(fn(ctypes.byref(d), ptr(inp.data), ptr(kernel.data),
+             ptr(skip.data if skip is not None else None), ptr(out.data), stream_ptr(stream)))
+    return out
+
+
 def relu_blocked(x: BlockedFeatureMap, stream=None) -> BlockedFeatureMap:
     """relu_blocked, in place; padding stays 0."""
     check(lib().dconv_cuda_relu_blocked(ptr(x.data), x.data.numel(), stream_ptr(stream)))

@@ -1018,3 +1018,27 @@ def test_tf32x3_full_size_plans_sampled_parity(config, n):
         nets.conv_tf32 = orig_conv
     assert len(rec) == sum(1 for st in plan.steps if st.kind == "tf32") > 0
     _check_sampled(config, rec, imgs, check)
+
+
+def test_python_dropin_tensor_core_conv():
+    """dconv.PreparedKernel + conv_direct_tc (the Python mirror of the C++
+    DevicePreparedKernel overload): split-TF32 meets conv_direct's fp32
+    tolerance with ReLU + skip; the single-pass TF32 kernel meets its own."""
+    ci, co, h = 256, 72, 11
+    x = po.uniform((2, ci, h, h), 9601, 0)
+    k = po.uniform((ci, co, 3, 3), 9602, 0)
+    skip = np.stack([po.pack_feature_map(po.uniform((co, h - 2, h - 2), 9603, i), 8)
+                     for i in range(2)])
+    shape = D.ConvShape(ci, co, h, h, 3, 3, 1)
+    xb = D.BlockedFeatureMap(ci, h, h, 8, n=2,
+                             data=dev(np.stack([po.pack_feature_map(x[i], 8) for i in range(2)])))
+    kb = D.BlockedKernel(ci, co, 3, 3, 8, 8, data=dev(po.pack_kernel(k, 8, 8)))
+    sk = D.BlockedFeatureMap(co, h - 2, h - 2, 8, n=2, data=dev(skip))
+    y3 = host(D.conv_direct_tc(xb, D.PreparedKernel(kb, shape, split=True), relu=True, skip=sk).data)
+    y1 = host(D.conv_direct_tc(xb, D.PreparedKernel(kb, shape, split=False)).data)
+    for i in range(2):
+        ref = po.pack_feature_map(po.conv_oracle64(x[i], k, 1), 8)
+        assert_tol(y3[i], np.maximum(ref + skip[i], 0), f"split-TF32 img {i}")
+        assert (np.abs(y1[i] - ref) <= tf32_bound(x[i], k)).all()
+    with pytest.raises(ValueError, match="layout error"):
+        D.PreparedKernel(D.BlockedKernel(ci, co, 3, 3, 8, 4), shape)
