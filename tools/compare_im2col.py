@@ -10,7 +10,9 @@ comparison runs on the GPU, outside the product path, with library code:
   * cuDNN fp32 convolution (TF32 disabled, cudnn.benchmark picks the
     algorithm; its workspace is measured as the allocator high-water mark
     above inputs + weights + output);
-  * this repository's direct kernels on the blocked layout (zero workspace).
+  * this repository's direct kernels on the blocked layout (zero workspace):
+    the fp32 FFMA kernel and, for stride-1 / 1x1 blocked layers, the
+    split-TF32 tensor-core kernel (same fp32 tolerance).
 
 Every layer is checked: the direct kernel's output must match im2col + SGEMM
 within twice the fp32 tolerance; cuDNN's deviation is reported beside it.
@@ -123,6 +125,15 @@ def main():
         cudnn_err = (cud - ref).abs().max().item()
         cudnn_tol = ((cud - ref).abs() - 2e-5 * ref.abs()).max().item() <= 2e-4
 
+        x3 = None
+        if not l.first and (l.s == 1 or l.h_f == 1):
+            wp = nets.prepare_tf32(l, w_blk, x3=True)
+            y3 = nets.Act(n, l.c_o, l.h_o, l.w_o)
+            run_x3 = lambda: nets.conv_tf32(l, n, xa, wp, y3, x3=True)  # noqa: E731
+            run_x3()
+            got3 = blocked_to_nchw(y3.buf, l.c_o)
+            err3 = ((got3 - ref).abs() - 2e-5 * ref.abs()).max().item()
+            x3 = (timed(run_x3, args.reps), err3 <= 2e-4)
         t_direct = timed(direct, args.reps)
         t_im2col = timed(im2col_gemm, args.reps)
         t_gemm = timed(gemm_only, args.reps)
@@ -143,6 +154,9 @@ def main():
             "cudnn_ms": round(t_cudnn, 4), "cudnn_tflops": round(gf / t_cudnn, 2),
             "cudnn_workspace_bytes": int(cudnn_ws),
             "cudnn_max_abs_dev": cudnn_err, "cudnn_within_tol": cudnn_tol,
+            "tf32x3_ms": round(x3[0], 4) if x3 else None,
+            "tf32x3_tflops": round(gf / x3[0], 2) if x3 else None,
+            "tf32x3_parity_ok": x3[1] if x3 else None,
         }
         rows.append(row)
         print(json.dumps(row), flush=True)
@@ -154,6 +168,15 @@ def main():
                "cudnn_fp32_tflops": round(tot["gflop"] / tot["cudnn_ms"], 2),
                "max_im2col_bytes": max(r["im2col_bytes"] for r in rows),
                "max_cudnn_workspace_bytes": max(r["cudnn_workspace_bytes"] for r in rows)}
+    sub = [r for r in rows if r["tf32x3_ms"] is not None]
+    if sub:
+        g = sum(r["gflop"] for r in sub)
+        summary["tf32x3_subset"] = {
+            "layers": len(sub), "all_parity_ok": all(r["tf32x3_parity_ok"] for r in sub),
+            "tf32x3_tflops": round(g / sum(r["tf32x3_ms"] for r in sub), 2),
+            "direct_ffma_tflops": round(g / sum(r["direct_ms"] for r in sub), 2),
+            "cudnn_fp32_tflops": round(g / sum(r["cudnn_ms"] for r in sub), 2),
+            "cudnn_within_tol_layers": sum(1 for r in sub if r["cudnn_within_tol"])}
     print(json.dumps({"summary": summary}), flush=True)
     if args.json:
         with open(args.json, "w") as f:
