@@ -71,7 +71,13 @@ __device__ __forceinline__ float4 hi4(float4 v) {
 
 // COLS = MT * N / 2: accumulator columns each epilogue thread totals in
 // registers (two epilogue warps per TMEM lane quarter, each half of N).
-template <int WF_T, int MT_T, int COLS>
+// DA ("dual accumulator", used for N = 64): per tap and M-tile one N' = 2N MMA
+// A_hi x [B_hi | B_lo] writes the head product and the first correction into
+// adjacent column blocks [main | corr], and A_lo x B_hi accumulates into corr:
+// two MMAs instead of three, A_hi read once, and the small terms are summed
+// apart from the head (no bits lost in its accumulator).  Weights per k-half
+// are [hi N rows | lo N rows]; TMEM per M-tile 2N columns.
+template <int WF_T, int MT_T, int COLS, bool DA>
 __global__ void __launch_bounds__(kThreadsX, 1)
     conv_tf32x3_kernel(const __grid_constant__ CUtensorMap tmap, const Tf32Params p) {
   extern __shared__ __align__(1024) float smem[];
@@ -208,7 +214,8 @@ __global__ void __launch_bounds__(kThreadsX, 1)
         // adds (see conv_tf32.cu); lo planes / lo weights at fixed offsets
         const uint32_t a_lo0 = ((a_base >> 4) & 0x3FFFu) | (((uint32_t)(p.plane_floats * 4) >> 4) << 16);
         const uint32_t a_hi = ((uint32_t)(p.PW * 16) >> 4) | (1u << 14);
-        const uint32_t b_lo0 = ((b_base >> 4) & 0x3FFFu) | (((uint32_t)(p.N * 16) >> 4) << 16);
+        const uint32_t b_lo0 =
+            ((b_base >> 4) & 0x3FFFu) | (((uint32_t)((DA ? 2 : 1) * p.N * 16) >> 4) << 16);
         const uint32_t b_hi = (128u >> 4) | (1u << 14);
         const uint32_t a_mt = (uint32_t)(kTileRows * p.PW);  // next M-tile (16 B units)
         const uint32_t b_tap = (uint32_t)(4 * p.N);          // next (n, m) tap: hi + lo
@@ -225,25 +232,37 @@ __global__ void __launch_bounds__(kThreadsX, 1)
 #pragma unroll
               for (int mt = 0; mt < kMtLoop; ++mt) {
                 if (mt >= mts) break;
-                const uint32_t d = acc_base + (uint32_t)(mt * p.N);
                 const uint32_t a = arow + (uint32_t)m + (uint32_t)mt * a_mt;
                 const uint32_t b = brow + (uint32_t)m * b_tap;
-                // small terms first, the head product last
-                umma_tf32_elect(d, a, a_hi, b + b_rem, b_hi, p.idesc, accum);
-                umma_tf32_elect(d, a + a_rem, a_hi, b, b_hi, p.idesc, 1u);
-                umma_tf32_elect(d, a, a_hi, b, b_hi, p.idesc, 1u);
+                if constexpr (DA) {
+                  const uint32_t d = acc_base + (uint32_t)(mt * 2 * p.N);
+                  umma_tf32_elect(d, a, a_hi, b, b_hi, p.idesc2, accum);  // [main | corr]
+                  umma_tf32_elect(d + (uint32_t)p.N, a + a_rem, a_hi, b, b_hi, p.idesc, 1u);
+                } else {
+                  const uint32_t d = acc_base + (uint32_t)(mt * p.N);
+                  // small terms first, the head product last
+                  umma_tf32_elect(d, a, a_hi, b + b_rem, b_hi, p.idesc, accum);
+                  umma_tf32_elect(d, a + a_rem, a_hi, b, b_hi, p.idesc, 1u);
+                  umma_tf32_elect(d, a, a_hi, b, b_hi, p.idesc, 1u);
+                }
               }
               accum = 1u;
             }
             if (WF_T > 0) continue;
             for (int m = 1; m < wf; ++m) {
               for (int mt = 0; mt < mts; ++mt) {
-                const uint32_t d = acc_base + (uint32_t)(mt * p.N);
                 const uint32_t a = arow + (uint32_t)m + (uint32_t)mt * a_mt;
                 const uint32_t b = brow + (uint32_t)m * b_tap;
-                umma_tf32_elect(d, a, a_hi, b + b_rem, b_hi, p.idesc, 1u);
-                umma_tf32_elect(d, a + a_rem, a_hi, b, b_hi, p.idesc, 1u);
-                umma_tf32_elect(d, a, a_hi, b, b_hi, p.idesc, 1u);
+                if constexpr (DA) {
+                  const uint32_t d = acc_base + (uint32_t)(mt * 2 * p.N);
+                  umma_tf32_elect(d, a, a_hi, b, b_hi, p.idesc2, 1u);
+                  umma_tf32_elect(d + (uint32_t)p.N, a + a_rem, a_hi, b, b_hi, p.idesc, 1u);
+                } else {
+                  const uint32_t d = acc_base + (uint32_t)(mt * p.N);
+                  umma_tf32_elect(d, a, a_hi, b + b_rem, b_hi, p.idesc, 1u);
+                  umma_tf32_elect(d, a + a_rem, a_hi, b, b_hi, p.idesc, 1u);
+                  umma_tf32_elect(d, a, a_hi, b, b_hi, p.idesc, 1u);
+                }
               }
             }
           }
@@ -324,7 +343,14 @@ __global__ void __launch_bounds__(kThreadsX, 1)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               float v[16];
-              tmem_ld16(lane_base + (uint32_t)set * kSetCols + (uint32_t)(mt * p.N + c0 + h * 16), v);
+              const uint32_t col = (uint32_t)((DA ? 2 : 1) * mt * p.N + c0 + h * 16);
+              tmem_ld16(lane_base + (uint32_t)set * kSetCols + col, v);
+              if constexpr (DA) {  // + the chunk's correction terms
+                float w[16];
+                tmem_ld16(lane_base + (uint32_t)set * kSetCols + col + (uint32_t)p.N, w);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] += w[i];
+              }
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
                 float& t = tot[j * 32 + h * 16 + i];
@@ -367,20 +393,27 @@ __global__ void __launch_bounds__(kThreadsX, 1)
   }
 }
 
-// Prepared weights: [cg][i'][n][m][hi/lo][k-half][N][4] from the blocked
+// Prepared weights: [cg][i'][n][m][hi/lo][k-half][N][4], or
+// [cg][i'][n][m][k-half][hi/lo][N][4] for DA (N = 64), from the blocked
 // kernel [jb][i'][n][m][ii][jj] (tensor.hpp:131-137): w_hi = w with the low
 // 13 mantissa bits cleared, w_lo = w - w_hi (exact).  Channel slots beyond
 // jb_count blocks are zero.
 __global__ void prepare_tf32x3_weights_kernel(const float* __restrict__ w, int ib_n, int h_f,
                                               int w_f, int jb_begin, int jb_count, int N,
-                                              int64_t total, float* __restrict__ out) {
+                                              int da, int64_t total, float* __restrict__ out) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     int64_t t = e;
     const int k4 = (int)(t % 4); t /= 4;
     const int co = (int)(t % N); t /= N;
-    const int kh = (int)(t % 2); t /= 2;
-    const int hl = (int)(t % 2); t /= 2;
+    int kh, hl;
+    if (da) {  // [k-half][hi/lo][N][4]: per k-half 2N rows, hi then lo
+      hl = (int)(t % 2); t /= 2;
+      kh = (int)(t % 2); t /= 2;
+    } else {   // [hi/lo][k-half][N][4]
+      kh = (int)(t % 2); t /= 2;
+      hl = (int)(t % 2); t /= 2;
+    }
     const int m = (int)(t % w_f); t /= w_f;
     const int n = (int)(t % h_f); t /= h_f;
     const int ib = (int)(t % ib_n); t /= ib_n;
@@ -398,29 +431,47 @@ __global__ void prepare_tf32x3_weights_kernel(const float* __restrict__ w, int i
 
 using X3Kernel = void (*)(const CUtensorMap, const Tf32Params);
 
-// (WF, MT, COLS) instantiations: WF in {3, 1, generic}, MT * N in {128, 256}
+// (WF, MT, COLS) instantiations: WF in {3, 1, generic}, MT * N in {128, 256};
+// DA (N <= 128): MT * N = 128
 template <int WF>
-X3Kernel pick_wf(int MT, int cols) {
-  if (MT == 1) return cols == 64 ? conv_tf32x3_kernel<WF, 1, 64> : conv_tf32x3_kernel<WF, 1, 128>;
-  if (MT == 2) return cols == 64 ? conv_tf32x3_kernel<WF, 2, 64> : conv_tf32x3_kernel<WF, 2, 128>;
-  return conv_tf32x3_kernel<WF, 4, 128>;
+X3Kernel pick_wf(int MT, int cols, bool da) {
+  if (da) return MT == 1 ? conv_tf32x3_kernel<WF, 1, 64, true> : conv_tf32x3_kernel<WF, 2, 64, true>;
+  if (MT == 1)
+    return cols == 64 ? conv_tf32x3_kernel<WF, 1, 64, false> : conv_tf32x3_kernel<WF, 1, 128, false>;
+  if (MT == 2)
+    return cols == 64 ? conv_tf32x3_kernel<WF, 2, 64, false> : conv_tf32x3_kernel<WF, 2, 128, false>;
+  return conv_tf32x3_kernel<WF, 4, 128, false>;
 }
 X3Kernel pick_x3_kernel(const Tf32Params& p) {
   const int cols = p.MT * p.N / 2;
-  if (p.w_f == 3) return pick_wf<3>(p.MT, cols);
-  if (p.w_f == 1) return pick_wf<1>(p.MT, cols);
-  return pick_wf<0>(p.MT, cols);
+  if (p.w_f == 3) return pick_wf<3>(p.MT, cols, p.da);
+  if (p.w_f == 1) return pick_wf<1>(p.MT, cols, p.da);
+  return pick_wf<0>(p.MT, cols, p.da);
 }
 
 void set_x3_attrs() {
   static bool done = false;
   if (done) return;
-  for (X3Kernel k : {pick_wf<3>(1, 64), pick_wf<3>(1, 128), pick_wf<3>(2, 64), pick_wf<3>(2, 128),
-                     pick_wf<3>(4, 128), pick_wf<1>(1, 64), pick_wf<1>(1, 128), pick_wf<1>(2, 64),
-                     pick_wf<1>(2, 128), pick_wf<1>(4, 128), pick_wf<0>(1, 64), pick_wf<0>(1, 128),
-                     pick_wf<0>(2, 64), pick_wf<0>(2, 128), pick_wf<0>(4, 128)})
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  for (bool da : {false, true})
+    for (int mt : {1, 2, 4})
+      for (int cols : {64, 128}) {
+        if (da && (cols != 64 || mt == 4)) continue;
+        if (!da && mt == 4 && cols == 64) continue;
+        for (X3Kernel k : {pick_wf<3>(mt, cols, da), pick_wf<1>(mt, cols, da),
+                           pick_wf<0>(mt, cols, da)})
+          cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      }
   done = true;
+}
+
+// separate correction accumulator for N = 64 (DCONV_X3_NO_DA: off); the
+// prepared weight layout follows it.  Measured: N = 64 layers +9..18% (two
+// MMAs per tap instead of three, an N = 64 MMA costing as much as N = 128);
+// N = 128 loses (MT halves to 1: twice the weight traffic per pixel; 512->128
+// 1x1 -30%), so it keeps three MMAs into one accumulator.
+bool use_da(int N) {
+  static const bool off = getenv("DCONV_X3_NO_DA") != nullptr;
+  return !off && N == 64;
 }
 
 }  // namespace
@@ -436,8 +487,8 @@ int launch_prepare_tf32x3(const float* w, int ib_n, int h_f, int w_f, int jb_beg
   const int N = tf32_channels(jb_count);
   const int64_t total = tf32x3_prepared_floats(ib_n, h_f, w_f, jb_count);
   const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 32);
-  prepare_tf32x3_weights_kernel<<<(unsigned)blocks, 256, 0, stream>>>(w, ib_n, h_f, w_f, jb_begin,
-                                                                      jb_count, N, total, out);
+  prepare_tf32x3_weights_kernel<<<(unsigned)blocks, 256, 0, stream>>>(
+      w, ib_n, h_f, w_f, jb_begin, jb_count, N, use_da(N) ? 1 : 0, total, out);
   dconv_host::count_launch();
   return dconv_host::check_launch("prepare_tf32x3_weights_kernel");
 }
@@ -478,18 +529,22 @@ int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream
   // units over the SMs.
   {
     double best = -1;
+    const bool da = use_da(p.N);
     for (int mt = kMaxMT; mt >= 1; --mt) {
       const int cols = mt * p.N / 2;
-      if (cols != 64 && cols != 128) continue;
+      if (da ? cols != 64 : (cols != 64 && cols != 128)) continue;
       const int st = stack_for(mt, rows_for(p.h_f));
       const int rg = st > 1 ? 1 : (p.h_o + mt * kTileRows - 1) / (mt * kTileRows);
       const int64_t units =
           (int64_t)((p.n + st - 1) / st) * rg * ((p.w_o + kTW - 1) / kTW) * p.n_cg;
       const double taps = (double)p.h_f * p.w_f;
       const double mma_cyc = p.N > 128 ? 128.0 : 71.0;
-      const double mma = taps * mt * 3 * mma_cyc;
+      // DA: one N' = 2N MMA + one N MMA per tap and M-tile
+      const double mma = da ? taps * mt * ((p.N > 64 ? 128.0 : 71.0) + 71.0)
+                            : taps * mt * 3 * mma_cyc;
       const double patch = (double)(mt * kTileRows - 1 + p.h_f) * (kTW - 1 + p.w_f) * 32.0;
-      const double smem_bytes = taps * mt * 3 * (4096.0 + p.N * 32.0) + taps * wtap + patch * 3;
+      const double operands = da ? 2 * 4096.0 + 3 * p.N * 32.0 : 3 * (4096.0 + p.N * 32.0);
+      const double smem_bytes = taps * mt * operands + taps * wtap + patch * 3;
       const double l2_bytes = taps * wtap + patch;
       const double unit =
           p.ib_n * std::max({mma, smem_bytes / 120.0, l2_bytes / 40.0}) + 1500.0;
@@ -504,7 +559,7 @@ int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream
     static const char* force_mt = getenv("DCONV_TF32_MT");
     if (force_mt) {
       const int mt = atoi(force_mt);
-      if (mt >= 1 && mt <= kMaxMT && (mt * p.N == 128 || mt * p.N == 256)) p.MT = mt;
+      if (mt >= 1 && mt <= kMaxMT && (mt * p.N == 128 || (!da && mt * p.N == 256))) p.MT = mt;
     }
   }
   // stage = G input blocks x R filter rows: <= 72 KB of hi/lo weights,
@@ -542,7 +597,7 @@ int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream
     if (p.NS >= 2) break;
     if (p.R > 1) {
       r_cap = p.R - 1;
-    } else if (p.MT > 1 && (p.MT / 2) * p.N >= 128) {
+    } else if (p.MT > 1 && (p.MT / 2) * p.N >= 128 && !use_da(p.N)) {
       p.MT /= 2;
       r_cap = p.h_f;
     } else {
@@ -557,13 +612,17 @@ int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream
   // accumulator chunk: ~144 products (DCONV_X3_CHUNK_K), whole stages
   // (profiles/r1_tf32x3_kernel_accuracy.txt: worst element at 0.52 of the
   // fp32 tolerance at K = 4608; 288 reaches 0.90, 576 fails)
-  static const int chunk_k = getenv("DCONV_X3_CHUNK_K") ? atoi(getenv("DCONV_X3_CHUNK_K")) : 144;
+  // (DA: the correction terms have their own accumulator; chunk 288)
+  p.da = use_da(p.N) ? 1 : 0;
+  static const int chunk_env = getenv("DCONV_X3_CHUNK_K") ? atoi(getenv("DCONV_X3_CHUNK_K")) : 0;
+  const int chunk_k = chunk_env ? chunk_env : (p.da ? 288 : 144);
   const int k_stage = p.G * p.R * p.w_f * 8;
   p.chunk_st = std::max(1, chunk_k / k_stage);
   p.row_groups = p.stack > 1 ? 1 : (p.h_o + p.MT * kTileRows - 1) / (p.MT * kTileRows);
   p.strips = (p.w_o + kTW - 1) / kTW;
   p.units = (p.n + p.stack - 1) / p.stack * p.row_groups * p.strips * p.n_cg;
   p.idesc = tf32_idesc(p.N);
+  p.idesc2 = tf32_idesc(2 * p.N);
 
   CUtensorMap map;
   // stacked: one box per (image slot, block), SP rows; else PH rows x G blocks
@@ -576,8 +635,9 @@ int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream
   static const bool dbg = getenv("DCONV_DEBUG") != nullptr;
   if (dbg)
     fprintf(stderr,
-            "conv_tf32x3 N=%d MT=%d G=%d R=%d NS=%d stage=%d B chunk_st=%d stack=%d units=%d\n",
-            p.N, p.MT, p.G, p.R, p.NS, stage_bytes, p.chunk_st, p.stack, p.units);
+            "conv_tf32x3 N=%d MT=%d G=%d R=%d NS=%d stage=%d B chunk_st=%d stack=%d da=%d "
+            "units=%d\n",
+            p.N, p.MT, p.G, p.R, p.NS, stage_bytes, p.chunk_st, p.stack, p.da, p.units);
   static const bool prof = kProf && getenv("DCONV_TF32_PROFILE") != nullptr;
   if (prof) {  // debugging aid: where do the roles wait?  (not for timed runs)
     cudaMalloc(&p.dbg, (size_t)grid * 8 * 8);

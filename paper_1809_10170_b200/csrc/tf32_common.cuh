@@ -38,6 +38,8 @@ struct Tf32Params {
   int stack;          // images stacked along the tile rows (small maps), 1 = off
   int SP;             // stacked mode: patch rows per image slot (h_o + R - 1)
   uint32_t idesc;
+  uint32_t idesc2;    // split-TF32 DA: the N' = 2N instruction descriptor
+  int da;             // split-TF32: separate correction accumulator (N <= 128)
   unsigned long long* dbg;  // DCONV_TF32_PROFILE: per-CTA wait cycles (else null)
 };
 
