@@ -250,7 +250,9 @@ def main_gpu(args):
         return float(t.item())
 
     # ---- per-layer tile autotune (plan build, untimed), warm-up, graph capture
-    tiles = {} if args.no_tune or args.algo != "ffma" else plan.autotune(stream)
+    # per-layer FFMA tile autotune (also for the FFMA layers of tensor-core
+    # plans, e.g. batch-1 layers of a split-TF32 plan)
+    tiles = {} if args.no_tune else plan.autotune(stream)
     for _ in range(args.warmup):
         plan.run(stream)
     stream.synchronize()
