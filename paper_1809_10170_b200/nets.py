@@ -299,6 +299,13 @@ class Step:
     layer: Optional[Layer] = None
 
 
+def _sm_count() -> int:
+    """SMs of the current device (148 on B200; the CPU tests have no GPU)."""
+    if torch.cuda.is_available():
+        return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    return 148
+
+
 # tensor-core plans: "tf32" (one TF32 pass, looser tolerance) and "tf32x3"
 # (split-TF32, the fp32 tolerance of the FFMA path)
 TC_ALGOS = ("tf32", "tf32x3")
@@ -500,7 +507,7 @@ class Plan:
         if epilogue & _abi.EPI_MAXPOOL:
             return False
         units = self.n * -(-l.h_o // 16) * -(-l.w_o // 8) * -(-l.c_o // 128)
-        return units < 148
+        return units < _sm_count()
 
     def _tf32_s2d_first(self, l: Layer, x, y: Act, epilogue: int, skip) -> Act:
         """TF32 path, stride-f first layer (GoogLeNet/ResNet 7x7/s2, AlexNet
