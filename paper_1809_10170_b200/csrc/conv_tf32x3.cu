@@ -10,13 +10,15 @@
 // (the dropped x_lo*w_lo term is ~2^-22 of a product).
 //   * Weights: hi and lo are prepared once (bit-exact split of the blocked
 //     kernel, like pack_kernel tensor.cpp:85-95) and streamed by bulk copy.
-//   * Activations: TMA stages the raw fp32 patch; two "split" warps clear
-//     the low bits in place and write the remainders into a second pair of
-//     planes of the same stage -- on chip, so no workspace is added.
+//   * Activations: TMA stages the raw fp32 patch (x_hi: the tensor core
+//     reads only an operand's TF32 bits); two "split" warps write the
+//     remainders x - trunc(x) into a second pair of planes of the same
+//     stage -- on chip, so no workspace is added.
 //   * Accumulation: the tensor core adds into its fp32 accumulator with an
 //     error that grows with the accumulator's magnitude (K = 4608 in one
 //     accumulator fails the fp32 bar: profiles/r1_tf32x3_accuracy.txt).  The
-//     reduction is therefore cut into chunks of ~144 products: the MMAs of a
+//     reduction is therefore cut into chunks of ~144 products (288 with the
+//     separate correction accumulator of 64-channel layers): the MMAs of a
 //     chunk go to one of two TMEM accumulator sets while the epilogue warps
 //     add the previous chunk into fp32 register totals (IEEE adds), the same
 //     two-level summation the FFMA kernel does with its TMEM fold
