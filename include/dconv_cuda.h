@@ -132,7 +132,10 @@ int dconv_cuda_conv_direct(const dconv_conv_desc* d, const float* in,
                            void* stream);
 
 /* tcgen05/TMEM TF32 variant (north_star "tensor-core variant"; looser
- * tolerance).  Stride 1, c_ib == c_ob == 8.  The weights are
+ * tolerance).  c_ib == c_ob == 8; stride 1, a 1x1 of any
+ * stride (subsampled view), or a k x k stride-s layer (computed as a
+ * stride-1 layer over the space-to-depth view of the input, which the TMA
+ * reads in place with element strides s: no copy).  The weights are
  * rearranged once (like pack_kernel, tensor.cpp:85-95) into the tensor-core
  * operand layout; the caller owns that buffer (no hidden allocation).
  *   dconv_cuda_tf32_prepared_size   -> floats of the prepared weight buffer

@@ -250,8 +250,11 @@ int tf32_prepared_size_impl(const dconv_conv_desc* d, int64_t* floats, bool x3) 
   if (rc) return rc;
   if (d->c_ib != 8 || d->c_ob != 8)
     return set_error(DCONV_EUNSUPPORTED, "TF32 path needs c_ib == c_ob == 8");
-  *floats = x3 ? dconv_dev::tf32x3_prepared_floats(r.ib_n, d->h_f, d->w_f, r.jb_count)
-               : dconv_dev::tf32_prepared_floats(r.ib_n, d->h_f, d->w_f, r.jb_count);
+  int ib, hf, wf;
+  dconv_dev::WSrc src;
+  dconv_dev::tc_geometry(r.ib_n, d->h_f, d->w_f, d->stride, ib, hf, wf, src);
+  *floats = x3 ? dconv_dev::tf32x3_prepared_floats(ib, hf, wf, r.jb_count)
+               : dconv_dev::tf32_prepared_floats(ib, hf, wf, r.jb_count);
   return DCONV_OK;
 }
 
@@ -265,9 +268,12 @@ int prepare_tf32_impl(const dconv_conv_desc* d, const float* w, float* w_prepare
   if (rc) return rc;
   if (d->c_ib != 8 || d->c_ob != 8)
     return set_error(DCONV_EUNSUPPORTED, "TF32 path needs c_ib == c_ob == 8");
-  return x3 ? dconv_dev::launch_prepare_tf32x3(w, r.ib_n, d->h_f, d->w_f, r.jb_begin, r.jb_count,
+  int ib, hf, wf;
+  dconv_dev::WSrc src;
+  dconv_dev::tc_geometry(r.ib_n, d->h_f, d->w_f, d->stride, ib, hf, wf, src);
+  return x3 ? dconv_dev::launch_prepare_tf32x3(w, ib, hf, wf, r.jb_begin, r.jb_count, src,
                                                w_prepared, as_stream(stream))
-            : dconv_dev::launch_prepare_tf32(w, r.ib_n, d->h_f, d->w_f, r.jb_begin, r.jb_count,
+            : dconv_dev::launch_prepare_tf32(w, ib, hf, wf, r.jb_begin, r.jb_count, src,
                                              w_prepared, as_stream(stream));
 }
 

@@ -49,17 +49,32 @@ extern int ffma_variant_override;  // -1 = heuristic (dconv_cuda_set_ffma_varian
 int launch_conv_ffma(const FfmaParams& p, cudaStream_t stream);
 
 // tcgen05/TMEM TF32 variant (conv_tf32.cu): weights prepared once into the
-// UMMA K-major layout by launch_prepare_tf32.
+// UMMA K-major layout by launch_prepare_tf32.  A k x k stride-s layer is
+// computed as a stride-1 layer over the space-to-depth view of its input
+// (s*s*C_i channels, ceil(k/s) filter, read in place by strided TMA); its
+// prepared weights are rearranged accordingly from the original ones (WSrc).
+struct WSrc {
+  int s, ib_o, hf_o, wf_o;  // space-to-depth factor, original input blocks and filter
+};
+// computed-layer geometry (ib_n, h_f, w_f) and weight source for a layer
+inline void tc_geometry(int ib_o, int h_f, int w_f, int stride, int& ib_n, int& hf, int& wf,
+                        WSrc& src) {
+  const int s = (stride > 1 && (h_f > 1 || w_f > 1)) ? stride : 1;
+  ib_n = ib_o * s * s;
+  hf = (h_f + s - 1) / s;
+  wf = (w_f + s - 1) / s;
+  src = WSrc{s, ib_o, h_f, w_f};
+}
 int64_t tf32_prepared_floats(int ib_n, int h_f, int w_f, int jb_count);
 int launch_prepare_tf32(const float* w, int ib_n, int h_f, int w_f, int jb_begin, int jb_count,
-                        float* out, cudaStream_t stream);
+                        const WSrc& src, float* out, cudaStream_t stream);
 int launch_conv_tf32(const FfmaParams& p, const float* w_prepared, cudaStream_t stream);
 
 // split-TF32 variant (conv_tf32x3.cu): fp32 tolerance on the tensor cores;
 // weights prepared once into hi/lo operand pairs.
 int64_t tf32x3_prepared_floats(int ib_n, int h_f, int w_f, int jb_count);
 int launch_prepare_tf32x3(const float* w, int ib_n, int h_f, int w_f, int jb_begin, int jb_count,
-                          float* out, cudaStream_t stream);
+                          const WSrc& src, float* out, cudaStream_t stream);
 int launch_conv_tf32x3(const FfmaParams& p, const float* w_prepared, cudaStream_t stream);
 
 // Generic (any c_ib / c_ob) reference-order kernel and the first-layer reader.

@@ -119,18 +119,23 @@ __global__ void __launch_bounds__(kThreadsT, 1)
             const int slots = min(p.stack, p.n - img);
             const uint32_t box = (uint32_t)(p.SP * p.PW * 4) * 4u;
             mbar_arrive_expect_tx(&full[buf], 2u * box * (uint32_t)(slots * Ge) + wbytes);
+            // the stage's blocks lie in one space-to-depth phase: coordinates
+            // once per stage (a division per copy made the producer the limit)
+            int cx, cy, c40;
+            tma_block_coords(p, img, ib0, x0, n0, cx, cy, c40);
             for (int k = 0; k < slots; ++k)
               for (int gi = 0; gi < Ge; ++gi) {
                 float* dst = sp + (gi * p.PH + k * p.SP) * p.PW * 4;
-                const int c4 = (img + k) * p.ib_n + ib0 + gi;
-                tma_load_5d(dst, &tmap, 0, 0, x0, n0, c4, &full[buf]);
-                tma_load_5d(dst + p.plane_floats, &tmap, 0, 1, x0, n0, c4, &full[buf]);
+                const int c4 = c40 + k * p.ib_o + gi;
+                tma_load_5d(dst, &tmap, 0, 0, cx, cy, c4, &full[buf]);
+                tma_load_5d(dst + p.plane_floats, &tmap, 0, 1, cx, cy, c4, &full[buf]);
               }
           } else {
             mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes);
-            tma_load_5d(sp, &tmap, 0, 0, x0, y0 + n0, img * p.ib_n + ib0, &full[buf]);
-            tma_load_5d(sp + p.plane_floats, &tmap, 0, 1, x0, y0 + n0, img * p.ib_n + ib0,
-                        &full[buf]);
+            int cx, cy, c4;  // a stage's G blocks lie in one space-to-depth phase
+            tma_block_coords(p, img, ib0, x0, y0 + n0, cx, cy, c4);
+            tma_load_5d(sp, &tmap, 0, 0, cx, cy, c4, &full[buf]);
+            tma_load_5d(sp + p.plane_floats, &tmap, 0, 1, cx, cy, c4, &full[buf]);
           }
           const float* wsrc =
               p.w + (((int64_t)cg * p.ib_n + ib0) * p.h_f + n0) * (int64_t)p.w_f * 2 * p.N * 4;
@@ -278,7 +283,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
 // blocks are zero.  Bit-exact permutation.
 __global__ void prepare_tf32_weights_kernel(const float* __restrict__ w, int ib_n, int h_f,
                                             int w_f, int jb_begin, int jb_count, int N,
-                                            int64_t total, float* __restrict__ out) {
+                                            const WSrc src, int64_t total, float* __restrict__ out) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     int64_t t = e;
@@ -293,7 +298,7 @@ __global__ void prepare_tf32_weights_kernel(const float* __restrict__ w, int ib_
     float v = 0.f;
     if (jl < jb_count) {
       const int jb = jb_begin + jl, jj = co % 8, ii = kh * 4 + k4;
-      v = w[(((((int64_t)jb * ib_n + ib) * h_f + n) * w_f + m) * 8 + ii) * 8 + jj];
+      v = weight_src(w, jb, ib, n, m, ii, jj, src);
     }
     out[e] = v;
   }
@@ -327,23 +332,25 @@ int64_t tf32_prepared_floats(int ib_n, int h_f, int w_f, int jb_count) {
 }
 
 int launch_prepare_tf32(const float* w, int ib_n, int h_f, int w_f, int jb_begin, int jb_count,
-                        float* out, cudaStream_t stream) {
+                        const WSrc& src, float* out, cudaStream_t stream) {
   const int N = tf32_channels(jb_count);
   const int64_t total = tf32_prepared_floats(ib_n, h_f, w_f, jb_count);
   int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 32);
   prepare_tf32_weights_kernel<<<(unsigned)blocks, 256, 0, stream>>>(w, ib_n, h_f, w_f, jb_begin,
-                                                                    jb_count, N, total, out);
+                                                                    jb_count, N, src, total, out);
   dconv_host::count_launch();
   return dconv_host::check_launch("prepare_tf32_weights_kernel");
 }
 
 int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t stream) {
   FfmaParams f = f0;
-  int64_t px_floats = 8;
-  if (int rc = prepare_view(f, px_floats, "conv_tf32")) return rc;
+  InView view;
+  if (int rc = prepare_view(f, view, "conv_tf32")) return rc;
   Tf32Params p{};
   p.w = w_prepared;
   copy_geometry(p, f);
+  p.s2d = view.s2d;
+  p.ib_o = view.ib;
   p.N = tf32_channels(f.jb_count);
   p.n_cg = (f.jb_count * 8 + p.N - 1) / p.N;
   // stage = G input blocks x R filter rows, <= 48 KB of weights
@@ -415,6 +422,9 @@ int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t
   p.G = p.R == p.h_f ? std::max(1, std::min({p.ib_n, (48 * 1024) / (p.h_f * p.w_f * wtap),
                                              (40 * 1024) / patch_blk_bytes}))
                      : 1;
+  // space-to-depth: a stage's blocks must lie in one phase
+  if (p.s2d > 1)
+    while (p.ib_o % p.G) --p.G;
   p.n_g = (p.ib_n + p.G - 1) / p.G;
   p.n_r = (p.h_f + p.R - 1) / p.R;
   if (p.PH > 256 || p.PW > 256 || p.G > 256)
@@ -435,8 +445,8 @@ int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t
 
   // tensor map over the input view: {c4, half, W, H, image*block}
   CUtensorMap map;
-  if (int rc = p.stack > 1 ? encode_input_map(&map, f, px_floats, p.PW, p.SP, 1)
-                           : encode_input_map(&map, f, px_floats, p.PW, p.PH, p.G))
+  if (int rc = p.stack > 1 ? encode_input_map(&map, view, p.PW, p.SP, 1)
+                           : encode_input_map(&map, view, p.PW, p.PH, p.G))
     return rc;
 
   static int sms = 0;
@@ -453,6 +463,10 @@ int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t
   }
   const size_t smem = (size_t)p.NS * stage_bytes + bar_bytes;
   const int grid = std::min(p.units, sms);
+  static const bool dbg = getenv("DCONV_DEBUG") != nullptr;
+  if (dbg)
+    fprintf(stderr, "conv_tf32 N=%d MT=%d G=%d R=%d NS=%d stage=%d B stack=%d s2d=%d units=%d\n",
+            p.N, p.MT, p.G, p.R, p.NS, stage_bytes, p.stack, p.s2d, p.units);
   static const bool prof = getenv("DCONV_TF32_PROFILE") != nullptr;
   if (prof) {  // debugging aid: where do the roles wait?  (not for timed runs)
     cudaMalloc(&p.dbg, (size_t)grid * 8 * 8);

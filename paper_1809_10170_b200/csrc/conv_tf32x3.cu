@@ -157,18 +157,23 @@ __global__ void __launch_bounds__(kThreadsX, 1)
             const int slots = min(p.stack, p.n - img);
             const uint32_t box = (uint32_t)(p.SP * p.PW * 4) * 4u;
             mbar_arrive_expect_tx(&full[buf], 2u * box * (uint32_t)(slots * Ge) + wbytes);
+            // the stage's blocks lie in one space-to-depth phase: coordinates
+            // once per stage (a division per copy made the producer the limit)
+            int cx, cy, c40;
+            tma_block_coords(p, img, ib0, x0, n0, cx, cy, c40);
             for (int k = 0; k < slots; ++k)
               for (int gi = 0; gi < Ge; ++gi) {
                 float* dst = sp + (gi * p.PH + k * p.SP) * p.PW * 4;
-                const int c4 = (img + k) * p.ib_n + ib0 + gi;
-                tma_load_5d(dst, &tmap, 0, 0, x0, n0, c4, &full[buf]);
-                tma_load_5d(dst + p.plane_floats, &tmap, 0, 1, x0, n0, c4, &full[buf]);
+                const int c4 = c40 + k * p.ib_o + gi;
+                tma_load_5d(dst, &tmap, 0, 0, cx, cy, c4, &full[buf]);
+                tma_load_5d(dst + p.plane_floats, &tmap, 0, 1, cx, cy, c4, &full[buf]);
               }
           } else {
             mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes);
-            tma_load_5d(sp, &tmap, 0, 0, x0, y0 + n0, img * p.ib_n + ib0, &full[buf]);
-            tma_load_5d(sp + p.plane_floats, &tmap, 0, 1, x0, y0 + n0, img * p.ib_n + ib0,
-                        &full[buf]);
+            int cx, cy, c4;  // a stage's G blocks lie in one space-to-depth phase
+            tma_block_coords(p, img, ib0, x0, y0 + n0, cx, cy, c4);
+            tma_load_5d(sp, &tmap, 0, 0, cx, cy, c4, &full[buf]);
+            tma_load_5d(sp + p.plane_floats, &tmap, 0, 1, cx, cy, c4, &full[buf]);
           }
           const float* wsrc =
               p.w + (((int64_t)cg * p.ib_n + ib0) * p.h_f + n0) * (int64_t)p.w_f * 4 * p.N * 4;
@@ -402,7 +407,7 @@ __global__ void __launch_bounds__(kThreadsX, 1)
 // jb_count blocks are zero.
 __global__ void prepare_tf32x3_weights_kernel(const float* __restrict__ w, int ib_n, int h_f,
                                               int w_f, int jb_begin, int jb_count, int N,
-                                              int da, int64_t total, float* __restrict__ out) {
+                                              int da, const WSrc src, int64_t total, float* __restrict__ out) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     int64_t t = e;
@@ -424,7 +429,7 @@ __global__ void prepare_tf32x3_weights_kernel(const float* __restrict__ w, int i
     float v = 0.f;
     if (jl < jb_count) {
       const int jb = jb_begin + jl, jj = co % 8, ii = kh * 4 + k4;
-      v = w[(((((int64_t)jb * ib_n + ib) * h_f + n) * w_f + m) * 8 + ii) * 8 + jj];
+      v = weight_src(w, jb, ib, n, m, ii, jj, src);
     }
     const float h = __uint_as_float(__float_as_uint(v) & kHiMask);
     out[e] = hl ? v - h : h;
@@ -485,23 +490,25 @@ int64_t tf32x3_prepared_floats(int ib_n, int h_f, int w_f, int jb_count) {
 }
 
 int launch_prepare_tf32x3(const float* w, int ib_n, int h_f, int w_f, int jb_begin, int jb_count,
-                          float* out, cudaStream_t stream) {
+                          const WSrc& src, float* out, cudaStream_t stream) {
   const int N = tf32_channels(jb_count);
   const int64_t total = tf32x3_prepared_floats(ib_n, h_f, w_f, jb_count);
   const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 32);
   prepare_tf32x3_weights_kernel<<<(unsigned)blocks, 256, 0, stream>>>(
-      w, ib_n, h_f, w_f, jb_begin, jb_count, N, use_da(N) ? 1 : 0, total, out);
+      w, ib_n, h_f, w_f, jb_begin, jb_count, N, use_da(N) ? 1 : 0, src, total, out);
   dconv_host::count_launch();
   return dconv_host::check_launch("prepare_tf32x3_weights_kernel");
 }
 
 int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream_t stream) {
   FfmaParams f = f0;
-  int64_t px_floats = 8;
-  if (int rc = prepare_view(f, px_floats, "conv_tf32x3")) return rc;
+  InView view;
+  if (int rc = prepare_view(f, view, "conv_tf32x3")) return rc;
   Tf32Params p{};
   p.w = w_prepared;
   copy_geometry(p, f);
+  p.s2d = view.s2d;
+  p.ib_o = view.ib;
   p.N = tf32_channels(f.jb_count);
   p.n_cg = (f.jb_count * 8 + p.N - 1) / p.N;
   const int sms = sm_count();
@@ -591,6 +598,9 @@ int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream
     p.G = p.R == p.h_f ? std::max(1, std::min({p.ib_n, (72 * 1024) / (p.h_f * p.w_f * wtap),
                                                (40 * 1024) / patch_blk_bytes}))
                        : 1;
+    // space-to-depth: a stage's blocks must lie in one phase
+    if (p.s2d > 1)
+      while (p.ib_o % p.G) --p.G;
     p.plane_floats = (p.G * p.PH * p.PW * 4 + 31) & ~31;  // 128 B aligned planes
     p.wstage_floats = p.G * p.R * p.w_f * 4 * p.N * 4;
     p.stage_floats = ((4 * p.plane_floats + p.wstage_floats) + 255) & ~255;  // 1 KB aligned
@@ -628,8 +638,8 @@ int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream
 
   CUtensorMap map;
   // stacked: one box per (image slot, block), SP rows; else PH rows x G blocks
-  if (int rc = p.stack > 1 ? encode_input_map(&map, f, px_floats, p.PW, p.SP, 1)
-                           : encode_input_map(&map, f, px_floats, p.PW, p.PH, p.G))
+  if (int rc = p.stack > 1 ? encode_input_map(&map, view, p.PW, p.SP, 1)
+                           : encode_input_map(&map, view, p.PW, p.PH, p.G))
     return rc;
   set_x3_attrs();
   const size_t smem = (size_t)p.NS * stage_bytes + bar_bytes;

@@ -35,6 +35,7 @@ struct Tf32Params {
   int row_groups, strips, units;
   int MT;             // M-tiles per unit (1..4)
   int chunk_st;       // split-TF32: stages per TMEM accumulator chunk
+  int s2d, ib_o;      // in-place space-to-depth factor (1 = off); original input blocks
   int stack;          // images stacked along the tile rows (small maps), 1 = off
   int SP;             // stacked mode: patch rows per image slot (h_o + R - 1)
   uint32_t idesc;
@@ -215,41 +216,102 @@ inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// Host side shared by both launchers: a 1x1 stride-s layer becomes a stride-1
-// 1x1 layer over the subsampled view; checks; the 5-D tensor map over the
-// input view {c4, half, W, H, image*block} with a PW x PH x G box.
-inline int prepare_view(FfmaParams& f, int64_t& px_floats, const char* who) {
-  px_floats = 8;
-  if (f.s > 1 && f.h_f == 1 && f.w_f == 1) {
-    px_floats = 8 * (int64_t)f.s;
-    f.in_row *= f.s;
-    f.h_i = f.h_o;
-    f.w_i = f.w_o;
-    f.s = 1;
-  }
-  if (f.s != 1) return dconv_host::set_error(DCONV_EUNSUPPORTED, "%s: stride %d (only 1)", who, f.s);
+// The input as the TMA sees it: the original view, even when the kernel
+// computes a re-shaped layer (below).
+struct InView {
+  const float* base;
+  int n, w_i, h_i, ib;     // original dims and input blocks per image
+  int64_t px_floats, row, blk;
+  int s2d;                 // space-to-depth factor (1 = off)
+};
+
+// Host side shared by both launchers.
+//   * A 1x1 stride-s layer becomes a stride-1 1x1 layer over the subsampled
+//     view (pixel stride 8s floats, row stride s rows).
+//   * A k x k stride-s layer becomes a stride-1 layer with s*s*C_i channels
+//     and a ceil(k/s) filter (space-to-depth: channel block phase*ib + b,
+//     phase = dy*s + dx, is pixel (s*y + dy, s*x + dx) of block b), read in
+//     place: the TMA traverses the original map with element strides s
+//     (tools/tma_stride_probe.cu), so no repacked copy exists.  The prepared
+//     weights follow the same channel order (prepare kernels).
+// Then the checks.
+inline int prepare_view(FfmaParams& f, InView& v, const char* who) {
+  v = InView{f.in, f.n, f.w_i, f.h_i, f.ib_n, 8, f.in_row, f.in_blk, 1};
   if (f.in_img != (int64_t)f.ib_n * f.in_blk)
     return dconv_host::set_error(DCONV_EUNSUPPORTED,
                                  "%s: input view must stack blocks densely per image", who);
+  if (f.s > 1 && f.h_f == 1 && f.w_f == 1) {
+    v.px_floats = 8 * (int64_t)f.s;
+    v.row = f.in_row * f.s;
+    v.h_i = f.h_o;
+    v.w_i = f.w_o;
+    f.h_i = f.h_o;
+    f.w_i = f.w_o;
+    f.s = 1;
+  } else if (f.s > 1) {
+    const int s = f.s;
+    v.s2d = s;
+    f.ib_n *= s * s;
+    f.h_f = (f.h_f + s - 1) / s;
+    f.w_f = (f.w_f + s - 1) / s;
+    f.h_i = f.h_o + f.h_f - 1;
+    f.w_i = f.w_o + f.w_f - 1;
+    f.s = 1;
+  }
   if (!encode_fn()) return dconv_host::set_error(DCONV_ECUDA, "cuTensorMapEncodeTiled unavailable");
   return DCONV_OK;
 }
 
-inline int encode_input_map(CUtensorMap* map, const FfmaParams& f, int64_t px_floats, int PW,
-                            int PH, int G) {
-  const cuuint64_t dims[5] = {4, 2, (cuuint64_t)f.w_i, (cuuint64_t)f.h_i,
-                              (cuuint64_t)f.n * f.ib_n};
-  const cuuint64_t strides[4] = {16, (cuuint64_t)px_floats * 4, (cuuint64_t)f.in_row * 4,
-                                 (cuuint64_t)f.in_blk * 4};
-  const cuuint32_t box[5] = {4, 1, (cuuint32_t)PW, (cuuint32_t)PH, (cuuint32_t)G};
-  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  const CUresult cr = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(f.in),
+// 5-D tensor map {c4, half, W, H, image*block} over the original view; the
+// box lands PW x PH pixels x G blocks (with element strides s2d: every s-th
+// column and row).
+inline int encode_input_map(CUtensorMap* map, const InView& v, int PW, int PH, int G) {
+  const cuuint64_t dims[5] = {4, 2, (cuuint64_t)v.w_i, (cuuint64_t)v.h_i, (cuuint64_t)v.n * v.ib};
+  const cuuint64_t strides[4] = {16, (cuuint64_t)v.px_floats * 4, (cuuint64_t)v.row * 4,
+                                 (cuuint64_t)v.blk * 4};
+  const cuuint32_t box[5] = {4, 1, (cuuint32_t)(PW * v.s2d), (cuuint32_t)(PH * v.s2d),
+                             (cuuint32_t)G};
+  const cuuint32_t estr[5] = {1, 1, (cuuint32_t)v.s2d, (cuuint32_t)v.s2d, 1};
+  if (box[2] > 256 || box[3] > 256)
+    return dconv_host::set_error(DCONV_EUNSUPPORTED, "TMA box %u x %u too large", box[2], box[3]);
+  const CUresult cr = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(v.base),
                                   dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS)
     return dconv_host::set_error(DCONV_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
   return DCONV_OK;
+}
+
+// Original blocked weight [jb][b][n][m][ii][jj] behind element (jb, ib, n, m,
+// ii, jj) of the computed (possibly space-to-depth) layer; 0 for the taps
+// the re-shaped filter adds past the original edge.
+__device__ __forceinline__ float weight_src(const float* __restrict__ w, int jb, int ib, int n,
+                                            int m, int ii, int jj, const WSrc& q) {
+  const int ph = ib / q.ib_o, b = ib - ph * q.ib_o;
+  const int dy = ph / q.s, dx = ph - dy * q.s;
+  const int no = q.s * n + dy, mo = q.s * m + dx;
+  if (no >= q.hf_o || mo >= q.wf_o) return 0.f;
+  return w[(((((int64_t)jb * q.ib_o + b) * q.hf_o + no) * q.wf_o + mo) * 8 + ii) * 8 + jj];
+}
+
+// TMA coordinates of input block ib (of the computed layer) for a tile at
+// (x0, row y) of image img: with space-to-depth, block ib = phase*ib_o + b
+// is pixel (s*y + dy, s*x + dx) of original block b.
+__device__ __forceinline__ void tma_block_coords(const Tf32Params& p, int img, int ib, int x0,
+                                                 int y, int& cx, int& cy, int& c4) {
+  const int s = p.s2d;
+  if (s == 1) {  // no space-to-depth (the common case: no divisions)
+    cx = x0;
+    cy = y;
+    c4 = img * p.ib_o + ib;
+    return;
+  }
+  const int ph = ib / p.ib_o, b = ib - ph * p.ib_o;
+  const int dy = ph / s, dx = ph - dy * s;
+  cx = s * x0 + dx;
+  cy = s * y + dy;
+  c4 = img * p.ib_o + b;
 }
 
 inline void copy_geometry(Tf32Params& p, const FfmaParams& f) {

@@ -458,10 +458,9 @@ class Plan:
                                                             x3=self.x3),
                                        l.name, "tf32", n * l.flops, l))
                 return y
-            if (tc and not l.first and l.s > 1 and l.h_f > 1
-                    and os.environ.get("DCONV_NO_S2D") is None):
-                return self._tf32_s2d_blocked(l, x, y, epilogue, skip, in_view)
-            if tc and not l.first and (l.s == 1 or (l.h_f == 1 and l.w_f == 1)):
+            if tc and not l.first:
+                # stride 1, 1x1 of any stride, and k x k stride s (the C-ABI
+                # reads the space-to-depth view of the input in place)
                 wp = prepare_tf32(l, w, x3=self.x3)
                 self.weights[l.name + ".tf32"] = wp
                 self.steps.append(Step(lambda st: conv_tf32(l, self.n, x, wp, y, epilogue, skip, st,
@@ -538,40 +537,6 @@ class Plan:
             lambda st: check(lib().dconv_cuda_pack_space_to_depth(
                 ptr(x), n, l.c_i, l.h_i, l.w_i, f, ptr(xb.buf), stream_ptr(st))),
             f"pack_{l.name}", "pack"))
-        self.steps.append(Step(lambda st: conv_tf32(lb, n, xb, wp, y, epilogue, skip, st,
-                                                    x3=self.x3),
-                               l.name, "tf32", n * l.flops, l))
-        return y
-
-    def _tf32_s2d_blocked(self, l: Layer, x: Act, y: Act, epilogue: int, skip,
-                          in_view=None) -> Act:
-        """TF32 path, strided blocked layer (ResNet's 3x3/s2): space-to-depth
-        of the (halo'd) input view + stride-1 tcgen05 conv with f*f*C_i
-        channels and a ceil(h_f/f)-wide filter; FLOPs counted as the original."""
-        f = l.s
-        cs = l.c_i * f * f
-        hs, ws = -(-l.h_i // f), -(-l.w_i // f)
-        hf, wf = -(-l.h_f // f), -(-l.w_f // f)
-        lb = Layer(l.name, cs, l.c_o, hs, ws, hf, wf, 1, False)
-        assert (lb.h_o, lb.w_o) == (l.h_o, l.w_o)
-        w = self.weights[l.name]
-        dense = torch.empty((l.c_i, l.c_o, l.h_f, l.w_f), dtype=torch.float32, device=w.device)
-        check(lib().dconv_cuda_unpack_kernel(ptr(w), l.c_i, l.c_o, l.h_f, l.w_f, CB, CB,
-                                             ptr(dense), stream_ptr(None)))
-        wpad = torch.zeros((l.c_i, l.c_o, hf * f, wf * f), dtype=torch.float32, device=w.device)
-        wpad[:, :, :l.h_f, :l.w_f] = dense
-        ws2d = (wpad.view(l.c_i, l.c_o, hf, f, wf, f).permute(3, 5, 0, 1, 2, 4)
-                .reshape(cs, l.c_o, hf, wf).contiguous())
-        wp = prepare_tf32(lb, pack_weights(ws2d, False), x3=self.x3)
-        self.weights[l.name + ".tf32"] = wp
-        xb = Act(self.n, cs, hs, ws, device=w.device)
-        n = self.n
-        view = in_view or x.full_view()
-        self.steps.append(Step(
-            lambda st: check(lib().dconv_cuda_space_to_depth_blocked(
-                view[0], view[1], view[2], view[3], n, l.c_i, l.h_i, l.w_i, f, ptr(xb.buf),
-                stream_ptr(st))),
-            f"s2d_{l.name}", "pack"))
         self.steps.append(Step(lambda st: conv_tf32(lb, n, xb, wp, y, epilogue, skip, st,
                                                     x3=self.x3),
                                l.name, "tf32", n * l.flops, l))

@@ -863,43 +863,73 @@ def test_tf32_space_to_depth_stem_matches_reader(config, name):
     assert np.abs(ya[0] - yb[0]).max() > 0  # the tcgen05 path really ran
 
 
-def test_tf32_space_to_depth_strided_blocked_layers():
-    """ResNet-50's 3x3/s2 convs on the TF32 path (blocked space-to-depth of
-    the top/left-padded input + stride-1 tcgen05 conv): each equals the FFMA
-    plan's layer output within the TF32 bound (teacher-forced: same input)."""
-    b = nets.build_plan("resnet50", 1, seed=19, algo="tf32")
-    assert sum(1 for s in b.steps if s.name.startswith("s2d_")) == 3
+@pytest.mark.parametrize("algo", ["tf32", "tf32x3"])
+def test_tensor_core_strided_layers_read_space_to_depth_in_place(algo, monkeypatch):
+    """ResNet-50's 3x3/s2 convs on the tensor-core paths: computed as stride-1
+    layers over the space-to-depth view of the (top/left-padded) input, read
+    in place by strided TMA -- the plan has no repack step -- and equal to
+    the fp64 oracle within the TF32 bound (tf32) or the chain's normwise fp32
+    bound (tf32x3; deep unnormalised activations, as the full-size chain
+    checks) on every row of the output (teacher-forced: the plan's own
+    input).  Batch 2 with the batch-1 FFMA routing of split-TF32 plans off."""
+    monkeypatch.setattr(nets.Plan, "_few_units", lambda self, l, epi: False)
+    b = nets.build_plan("resnet50", 2, seed=19, algo=algo)
+    assert not any(st.name.startswith("s2d_") for st in b.steps)
     rec = {}
     orig = nets.conv_tf32
 
     def spy(l, n, x, wp, out, epilogue=0, skip=None, stream=None, in_view=None, **kw):
         orig(l, n, x, wp, out, epilogue, skip, stream, in_view, **kw)
         torch.cuda.synchronize()
-        rec[l.name] = (l, x.buf.clone(), out.buf.clone(), out, epilogue)
+        if l.s > 1 and l.h_f > 1:
+            rec[l.name] = (l, host(x.buf), host(out.buf), out, epilogue)
     nets.conv_tf32 = spy
     try:
         b.run()
     finally:
         nets.conv_tf32 = orig
-    for name in ("s2b1_c2", "s3b1_c2", "s4b1_c2"):
-        lb, xs2d, yout, out, epi = rec[name]
-        lo = [l for _, l in nets.resnet50_layers() if l.name == name][0]
-        # undo the space-to-depth on the host: xs2d[(dy*2+dx)*C + c] at (ys, xs)
-        xs = host(xs2d)[0]
-        c, f = lo.c_i, lo.s
-        blk = xs.transpose(0, 3, 1, 2).reshape(-1, xs.shape[1], xs.shape[2])[:c * f * f]
-        x = np.zeros((c, blk.shape[1] * f, blk.shape[2] * f), np.float32)
-        for dy in range(f):
-            for dx in range(f):
-                x[:, dy::f, dx::f] = blk[(dy * f + dx) * c:(dy * f + dx + 1) * c]
-        x = x[:, :lo.h_i, :lo.w_i]
-        k = po.unpack_kernel(host(b.weights[name]), lo.c_i, lo.c_o)
-        want = po.pack_feature_map(po.conv_oracle64(x, k, f), 8)
-        if epi & _abi.EPI_RELU:
-            want = np.maximum(want, 0)
-        got = host(yout)[0][:, out.halo:out.halo + lo.h_o, out.halo:out.halo + lo.w_o]
-        bound = 2.0 ** -9 * po.pack_feature_map(po.conv_oracle64(np.abs(x), np.abs(k), f), 8) + 1e-5
-        assert (np.abs(got - want) <= bound).all(), name
+    assert sorted(rec) == ["s2b1_c2", "s3b1_c2", "s4b1_c2"]
+    for name, (l, xs, ys, out, epi) in rec.items():
+        kb = po.pack_kernel(po.unpack_kernel(host(b.weights[name]), l.c_i, l.c_o), 8, 8)
+        for i in range(2):
+            xb = np.ascontiguousarray(xs[i][:, :l.h_i, :l.w_i, :])
+            want = po.conv_oracle64_blocked(xb, kb, l.c_i, l.c_o, l.s, 0, l.h_o)
+            if epi & _abi.EPI_RELU:
+                want = np.maximum(want, 0)
+            got = ys[i][:, out.halo:out.halo + l.h_o, out.halo:out.halo + l.w_o]
+            if algo == "tf32x3":
+                scale = max(1.0, float(np.abs(want).max()))
+                err = float(np.abs(got - want).max())
+                assert err <= 1e-5 * scale + 1e-4, f"{name} img {i}: err {err} scale {scale}"
+            else:
+                bound = 2.0 ** -9 * po.conv_oracle64_blocked(np.abs(xb), np.abs(kb), l.c_i, l.c_o,
+                                                             l.s, 0, l.h_o) + 1e-5
+                assert (np.abs(got - want) <= bound).all(), name
+
+
+@pytest.mark.parametrize("x3", [False, True])
+@pytest.mark.parametrize("ci,co,h,f,s,n", [(64, 72, 21, 3, 2, 2), (24, 256, 17, 5, 2, 1),
+                                            (16, 64, 27, 3, 3, 2), (40, 136, 15, 3, 2, 3)])
+def test_tensor_core_strided_kxk_through_the_abi(ci, co, h, f, s, n, x3):
+    """k x k stride-s layers straight through the tensor-core C-ABI (in-place
+    space-to-depth, ragged channel counts, stride 3, stacked 7x7 tiles)."""
+    l = nets.Layer("s", ci, co, h, h, f, f, s)
+    x = po.uniform((n, ci, h, h), 9950 + ci, s)
+    k = po.uniform((ci, co, f, f), 9951 + ci, s)
+    a = nets.Act(n, ci, h, h)
+    a.buf.copy_(dev(np.stack([po.pack_feature_map(x[i], 8) for i in range(n)])))
+    wp = nets.prepare_tf32(l, nets.pack_weights(dev(k), False), x3=x3)
+    y = nets.Act(n, co, l.h_o, l.w_o)
+    nets.conv_tf32(l, n, a, wp, y, _abi.EPI_RELU, x3=x3)
+    got = host(y.buf)
+    for i in range(n):
+        want = np.maximum(po.pack_feature_map(po.conv_oracle64(x[i], k, s), 8), 0)
+        if x3:
+            assert_tol(got[i], want, f"img {i}")
+        else:
+            bound = 2.0 ** -9 * po.pack_feature_map(po.conv_oracle64(np.abs(x[i]), np.abs(k), s), 8)
+            assert (np.abs(got[i] - want) <= bound + 1e-5).all()
+        assert np.abs(got[i] - want).max() > 0  # the tensor-core path really ran
 
 
 @pytest.mark.parametrize("config,n", [("vgg16", 32), ("resnet50", 256), ("googlenet", 64)])
