@@ -213,7 +213,9 @@ int dconv_cuda_pack_space_to_depth(const float* src, int n, int c, int h, int w,
                                    float* dst, void* stream);
 
 /* The same for a blocked (c_b = 8) map view with strides in floats: a stride-f
- * blocked layer becomes a stride-1 layer over the result (TF32 path). */
+ * blocked layer becomes a stride-1 layer over the result.  (The tensor-core
+ * conv calls read this view in place with strided TMA and need no copy; this
+ * materialises it, e.g. for other consumers.) */
 int dconv_cuda_space_to_depth_blocked(const float* src, int64_t in_img_stride,
                                       int64_t in_blk_stride, int64_t in_row_stride, int n, int c,
                                       int h, int w, int f, float* dst, void* stream);

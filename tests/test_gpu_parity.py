@@ -1072,3 +1072,26 @@ def test_python_dropin_tensor_core_conv():
         assert (np.abs(y1[i] - ref) <= tf32_bound(x[i], k)).all()
     with pytest.raises(ValueError, match="layout error"):
         D.PreparedKernel(D.BlockedKernel(ci, co, 3, 3, 8, 4), shape)
+
+
+def test_space_to_depth_blocked_bitexact():
+    """dconv_cuda_space_to_depth_blocked (C-ABI utility; the tensor-core
+    kernels read this view in place instead): channel (dy*f + dx)*C + c at
+    (y, x) is pixel (f*y + dy, f*x + dx), zero outside, bit-exact."""
+    n, c, h, w, f = 2, 16, 9, 11, 2
+    x = po.uniform((n, c, h, w), 9960, 0)
+    xb = dev(np.stack([po.pack_feature_map(x[i], 8) for i in range(n)]))
+    hs, ws = -(-h // f), -(-w // f)
+    out = torch.empty((n, (c * f * f + 7) // 8, hs, ws, 8), device="cuda")
+    blk = h * w * 8
+    _abi.check(_abi.lib().dconv_cuda_space_to_depth_blocked(
+        _abi.ptr(xb), 2 * blk, blk, w * 8, n, c, h, w, f, _abi.ptr(out), _abi.stream_ptr()))
+    got = host(out)
+    for i in range(n):
+        xp = np.zeros((c, hs * f, ws * f), np.float32)
+        xp[:, :h, :w] = x[i]
+        want = np.zeros((c * f * f, hs, ws), np.float32)
+        for dy in range(f):
+            for dx in range(f):
+                want[(dy * f + dx) * c:(dy * f + dx + 1) * c] = xp[:, dy::f, dx::f]
+        assert np.array_equal(got[i], po.pack_feature_map(want, 8))
