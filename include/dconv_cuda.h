@@ -236,11 +236,11 @@ int dconv_cuda_maxpool2x2_blocked(const float* in, int n, int n_blocks, int h,
 /* Zeroes a float buffer (halo buffers are zeroed once, outside timing). */
 int dconv_cuda_zero(float* x, int64_t count, void* stream);
 
-/* Tile selector override for the FFMA kernel (the GPU analogue of the
- * reference's BlockingParams choice, model.hpp:85-109): -1 = heuristic,
- * 0 = CTA tile 128 pixels x 128 channels, 1 = 256 pixels x 64 channels,
- * 2 = 128 pixels x 64 channels (batch-1 layers).  Process-wide; a descriptor's tile_variant (if non-zero) takes precedence. */
-int dconv_cuda_set_ffma_variant(int variant);
+/* Test hook for the FFMA launcher's per-(device, kernel, ks) cache of
+ * co-resident clusters: the cached answer for CTA tile `tile_variant`
+ * (1..3, as dconv_conv_desc.tile_variant) and cluster size ks next to a fresh
+ * cudaOccupancyMaxActiveClusters query of the same instantiation. */
+int dconv_cuda_ffma_cluster_slots(int tile_variant, int ks, int* cached, int* fresh);
 
 /* Launch accounting: number of device kernels this library launched since
  * load (for bench.py's gpu_launches claim) and the name of the last kernel. */

@@ -263,15 +263,39 @@ static tile_fn find_tile(int c_ob, int w_ob) {  /* micro_kernel.hpp:43-46 */
   return NULL;
 }
 
-static int conv_direct_impl(const float* in, const float* k, int n_img,
-                            int c_i, int c_o, int h_i, int w_i, int h_f,
-                            int w_f, int s, int c_ib, int c_ob, int w_ob,
-                            int threads, float* out, int literal) {
+int orc_direct_job_init(orc_direct_job* jb_, const float* in, const float* k, int n_img,
+                        int c_i, int c_o, int h_i, int w_i, int h_f, int w_f, int s,
+                        int c_ib, int c_ob, int w_ob, int threads, float* out) {
+  orc_direct_job* J = jb_;
   int h_o, w_o;
   if (orc_conv_shape(c_i, c_o, h_i, w_i, h_f, w_f, s, &h_o, &w_o)) return -1;
   if (c_ib < 1 || c_ob < 1 || w_ob < 1) return -1;
-  const int ib_n = orc_round_up(c_i, c_ib) / c_ib;
-  const int jb_n = orc_round_up(c_o, c_ob) / c_ob;
+  memset(J, 0, sizeof(*J));
+  J->in = in; J->k = k; J->out = out;
+  J->n_img = n_img; J->c_i = c_i; J->c_o = c_o; J->h_i = h_i; J->w_i = w_i;
+  J->h_f = h_f; J->w_f = w_f; J->s = s; J->c_ib = c_ib; J->c_ob = c_ob; J->w_ob = w_ob;
+  J->h_o = h_o; J->w_o = w_o;
+  J->ib_n = orc_round_up(c_i, c_ib) / c_ib;
+  J->jb_n = orc_round_up(c_o, c_ob) / c_ob;
+  if (threads < 1) threads = 1;
+  /* j' in parallel (PAPER.md:332, :366-377), refined into row bands of the
+   * output block when there are fewer (image, j') pairs than threads, so
+   * narrow layers (C_o = 64 -> 8 blocks) still use every core.  Every output
+   * element is owned by exactly one unit and accumulated in the same order,
+   * so the result is bitwise independent of the thread count (SPEC.md:348). */
+  int bands = 1;
+  while (n_img * J->jb_n * bands < 4 * threads && bands * 2 <= h_o) bands *= 2;
+  J->bands = bands;
+  J->rows_per = (h_o + bands - 1) / bands;
+  J->units = n_img * J->jb_n * bands;
+  return J->units;
+}
+
+/* One parallel unit (image, j', row band) of Alg. 3. */
+static void direct_unit(const orc_direct_job* J, int u, int literal) {
+  const int h_i = J->h_i, w_i = J->w_i, h_f = J->h_f, w_f = J->w_f, s = J->s;
+  const int c_ib = J->c_ib, c_ob = J->c_ob, w_ob = J->w_ob, h_o = J->h_o, w_o = J->w_o;
+  const int ib_n = J->ib_n, jb_n = J->jb_n;
   const size_t in_img = (size_t)ib_n * h_i * w_i * c_ib;
   const size_t out_img = (size_t)jb_n * h_o * w_o * c_ob;
   const size_t out_blk = (size_t)h_o * w_o * c_ob;
@@ -279,62 +303,64 @@ static int conv_direct_impl(const float* in, const float* k, int n_img,
   const int row_pitch = w_i * c_ib;
   const int col_stride = s * c_ib;
   tile_fn full = literal ? NULL : find_tile(c_ob, w_ob);
+  const int band = u % J->bands, t = u / J->bands;
+  const int img = t / jb_n, jb = t % jb_n;
+  const int l0 = band * J->rows_per, l1 = (l0 + J->rows_per < h_o) ? l0 + J->rows_per : h_o;
+  if (l0 >= l1) return;
+  const float* inp = J->in + (size_t)img * in_img;
+  float* ob = J->out + (size_t)img * out_img + (size_t)jb * out_blk;
+  memset(ob + (size_t)l0 * w_o * c_ob, 0,
+         sizeof(float) * (size_t)(l1 - l0) * w_o * c_ob);  /* SPEC.md:358 */
+  for (int ib = 0; ib < ib_n; ++ib) {               /* i' */
+    const float* w = J->k + ((size_t)jb * ib_n + ib) * slab;  /* tensor.hpp:138-140 */
+    const float* inb = inp + (size_t)ib * h_i * w_i * c_ib;
+    for (int l = l0; l < l1; ++l)                   /* l */
+      for (int kb = 0; kb * w_ob < w_o; ++kb) {     /* k' */
+        const int wob = (w_o - kb * w_ob) < w_ob ? (w_o - kb * w_ob) : w_ob;
+        float* ot = ob + ((size_t)l * w_o + (size_t)kb * w_ob) * c_ob;
+        if (literal) {
+          /* PAPER.md:349 literal: column s*k'*w_ob + kk + m (wrong for s>1) */
+          for (int n = 0; n < h_f; ++n)
+            for (int m = 0; m < w_f; ++m)
+              for (int ii = 0; ii < c_ib; ++ii)
+                for (int kk = 0; kk < wob; ++kk) {
+                  const int col = s * kb * w_ob + kk + m;
+                  const float a =
+                      inb[((size_t)(l * s + n) * w_i + col) * c_ib + ii];
+                  const float* wp = w + ((size_t)(n * w_f + m) * c_ib + ii) * c_ob;
+                  for (int jj = 0; jj < c_ob; ++jj) ot[kk * c_ob + jj] += a * wp[jj];
+                }
+          continue;
+        }
+        /* stride fix SPEC.md:354: column s*(k'*w_ob + kk) + m */
+        const float* it =
+            inb + ((size_t)(l * s) * w_i + (size_t)kb * w_ob * s) * c_ib;
+        if (full && wob == w_ob)
+          full(it, w, ot, h_f, w_f, c_ib, row_pitch, col_stride);
+        else  /* edge tile, identical order (SPEC.md:316-324) */
+          tile_generic(it, w, ot, h_f, w_f, c_ib, row_pitch, col_stride,
+                       c_ob, wob);
+      }
+  }
+}
+
+void orc_direct_job_unit(const orc_direct_job* J, int u) { direct_unit(J, u, 0); }
+
+static int conv_direct_impl(const float* in, const float* k, int n_img,
+                            int c_i, int c_o, int h_i, int w_i, int h_f,
+                            int w_f, int s, int c_ib, int c_ob, int w_ob,
+                            int threads, float* out, int literal) {
 #ifdef _OPENMP
   if (threads <= 0) threads = omp_get_max_threads();
 #else
   threads = 1;
 #endif
-  /* j' in parallel (PAPER.md:332, :366-377), refined into row bands of the
-   * output block when there are fewer (image, j') pairs than threads, so
-   * narrow layers (C_o = 64 -> 8 blocks) still use every core.  Every output
-   * element is owned by exactly one unit and accumulated in the same order,
-   * so the result is bitwise independent of the thread count (SPEC.md:348). */
-  int bands = 1;
-  while (n_img * jb_n * bands < 4 * threads && bands * 2 <= h_o) bands *= 2;
-  const int rows_per = (h_o + bands - 1) / bands;
-  const int units = n_img * jb_n * bands;
+  orc_direct_job J;
+  const int units = orc_direct_job_init(&J, in, k, n_img, c_i, c_o, h_i, w_i, h_f, w_f, s,
+                                        c_ib, c_ob, w_ob, threads, out);
+  if (units < 0) return -1;
 #pragma omp parallel for schedule(dynamic, 1) num_threads(threads)
-  for (int u = 0; u < units; ++u) {
-    const int band = u % bands, t = u / bands;
-    const int img = t / jb_n, jb = t % jb_n;
-    const int l0 = band * rows_per, l1 = (l0 + rows_per < h_o) ? l0 + rows_per : h_o;
-    if (l0 >= l1) continue;
-    const float* inp = in + (size_t)img * in_img;
-    float* ob = out + (size_t)img * out_img + (size_t)jb * out_blk;
-    memset(ob + (size_t)l0 * w_o * c_ob, 0,
-           sizeof(float) * (size_t)(l1 - l0) * w_o * c_ob);
-    for (int ib = 0; ib < ib_n; ++ib) {               /* i' */
-      const float* w = k + ((size_t)jb * ib_n + ib) * slab;  /* tensor.hpp:138-140 */
-      const float* inb = inp + (size_t)ib * h_i * w_i * c_ib;
-      for (int l = l0; l < l1; ++l)                   /* l */
-        for (int kb = 0; kb * w_ob < w_o; ++kb) {     /* k' */
-          const int wob = (w_o - kb * w_ob) < w_ob ? (w_o - kb * w_ob) : w_ob;
-          float* ot = ob + ((size_t)l * w_o + (size_t)kb * w_ob) * c_ob;
-          if (literal) {
-            /* PAPER.md:349 literal: column s*k'*w_ob + kk + m (wrong for s>1) */
-            for (int n = 0; n < h_f; ++n)
-              for (int m = 0; m < w_f; ++m)
-                for (int ii = 0; ii < c_ib; ++ii)
-                  for (int kk = 0; kk < wob; ++kk) {
-                    const int col = s * kb * w_ob + kk + m;
-                    const float a =
-                        inb[((size_t)(l * s + n) * w_i + col) * c_ib + ii];
-                    const float* wp = w + ((size_t)(n * w_f + m) * c_ib + ii) * c_ob;
-                    for (int jj = 0; jj < c_ob; ++jj) ot[kk * c_ob + jj] += a * wp[jj];
-                  }
-            continue;
-          }
-          /* stride fix SPEC.md:354: column s*(k'*w_ob + kk) + m */
-          const float* it =
-              inb + ((size_t)(l * s) * w_i + (size_t)kb * w_ob * s) * c_ib;
-          if (full && wob == w_ob)
-            full(it, w, ot, h_f, w_f, c_ib, row_pitch, col_stride);
-          else  /* edge tile, identical order */
-            tile_generic(it, w, ot, h_f, w_f, c_ib, row_pitch, col_stride,
-                         c_ob, wob);
-        }
-    }
-  }
+  for (int u = 0; u < units; ++u) direct_unit(&J, u, literal);
   return 0;
 }
 

@@ -86,6 +86,23 @@ int orc_conv_direct(const float* in, const float* k, int n_img, int c_i,
                     int c_o, int h_i, int w_i, int h_f, int w_f, int stride,
                     int c_ib, int c_ob, int w_ob, int threads, float* out);
 
+/* The same computation split into its parallel units (image, j', row band),
+ * for an external scheduler: the reference's ThreadPool (thread_pool.cpp:64-97)
+ * runs orc_direct_job_unit over [0, units) in oracle/ref_shim.cpp. */
+typedef struct orc_direct_job {
+  const float* in;
+  const float* k;
+  float* out;
+  int n_img, c_i, c_o, h_i, w_i, h_f, w_f, s, c_ib, c_ob, w_ob, h_o, w_o;
+  int ib_n, jb_n, bands, rows_per, units;
+} orc_direct_job;
+/* Returns the unit count (bands sized for `threads`), or -1 on a shape or
+ * parameter error. */
+int orc_direct_job_init(orc_direct_job* job, const float* in, const float* k, int n_img,
+                        int c_i, int c_o, int h_i, int w_i, int h_f, int w_f, int stride,
+                        int c_ib, int c_ob, int w_ob, int threads, float* out);
+void orc_direct_job_unit(const orc_direct_job* job, int u);
+
 /* The paper's literal Alg. 3 input index s*k'*w_ob + kk + m,
  * kept only for the mutation test of SPEC.md:622. */
 int orc_conv_direct_literal_alg3(const float* in, const float* k, int c_i,

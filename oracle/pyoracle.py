@@ -71,7 +71,8 @@ def ref():
         l.ref_layout_transform_count.restype = ctypes.c_uint64
         l.ref_blocked_kernel_offset.restype = ctypes.c_size_t
         l.ref_blocked_kernel_offset.argtypes = [_I] * 12
-        l.ref_conv_reordered_batch.argtypes = [_F, _F] + [_I] * 10 + [_F]
+        l.ref_conv_reordered_batch.argtypes = [_F, _F] + [_I] * 9 + [_F]
+        l.ref_pool_conv_direct.argtypes = [_F, _F] + [_I] * 12 + [_F]
         _ref = l
     return _ref
 
@@ -169,6 +170,29 @@ def conv_direct(xb: np.ndarray, kb: np.ndarray, ci: int, co: int, s: int,
     out = np.empty((n, jb_n, ho, wo, c_ob), np.float32)
     rc = orc().orc_conv_direct(_fp(np.ascontiguousarray(x4)), _fp(np.ascontiguousarray(kb)),
                                n, ci, co, hi, wi, hf, wf, s, c_ib, c_ob, w_ob, threads, _fp(out))
+    if rc:
+        raise ValueError("conv_direct: parameter/layout error")
+    return out if xb.ndim == 5 else out[0]
+
+
+def conv_direct_pool(xb: np.ndarray, kb: np.ndarray, ci: int, co: int, s: int,
+                     workers: int, w_ob: int = 0, out: np.ndarray = None) -> np.ndarray:
+    """The same restated Alg. 3, scheduled on the reference's own ThreadPool
+    (oracle/_ref, thread_pool.cpp) with ``workers`` pool threads plus the
+    caller (DCONV_THREADS = workers).  Bitwise equal to conv_direct."""
+    r = ref()
+    if r is None:
+        raise RuntimeError("oracle/_ref/libdconv_ref.so was not built")
+    x4 = xb if xb.ndim == 5 else xb[None]
+    n, nb, hi, wi, c_ib = x4.shape
+    jb_n, _, hf, wf, _, c_ob = kb.shape
+    ho, wo = conv_shape(ci, co, hi, wi, hf, wf, s)
+    if w_ob <= 0:
+        w_ob = {8: 14, 16: 7, 32: 3}.get(c_ob, 4)
+    if out is None:
+        out = np.empty((n, jb_n, ho, wo, c_ob), np.float32)
+    rc = r.ref_pool_conv_direct(_fp(np.ascontiguousarray(x4)), _fp(np.ascontiguousarray(kb)),
+                                n, ci, co, hi, wi, hf, wf, s, c_ib, c_ob, w_ob, workers, _fp(out))
     if rc:
         raise ValueError("conv_direct: parameter/layout error")
     return out if xb.ndim == 5 else out[0]

@@ -13,6 +13,7 @@
 #include "dconv/shape.hpp"
 #include "dconv/tensor.hpp"
 #include "dconv/thread_pool.hpp"
+#include "oracle.h"
 
 using namespace dconv;
 
@@ -137,6 +138,29 @@ int ref_conv_reordered_batch(const float* in, const float* k, int n_img,
   } catch (const std::invalid_argument&) {
     return -1;
   }
+}
+
+// Restated Alg. 3 (oracle.c, orc_direct_job_*) scheduled on the reference's
+// own ThreadPool (thread_pool.cpp:64-97): `workers` pool threads + the
+// calling thread (the caller participates, thread_pool.cpp:84-90), i.e. the
+// reference's runtime with DCONV_THREADS = workers (thread_pool.cpp:23-30).
+// The CPU baseline the BASELINE.md plan asks for; outputs are identical to
+// orc_conv_direct (same units, same per-element order).
+static void direct_task(void* p, int chunk) {
+  orc_direct_job_unit(static_cast<const orc_direct_job*>(p), chunk);
+}
+int ref_pool_conv_direct(const float* in, const float* k, int n_img, int ci, int co,
+                         int hi, int wi, int hf, int wf, int s, int cib, int cob,
+                         int wob, int workers, float* out) {
+  static ThreadPool* pool = nullptr;
+  if (!pool) pool = new ThreadPool(workers);
+  pool->ensure(workers);
+  orc_direct_job job;
+  const int units = orc_direct_job_init(&job, in, k, n_img, ci, co, hi, wi, hf, wf, s, cib,
+                                        cob, wob, workers + 1, out);
+  if (units < 0) return -1;
+  pool->run(units, direct_task, &job);
+  return 0;
 }
 
 }  // extern "C"

@@ -79,8 +79,8 @@ _SIGS = {
     "dconv_cuda_add_blocked": (_I, [_P, _P, _P, _L, _I, _P]),
     "dconv_cuda_maxpool2x2_blocked": (_I, [_P] + [_I] * 5 + [_P, _L, _L, _L, _P]),
     "dconv_cuda_zero": (_I, [_P, _L, _P]),
-    "dconv_cuda_set_ffma_variant": (_I, [_I]),
     "dconv_cuda_launch_count": (_L, []),
+    "dconv_cuda_ffma_cluster_slots": (_I, [_I, _I, _P, _P]),
     "dconv_cuda_fp32_peak_probe": (ctypes.c_double, [_P]),
     "dconv_cuda_ffma2_pattern_probe": (ctypes.c_double, [_P]),
     "dconv_file_payload_floats": (_L, [ctypes.POINTER(FileHeader)]),

@@ -5,6 +5,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 #include "conv_kernels.h"
@@ -41,6 +44,40 @@ int check_launch(const char* kernel) {
   return DCONV_OK;
 }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+
+namespace {
+std::mutex g_dev_mu;
+std::vector<std::pair<int, int>> g_sms;                 // (device, SMs)
+std::vector<std::pair<int, const void*>> g_attr_done;   // (device, kernel)
+}  // namespace
+
+int device_sms(int dev) {
+  std::lock_guard<std::mutex> lock(g_dev_mu);
+  for (const auto& e : g_sms)
+    if (e.first == dev) return e.second;
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      sms < 1) {
+    cudaGetLastError();
+    return 148;  // not cached: retried on the next call
+  }
+  g_sms.emplace_back(dev, sms);
+  return sms;
+}
+
+bool first_use_on_device(const void* kernel, int dev) {
+  std::lock_guard<std::mutex> lock(g_dev_mu);
+  for (const auto& e : g_attr_done)
+    if (e.first == dev && e.second == kernel) return false;
+  g_attr_done.emplace_back(dev, kernel);
+  return true;
+}
 }  // namespace dconv_host
 
 using dconv_host::set_error;
@@ -482,10 +519,9 @@ int dconv_cuda_zero(float* x, int64_t count, void* stream) {
   return DCONV_OK;
 }
 
-int dconv_cuda_set_ffma_variant(int variant) {
-  if (variant < -1 || variant > 2) return set_error(DCONV_EPARAM, "variant %d", variant);
-  dconv_dev::ffma_variant_override = variant;
-  return DCONV_OK;
+int dconv_cuda_ffma_cluster_slots(int tile_variant, int ks, int* cached, int* fresh) {
+  if (!cached || !fresh) return set_error(DCONV_EPARAM, "null output");
+  return dconv_dev::ffma_cluster_slots_probe(tile_variant, ks, cached, fresh);
 }
 
 int64_t dconv_cuda_launch_count(void) {

@@ -202,4 +202,10 @@ bool pdl_enabled();  // DCONV_NO_PDL unset
 int set_error(int code, const char* fmt, ...);
 int check_launch(const char* kernel);
 void count_launch();
+// current device and its SM count (cached per device)
+int current_device();
+int device_sms(int dev);
+// true exactly once per (kernel, device): the caller then sets that kernel's
+// function attributes on the current device (attributes are per device)
+bool first_use_on_device(const void* kernel, int dev);
 }  // namespace dconv_host

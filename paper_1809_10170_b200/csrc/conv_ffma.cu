@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -1015,31 +1016,48 @@ size_t configure(FfmaParams& p, int ks, bool fine) {
   return (size_t)p.NS * p.stage_floats * 4 + (ks > 1 ? red_bytes : 0) + bar_bytes;
 }
 
-// co-resident clusters of ks CTAs at ~200 KB smem (GPC-limited); cached
+// co-resident clusters of ks CTAs at ~200 KB smem (GPC-limited).  Cached per
+// (device, kernel instantiation, ks): every conv_ffma_kernel<...> has its own
+// register / smem footprint, so the occupancy answer of one must not be
+// reused for another.
+int device_index() { return dconv_host::current_device(); }
+
 template <class K>
 int cluster_slots(K kernel, int ks, int sms, int threads) {
-  static int cache[kMaxKs + 1] = {0};
   if (ks == 1) return sms;
-  if (!cache[ks]) {
-    cudaLaunchConfig_t cfg{};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = ks;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(ks * 64);
-    cfg.blockDim = dim3(threads);
-    cfg.dynamicSmemBytes = 200 * 1024;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess || n < 1) {
-      cudaGetLastError();
-      n = -1;
-    }
-    cache[ks] = n;
+  struct Entry {
+    int dev;
+    const void* fn;
+    int ks, n;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;
+  const int dev = device_index();
+  const void* fn = reinterpret_cast<const void*>(kernel);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    for (const Entry& e : cache)
+      if (e.dev == dev && e.fn == fn && e.ks == ks) return e.n;
   }
-  return cache[ks];
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = ks;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(ks * 64);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = 200 * 1024;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = -1;
+  }
+  std::lock_guard<std::mutex> lock(mu);
+  cache.push_back({dev, fn, ks, n});
+  return n;
 }
 
 template <class K>
@@ -1124,19 +1142,15 @@ template <int BM, int BN, int WF, int NW, int TPX, int TCO>
 int launch_variant(FfmaParams p, cudaStream_t stream) {
   constexpr int threads = (NW + 8) * 32;
   constexpr int CG = BN / 8;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int dev = device_index();
+  const int sms = dconv_host::device_sms(dev);
   const int co_groups = (p.jb_count + CG - 1) / CG;
   auto kernel = conv_ffma_kernel<BM, BN, WF, NW, TPX, TCO>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  // kernel attributes are per device: set once for each device this
+  // instantiation is launched on
+  if (dconv_host::first_use_on_device(reinterpret_cast<const void*>(kernel), dev)) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr_set = true;
   }
   // the DSMEM split-K reduction: 8 warps, 8 channels x 4 or 8 pixels/thread
   const bool no_split = knobs().no_splitk || NW != 8 || (TPX != 8 && TPX != 4) ||
@@ -1229,9 +1243,55 @@ int launch_wf(const FfmaParams& p, cudaStream_t stream) {
   }
 }
 
+// fresh (uncached) occupancy query, for the cache check below
+template <class K>
+int cluster_slots_fresh(K kernel, int ks, int threads) {
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = ks;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(ks * 64);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = 200 * 1024;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = -1;
+  }
+  return n;
+}
+
+template <int BM, int BN, int NW, int TPX, int TCO>
+int probe_slots(int ks, int* cached, int* fresh) {
+  auto kernel = conv_ffma_kernel<BM, BN, 3, NW, TPX, TCO>;
+  const int dev = device_index();
+  if (dconv_host::first_use_on_device(reinterpret_cast<const void*>(kernel), dev)) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  }
+  constexpr int threads = (NW + 8) * 32;
+  *cached = cluster_slots(kernel, ks, dconv_host::device_sms(dev), threads);
+  *fresh = cluster_slots_fresh(kernel, ks, threads);
+  return DCONV_OK;
+}
+
 }  // namespace
 
-int ffma_variant_override = -1;  // test/tuning hook (dconv_cuda_set_ffma_variant)
+// Test hook: the cached co-resident cluster count of one CTA-tile
+// instantiation (3x3 filters) next to a fresh occupancy query.
+int ffma_cluster_slots_probe(int tile_variant, int ks, int* cached, int* fresh) {
+  if (ks < 2 || ks > kMaxKs) return dconv_host::set_error(DCONV_EPARAM, "ks %d", ks);
+  switch (tile_variant) {
+    case 1: return probe_slots<128, 128, 8, 8, 8>(ks, cached, fresh);
+    case 2: return probe_slots<256, 64, 8, 8, 8>(ks, cached, fresh);
+    case 3: return probe_slots<128, 64, 8, 4, 8>(ks, cached, fresh);
+    default: return dconv_host::set_error(DCONV_EPARAM, "tile_variant %d", tile_variant);
+  }
+}
 
 int launch_conv_ffma(const FfmaParams& p0, cudaStream_t stream) {
   FfmaParams p = p0;
@@ -1249,7 +1309,7 @@ int launch_conv_ffma(const FfmaParams& p0, cudaStream_t stream) {
                     : 0u;
   static const bool no_skip_prefetch = getenv("DCONV_NO_SKIP_PREFETCH") != nullptr;
   p.skip_prefetch = (p.epi & DCONV_EPI_ADD) && !no_skip_prefetch;
-  int v = p.variant >= 0 ? p.variant : ffma_variant_override;
+  int v = p.variant;  // desc.tile_variant - 1; -1 = selector
   // measured (tools/sweep_variants.py): 256 px x 64 ch wins on every 3x3 /
   // 5x5 layer of the configs; 1x1 layers with >= 128 output channels
   // (little reuse per staged pixel) prefer 128 px x 128 ch

@@ -209,14 +209,10 @@ int launch_first_px(const GenericParams& p, const FirstTile& t, cudaStream_t str
   const size_t patch = (((size_t)p.c_i * t.PH * t.PWs + 3) & ~size_t(3)) * 4;
   const size_t smem = w_bytes + 2 * patch;  // weights + double-buffered patch
   auto kernel = conv_first_kernel<S, WF, PX>;
-  static int per_sm = 0, sms = 0;
-  if (!per_sm) {
+  const int dev = dconv_host::current_device();
+  const int sms = dconv_host::device_sms(dev);
+  if (dconv_host::first_use_on_device(reinterpret_cast<const void*>(kernel), dev))
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    per_sm = -1;
-  }
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, smem) != cudaSuccess ||
       occ < 1) {
@@ -248,12 +244,7 @@ int launch_first_px(const GenericParams& p, const FirstTile& t, cudaStream_t str
 
 template <int S, int WF>
 int launch_first(const GenericParams& p, cudaStream_t stream) {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = dconv_host::device_sms(dconv_host::current_device());
   const size_t w_bytes = (size_t)p.h_f * WF * p.c_i * kCG * 8 * 4;
   const size_t budget = 220 * 1024;
   const int co_groups = (p.jb_count + kCG - 1) / kCG;

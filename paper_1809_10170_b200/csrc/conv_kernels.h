@@ -44,9 +44,8 @@ struct FfmaParams {
   long long* dbg;              // DCONV_FFMA_PROFILE: per-CTA phase clocks (else null)
 };
 
-extern int ffma_variant_override;  // -1 = heuristic (dconv_cuda_set_ffma_variant)
-
 int launch_conv_ffma(const FfmaParams& p, cudaStream_t stream);
+int ffma_cluster_slots_probe(int tile_variant, int ks, int* cached, int* fresh);
 
 // tcgen05/TMEM TF32 variant (conv_tf32.cu): weights prepared once into the
 // UMMA K-major layout by launch_prepare_tf32.  A k x k stride-s layer is

@@ -360,12 +360,7 @@ int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t
   // balance (a ragged last wave costs a full round) / load-bound cost; ties
   // go to the larger MT.
   {
-    static int sms = 0;
-    if (!sms) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = tf32::sm_count();
     const int strips = (p.w_o + kTW - 1) / kTW;
     // time = rounds x per-unit cycles; a unit streams ib_n input blocks, each
     // max(MMA time, load time): 9*MT MMAs of ~78 cycles (N <= 128) against its
@@ -374,6 +369,8 @@ int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t
     double best = -1;
     for (int mt = kMaxMT; mt >= 1; --mt) {
       if (mt * p.N > 512) continue;  // accumulators: MT x N TMEM columns
+      // TMA box rows of a strided (space-to-depth) read: (PH) x s <= 256
+      if (mt > 1 && (mt * kTileRows - 1 + p.h_f) * p.s2d > 256) continue;
       // small maps stack images along the tile rows (below)
       const int sp = p.h_o + p.h_f - 1;
       const int st = !(p.epi & DCONV_EPI_MAXPOOL) && p.h_o + sp <= mt * kTileRows
@@ -449,18 +446,13 @@ int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t
                            : encode_input_map(&map, view, p.PW, p.PH, p.G))
     return rc;
 
-  static int sms = 0;
-  static bool attr = false;
-  if (!attr) {
+  const int dev = dconv_host::current_device();
+  const int sms = dconv_host::device_sms(dev);
+  if (dconv_host::first_use_on_device(reinterpret_cast<const void*>(conv_tf32_kernel<0, 0>), dev))
     for (auto k : {conv_tf32_kernel<0, 0>, conv_tf32_kernel<3, 1>, conv_tf32_kernel<3, 2>,
                    conv_tf32_kernel<3, 3>, conv_tf32_kernel<3, 4>, conv_tf32_kernel<1, 1>,
                    conv_tf32_kernel<1, 2>, conv_tf32_kernel<1, 3>, conv_tf32_kernel<1, 4>})
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    attr = true;
-  }
   const size_t smem = (size_t)p.NS * stage_bytes + bar_bytes;
   const int grid = std::min(p.units, sms);
   static const bool dbg = getenv("DCONV_DEBUG") != nullptr;

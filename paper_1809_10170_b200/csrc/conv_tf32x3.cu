@@ -457,8 +457,10 @@ X3Kernel pick_x3_kernel(const Tf32Params& p) {
 }
 
 void set_x3_attrs() {
-  static bool done = false;
-  if (done) return;
+  // attributes are per device: once for each device the kernels run on
+  if (!dconv_host::first_use_on_device(reinterpret_cast<const void*>(&set_x3_attrs),
+                                       dconv_host::current_device()))
+    return;
   for (bool da : {false, true})
     for (int mt : {1, 2, 4})
       for (int cols : {64, 128}) {
@@ -468,7 +470,6 @@ void set_x3_attrs() {
                            pick_wf<0>(mt, cols, da)})
           cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       }
-  done = true;
 }
 
 // separate correction accumulator for N = 64 (DCONV_X3_NO_DA: off); the
@@ -542,6 +543,8 @@ int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream
     for (int mt = kMaxMT; mt >= 1; --mt) {
       const int cols = mt * p.N / 2;
       if (da ? cols != 64 : (cols != 64 && cols != 128)) continue;
+      // TMA box rows of a strided (space-to-depth) read: (PH) x s <= 256
+      if ((mt * kTileRows - 1 + p.h_f) * p.s2d > 256) continue;
       const int st = stack_for(mt, rows_for(p.h_f));
       const int rg = st > 1 ? 1 : (p.h_o + mt * kTileRows - 1) / (mt * kTileRows);
       const int64_t units =
@@ -564,7 +567,9 @@ int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream
         p.MT = mt;
       }
     }
-    if (best < 0) return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_tf32x3: N = %d", p.N);
+    if (best < 0)
+      return dconv_host::set_error(DCONV_EUNSUPPORTED,
+                                   "conv_tf32x3: no M-tile count for N = %d, stride %d", p.N, p.s2d);
     static const char* force_mt = getenv("DCONV_TF32_MT");
     if (force_mt) {
       const int mt = atoi(force_mt);

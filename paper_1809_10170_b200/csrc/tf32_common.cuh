@@ -204,15 +204,16 @@ __device__ __forceinline__ void emit32(const Tf32Params& p, float (&v)[32], int 
 }
 
 inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
+  // driver entry point, resolved once (thread-safe static initialisation)
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
             cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    return PFN_cuTensorMapEncodeTiled_v12000(nullptr);
+  }();
   return fn;
 }
 
@@ -250,6 +251,11 @@ inline int prepare_view(FfmaParams& f, InView& v, const char* who) {
     f.s = 1;
   } else if (f.s > 1) {
     const int s = f.s;
+    // the TMA traverses the original map with element strides s: the tensor
+    // map encoder allows strides of at most 8
+    if (s > 8)
+      return dconv_host::set_error(DCONV_EUNSUPPORTED,
+                                   "%s: k x k stride %d > 8 (TMA element stride limit)", who, s);
     v.s2d = s;
     f.ib_n *= s * s;
     f.h_f = (f.h_f + s - 1) / s;
@@ -332,15 +338,7 @@ inline uint32_t tf32_idesc(int N) {
          ((uint32_t)(128 >> 4) << 24);
 }
 
-inline int sm_count() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return sms;
-}
+inline int sm_count() { return dconv_host::device_sms(dconv_host::current_device()); }
 
 }  // namespace tf32
 }  // namespace dconv_dev

@@ -210,15 +210,32 @@ def make_desc(shape: ConvShape, n: int, c_ib: int, c_ob: int,
     return d
 
 
+def _check_map(m: BlockedFeatureMap, shape: ConvShape, c_b: int, n: int, what: str) -> None:
+    """A caller-supplied output / skip map must have the output geometry (the
+    C++ overload's checks, dropin.cpp): otherwise the kernel would write or
+    read past the end of its buffer."""
+    if (m.channels, m.height, m.width) != (shape.c_o, shape.h_o, shape.w_o):
+        raise ValueError(f"conv: {what} dims do not match shape")
+    if m.c_b != c_b:
+        raise ValueError(f"conv_direct: layout error ({what} c_b != c_ob)")
+    if m.n != n:
+        raise ValueError(f"conv: {what} batch does not match input")
+    need = n * (round_up(shape.c_o, c_b) // c_b) * shape.h_o * shape.w_o * c_b
+    if m.data.numel() < need or not m.data.is_contiguous():
+        raise ValueError(f"conv: {what} buffer too small or not contiguous")
+
+
 def conv_direct(inp: BlockedFeatureMap, kernel: BlockedKernel, shape: ConvShape,
                 params: BlockingParams, workers: int = 0, *,
                 relu: bool = False, skip: Optional[BlockedFeatureMap] = None,
                 out: Optional[BlockedFeatureMap] = None,
-                algo: int = _abi.ALGO_AUTO, stream=None) -> BlockedFeatureMap:
+                algo: int = _abi.ALGO_AUTO, tile_variant: int = 0,
+                stream=None) -> BlockedFeatureMap:
     """conv_direct: blocked in (c_b == c_ib) x blocked
     kernel (c_ob, c_ib) -> blocked out (c_b == c_ob).  ``workers`` is the
     reference's CPU thread count; on the GPU the grid replaces the pool and
-    the result is bitwise independent of it."""
+    the result is bitwise independent of it.  ``tile_variant``
+    picks the FFMA CTA tile (dconv_conv_desc.tile_variant; 0 = selector)."""
     if inp.c_b != params.c_ib or kernel.c_ib != params.c_ib:
         raise ValueError("conv_direct: layout error (input c_b / kernel c_ib "
                          "must equal params.c_ib)")
@@ -229,8 +246,13 @@ def conv_direct(inp: BlockedFeatureMap, kernel: BlockedKernel, shape: ConvShape,
     if (kernel.c_i, kernel.c_o, kernel.h_f, kernel.w_f) != (
             shape.c_i, shape.c_o, shape.h_f, shape.w_f):
         raise ValueError("conv: kernel dims do not match shape")
+    if skip is not None:
+        _check_map(skip, shape, params.c_ob, inp.n, "skip")
+    if out is not None:
+        _check_map(out, shape, params.c_ob, inp.n, "output")
     epi = (_abi.EPI_RELU if relu else 0) | (_abi.EPI_ADD if skip is not None else 0)
     d = make_desc(shape, inp.n, params.c_ib, params.c_ob, epi, algo)
+    d.tile_variant = tile_variant
     if out is None:
         out = BlockedFeatureMap(shape.c_o, shape.h_o, shape.w_o, params.c_ob,
                                 n=inp.n, device=inp.data.device,
@@ -272,15 +294,21 @@ class PreparedKernel:
 def conv_direct_tc(inp: BlockedFeatureMap, kernel: PreparedKernel, *, relu: bool = False,
                    skip: Optional[BlockedFeatureMap] = None,
                    out: Optional[BlockedFeatureMap] = None, stream=None) -> BlockedFeatureMap:
-    """conv_direct on the tcgen05 tensor cores (c_b = 8; stride 1, or a 1x1 of
-    any stride): the split-TF32 kernel for a ``PreparedKernel(split=True)``
-    (fp32 tolerance), else one TF32 pass (looser tolerance)."""
+    """conv_direct on the tcgen05 tensor cores (c_b = 8; any k x k stride-s
+    layer with s <= 8 -- stride-s layers are computed over the space-to-depth
+    view of the input, read in place): the split-TF32 kernel for a
+    ``PreparedKernel(split=True)`` (fp32 tolerance), else one TF32 pass
+    (looser tolerance)."""
     import ctypes
     shape = kernel.shape
     if inp.c_b != 8:
         raise ValueError("conv_direct: layout error (tensor-core path needs c_b = 8)")
     if (inp.channels, inp.height, inp.width) != (shape.c_i, shape.h_i, shape.w_i):
         raise ValueError("conv: input dims do not match shape")
+    if skip is not None:
+        _check_map(skip, shape, 8, inp.n, "skip")
+    if out is not None:
+        _check_map(out, shape, 8, inp.n, "output")
     epi = (_abi.EPI_RELU if relu else 0) | (_abi.EPI_ADD if skip is not None else 0)
     d = make_desc(shape, inp.n, 8, 8, epi,
                   _abi.ALGO_TF32X3 if kernel.split else _abi.ALGO_TF32)

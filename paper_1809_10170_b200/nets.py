@@ -180,13 +180,21 @@ class Act:
     def interior(self) -> torch.Tensor:
         return self.buf[:, :, self.halo:self.halo + self.h, self.halo:self.halo + self.w, :]
 
-    def block_view(self, b0: int) -> "Act":
-        """The same map seen from output block b0 on (a rank's C_o slice
-        inside the full buffer): base() moves, strides stay."""
+    def block_view(self, b0: int, count: Optional[int] = None) -> "Act":
+        """The same map seen from output block b0 on (a rank's C_o slice of
+        ``count`` blocks inside the full buffer): base() moves, strides stay,
+        and the view's channel count covers only its blocks."""
         import copy
         v = copy.copy(self)
         v.off = self.off + b0 * self.blk
+        nb = nblk(self.c) - b0 if count is None else count
+        v.c = max(0, min(self.c - b0 * CB, nb * CB))
         return v
+
+    def clone_zeros(self) -> "Act":
+        """Same geometry, fresh zeroed buffer (halo ring and padding 0)."""
+        return Act(self.n, self.c, self.h, self.w, halo=self.halo, pad_hi_only=self.pad_hi_only,
+                   device=self.buf.device)
 
 
 def conv(l: Layer, n: int, x: "Act|torch.Tensor", w: torch.Tensor, out: Act,
@@ -238,8 +246,9 @@ def conv(l: Layer, n: int, x: "Act|torch.Tensor", w: torch.Tensor, out: Act,
 def conv_tf32(l: Layer, n: int, x: "Act", wprep: torch.Tensor, out: Act,
               epilogue: int = 0, skip: Optional[Act] = None, stream=None,
               in_view: Optional[Tuple[int, int, int, int]] = None, x3: bool = False) -> None:
-    """tcgen05/TMEM TF32 launch of a blocked layer (stride 1, or a 1x1 of any
-    stride; weights prepared by prepare_tf32).  ``x3``: the split-TF32 kernel
+    """tcgen05/TMEM TF32 launch of a blocked layer (any k x k stride-s layer,
+    s <= 8: strided layers run over the space-to-depth view of the input,
+    read in place; weights prepared by prepare_tf32).  ``x3``: the split-TF32 kernel
     (fp32 tolerance; weights prepared with ``x3=True``)."""
     d = _desc(l, n, epilogue)
     d.out_img_stride, d.out_blk_stride, d.out_row_stride = out.img, out.blk, out.row
@@ -327,7 +336,14 @@ class Plan:
     algo: str = "ffma"   # "tf32" / "tf32x3": blocked layers on the tcgen05 path
     # C_o-shard exchange: "nccl" = slice + all-gather; "peer" = the conv/pool
     # epilogue stores into every rank's full map (symmetric memory over
-    # NVLink) followed by a device barrier -- no collective on the data path
+    # NVLink) followed by a device barrier -- no collective on the data path.
+    # Emulation of all `world` ranks on one device (tests, bench parity; the
+    # ranks' launches run one after another, nothing waits on another rank):
+    # "emulate" = every rank's launches of a layer (its C_o slice, the same
+    # kernel configuration a real rank runs) into one full map -- what the
+    # all-gather assembles; "emulate_peer" = every rank keeps its own full
+    # map and its conv / pool epilogues also store into the other ranks'
+    # copies (peer stores into local buffers, the fused-gather addressing).
     gather_mode: str = "nccl"
     weights: Dict[str, torch.Tensor] = field(default_factory=dict)
     tiles: Dict[str, int] = field(default_factory=dict)  # autotuned FFMA CTA tile per layer
@@ -475,13 +491,15 @@ class Plan:
         rank, world, _ = self.shard
         if self.n != 1:
             raise ValueError("C_o sharding is the batch-1 mode")
+        if self.gather_mode in ("emulate", "emulate_peer"):
+            return self._conv_emulated(l, x, y, epilogue, skip, in_view, kind)
         b0, cnt = block_range(nblk(l.c_o), world, rank)
         flops = l.flops * min(cnt * CB, l.c_o - b0 * CB) // l.c_o
         if self.gather_mode == "peer" and gather:
             # fused gather: this rank's blocks go straight into every rank's
             # full map (local store + NVLink peer stores), then one barrier
             self._adopt_symmetric(y)
-            yv, peers = y.block_view(b0), self._peer_ptrs(y, b0)
+            yv, peers = y.block_view(b0, cnt), self._peer_ptrs(y, b0)
             self.steps.append(Step(lambda st: conv(l, self.n, x, w, yv, epilogue, skip, st,
                                                    in_view, (b0, cnt),
                                                    tile_variant=self.tiles.get(l.name, 0),
@@ -496,6 +514,39 @@ class Plan:
         if gather:
             self._gather(l.name, y, ys)
         return ys
+
+    @staticmethod
+    def _copies(a: Act, world: int) -> List[Act]:
+        """emulate_peer: rank r's own full copy of map ``a`` (copy 0 is ``a``)."""
+        if getattr(a, "copies", None) is None:
+            a.copies = [a] + [a.clone_zeros() for _ in range(world - 1)]
+        return a.copies
+
+    def _conv_emulated(self, l: Layer, x, y: Act, epilogue: int, skip: Optional[Act],
+                       in_view, kind: str) -> Act:
+        """Every rank's launch of layer ``l`` on this device, rank by rank."""
+        from .shard import block_range
+        _, world, _ = self.shard
+        w = self.weights[l.name]
+        peer_mode = self.gather_mode == "emulate_peer"
+        ys = self._copies(y, world) if peer_mode else [y] * world
+        xs = (self._copies(x, world) if peer_mode and isinstance(x, Act) else [x] * world)
+        sks = (self._copies(skip, world) if peer_mode and skip is not None else [skip] * world)
+        for r in range(world):
+            b0, cnt = block_range(nblk(l.c_o), world, r)
+            flops = l.flops * min(cnt * CB, l.c_o - b0 * CB) // l.c_o
+            yv = ys[r].block_view(b0, cnt)
+            peers = [ys[q].base() + 4 * b0 * ys[q].blk for q in range(world) if q != r] \
+                if peer_mode else None
+            iv = in_view
+            if in_view is not None and xs[r] is not x:
+                iv = (xs[r].buf.data_ptr() + (in_view[0] - x.buf.data_ptr()),) + tuple(in_view[1:])
+            self.steps.append(Step(
+                lambda st, xr=xs[r], yv=yv, skr=sks[r], iv=iv, b0=b0, cnt=cnt, peers=peers:
+                conv(l, self.n, xr, w, yv, epilogue, skr, st, iv, (b0, cnt),
+                     tile_variant=self.tiles.get(l.name, 0), peers=peers),
+                f"{l.name}@r{r}", kind, flops, l))
+        return y
 
     def _few_units(self, l: Layer, epilogue: int) -> bool:
         """Split-TF32 plans run a layer on the FFMA kernel (same fp32
@@ -544,16 +595,33 @@ class Plan:
 
     def pool_into(self, name: str, src_local: Act, z: Act) -> None:
         """2x2/s2 max-pool of this rank's result into z (gathered if sharded)."""
-        if self.shard is None:
+        if self.shard is None or self.gather_mode == "emulate":
+            # (emulate: src_local is the full map every rank's conv wrote;
+            # pooling it equals pooling the slices -- max is exact)
             self.steps.append(Step(lambda st: maxpool_into(src_local, z, st), name, "pool"))
+            return
+        if self.gather_mode == "emulate_peer":
+            from .shard import block_range
+            _, world, _ = self.shard
+            srcs, zs = self._copies(src_local, world), self._copies(z, world)
+            for r in range(world):
+                b0, cnt = block_range(nblk(z.c), world, r)
+                src, zv = srcs[r].block_view(b0, cnt), zs[r].block_view(b0, cnt)
+                peers = [zs[q].base() + 4 * b0 * zs[q].blk for q in range(world) if q != r]
+
+                def pool_all(st, src=src, zv=zv, peers=peers):
+                    maxpool_into(src, zv, st)
+                    for pp in peers:
+                        maxpool_into(src, zv, st, out_ptr=pp)
+                self.steps.append(Step(pool_all, f"{name}@r{r}", "pool"))
             return
         if self.gather_mode == "peer":
             # pool this rank's slice into every rank's z (local + peers)
             from .shard import block_range
             rank, world, _ = self.shard
-            b0, _cnt = block_range(nblk(z.c), world, rank)
+            b0, cnt = block_range(nblk(z.c), world, rank)
             self._adopt_symmetric(z)
-            zv, peers = z.block_view(b0), self._peer_ptrs(z, b0)
+            zv, peers = z.block_view(b0, cnt), self._peer_ptrs(z, b0)
 
             def pool_all(st, src=src_local, zv=zv, peers=peers):
                 maxpool_into(src, zv, st)
@@ -583,7 +651,7 @@ def build_plan(config: str, n: int, seed: int = 1809, device="cuda",
     exchange ``gather_mode`` "nccl" (all-gather) or "peer" (fused peer stores
     + barrier); ``algo`` = "tf32" runs the stride-1 blocked layers on the
     tcgen05 TF32 kernel."""
-    if gather_mode not in ("nccl", "peer"):
+    if gather_mode not in ("nccl", "peer", "emulate", "emulate_peer"):
         raise ValueError(f"gather_mode {gather_mode!r}")
     layers = CONFIGS[config]
     p = Plan(config, n, list(layers), shard=shard, algo=algo, gather_mode=gather_mode)

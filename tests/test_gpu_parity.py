@@ -46,7 +46,7 @@ from paper_1809_10170_b200 import dconv as D  # noqa: E402
 from paper_1809_10170_b200 import _abi, nets  # noqa: E402
 
 
-def run_conv(x, k, s, c_ib, c_ob, algo=_abi.ALGO_AUTO, relu=False, skip=None):
+def run_conv(x, k, s, c_ib, c_ob, algo=_abi.ALGO_AUTO, relu=False, skip=None, tile_variant=0):
     """dense numpy x [c][h][w], k [ci][co][hf][wf] -> blocked numpy output."""
     ci, hi, wi = x.shape
     _, co, hf, wf = k.shape
@@ -57,7 +57,7 @@ def run_conv(x, k, s, c_ib, c_ob, algo=_abi.ALGO_AUTO, relu=False, skip=None):
     if skip is not None:
         sk = D.BlockedFeatureMap(co, shape.h_o, shape.w_o, c_ob, data=dev(skip[None]))
     y = D.conv_direct(xb, kb, shape, D.BlockingParams(c_ob, 1, c_ib), relu=relu, skip=sk,
-                      algo=algo)
+                      algo=algo, tile_variant=tile_variant)
     return host(y.data)[0]
 
 
@@ -333,50 +333,40 @@ def test_first_layer_reader_variants(s, f, ci, co):
 def test_ffma_tile_variants(variant):
     """The FFMA CTA tiles (128 px x 128 ch, 256 px x 64 ch, 128 px x 64 ch) on ragged shapes,
     strides, filter widths 1/3/5/7 (templated and runtime), and a K = 4608
-    layer where the TMEM two-level sum matters."""
-    lib = _abi.lib()
-    _abi.check(lib.dconv_cuda_set_ffma_variant(variant))
-    try:
-        cases = [(64, 64, 58, 58, 3, 1), (24, 40, 17, 23, 5, 1), (16, 136, 19, 21, 7, 2),
-                 (96, 72, 13, 31, 1, 2), (512, 128, 16, 16, 3, 1), (200, 16, 9, 9, 3, 2)]
-        for t, (ci, co, hi, wi, f, s) in enumerate(cases):
-            x = po.uniform((ci, hi, wi), 7000 + t, variant)
-            k = po.uniform((ci, co, f, f), 7000 + t, 10 + variant)
-            want = po.pack_feature_map(po.conv_oracle64(x, k, s), 8)
-            assert_tol(run_conv(x, k, s, 8, 8, algo=_abi.ALGO_FFMA), want,
-                       f"variant {variant} case {t}")
-    finally:
-        lib.dconv_cuda_set_ffma_variant(-1)
+    layer where the TMEM two-level sum matters (desc.tile_variant)."""
+    cases = [(64, 64, 58, 58, 3, 1), (24, 40, 17, 23, 5, 1), (16, 136, 19, 21, 7, 2),
+             (96, 72, 13, 31, 1, 2), (512, 128, 16, 16, 3, 1), (200, 16, 9, 9, 3, 2)]
+    for t, (ci, co, hi, wi, f, s) in enumerate(cases):
+        x = po.uniform((ci, hi, wi), 7000 + t, variant)
+        k = po.uniform((ci, co, f, f), 7000 + t, 10 + variant)
+        want = po.pack_feature_map(po.conv_oracle64(x, k, s), 8)
+        assert_tol(run_conv(x, k, s, 8, 8, algo=_abi.ALGO_FFMA, tile_variant=variant + 1), want,
+                   f"variant {variant} case {t}")
 
 
 @pytest.mark.parametrize("variant", [0, 1, 2])
 def test_batched_stacked_tiles(variant):
     """Pixel tiles over the batch-stacked output span several images (maps of
     height 1..9 with tiles of up to 64 rows): every image checked."""
-    lib = _abi.lib()
-    _abi.check(lib.dconv_cuda_set_ffma_variant(variant))
-    try:
-        rng = np.random.default_rng(900 + variant)
-        for t in range(14):
-            n = int(rng.integers(2, 7))
-            f = int(rng.choice([1, 3, 5]))
-            s = int(rng.choice([1, 2]))
-            ho, wo = int(rng.integers(1, 10)), int(rng.integers(1, 16))
-            ci, co = int(rng.integers(1, 40)), int(rng.integers(1, 150))
-            hi, wi = (ho - 1) * s + f, (wo - 1) * s + f
-            x = po.uniform((n, ci, hi, wi), 950 + t, variant)
-            k = po.uniform((ci, co, f, f), 960 + t, variant)
-            l = nets.Layer("b", ci, co, hi, wi, f, f, s)
-            a = nets.Act(n, ci, hi, wi)
-            a.buf.copy_(dev(np.stack([po.pack_feature_map(x[i], 8) for i in range(n)])))
-            y = nets.Act(n, co, ho, wo)
-            nets.conv(l, n, a, nets.pack_weights(dev(k), False), y)
-            got = host(y.buf)
-            for i in range(n):
-                want = po.pack_feature_map(po.conv_oracle64(x[i], k, s), 8)
-                assert_tol(got[i], want, f"v{variant} case {t} img {i} ({n},{ci},{co},{hi},{wi},{f},{s})")
-    finally:
-        lib.dconv_cuda_set_ffma_variant(-1)
+    rng = np.random.default_rng(900 + variant)
+    for t in range(14):
+        n = int(rng.integers(2, 7))
+        f = int(rng.choice([1, 3, 5]))
+        s = int(rng.choice([1, 2]))
+        ho, wo = int(rng.integers(1, 10)), int(rng.integers(1, 16))
+        ci, co = int(rng.integers(1, 40)), int(rng.integers(1, 150))
+        hi, wi = (ho - 1) * s + f, (wo - 1) * s + f
+        x = po.uniform((n, ci, hi, wi), 950 + t, variant)
+        k = po.uniform((ci, co, f, f), 960 + t, variant)
+        l = nets.Layer("b", ci, co, hi, wi, f, f, s)
+        a = nets.Act(n, ci, hi, wi)
+        a.buf.copy_(dev(np.stack([po.pack_feature_map(x[i], 8) for i in range(n)])))
+        y = nets.Act(n, co, ho, wo)
+        nets.conv(l, n, a, nets.pack_weights(dev(k), False), y, tile_variant=variant + 1)
+        got = host(y.buf)
+        for i in range(n):
+            want = po.pack_feature_map(po.conv_oracle64(x[i], k, s), 8)
+            assert_tol(got[i], want, f"v{variant} case {t} img {i} ({n},{ci},{co},{hi},{wi},{f},{s})")
 
 
 # ------------------------------------------------ chains (wiring, teacher-forced)
@@ -545,36 +535,51 @@ def test_co_shard_peer_gather_plan_world1():
         dist.destroy_process_group()
 
 
+def test_cluster_slots_cached_per_kernel():
+    """The launcher caches co-resident cluster counts per (device, kernel
+    instantiation, ks): driving all three CTA tiles in one process gives each
+    its own answer, equal to a fresh occupancy query of that kernel; then a
+    batch-1 split-K layer runs correctly on each tile in turn."""
+    lib = _abi.lib()
+    for ks in (2, 4, 8, 16):
+        for variant in (1, 2, 3, 1):
+            cached, fresh = ctypes.c_int(0), ctypes.c_int(0)
+            _abi.check(lib.dconv_cuda_ffma_cluster_slots(variant, ks, ctypes.byref(cached),
+                                                         ctypes.byref(fresh)))
+            assert cached.value == fresh.value, (variant, ks, cached.value, fresh.value)
+    x = po.uniform((64, 30, 30), 4242, 0)
+    k = po.uniform((64, 64, 3, 3), 4242, 1)
+    want = po.pack_feature_map(po.conv_oracle64(x, k, 1), 8)
+    for variant in (1, 2, 3, 2):
+        assert_tol(run_conv(x, k, 1, 8, 8, algo=_abi.ALGO_FFMA, tile_variant=variant), want,
+                   f"tile {variant}")
+
+
 @pytest.mark.parametrize("ks", [2, 3, 4, 6, 8, 12, 16])
 def test_cluster_split_k(ks, monkeypatch):
     """Split-K over a thread-block cluster with the DSMEM reduction, forced
     to ks CTAs per unit: several units per cluster (barrier phases), ragged
     stage splits, every CTA tile; bitwise repeatable."""
     monkeypatch.setenv("DCONV_KSPLIT", str(ks))
-    lib = _abi.lib()
-    try:
-        cases = [(64, 64, 58, 58, 3, 1, 1), (40, 136, 17, 23, 3, 1, 3), (96, 72, 13, 31, 1, 2, 2),
-                 (200, 24, 9, 9, 3, 2, 4), (24, 40, 17, 23, 5, 1, 2), (512, 128, 9, 9, 3, 1, 2)]
-        for variant in (0, 1, 2):
-            _abi.check(lib.dconv_cuda_set_ffma_variant(variant))
-            for t, (ci, co, hi, wi, f, s, n) in enumerate(cases):
-                x = po.uniform((n, ci, hi, wi), 8000 + t, ks)
-                k = po.uniform((ci, co, f, f), 8100 + t, ks)
-                l = nets.Layer("k", ci, co, hi, wi, f, f, s)
-                a = nets.Act(n, ci, hi, wi)
-                a.buf.copy_(dev(np.stack([po.pack_feature_map(x[i], 8) for i in range(n)])))
-                wb = nets.pack_weights(dev(k), False)
-                y = nets.Act(n, co, l.h_o, l.w_o)
-                nets.conv(l, n, a, wb, y, epilogue=_abi.EPI_RELU)
-                got = host(y.buf)
-                y2 = nets.Act(n, co, l.h_o, l.w_o)
-                nets.conv(l, n, a, wb, y2, epilogue=_abi.EPI_RELU)
-                assert np.array_equal(got, host(y2.buf)), "split-K not bitwise repeatable"
-                for i in range(n):
-                    want = np.maximum(po.pack_feature_map(po.conv_oracle64(x[i], k, s), 8), 0)
-                    assert_tol(got[i], want, f"ks={ks} v{variant} case {t} img {i}")
-    finally:
-        lib.dconv_cuda_set_ffma_variant(-1)
+    cases = [(64, 64, 58, 58, 3, 1, 1), (40, 136, 17, 23, 3, 1, 3), (96, 72, 13, 31, 1, 2, 2),
+             (200, 24, 9, 9, 3, 2, 4), (24, 40, 17, 23, 5, 1, 2), (512, 128, 9, 9, 3, 1, 2)]
+    for variant in (0, 1, 2):
+        for t, (ci, co, hi, wi, f, s, n) in enumerate(cases):
+            x = po.uniform((n, ci, hi, wi), 8000 + t, ks)
+            k = po.uniform((ci, co, f, f), 8100 + t, ks)
+            l = nets.Layer("k", ci, co, hi, wi, f, f, s)
+            a = nets.Act(n, ci, hi, wi)
+            a.buf.copy_(dev(np.stack([po.pack_feature_map(x[i], 8) for i in range(n)])))
+            wb = nets.pack_weights(dev(k), False)
+            y = nets.Act(n, co, l.h_o, l.w_o)
+            nets.conv(l, n, a, wb, y, epilogue=_abi.EPI_RELU, tile_variant=variant + 1)
+            got = host(y.buf)
+            y2 = nets.Act(n, co, l.h_o, l.w_o)
+            nets.conv(l, n, a, wb, y2, epilogue=_abi.EPI_RELU, tile_variant=variant + 1)
+            assert np.array_equal(got, host(y2.buf)), "split-K not bitwise repeatable"
+            for i in range(n):
+                want = np.maximum(po.pack_feature_map(po.conv_oracle64(x[i], k, s), 8), 0)
+                assert_tol(got[i], want, f"ks={ks} v{variant} case {t} img {i}")
 
 
 # ---------------------------------------------------------- TF32 tensor cores
@@ -700,25 +705,20 @@ def test_ffma_fused_maxpool_epilogue(ci, co, h, w, n, variant):
     and lane^1 horizontal window partners) equals the FFMA conv with the
     same tile followed by the bit-exact pool kernel, bit for bit; windows
     span stacked images."""
-    lib = _abi.lib()
-    _abi.check(lib.dconv_cuda_set_ffma_variant(variant))
-    try:
-        l = nets.Layer("p", ci, co, h, w, 3, 3, 1)
-        x = po.uniform((n, ci, h, w), 9800 + ci, co)
-        k = po.uniform((ci, co, 3, 3), 9801 + ci, co)
-        a = nets.Act(n, ci, h, w)
-        a.buf.copy_(dev(np.stack([po.pack_feature_map(x[i], 8) for i in range(n)])))
-        wb = nets.pack_weights(dev(k), False)
-        z = nets.Act(n, co, l.h_o // 2, l.w_o // 2, halo=1)
-        nets.conv(l, n, a, wb, z, _abi.EPI_RELU | _abi.EPI_MAXPOOL)
-        got = host(z.buf)
-        for i in range(n):
-            y = np.maximum(po.conv_oracle64(x[i], k, 1), 0)
-            want = po.pack_feature_map(y.reshape(co, l.h_o // 2, 2, l.w_o // 2, 2).max(axis=(2, 4)), 8)
-            assert_tol(got[i, :, 1:-1, 1:-1], want, f"fused pool img {i}")
-            assert not got[i, :, 0].any() and not got[i, :, :, 0].any()
-    finally:
-        lib.dconv_cuda_set_ffma_variant(-1)
+    l = nets.Layer("p", ci, co, h, w, 3, 3, 1)
+    x = po.uniform((n, ci, h, w), 9800 + ci, co)
+    k = po.uniform((ci, co, 3, 3), 9801 + ci, co)
+    a = nets.Act(n, ci, h, w)
+    a.buf.copy_(dev(np.stack([po.pack_feature_map(x[i], 8) for i in range(n)])))
+    wb = nets.pack_weights(dev(k), False)
+    z = nets.Act(n, co, l.h_o // 2, l.w_o // 2, halo=1)
+    nets.conv(l, n, a, wb, z, _abi.EPI_RELU | _abi.EPI_MAXPOOL, tile_variant=variant + 1)
+    got = host(z.buf)
+    for i in range(n):
+        y = np.maximum(po.conv_oracle64(x[i], k, 1), 0)
+        want = po.pack_feature_map(y.reshape(co, l.h_o // 2, 2, l.w_o // 2, 2).max(axis=(2, 4)), 8)
+        assert_tol(got[i, :, 1:-1, 1:-1], want, f"fused pool img {i}")
+        assert not got[i, :, 0].any() and not got[i, :, :, 0].any()
 
 
 @pytest.mark.parametrize("ci,co,h,w,n", [(16, 64, 34, 26, 2), (24, 264, 18, 18, 1), (8, 40, 66, 10, 3)])
@@ -883,12 +883,29 @@ def test_tensor_core_strided_layers_read_space_to_depth_in_place(algo, monkeypat
         torch.cuda.synchronize()
         if l.s > 1 and l.h_f > 1:
             rec[l.name] = (l, host(x.buf), host(out.buf), out, epilogue)
+            calls[l.name] = (l, n, x, wp, out, epilogue, skip, in_view, kw)
+    calls = {}
     nets.conv_tf32 = spy
     try:
         b.run()
     finally:
         nets.conv_tf32 = orig
     assert sorted(rec) == ["s2b1_c2", "s3b1_c2", "s4b1_c2"]
+    if algo == "tf32x3":
+        # per element at the fp32 tolerance: the same launches (in-place
+        # strided TMA) on fresh uniform[-1,1] inputs, where the bound applies
+        for name, (l, n, x, wp, out, epilogue, skip, in_view, kw) in calls.items():
+            nets._fill(x.buf, 77, len(name))
+            orig(l, n, x, wp, out, epilogue, skip, None, in_view, **kw)
+            xs, ys = host(x.buf), host(out.buf)
+            kb = po.pack_kernel(po.unpack_kernel(host(b.weights[name]), l.c_i, l.c_o), 8, 8)
+            for i in range(2):
+                xb = np.ascontiguousarray(xs[i][:, :l.h_i, :l.w_i, :])
+                want = po.conv_oracle64_blocked(xb, kb, l.c_i, l.c_o, l.s, 0, l.h_o)
+                if epilogue & _abi.EPI_RELU:
+                    want = np.maximum(want, 0)
+                got = ys[i][:, out.halo:out.halo + l.h_o, out.halo:out.halo + l.w_o]
+                assert_tol(got, want, f"{name} fresh input img {i}")
     for name, (l, xs, ys, out, epi) in rec.items():
         kb = po.pack_kernel(po.unpack_kernel(host(b.weights[name]), l.c_i, l.c_o), 8, 8)
         for i in range(2):
@@ -909,7 +926,8 @@ def test_tensor_core_strided_layers_read_space_to_depth_in_place(algo, monkeypat
 
 @pytest.mark.parametrize("x3", [False, True])
 @pytest.mark.parametrize("ci,co,h,f,s,n", [(64, 72, 21, 3, 2, 2), (24, 256, 17, 5, 2, 1),
-                                            (16, 64, 27, 3, 3, 2), (40, 136, 15, 3, 2, 3)])
+                                            (16, 64, 27, 3, 3, 2), (40, 136, 15, 3, 2, 3),
+                                            (8, 96, 59, 11, 4, 2), (64, 128, 57, 5, 4, 8)])
 def test_tensor_core_strided_kxk_through_the_abi(ci, co, h, f, s, n, x3):
     """k x k stride-s layers straight through the tensor-core C-ABI (in-place
     space-to-depth, ragged channel counts, stride 3, stacked 7x7 tiles)."""
@@ -930,6 +948,19 @@ def test_tensor_core_strided_kxk_through_the_abi(ci, co, h, f, s, n, x3):
             bound = 2.0 ** -9 * po.pack_feature_map(po.conv_oracle64(np.abs(x[i]), np.abs(k), s), 8)
             assert (np.abs(got[i] - want) <= bound + 1e-5).all()
         assert np.abs(got[i] - want).max() > 0  # the tensor-core path really ran
+
+
+def test_tensor_core_rejects_stride_over_8():
+    """Strides > 8 exceed the TMA element-stride limit: a clear
+    EUNSUPPORTED, not a tensor-map encode failure."""
+    l = nets.Layer("s9", 8, 8, 28, 28, 10, 10, 9)
+    a = nets.Act(1, 8, 28, 28)
+    y = nets.Act(1, 8, l.h_o, l.w_o)
+    for x3 in (False, True):
+        with pytest.raises(RuntimeError, match="stride"):
+            wp = nets.prepare_tf32(l, nets.pack_weights(dev(po.uniform((8, 8, 10, 10), 1, 2)),
+                                                        False), x3=x3)
+            nets.conv_tf32(l, 1, a, wp, y, x3=x3)
 
 
 @pytest.mark.parametrize("config,n", [("vgg16", 32), ("resnet50", 256), ("googlenet", 64)])
