@@ -124,14 +124,14 @@ int orcg_conv_oracle64(const float* in, int n, int c_i, int h_i, int w_i, int in
   p.h_f = h_f; p.w_f = w_f; p.s = s;
   p.h_o = (h_i - h_f) / s + 1;
   p.w_o = (w_i - w_f) / s + 1;
-  // largest pixel tile whose 8-channel patch fits 96 KB
+  // largest pixel tile whose 8-channel patch + weights fit 190 KB
   const size_t w_bytes = (size_t)8 * h_f * w_f * 8 * 4;
   bool found = false;
   for (int tw : {32, 16, 8, 4}) {
     for (int ppt = kMaxPpt; ppt >= 1 && !found; --ppt) {
       const int th = (kThreads / tw) * ppt;
       const int ph = (th - 1) * s + h_f, pw = (tw - 1) * s + w_f;
-      if ((size_t)8 * ph * pw * 4 + w_bytes <= 96 * 1024) {
+      if ((size_t)8 * ph * pw * 4 + w_bytes <= 190 * 1024) {
         p.TW = tw; p.PPT = ppt; p.TH = th; p.PH = ph; p.PW = pw;
         found = true;
       }
@@ -142,7 +142,7 @@ int orcg_conv_oracle64(const float* in, int n, int c_i, int h_i, int w_i, int in
   p.tiles_x = (p.w_o + p.TW - 1) / p.TW;
   p.tiles_y = (p.h_o + p.TH - 1) / p.TH;
   const size_t smem = (size_t)8 * p.PH * p.PW * 4 + w_bytes;
-  cudaFuncSetAttribute(og_conv64, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(og_conv64, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   dim3 grid((unsigned)(n * p.tiles_x * p.tiles_y), (unsigned)((c_o + 7) / 8));
   og_conv64<<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(p);
   const cudaError_t e = cudaGetLastError();

@@ -6,6 +6,7 @@ Tolerance (BASELINE.json north_star): fp32 direct conv
 |a - b| <= 1e-4 + 1e-5*|b| per element against conv_oracle64
 (reference.cpp:70-87); layout repacks, ReLU, skip-add and max-pool bit-exact.
 """
+import ctypes
 import zlib
 
 import numpy as np
