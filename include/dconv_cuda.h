@@ -236,6 +236,14 @@ int dconv_cuda_maxpool2x2_blocked(const float* in, int n, int n_blocks, int h,
 /* Zeroes a float buffer (halo buffers are zeroed once, outside timing). */
 int dconv_cuda_zero(float* x, int64_t count, void* stream);
 
+/* Write-ownership check (the GPU analogue of the reference's debug ownership
+ * map), in the debug build libdconv_b200_own.so only (csrc
+ * `make own`; the product build returns DCONV_EUNSUPPORTED): while set,
+ * every conv kernel store of an output element at address a with
+ * base <= a < base + n also does atomicAdd(&counts[a - base], 1), so each
+ * element of an output view must end at exactly 1.  counts = NULL clears. */
+int dconv_debug_set_ownership(unsigned* counts, const float* base, int64_t n);
+
 /* Test hook for the FFMA launcher's per-(device, kernel, ks) cache of
  * co-resident clusters: the cached answer for CTA tile `tile_variant`
  * (1..3, as dconv_conv_desc.tile_variant) and cluster size ks next to a fresh

@@ -81,6 +81,7 @@ _SIGS = {
     "dconv_cuda_zero": (_I, [_P, _L, _P]),
     "dconv_cuda_launch_count": (_L, []),
     "dconv_cuda_ffma_cluster_slots": (_I, [_I, _I, _P, _P]),
+    "dconv_debug_set_ownership": (_I, [_P, _P, _L]),
     "dconv_cuda_fp32_peak_probe": (ctypes.c_double, [_P]),
     "dconv_cuda_ffma2_pattern_probe": (ctypes.c_double, [_P]),
     "dconv_file_payload_floats": (_L, [ctypes.POINTER(FileHeader)]),

@@ -82,6 +82,12 @@ bool first_use_on_device(const void* kernel, int dev) {
 
 using dconv_host::set_error;
 
+#ifdef DCONV_DEBUG_OWNERSHIP
+namespace dconv_dev {
+__device__ OwnMap g_own = {nullptr, nullptr, 0};
+}
+#endif
+
 extern "C" {
 
 int dconv_conv_shape(int c_i, int c_o, int h_i, int w_i, int h_f, int w_f,
@@ -517,6 +523,18 @@ int dconv_cuda_zero(float* x, int64_t count, void* stream) {
   if (cudaMemsetAsync(x, 0, sizeof(float) * count, as_stream(stream)) != cudaSuccess)
     return dconv_host::check_launch("cudaMemsetAsync");
   return DCONV_OK;
+}
+
+int dconv_debug_set_ownership(unsigned* counts, const float* base, int64_t n) {
+#ifdef DCONV_DEBUG_OWNERSHIP
+  const dconv_dev::OwnMap m{counts, base, (long long)n};
+  const cudaError_t e = cudaMemcpyToSymbol(dconv_dev::g_own, &m, sizeof(m));
+  if (e != cudaSuccess) return set_error(DCONV_ECUDA, "ownership map: %s", cudaGetErrorString(e));
+  return DCONV_OK;
+#else
+  (void)counts; (void)base; (void)n;
+  return set_error(DCONV_EUNSUPPORTED, "not an ownership-debug build (make own)");
+#endif
 }
 
 int dconv_cuda_ffma_cluster_slots(int tile_variant, int ks, int* cached, int* fresh) {

@@ -194,6 +194,31 @@ __device__ __forceinline__ float4 lds128(const float* p) {
   return *reinterpret_cast<const float4*>(p);
 }
 
+// Write-ownership debug build (make own -> libdconv_b200_own.so, compiled
+// with -DDCONV_DEBUG_OWNERSHIP -rdc=true): every store of a conv output
+// element also counts itself in a map set by dconv_debug_set_ownership, so a
+// test can assert that each element of the output view is written exactly
+// once -- the GPU analogue of the reference's debug ownership map
+// (SPEC.md:350).  The product build compiles the hook to nothing.
+#ifdef DCONV_DEBUG_OWNERSHIP
+struct OwnMap {
+  unsigned* counts;
+  const float* base;
+  long long n;
+};
+extern __device__ OwnMap g_own;
+__device__ __forceinline__ void own_mark(const float* p, int nf) {
+  const OwnMap m = g_own;
+  if (!m.counts) return;
+  const long long i = p - m.base;
+  for (int k = 0; k < nf; ++k)
+    if (i + k >= 0 && i + k < m.n) atomicAdd(&m.counts[i + k], 1u);
+}
+#define DCONV_OWN(p, nf) ::dconv_dev::own_mark((p), (nf))
+#else
+#define DCONV_OWN(p, nf) ((void)0)
+#endif
+
 }  // namespace dconv_dev
 
 // Host-side helpers shared by the launchers (defined in abi.cu).

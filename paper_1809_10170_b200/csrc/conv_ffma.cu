@@ -43,14 +43,15 @@ constexpr int kCB = 8;          // channel block of this kernel (c_ib = c_ob)
 constexpr int kMaxStages = 8;
 constexpr int kMaxKs = 16;      // split-K cluster size (> 8 is the non-portable opt-in)
 
-// Tuning / debugging overrides, read once per process.
+// Tuning / debugging overrides, read once per process --
+// except DCONV_KSPLIT, read at every launch so a test can force several
+// split factors in one process.
 struct Knobs {
-  int force_g = 0, flush_every = 0, ksplit = 0;
+  int force_g = 0, flush_every = 0;
   bool no_splitk = false, no_tailsplit = false, debug = false;
   Knobs() {
     if (const char* e = getenv("DCONV_FORCE_G")) force_g = atoi(e);
     if (const char* e = getenv("DCONV_FLUSH_EVERY")) flush_every = atoi(e);
-    if (const char* e = getenv("DCONV_KSPLIT")) ksplit = atoi(e);
     no_splitk = getenv("DCONV_NO_SPLITK") != nullptr;
     no_tailsplit = getenv("DCONV_NO_TAILSPLIT") != nullptr;
     debug = getenv("DCONV_DEBUG") != nullptr;
@@ -59,6 +60,10 @@ struct Knobs {
 const Knobs& knobs() {
   static const Knobs k;
   return k;
+}
+int ksplit_knob() {
+  const char* e = getenv("DCONV_KSPLIT");
+  return e ? atoi(e) : 0;
 }
 constexpr int kComputeWarps = 8;  // default: 2 compute warpgroups, 8x8 outputs / thread
 constexpr int kThreads = (kComputeWarps + 4) * 32;  // + producer warpgroup
@@ -379,6 +384,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
                     for (int c = 0; c < 8; ++c) o[c] = fmaxf(o[c], 0.f);
                   }
                   float* dst = p.out + ooff[kk];
+                  DCONV_OWN(dst, 8);
                   *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
                   *reinterpret_cast<float4*>(dst + 4) = make_float4(o[4], o[5], o[6], o[7]);
                   for (int pi = 0; pi < p.n_peers; ++pi) {
@@ -648,6 +654,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
       }
       float* o = p.out + (int64_t)jl * p.out_blk + (int64_t)img * p.out_img +
                  (int64_t)y * p.out_row + (int64_t)x * kCB;
+      DCONV_OWN(o, 8);
 #pragma unroll
       for (int c = 0; c < 8; c += 4)
         *reinterpret_cast<float4*>(o + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
@@ -724,6 +731,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
           }
           const int64_t off = (int64_t)jl * p.out_blk + (int64_t)img * p.out_img +
                               (int64_t)y * p.out_row + (int64_t)x * kCB + hf * 4;
+          DCONV_OWN(p.out + off, 4);
           *reinterpret_cast<float4*>(p.out + off) = v;
           for (int pi = 0; pi < p.n_peers; ++pi)
             *reinterpret_cast<float4*>(p.peer_out[pi] + off) = v;
@@ -766,6 +774,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
         tile_row(p, tr, ty, img, y, prow);
         float* o = p.out + (int64_t)jl * p.out_blk + (int64_t)img * p.out_img +
                    (int64_t)(y >> 1) * p.out_row + (int64_t)(x >> 1) * kCB;
+        DCONV_OWN(o, 8);
         *reinterpret_cast<float4*>(o) = make_float4(v[0], v[1], v[2], v[3]);
         *reinterpret_cast<float4*>(o + 4) = make_float4(v[4], v[5], v[6], v[7]);
       };
@@ -1183,7 +1192,8 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
     if (configure<BN, NW, TPX, TCO>(t, 2, true))
       best_ks = best_split(units, slots, t.n_g * t.n_r, unit_cycles(p, BM, BN), nullptr);
   }
-  if (knobs().ksplit) best_ks = std::max(1, std::min(knobs().ksplit, std::min(kMaxKs, S)));
+  if (const int kf = ksplit_knob(); kf && !no_split)
+    best_ks = std::max(1, std::min(kf, std::min(kMaxKs, S)));
   if (best_ks > 1) {
     FfmaParams r = p;
     const size_t smem = configure<BN, NW, TPX, TCO>(r, best_ks, true);

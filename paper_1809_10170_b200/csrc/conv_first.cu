@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(256, 2)
         v1.x = fmaxf(v1.x, 0.f); v1.y = fmaxf(v1.y, 0.f);
         v1.z = fmaxf(v1.z, 0.f); v1.w = fmaxf(v1.w, 0.f);
       }
+      DCONV_OWN(obase + x * 8, 8);
       *reinterpret_cast<float4*>(obase + x * 8) = v0;
       *reinterpret_cast<float4*>(obase + x * 8 + 4) = v1;
       for (int q = 0; q < p.n_peers; ++q) {  // fused C_o-shard gather

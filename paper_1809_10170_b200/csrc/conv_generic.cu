@@ -56,9 +56,10 @@ __global__ void conv_generic_kernel(const GenericParams p) {
             acc = fmaf(ip[ii], wp[(int64_t)ii * p.c_ob], acc);
         }
     }
-    p.out[(int64_t)img * p.out_img + (int64_t)jl * p.out_blk +
-          (int64_t)y * p.out_row + (int64_t)x * p.c_ob + jj] =
-        epilogue(acc, p, img, jl, y, x, jj);
+    float* o = p.out + (int64_t)img * p.out_img + (int64_t)jl * p.out_blk +
+               (int64_t)y * p.out_row + (int64_t)x * p.c_ob + jj;
+    DCONV_OWN(o, 1);
+    *o = epilogue(acc, p, img, jl, y, x, jj);
   }
 }
 
@@ -86,9 +87,10 @@ __global__ void conv_first_layer_kernel(const GenericParams p) {
                         x * p.s + m],
                      wp[(int64_t)ii * p.c_ob], acc);
       }
-    p.out[(int64_t)img * p.out_img + (int64_t)jl * p.out_blk +
-          (int64_t)y * p.out_row + (int64_t)x * p.c_ob + jj] =
-        epilogue(acc, p, img, jl, y, x, jj);
+    float* o = p.out + (int64_t)img * p.out_img + (int64_t)jl * p.out_blk +
+               (int64_t)y * p.out_row + (int64_t)x * p.c_ob + jj;
+    DCONV_OWN(o, 1);
+    *o = epilogue(acc, p, img, jl, y, x, jj);
   }
 }
 

@@ -160,6 +160,7 @@ __device__ __forceinline__ void emit32(const Tf32Params& p, float (&v)[32], int 
       float* o = p.out + (int64_t)img * p.out_img + (int64_t)jb * p.out_blk +
                  (int64_t)(y >> 1) * p.out_row + (int64_t)(x >> 1) * 8;
       const float* vv = v + b * 8;
+      DCONV_OWN(o, 8);
       *reinterpret_cast<float4*>(o) = make_float4(vv[0], vv[1], vv[2], vv[3]);
       *reinterpret_cast<float4*>(o + 4) = make_float4(vv[4], vv[5], vv[6], vv[7]);
     }
@@ -198,6 +199,7 @@ __device__ __forceinline__ void emit32(const Tf32Params& p, float (&v)[32], int 
 #pragma unroll
       for (int i = 0; i < 8; ++i) vv[i] = fmaxf(vv[i], 0.f);
     }
+    DCONV_OWN(o, 8);
     *reinterpret_cast<float4*>(o) = make_float4(vv[0], vv[1], vv[2], vv[3]);
     *reinterpret_cast<float4*>(o + 4) = make_float4(vv[4], vv[5], vv[6], vv[7]);
   }
