@@ -14,6 +14,7 @@
 // 7*S + WF input values and reuses it across the WF filter columns
 // (s*(k'*w_ob + kk) + m indexing).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "conv_kernels.h"
@@ -263,6 +264,12 @@ int launch_first(const GenericParams& p, cudaStream_t stream) {
 
 int launch_conv_first_fast(const GenericParams& p, cudaStream_t stream) {
   if (p.c_ob != 8 || p.h_f != p.w_f) return DCONV_EUNSUPPORTED;
+  // many-tile layers: the TMA-store reader (conv_reader.cu)
+  static const bool no_reader = getenv("DCONV_NO_READER") != nullptr;
+  if (!no_reader) {
+    const int rc = launch_conv_reader(p, stream);
+    if (rc != DCONV_EUNSUPPORTED) return rc;
+  }
   if (p.s == 1 && p.w_f == 3) return launch_first<1, 3>(p, stream);
   if (p.s == 2 && p.w_f == 7) return launch_first<2, 7>(p, stream);
   if (p.s == 4 && p.w_f == 11) return launch_first<4, 11>(p, stream);

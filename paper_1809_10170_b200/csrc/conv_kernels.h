@@ -98,5 +98,8 @@ int launch_conv_first_layer(const GenericParams& p, cudaStream_t stream);
 // register-tiled first-layer reader (c_ob = 8); DCONV_EUNSUPPORTED if no
 // specialisation matches (the caller then uses launch_conv_first_layer).
 int launch_conv_first_fast(const GenericParams& p, cudaStream_t stream);
+// first-layer reader with TMA-stored output tiles (conv_reader.cu): 3x3/s1 and
+// 7x7/s2 on many tiles, ReLU / plain epilogue; DCONV_EUNSUPPORTED otherwise.
+int launch_conv_reader(const GenericParams& p, cudaStream_t stream);
 
 }  // namespace dconv_dev

@@ -1127,3 +1127,33 @@ def test_space_to_depth_blocked_bitexact():
             for dx in range(f):
                 want[(dy * f + dx) * c:(dy * f + dx + 1) * c] = xp[:, dy::f, dx::f]
         assert np.array_equal(got[i], po.pack_feature_map(want, 8))
+
+
+@pytest.mark.parametrize("f,s,h,w,co,n", [(3, 1, 34, 45, 64, 40), (3, 1, 20, 226, 40, 30),
+                                           (7, 2, 41, 39, 96, 36), (7, 2, 229, 229, 64, 6),
+                                           (3, 1, 226, 226, 72, 3)])
+def test_first_layer_tma_reader_every_element(f, s, h, w, co, n):
+    """The TMA-store first-layer reader (conv_reader.cu; many-tile layers):
+    ragged tiles in both directions (clipped by the tensor store), partial
+    and multiple 64-channel groups, a halo'd output view, ReLU -- every
+    element against the fp64 GPU referee, and bitwise equal to the
+    register-tiled reader it replaces except for summation order (both
+    within the fp32 bound)."""
+    from oracle import gpu_oracle as go
+    l = nets.Layer("r", 3, co, h, w, f, f, s, first=True)
+    xd = torch.empty((n, 3, h, w), device="cuda")
+    nets._fill(xd, 61 + f, co)
+    wd = torch.empty((3, co, f, f), device="cuda")
+    nets._fill(wd, 62 + f, co)
+    wb = nets.pack_weights(wd, True)
+    y = nets.Act(n, co, l.h_o, l.w_o, halo=1)
+    before = _abi.lib().dconv_cuda_launch_count()
+    nets.conv(l, n, xd, wb, y, _abi.EPI_RELU)
+    torch.cuda.synchronize()
+    want = go.conv64_act(xd, l, wd).clamp_min(0.0)
+    ok, nbad, err, ratio = go.check_tol(y.buf[:, :, 1:-1, 1:-1, :], want)
+    assert ok, f"{nbad} bad, max err {err}"
+    # halo ring untouched
+    assert not y.buf[:, :, 0].any() and not y.buf[:, :, -1].any()
+    assert not y.buf[:, :, :, 0].any() and not y.buf[:, :, :, -1].any()
+    assert _abi.lib().dconv_cuda_launch_count() == before + 1
