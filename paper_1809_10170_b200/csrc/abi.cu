@@ -222,7 +222,8 @@ int conv_direct_impl(const dconv_conv_desc* d, const float* in, const float* w,
   int rc = resolve(d, false, 0, in, w, skip, out, &r);
   if (rc) return rc;
   const bool ffma_ok =
-      d->c_ib == 8 && d->c_ob == 8 && aligned16(in) && aligned16(w) &&
+      d->c_ib == d->c_ob && (d->c_ib == 8 || d->c_ib == 16 || d->c_ib == 32) &&
+      aligned16(in) && aligned16(w) &&
       aligned16(out) && (!skip || aligned16(skip)) &&
       ((r.in_img | r.in_blk | r.in_row | r.out_img | r.out_blk | r.out_row |
         r.sk_img | r.sk_blk | r.sk_row) & 3) == 0;
@@ -231,12 +232,13 @@ int conv_direct_impl(const dconv_conv_desc* d, const float* in, const float* w,
   if (algo == DCONV_ALGO_FFMA) {
     if (!ffma_ok)
       return set_error(DCONV_EUNSUPPORTED,
-                       "FFMA kernel needs c_ib == c_ob == 8 and 16-byte "
+                       "FFMA kernel needs c_ib == c_ob in {8, 16, 32} and 16-byte "
                        "aligned views (got c_ib=%d c_ob=%d)", d->c_ib, d->c_ob);
     dconv_dev::FfmaParams p{};
     p.in = in; p.w = w; p.skip = skip; p.out = out;
     p.n = d->n; p.h_i = d->h_i; p.w_i = d->w_i; p.h_o = d->h_o; p.w_o = d->w_o;
     p.h_f = d->h_f; p.w_f = d->w_f; p.s = d->stride;
+    p.cbs = d->c_ib;
     p.ib_n = r.ib_n; p.jb_n = r.jb_n; p.jb_begin = r.jb_begin; p.jb_count = r.jb_count;
     p.in_img = r.in_img; p.in_blk = r.in_blk; p.in_row = r.in_row;
     p.out_img = r.out_img; p.out_blk = r.out_blk; p.out_row = r.out_row;
@@ -334,6 +336,7 @@ int conv_tf32_impl(const dconv_conv_desc* d, const float* in, const float* w_pre
   p.in = in; p.w = nullptr; p.skip = skip; p.out = out;
   p.n = d->n; p.h_i = d->h_i; p.w_i = d->w_i; p.h_o = d->h_o; p.w_o = d->w_o;
   p.h_f = d->h_f; p.w_f = d->w_f; p.s = d->stride;
+  p.cbs = 8;
   p.ib_n = r.ib_n; p.jb_n = r.jb_n; p.jb_begin = r.jb_begin; p.jb_count = r.jb_count;
   p.in_img = r.in_img; p.in_blk = r.in_blk; p.in_row = r.in_row;
   p.out_img = r.out_img; p.out_blk = r.out_blk; p.out_row = r.out_row;

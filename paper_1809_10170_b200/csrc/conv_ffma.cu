@@ -39,7 +39,8 @@ namespace dconv_dev {
 
 namespace {
 
-constexpr int kCB = 8;          // channel block of this kernel (c_ib = c_ob)
+constexpr int kCB = 8;          // channels per math sub-block (a thread's 8 output channels,
+                                // one input slice of a tap); storage blocks are CBS = 8/16/32
 constexpr int kMaxStages = 8;
 constexpr int kMaxKs = 16;      // split-K cluster size (> 8 is the non-portable opt-in)
 
@@ -224,9 +225,20 @@ __host__ __device__ __forceinline__ int wchunk(int c, int wstride) {
 // warp) and an epilogue warpgroup: when p.epi_wg, the compute warps hand each
 // finished tile to the epilogue warps through TMEM and go straight on to the
 // next unit, so skip-add / ReLU / stores overlap the next tile's FFMA2s.
-template <int BM, int BN, int WF, int NW, int TPX, int TCO>
+// CBS: channel block of the stored maps and kernels (c_ib = c_ob = CBS, 8 /
+// 16 / 32).  A pixel of a staged row is CBS floats; the math walks it as
+// CBS / 8 sub-blocks of 8 channels, and an 8-channel output sub-block jl8 is
+// storage block jl8 / SUB at channel offset (jl8 % SUB) * 8 of the pencil.
+// jb_begin / jb_count count 8-channel sub-blocks, ib_n storage blocks.
+template <int CBS>
+__device__ __forceinline__ int64_t sub_off(int jl8, int64_t blk) {
+  return (int64_t)(jl8 / (CBS / 8)) * blk + (jl8 % (CBS / 8)) * 8;
+}
+
+template <int BM, int BN, int WF, int NW, int TPX, int TCO, int CBS>
 __global__ void __launch_bounds__((NW + 8) * 32, 1)
     conv_ffma_kernel(const FfmaParams p) {
+  constexpr int SUB = CBS / kCB;  // 8-channel sub-blocks per storage block
   // TCO: channels per thread (1 or 2 output blocks)
   constexpr int NBLK = TCO / 8;
   constexpr int AV = NW == 8 ? 4 : 2;  // activation channels per LDS
@@ -351,13 +363,13 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
                 const bool ok = blk_ok && ty < tr.th && x < p.w_o;
                 int img = 0, y = 0, prow;
                 if (ok) tile_row(p, tr, ty, img, y, prow);
-                ooff[kk] = ok ? (int64_t)jl * p.out_blk + (int64_t)img * p.out_img +
-                                    (int64_t)y * p.out_row + (int64_t)x * kCB
+                ooff[kk] = ok ? sub_off<CBS>(jl, p.out_blk) + (int64_t)img * p.out_img +
+                                    (int64_t)y * p.out_row + (int64_t)x * CBS
                               : -1;
                 if ((p.epi & DCONV_EPI_ADD) && ok) {
                   const float4* sk = reinterpret_cast<const float4*>(
-                      p.skip + (int64_t)jl * p.sk_blk + (int64_t)img * p.sk_img +
-                      (int64_t)y * p.sk_row + (int64_t)x * kCB);
+                      p.skip + sub_off<CBS>(jl, p.sk_blk) + (int64_t)img * p.sk_img +
+                      (int64_t)y * p.sk_row + (int64_t)x * CBS);
                   sk4[2 * kk] = __ldg(sk);
                   sk4[2 * kk + 1] = __ldg(sk + 1);
                 }
@@ -431,15 +443,16 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
       if ((p.epi & DCONV_EPI_ADD) && rank == 0 && p.skip_prefetch) {
         // the epilogue reads this unit's skip tile once: pull it into L2 now,
         // a unit ahead of the read, so the ADD epilogue does not wait on HBM
-        const uint32_t row_bytes = (uint32_t)(min(p.TW, p.w_o - tx0) * kCB * 4);
+        const uint32_t row_bytes = (uint32_t)(min(p.TW, p.w_o - tx0) * CBS * 4);
         for (int t = pt; t < cg_valid * tr.th; t += 32 * kProdWarps) {
           const int c = t / tr.th, ty = t - c * tr.th;
           int img, y, prow;
           tile_row(p, tr, ty, img, y, prow);
-          bulk_prefetch_l2(p.skip + (int64_t)(jb0 + c - p.jb_begin) * p.sk_blk +
-                               (int64_t)img * p.sk_img + (int64_t)y * p.sk_row +
-                               (int64_t)tx0 * kCB,
-                           row_bytes);
+          if ((c % SUB) == 0)  // one prefetch per storage block row
+            bulk_prefetch_l2(p.skip + sub_off<CBS>(jb0 + c - p.jb_begin, p.sk_blk) +
+                                 (int64_t)img * p.sk_img + (int64_t)y * p.sk_row +
+                                 (int64_t)tx0 * CBS,
+                             row_bytes);
         }
       }
       for (int st = st0; st < st1; ++st, ++gs) {
@@ -454,13 +467,14 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
         const int n_full = rest / p.h_o, last_cnt = rest - n_full * p.h_o;
         const int total_rows = rows_first + n_full * (seg_rows_full + Re) +
                                (last_cnt ? (last_cnt - 1) * p.sy + Re : 0);
-        const uint32_t patch_bytes = (uint32_t)(Ge * total_rows * cols * kCB * 4);
-        const uint32_t wbytes = (uint32_t)(Re * p.w_f * kCB * kCB * 4) * Ge;
+        const uint32_t patch_bytes = (uint32_t)(Ge * total_rows * cols * CBS * 4);
+        const uint32_t wbytes = (uint32_t)(Re * p.w_f * CBS * CBS * 4) * Ge;
+        const int n_wblk = (cg_valid + SUB - 1) / SUB;  // storage blocks of weights
         float* sp = smem + buf * p.stage_floats;
         float* sw = sp + p.patch_floats;
         // one expect_tx per stage; copies of other warps may complete before
         // it (the transaction count is allowed to run ahead within a phase)
-        if (pt == 0) mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes * cg_valid);
+        if (pt == 0) mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes * n_wblk);
         __syncwarp();
         for (int j = 0; j < n_seg; ++j) {
           int img, y_start, rows, prow0;
@@ -472,17 +486,18 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
             prow0 = (tr.cnt0 - 1) * p.sy + p.R + (j - 1) * (seg_rows_full + p.R);
           }
           const float* src0 = p.in + (int64_t)img * p.in_img +
-                              (int64_t)(y_start * p.sy + n0) * p.in_row + (int64_t)col0 * kCB;
+                              (int64_t)(y_start * p.sy + n0) * p.in_row + (int64_t)col0 * CBS;
           for (int t = pt; t < Ge * rows; t += 32 * kProdWarps) {
             const int gi = t / rows, pr = t - gi * rows;
             const float* src = src0 + (int64_t)(ib0 + gi) * p.in_blk + (int64_t)pr * p.in_row;
-            float* dst = sp + ((gi * p.PH + prow0 + pr) * p.PW) * kCB;
-            bulk_g2s(dst, src, (uint32_t)(cols * kCB * 4), &full[buf]);
+            float* dst = sp + ((gi * p.PH + prow0 + pr) * p.PW) * CBS;
+            bulk_g2s(dst, src, (uint32_t)(cols * CBS * 4), &full[buf]);
           }
         }
-        for (int c = pt; c < cg_valid; c += 32 * kProdWarps) {
-          const float* src = p.w + ((int64_t)(jb0 + c) * p.ib_n + ib0) * p.slab_floats +
-                             (int64_t)n0 * p.w_f * kCB * kCB;
+        for (int c = pt; c < n_wblk; c += 32 * kProdWarps) {
+          // storage block J = jb0 / SUB + c of the blocked kernel
+          const float* src = p.w + ((int64_t)(jb0 / SUB + c) * p.ib_n + ib0) * p.slab_floats +
+                             (int64_t)n0 * p.w_f * CBS * CBS;
           bulk_g2s(sw + wchunk<TCO>(c, p.wstride_floats), src, wbytes, &full[buf]);
         }
       }
@@ -520,7 +535,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
       const int ty = (int)__umulhi((unsigned)q, p.tw_magic), tx = q - ty * p.TW;
       int img, y, prow;
       tile_row(p, tr, ty, img, y, prow);
-      poff[k] = (ty < tr.th && tx0 + tx < p.w_o) ? (prow * p.PW + tx * p.s) * kCB : 0;
+      poff[k] = (ty < tr.th && tx0 + tx < p.w_o) ? (prow * p.PW + tx * p.s) * CBS : 0;
     }
     uint64_t acc[TPX][TCO / 2];
 #pragma unroll
@@ -537,7 +552,10 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
       const int Ge = min(p.G, p.ib_n - g * p.G);
       const int Re = min(p.R, p.h_f - r * p.R);
       const float* sp = smem + buf * p.stage_floats;
-      const float* sw = sp + p.patch_floats + wchunk<TCO>(cb, p.wstride_floats);
+      // this thread's output sub-block cb: weight chunk of storage block
+      // cb / SUB, column offset (cb % SUB) * 8 in its CBS-wide rows
+      const float* sw = sp + p.patch_floats + wchunk<TCO>(cb / SUB, p.wstride_floats) +
+                        (cb % SUB) * kCB;
       const int sw2 = NBLK > 1 ? wchunk<TCO>(cb + 1, p.wstride_floats) - wchunk<TCO>(cb, p.wstride_floats) : 0;
       // per-pixel patch pointers once per stage; rows and taps then add a
       // warp-uniform offset (measured +1%; swapping the channel-half order
@@ -546,9 +564,15 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
 #pragma unroll
       for (int k = 0; k < TPX; ++k) pk[k] = sp + poff[k];
       // one filter tap of one input block: 8 channels x (8 px x TCO ch)
+      // c_b = 32: a pixel is one 128-byte pencil, so the 4 lanes of a
+      // quarter-warp that read 4 pixels' same channel quarter hit one bank
+      // group; odd lanes take the two channel halves in the other order
+      // (activations 2-way instead of 4-way, weights 2-way instead of none)
+      const int hswap = CBS == 32 ? (lane & 1) : 0;
       auto tap = [&](const float* pw, int aoff) {
 #pragma unroll
-        for (int half = 0; half < 8 / AV; ++half) {
+        for (int half_i = 0; half_i < 8 / AV; ++half_i) {
+          const int half = half_i ^ hswap;
           float a[TPX][AV];
 #pragma unroll
           for (int k = 0; k < TPX; ++k) {
@@ -564,7 +588,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
           for (int i4 = 0; i4 < AV; ++i4) {
 #pragma unroll
             for (int bb = 0; bb < NBLK; ++bb) {
-              const float* pb = pw + bb * sw2 + (half * AV + i4) * kCB;
+              const float* pb = pw + bb * sw2 + (half * AV + i4) * CBS;
               const float4 b0 = lds128(pb);
               const float4 b1 = lds128(pb + 4);
               uint64_t bp[4];
@@ -583,16 +607,21 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
       if (WF == 1 && Re == 1) {
         // 1x1 filters: a stage is Ge input blocks of one tap each; unrolled
         // so the accumulators stay put across blocks (no register rotation)
-        const int gstride = p.PH * p.PW * kCB, wgstride = p.R * kCB * kCB;
+        const int gstride = p.PH * p.PW * CBS, wgstride = p.R * CBS * CBS;
 #pragma unroll 4
-        for (int gi = 0; gi < Ge; ++gi) tap(sw + gi * wgstride, gi * gstride);
+        for (int gi = 0; gi < Ge * SUB; ++gi)  // 8-channel input sub-blocks
+          tap(sw + (gi / SUB) * wgstride + (gi % SUB) * kCB * CBS,
+              (gi / SUB) * gstride + (gi % SUB) * kCB);
       } else {
         for (int gi = 0; gi < Ge; ++gi) {
-          for (int n = 0; n < Re; ++n) {
-            const int row_off = ((gi * p.PH + n) * p.PW) * kCB;
-            const float* pw_row = sw + ((gi * p.R + n) * wf) * (kCB * kCB);
+#pragma unroll 1
+          for (int sb = 0; sb < SUB; ++sb) {  // 8-channel input sub-blocks
+            for (int n = 0; n < Re; ++n) {
+              const int row_off = ((gi * p.PH + n) * p.PW) * CBS + sb * kCB;
+              const float* pw_row = sw + ((gi * p.R + n) * wf) * (CBS * CBS) + sb * kCB * CBS;
 #pragma unroll(WF > 0 ? WF : 1)
-            for (int m = 0; m < wf; ++m) tap(pw_row + m * (kCB * kCB), row_off + m * kCB);
+              for (int m = 0; m < wf; ++m) tap(pw_row + m * (CBS * CBS), row_off + m * CBS);
+            }
           }
         }
       }
@@ -640,8 +669,8 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
       int img, y, prow;
       tile_row(p, tr, ty, img, y, prow);
       if (p.epi & DCONV_EPI_ADD) {
-        const float* sk = p.skip + (int64_t)jl * p.sk_blk + (int64_t)img * p.sk_img +
-                          (int64_t)y * p.sk_row + (int64_t)x * kCB;
+        const float* sk = p.skip + sub_off<CBS>(jl, p.sk_blk) + (int64_t)img * p.sk_img +
+                          (int64_t)y * p.sk_row + (int64_t)x * CBS;
 #pragma unroll
         for (int c = 0; c < 8; c += 4) {
           const float4 s4 = *reinterpret_cast<const float4*>(sk + c);
@@ -652,8 +681,8 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
 #pragma unroll
         for (int c = 0; c < 8; ++c) v[c] = fmaxf(v[c], 0.f);
       }
-      float* o = p.out + (int64_t)jl * p.out_blk + (int64_t)img * p.out_img +
-                 (int64_t)y * p.out_row + (int64_t)x * kCB;
+      float* o = p.out + sub_off<CBS>(jl, p.out_blk) + (int64_t)img * p.out_img +
+                 (int64_t)y * p.out_row + (int64_t)x * CBS;
       DCONV_OWN(o, 8);
 #pragma unroll
       for (int c = 0; c < 8; c += 4)
@@ -721,16 +750,16 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
           tile_row(p, tr, ty, img, y, prow);
           if (p.epi & DCONV_EPI_ADD) {
             const float4 s4 = __ldg(reinterpret_cast<const float4*>(
-                p.skip + (int64_t)jl * p.sk_blk + (int64_t)img * p.sk_img + (int64_t)y * p.sk_row +
-                (int64_t)x * kCB + hf * 4));
+                p.skip + sub_off<CBS>(jl, p.sk_blk) + (int64_t)img * p.sk_img +
+                (int64_t)y * p.sk_row + (int64_t)x * CBS + hf * 4));
             v.x += s4.x; v.y += s4.y; v.z += s4.z; v.w += s4.w;
           }
           if (p.epi & DCONV_EPI_RELU) {
             v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f);
             v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
           }
-          const int64_t off = (int64_t)jl * p.out_blk + (int64_t)img * p.out_img +
-                              (int64_t)y * p.out_row + (int64_t)x * kCB + hf * 4;
+          const int64_t off = sub_off<CBS>(jl, p.out_blk) + (int64_t)img * p.out_img +
+                              (int64_t)y * p.out_row + (int64_t)x * CBS + hf * 4;
           DCONV_OWN(p.out + off, 4);
           *reinterpret_cast<float4*>(p.out + off) = v;
           for (int pi = 0; pi < p.n_peers; ++pi)
@@ -772,8 +801,8 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
         if (cb >= cg_valid || (tx & 1) || ty >= tr.th || x >= p.w_o) return;
         int img, y, prow;
         tile_row(p, tr, ty, img, y, prow);
-        float* o = p.out + (int64_t)jl * p.out_blk + (int64_t)img * p.out_img +
-                   (int64_t)(y >> 1) * p.out_row + (int64_t)(x >> 1) * kCB;
+        float* o = p.out + sub_off<CBS>(jl, p.out_blk) + (int64_t)img * p.out_img +
+                   (int64_t)(y >> 1) * p.out_row + (int64_t)(x >> 1) * CBS;
         DCONV_OWN(o, 8);
         *reinterpret_cast<float4*>(o) = make_float4(v[0], v[1], v[2], v[3]);
         *reinterpret_cast<float4*>(o + 4) = make_float4(v[4], v[5], v[6], v[7]);
@@ -883,7 +912,7 @@ constexpr double kLaunchFill = 2500.0;   // first stage in flight, cycles
 
 // One unit's FFMA2 cycles (BM x BN outputs x the whole reduction) + overhead.
 double unit_cycles(const FfmaParams& p, int BM, int BN) {
-  return (double)BM * BN * p.ib_n * kCB * p.h_f * p.w_f / kFfmaPerCycle + kUnitOverhead;
+  return (double)BM * BN * p.ib_n * p.cbs * p.h_f * p.w_f / kFfmaPerCycle + kUnitOverhead;
 }
 
 // Few units (< SMs): every unit's K range split over a cluster of ks CTAs,
@@ -946,7 +975,7 @@ void pick_tile(FfmaParams& p, int BM, int BN, int co_groups, int sms, const int*
     const double rows = max_patch_rows(q, p.h_f);
     // producer copies per input block vs FFMA2 cycles per input block
     const double copy_ratio = kCopyCycles * rows /
-                              ((double)BM * BN * kCB * p.h_f * p.w_f / kFfmaPerCycle);
+                              ((double)BM * BN * p.cbs * p.h_f * p.w_f / kFfmaPerCycle);
     const double score = 1.0 / (cycles * std::max(1.0, copy_ratio));
     const int64_t patch = (int64_t)((std::min<int64_t>(th, vh) - 1) * p.sy + p.h_f) *
                           ((std::min(tw, p.w_o) - 1) * p.s + p.w_f);
@@ -969,19 +998,19 @@ void pick_tile(FfmaParams& p, int BM, int BN, int co_groups, int sms, const int*
 // units, or split-K whose 64 KB partial buffer shares smem with the ring),
 // NS ring depth, TMEM fold interval.  Returns the dynamic smem bytes, or 0 if
 // two stages do not fit.
-template <int BN, int NW, int TPX, int TCO>
+template <int BN, int NW, int TPX, int TCO, int CBS>
 size_t configure(FfmaParams& p, int ks, bool fine) {
-  constexpr int CG = BN / 8;
+  constexpr int CG = BN / CBS;  // weight chunks (output storage blocks) per stage
   // patch budget: 1x1 layers stage twice the input blocks per stage (their
   // stages are short: one tap per block; ResNet-50 256->64 at 56x56 +17%)
   static const int patch_kb = getenv("DCONV_PATCH_BUDGET") ? atoi(getenv("DCONV_PATCH_BUDGET")) : 0;
   const int kWeightBudget = 40 * 1024;
   const int kPatchBudget = (patch_kb ? patch_kb : (p.h_f * p.w_f == 1 ? 64 : 32)) * 1024;
-  const int full_taps_bytes = CG * p.h_f * p.w_f * kCB * kCB * 4;
+  const int full_taps_bytes = CG * p.h_f * p.w_f * CBS * CBS * 4;
   if (full_taps_bytes <= kWeightBudget) {
     p.R = p.h_f;
     p.PH = max_patch_rows(p, p.R);
-    const int patch1 = p.PH * p.PW * kCB * 4;
+    const int patch1 = p.PH * p.PW * CBS * 4;
     p.G = std::max(1, std::min(kWeightBudget / full_taps_bytes,
                                kPatchBudget / std::max(1, patch1)));
     p.G = std::min(p.G, p.ib_n);
@@ -989,22 +1018,22 @@ size_t configure(FfmaParams& p, int ks, bool fine) {
       // finer stages (split-K shares smem with its 64 KB partial buffer):
       // keep each stage <= 36 KB so the ring stays >= 4 deep; 1x1 layers
       // still group several input blocks per stage
-      const int per_block = patch1 + CG * p.R * p.w_f * kCB * kCB * 4;
+      const int per_block = patch1 + CG * p.R * p.w_f * CBS * CBS * 4;
       p.G = std::max(1, std::min(p.G, (36 * 1024) / per_block));
     }
     if (knobs().force_g) p.G = std::max(1, std::min(p.ib_n, knobs().force_g));
   } else {
     p.G = 1;
-    p.R = std::max(1, kWeightBudget / (CG * p.w_f * kCB * kCB * 4));
+    p.R = std::max(1, kWeightBudget / (CG * p.w_f * CBS * CBS * 4));
     p.R = std::min(p.R, p.h_f);
     p.PH = max_patch_rows(p, p.R);
   }
   p.n_g = (p.ib_n + p.G - 1) / p.G;
   p.n_r = (p.h_f + p.R - 1) / p.R;
-  p.patch_floats = p.G * p.PH * p.PW * kCB;
+  p.patch_floats = p.G * p.PH * p.PW * CBS;
   // +16 B per block chunk: the 8 lanes of a warp that read different output
   // blocks hit distinct 16-byte bank groups of the weight stage.
-  p.wstride_floats = p.G * p.R * p.w_f * kCB * kCB + (TCO == 8 ? 4 : 0);
+  p.wstride_floats = p.G * p.R * p.w_f * CBS * CBS + (TCO == 8 ? 4 : 0);
   p.stage_floats = (p.patch_floats + wchunk<TCO>(CG, p.wstride_floats) + 31) & ~31;  // 128 B aligned
   const int S = p.n_g * p.n_r;
   const int kSmemBudget = 220 * 1024;
@@ -1018,7 +1047,7 @@ size_t configure(FfmaParams& p, int ks, bool fine) {
   // the ring spans unit boundaries (the producer prefetches the next unit), so
   // its depth is set by shared memory alone, not by the stages per unit
   // partial sums cover >= 256 products before folding into the TMEM total
-  const int k_stage = p.G * p.R * p.w_f * kCB;
+  const int k_stage = p.G * p.R * p.w_f * CBS;
   p.flush_every = std::max(1, (256 + k_stage - 1) / k_stage);
   if (knobs().flush_every) p.flush_every = std::max(1, knobs().flush_every);
   if (p.NS < 2) return 0;
@@ -1147,14 +1176,14 @@ int launch_units(K kernel, int threads, FfmaParams p, size_t smem, int unit_begi
   return dconv_host::check_launch("conv_ffma_kernel");
 }
 
-template <int BM, int BN, int WF, int NW, int TPX, int TCO>
+template <int BM, int BN, int WF, int NW, int TPX, int TCO, int CBS>
 int launch_variant(FfmaParams p, cudaStream_t stream) {
   constexpr int threads = (NW + 8) * 32;
   constexpr int CG = BN / 8;
   const int dev = device_index();
   const int sms = dconv_host::device_sms(dev);
   const int co_groups = (p.jb_count + CG - 1) / CG;
-  auto kernel = conv_ffma_kernel<BM, BN, WF, NW, TPX, TCO>;
+  auto kernel = conv_ffma_kernel<BM, BN, WF, NW, TPX, TCO, CBS>;
   // kernel attributes are per device: set once for each device this
   // instantiation is launched on
   if (dconv_host::first_use_on_device(reinterpret_cast<const void*>(kernel), dev)) {
@@ -1175,12 +1204,12 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   // q / TW for q < BM by multiply-high (exact: BM * TW < 2^32)
   p.tw_magic = (unsigned)(((uint64_t(1) << 32) + p.TW - 1) / p.TW);
   p.PW = (p.TWe - 1) * p.s + p.w_f;
-  p.slab_floats = p.h_f * p.w_f * kCB * kCB;
+  p.slab_floats = p.h_f * p.w_f * CBS * CBS;
   const int units = p.tiles_y * p.tiles_x * co_groups;
   const bool fine = (int64_t)units * 2 < sms;  // batch-1 layers: split-K over fine stages
 
   FfmaParams q = p;
-  if (!configure<BN, NW, TPX, TCO>(q, 1, fine))
+  if (!configure<BN, NW, TPX, TCO, CBS>(q, 1, fine))
     return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_ffma: stage does not fit smem twice");
   const int S = q.n_g * q.n_r;
 
@@ -1189,14 +1218,14 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   int best_ks = 1;
   if (units < sms && !no_split) {
     FfmaParams t = p;
-    if (configure<BN, NW, TPX, TCO>(t, 2, true))
+    if (configure<BN, NW, TPX, TCO, CBS>(t, 2, true))
       best_ks = best_split(units, slots, t.n_g * t.n_r, unit_cycles(p, BM, BN), nullptr);
   }
   if (const int kf = ksplit_knob(); kf && !no_split)
     best_ks = std::max(1, std::min(kf, std::min(kMaxKs, S)));
   if (best_ks > 1) {
     FfmaParams r = p;
-    const size_t smem = configure<BN, NW, TPX, TCO>(r, best_ks, true);
+    const size_t smem = configure<BN, NW, TPX, TCO, CBS>(r, best_ks, true);
     if (!smem) return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_ffma: split stage");
     const int clusters = std::min(units, std::max(1, cluster_slots(kernel, best_ks, sms, threads)));
     if (knobs().debug)
@@ -1215,7 +1244,7 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
     static const bool pow2_only = getenv("DCONV_TAIL_POW2") != nullptr;
     for (int ks = kMaxKs; ks >= 2; ks = pow2_only ? ks / 2 : ks - 1) {
       FfmaParams t = p;
-      if (!configure<BN, NW, TPX, TCO>(t, ks, true)) continue;
+      if (!configure<BN, NW, TPX, TCO, CBS>(t, ks, true)) continue;
       if (ks > t.n_g * t.n_r) continue;
       const int slots = cluster_slots(kernel, ks, sms, threads);
       if (slots >= tail) {
@@ -1224,7 +1253,7 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
       }
     }
   }
-  const size_t smem_main = configure<BN, NW, TPX, TCO>(q, 1, fine);
+  const size_t smem_main = configure<BN, NW, TPX, TCO, CBS>(q, 1, fine);
   if (knobs().debug && tail_ks > 1)
     for (int ks = 2; ks <= kMaxKs; ++ks)
       fprintf(stderr, "  cluster_slots(%d) = %d\n", ks, cluster_slots(kernel, ks, sms, threads));
@@ -1239,17 +1268,25 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   int rc = launch_units(kernel, threads, q, smem_main, 0, main_units, sms, stream);
   if (rc) return rc;
   FfmaParams t = p;
-  const size_t smem_tail = configure<BN, NW, TPX, TCO>(t, tail_ks, true);
+  const size_t smem_tail = configure<BN, NW, TPX, TCO, CBS>(t, tail_ks, true);
   return launch_units(kernel, threads, t, smem_tail, main_units, tail, tail, stream);
 }
 
-template <int BM, int BN, int NW = 8, int TPX = 8, int TCO = 8>
+template <int BM, int BN, int NW = 8, int TPX = 8, int TCO = 8, int CBS = 8>
 int launch_wf(const FfmaParams& p, cudaStream_t stream) {
+  if constexpr (CBS != 8) {
+    // c_b = 16 / 32: filter widths 1 and 3 specialised, any other at run time
+    switch (p.w_f) {
+      case 1: return launch_variant<BM, BN, 1, NW, TPX, TCO, CBS>(p, stream);
+      case 3: return launch_variant<BM, BN, 3, NW, TPX, TCO, CBS>(p, stream);
+      default: return launch_variant<BM, BN, 0, NW, TPX, TCO, CBS>(p, stream);
+    }
+  }
   switch (p.w_f) {
-    case 1: return launch_variant<BM, BN, 1, NW, TPX, TCO>(p, stream);
-    case 3: return launch_variant<BM, BN, 3, NW, TPX, TCO>(p, stream);
-    case 5: return launch_variant<BM, BN, 5, NW, TPX, TCO>(p, stream);
-    default: return launch_variant<BM, BN, 0, NW, TPX, TCO>(p, stream);
+    case 1: return launch_variant<BM, BN, 1, NW, TPX, TCO, 8>(p, stream);
+    case 3: return launch_variant<BM, BN, 3, NW, TPX, TCO, 8>(p, stream);
+    case 5: return launch_variant<BM, BN, 5, NW, TPX, TCO, 8>(p, stream);
+    default: return launch_variant<BM, BN, 0, NW, TPX, TCO, 8>(p, stream);
   }
 }
 
@@ -1277,7 +1314,7 @@ int cluster_slots_fresh(K kernel, int ks, int threads) {
 
 template <int BM, int BN, int NW, int TPX, int TCO>
 int probe_slots(int ks, int* cached, int* fresh) {
-  auto kernel = conv_ffma_kernel<BM, BN, 3, NW, TPX, TCO>;
+  auto kernel = conv_ffma_kernel<BM, BN, 3, NW, TPX, TCO, 8>;
   const int dev = device_index();
   if (dconv_host::first_use_on_device(reinterpret_cast<const void*>(kernel), dev)) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -1319,11 +1356,29 @@ int launch_conv_ffma(const FfmaParams& p0, cudaStream_t stream) {
                     : 0u;
   static const bool no_skip_prefetch = getenv("DCONV_NO_SKIP_PREFETCH") != nullptr;
   p.skip_prefetch = (p.epi & DCONV_EPI_ADD) && !no_skip_prefetch;
+  // c_b = 16 / 32 storage blocks: the kernel counts output blocks in
+  // 8-channel sub-blocks (a thread's channel tile)
+  const int sub = p.cbs / kCB;
+  if (p.cbs != 8 && p.cbs != 16 && p.cbs != 32)
+    return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_ffma: c_b %d", p.cbs);
+  p.jb_begin *= sub;
+  p.jb_count *= sub;
   int v = p.variant;  // desc.tile_variant - 1; -1 = selector
   // measured (tools/sweep_variants.py): 256 px x 64 ch wins on every 3x3 /
   // 5x5 layer of the configs; 1x1 layers with >= 128 output channels
   // (little reuse per staged pixel) prefer 128 px x 128 ch
   if (v < 0) v = (p.h_f * p.w_f == 1 && p.jb_count >= 16) ? 0 : 1;
+  if (p.cbs != 8) {
+    // c_b = 16 / 32: the two main CTA tiles (the 128 x 64 batch-1 tile
+    // runs as 256 x 64)
+    if (p.epi & DCONV_EPI_MAXPOOL)
+      return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_ffma: fused pool needs c_b = 8");
+    if (p.cbs == 16)
+      return v == 0 ? launch_wf<128, 128, 8, 8, 8, 16>(p, stream)
+                    : launch_wf<256, 64, 8, 8, 8, 16>(p, stream);
+    return v == 0 ? launch_wf<128, 128, 8, 8, 8, 32>(p, stream)
+                  : launch_wf<256, 64, 8, 8, 8, 32>(p, stream);
+  }
   switch (v) {
     // Measured on B200 and not instantiated (tools/variant_run.sh): 12
     // compute warps with 2-channel activation loads (<192,128,12>,

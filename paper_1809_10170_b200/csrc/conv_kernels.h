@@ -16,9 +16,10 @@ struct FfmaParams {
   const float* skip;
   float* out;
   int n, h_i, w_i, h_o, w_o, h_f, w_f, s;
-  int ib_n;                 // input channel blocks (padded C_i / 8)
-  int jb_n;                 // output channel blocks in the weights
-  int jb_begin, jb_count;   // output blocks computed
+  int cbs;                  // channel block of maps and kernel (c_ib = c_ob): 8, 16, 32
+  int ib_n;                 // input channel blocks (padded C_i / cbs)
+  int jb_n;                 // output channel blocks in the weights (of cbs)
+  int jb_begin, jb_count;   // output 8-channel sub-blocks computed (launcher: * cbs/8)
   int64_t in_img, in_blk, in_row;
   int64_t out_img, out_blk, out_row;
   int64_t sk_img, sk_blk, sk_row;

@@ -1157,3 +1157,33 @@ def test_first_layer_tma_reader_every_element(f, s, h, w, co, n):
     assert not y.buf[:, :, 0].any() and not y.buf[:, :, -1].any()
     assert not y.buf[:, :, :, 0].any() and not y.buf[:, :, :, -1].any()
     assert _abi.lib().dconv_cuda_launch_count() == before + 1
+
+
+@pytest.mark.parametrize("cb", [16, 32])
+@pytest.mark.parametrize("tv", [0, 1, 2])
+def test_ffma_wide_channel_blocks(cb, tv, monkeypatch):
+    """c_ib = c_ob = 16 / 32 (the reference's wider BlockingParams,
+    micro_kernel.hpp:43-46) on the FFMA kernel: 64- / 128-byte pencils staged
+    whole, walked as 8-channel sub-blocks; ragged C_i / C_o (padded storage
+    blocks), strides, 1x1 / 3x3 / 5x5 filters, ReLU and skip-add epilogues,
+    the selector, each CTA tile and forced split-K -- against conv_oracle64."""
+    cases = [(64, 64, 30, 30, 3, 1, 2), (40, 72, 17, 23, 5, 1, 1), (96, 80, 13, 31, 1, 2, 3),
+             (200, 48, 9, 9, 3, 2, 2), (512, 128, 16, 16, 3, 1, 1), (24, 136, 12, 12, 1, 1, 4)]
+    if tv == 2:
+        monkeypatch.setenv("DCONV_KSPLIT", "4")
+    for t, (ci, co, hi, wi, f, s, n) in enumerate(cases):
+        x = po.uniform((n, ci, hi, wi), 7700 + t, cb)
+        k = po.uniform((ci, co, f, f), 7710 + t, cb)
+        shape = D.ConvShape(ci, co, hi, wi, f, f, s)
+        xb = D.BlockedFeatureMap(ci, hi, wi, cb, n=n, data=dev(np.stack(
+            [po.pack_feature_map(x[i], cb) for i in range(n)])))
+        kb = D.BlockedKernel(ci, co, f, f, cb, cb, data=dev(po.pack_kernel(k, cb, cb)))
+        skip_np = np.stack([po.pack_feature_map(po.uniform((co, shape.h_o, shape.w_o), 7720 + t, i),
+                                                cb) for i in range(n)])
+        sk = D.BlockedFeatureMap(co, shape.h_o, shape.w_o, cb, n=n, data=dev(skip_np))
+        y = D.conv_direct(xb, kb, shape, D.BlockingParams(cb, 1, cb), relu=True, skip=sk,
+                          algo=_abi.ALGO_FFMA, tile_variant=tv)
+        got = host(y.data)
+        for i in range(n):
+            want = np.maximum(po.pack_feature_map(po.conv_oracle64(x[i], k, s), cb) + skip_np[i], 0)
+            assert_tol(got[i], want, f"c_b {cb} tile {tv} case {t} img {i}")
