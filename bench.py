@@ -536,10 +536,32 @@ def roofline_for(ctx, args, plan, med, clk_max):
         bound = "fp32"
     total = sum(med.values())
     achieved = kflops / (kms * 1e-3) / 1e12 if kms else 0.0
+    # per-launch roofline: max(FLOPs / compute peak, compulsory bytes / HBM);
+    # the step's bound is their sum (ResNet's 64-channel 1x1 layers sit near
+    # the FP32 ridge and below the TF32 one: there HBM is the limit)
+    hbm = pk.get("hbm_gbs") or 6650.0
+    fp_peak = nominal_fp32_tflops(clk_max or 1965.0)
+    tc_peak = (pk.get("bf16_tflops") or FALLBACK_BF16_TFLOPS) / 2
+    bound_ms, meas_ms = 0.0, 0.0
+    for s in plan.steps:
+        if not (s.flops or s.bytes):
+            continue
+        if s.kind == "tf32":
+            t_c = s.flops * (3 if args.algo == "tf32x3" else 1) / (tc_peak * 1e12) * 1e3
+        else:
+            t_c = s.flops / (fp_peak * 1e12) * 1e3
+        t_m = s.bytes / (hbm * 1e9) * 1e3
+        bound_ms += max(t_c, t_m)
+        meas_ms += med[s.name]
     return roof_algo, {"bound": bound, "achieved": round(achieved, 2), "peak": round(peak, 2),
                        "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if peak else None,
                        "peak_source": src,
-                       "share_of_step": round(kms / total, 4) if total else None}
+                       "share_of_step": round(kms / total, 4) if total else None,
+                       "step_bound_ms": round(bound_ms, 4),
+                       "frac_of_step_bound": round(bound_ms / meas_ms, 4) if meas_ms else None,
+                       "step_bound_note": (f"sum over launches of max(FLOPs / {fp_peak:.1f} FP32 "
+                                           f"or {tc_peak:.0f} TF32 TFLOP/s, compulsory bytes / "
+                                           f"{hbm:.0f} GB/s HBM (MEASURED_PEAKS.json))")}
 
 
 def measure_config(ctx, args, config: str, batch: int, headline: bool) -> dict:
@@ -620,6 +642,10 @@ def measure_config(ctx, args, config: str, batch: int, headline: bool) -> dict:
             if s.kind in ("conv", "first"):
                 rec["frac_fp32_peak"] = round(rec["gflops"] / 1e3 / nominal_fp32_tflops(
                     clk.max_mhz or 1965.0), 3)
+        if s.bytes:
+            rec["gbps"] = round(s.bytes / (med[s.name] * 1e-3) / 1e9, 1)
+            if s.flops:
+                rec["flop_per_byte"] = round(s.flops / s.bytes, 1)
         layers.append(rec)
     fits_l2 = config in ("cfg1", "alexnet")
     rec = {

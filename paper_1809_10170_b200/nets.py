@@ -306,6 +306,24 @@ class Step:
     kind: str
     flops: int = 0      # algorithmic FLOPs of this launch on this rank
     layer: Optional[Layer] = None
+    bytes: int = 0      # compulsory HBM bytes of this launch (the roofline's other axis)
+
+
+def conv_bytes(l: Layer, n: int, epilogue: int = 0) -> int:
+    """Compulsory bytes of one conv launch over n images: input
+    read once, output written once (a quarter with the fused 2x2 pool), the
+    skip map read once with an ADD epilogue, the weights read once (unpadded
+    channel counts)."""
+    out = l.c_o * l.h_o * l.w_o
+    if epilogue & _abi.EPI_MAXPOOL:
+        out //= 4
+    skip = l.c_o * l.h_o * l.w_o if epilogue & _abi.EPI_ADD else 0
+    return 4 * (n * (l.c_i * l.h_i * l.w_i + out + skip) + l.c_i * l.c_o * l.h_f * l.w_f)
+
+
+def pool_bytes(a: "Act") -> int:
+    """2x2/s2 max-pool of a map: read it once, write a quarter."""
+    return 4 * a.n * a.c * a.h * a.w * 5 // 4
 
 
 def _sm_count() -> int:
@@ -469,10 +487,12 @@ class Plan:
                 self.steps.append(Step(
                     lambda st: check(lib().dconv_cuda_pack_feature_map(
                         ptr(x), n, l.c_i, l.h_i, l.w_i, CB, 0, ptr(xb.buf), stream_ptr(st))),
-                    f"pack_{l.name}", "pack"))
+                    f"pack_{l.name}", "pack",
+                    bytes=4 * n * l.h_i * l.w_i * (l.c_i + nblk(l.c_i) * CB)))
                 self.steps.append(Step(lambda st: conv_tf32(lb, n, xb, wp, y, epilogue, skip, st,
                                                             x3=self.x3),
-                                       l.name, "tf32", n * l.flops, l))
+                                       l.name, "tf32", n * l.flops, l,
+                                       conv_bytes(lb, n, epilogue)))
                 return y
             if tc and not l.first:
                 # stride 1, 1x1 of any stride, and k x k stride s (the C-ABI
@@ -481,11 +501,13 @@ class Plan:
                 self.weights[l.name + ".tf32"] = wp
                 self.steps.append(Step(lambda st: conv_tf32(l, self.n, x, wp, y, epilogue, skip, st,
                                                             in_view, x3=self.x3),
-                                       l.name, "tf32", self.n * l.flops, l))
+                                       l.name, "tf32", self.n * l.flops, l,
+                                       conv_bytes(l, self.n, epilogue)))
                 return y
             self.steps.append(Step(lambda st: conv(l, self.n, x, w, y, epilogue, skip, st, in_view,
                                                    tile_variant=self.tiles.get(l.name, 0)),
-                                   l.name, kind, self.n * l.flops, l))
+                                   l.name, kind, self.n * l.flops, l,
+                                   conv_bytes(l, self.n, epilogue)))
             return y
         from .shard import block_range
         rank, world, _ = self.shard
@@ -587,10 +609,10 @@ class Plan:
         self.steps.append(Step(
             lambda st: check(lib().dconv_cuda_pack_space_to_depth(
                 ptr(x), n, l.c_i, l.h_i, l.w_i, f, ptr(xb.buf), stream_ptr(st))),
-            f"pack_{l.name}", "pack"))
+            f"pack_{l.name}", "pack", bytes=4 * n * (l.c_i * l.h_i * l.w_i + cs * hs * ws)))
         self.steps.append(Step(lambda st: conv_tf32(lb, n, xb, wp, y, epilogue, skip, st,
                                                     x3=self.x3),
-                               l.name, "tf32", n * l.flops, l))
+                               l.name, "tf32", n * l.flops, l, conv_bytes(lb, n, epilogue)))
         return y
 
     def pool_into(self, name: str, src_local: Act, z: Act) -> None:
@@ -598,7 +620,8 @@ class Plan:
         if self.shard is None or self.gather_mode == "emulate":
             # (emulate: src_local is the full map every rank's conv wrote;
             # pooling it equals pooling the slices -- max is exact)
-            self.steps.append(Step(lambda st: maxpool_into(src_local, z, st), name, "pool"))
+            self.steps.append(Step(lambda st: maxpool_into(src_local, z, st), name, "pool",
+                                   bytes=pool_bytes(src_local)))
             return
         if self.gather_mode == "emulate_peer":
             from .shard import block_range
