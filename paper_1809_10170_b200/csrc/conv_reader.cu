@@ -333,17 +333,30 @@ int pick_width(const GenericParams& g, cudaStream_t stream) {
   // tile width 32 unless the map width wastes less with 16 (112 = 7 x 16)
   const int waste32 = (g.w_o + 31) / 32 * 32 - g.w_o;
   const int waste16 = (g.w_o + 15) / 16 * 16 - g.w_o;
+  const bool w16 = waste16 < waste32;
+  const int sms = dconv_host::device_sms(dconv_host::current_device());
+  const int64_t groups = (g.jb_count + kBlocks - 1) / kBlocks;
+  auto tiles = [&](int tw, int r) {
+    const int th = r * (32 / tw);
+    return (int64_t)g.n * ((g.h_o + th - 1) / th) * ((g.w_o + tw - 1) / tw) * groups;
+  };
+  // few tiles (batch-1 maps): 2 accumulator rows per thread, 4x the tiles
+  if (WF > 7 || tiles(w16 ? 16 : 32, 8) < sms) {
+    if (w16) return launch_reader<3, S, WF, 16, 2, 1>(g, stream);
+    return launch_reader<3, S, WF, 32, 2, 1>(g, stream);
+  }
   // 3x3: two CTAs per SM (one CTA's barrier / epilogue overlaps the other's
-  // FFMA2s; 120 registers).  Wide filters (7x7/s2): one CTA per SM with the
-  // full register file -- measured on B200 (GoogLeNet stem b64 / b256):
-  // 304 / 1146 us against 309 / 1193 us with two CTAs of 4-row threads.
-  if constexpr (WF > 3) {
-    if (waste16 < waste32) return launch_reader<3, S, WF, 16, 8, 1>(g, stream);
+  // FFMA2s; 120 registers).  7x7/s2: one CTA per SM with the full register
+  // file -- measured on B200 (GoogLeNet stem b64 / b256): 304 / 1146 us
+  // against 309 / 1193 us with two CTAs of 4-row threads.
+  if constexpr (WF == 7) {
+    if (w16) return launch_reader<3, S, WF, 16, 8, 1>(g, stream);
     return launch_reader<3, S, WF, 32, 8, 1>(g, stream);
-  } else {
-    if (waste16 < waste32) return launch_reader<3, S, WF, 16, 8, 2>(g, stream);
+  } else if constexpr (WF == 3) {
+    if (w16) return launch_reader<3, S, WF, 16, 8, 2>(g, stream);
     return launch_reader<3, S, WF, 32, 8, 2>(g, stream);
   }
+  return DCONV_EUNSUPPORTED;
 }
 
 }  // namespace
@@ -352,12 +365,9 @@ int launch_conv_reader(const GenericParams& g, cudaStream_t stream) {
   // many-tile layers with a ReLU / plain epilogue written to this rank's map only
   if (g.c_ob != 8 || g.c_i != 3 || g.h_f != g.w_f || g.n_peers || (g.epi & ~DCONV_EPI_RELU))
     return DCONV_EUNSUPPORTED;
-  const int sms = dconv_host::device_sms(dconv_host::current_device());
-  const int64_t tiles = (int64_t)g.n * ((g.h_o + 7) / 8) * ((g.w_o + 31) / 32) *
-                        ((g.jb_count + kBlocks - 1) / kBlocks);
-  if (tiles < 2 * sms) return DCONV_EUNSUPPORTED;  // batch-1 maps: the split reader
   if (g.s == 1 && g.w_f == 3) return pick_width<1, 3>(g, stream);
   if (g.s == 2 && g.w_f == 7) return pick_width<2, 7>(g, stream);
+  if (g.s == 4 && g.w_f == 11) return pick_width<4, 11>(g, stream);
   return DCONV_EUNSUPPORTED;
 }
 

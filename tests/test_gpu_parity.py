@@ -1187,3 +1187,24 @@ def test_ffma_wide_channel_blocks(cb, tv, monkeypatch):
         for i in range(n):
             want = np.maximum(po.pack_feature_map(po.conv_oracle64(x[i], k, s), cb) + skip_np[i], 0)
             assert_tol(got[i], want, f"c_b {cb} tile {tv} case {t} img {i}")
+
+
+@pytest.mark.parametrize("f,s,h,co,n", [(11, 4, 227, 96, 1), (7, 2, 229, 64, 1), (3, 1, 226, 64, 1),
+                                         (11, 4, 51, 40, 3), (3, 1, 30, 72, 2)])
+def test_first_layer_tma_reader_few_tiles(f, s, h, co, n):
+    """The TMA-store reader's few-tile form (2 accumulator rows per thread:
+    batch-1 stems incl. AlexNet's 11x11/s4) -- every element against the
+    fp64 GPU referee, halo untouched."""
+    from oracle import gpu_oracle as go
+    l = nets.Layer("r", 3, co, h, h, f, f, s, first=True)
+    xd = torch.empty((n, 3, h, h), device="cuda")
+    nets._fill(xd, 71 + f, co)
+    wd = torch.empty((3, co, f, f), device="cuda")
+    nets._fill(wd, 72 + f, co)
+    y = nets.Act(n, co, l.h_o, l.w_o, halo=1)
+    nets.conv(l, n, xd, nets.pack_weights(wd, True), y, _abi.EPI_RELU)
+    torch.cuda.synchronize()
+    want = go.conv64_act(xd, l, wd).clamp_min(0.0)
+    ok, nbad, err, ratio = go.check_tol(y.buf[:, :, 1:-1, 1:-1, :], want)
+    assert ok, f"{nbad} bad, max err {err}"
+    assert not y.buf[:, :, 0].any() and not y.buf[:, :, :, -1].any()
