@@ -326,6 +326,18 @@ def pool_bytes(a: "Act") -> int:
     return 4 * a.n * a.c * a.h * a.w * 5 // 4
 
 
+def _on_stream(st):
+    """Context that makes torch's current stream the plan's launch stream
+    (collectives and symmetric-memory barriers are enqueued on the current
+    stream; the conv kernels on the stream a step is given)."""
+    import contextlib
+    if st is None:
+        return contextlib.nullcontext()
+    if isinstance(st, torch.cuda.Stream):
+        return torch.cuda.stream(st)
+    return torch.cuda.stream(torch.cuda.ExternalStream(int(st)))
+
+
 def _sm_count() -> int:
     """SMs of the current device (148 on B200; the CPU tests have no GPU)."""
     if torch.cuda.is_available():
@@ -452,13 +464,20 @@ class Plan:
 
     def _barrier(self, name: str, full: Act) -> None:
         h = full.symm
-        self.steps.append(Step(lambda st: h.barrier(channel=0), f"barrier_{name}", "barrier"))
+
+        def run(st):
+            with _on_stream(st):  # ordered after this rank's stores on the plan's stream
+                h.barrier(channel=0)
+        self.steps.append(Step(run, f"barrier_{name}", "barrier"))
 
     def _gather(self, name: str, full: Act, local: Act) -> None:
         from .shard import all_gather_blocks
         group = self.shard[2]
-        self.steps.append(Step(lambda st: all_gather_blocks(full.buf[0], local.buf[0], group),
-                               f"gather_{name}", "gather"))
+
+        def run(st):
+            with _on_stream(st):  # NCCL enqueues on the current stream: the plan's
+                all_gather_blocks(full.buf[0], local.buf[0], group)
+        self.steps.append(Step(run, f"gather_{name}", "gather"))
 
     def conv_into(self, l: Layer, x, y: Act, epilogue: int = 0, skip: Optional[Act] = None,
                   gather: bool = True, in_view=None) -> Act:

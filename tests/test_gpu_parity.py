@@ -456,6 +456,14 @@ def test_co_shard_plan_world1_matches_unsharded():
         torch.cuda.synchronize()
         assert any(s.kind == "gather" for s in b.steps)
         assert torch.equal(a.output.buf, b.output.buf)
+        # on a side stream (as bench.py runs plans): the all-gathers must be
+        # ordered after the convs on that stream, not on torch's current one
+        b.output.buf.zero_()
+        side = torch.cuda.Stream()
+        for _ in range(3):
+            b.run(side)
+        side.synchronize()
+        assert torch.equal(a.output.buf, b.output.buf)
     finally:
         dist.destroy_process_group()
 

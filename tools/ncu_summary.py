@@ -2,7 +2,9 @@
 summaries: the per-launch list of one VGG-16 b32 step with each kernel's
 share, and the key `--set full` counters of the top conv kernels.
 
-usage: python tools/ncu_summary.py gpurun_out/round profiles r1
+usage: python tools/ncu_summary.py gpurun_out/round profiles r2
+(full captures are read from the .ncu-rep, or from the `--page raw --csv`
+text export NAME.raw.csv plus NAME.src.csv that tools/profile_round.sh keeps)
 """
 import csv
 import json
@@ -74,9 +76,38 @@ def step_summary(ls, first="conv_first"):
     }
 
 
+def stall_by_opcode(src_csv: str, top: int = 4):
+    """Sampled warp stalls of a capture's source page, per stall reason: the
+    opcodes they sit on (e.g. long_scoreboard on the BRA of an mbarrier
+    try_wait loop = a producer / epilogue warp idling, not the math warps)."""
+    rows = list(csv.reader(open(src_csv)))
+    h = rows[1]
+    body = rows[2:]
+    i_src = h.index("Source")
+    cols = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
+    per = defaultdict(lambda: defaultdict(int))
+    for x in body:
+        ops = [o for o in x[i_src].split() if not o.startswith("@")]
+        k = ops[0].split(".")[0] if ops else "?"
+        for c in cols:
+            v = int(x[h.index(c)] or 0)
+            if v:
+                per[c][k] += v
+    tot = sum(sum(d.values()) for d in per.values())
+    out = {}
+    for c in sorted(per, key=lambda c: -sum(per[c].values()))[:8]:
+        n = sum(per[c].values())
+        out[c] = {"share": round(n / tot, 3),
+                  "top_opcodes": dict(sorted(per[c].items(), key=lambda kv: -kv[1])[:top])}
+    return out
+
+
 def full_metrics(rep: str):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    if rep.endswith(".raw.csv"):
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     h, units, vals = rows[0], rows[1], rows[2]
     d = {"Kernel Name": vals[h.index("Kernel Name")]}
@@ -93,29 +124,48 @@ def full_metrics(rep: str):
             except ValueError:
                 pass
     d["top_stalls_per_issue"] = sorted(stalls, key=lambda t: -t[1])[:8]
+    src = rep.replace(".raw.csv", ".src.csv")
+    if src != rep and os.path.exists(src):
+        d["sampled_stalls_by_opcode"] = stall_by_opcode(src)
     return d
+
+
+def find_rep(src: str, name: str):
+    for ext in (".ncu-rep", ".raw.csv"):
+        p = os.path.join(src, name + ext)
+        if os.path.exists(p):
+            return p
+    return None
 
 
 def main():
     src, dst, tag = sys.argv[1], sys.argv[2], sys.argv[3]
     ls = launches(os.path.join(src, "launches_vgg16.csv"))
-    summ = step_summary(ls)
+    summ = step_summary(ls, first="conv_reader")
     summ["source"] = ("ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 "
                       "python bench.py --steps 2 --warmup 3 --no-cpu-baseline (cold-cache, "
                       "serialised launches; the share is what must agree with bench.py)")
     json.dump(summ, open(os.path.join(dst, f"{tag}_ncu_launches_vgg16_b32.json"), "w"), indent=1)
     full = {}
-    for name, rep in (("vgg16_conv1_2_b32", "full_conv1_2.ncu-rep"),
-                      ("vgg16_conv4_2_b32", "full_conv4_2.ncu-rep")):
-        p = os.path.join(src, rep)
-        if os.path.exists(p):
+    for name, rep in (("vgg16_conv1_2_b32", "full_conv1_2"),
+                      ("vgg16_conv4_2_b32", "full_conv4_2")):
+        p = find_rep(src, rep)
+        if p:
             full[name] = full_metrics(p)
     json.dump(full, open(os.path.join(dst, f"{tag}_ncu_full_conv_ffma.json"), "w"), indent=1)
+    rd = {}
+    for name, rep in (("vgg16_conv1_1_b32", "full_reader_conv1_1"),
+                      ("googlenet_stem_7x7s2_b64", "full_reader_stem")):
+        p = find_rep(src, rep)
+        if p:
+            rd[name] = full_metrics(p)
+    if rd:
+        json.dump(rd, open(os.path.join(dst, f"{tag}_ncu_full_conv_reader.json"), "w"), indent=1)
     x3 = {}
-    for name, rep in (("vgg16_conv4_2_b32", "full_x3_conv4_2.ncu-rep"),
-                      ("resnet50_1x1_1024_256_b256", "full_x3_r50_1x1.ncu-rep")):
-        p = os.path.join(src, rep)
-        if os.path.exists(p):
+    for name, rep in (("vgg16_conv4_2_b32", "full_x3_conv4_2"),
+                      ("resnet50_1x1_1024_256_b256", "full_x3_r50_1x1")):
+        p = find_rep(src, rep)
+        if p:
             x3[name] = full_metrics(p)
     if x3:
         json.dump(x3, open(os.path.join(dst, f"{tag}_ncu_full_conv_tf32x3.json"), "w"), indent=1)
