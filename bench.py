@@ -287,7 +287,7 @@ def run_reference_arm(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    cb = cpu_reference(args.config, args.cpu_seconds * 2, runs=1)
+    cb = cpu_reference(args.config, args.cpu_seconds, runs=2)
     batch = args.batch or DEFAULT_BATCH[args.config]
     line = {
         "metric": METRIC, "impl": "reference", "value": cb["value"],
