@@ -7,11 +7,10 @@ import sys
 import torch
 
 sys.path.insert(0, ".")
-from paper_1809_10170_b200 import _abi, nets  # noqa: E402
+from paper_1809_10170_b200 import nets  # noqa: E402
 
 
 def main(config="vgg16", batch=32, reps=5):
-    lib = _abi.lib()
     seen = {}
     for l in nets.CONFIGS[config]:
         if l.first:
@@ -25,20 +24,18 @@ def main(config="vgg16", batch=32, reps=5):
         wb = nets.pack_weights(w, False)
         y = nets.Act(batch, l.c_o, l.h_o, l.w_o)
         res = {}
-        for v in (0, 1):
-            _abi.check(lib.dconv_cuda_set_ffma_variant(v))
+        for v in (1, 2, 3):  # dconv_conv_desc.tile_variant
             ts = []
             for r in range(reps + 1):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record()
-                nets.conv(l, batch, x, wb, y)
+                nets.conv(l, batch, x, wb, y, tile_variant=v)
                 b.record()
                 b.synchronize()
                 if r:
                     ts.append(a.elapsed_time(b))
             ms = statistics.median(ts)
             res[v] = round(batch * l.flops / (ms * 1e-3) / 1e12, 2)
-        lib.dconv_cuda_set_ffma_variant(-1)
         seen[key] = res
         print(json.dumps({"layer": l.name, "shape": key, "tflops_by_variant": res}), flush=True)
 
