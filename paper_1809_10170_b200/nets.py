@@ -489,30 +489,11 @@ class Plan:
             tc = self.algo in TC_ALGOS and not (self.x3 and self._few_units(l, epilogue))
             if tc and l.first and l.s > 1 and in_view is None:
                 return self._tf32_s2d_first(l, x, y, epilogue, skip)
-            if tc and l.first and l.s == 1 and in_view is None:
-                # TF32 path, stride-1 first layer (VGG conv1_1): zero-pad the
-                # image to one 8-channel block (a pack kernel, SPEC.md:121's
-                # first-layer choice) and run it as a blocked tcgen05 layer;
-                # FLOPs are still counted with the real C_i
-                lb = Layer(l.name, l.c_i, l.c_o, l.h_i, l.w_i, l.h_f, l.w_f, l.s, False)
-                dense = torch.empty((l.c_i, l.c_o, l.h_f, l.w_f), dtype=torch.float32,
-                                    device=w.device)
-                check(lib().dconv_cuda_unpack_kernel(ptr(w), l.c_i, l.c_o, l.h_f, l.w_f, CB, l.c_i,
-                                                     ptr(dense), stream_ptr(None)))
-                wp = prepare_tf32(lb, pack_weights(dense, False), x3=self.x3)
-                self.weights[l.name + ".tf32"] = wp
-                xb = Act(self.n, l.c_i, l.h_i, l.w_i, device=w.device)
-                n = self.n
-                self.steps.append(Step(
-                    lambda st: check(lib().dconv_cuda_pack_feature_map(
-                        ptr(x), n, l.c_i, l.h_i, l.w_i, CB, 0, ptr(xb.buf), stream_ptr(st))),
-                    f"pack_{l.name}", "pack",
-                    bytes=4 * n * l.h_i * l.w_i * (l.c_i + nblk(l.c_i) * CB)))
-                self.steps.append(Step(lambda st: conv_tf32(lb, n, xb, wp, y, epilogue, skip, st,
-                                                            x3=self.x3),
-                                       l.name, "tf32", n * l.flops, l,
-                                       conv_bytes(lb, n, epilogue)))
-                return y
+            # (stride-1 first layers -- VGG conv1_1 -- run on the FFMA
+            # first-layer reader below in the tensor-core plans too: it reads
+            # the dense image in place, where the tcgen05 kernel would need a
+            # channel-padded copy of it, and is as fast: 0.14 ms against
+            # 0.03 ms pack + 0.14 ms split-TF32 at VGG b32)
             if tc and not l.first:
                 # stride 1, 1x1 of any stride, and k x k stride s (the C-ABI
                 # reads the space-to-depth view of the input in place)

@@ -834,22 +834,18 @@ def test_autotuned_plan_matches_default_tiles():
         assert float(np.abs(x - y).max()) <= 1e-5 * scale + 1e-4, name
 
 
-def test_tf32_first_layer_packs_and_matches_ffma_plan():
-    """TF32 plans run VGG's stride-1 first layer as pack (8-channel block,
-    zero-padded) + tcgen05 conv; its output equals the FFMA first-layer
-    reader's within the TF32 bound."""
+def test_tf32_plans_read_the_stride1_first_layer_in_place():
+    """Tensor-core plans run VGG's stride-1 first layer on the FFMA
+    first-layer reader (dense image read in place: no padded copy, no pack
+    launch); its output is the FFMA plan's, bit for bit."""
     a = nets.build_plan("vgg16", 1, seed=13)
-    b = nets.build_plan("vgg16", 1, seed=13, algo="tf32")
-    assert [s.kind for s in b.steps[:2]] == ["pack", "tf32"]
-    a.run()
-    b.run()
-    torch.cuda.synchronize()
-    ya, yb = host(a.outputs["conv1_1"].buf), host(b.outputs["conv1_1"].buf)
-    l = nets.VGG16[0]
-    x = host(a.input)[0]
-    k = po.unpack_kernel(host(a.weights[l.name]), l.c_i, l.c_o)
-    bound = 2.0 ** -9 * po.pack_feature_map(po.conv_oracle64(np.abs(x), np.abs(k), 1), 8) + 1e-5
-    assert (np.abs(ya[0, :, 1:-1, 1:-1] - yb[0, :, 1:-1, 1:-1]) <= 2 * bound).all()
+    for algo in ("tf32", "tf32x3"):
+        b = nets.build_plan("vgg16", 1, seed=13, algo=algo)
+        assert b.steps[0].kind == "first" and not any(s.kind == "pack" for s in b.steps)
+        a.run()
+        b.run()
+        torch.cuda.synchronize()
+        assert torch.equal(a.outputs["conv1_1"].buf, b.outputs["conv1_1"].buf), algo
 
 
 @pytest.mark.parametrize("config,name", [("googlenet", "conv1_7x7_s2"), ("alexnet", "conv1")])
