@@ -436,6 +436,23 @@ class Plan:
             return [a.buf for a in self.outputs.values()]
         return [self.output.buf]
 
+    def io_map(self):
+        """(inputs, outputs): [(device tensor, index of the step that reads it
+        last)] and [(device tensor, index of the step that writes it)] -- the
+        points after which a streamed batch may refill an input buffer, and
+        before which the previous batch's result must have left."""
+        names = [s.name for s in self.steps]
+        ins = []
+        if self.input is not None:  # read by the first launch (a reader or a repack)
+            ins.append((self.input, 0))
+        for name, a in self.per_layer_inputs.items():
+            ins.append((a.buf, names.index(name)))
+        if self.per_layer_inputs:
+            outs = [(a.buf, names.index(name)) for name, a in self.outputs.items()]
+        else:
+            outs = [(self.output.buf, len(self.steps) - 1)]
+        return ins, outs
+
     # -- building blocks ----------------------------------------------------
     def _local(self, full: Act, c: int) -> Act:
         return Act(self.n, c, full.h, full.w, halo=full.halo, pad_hi_only=full.pad_hi_only,
@@ -656,6 +673,70 @@ class Plan:
         zs = self._local(z, src_local.c)
         self.steps.append(Step(lambda st: maxpool_into(src_local, zs, st), name, "pool"))
         self._gather(name, z, zs)
+
+
+class Pipeline:
+    """Streams batches through a plan the way a server would: the host->device
+    copy of batch i+1 (pinned host buffers, a copy stream) starts as soon as
+    batch i's kernels have consumed that input buffer, and the device->host
+    copy of batch i's result overlaps batch i+1's kernels; only the first
+    copy in and the last copy out are exposed.  Every batch still moves all
+    of its bytes both ways.  Synchronisation is by CUDA events on three
+    streams (compute, copy in, copy out); the plan's own buffers are reused
+    (an input buffer is refilled only after its consuming launch, an output
+    buffer overwritten only after its previous copy-out)."""
+
+    def __init__(self, plan: Plan, host_inputs: List[torch.Tensor],
+                 host_outputs: List[torch.Tensor], stream=None):
+        self.plan = plan
+        self.ins, self.outs = plan.io_map()
+        if len(host_inputs) != len(self.ins) or len(host_outputs) != len(self.outs):
+            raise ValueError("Pipeline: one host buffer per plan input / output")
+        self.h_in, self.h_out = host_inputs, host_outputs
+        self.compute = stream or torch.cuda.Stream()
+        self.copy_in, self.copy_out = torch.cuda.Stream(), torch.cuda.Stream()
+        ev = lambda: torch.cuda.Event()  # noqa: E731
+        self.in_ready = [ev() for _ in self.ins]      # H2D of the current batch done
+        self.in_free = [ev() for _ in self.ins]       # its consumer launch done
+        self.out_ready = [ev() for _ in self.outs]    # producer launch done
+        self.out_free = [ev() for _ in self.outs]     # D2H of the previous batch done
+        self.consumer = {i: k for k, (_, i) in enumerate(self.ins)}
+        self.producer = {i: k for k, (_, i) in enumerate(self.outs)}
+
+    def _h2d(self, k: int, after_consumer: bool) -> None:
+        with torch.cuda.stream(self.copy_in):
+            if after_consumer:
+                self.copy_in.wait_event(self.in_free[k])
+            self.ins[k][0].copy_(self.h_in[k], non_blocking=True)
+            self.in_ready[k].record(self.copy_in)
+
+    def run(self, batches: int) -> None:
+        """Enqueue `batches` batches (asynchronous; synchronise the streams or
+        `done()` to wait)."""
+        for k in range(len(self.ins)):
+            self._h2d(k, after_consumer=False)
+        for b in range(batches):
+            for i, st in enumerate(self.plan.steps):
+                if i in self.consumer:
+                    self.compute.wait_event(self.in_ready[self.consumer[i]])
+                if i in self.producer and b > 0:
+                    self.compute.wait_event(self.out_free[self.producer[i]])
+                st.fn(self.compute)
+                if i in self.consumer:
+                    k = self.consumer[i]
+                    self.in_free[k].record(self.compute)
+                    if b + 1 < batches:
+                        self._h2d(k, after_consumer=True)
+                if i in self.producer:
+                    k = self.producer[i]
+                    self.out_ready[k].record(self.compute)
+                    with torch.cuda.stream(self.copy_out):
+                        self.copy_out.wait_event(self.out_ready[k])
+                        self.h_out[k].copy_(self.outs[k][0], non_blocking=True)
+                        self.out_free[k].record(self.copy_out)
+
+    def streams(self):
+        return self.compute, self.copy_in, self.copy_out
 
 
 def _fill(t: torch.Tensor, seed: int, stream_id: int, scale: float = 1.0) -> None:

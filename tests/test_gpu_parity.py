@@ -1212,3 +1212,29 @@ def test_first_layer_tma_reader_few_tiles(f, s, h, co, n):
     ok, nbad, err, ratio = go.check_tol(y.buf[:, :, 1:-1, 1:-1, :], want)
     assert ok, f"{nbad} bad, max err {err}"
     assert not y.buf[:, :, 0].any() and not y.buf[:, :, :, -1].any()
+
+
+@pytest.mark.parametrize("config", ["vgg16", "googlenet"])
+def test_pipeline_streams_batches(config):
+    """nets.Pipeline (the streaming e2e path): copies of neighbouring batches
+    overlap the kernels, yet every batch's result is the plan's own.  The
+    host input is then halved: conv, ReLU and max-pool are positively
+    homogeneous and x/2 is exact, so the streamed result must be exactly half
+    -- a stale input buffer or an early copy-out would show."""
+    plan = nets.build_plan(config, 2, seed=44)
+    plan.run()
+    torch.cuda.synchronize()
+    ref = [t.clone() for t in plan.io_outputs()]
+    h_in = [t.cpu().pin_memory() for t in plan.io_inputs()]
+    h_out = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in plan.io_outputs()]
+    pipe = nets.Pipeline(plan, h_in, h_out)
+    pipe.run(3)
+    torch.cuda.synchronize()
+    for h, r in zip(h_out, ref):
+        assert torch.equal(h, r.cpu())
+    for h in h_in:
+        h.mul_(0.5)
+    pipe.run(2)
+    torch.cuda.synchronize()
+    for h, r in zip(h_out, ref):
+        assert torch.equal(h, (0.5 * r).cpu())
