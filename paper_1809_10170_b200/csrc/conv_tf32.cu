@@ -189,13 +189,20 @@ __global__ void __launch_bounds__(kThreadsT, 1)
         const uint32_t b_tap = (uint32_t)(2 * p.N);          // next (n, m) tap
         uint32_t accum = st == 0 ? 0u : 1u;
         const int wf = WF_T > 0 ? WF_T : p.w_f;
+        // space-to-depth: skip the taps of this stage's phase that multiply
+        // structurally zero weights (the first MMA of a unit is always issued
+        // so the accumulator is initialised)
+        int nmax, mmax;
+        s2d_valid_taps(p, g * p.G, nmax, mmax);
         for (int gi = 0; gi < Ge; ++gi)
           for (int n = 0; n < Re; ++n) {
+            const bool row_ok = r * p.R + n < nmax;
             const uint32_t arow = a_lo0 + (uint32_t)((gi * p.PH + n) * p.PW);
             const uint32_t brow = b_lo0 + (uint32_t)((gi * p.R + n) * wf) * b_tap;
             if (MT_T > 0 && mts == MT_T) {
 #pragma unroll
               for (int m = 0; m < (WF_T > 0 ? WF_T : 1); ++m) {
+                if (accum && !(row_ok && m < mmax)) continue;
 #pragma unroll
                 for (int mt = 0; mt < MT_T; ++mt)
                   umma_tf32_elect(acc_base + (uint32_t)(mt * p.N),
@@ -205,15 +212,18 @@ __global__ void __launch_bounds__(kThreadsT, 1)
               }
               if (WF_T > 0) continue;
               for (int m = 1; m < wf; ++m) {
+                if (accum && !(row_ok && m < mmax)) continue;
 #pragma unroll
                 for (int mt = 0; mt < MT_T; ++mt)
                   umma_tf32_elect(acc_base + (uint32_t)(mt * p.N),
                                   arow + (uint32_t)m + (uint32_t)mt * a_mt, a_hi,
-                                  brow + (uint32_t)m * b_tap, b_hi, p.idesc, 1u);
+                                  brow + (uint32_t)m * b_tap, b_hi, p.idesc, accum);
+                accum = 1u;
               }
               continue;
             }
             for (int m = 0; m < wf; ++m) {
+              if (accum && !(row_ok && m < mmax)) continue;
               const uint32_t blo = brow + (uint32_t)m * b_tap;
               uint32_t alo = arow + (uint32_t)m;
               for (int mt = 0; mt < mts; ++mt, alo += a_mt)
@@ -343,7 +353,7 @@ int launch_prepare_tf32(const float* w, int ib_n, int h_f, int w_f, int jb_begin
 }
 
 int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t stream) {
-  FfmaParams f = f0;
+  FfmaParams f = f0;  // (f0: the original filter, before the space-to-depth view)
   InView view;
   if (int rc = prepare_view(f, view, "conv_tf32")) return rc;
   Tf32Params p{};
@@ -351,6 +361,8 @@ int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t
   copy_geometry(p, f);
   p.s2d = view.s2d;
   p.ib_o = view.ib;
+  p.hf_o = f0.h_f;
+  p.wf_o = f0.w_f;
   p.N = tf32_channels(f.jb_count);
   p.n_cg = (f.jb_count * 8 + p.N - 1) / p.N;
   // stage = G input blocks x R filter rows, <= 48 KB of weights

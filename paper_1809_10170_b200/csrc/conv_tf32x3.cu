@@ -230,12 +230,19 @@ __global__ void __launch_bounds__(kThreadsX, 1)
         const uint32_t b_rem = (uint32_t)(2 * p.N);             // lo weights of a tap
         const int wf = WF_T > 0 ? WF_T : p.w_f;
         constexpr int kMtLoop = MT_T > 0 ? MT_T : kMaxMT;
+        // space-to-depth: skip the taps of this stage's phase that multiply
+        // structurally zero weights (the first MMA of a chunk is always
+        // issued, initialising its accumulator set)
+        int nmax, mmax;
+        s2d_valid_taps(p, g * p.G, nmax, mmax);
         for (int gi = 0; gi < Ge; ++gi)
           for (int n = 0; n < Re; ++n) {
+            const bool row_ok = r * p.R + n < nmax;
             const uint32_t arow = a_lo0 + (uint32_t)((gi * p.PH + n) * p.PW);
             const uint32_t brow = b_lo0 + (uint32_t)((gi * p.R + n) * wf) * b_tap;
 #pragma unroll
             for (int m = 0; m < (WF_T > 0 ? WF_T : 1); ++m) {
+              if (accum && !(row_ok && m < mmax)) continue;
 #pragma unroll
               for (int mt = 0; mt < kMtLoop; ++mt) {
                 if (mt >= mts) break;
@@ -257,20 +264,22 @@ __global__ void __launch_bounds__(kThreadsX, 1)
             }
             if (WF_T > 0) continue;
             for (int m = 1; m < wf; ++m) {
+              if (accum && !(row_ok && m < mmax)) continue;
               for (int mt = 0; mt < mts; ++mt) {
                 const uint32_t a = arow + (uint32_t)m + (uint32_t)mt * a_mt;
                 const uint32_t b = brow + (uint32_t)m * b_tap;
                 if constexpr (DA) {
                   const uint32_t d = acc_base + (uint32_t)(mt * 2 * p.N);
-                  umma_tf32_elect(d, a, a_hi, b, b_hi, p.idesc2, 1u);
+                  umma_tf32_elect(d, a, a_hi, b, b_hi, p.idesc2, accum);
                   umma_tf32_elect(d + (uint32_t)p.N, a + a_rem, a_hi, b, b_hi, p.idesc, 1u);
                 } else {
                   const uint32_t d = acc_base + (uint32_t)(mt * p.N);
-                  umma_tf32_elect(d, a, a_hi, b + b_rem, b_hi, p.idesc, 1u);
+                  umma_tf32_elect(d, a, a_hi, b + b_rem, b_hi, p.idesc, accum);
                   umma_tf32_elect(d, a + a_rem, a_hi, b, b_hi, p.idesc, 1u);
                   umma_tf32_elect(d, a, a_hi, b, b_hi, p.idesc, 1u);
                 }
               }
+              accum = 1u;
             }
           }
         umma_commit_elect(&empty[buf]);  // stage smem free once these MMAs retire
@@ -502,7 +511,7 @@ int launch_prepare_tf32x3(const float* w, int ib_n, int h_f, int w_f, int jb_beg
 }
 
 int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream_t stream) {
-  FfmaParams f = f0;
+  FfmaParams f = f0;  // (f0: the original filter, before the space-to-depth view)
   InView view;
   if (int rc = prepare_view(f, view, "conv_tf32x3")) return rc;
   Tf32Params p{};
@@ -510,6 +519,8 @@ int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream
   copy_geometry(p, f);
   p.s2d = view.s2d;
   p.ib_o = view.ib;
+  p.hf_o = f0.h_f;
+  p.wf_o = f0.w_f;
   p.N = tf32_channels(f.jb_count);
   p.n_cg = (f.jb_count * 8 + p.N - 1) / p.N;
   const int sms = sm_count();

@@ -36,6 +36,7 @@ struct Tf32Params {
   int MT;             // M-tiles per unit (1..4)
   int chunk_st;       // split-TF32: stages per TMEM accumulator chunk
   int s2d, ib_o;      // in-place space-to-depth factor (1 = off); original input blocks
+  int hf_o, wf_o;     // original filter (s2d: taps s*n'+dy >= hf_o are structurally zero)
   int stack;          // images stacked along the tile rows (small maps), 1 = off
   int SP;             // stacked mode: patch rows per image slot (h_o + R - 1)
   uint32_t idesc;
@@ -320,6 +321,22 @@ __device__ __forceinline__ void tma_block_coords(const Tf32Params& p, int img, i
   cx = s * x0 + dx;
   cy = s * y + dy;
   c4 = img * p.ib_o + b;
+}
+
+// Space-to-depth layers: a stage holds input blocks of one phase (dy, dx);
+// its taps (n', m') with s*n'+dy >= hf_o or s*m'+dx >= wf_o multiply zero
+// weights.  Returns the valid tap rows / columns of the stage's phase (the
+// MMA issuers skip the rest: 3x3/s2 computes 9 of 16 taps, 7x7/s2 49 of 64).
+__device__ __forceinline__ void s2d_valid_taps(const Tf32Params& p, int ib0, int& nmax,
+                                               int& mmax) {
+  if (p.s2d <= 1) {
+    nmax = p.h_f;
+    mmax = p.w_f;
+    return;
+  }
+  const int phase = ib0 / p.ib_o, dy = phase / p.s2d, dx = phase - dy * p.s2d;
+  nmax = (p.hf_o - dy + p.s2d - 1) / p.s2d;
+  mmax = (p.wf_o - dx + p.s2d - 1) / p.s2d;
 }
 
 inline void copy_geometry(Tf32Params& p, const FfmaParams& f) {
