@@ -64,8 +64,9 @@ def parse(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="vgg16", choices=sorted(DEFAULT_BATCH))
     ap.add_argument("--batch", type=int, default=0, help="global batch (0 = config default)")
-    ap.add_argument("--extra", default="cfg1,alexnet,googlenet,resnet50",
-                    help="other configs measured in the same run (comma list, 'none')")
+    ap.add_argument("--extra", default="cfg1,alexnet,googlenet,resnet50,vgg16:1,googlenet:1,resnet50:1",
+                    help="other configs measured in the same run: comma list of CONFIG "
+                         "(BASELINE batch) or CONFIG:BATCH; 'none'")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-tune", action="store_true",
@@ -670,7 +671,9 @@ def measure_config(ctx, args, config: str, batch: int, headline: bool) -> dict:
             if s.flops:
                 rec["flop_per_byte"] = round(s.flops / s.bytes, 1)
         layers.append(rec)
-    fits_l2 = config in ("cfg1", "alexnet")
+    # working set ~ the compulsory bytes of one step against the 126 MB L2
+    ws_bytes = sum(s.bytes for s in plan.steps)
+    fits_l2 = ws_bytes < 126e6
     rec = {
         "config": config, "global_batch": batch, "per_rank_batch": n_local,
         "value": round(value, 1), "ms_per_step": round(ms_step, 4),
@@ -678,8 +681,9 @@ def measure_config(ctx, args, config: str, batch: int, headline: bool) -> dict:
         "e2e": {"value": round(e2e_value, 1), "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 4), "mode": e2e_mode},
         "timing_policy": policy,
-        "l2": ("working set fits the 126 MB L2 (batch 1): warm-L2 value, l2_flushed beside it"
-               if fits_l2 else "per-step working set > 126 MB L2 (activations streamed)"),
+        "l2": (f"working set ~{ws_bytes / 1e6:.0f} MB fits the 126 MB L2: warm-L2 value, "
+               "l2_flushed beside it" if fits_l2 else
+               f"per-step working set ~{ws_bytes / 1e6:.0f} MB > 126 MB L2 (streamed)"),
         "roofline": roof, "roof_algo": roof_algo, "gpu_launches": int(gpu_launches),
         "clocks": clk.summary(),
         "tiles": {k: ["", "128x128", "256x64", "128x64"][v] for k, v in tiles.items()},
@@ -703,11 +707,15 @@ def main_gpu(args):
               file=sys.stderr, flush=True)
     extras = []
     if args.extra != "none" and not ctx.co_shard:
-        for cfg in [c for c in args.extra.split(",") if c and c != args.config]:
+        for item in [c for c in args.extra.split(",") if c]:
+            cfg, _, b = item.partition(":")
+            eb = int(b) if b else DEFAULT_BATCH[cfg]
+            if cfg == args.config and eb == batch:
+                continue
             try:
-                extras.append(measure_config(ctx, args, cfg, DEFAULT_BATCH[cfg], False))
+                extras.append(measure_config(ctx, args, cfg, eb, False))
             except SystemExit as ex:  # e.g. batch not divisible by the ranks
-                extras.append({"config": cfg, "skipped": str(ex)})
+                extras.append({"config": cfg, "global_batch": eb, "skipped": str(ex)})
 
     traffic, traffic_note = None, None
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
