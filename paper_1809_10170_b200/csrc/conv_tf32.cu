@@ -134,8 +134,12 @@ __global__ void __launch_bounds__(kThreadsT, 1)
             mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes);
             int cx, cy, c4;  // a stage's G blocks lie in one space-to-depth phase
             tma_block_coords(p, img, ib0, x0, y0 + n0, cx, cy, c4);
-            tma_load_5d(sp, &tmap, 0, 0, cx, cy, c4, &full[buf]);
-            tma_load_5d(sp + p.plane_floats, &tmap, 0, 1, cx, cy, c4, &full[buf]);
+            if (p.wide) {  // whole pencils, one box (32-byte swizzle)
+              tma_load_4d(sp, &tmap, 0, cx, cy, c4, &full[buf]);
+            } else {
+              tma_load_5d(sp, &tmap, 0, 0, cx, cy, c4, &full[buf]);
+              tma_load_5d(sp + p.plane_floats, &tmap, 0, 1, cx, cy, c4, &full[buf]);
+            }
           }
           const float* wsrc =
               p.w + (((int64_t)cg * p.ib_n + ib0) * p.h_f + n0) * (int64_t)p.w_f * 2 * p.N * 4;
@@ -181,11 +185,11 @@ __global__ void __launch_bounds__(kThreadsT, 1)
         // A descriptor's low word (start >> 4 | LBO >> 4 << 16) advances by
         // the byte offset >> 4 (smem < 256 KB: no carry), the high word
         // (SBO, version) is fixed -- a 32-bit add per MMA.
-        const uint32_t a_lo0 = ((a_base >> 4) & 0x3FFFu) | (((uint32_t)(p.plane_floats * 4) >> 4) << 16);
-        const uint32_t a_hi = ((uint32_t)(p.PW * 16) >> 4) | (1u << 14);
+        const ADesc ad = a_desc(p, a_base);
+        const uint32_t a_lo0 = ad.lo0, a_hi = ad.hi, au = ad.unit;
         const uint32_t b_lo0 = ((b_base >> 4) & 0x3FFFu) | (((uint32_t)(p.N * 16) >> 4) << 16);
         const uint32_t b_hi = (128u >> 4) | (1u << 14);
-        const uint32_t a_mt = (uint32_t)(kTileRows * p.PW);  // next M-tile (16 B units)
+        const uint32_t a_mt = (uint32_t)(kTileRows * p.PW) * au;  // next M-tile (16 B units)
         const uint32_t b_tap = (uint32_t)(2 * p.N);          // next (n, m) tap
         uint32_t accum = st == 0 ? 0u : 1u;
         const int wf = WF_T > 0 ? WF_T : p.w_f;
@@ -197,7 +201,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
         for (int gi = 0; gi < Ge; ++gi)
           for (int n = 0; n < Re; ++n) {
             const bool row_ok = r * p.R + n < nmax;
-            const uint32_t arow = a_lo0 + (uint32_t)((gi * p.PH + n) * p.PW);
+            const uint32_t arow = a_lo0 + (uint32_t)((gi * p.PH + n) * p.PW) * au;
             const uint32_t brow = b_lo0 + (uint32_t)((gi * p.R + n) * wf) * b_tap;
             if (MT_T > 0 && mts == MT_T) {
 #pragma unroll
@@ -206,7 +210,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
 #pragma unroll
                 for (int mt = 0; mt < MT_T; ++mt)
                   umma_tf32_elect(acc_base + (uint32_t)(mt * p.N),
-                                  arow + (uint32_t)m + (uint32_t)mt * a_mt, a_hi,
+                                  arow + (uint32_t)m * au + (uint32_t)mt * a_mt, a_hi,
                                   brow + (uint32_t)m * b_tap, b_hi, p.idesc, accum);
                 accum = 1u;
               }
@@ -216,7 +220,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
 #pragma unroll
                 for (int mt = 0; mt < MT_T; ++mt)
                   umma_tf32_elect(acc_base + (uint32_t)(mt * p.N),
-                                  arow + (uint32_t)m + (uint32_t)mt * a_mt, a_hi,
+                                  arow + (uint32_t)m * au + (uint32_t)mt * a_mt, a_hi,
                                   brow + (uint32_t)m * b_tap, b_hi, p.idesc, accum);
                 accum = 1u;
               }
@@ -225,7 +229,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
             for (int m = 0; m < wf; ++m) {
               if (accum && !(row_ok && m < mmax)) continue;
               const uint32_t blo = brow + (uint32_t)m * b_tap;
-              uint32_t alo = arow + (uint32_t)m;
+              uint32_t alo = arow + (uint32_t)m * au;
               for (int mt = 0; mt < mts; ++mt, alo += a_mt)
                 umma_tf32_elect(acc_base + (uint32_t)(mt * p.N), alo, a_hi, blo, b_hi, p.idesc,
                                 accum);
@@ -454,7 +458,12 @@ int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t
 
   // tensor map over the input view: {c4, half, W, H, image*block}
   CUtensorMap map;
+  // 1x1 layers: whole pencils per TMA box (DCONV_TF32_NO_WIDE=1: half planes)
+  static const bool no_wide = getenv("DCONV_TF32_NO_WIDE") != nullptr;
+  p.wide = (!no_wide && p.h_f == 1 && p.w_f == 1 && p.stack == 1 && p.PW == kTW &&
+            p.s2d == 1 && (p.PH % 4) == 0) ? 1 : 0;
   if (int rc = p.stack > 1 ? encode_input_map(&map, view, p.PW, p.SP, 1)
+               : p.wide    ? encode_input_map_wide(&map, view, p.PW, p.PH, p.G)
                            : encode_input_map(&map, view, p.PW, p.PH, p.G))
     return rc;
 

@@ -172,8 +172,12 @@ __global__ void __launch_bounds__(kThreadsX, 1)
             mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes);
             int cx, cy, c4;  // a stage's G blocks lie in one space-to-depth phase
             tma_block_coords(p, img, ib0, x0, y0 + n0, cx, cy, c4);
-            tma_load_5d(sp, &tmap, 0, 0, cx, cy, c4, &full[buf]);
-            tma_load_5d(sp + p.plane_floats, &tmap, 0, 1, cx, cy, c4, &full[buf]);
+            if (p.wide) {  // whole pencils, one box (32-byte swizzle)
+              tma_load_4d(sp, &tmap, 0, cx, cy, c4, &full[buf]);
+            } else {
+              tma_load_5d(sp, &tmap, 0, 0, cx, cy, c4, &full[buf]);
+              tma_load_5d(sp + p.plane_floats, &tmap, 0, 1, cx, cy, c4, &full[buf]);
+            }
           }
           const float* wsrc =
               p.w + (((int64_t)cg * p.ib_n + ib0) * p.h_f + n0) * (int64_t)p.w_f * 4 * p.N * 4;
@@ -219,12 +223,12 @@ __global__ void __launch_bounds__(kThreadsX, 1)
         const uint32_t b_base = smem_u32(sp + 4 * p.plane_floats);
         // descriptor low words (start >> 4 | LBO >> 4 << 16) advance by 32-bit
         // adds (see conv_tf32.cu); lo planes / lo weights at fixed offsets
-        const uint32_t a_lo0 = ((a_base >> 4) & 0x3FFFu) | (((uint32_t)(p.plane_floats * 4) >> 4) << 16);
-        const uint32_t a_hi = ((uint32_t)(p.PW * 16) >> 4) | (1u << 14);
+        const ADesc ad = a_desc(p, a_base);
+        const uint32_t a_lo0 = ad.lo0, a_hi = ad.hi, au = ad.unit;
         const uint32_t b_lo0 =
             ((b_base >> 4) & 0x3FFFu) | (((uint32_t)((DA ? 2 : 1) * p.N * 16) >> 4) << 16);
         const uint32_t b_hi = (128u >> 4) | (1u << 14);
-        const uint32_t a_mt = (uint32_t)(kTileRows * p.PW);  // next M-tile (16 B units)
+        const uint32_t a_mt = (uint32_t)(kTileRows * p.PW) * au;  // next M-tile (16 B units)
         const uint32_t b_tap = (uint32_t)(4 * p.N);          // next (n, m) tap: hi + lo
         const uint32_t a_rem = (uint32_t)(p.plane_floats / 2);  // lo planes (16 B units)
         const uint32_t b_rem = (uint32_t)(2 * p.N);             // lo weights of a tap
@@ -238,7 +242,7 @@ __global__ void __launch_bounds__(kThreadsX, 1)
         for (int gi = 0; gi < Ge; ++gi)
           for (int n = 0; n < Re; ++n) {
             const bool row_ok = r * p.R + n < nmax;
-            const uint32_t arow = a_lo0 + (uint32_t)((gi * p.PH + n) * p.PW);
+            const uint32_t arow = a_lo0 + (uint32_t)((gi * p.PH + n) * p.PW) * au;
             const uint32_t brow = b_lo0 + (uint32_t)((gi * p.R + n) * wf) * b_tap;
 #pragma unroll
             for (int m = 0; m < (WF_T > 0 ? WF_T : 1); ++m) {
@@ -653,8 +657,13 @@ int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream
   p.idesc2 = tf32_idesc(2 * p.N);
 
   CUtensorMap map;
-  // stacked: one box per (image slot, block), SP rows; else PH rows x G blocks
+  // stacked: one box per (image slot, block), SP rows; else PH rows x G blocks;
+  // 1x1 layers: whole pencils per box (DCONV_TF32_NO_WIDE=1: half planes)
+  static const bool no_wide = getenv("DCONV_TF32_NO_WIDE") != nullptr;
+  p.wide = (!no_wide && p.h_f == 1 && p.w_f == 1 && p.stack == 1 && p.PW == kTW &&
+            p.s2d == 1 && (p.PH % 4) == 0) ? 1 : 0;
   if (int rc = p.stack > 1 ? encode_input_map(&map, view, p.PW, p.SP, 1)
+               : p.wide    ? encode_input_map_wide(&map, view, p.PW, p.PH, p.G)
                            : encode_input_map(&map, view, p.PW, p.PH, p.G))
     return rc;
   set_x3_attrs();

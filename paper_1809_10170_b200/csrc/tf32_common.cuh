@@ -37,6 +37,8 @@ struct Tf32Params {
   int chunk_st;       // split-TF32: stages per TMEM accumulator chunk
   int s2d, ib_o;      // in-place space-to-depth factor (1 = off); original input blocks
   int hf_o, wf_o;     // original filter (s2d: taps s*n'+dy >= hf_o are structurally zero)
+  int wide;           // 1x1 layers: whole 32-byte pencils by one TMA box, 32-byte-swizzled
+                      // K-major A (see encode_input_map_wide); 0: two 16-byte half planes
   int stack;          // images stacked along the tile rows (small maps), 1 = off
   int SP;             // stacked mode: patch rows per image slot (h_o + R - 1)
   uint32_t idesc;
@@ -51,6 +53,16 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, i
       "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
       "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
       "r"(smem_u32(bar))
       : "memory");
 }
@@ -290,6 +302,52 @@ inline int encode_input_map(CUtensorMap* map, const InView& v, int PW, int PH, i
   if (cr != CUDA_SUCCESS)
     return dconv_host::set_error(DCONV_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
   return DCONV_OK;
+}
+
+// 1x1 layers ("wide" A): 4-D map {8 ch, W, H, image*block} whose innermost box
+// row is a whole 32-byte pencil, stored with the 32-byte swizzle: the canonical
+// K-major SWIZZLE_32B UMMA layout (8 pixels x 32 B atoms, SBO 256 B), so one
+// box replaces the two 16-byte half-plane boxes -- each 32-byte sector crosses
+// the L2->SM crossbar once instead of twice (ncu: 2.0 GB of TMA reads for an
+// 822 MB input on ResNet-50's 256->64 1x1 at 56x56 b256 with half planes).
+inline int encode_input_map_wide(CUtensorMap* map, const InView& v, int PW, int PH, int G) {
+  const cuuint64_t dims[4] = {8, (cuuint64_t)v.w_i, (cuuint64_t)v.h_i, (cuuint64_t)v.n * v.ib};
+  const cuuint64_t strides[3] = {(cuuint64_t)v.px_floats * 4, (cuuint64_t)v.row * 4,
+                                 (cuuint64_t)v.blk * 4};
+  const cuuint32_t box[4] = {8, (cuuint32_t)PW, (cuuint32_t)PH, (cuuint32_t)G};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  if (box[1] > 256 || box[2] > 256 || box[3] > 256)
+    return dconv_host::set_error(DCONV_EUNSUPPORTED, "TMA box %u x %u x %u too large", box[1],
+                                 box[2], box[3]);
+  const CUresult cr = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(v.base),
+                                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                  CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS)
+    return dconv_host::set_error(DCONV_ECUDA, "cuTensorMapEncodeTiled (wide) failed (%d)", (int)cr);
+  return DCONV_OK;
+}
+
+// A-operand descriptor words of a stage: low word (start >> 4 | LBO >> 4 << 16)
+// and high word (SBO >> 4, version 1, layout).  Half planes: no swizzle,
+// core matrices 8 px x 16 B, LBO = one plane (the second K half), SBO = one
+// tile row.  Wide: SWIZZLE_32B K-major (layout type 6), 8 px x 32 B atoms,
+// SBO 256 B.  `unit` = 16-byte units per pixel step (2 when wide).
+struct ADesc {
+  uint32_t lo0, hi, unit;
+};
+__device__ __forceinline__ ADesc a_desc(const Tf32Params& p, uint32_t a_base) {
+  ADesc d;
+  if (p.wide) {
+    d.lo0 = ((a_base >> 4) & 0x3FFFu) | (1u << 16);
+    d.hi = (256u >> 4) | (1u << 14) | (6u << 29);
+    d.unit = 2u;
+  } else {
+    d.lo0 = ((a_base >> 4) & 0x3FFFu) | (((uint32_t)(p.plane_floats * 4) >> 4) << 16);
+    d.hi = ((uint32_t)(p.PW * 16) >> 4) | (1u << 14);
+    d.unit = 1u;
+  }
+  return d;
 }
 
 // Original blocked weight [jb][b][n][m][ii][jj] behind element (jb, ib, n, m,
