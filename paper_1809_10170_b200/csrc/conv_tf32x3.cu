@@ -46,8 +46,13 @@ constexpr int kEpiWarpsX = 8;
 constexpr int kThreadsX = (4 + kEpiWarpsX) * 32;
 constexpr uint32_t kHiMask = 0xFFFFE000u;  // TF32: sign, exponent, 10 mantissa bits
 // Role wait-cycle instrumentation (DCONV_TF32_PROFILE), compiled in only when
-// set here: it costs registers in the 56-register producer/MMA/split group.
+// built with -DDCONV_X3_PROF (tools/build_x3_prof.sh): it costs registers in
+// the 56-register producer/MMA/split group.
+#ifdef DCONV_X3_PROF
+constexpr bool kProf = true;
+#else
 constexpr bool kProf = false;
+#endif
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
@@ -595,6 +600,7 @@ int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream
   // <= 40 KB of patch (hi + lo planes); at least two stages in 220 KB --
   // else fewer filter rows per stage, then fewer M-tiles
   const int bar_bytes = (3 * kMaxStagesT + 4) * 8 + 16;
+  static const bool no_deep = getenv("DCONV_X3_SHALLOW") != nullptr;  // A/B only
   int stage_bytes = 0;
   for (int r_cap = p.h_f;; ) {
     p.R = rows_for(r_cap);
@@ -618,6 +624,16 @@ int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream
     p.G = p.R == p.h_f ? std::max(1, std::min({p.ib_n, (72 * 1024) / (p.h_f * p.w_f * wtap),
                                                (40 * 1024) / patch_blk_bytes}))
                        : 1;
+    // 1x1 layers: at least 4 ring stages (smaller G) -- their stages are
+    // short, and with 2 the TMA -> split -> MMA hand-off is exposed
+    // (ResNet-50 1024->256 1x1 b256: the split warps waited on TMA half the time)
+    // (>= 32 input blocks: the short-K layers are epilogue-bound, measured
+    // 2% slower with the deeper ring: ResNet-50 64->256 1x1 + skip-add)
+    if (p.h_f * p.w_f == 1 && p.ib_n >= 32 && !no_deep)
+      while (p.G > 1 &&
+             4 * (((4 * ((p.G * p.PH * p.PW * 4 + 31) & ~31) + p.G * p.R * p.w_f * 4 * p.N * 4) +
+                   255) & ~255) * 4 > 220 * 1024 - bar_bytes)
+        --p.G;
     // space-to-depth: a stage's blocks must lie in one phase
     if (p.s2d > 1)
       while (p.ib_o % p.G) --p.G;
