@@ -125,8 +125,13 @@ __global__ void __launch_bounds__(kThreadsT, 1)
             tma_block_coords(p, img, ib0, x0, n0, cx, cy, c40);
             for (int k = 0; k < slots; ++k)
               for (int gi = 0; gi < Ge; ++gi) {
-                float* dst = sp + (gi * p.PH + k * p.SP) * p.PW * 4;
                 const int c4 = c40 + k * p.ib_o + gi;
+                if (p.wide) {  // whole pencils: 8 floats per pixel, one box
+                  tma_load_4d(sp + (gi * p.PH + k * p.SP) * p.PW * 8, &tmap, 0, cx, cy, c4,
+                              &full[buf]);
+                  continue;
+                }
+                float* dst = sp + (gi * p.PH + k * p.SP) * p.PW * 4;
                 tma_load_5d(dst, &tmap, 0, 0, cx, cy, c4, &full[buf]);
                 tma_load_5d(dst + p.plane_floats, &tmap, 0, 1, cx, cy, c4, &full[buf]);
               }
@@ -435,6 +440,18 @@ int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t
   p.G = p.R == p.h_f ? std::max(1, std::min({p.ib_n, (48 * 1024) / (p.h_f * p.w_f * wtap),
                                              (40 * 1024) / patch_blk_bytes}))
                      : 1;
+  // 1x1 layers with >= 256 input channels: at least 4 ring stages (as the
+  // split-TF32 kernel: with 2 the TMA -> MMA hand-off is exposed)
+  {
+    static const bool shallow = getenv("DCONV_X3_SHALLOW") != nullptr;  // A/B only
+    const int bar = (2 * kMaxStagesT + 4) * 8 + 16;
+    auto stage_of = [&](int g) {
+      const int plane = (g * p.PH * p.PW * 4 + 31) & ~31;
+      return ((2 * plane + g * p.R * p.w_f * 2 * p.N * 4) + 255) & ~255;
+    };
+    if (p.h_f * p.w_f == 1 && p.ib_n >= 32 && !shallow)
+      while (p.G > 1 && 4 * stage_of(p.G) * 4 > 220 * 1024 - bar) --p.G;
+  }
   // space-to-depth: a stage's blocks must lie in one phase
   if (p.s2d > 1)
     while (p.ib_o % p.G) --p.G;
@@ -460,11 +477,14 @@ int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t
   CUtensorMap map;
   // 1x1 layers: whole pencils per TMA box (DCONV_TF32_NO_WIDE=1: half planes)
   static const bool no_wide = getenv("DCONV_TF32_NO_WIDE") != nullptr;
-  p.wide = (!no_wide && p.h_f == 1 && p.w_f == 1 && p.stack == 1 && p.PW == kTW &&
-            p.s2d == 1 && (p.PH % 4) == 0) ? 1 : 0;
-  if (int rc = p.stack > 1 ? encode_input_map(&map, view, p.PW, p.SP, 1)
-               : p.wide    ? encode_input_map_wide(&map, view, p.PW, p.PH, p.G)
-                           : encode_input_map(&map, view, p.PW, p.PH, p.G))
+  // (stacked tiles: one box of SP rows per image slot; slot rows start on
+  // 8-pixel = 256-byte swizzle atoms since PW = 8)
+  p.wide = (!no_wide && p.h_f == 1 && p.w_f == 1 && p.PW == kTW && p.s2d == 1 &&
+            (p.PH % 4) == 0) ? 1 : 0;
+  if (int rc = p.wide ? encode_input_map_wide(&map, view, p.PW, p.stack > 1 ? p.SP : p.PH,
+                                              p.stack > 1 ? 1 : p.G)
+               : p.stack > 1 ? encode_input_map(&map, view, p.PW, p.SP, 1)
+                             : encode_input_map(&map, view, p.PW, p.PH, p.G))
     return rc;
 
   const int dev = dconv_host::current_device();

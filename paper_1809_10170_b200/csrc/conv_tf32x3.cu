@@ -168,8 +168,13 @@ __global__ void __launch_bounds__(kThreadsX, 1)
             tma_block_coords(p, img, ib0, x0, n0, cx, cy, c40);
             for (int k = 0; k < slots; ++k)
               for (int gi = 0; gi < Ge; ++gi) {
-                float* dst = sp + (gi * p.PH + k * p.SP) * p.PW * 4;
                 const int c4 = c40 + k * p.ib_o + gi;
+                if (p.wide) {  // whole pencils: 8 floats per pixel, one box
+                  tma_load_4d(sp + (gi * p.PH + k * p.SP) * p.PW * 8, &tmap, 0, cx, cy, c4,
+                              &full[buf]);
+                  continue;
+                }
+                float* dst = sp + (gi * p.PH + k * p.SP) * p.PW * 4;
                 tma_load_5d(dst, &tmap, 0, 0, cx, cy, c4, &full[buf]);
                 tma_load_5d(dst + p.plane_floats, &tmap, 0, 1, cx, cy, c4, &full[buf]);
               }
@@ -676,11 +681,14 @@ int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream
   // stacked: one box per (image slot, block), SP rows; else PH rows x G blocks;
   // 1x1 layers: whole pencils per box (DCONV_TF32_NO_WIDE=1: half planes)
   static const bool no_wide = getenv("DCONV_TF32_NO_WIDE") != nullptr;
-  p.wide = (!no_wide && p.h_f == 1 && p.w_f == 1 && p.stack == 1 && p.PW == kTW &&
-            p.s2d == 1 && (p.PH % 4) == 0) ? 1 : 0;
-  if (int rc = p.stack > 1 ? encode_input_map(&map, view, p.PW, p.SP, 1)
-               : p.wide    ? encode_input_map_wide(&map, view, p.PW, p.PH, p.G)
-                           : encode_input_map(&map, view, p.PW, p.PH, p.G))
+  // (stacked tiles: one box of SP rows per image slot; slot rows start on
+  // 8-pixel = 256-byte swizzle atoms since PW = 8)
+  p.wide = (!no_wide && p.h_f == 1 && p.w_f == 1 && p.PW == kTW && p.s2d == 1 &&
+            (p.PH % 4) == 0) ? 1 : 0;
+  if (int rc = p.wide ? encode_input_map_wide(&map, view, p.PW, p.stack > 1 ? p.SP : p.PH,
+                                              p.stack > 1 ? 1 : p.G)
+               : p.stack > 1 ? encode_input_map(&map, view, p.PW, p.SP, 1)
+                             : encode_input_map(&map, view, p.PW, p.PH, p.G))
     return rc;
   set_x3_attrs();
   const size_t smem = (size_t)p.NS * stage_bytes + bar_bytes;
