@@ -399,6 +399,20 @@ int conv_first_impl(const dconv_conv_desc* d, const float* in_dense, int64_t in_
                        (!skip || aligned16(skip)) &&
                        ((r.out_img | r.out_blk | r.out_row | r.sk_img | r.sk_blk |
                          r.sk_row) & 3) == 0;
+  static const bool no_reader = getenv("DCONV_NO_READER") != nullptr;
+  if (fast_ok && d->algo != DCONV_ALGO_GENERIC && n_peers && !no_reader) {
+    // the TMA-store reader writes this rank's map only: run it there, then
+    // copy the rank's blocks into the peers' maps, so every copy holds the
+    // same values as the all-gather of readers' slices (bitwise)
+    dconv_dev::GenericParams local = p;
+    local.n_peers = 0;
+    rc = dconv_dev::launch_conv_reader(local, as_stream(stream));
+    if (rc == DCONV_OK)
+      return dconv_dev::launch_copy_pencils_peers(out, d->n, r.jb_count, d->h_o, d->w_o,
+                                                  r.out_img, r.out_blk, r.out_row, peers,
+                                                  n_peers, as_stream(stream));
+    if (rc != DCONV_EUNSUPPORTED) return rc;
+  }
   if (fast_ok && d->algo != DCONV_ALGO_GENERIC) {
     rc = dconv_dev::launch_conv_first_fast(p, as_stream(stream));
     if (rc != DCONV_EUNSUPPORTED) return rc;

@@ -22,6 +22,11 @@ int grid_for(int64_t total, int per_thread = 1) {
   return (int)blocks;
 }
 
+struct PeerList {
+  float* p[8];
+  int n;
+};
+
 #define GRID_STRIDE(e, total)                                            \
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (total); \
        e += (int64_t)gridDim.x * blockDim.x)
@@ -279,6 +284,32 @@ __global__ void maxpool2x2_8_dev(const float* __restrict__ in, int n_blocks, int
   }
 }
 
+// fused C_o-shard gather of a first layer run on the TMA-store reader (which
+// writes this rank's map only): the rank's blocks, one 32-byte pencil per
+// thread, copied from its own map into every peer's copy at the same offset
+// (NVLink stores).  The values are the reader's, so every rank's copy is
+// bitwise the all-gathered map.
+__global__ void copy_pencils_peers_dev(const float* __restrict__ src, int n_blocks, int h,
+                                       int w, int64_t pencils, int64_t img_s, int64_t blk_s,
+                                       int64_t row_s, PeerList peers) {
+  GRID_STRIDE(e, pencils) {
+    int64_t t = e;
+    const int x = (int)(t % w); t /= w;
+    const int y = (int)(t % h); t /= h;
+    const int b = (int)(t % n_blocks);
+    const int img = (int)(t / n_blocks);
+    const int64_t off = (int64_t)img * img_s + (int64_t)b * blk_s + (int64_t)y * row_s +
+                        (int64_t)x * 8;
+    const float4 a = __ldg(reinterpret_cast<const float4*>(src + off));
+    const float4 c = __ldg(reinterpret_cast<const float4*>(src + off + 4));
+    for (int q = 0; q < peers.n; ++q) {
+      float4* o = reinterpret_cast<float4*>(peers.p[q] + off);
+      o[0] = a;
+      o[1] = c;
+    }
+  }
+}
+
 }  // namespace
 
 int launch_pack_kernel(const float* src, int c_i, int c_o, int h_f, int w_f,
@@ -372,6 +403,19 @@ int launch_add(const float* a, const float* b, float* o, int64_t count,
     add1_dev<<<grid_for(count), 256, 0, st>>>(a, b, o, count, relu);
   dconv_host::count_launch();
   return dconv_host::check_launch("add_dev");
+}
+
+int launch_copy_pencils_peers(const float* src, int n, int n_blocks, int h, int w,
+                              int64_t img_s, int64_t blk_s, int64_t row_s,
+                              float* const* peers, int n_peers, cudaStream_t st) {
+  PeerList pl{};
+  pl.n = n_peers;
+  for (int q = 0; q < n_peers; ++q) pl.p[q] = peers[q];
+  const int64_t pencils = (int64_t)n * n_blocks * h * w;
+  copy_pencils_peers_dev<<<grid_for(pencils), 256, 0, st>>>(src, n_blocks, h, w, pencils, img_s,
+                                                            blk_s, row_s, pl);
+  dconv_host::count_launch();
+  return dconv_host::check_launch("copy_pencils_peers_dev");
 }
 
 int launch_maxpool2x2(const float* in, int n, int n_blocks, int h, int w,

@@ -22,6 +22,11 @@ int launch_add(const float* a, const float* b, float* o, int64_t count,
 int launch_maxpool2x2(const float* in, int n, int n_blocks, int h, int w,
                       int c_b, float* out, int64_t o_img, int64_t o_blk,
                       int64_t o_row, cudaStream_t st);
+// copy [n][n_blocks][h][w][8] pencils of a strided map into each peer's copy
+// at the same offsets (the reader's fused C_o-shard gather)
+int launch_copy_pencils_peers(const float* src, int n, int n_blocks, int h, int w,
+                              int64_t img_s, int64_t blk_s, int64_t row_s,
+                              float* const* peers, int n_peers, cudaStream_t st);
 double fp32_peak_probe(cudaStream_t st);
 double ffma2_pattern_probe(cudaStream_t st);
 }  // namespace dconv_dev
