@@ -161,6 +161,11 @@ __device__ __forceinline__ void cp_async_wait() {
 // kernel in the stream is still running; it must pdl_wait() before touching
 // data that kernel produces.  pdl_launch_dependents() lets the next kernel
 // start launching (it still waits for this grid in its own pdl_wait).
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

@@ -264,6 +264,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const long long t_start = p.dbg ? clock64() : 0;
+  if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 16 + 0] = (long long)globaltimer_ns();
   const int S = p.n_g * p.n_r;                 // stages per work unit
   const int co_groups = (p.jb_count + CG - 1) / CG;
   const int n_units = p.unit_count;             // this launch's units: [unit_begin, +count)
@@ -431,6 +432,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
     constexpr int kProdWarps = 4;
     const int pw = warp - NW;
     const int pt = pw * 32 + lane;  // producer thread index
+    if (p.dbg && pt == 0) p.dbg[blockIdx.x * 16 + 8] = clock64() - t_start;
     int gs = 0;
     const int seg_rows_full = (p.h_o - 1) * p.sy;  // + Re per full segment
     for (int u = cluster_id; u < n_units; u += n_clusters) {
@@ -476,6 +478,16 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
         // it (the transaction count is allowed to run ahead within a phase)
         if (pt == 0) mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes * n_wblk);
         __syncwarp();
+        // the stage's copies are numbered in one sequence (segments' rows,
+        // then weight chunks) and dealt round-robin over the producer warps
+        // (copy c -> warp c % 4, lane c / 4 % 32): a bulk copy takes uniform
+        // operands, so a warp issues its lanes' copies one after another, and
+        // few-row stages (batch 1) would otherwise all land on warp 0
+        const int me = pw + kProdWarps * lane;
+        int cbase = 0;
+        auto first_mine = [&](int base) {
+          return base + ((me - base) % (32 * kProdWarps) + 32 * kProdWarps) % (32 * kProdWarps);
+        };
         for (int j = 0; j < n_seg; ++j) {
           int img, y_start, rows, prow0;
           if (j == 0) {
@@ -487,19 +499,24 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
           }
           const float* src0 = p.in + (int64_t)img * p.in_img +
                               (int64_t)(y_start * p.sy + n0) * p.in_row + (int64_t)col0 * CBS;
-          for (int t = pt; t < Ge * rows; t += 32 * kProdWarps) {
+          const int n_cp = Ge * rows;
+          for (int c = first_mine(cbase); c < cbase + n_cp; c += 32 * kProdWarps) {
+            const int t = c - cbase;
             const int gi = t / rows, pr = t - gi * rows;
             const float* src = src0 + (int64_t)(ib0 + gi) * p.in_blk + (int64_t)pr * p.in_row;
             float* dst = sp + ((gi * p.PH + prow0 + pr) * p.PW) * CBS;
             bulk_g2s(dst, src, (uint32_t)(cols * CBS * 4), &full[buf]);
           }
+          cbase += n_cp;
         }
-        for (int c = pt; c < n_wblk; c += 32 * kProdWarps) {
+        for (int cc = first_mine(cbase); cc < cbase + n_wblk; cc += 32 * kProdWarps) {
+          const int c = cc - cbase;
           // storage block J = jb0 / SUB + c of the blocked kernel
           const float* src = p.w + ((int64_t)(jb0 / SUB + c) * p.ib_n + ib0) * p.slab_floats +
                              (int64_t)n0 * p.w_f * CBS * CBS;
           bulk_g2s(sw + wchunk<TCO>(c, p.wstride_floats), src, wbytes, &full[buf]);
         }
+        if (p.dbg && pt == 0 && gs == 0) p.dbg[blockIdx.x * 16 + 9] = clock64() - t_start;
       }
     }
     return;
@@ -516,7 +533,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
   const int cb = (wc * 8 + (lane >> 2)) * NBLK;  // first output block within the CTA tile
 
   const uint32_t tmem_base = tmem_on ? *tmem_slot : 0u;
-  if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 1] = clock64() - t_start;  // setup done
+  if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 1] = clock64() - t_start;  // setup done
   const uint32_t taddr = tmem_base + ((uint32_t)((warp & 3) * 32) << 16) +
                          (uint32_t)((warp >> 2) * TPX * TCO);
   const int wf = WF > 0 ? WF : p.w_f;
@@ -546,8 +563,9 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
 
     for (int st = st0; st < st1; ++st, ++gs) {
       const int buf = gs % p.NS;
+      if (p.dbg && tid == 0 && gs == 0) p.dbg[blockIdx.x * 16 + 10] = clock64() - t_start;
       mbar_wait(&full[buf], (gs / p.NS) & 1);
-      if (p.dbg && tid == 0 && gs == 0) p.dbg[blockIdx.x * 8 + 2] = clock64() - t_start;
+      if (p.dbg && tid == 0 && gs == 0) p.dbg[blockIdx.x * 16 + 2] = clock64() - t_start;
       const int g = st / p.n_r, r = st - g * p.n_r;
       const int Ge = min(p.G, p.ib_n - g * p.G);
       const int Re = min(p.R, p.h_f - r * p.R);
@@ -639,7 +657,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
           for (int c = 0; c < TCO / 2; ++c) acc[k][c] = 0ull;
       }
     }
-    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 3] = clock64() - t_start;  // loop end
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 3] = clock64() - t_start;  // loop end
     if (p.epi_wg) {
       // hand the finished tile to the epilogue warpgroup (TMEM result buffer
       // unit_iter & 1) and go on with the next unit
@@ -721,13 +739,13 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
       }
       // every compute warp's stores issued: one fence, ks relaxed arrives
       asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
-      if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 4] = clock64() - t_start;  // published
+      if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 4] = clock64() - t_start;  // published
       if (tid == 0) {
         fence_cluster();
         for (int q = 0; q < ks; ++q) mbar_arrive_remote_relaxed(ready, q);
       }
       mbar_wait_cluster(ready, unit_iter & 1);
-      if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 5] = clock64() - t_start;  // all ready
+      if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 5] = clock64() - t_start;  // all ready
       if (cb < cg_valid) {
         const int jl = jb0 + cb - p.jb_begin;
         const int i_lo = rank * kItems / ks, i_hi = (rank + 1) * kItems / ks;
@@ -766,7 +784,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
             *reinterpret_cast<float4*>(p.peer_out[pi] + off) = v;
         }
       }
-      if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 6] = clock64() - t_start;  // reduced
+      if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 6] = clock64() - t_start;  // reduced
       if (!last_unit) {
         // every compute warp has read its slots: the ranks may publish again
         asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
@@ -841,7 +859,10 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
   // (push model: every remote access to this CTA's smem -- the peers'
   // partial stores and arrives -- completes before its last `ready` wait, so
   // no exit barrier is needed)
-  if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 7] = clock64() - t_start;  // exit
+  if (p.dbg && tid == 0) {
+    p.dbg[blockIdx.x * 16 + 7] = clock64() - t_start;  // exit
+    p.dbg[blockIdx.x * 16 + 11] = (long long)globaltimer_ns();
+  }
 
   if (tmem_on) {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1114,8 +1135,8 @@ int launch_units(K kernel, int threads, FfmaParams p, size_t smem, int unit_begi
   static const bool prof = getenv("DCONV_FFMA_PROFILE") != nullptr;
   if (prof) {  // debugging aid: per-CTA phase clocks of one extra launch
     const int grid = p.ksplit == 1 ? clusters : clusters * p.ksplit;
-    cudaMalloc(&p.dbg, (size_t)grid * 8 * 8);
-    cudaMemset(p.dbg, 0, (size_t)grid * 8 * 8);
+    cudaMalloc(&p.dbg, (size_t)grid * 16 * 8);
+    cudaMemset(p.dbg, 0, (size_t)grid * 16 * 8);
     if (p.ksplit == 1) {
       kernel<<<clusters, threads, smem, stream>>>(p);
     } else {
@@ -1133,15 +1154,22 @@ int launch_units(K kernel, int threads, FfmaParams p, size_t smem, int unit_begi
       cfg.numAttrs = 1;
       cudaLaunchKernelEx(&cfg, kernel, p);
     }
-    std::vector<long long> h((size_t)grid * 8);
+    std::vector<long long> h((size_t)grid * 16);
     cudaMemcpy(h.data(), p.dbg, h.size() * 8, cudaMemcpyDeviceToHost);
-    double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int b = 0; b < grid; ++b)
-      for (int i = 1; i < 8; ++i) a[i] += h[b * 8 + i];
+    double a[16] = {};
+    long long g0 = h[0], g1 = h[11], gmax0 = h[0];
+    for (int b = 0; b < grid; ++b) {
+      for (int i = 1; i < 11; ++i) a[i] += h[b * 16 + i];
+      g0 = std::min(g0, h[b * 16]);
+      gmax0 = std::max(gmax0, h[b * 16]);
+      g1 = std::max(g1, h[b * 16 + 11]);
+    }
+    for (double& v : a) v /= grid;
     fprintf(stderr, "conv_ffma profile: grid=%d ks=%d avg cycles: setup=%.0f first_data=%.0f "
-            "loop_end=%.0f published=%.0f all_ready=%.0f reduced=%.0f exit=%.0f\n", grid,
-            p.ksplit, a[1] / grid, a[2] / grid, a[3] / grid, a[4] / grid, a[5] / grid,
-            a[6] / grid, a[7] / grid);
+            "loop_end=%.0f published=%.0f all_ready=%.0f reduced=%.0f exit=%.0f | producer "
+            "start=%.0f stage0_issued=%.0f | compute first_wait=%.0f | CTA start spread %lld ns, "
+            "first start -> last exit %lld ns\n", grid, p.ksplit, a[1], a[2], a[3], a[4], a[5],
+            a[6], a[7], a[8], a[9], a[10], gmax0 - g0, g1 - g0);
     cudaFree(p.dbg);
     p.dbg = nullptr;
   }
