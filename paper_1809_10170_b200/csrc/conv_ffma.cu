@@ -439,6 +439,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
       TileRows tr;
       int tx0, jb0, cg_valid;
       decode(u, tr, tx0, jb0, cg_valid);
+      if (p.dbg && pt == 0 && gs == 0) p.dbg[blockIdx.x * 16 + 12] = clock64() - t_start;
       const int col0 = tx0 * p.s;
       const int cols = min(p.PW, p.w_i - col0);
       const int n_seg = 1 + (tr.th - tr.cnt0 + p.h_o - 1) / p.h_o;
@@ -478,6 +479,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
         // it (the transaction count is allowed to run ahead within a phase)
         if (pt == 0) mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes * n_wblk);
         __syncwarp();
+        if (p.dbg && pt == 0 && gs == 0) p.dbg[blockIdx.x * 16 + 13] = clock64() - t_start;
         // the stage's copies are numbered in one sequence (segments' rows,
         // then weight chunks) and dealt round-robin over the producer warps
         // (copy c -> warp c % 4, lane c / 4 % 32): a bulk copy takes uniform
@@ -1159,7 +1161,7 @@ int launch_units(K kernel, int threads, FfmaParams p, size_t smem, int unit_begi
     double a[16] = {};
     long long g0 = h[0], g1 = h[11], gmax0 = h[0];
     for (int b = 0; b < grid; ++b) {
-      for (int i = 1; i < 11; ++i) a[i] += h[b * 16 + i];
+      for (int i = 1; i < 16; ++i) a[i] += h[b * 16 + i];
       g0 = std::min(g0, h[b * 16]);
       gmax0 = std::max(gmax0, h[b * 16]);
       g1 = std::max(g1, h[b * 16 + 11]);
@@ -1167,9 +1169,9 @@ int launch_units(K kernel, int threads, FfmaParams p, size_t smem, int unit_begi
     for (double& v : a) v /= grid;
     fprintf(stderr, "conv_ffma profile: grid=%d ks=%d avg cycles: setup=%.0f first_data=%.0f "
             "loop_end=%.0f published=%.0f all_ready=%.0f reduced=%.0f exit=%.0f | producer "
-            "start=%.0f stage0_issued=%.0f | compute first_wait=%.0f | CTA start spread %lld ns, "
+            "start=%.0f decoded=%.0f expect_tx=%.0f stage0_issued=%.0f | compute first_wait=%.0f | CTA start spread %lld ns, "
             "first start -> last exit %lld ns\n", grid, p.ksplit, a[1], a[2], a[3], a[4], a[5],
-            a[6], a[7], a[8], a[9], a[10], gmax0 - g0, g1 - g0);
+            a[6], a[7], a[8], a[12], a[13], a[9], a[10], gmax0 - g0, g1 - g0);
     cudaFree(p.dbg);
     p.dbg = nullptr;
   }
