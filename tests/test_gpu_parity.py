@@ -1133,6 +1133,31 @@ def test_space_to_depth_blocked_bitexact():
         assert np.array_equal(got[i], po.pack_feature_map(want, 8))
 
 
+@pytest.mark.parametrize("c,f,h,w", [(3, 2, 229, 229), (3, 2, 9, 12), (3, 4, 227, 227),
+                                     (3, 3, 13, 10), (5, 2, 9, 11)])
+def test_pack_space_to_depth_bitexact(c, f, h, w):
+    """dconv_cuda_pack_space_to_depth (the tensor-core plans' strided-stem
+    pack of the dense image): s2d channel (dy*f + dx)*C + c at (ys, xs) is
+    input (c, f*ys + dy, f*xs + dx), zero outside the image and in the pad
+    channels, blocked by 8 -- bit-exact (C = 3, f = 2 / 4: the per-pixel
+    kernel; other shapes: the per-element one)."""
+    n = 3
+    x = po.uniform((n, c, h, w), 9970 + f, 0)
+    hs, ws = -(-h // f), -(-w // f)
+    out = torch.full((n, (c * f * f + 7) // 8, hs, ws, 8), float("nan"), device="cuda")
+    _abi.check(_abi.lib().dconv_cuda_pack_space_to_depth(
+        _abi.ptr(dev(x)), n, c, h, w, f, _abi.ptr(out), _abi.stream_ptr()))
+    got = host(out)
+    for i in range(n):
+        xp = np.zeros((c, hs * f, ws * f), np.float32)
+        xp[:, :h, :w] = x[i]
+        want = np.zeros((c * f * f, hs, ws), np.float32)
+        for dy in range(f):
+            for dx in range(f):
+                want[(dy * f + dx) * c:(dy * f + dx + 1) * c] = xp[:, dy::f, dx::f]
+        assert np.array_equal(got[i], po.pack_feature_map(want, 8))
+
+
 @pytest.mark.parametrize("f,s,h,w,co,n", [(3, 1, 34, 45, 64, 40), (3, 1, 20, 226, 40, 30),
                                            (7, 2, 41, 39, 96, 36), (7, 2, 229, 229, 64, 6),
                                            (3, 1, 226, 226, 72, 3)])
