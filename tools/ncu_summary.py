@@ -148,7 +148,9 @@ def main():
     json.dump(summ, open(os.path.join(dst, f"{tag}_ncu_launches_vgg16_b32.json"), "w"), indent=1)
     full = {}
     for name, rep in (("vgg16_conv1_2_b32", "full_conv1_2"),
-                      ("vgg16_conv4_2_b32", "full_conv4_2")):
+                      ("vgg16_conv4_2_b32", "full_conv4_2"),
+                      ("resnet50_1x1_64_256_skip_b256", "full_ffma_r50_s1c3"),
+                      ("resnet50_1x1_256_1024_skip_b256", "full_ffma_r50_s3c3")):
         p = find_rep(src, rep)
         if p:
             full[name] = full_metrics(p)

@@ -31,7 +31,9 @@ if algo in ("tf32", "tf32x3"):
     wp = nets.prepare_tf32(l, w, x3=x3)
     run = lambda: nets.conv_tf32(l, n, x, wp, y, epi, sk, x3=x3)  # noqa: E731
 else:
-    run = lambda: nets.conv(l, n, x, w, y, epi, sk)  # noqa: E731
+    import os
+    tv = int(os.environ.get("TILE", "0"))  # desc.tile_variant (0 = selector)
+    run = lambda: nets.conv(l, n, x, w, y, epi, sk, tile_variant=tv)  # noqa: E731
 for _ in range(reps):
     run()
 torch.cuda.synchronize()

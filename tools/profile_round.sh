@@ -6,7 +6,8 @@
 #      extra_configs + the CPU baseline), the split-TF32 and TF32 paths, the
 #      CPU reference arm, C_o-sharded ResNet-50 b1 (NCCL / fused peer, 1 rank)
 #   2. ncu launch list of one VGG-16 b32 step (FFMA and split-TF32)
-#   3. ncu --set full of the top kernels: FFMA VGG conv1_2 / conv4_2, the
+#   3. ncu --set full of the top kernels: FFMA VGG conv1_2 / conv4_2 and two
+#      ResNet-50 b256 1x1 layers (64->256 56x56, 256->1024 14x14, skip-add), the
 #      TMA-store first-layer reader (VGG conv1_1 b32, 7x7/s2 stem b64),
 #      split-TF32 VGG conv4_2 and ResNet 1024->256 1x1
 #   (direct vs im2col vs cuDNN: IM2COL=1)
@@ -43,6 +44,8 @@ full() {  # name kernel-regex one_layer args...  (FS: launches to skip; tail-spl
 }
 FS=4 full conv1_2 conv_ffma 64 64 226 226 3 1 32 3
 FS=4 full conv4_2 conv_ffma 512 512 30 30 3 1 32 3
+FS=4 full ffma_r50_s1c3 conv_ffma 64 256 56 56 1 1 256 3 ffma_add
+FS=4 full ffma_r50_s3c3 conv_ffma 256 1024 14 14 1 1 256 3 ffma_add
 full reader_conv1_1 conv_reader 3 64 226 226 3 1 32 3 first
 full reader_stem conv_reader 3 64 229 229 7 2 64 3 first
 full x3_conv4_2 conv_tf32x3 512 512 30 30 3 1 32 3 tf32x3
