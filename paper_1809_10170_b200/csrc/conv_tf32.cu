@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 #include "tf32_common.cuh"
 
@@ -41,7 +42,10 @@ constexpr int kThreadsT = (2 + kEpiWarps) * 32;
 
 // WF_T / MT_T: filter width and M-tiles per unit as compile-time constants
 // (0 = runtime), so the per-stage MMA walk unrolls into straight-line issue.
-template <int WF_T, int MT_T>
+// VAR: the tap walk (kWalkPlain / kWalkS2D / kWalkWide), one per instantiation
+// -- the MMA issuer is latency-bound on N = 64 and small-map layers, and a
+// runtime choice between walks measured 3-19% slower than a single walk.
+template <int WF_T, int MT_T, int VAR>
 __global__ void __launch_bounds__(kThreadsT, 1)
     conv_tf32_kernel(const __grid_constant__ CUtensorMap tmap, const Tf32Params p) {
   extern __shared__ __align__(1024) float smem[];
@@ -203,44 +207,97 @@ __global__ void __launch_bounds__(kThreadsT, 1)
         // so the accumulator is initialised)
         int nmax, mmax;
         s2d_valid_taps(p, g * p.G, nmax, mmax);
-        for (int gi = 0; gi < Ge; ++gi)
-          for (int n = 0; n < Re; ++n) {
-            const bool row_ok = r * p.R + n < nmax;
-            const uint32_t arow = a_lo0 + (uint32_t)((gi * p.PH + n) * p.PW) * au;
-            const uint32_t brow = b_lo0 + (uint32_t)((gi * p.R + n) * wf) * b_tap;
-            if (MT_T > 0 && mts == MT_T) {
-#pragma unroll
-              for (int m = 0; m < (WF_T > 0 ? WF_T : 1); ++m) {
-                if (accum && !(row_ok && m < mmax)) continue;
-#pragma unroll
-                for (int mt = 0; mt < MT_T; ++mt)
-                  umma_tf32_elect(acc_base + (uint32_t)(mt * p.N),
-                                  arow + (uint32_t)m * au + (uint32_t)mt * a_mt, a_hi,
-                                  brow + (uint32_t)m * b_tap, b_hi, p.idesc, accum);
+        // the tap walk, specialised: without space-to-depth no tap is
+        // skipped and the issuer loop carries no per-tap test (the test
+        // cost 15-19% on N = 64 / 14x14 layers: the issuer is latency-bound)
+        auto walk = [&](auto s2d_tag, auto wide_tag) {
+          constexpr bool S2D = decltype(s2d_tag)::value;
+          constexpr uint32_t AU = decltype(wide_tag)::value ? 2u : 1u;  // A start unit
+          for (int gi = 0; gi < Ge; ++gi)
+            for (int n = 0; n < Re; ++n) {
+              const bool row_ok = !S2D || r * p.R + n < nmax;
+              const uint32_t arow = a_lo0 + (uint32_t)((gi * p.PH + n) * p.PW) * AU;
+              const uint32_t brow = b_lo0 + (uint32_t)((gi * p.R + n) * wf) * b_tap;
+              if (MT_T > 0 && mts == MT_T) {
+  #pragma unroll
+                for (int m = 0; m < (WF_T > 0 ? WF_T : 1); ++m) {
+                  if (S2D && accum && !(row_ok && m < mmax)) continue;
+  #pragma unroll
+                  for (int mt = 0; mt < MT_T; ++mt)
+                    umma_tf32_elect(acc_base + (uint32_t)(mt * p.N),
+                                    arow + (uint32_t)m * AU + (uint32_t)mt * a_mt, a_hi,
+                                    brow + (uint32_t)m * b_tap, b_hi, p.idesc, accum);
+                  accum = 1u;
+                }
+                if (WF_T > 0) continue;
+                for (int m = 1; m < wf; ++m) {
+                  if (S2D && accum && !(row_ok && m < mmax)) continue;
+  #pragma unroll
+                  for (int mt = 0; mt < MT_T; ++mt)
+                    umma_tf32_elect(acc_base + (uint32_t)(mt * p.N),
+                                    arow + (uint32_t)m * AU + (uint32_t)mt * a_mt, a_hi,
+                                    brow + (uint32_t)m * b_tap, b_hi, p.idesc, S2D ? accum : 1u);
+                  accum = 1u;
+                }
+                continue;
+              }
+              for (int m = 0; m < wf; ++m) {
+                if (S2D && accum && !(row_ok && m < mmax)) continue;
+                const uint32_t blo = brow + (uint32_t)m * b_tap;
+                uint32_t alo = arow + (uint32_t)m * AU;
+                for (int mt = 0; mt < mts; ++mt, alo += a_mt)
+                  umma_tf32_elect(acc_base + (uint32_t)(mt * p.N), alo, a_hi, blo, b_hi, p.idesc,
+                                  accum);
                 accum = 1u;
               }
-              if (WF_T > 0) continue;
-              for (int m = 1; m < wf; ++m) {
-                if (accum && !(row_ok && m < mmax)) continue;
-#pragma unroll
-                for (int mt = 0; mt < MT_T; ++mt)
-                  umma_tf32_elect(acc_base + (uint32_t)(mt * p.N),
-                                  arow + (uint32_t)m * au + (uint32_t)mt * a_mt, a_hi,
-                                  brow + (uint32_t)m * b_tap, b_hi, p.idesc, accum);
+            }
+        };
+        if constexpr (VAR == kWalkS2D) {
+          walk(std::true_type{}, std::false_type{});
+        } else if constexpr (VAR == kWalkWide) {
+          walk(std::false_type{}, std::true_type{});
+        } else {
+          // plain layers: the tap walk exactly as before the space-to-depth
+          // and wide-A variants existed (its issue latency is what N = 64
+          // and small-map layers are bound by)
+          const uint32_t a_lo0n =
+              ((a_base >> 4) & 0x3FFFu) | (((uint32_t)(p.plane_floats * 4) >> 4) << 16);
+          const uint32_t a_hin = ((uint32_t)(p.PW * 16) >> 4) | (1u << 14);
+          const uint32_t a_mtn = (uint32_t)(kTileRows * p.PW);
+          for (int gi = 0; gi < Ge; ++gi)
+            for (int n = 0; n < Re; ++n) {
+              const uint32_t arow = a_lo0n + (uint32_t)((gi * p.PH + n) * p.PW);
+              const uint32_t brow = b_lo0 + (uint32_t)((gi * p.R + n) * wf) * b_tap;
+              if (MT_T > 0 && mts == MT_T) {
+  #pragma unroll
+                for (int m = 0; m < (WF_T > 0 ? WF_T : 1); ++m) {
+  #pragma unroll
+                  for (int mt = 0; mt < MT_T; ++mt)
+                    umma_tf32_elect(acc_base + (uint32_t)(mt * p.N),
+                                    arow + (uint32_t)m + (uint32_t)mt * a_mtn, a_hin,
+                                    brow + (uint32_t)m * b_tap, b_hi, p.idesc, accum);
+                  accum = 1u;
+                }
+                if (WF_T > 0) continue;
+                for (int m = 1; m < wf; ++m) {
+  #pragma unroll
+                  for (int mt = 0; mt < MT_T; ++mt)
+                    umma_tf32_elect(acc_base + (uint32_t)(mt * p.N),
+                                    arow + (uint32_t)m + (uint32_t)mt * a_mtn, a_hin,
+                                    brow + (uint32_t)m * b_tap, b_hi, p.idesc, 1u);
+                }
+                continue;
+              }
+              for (int m = 0; m < wf; ++m) {
+                const uint32_t blo = brow + (uint32_t)m * b_tap;
+                uint32_t alo = arow + (uint32_t)m;
+                for (int mt = 0; mt < mts; ++mt, alo += a_mtn)
+                  umma_tf32_elect(acc_base + (uint32_t)(mt * p.N), alo, a_hin, blo, b_hi, p.idesc,
+                                  accum);
                 accum = 1u;
               }
-              continue;
             }
-            for (int m = 0; m < wf; ++m) {
-              if (accum && !(row_ok && m < mmax)) continue;
-              const uint32_t blo = brow + (uint32_t)m * b_tap;
-              uint32_t alo = arow + (uint32_t)m * au;
-              for (int mt = 0; mt < mts; ++mt, alo += a_mt)
-                umma_tf32_elect(acc_base + (uint32_t)(mt * p.N), alo, a_hi, blo, b_hi, p.idesc,
-                                accum);
-              accum = 1u;
-            }
-          }
+        }
         if (p.dbg) prof[4] += clock64() - t_issue;
         umma_commit_elect(&empty[buf]);  // stage smem free once these MMAs retire
         if (st == S - 1) umma_commit_elect(&acc_full[ab]);
@@ -326,14 +383,25 @@ __global__ void prepare_tf32_weights_kernel(const float* __restrict__ w, int ib_
 }  // namespace
 
 using Tf32Kernel = void (*)(const CUtensorMap, const Tf32Params);
+// instantiated walks: 3x3 plain / space-to-depth (11x11/s4 -> 3x3), 1x1 plain /
+// wide (a strided 1x1 is a subsampled view, never space-to-depth), generic
+// plain / space-to-depth (3x3/s2 -> 2x2, 7x7/s2 -> 4x4)
+template <int V>
+Tf32Kernel tf32_kernel_for(int wf, int mt) {
+  static const Tf32Kernel k3[4] = {conv_tf32_kernel<3, 1, V>, conv_tf32_kernel<3, 2, V>,
+                                   conv_tf32_kernel<3, 3, V>, conv_tf32_kernel<3, 4, V>};
+  if (wf == 3) return k3[mt - 1];
+  return conv_tf32_kernel<0, 0, V>;
+}
 Tf32Kernel pick_tf32_kernel(const Tf32Params& p) {
-  static const Tf32Kernel k3[4] = {conv_tf32_kernel<3, 1>, conv_tf32_kernel<3, 2>,
-                                   conv_tf32_kernel<3, 3>, conv_tf32_kernel<3, 4>};
-  static const Tf32Kernel k1[4] = {conv_tf32_kernel<1, 1>, conv_tf32_kernel<1, 2>,
-                                   conv_tf32_kernel<1, 3>, conv_tf32_kernel<1, 4>};
-  if (p.w_f == 3) return k3[p.MT - 1];
-  if (p.w_f == 1) return k1[p.MT - 1];
-  return conv_tf32_kernel<0, 0>;
+  static const Tf32Kernel k1[2][4] = {
+      {conv_tf32_kernel<1, 1, kWalkPlain>, conv_tf32_kernel<1, 2, kWalkPlain>,
+       conv_tf32_kernel<1, 3, kWalkPlain>, conv_tf32_kernel<1, 4, kWalkPlain>},
+      {conv_tf32_kernel<1, 1, kWalkWide>, conv_tf32_kernel<1, 2, kWalkWide>,
+       conv_tf32_kernel<1, 3, kWalkWide>, conv_tf32_kernel<1, 4, kWalkWide>}};
+  if (p.w_f == 1) return k1[p.wide ? 1 : 0][p.MT - 1];
+  return p.s2d > 1 ? tf32_kernel_for<kWalkS2D>(p.w_f, p.MT)
+                   : tf32_kernel_for<kWalkPlain>(p.w_f, p.MT);
 }
 
 // Channels per unit: an M=128 MMA costs ~71 cycles for any N <= 128 and ~128
@@ -489,11 +557,11 @@ int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t
 
   const int dev = dconv_host::current_device();
   const int sms = dconv_host::device_sms(dev);
-  if (dconv_host::first_use_on_device(reinterpret_cast<const void*>(conv_tf32_kernel<0, 0>), dev))
-    for (auto k : {conv_tf32_kernel<0, 0>, conv_tf32_kernel<3, 1>, conv_tf32_kernel<3, 2>,
-                   conv_tf32_kernel<3, 3>, conv_tf32_kernel<3, 4>, conv_tf32_kernel<1, 1>,
-                   conv_tf32_kernel<1, 2>, conv_tf32_kernel<1, 3>, conv_tf32_kernel<1, 4>})
+  {
+    const Tf32Kernel k = pick_tf32_kernel(p);
+    if (dconv_host::first_use_on_device(reinterpret_cast<const void*>(k), dev))
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  }
   const size_t smem = (size_t)p.NS * stage_bytes + bar_bytes;
   const int grid = std::min(p.units, sms);
   static const bool dbg = getenv("DCONV_DEBUG") != nullptr;

@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "tf32_common.cuh"
@@ -84,7 +85,7 @@ __device__ __forceinline__ float4 hi4(float4 v) {
 // two MMAs instead of three, A_hi read once, and the small terms are summed
 // apart from the head (no bits lost in its accumulator).  Weights per k-half
 // are [hi N rows | lo N rows]; TMEM per M-tile 2N columns.
-template <int WF_T, int MT_T, int COLS, bool DA>
+template <int WF_T, int MT_T, int COLS, bool DA, int VAR>  // VAR: tap walk (conv_tf32.cu)
 __global__ void __launch_bounds__(kThreadsX, 1)
     conv_tf32x3_kernel(const __grid_constant__ CUtensorMap tmap, const Tf32Params p) {
   extern __shared__ __align__(1024) float smem[];
@@ -249,53 +250,116 @@ __global__ void __launch_bounds__(kThreadsX, 1)
         // issued, initialising its accumulator set)
         int nmax, mmax;
         s2d_valid_taps(p, g * p.G, nmax, mmax);
-        for (int gi = 0; gi < Ge; ++gi)
-          for (int n = 0; n < Re; ++n) {
-            const bool row_ok = r * p.R + n < nmax;
-            const uint32_t arow = a_lo0 + (uint32_t)((gi * p.PH + n) * p.PW) * au;
-            const uint32_t brow = b_lo0 + (uint32_t)((gi * p.R + n) * wf) * b_tap;
-#pragma unroll
-            for (int m = 0; m < (WF_T > 0 ? WF_T : 1); ++m) {
-              if (accum && !(row_ok && m < mmax)) continue;
-#pragma unroll
-              for (int mt = 0; mt < kMtLoop; ++mt) {
-                if (mt >= mts) break;
-                const uint32_t a = arow + (uint32_t)m + (uint32_t)mt * a_mt;
-                const uint32_t b = brow + (uint32_t)m * b_tap;
-                if constexpr (DA) {
-                  const uint32_t d = acc_base + (uint32_t)(mt * 2 * p.N);
-                  umma_tf32_elect(d, a, a_hi, b, b_hi, p.idesc2, accum);  // [main | corr]
-                  umma_tf32_elect(d + (uint32_t)p.N, a + a_rem, a_hi, b, b_hi, p.idesc, 1u);
-                } else {
-                  const uint32_t d = acc_base + (uint32_t)(mt * p.N);
-                  // small terms first, the head product last
-                  umma_tf32_elect(d, a, a_hi, b + b_rem, b_hi, p.idesc, accum);
-                  umma_tf32_elect(d, a + a_rem, a_hi, b, b_hi, p.idesc, 1u);
-                  umma_tf32_elect(d, a, a_hi, b, b_hi, p.idesc, 1u);
+        // the tap walk, specialised: without space-to-depth no tap is
+        // skipped and the issuer loop carries no per-tap test (the test
+        // cost 15-19% on N = 64 / 14x14 layers: the issuer is latency-bound)
+        auto walk = [&](auto s2d_tag, auto wide_tag) {
+          constexpr bool S2D = decltype(s2d_tag)::value;
+          constexpr uint32_t AU = decltype(wide_tag)::value ? 2u : 1u;  // A start unit
+          for (int gi = 0; gi < Ge; ++gi)
+            for (int n = 0; n < Re; ++n) {
+              const bool row_ok = !S2D || r * p.R + n < nmax;
+              const uint32_t arow = a_lo0 + (uint32_t)((gi * p.PH + n) * p.PW) * AU;
+              const uint32_t brow = b_lo0 + (uint32_t)((gi * p.R + n) * wf) * b_tap;
+  #pragma unroll
+              for (int m = 0; m < (WF_T > 0 ? WF_T : 1); ++m) {
+                if (S2D && accum && !(row_ok && m < mmax)) continue;
+  #pragma unroll
+                for (int mt = 0; mt < kMtLoop; ++mt) {
+                  if (mt >= mts) break;
+                  const uint32_t a = arow + (uint32_t)m + (uint32_t)mt * a_mt;
+                  const uint32_t b = brow + (uint32_t)m * b_tap;
+                  if constexpr (DA) {
+                    const uint32_t d = acc_base + (uint32_t)(mt * 2 * p.N);
+                    umma_tf32_elect(d, a, a_hi, b, b_hi, p.idesc2, accum);  // [main | corr]
+                    umma_tf32_elect(d + (uint32_t)p.N, a + a_rem, a_hi, b, b_hi, p.idesc, 1u);
+                  } else {
+                    const uint32_t d = acc_base + (uint32_t)(mt * p.N);
+                    // small terms first, the head product last
+                    umma_tf32_elect(d, a, a_hi, b + b_rem, b_hi, p.idesc, accum);
+                    umma_tf32_elect(d, a + a_rem, a_hi, b, b_hi, p.idesc, 1u);
+                    umma_tf32_elect(d, a, a_hi, b, b_hi, p.idesc, 1u);
+                  }
+                }
+                accum = 1u;
+              }
+              if (WF_T > 0) continue;
+              for (int m = 1; m < wf; ++m) {
+                if (S2D && accum && !(row_ok && m < mmax)) continue;
+                for (int mt = 0; mt < mts; ++mt) {
+                  const uint32_t a = arow + (uint32_t)m + (uint32_t)mt * a_mt;
+                  const uint32_t b = brow + (uint32_t)m * b_tap;
+                  if constexpr (DA) {
+                    const uint32_t d = acc_base + (uint32_t)(mt * 2 * p.N);
+                    umma_tf32_elect(d, a, a_hi, b, b_hi, p.idesc2, S2D ? accum : 1u);
+                    umma_tf32_elect(d + (uint32_t)p.N, a + a_rem, a_hi, b, b_hi, p.idesc, 1u);
+                  } else {
+                    const uint32_t d = acc_base + (uint32_t)(mt * p.N);
+                    umma_tf32_elect(d, a, a_hi, b + b_rem, b_hi, p.idesc, S2D ? accum : 1u);
+                    umma_tf32_elect(d, a + a_rem, a_hi, b, b_hi, p.idesc, 1u);
+                    umma_tf32_elect(d, a, a_hi, b, b_hi, p.idesc, 1u);
+                  }
+                }
+                accum = 1u;
+              }
+            }
+        };
+        if constexpr (VAR == kWalkS2D) {
+          walk(std::true_type{}, std::false_type{});
+        } else if constexpr (VAR == kWalkWide) {
+          walk(std::false_type{}, std::true_type{});
+        } else {
+          // plain layers: the tap walk exactly as before the space-to-depth
+          // and wide-A variants existed (its issue latency is what N = 64
+          // and small-map layers are bound by)
+          const uint32_t a_lo0n =
+              ((a_base >> 4) & 0x3FFFu) | (((uint32_t)(p.plane_floats * 4) >> 4) << 16);
+          const uint32_t a_hin = ((uint32_t)(p.PW * 16) >> 4) | (1u << 14);
+          const uint32_t a_mtn = (uint32_t)(kTileRows * p.PW);
+          for (int gi = 0; gi < Ge; ++gi)
+            for (int n = 0; n < Re; ++n) {
+              const uint32_t arow = a_lo0n + (uint32_t)((gi * p.PH + n) * p.PW);
+              const uint32_t brow = b_lo0 + (uint32_t)((gi * p.R + n) * wf) * b_tap;
+  #pragma unroll
+              for (int m = 0; m < (WF_T > 0 ? WF_T : 1); ++m) {
+  #pragma unroll
+                for (int mt = 0; mt < kMtLoop; ++mt) {
+                  if (mt >= mts) break;
+                  const uint32_t a = arow + (uint32_t)m + (uint32_t)mt * a_mtn;
+                  const uint32_t b = brow + (uint32_t)m * b_tap;
+                  if constexpr (DA) {
+                    const uint32_t d = acc_base + (uint32_t)(mt * 2 * p.N);
+                    umma_tf32_elect(d, a, a_hin, b, b_hi, p.idesc2, accum);  // [main | corr]
+                    umma_tf32_elect(d + (uint32_t)p.N, a + a_rem, a_hin, b, b_hi, p.idesc, 1u);
+                  } else {
+                    const uint32_t d = acc_base + (uint32_t)(mt * p.N);
+                    // small terms first, the head product last
+                    umma_tf32_elect(d, a, a_hin, b + b_rem, b_hi, p.idesc, accum);
+                    umma_tf32_elect(d, a + a_rem, a_hin, b, b_hi, p.idesc, 1u);
+                    umma_tf32_elect(d, a, a_hin, b, b_hi, p.idesc, 1u);
+                  }
+                }
+                accum = 1u;
+              }
+              if (WF_T > 0) continue;
+              for (int m = 1; m < wf; ++m) {
+                for (int mt = 0; mt < mts; ++mt) {
+                  const uint32_t a = arow + (uint32_t)m + (uint32_t)mt * a_mtn;
+                  const uint32_t b = brow + (uint32_t)m * b_tap;
+                  if constexpr (DA) {
+                    const uint32_t d = acc_base + (uint32_t)(mt * 2 * p.N);
+                    umma_tf32_elect(d, a, a_hin, b, b_hi, p.idesc2, 1u);
+                    umma_tf32_elect(d + (uint32_t)p.N, a + a_rem, a_hin, b, b_hi, p.idesc, 1u);
+                  } else {
+                    const uint32_t d = acc_base + (uint32_t)(mt * p.N);
+                    umma_tf32_elect(d, a, a_hin, b + b_rem, b_hi, p.idesc, 1u);
+                    umma_tf32_elect(d, a + a_rem, a_hin, b, b_hi, p.idesc, 1u);
+                    umma_tf32_elect(d, a, a_hin, b, b_hi, p.idesc, 1u);
+                  }
                 }
               }
-              accum = 1u;
             }
-            if (WF_T > 0) continue;
-            for (int m = 1; m < wf; ++m) {
-              if (accum && !(row_ok && m < mmax)) continue;
-              for (int mt = 0; mt < mts; ++mt) {
-                const uint32_t a = arow + (uint32_t)m + (uint32_t)mt * a_mt;
-                const uint32_t b = brow + (uint32_t)m * b_tap;
-                if constexpr (DA) {
-                  const uint32_t d = acc_base + (uint32_t)(mt * 2 * p.N);
-                  umma_tf32_elect(d, a, a_hi, b, b_hi, p.idesc2, accum);
-                  umma_tf32_elect(d + (uint32_t)p.N, a + a_rem, a_hi, b, b_hi, p.idesc, 1u);
-                } else {
-                  const uint32_t d = acc_base + (uint32_t)(mt * p.N);
-                  umma_tf32_elect(d, a, a_hi, b + b_rem, b_hi, p.idesc, accum);
-                  umma_tf32_elect(d, a + a_rem, a_hi, b, b_hi, p.idesc, 1u);
-                  umma_tf32_elect(d, a, a_hi, b, b_hi, p.idesc, 1u);
-                }
-              }
-              accum = 1u;
-            }
-          }
+        }
         umma_commit_elect(&empty[buf]);  // stage smem free once these MMAs retire
         if (++ci == p.chunk_st || st == S - 1) {
           umma_commit_elect(&chunk_full[cs & 1]);
@@ -463,36 +527,33 @@ using X3Kernel = void (*)(const CUtensorMap, const Tf32Params);
 
 // (WF, MT, COLS) instantiations: WF in {3, 1, generic}, MT * N in {128, 256};
 // DA (N <= 128): MT * N = 128
-template <int WF>
+template <int WF, int V>
 X3Kernel pick_wf(int MT, int cols, bool da) {
-  if (da) return MT == 1 ? conv_tf32x3_kernel<WF, 1, 64, true> : conv_tf32x3_kernel<WF, 2, 64, true>;
+  if (da)
+    return MT == 1 ? conv_tf32x3_kernel<WF, 1, 64, true, V> : conv_tf32x3_kernel<WF, 2, 64, true, V>;
   if (MT == 1)
-    return cols == 64 ? conv_tf32x3_kernel<WF, 1, 64, false> : conv_tf32x3_kernel<WF, 1, 128, false>;
+    return cols == 64 ? conv_tf32x3_kernel<WF, 1, 64, false, V>
+                      : conv_tf32x3_kernel<WF, 1, 128, false, V>;
   if (MT == 2)
-    return cols == 64 ? conv_tf32x3_kernel<WF, 2, 64, false> : conv_tf32x3_kernel<WF, 2, 128, false>;
-  return conv_tf32x3_kernel<WF, 4, 128, false>;
+    return cols == 64 ? conv_tf32x3_kernel<WF, 2, 64, false, V>
+                      : conv_tf32x3_kernel<WF, 2, 128, false, V>;
+  return conv_tf32x3_kernel<WF, 4, 128, false, V>;
 }
+// walks as in conv_tf32.cu: 3x3 / generic plain or space-to-depth, 1x1 plain or wide
 X3Kernel pick_x3_kernel(const Tf32Params& p) {
   const int cols = p.MT * p.N / 2;
-  if (p.w_f == 3) return pick_wf<3>(p.MT, cols, p.da);
-  if (p.w_f == 1) return pick_wf<1>(p.MT, cols, p.da);
-  return pick_wf<0>(p.MT, cols, p.da);
+  if (p.w_f == 1)
+    return p.wide ? pick_wf<1, kWalkWide>(p.MT, cols, p.da) : pick_wf<1, kWalkPlain>(p.MT, cols, p.da);
+  if (p.s2d > 1)
+    return p.w_f == 3 ? pick_wf<3, kWalkS2D>(p.MT, cols, p.da) : pick_wf<0, kWalkS2D>(p.MT, cols, p.da);
+  return p.w_f == 3 ? pick_wf<3, kWalkPlain>(p.MT, cols, p.da) : pick_wf<0, kWalkPlain>(p.MT, cols, p.da);
 }
 
-void set_x3_attrs() {
-  // attributes are per device: once for each device the kernels run on
-  if (!dconv_host::first_use_on_device(reinterpret_cast<const void*>(&set_x3_attrs),
-                                       dconv_host::current_device()))
-    return;
-  for (bool da : {false, true})
-    for (int mt : {1, 2, 4})
-      for (int cols : {64, 128}) {
-        if (da && (cols != 64 || mt == 4)) continue;
-        if (!da && mt == 4 && cols == 64) continue;
-        for (X3Kernel k : {pick_wf<3>(mt, cols, da), pick_wf<1>(mt, cols, da),
-                           pick_wf<0>(mt, cols, da)})
-          cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      }
+void set_x3_attrs(X3Kernel k) {
+  // attributes are per device: once for each (kernel, device)
+  if (dconv_host::first_use_on_device(reinterpret_cast<const void*>(k),
+                                      dconv_host::current_device()))
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 
 // separate correction accumulator for N = 64 (DCONV_X3_NO_DA: off); the
@@ -690,7 +751,7 @@ int launch_conv_tf32x3(const FfmaParams& f0, const float* w_prepared, cudaStream
                : p.stack > 1 ? encode_input_map(&map, view, p.PW, p.SP, 1)
                              : encode_input_map(&map, view, p.PW, p.PH, p.G))
     return rc;
-  set_x3_attrs();
+  set_x3_attrs(pick_x3_kernel(p));
   const size_t smem = (size_t)p.NS * stage_bytes + bar_bytes;
   const int grid = std::min(p.units, sms);
   static const bool dbg = getenv("DCONV_DEBUG") != nullptr;

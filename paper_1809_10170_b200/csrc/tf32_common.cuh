@@ -333,6 +333,10 @@ inline int encode_input_map_wide(CUtensorMap* map, const InView& v, int PW, int 
 // core matrices 8 px x 16 B, LBO = one plane (the second K half), SBO = one
 // tile row.  Wide: SWIZZLE_32B K-major (layout type 6), 8 px x 32 B atoms,
 // SBO 256 B.  `unit` = 16-byte units per pixel step (2 when wide).
+// tap-walk variants of the tensor-core kernels (template parameter VAR)
+constexpr int kWalkPlain = 0;  // stride-1 layers, half-plane A
+constexpr int kWalkS2D = 1;    // space-to-depth view: skip structurally zero taps
+constexpr int kWalkWide = 2;   // 1x1 whole-pencil (32-byte swizzled) A
 struct ADesc {
   uint32_t lo0, hi, unit;
 };
