@@ -197,7 +197,7 @@ def _cpu_layers(config: str):
 
 
 def cpu_reference(config: str, budget_s: float, trials: int = 9, warm: int = 2,
-                  runs: int = 2, alg2: bool = True) -> dict:
+                  runs: int = 3, alg2: bool = True) -> dict:
     """Restated reference Alg. 3 (oracle/oracle.c: j' parallel, i', l, k', n,
     m, ii, kk, jj; AVX2 8 x 14 tile) on the reference's own ThreadPool
     (thread_pool.cpp:64-97, oracle/_ref) with DCONV_THREADS = physical
@@ -223,6 +223,11 @@ def cpu_reference(config: str, budget_s: float, trials: int = 9, warm: int = 2,
             po.conv_direct_pool(xb[None], kb, l.c_i, l.c_o, l.s, workers, w_ob=14, out=o)
         return time.perf_counter() - t0
 
+    # settle the host first (pool threads spun up, pages touched, clocks
+    # ramped): without it the first run read ~25% below the second
+    t_settle = time.perf_counter()
+    while time.perf_counter() - t_settle < 1.5:
+        one()
     run_vals, all_min, samples = [], None, 0
     for _ in range(runs):
         ws = [one() for _ in range(warm)]
@@ -244,7 +249,8 @@ def cpu_reference(config: str, budget_s: float, trials: int = 9, warm: int = 2,
         "sample": (f"1 image of {config} ({len(layers)} layers, {flops / 1e9:.2f} GFLOP) through "
                    f"restated Alg. 3 (oracle/oracle.c, c_ob=8 w_ob=14 AVX2 tile) on the "
                    f"reference ThreadPool (DCONV_THREADS={workers} + caller = {threads} threads "
-                   f"= physical cores); median of <=9 samples after 2 warm-ups, {runs} runs; "
+                   f"= physical cores); after 1.5 s of settling passes, median of <=9 samples "
+                   f"after 2 warm-ups, {runs} runs (median reported); "
                    f"the reference's own conv_direct is absent from the snapshot"),
         "seconds_per_sample": flops / value / 1e9,
     }
@@ -288,7 +294,7 @@ def run_reference_arm(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    cb = cpu_reference(args.config, args.cpu_seconds, runs=2)
+    cb = cpu_reference(args.config, args.cpu_seconds, runs=3)
     batch = args.batch or DEFAULT_BATCH[args.config]
     line = {
         "metric": METRIC, "impl": "reference", "value": cb["value"],
