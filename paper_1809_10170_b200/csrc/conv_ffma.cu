@@ -288,6 +288,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
       mbar_init(&res_empty[i], 4);
     }
     fence_mbar_init();
+    if (p.dbg) p.dbg[blockIdx.x * 16 + 14] = clock64() - t_start;  // barriers initialised
   }
   // TMEM: running totals [0, 128) + (epilogue hand-off) 2 result buffers
   constexpr int kResCols = (NW / 4) * TPX * TCO;
@@ -310,6 +311,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
   // arrive now, wait only right before the first publish (the ranks' setup
   // and main loops overlap the barrier instead of waiting on it)
   if (ks > 1) cluster_arrive_release();
+  if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 15] = clock64() - t_start;  // setup done
 
   // unit u -> (co group fastest: concurrently running CTAs share the pixel
   // tile's patch rows in L2, consecutive waves reuse the weight slabs)
@@ -1168,10 +1170,11 @@ int launch_units(K kernel, int threads, FfmaParams p, size_t smem, int unit_begi
     }
     for (double& v : a) v /= grid;
     fprintf(stderr, "conv_ffma profile: grid=%d ks=%d avg cycles: setup=%.0f first_data=%.0f "
-            "loop_end=%.0f published=%.0f all_ready=%.0f reduced=%.0f exit=%.0f | producer "
+            "loop_end=%.0f published=%.0f all_ready=%.0f reduced=%.0f exit=%.0f | bars_init=%.0f "
+            "common_setup=%.0f | producer "
             "start=%.0f decoded=%.0f expect_tx=%.0f stage0_issued=%.0f | compute first_wait=%.0f | CTA start spread %lld ns, "
             "first start -> last exit %lld ns\n", grid, p.ksplit, a[1], a[2], a[3], a[4], a[5],
-            a[6], a[7], a[8], a[12], a[13], a[9], a[10], gmax0 - g0, g1 - g0);
+            a[6], a[7], a[14], a[15], a[8], a[12], a[13], a[9], a[10], gmax0 - g0, g1 - g0);
     cudaFree(p.dbg);
     p.dbg = nullptr;
   }
