@@ -692,7 +692,7 @@ def measure_config(ctx, args, config: str, batch: int, headline: bool) -> dict:
                f"per-step working set ~{ws_bytes / 1e6:.0f} MB > 126 MB L2 (streamed)"),
         "roofline": roof, "roof_algo": roof_algo, "gpu_launches": int(gpu_launches),
         "clocks": clk.summary(),
-        "tiles": {k: ["", "128x128", "256x64", "128x64"][v] for k, v in tiles.items()},
+        "tiles": {k: ["", "128x128", "256x64", "128x64", "256x32"][v] for k, v in tiles.items()},
         "layers": layers,
     }
     if parity is not None:

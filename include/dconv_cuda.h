@@ -103,7 +103,8 @@ typedef struct dconv_conv_desc {
   int co_block_begin;      /* first output block j' computed (C_o sharding) */
   int co_block_count;      /* number of output blocks computed; 0 = all */
   int tile_variant;        /* FFMA CTA tile: 0 = selector, 1 = 128 px x 128 ch,
-                              2 = 256 px x 64 ch, 3 = 128 px x 64 ch;
+                              2 = 256 px x 64 ch, 3 = 128 px x 64 ch,
+                              4 = 256 px x 32 ch (c_b = 8);
                               see Plan.autotune in nets.py */
 } dconv_conv_desc;
 
@@ -246,7 +247,7 @@ int dconv_debug_set_ownership(unsigned* counts, const float* base, int64_t n);
 
 /* Test hook for the FFMA launcher's per-(device, kernel, ks) cache of
  * co-resident clusters: the cached answer for CTA tile `tile_variant`
- * (1..3, as dconv_conv_desc.tile_variant) and cluster size ks next to a fresh
+ * (1..4, as dconv_conv_desc.tile_variant) and cluster size ks next to a fresh
  * cudaOccupancyMaxActiveClusters query of the same instantiation. */
 int dconv_cuda_ffma_cluster_slots(int tile_variant, int ks, int* cached, int* fresh);
 

@@ -246,7 +246,11 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
   constexpr int kTmemCols = (NW / 4) * TPX * TCO <= 128 ? 128 : ((NW / 4) * TPX * TCO <= 256 ? 256 : 512);
   constexpr int PG = BM / TPX;   // pixel groups (TPX pixels each)
   constexpr int CGT = BN / TCO;  // channel thread groups == output blocks
-  constexpr int WPG = PG / 4;    // warps along pixels
+  // warp shape: PPW pixel groups x CPW channel groups per warp (4 x 8; the
+  // 32-channel tile, CGT = 4: 8 x 4)
+  constexpr int PPW = CGT >= 8 ? 4 : 8, CPW = 32 / PPW;
+  static_assert(CGT % CPW == 0 || CGT == CPW, "warp shape");
+  constexpr int WPG = PG / PPW;  // warps along pixels
   constexpr int NP = TPX * TCO / 2;  // accumulator pairs per thread
   static_assert(PG * CGT == NW * 32, "thread tile mismatch");
   constexpr int CG = BN / 8;     // output blocks per CTA tile
@@ -344,8 +348,8 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
 #pragma unroll 1
           for (int half = 0; half < 2; ++half) {
             const int cw = qd + 4 * half;  // the compute warp whose tile this lane holds
-            const int pg = (cw % WPG) * 4 + (lane & 3);
-            const int cb = (cw / WPG) * 8 + (lane >> 2);
+            const int pg = (cw % WPG) * PPW + (lane % PPW);
+            const int cb = (cw / WPG) * CPW + lane / PPW;
             const int jl = jb0 + cb - p.jb_begin;
             const uint32_t tr_addr = tmem_base + ((uint32_t)(qd * 32) << 16) +
                                      (uint32_t)(kResCols * (1 + rb) + half * TPX * TCO);
@@ -533,8 +537,8 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
     asm volatile("setmaxnreg.inc.sync.aligned.u32 152;");
   }
   const int wr = warp % WPG, wc = warp / WPG;
-  const int pg = wr * 4 + (lane & 3);
-  const int cb = (wc * 8 + (lane >> 2)) * NBLK;  // first output block within the CTA tile
+  const int pg = wr * PPW + (lane % PPW);
+  const int cb = (wc * CPW + lane / PPW) * NBLK;  // first output block within the CTA tile
 
   const uint32_t tmem_base = tmem_on ? *tmem_slot : 0u;
   if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 1] = clock64() - t_start;  // setup done
@@ -590,7 +594,10 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
       // quarter-warp that read 4 pixels' same channel quarter hit one bank
       // group; odd lanes take the two channel halves in the other order
       // (activations 2-way instead of 4-way, weights 2-way instead of none)
-      const int hswap = CBS == 32 ? (lane & 1) : 0;
+      // 8 x 4 warp shape: a quarter-warp reads 8 pixels 32 B apart (two
+      // bank rows); lanes 4-7 of it take the channel halves in the other order
+      // so its 16-byte reads land on 8 distinct bank groups
+      const int hswap = CBS == 32 ? (lane & 1) : (PPW == 8 ? ((lane >> 2) & 1) : 0);
       auto tap = [&](const float* pw, int aoff) {
 #pragma unroll
         for (int half_i = 0; half_i < 8 / AV; ++half_i) {
@@ -1369,6 +1376,7 @@ int ffma_cluster_slots_probe(int tile_variant, int ks, int* cached, int* fresh) 
     case 1: return probe_slots<128, 128, 8, 8, 8>(ks, cached, fresh);
     case 2: return probe_slots<256, 64, 8, 8, 8>(ks, cached, fresh);
     case 3: return probe_slots<128, 64, 8, 4, 8>(ks, cached, fresh);
+    case 4: return probe_slots<256, 32, 8, 4, 8>(ks, cached, fresh);
     default: return dconv_host::set_error(DCONV_EPARAM, "tile_variant %d", tile_variant);
   }
 }
@@ -1400,7 +1408,9 @@ int launch_conv_ffma(const FfmaParams& p0, cudaStream_t stream) {
   // measured (tools/sweep_variants.py): 256 px x 64 ch wins on every 3x3 /
   // 5x5 layer of the configs; 1x1 layers with >= 128 output channels
   // (little reuse per staged pixel) prefer 128 px x 128 ch
-  if (v < 0) v = (p.h_f * p.w_f == 1 && p.jb_count >= 16) ? 0 : 1;
+  if (v < 0)
+    v = (p.h_f * p.w_f == 1 && p.jb_count >= 16) ? 0
+        : (p.jb_count <= 4 && !(p.epi & DCONV_EPI_MAXPOOL)) ? 3 : 1;
   if (p.cbs != 8) {
     // c_b = 16 / 32: the two main CTA tiles (the 128 x 64 batch-1 tile
     // runs as 256 x 64)
@@ -1426,6 +1436,11 @@ int launch_conv_ffma(const FfmaParams& p0, cudaStream_t stream) {
       if (p.epi & DCONV_EPI_MAXPOOL)
         return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_ffma: 128x64 tile has no fused pool");
       return launch_wf<128, 64, 8, 4, 8>(p, stream);
+    case 3:  // 256 px x 32 channels, 4 px x 8 ch per thread: layers with C_o = 32
+             // (or C_o / 32 odd: no half-empty 64-channel group)
+      if (p.epi & DCONV_EPI_MAXPOOL)
+        return dconv_host::set_error(DCONV_EUNSUPPORTED, "conv_ffma: 256x32 tile has no fused pool");
+      return launch_wf<256, 32, 8, 4, 8>(p, stream);
     default: return launch_wf<256, 64>(p, stream);  // 256 px x 64 channels
   }
 }

@@ -407,7 +407,12 @@ class Plan:
             if st.kind != "conv":
                 continue
             best, best_ms = 0, None
-            for v in variants:
+            # the 256 px x 32 ch tile only where 64-channel groups leave one
+            # half empty (C_o = 32, 224, ...)
+            l = st.layer
+            vs = tuple(variants) + ((4,) if l is not None and l.c_o % 64 and 4 not in variants
+                                    else ())
+            for v in vs:
                 self.tiles[st.name] = v
                 ts = []
                 for r in range(reps + 1):

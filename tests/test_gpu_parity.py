@@ -330,9 +330,9 @@ def test_first_layer_reader_variants(s, f, ci, co):
         assert_tol(got[i], want, f"first s={s} f={f} img {i}")
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
 def test_ffma_tile_variants(variant):
-    """The FFMA CTA tiles (128 px x 128 ch, 256 px x 64 ch, 128 px x 64 ch) on ragged shapes,
+    """The FFMA CTA tiles (128 px x 128 ch, 256 px x 64 ch, 128 px x 64 ch, 256 px x 32 ch) on ragged shapes,
     strides, filter widths 1/3/5/7 (templated and runtime), and a K = 4608
     layer where the TMEM two-level sum matters (desc.tile_variant)."""
     cases = [(64, 64, 58, 58, 3, 1), (24, 40, 17, 23, 5, 1), (16, 136, 19, 21, 7, 2),
@@ -345,7 +345,36 @@ def test_ffma_tile_variants(variant):
                    f"variant {variant} case {t}")
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("ks", [0, 1, 2, 4])
+def test_ffma_32_channel_tile_epilogues(ks, monkeypatch):
+    """The 256 px x 32 ch CTA tile (8 x 4 warp shape, lanes 4-7 of a
+    quarter-warp reading the channel halves swapped): GoogLeNet's 5x5 16->32
+    and 3x3 112->224 (seven 32-channel groups) shapes and a ragged C_o, with
+    the fused skip-add + ReLU epilogue (epilogue warpgroup) and forced split-K
+    factors (DSMEM reduction) -- every image against the oracle."""
+    if ks:
+        monkeypatch.setenv("DCONV_KSPLIT", str(ks))
+    cases = [(16, 32, 12, 12, 5, 1, 3), (112, 224, 9, 9, 3, 1, 2), (40, 20, 11, 13, 3, 2, 2),
+             (64, 96, 8, 8, 1, 1, 3)]
+    for t, (ci, co, hi, wi, f, s, n) in enumerate(cases):
+        l = nets.Layer("t32", ci, co, hi, wi, f, f, s)
+        x = po.uniform((n, ci, hi, wi), 1200 + t, ks)
+        k = po.uniform((ci, co, f, f), 1210 + t, ks)
+        sk = po.uniform((n, co, l.h_o, l.w_o), 1220 + t, ks)
+        a = nets.Act(n, ci, hi, wi)
+        a.buf.copy_(dev(np.stack([po.pack_feature_map(x[i], 8) for i in range(n)])))
+        skip = nets.Act(n, co, l.h_o, l.w_o)
+        skip.buf.copy_(dev(np.stack([po.pack_feature_map(sk[i], 8) for i in range(n)])))
+        y = nets.Act(n, co, l.h_o, l.w_o)
+        nets.conv(l, n, a, nets.pack_weights(dev(k), False), y, _abi.EPI_ADD | _abi.EPI_RELU,
+                  skip, tile_variant=4)
+        got = host(y.buf)
+        for i in range(n):
+            want = np.maximum(po.conv_oracle64(x[i], k, s) + sk[i], 0)
+            assert_tol(got[i], po.pack_feature_map(want, 8), f"ks {ks} case {t} img {i}")
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
 def test_batched_stacked_tiles(variant):
     """Pixel tiles over the batch-stacked output span several images (maps of
     height 1..9 with tiles of up to 64 rows): every image checked."""
@@ -551,7 +580,7 @@ def test_cluster_slots_cached_per_kernel():
     batch-1 split-K layer runs correctly on each tile in turn."""
     lib = _abi.lib()
     for ks in (2, 4, 8, 16):
-        for variant in (1, 2, 3, 1):
+        for variant in (1, 2, 3, 4, 1):
             cached, fresh = ctypes.c_int(0), ctypes.c_int(0)
             _abi.check(lib.dconv_cuda_ffma_cluster_slots(variant, ks, ctypes.byref(cached),
                                                          ctypes.byref(fresh)))
