@@ -219,10 +219,10 @@ __global__ void __launch_bounds__(kThreadsT, 1)
               const uint32_t arow = a_lo0 + (uint32_t)((gi * p.PH + n) * p.PW) * AU;
               const uint32_t brow = b_lo0 + (uint32_t)((gi * p.R + n) * wf) * b_tap;
               if (MT_T > 0 && mts == MT_T) {
-  #pragma unroll
+#pragma unroll
                 for (int m = 0; m < (WF_T > 0 ? WF_T : 1); ++m) {
                   if (S2D && accum && !(row_ok && m < mmax)) continue;
-  #pragma unroll
+#pragma unroll
                   for (int mt = 0; mt < MT_T; ++mt)
                     umma_tf32_elect(acc_base + (uint32_t)(mt * p.N),
                                     arow + (uint32_t)m * AU + (uint32_t)mt * a_mt, a_hi,
@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
                 if (WF_T > 0) continue;
                 for (int m = 1; m < wf; ++m) {
                   if (S2D && accum && !(row_ok && m < mmax)) continue;
-  #pragma unroll
+#pragma unroll
                   for (int mt = 0; mt < MT_T; ++mt)
                     umma_tf32_elect(acc_base + (uint32_t)(mt * p.N),
                                     arow + (uint32_t)m * AU + (uint32_t)mt * a_mt, a_hi,
@@ -257,46 +257,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
         } else if constexpr (VAR == kWalkWide) {
           walk(std::false_type{}, std::true_type{});
         } else {
-          // plain layers: the tap walk exactly as before the space-to-depth
-          // and wide-A variants existed (its issue latency is what N = 64
-          // and small-map layers are bound by)
-          const uint32_t a_lo0n =
-              ((a_base >> 4) & 0x3FFFu) | (((uint32_t)(p.plane_floats * 4) >> 4) << 16);
-          const uint32_t a_hin = ((uint32_t)(p.PW * 16) >> 4) | (1u << 14);
-          const uint32_t a_mtn = (uint32_t)(kTileRows * p.PW);
-          for (int gi = 0; gi < Ge; ++gi)
-            for (int n = 0; n < Re; ++n) {
-              const uint32_t arow = a_lo0n + (uint32_t)((gi * p.PH + n) * p.PW);
-              const uint32_t brow = b_lo0 + (uint32_t)((gi * p.R + n) * wf) * b_tap;
-              if (MT_T > 0 && mts == MT_T) {
-  #pragma unroll
-                for (int m = 0; m < (WF_T > 0 ? WF_T : 1); ++m) {
-  #pragma unroll
-                  for (int mt = 0; mt < MT_T; ++mt)
-                    umma_tf32_elect(acc_base + (uint32_t)(mt * p.N),
-                                    arow + (uint32_t)m + (uint32_t)mt * a_mtn, a_hin,
-                                    brow + (uint32_t)m * b_tap, b_hi, p.idesc, accum);
-                  accum = 1u;
-                }
-                if (WF_T > 0) continue;
-                for (int m = 1; m < wf; ++m) {
-  #pragma unroll
-                  for (int mt = 0; mt < MT_T; ++mt)
-                    umma_tf32_elect(acc_base + (uint32_t)(mt * p.N),
-                                    arow + (uint32_t)m + (uint32_t)mt * a_mtn, a_hin,
-                                    brow + (uint32_t)m * b_tap, b_hi, p.idesc, 1u);
-                }
-                continue;
-              }
-              for (int m = 0; m < wf; ++m) {
-                const uint32_t blo = brow + (uint32_t)m * b_tap;
-                uint32_t alo = arow + (uint32_t)m;
-                for (int mt = 0; mt < mts; ++mt, alo += a_mtn)
-                  umma_tf32_elect(acc_base + (uint32_t)(mt * p.N), alo, a_hin, blo, b_hi, p.idesc,
-                                  accum);
-                accum = 1u;
-              }
-            }
+          walk(std::false_type{}, std::false_type{});
         }
         if (p.dbg) prof[4] += clock64() - t_issue;
         umma_commit_elect(&empty[buf]);  // stage smem free once these MMAs retire

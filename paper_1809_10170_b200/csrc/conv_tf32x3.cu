@@ -261,10 +261,10 @@ __global__ void __launch_bounds__(kThreadsX, 1)
               const bool row_ok = !S2D || r * p.R + n < nmax;
               const uint32_t arow = a_lo0 + (uint32_t)((gi * p.PH + n) * p.PW) * AU;
               const uint32_t brow = b_lo0 + (uint32_t)((gi * p.R + n) * wf) * b_tap;
-  #pragma unroll
+#pragma unroll
               for (int m = 0; m < (WF_T > 0 ? WF_T : 1); ++m) {
                 if (S2D && accum && !(row_ok && m < mmax)) continue;
-  #pragma unroll
+#pragma unroll
                 for (int mt = 0; mt < kMtLoop; ++mt) {
                   if (mt >= mts) break;
                   const uint32_t a = arow + (uint32_t)m + (uint32_t)mt * a_mt;
@@ -309,56 +309,7 @@ __global__ void __launch_bounds__(kThreadsX, 1)
         } else if constexpr (VAR == kWalkWide) {
           walk(std::false_type{}, std::true_type{});
         } else {
-          // plain layers: the tap walk exactly as before the space-to-depth
-          // and wide-A variants existed (its issue latency is what N = 64
-          // and small-map layers are bound by)
-          const uint32_t a_lo0n =
-              ((a_base >> 4) & 0x3FFFu) | (((uint32_t)(p.plane_floats * 4) >> 4) << 16);
-          const uint32_t a_hin = ((uint32_t)(p.PW * 16) >> 4) | (1u << 14);
-          const uint32_t a_mtn = (uint32_t)(kTileRows * p.PW);
-          for (int gi = 0; gi < Ge; ++gi)
-            for (int n = 0; n < Re; ++n) {
-              const uint32_t arow = a_lo0n + (uint32_t)((gi * p.PH + n) * p.PW);
-              const uint32_t brow = b_lo0 + (uint32_t)((gi * p.R + n) * wf) * b_tap;
-  #pragma unroll
-              for (int m = 0; m < (WF_T > 0 ? WF_T : 1); ++m) {
-  #pragma unroll
-                for (int mt = 0; mt < kMtLoop; ++mt) {
-                  if (mt >= mts) break;
-                  const uint32_t a = arow + (uint32_t)m + (uint32_t)mt * a_mtn;
-                  const uint32_t b = brow + (uint32_t)m * b_tap;
-                  if constexpr (DA) {
-                    const uint32_t d = acc_base + (uint32_t)(mt * 2 * p.N);
-                    umma_tf32_elect(d, a, a_hin, b, b_hi, p.idesc2, accum);  // [main | corr]
-                    umma_tf32_elect(d + (uint32_t)p.N, a + a_rem, a_hin, b, b_hi, p.idesc, 1u);
-                  } else {
-                    const uint32_t d = acc_base + (uint32_t)(mt * p.N);
-                    // small terms first, the head product last
-                    umma_tf32_elect(d, a, a_hin, b + b_rem, b_hi, p.idesc, accum);
-                    umma_tf32_elect(d, a + a_rem, a_hin, b, b_hi, p.idesc, 1u);
-                    umma_tf32_elect(d, a, a_hin, b, b_hi, p.idesc, 1u);
-                  }
-                }
-                accum = 1u;
-              }
-              if (WF_T > 0) continue;
-              for (int m = 1; m < wf; ++m) {
-                for (int mt = 0; mt < mts; ++mt) {
-                  const uint32_t a = arow + (uint32_t)m + (uint32_t)mt * a_mtn;
-                  const uint32_t b = brow + (uint32_t)m * b_tap;
-                  if constexpr (DA) {
-                    const uint32_t d = acc_base + (uint32_t)(mt * 2 * p.N);
-                    umma_tf32_elect(d, a, a_hin, b, b_hi, p.idesc2, 1u);
-                    umma_tf32_elect(d + (uint32_t)p.N, a + a_rem, a_hin, b, b_hi, p.idesc, 1u);
-                  } else {
-                    const uint32_t d = acc_base + (uint32_t)(mt * p.N);
-                    umma_tf32_elect(d, a, a_hin, b + b_rem, b_hi, p.idesc, 1u);
-                    umma_tf32_elect(d, a + a_rem, a_hin, b, b_hi, p.idesc, 1u);
-                    umma_tf32_elect(d, a, a_hin, b, b_hi, p.idesc, 1u);
-                  }
-                }
-              }
-            }
+          walk(std::false_type{}, std::false_type{});
         }
         umma_commit_elect(&empty[buf]);  // stage smem free once these MMAs retire
         if (++ci == p.chunk_st || st == S - 1) {
