@@ -466,7 +466,12 @@ int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t
   if (p.stack > 1)
     while ((p.PH * p.PW) % 8) ++p.PH;
   const int patch_blk_bytes = 2 * p.PH * p.PW * 16;  // both planes
-  p.G = p.R == p.h_f ? std::max(1, std::min({p.ib_n, (48 * 1024) / (p.h_f * p.w_f * wtap),
+  // space-to-depth layers: a 72 KB weight budget (two input blocks of a 2x2
+  // phase filter at N = 256): their stages carry few valid taps, and the
+  // per-stage hand-offs, not the loads, bound them
+  static const int s2d_wkb = getenv("DCONV_S2D_WKB") ? atoi(getenv("DCONV_S2D_WKB")) : 72;
+  const int wbudget = (p.s2d > 1 ? s2d_wkb : 48) * 1024;
+  p.G = p.R == p.h_f ? std::max(1, std::min({p.ib_n, wbudget / (p.h_f * p.w_f * wtap),
                                              (40 * 1024) / patch_blk_bytes}))
                      : 1;
   // 1x1 layers with >= 256 input channels: at least 4 ring stages (as the
