@@ -853,7 +853,7 @@ def test_autotuned_plan_matches_default_tiles():
     a = nets.build_plan("googlenet", 2, seed=11)
     b = nets.build_plan("googlenet", 2, seed=11)
     tiles = b.autotune()
-    assert set(tiles.values()) <= {1, 2, 3}
+    assert set(tiles.values()) <= {1, 2, 3, 4}
     a.run()
     b.run()
     torch.cuda.synchronize()
