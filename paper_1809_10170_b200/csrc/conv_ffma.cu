@@ -44,6 +44,15 @@ constexpr int kCB = 8;          // channels per math sub-block (a thread's 8 out
 constexpr int kMaxStages = 8;
 constexpr int kMaxKs = 16;      // split-K cluster size (> 8 is the non-portable opt-in)
 
+// Per-CTA phase clocks (DCONV_FFMA_PROFILE=1): compiled in only with
+// -DDCONV_FFMA_PROF (tools/build_prof.sh) -- the stamps' tests cost the
+// product build 1.7% on VGG-16 b32 and 7% on 1x1 layers.
+#ifdef DCONV_FFMA_PROF
+constexpr bool kFfmaProf = true;
+#else
+constexpr bool kFfmaProf = false;
+#endif
+
 // Tuning / debugging overrides, read once per process --
 // except DCONV_KSPLIT, read at every launch so a test can force several
 // split factors in one process.
@@ -267,8 +276,8 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const long long t_start = p.dbg ? clock64() : 0;
-  if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 16 + 0] = (long long)globaltimer_ns();
+  const long long t_start = kFfmaProf && p.dbg ? clock64() : 0;
+  if (kFfmaProf && p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 16 + 0] = (long long)globaltimer_ns();
   const int S = p.n_g * p.n_r;                 // stages per work unit
   const int co_groups = (p.jb_count + CG - 1) / CG;
   const int n_units = p.unit_count;             // this launch's units: [unit_begin, +count)
@@ -315,7 +324,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
   // arrive now, wait only right before the first publish (the ranks' setup
   // and main loops overlap the barrier instead of waiting on it)
   if (ks > 1) cluster_arrive_release();
-  if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 15] = clock64() - t_start;  // setup done
+  if (kFfmaProf && p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 15] = clock64() - t_start;  // setup done
 
   // unit u -> (co group fastest: concurrently running CTAs share the pixel
   // tile's patch rows in L2, consecutive waves reuse the weight slabs)
@@ -438,14 +447,14 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
     constexpr int kProdWarps = 4;
     const int pw = warp - NW;
     const int pt = pw * 32 + lane;  // producer thread index
-    if (p.dbg && pt == 0) p.dbg[blockIdx.x * 16 + 8] = clock64() - t_start;
+    if (kFfmaProf && p.dbg && pt == 0) p.dbg[blockIdx.x * 16 + 8] = clock64() - t_start;
     int gs = 0;
     const int seg_rows_full = (p.h_o - 1) * p.sy;  // + Re per full segment
     for (int u = cluster_id; u < n_units; u += n_clusters) {
       TileRows tr;
       int tx0, jb0, cg_valid;
       decode(u, tr, tx0, jb0, cg_valid);
-      if (p.dbg && pt == 0 && gs == 0) p.dbg[blockIdx.x * 16 + 12] = clock64() - t_start;
+      if (kFfmaProf && p.dbg && pt == 0 && gs == 0) p.dbg[blockIdx.x * 16 + 12] = clock64() - t_start;
       const int col0 = tx0 * p.s;
       const int cols = min(p.PW, p.w_i - col0);
       const int n_seg = 1 + (tr.th - tr.cnt0 + p.h_o - 1) / p.h_o;
@@ -485,7 +494,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
         // it (the transaction count is allowed to run ahead within a phase)
         if (pt == 0) mbar_arrive_expect_tx(&full[buf], patch_bytes + wbytes * n_wblk);
         __syncwarp();
-        if (p.dbg && pt == 0 && gs == 0) p.dbg[blockIdx.x * 16 + 13] = clock64() - t_start;
+        if (kFfmaProf && p.dbg && pt == 0 && gs == 0) p.dbg[blockIdx.x * 16 + 13] = clock64() - t_start;
         // the stage's copies are numbered in one sequence (segments' rows,
         // then weight chunks) and dealt round-robin over the producer warps
         // (copy c -> warp c % 4, lane c / 4 % 32): a bulk copy takes uniform
@@ -524,7 +533,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
                              (int64_t)n0 * p.w_f * CBS * CBS;
           bulk_g2s(sw + wchunk<TCO>(c, p.wstride_floats), src, wbytes, &full[buf]);
         }
-        if (p.dbg && pt == 0 && gs == 0) p.dbg[blockIdx.x * 16 + 9] = clock64() - t_start;
+        if (kFfmaProf && p.dbg && pt == 0 && gs == 0) p.dbg[blockIdx.x * 16 + 9] = clock64() - t_start;
       }
     }
     return;
@@ -541,7 +550,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
   const int cb = (wc * CPW + lane / PPW) * NBLK;  // first output block within the CTA tile
 
   const uint32_t tmem_base = tmem_on ? *tmem_slot : 0u;
-  if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 1] = clock64() - t_start;  // setup done
+  if (kFfmaProf && p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 1] = clock64() - t_start;  // setup done
   const uint32_t taddr = tmem_base + ((uint32_t)((warp & 3) * 32) << 16) +
                          (uint32_t)((warp >> 2) * TPX * TCO);
   const int wf = WF > 0 ? WF : p.w_f;
@@ -571,9 +580,9 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
 
     for (int st = st0; st < st1; ++st, ++gs) {
       const int buf = gs % p.NS;
-      if (p.dbg && tid == 0 && gs == 0) p.dbg[blockIdx.x * 16 + 10] = clock64() - t_start;
+      if (kFfmaProf && p.dbg && tid == 0 && gs == 0) p.dbg[blockIdx.x * 16 + 10] = clock64() - t_start;
       mbar_wait(&full[buf], (gs / p.NS) & 1);
-      if (p.dbg && tid == 0 && gs == 0) p.dbg[blockIdx.x * 16 + 2] = clock64() - t_start;
+      if (kFfmaProf && p.dbg && tid == 0 && gs == 0) p.dbg[blockIdx.x * 16 + 2] = clock64() - t_start;
       const int g = st / p.n_r, r = st - g * p.n_r;
       const int Ge = min(p.G, p.ib_n - g * p.G);
       const int Re = min(p.R, p.h_f - r * p.R);
@@ -668,7 +677,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
           for (int c = 0; c < TCO / 2; ++c) acc[k][c] = 0ull;
       }
     }
-    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 3] = clock64() - t_start;  // loop end
+    if (kFfmaProf && p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 3] = clock64() - t_start;  // loop end
     if (p.epi_wg) {
       // hand the finished tile to the epilogue warpgroup (TMEM result buffer
       // unit_iter & 1) and go on with the next unit
@@ -750,13 +759,13 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
       }
       // every compute warp's stores issued: one fence, ks relaxed arrives
       asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
-      if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 4] = clock64() - t_start;  // published
+      if (kFfmaProf && p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 4] = clock64() - t_start;  // published
       if (tid == 0) {
         fence_cluster();
         for (int q = 0; q < ks; ++q) mbar_arrive_remote_relaxed(ready, q);
       }
       mbar_wait_cluster(ready, unit_iter & 1);
-      if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 5] = clock64() - t_start;  // all ready
+      if (kFfmaProf && p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 5] = clock64() - t_start;  // all ready
       if (cb < cg_valid) {
         const int jl = jb0 + cb - p.jb_begin;
         const int i_lo = rank * kItems / ks, i_hi = (rank + 1) * kItems / ks;
@@ -795,7 +804,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
             *reinterpret_cast<float4*>(p.peer_out[pi] + off) = v;
         }
       }
-      if (p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 6] = clock64() - t_start;  // reduced
+      if (kFfmaProf && p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 6] = clock64() - t_start;  // reduced
       if (!last_unit) {
         // every compute warp has read its slots: the ranks may publish again
         asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
@@ -870,7 +879,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
   // (push model: every remote access to this CTA's smem -- the peers'
   // partial stores and arrives -- completes before its last `ready` wait, so
   // no exit barrier is needed)
-  if (p.dbg && tid == 0) {
+  if (kFfmaProf && p.dbg && tid == 0) {
     p.dbg[blockIdx.x * 16 + 7] = clock64() - t_start;  // exit
     p.dbg[blockIdx.x * 16 + 11] = (long long)globaltimer_ns();
   }
@@ -1143,7 +1152,7 @@ int launch_units(K kernel, int threads, FfmaParams p, size_t smem, int unit_begi
   // producer L2 prefetch would cost a bulk op per 256-B skip row and make
   // the single producer warp the bottleneck (measured on 1x1 layers)
   if (p.epi_wg) p.skip_prefetch = 0;
-  static const bool prof = getenv("DCONV_FFMA_PROFILE") != nullptr;
+  static const bool prof = kFfmaProf && getenv("DCONV_FFMA_PROFILE") != nullptr;  // profiling builds only
   if (prof) {  // debugging aid: per-CTA phase clocks of one extra launch
     const int grid = p.ksplit == 1 ? clusters : clusters * p.ksplit;
     cudaMalloc(&p.dbg, (size_t)grid * 16 * 8);
@@ -1408,9 +1417,12 @@ int launch_conv_ffma(const FfmaParams& p0, cudaStream_t stream) {
   // measured (tools/sweep_variants.py): 256 px x 64 ch wins on every 3x3 /
   // 5x5 layer of the configs; 1x1 layers with >= 128 output channels
   // (little reuse per staged pixel) prefer 128 px x 128 ch
+  // (the 32-channel tile by default only for layers of <= 32 channels, not
+  // for <= 32-channel C_o slices of wider layers: a slice then runs the
+  // unsharded layer's tiling, so C_o-sharded ranks reproduce it bitwise)
   if (v < 0)
     v = (p.h_f * p.w_f == 1 && p.jb_count >= 16) ? 0
-        : (p.jb_count <= 4 && !(p.epi & DCONV_EPI_MAXPOOL)) ? 3 : 1;
+        : (p.jb_n * sub <= 4 && !(p.epi & DCONV_EPI_MAXPOOL)) ? 3 : 1;
   if (p.cbs != 8) {
     // c_b = 16 / 32: the two main CTA tiles (the 128 x 64 batch-1 tile
     // runs as 256 x 64)

@@ -39,6 +39,13 @@ namespace {
 using namespace tf32;
 constexpr int kEpiWarps = 8;   // 2 per TMEM lane quarter, each half of the columns
 constexpr int kThreadsT = (2 + kEpiWarps) * 32;
+// Per-role wait clocks (DCONV_TF32_PROFILE=1): compiled in only with
+// -DDCONV_TF32_PROF (tools/build_prof.sh), no cost in the product build.
+#ifdef DCONV_TF32_PROF
+constexpr bool kTf32Prof = true;
+#else
+constexpr bool kTf32Prof = false;
+#endif
 
 // WF_T / MT_T: filter width and M-tiles per unit as compile-time constants
 // (0 = runtime), so the per-stage MMA walk unrolls into straight-line issue.
@@ -60,7 +67,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = p.n_g * p.n_r;
   long long prof[6] = {0, 0, 0, 0, 0, 0};  // DCONV_TF32_PROFILE only
-  const long long prof_t0 = p.dbg ? clock64() : 0;
+  const long long prof_t0 = kTf32Prof && p.dbg ? clock64() : 0;
   const uint32_t tmem_cols = 512;
   const int nacc = p.MT * p.N <= 256 ? 2 : 1;
   const uint32_t acc_cols = (uint32_t)(p.MT * p.N);
@@ -107,9 +114,9 @@ __global__ void __launch_bounds__(kThreadsT, 1)
           if (st > 0 && ++r == p.n_r) { r = 0; ++g; }
           if (gs > 0 && ++buf == p.NS) { buf = 0; phase ^= 1u; }
           if (gs >= p.NS) {
-            const long long t0 = p.dbg ? clock64() : 0;
+            const long long t0 = kTf32Prof && p.dbg ? clock64() : 0;
             mbar_wait_backoff(&empty[buf], phase ^ 1u, 64);
-            if (p.dbg) prof[0] += clock64() - t0;
+            if (kTf32Prof && p.dbg) prof[0] += clock64() - t0;
           }
           const int ib0 = g * p.G, n0 = r * p.R;
           const int Ge = min(p.G, p.ib_n - ib0), Re = min(p.R, p.h_f - n0);
@@ -168,9 +175,9 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       const int ab = nacc == 2 ? (ui & 1) : 0, au = nacc == 2 ? (ui >> 1) : ui;
       const uint32_t acc_base = tmem_base + (uint32_t)ab * acc_cols;
       if (au > 0) {
-        const long long t0 = p.dbg ? clock64() : 0;
+        const long long t0 = kTf32Prof && p.dbg ? clock64() : 0;
         mbar_wait(&acc_empty[ab], (au - 1) & 1);  // epilogue drained this TMEM set
-        if (p.dbg) prof[2] += clock64() - t0;
+        if (kTf32Prof && p.dbg) prof[2] += clock64() - t0;
       }
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       int g = 0, r = 0;
@@ -178,12 +185,12 @@ __global__ void __launch_bounds__(kThreadsT, 1)
         if (st > 0 && ++r == p.n_r) { r = 0; ++g; }
         if (gs > 0 && ++buf == p.NS) { buf = 0; phase ^= 1u; }
         {
-          const long long t0 = p.dbg ? clock64() : 0;
+          const long long t0 = kTf32Prof && p.dbg ? clock64() : 0;
           mbar_wait(&full[buf], phase);
-          if (p.dbg) prof[1] += clock64() - t0;
+          if (kTf32Prof && p.dbg) prof[1] += clock64() - t0;
         }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const long long t_issue = p.dbg ? clock64() : 0;
+        const long long t_issue = kTf32Prof && p.dbg ? clock64() : 0;
         const int Ge = min(p.G, p.ib_n - g * p.G);
         const int Re = min(p.R, p.h_f - r * p.R);
         const float* sp = smem + buf * p.stage_floats;
@@ -259,11 +266,11 @@ __global__ void __launch_bounds__(kThreadsT, 1)
         } else {
           walk(std::false_type{}, std::false_type{});
         }
-        if (p.dbg) prof[4] += clock64() - t_issue;
+        if (kTf32Prof && p.dbg) prof[4] += clock64() - t_issue;
         umma_commit_elect(&empty[buf]);  // stage smem free once these MMAs retire
         if (st == S - 1) umma_commit_elect(&acc_full[ab]);
         __syncwarp();
-        if (p.dbg) prof[5] += clock64() - t_issue;
+        if (kTf32Prof && p.dbg) prof[5] += clock64() - t_issue;
       }
     }
   } else {
@@ -300,7 +307,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
     }
   }
 
-  if (p.dbg) {  // per-role cycle sums, kept in registers during the loop
+  if (kTf32Prof && p.dbg) {  // per-role cycle sums, kept in registers during the loop
     if (threadIdx.x == 0) p.dbg[blockIdx.x * 8 + 0] = prof[0];
     if (threadIdx.x == 32)
       for (int i = 1; i < 6; ++i) p.dbg[blockIdx.x * 8 + i] = prof[i];
@@ -534,7 +541,7 @@ int launch_conv_tf32(const FfmaParams& f0, const float* w_prepared, cudaStream_t
   if (dbg)
     fprintf(stderr, "conv_tf32 N=%d MT=%d G=%d R=%d NS=%d stage=%d B stack=%d s2d=%d units=%d\n",
             p.N, p.MT, p.G, p.R, p.NS, stage_bytes, p.stack, p.s2d, p.units);
-  static const bool prof = getenv("DCONV_TF32_PROFILE") != nullptr;
+  static const bool prof = kTf32Prof && getenv("DCONV_TF32_PROFILE") != nullptr;  // profiling builds only
   if (prof) {  // debugging aid: where do the roles wait?  (not for timed runs)
     cudaMalloc(&p.dbg, (size_t)grid * 8 * 8);
     cudaMemsetAsync(p.dbg, 0, (size_t)grid * 8 * 8, stream);

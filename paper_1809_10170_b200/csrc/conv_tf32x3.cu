@@ -47,7 +47,7 @@ constexpr int kEpiWarpsX = 8;
 constexpr int kThreadsX = (4 + kEpiWarpsX) * 32;
 constexpr uint32_t kHiMask = 0xFFFFE000u;  // TF32: sign, exponent, 10 mantissa bits
 // Role wait-cycle instrumentation (DCONV_TF32_PROFILE), compiled in only when
-// built with -DDCONV_X3_PROF (tools/build_x3_prof.sh): it costs registers in
+// built with -DDCONV_X3_PROF (tools/build_prof.sh): it costs registers in
 // the 56-register producer/MMA/split group.
 #ifdef DCONV_X3_PROF
 constexpr bool kProf = true;
