@@ -225,8 +225,9 @@ def cpu_reference(config: str, budget_s: float, trials: int = 9, warm: int = 2,
 
     # settle the host first (pool threads spun up, pages touched, clocks
     # ramped): without it the first run read ~25% below the second
+    settle_s = float(os.environ.get("DCONV_CPU_SETTLE", "1.5"))
     t_settle = time.perf_counter()
-    while time.perf_counter() - t_settle < 1.5:
+    while time.perf_counter() - t_settle < settle_s:
         one()
     run_vals, all_min, samples = [], None, 0
     for _ in range(runs):
