@@ -449,6 +449,8 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
     const int pt = pw * 32 + lane;  // producer thread index
     if (kFfmaProf && p.dbg && pt == 0) p.dbg[blockIdx.x * 16 + 8] = clock64() - t_start;
     int gs = 0;
+    int pbuf = 0;            // ring slot of stage gs (gs % NS)
+    uint32_t pphase = 0u;    // (gs / NS) & 1
     const int seg_rows_full = (p.h_o - 1) * p.sy;  // + Re per full segment
     for (int u = cluster_id; u < n_units; u += n_clusters) {
       TileRows tr;
@@ -473,10 +475,12 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
                              row_bytes);
         }
       }
+      int g = st0 / p.n_r, r = st0 - g * p.n_r;
       for (int st = st0; st < st1; ++st, ++gs) {
-        const int buf = gs % p.NS;
-        if (gs >= p.NS) mbar_wait(&empty[buf], ((gs / p.NS) - 1) & 1);
-        const int g = st / p.n_r, r = st - g * p.n_r;
+        const int buf = pbuf;
+        if (gs >= p.NS) mbar_wait(&empty[buf], pphase ^ 1u);
+        if (++pbuf == p.NS) { pbuf = 0; pphase ^= 1u; }
+        if (st > st0 && ++r == p.n_r) { r = 0; ++g; }
         const int ib0 = g * p.G, Ge = min(p.G, p.ib_n - ib0);
         const int n0 = r * p.R, Re = min(p.R, p.h_f - n0);
         // rows of each segment this stage: (cnt-1)*s + Re
@@ -556,6 +560,8 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
   const int wf = WF > 0 ? WF : p.w_f;
 
   int gs = 0, unit_iter = 0;
+  int rbuf = 0;            // ring slot of stage gs (gs % NS)
+  uint32_t rphase = 0u;    // its full-barrier phase ((gs / NS) & 1)
   for (int u = cluster_id; u < n_units; u += n_clusters, ++unit_iter) {
     TileRows tr;
     int tx0, jb0, cg_valid;
@@ -577,13 +583,18 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
 #pragma unroll
       for (int c = 0; c < TCO / 2; ++c) acc[k][c] = 0ull;
     bool have_total = false;
+    // per-stage bookkeeping by counters, not divisions (scalar work in this
+    // loop showed up in the headline: a modulo per stage cost 1%)
+    int fold_in = p.flush_every;  // stages until the next TMEM fold
+    int g = st0 / p.n_r, r = st0 - g * p.n_r;
 
     for (int st = st0; st < st1; ++st, ++gs) {
-      const int buf = gs % p.NS;
+      const int buf = rbuf;
       if (kFfmaProf && p.dbg && tid == 0 && gs == 0) p.dbg[blockIdx.x * 16 + 10] = clock64() - t_start;
-      mbar_wait(&full[buf], (gs / p.NS) & 1);
+      mbar_wait(&full[buf], rphase);
+      if (++rbuf == p.NS) { rbuf = 0; rphase ^= 1u; }
       if (kFfmaProf && p.dbg && tid == 0 && gs == 0) p.dbg[blockIdx.x * 16 + 2] = clock64() - t_start;
-      const int g = st / p.n_r, r = st - g * p.n_r;
+      if (st > st0 && ++r == p.n_r) { r = 0; ++g; }
       const int Ge = min(p.G, p.ib_n - g * p.G);
       const int Re = min(p.R, p.h_f - r * p.R);
       const float* sp = smem + buf * p.stage_floats;
@@ -667,7 +678,8 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
       if (lane == 0) mbar_arrive(&empty[buf]);
       // fold the partial sum into the TMEM running total every flush_every
       // stages (never after the last stage: the epilogue folds it)
-      if (use_tmem && (st - st0 + 1) % p.flush_every == 0 && st + 1 < st1) {
+      if (use_tmem && --fold_in == 0 && st + 1 < st1) {
+        fold_in = p.flush_every;
         tmem_fold<NP>(taddr, &acc[0][0], have_total, true);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         have_total = true;
