@@ -618,18 +618,25 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
       // bank rows); lanes 4-7 of it take the channel halves in the other order
       // so its 16-byte reads land on 8 distinct bank groups
       const int hswap = CBS == 32 ? (lane & 1) : (PPW == 8 ? ((lane >> 2) & 1) : 0);
-      auto tap = [&](const float* pw, int aoff) {
+      // dense (1x1/s1 tiles no wider than the map): the staged patch is the
+      // tile itself, pixel q at q * CBS floats, so a thread's TPX pixels sit
+      // at compile-time offsets from ONE pointer (pd): no per-pixel address
+      // arithmetic per input block (it cost the 1x1 loop ~8%: ncu source
+      // page, profiles/r2_ncu_src_1x1.txt)
+      const float* pd = sp + pg * CBS;
+      auto tap = [&](const float* pw, int aoff, auto dense) {
 #pragma unroll
         for (int half_i = 0; half_i < 8 / AV; ++half_i) {
           const int half = half_i ^ hswap;
           float a[TPX][AV];
 #pragma unroll
           for (int k = 0; k < TPX; ++k) {
+            const float* pa = decltype(dense)::value ? pd + k * (PG * CBS) : pk[k];
             if constexpr (AV == 4) {
-              const float4 t = lds128(pk[k] + aoff + half * 4);
+              const float4 t = lds128(pa + aoff + half * 4);
               a[k][0] = t.x; a[k][1] = t.y; a[k][2] = t.z; a[k][3] = t.w;
             } else {
-              const float2 t = *reinterpret_cast<const float2*>(pk[k] + aoff + half * 2);
+              const float2 t = *reinterpret_cast<const float2*>(pa + aoff + half * 2);
               a[k][0] = t.x; a[k][1] = t.y;
             }
           }
@@ -657,10 +664,17 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
         // 1x1 filters: a stage is Ge input blocks of one tap each; unrolled
         // so the accumulators stay put across blocks (no register rotation)
         const int gstride = p.PH * p.PW * CBS, wgstride = p.R * CBS * CBS;
+        if (p.dense1x1) {
 #pragma unroll 4
-        for (int gi = 0; gi < Ge * SUB; ++gi)  // 8-channel input sub-blocks
-          tap(sw + (gi / SUB) * wgstride + (gi % SUB) * kCB * CBS,
-              (gi / SUB) * gstride + (gi % SUB) * kCB);
+          for (int gi = 0; gi < Ge * SUB; ++gi)  // 8-channel input sub-blocks
+            tap(sw + (gi / SUB) * wgstride + (gi % SUB) * kCB * CBS,
+                (gi / SUB) * gstride + (gi % SUB) * kCB, std::true_type{});
+        } else {
+#pragma unroll 4
+          for (int gi = 0; gi < Ge * SUB; ++gi)
+            tap(sw + (gi / SUB) * wgstride + (gi % SUB) * kCB * CBS,
+                (gi / SUB) * gstride + (gi % SUB) * kCB, std::false_type{});
+        }
       } else {
         for (int gi = 0; gi < Ge; ++gi) {
 #pragma unroll 1
@@ -669,7 +683,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
               const int row_off = ((gi * p.PH + n) * p.PW) * CBS + sb * kCB;
               const float* pw_row = sw + ((gi * p.R + n) * wf) * (CBS * CBS) + sb * kCB * CBS;
 #pragma unroll(WF > 0 ? WF : 1)
-              for (int m = 0; m < wf; ++m) tap(pw_row + m * (CBS * CBS), row_off + m * CBS);
+              for (int m = 0; m < wf; ++m) tap(pw_row + m * (CBS * CBS), row_off + m * CBS, std::false_type{});
             }
           }
         }
@@ -1074,6 +1088,9 @@ size_t configure(FfmaParams& p, int ks, bool fine) {
       const int per_block = patch1 + CG * p.R * p.w_f * CBS * CBS * 4;
       p.G = std::max(1, std::min(p.G, (36 * 1024) / per_block));
     }
+    // 1x1 layers: the consumers' block loop is unrolled by 4 (its remainder
+    // loop rotates the accumulators through 28 MOVs per block)
+    if (p.h_f * p.w_f == 1 && CBS == 8 && p.G > 4) p.G &= ~3;
     if (knobs().force_g) p.G = std::max(1, std::min(p.ib_n, knobs().force_g));
   } else {
     p.G = 1;
@@ -1104,6 +1121,15 @@ size_t configure(FfmaParams& p, int ks, bool fine) {
   p.flush_every = std::max(1, (256 + k_stage - 1) / k_stage);
   if (knobs().flush_every) p.flush_every = std::max(1, knobs().flush_every);
   if (p.NS < 2) return 0;
+  // 1x1/s1 tiles no wider than the map: the patch is the tile itself (tile
+  // row r = patch row r, PW = TW), so the consumers address a thread's pixels
+  // from one pointer.  Pixels past the tile's last row read on into the
+  // stage (never stored): the stage must hold BM pixels from the last block.
+  constexpr int BM = NW * 32 * TPX * TCO / BN;
+  static const bool no_dense = getenv("DCONV_NO_DENSE1X1") != nullptr;
+  p.dense1x1 = (!no_dense && p.h_f == 1 && p.w_f == 1 && p.s == 1 && p.sy == 1 && p.TWe == p.TW &&
+                p.PW == p.TW &&
+                (p.G - 1) * p.PH * p.PW * CBS + BM * CBS <= p.stage_floats) ? 1 : 0;
   return (size_t)p.NS * p.stage_floats * 4 + (ks > 1 ? red_bytes : 0) + bar_bytes;
 }
 

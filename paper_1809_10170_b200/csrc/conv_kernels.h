@@ -42,6 +42,7 @@ struct FfmaParams {
   int n_peers;
   float* peer_out[kMaxPeers];
   int epi_wg;                  // 1: compute warps hand tiles to the epilogue warpgroup
+  int dense1x1;                // 1: 1x1/s1 stage whose patch is the tile itself (pixel q at q * c_b)
   long long* dbg;              // DCONV_FFMA_PROFILE: per-CTA phase clocks (else null)
 };
 
