@@ -563,12 +563,20 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
   int rbuf = 0;            // ring slot of stage gs (gs % NS)
   uint32_t rphase = 0u;    // its full-barrier phase ((gs / NS) & 1)
   for (int u = cluster_id; u < n_units; u += n_clusters, ++unit_iter) {
-    TileRows tr;
-    int tx0, jb0, cg_valid;
-    decode(u, tr, tx0, jb0, cg_valid);
+    TileRows tr{};
+    int tx0 = 0, jb0 = 0, cg_valid = 0;
+    // dense 1x1 tiles handed to the epilogue warpgroup need no tile geometry
+    // in the compute warps: pixels are addressed from one pointer and the
+    // epilogue warps decode the unit themselves (short-K units: the decode's
+    // divisions were ~10% of a 64-channel unit)
+    const bool geom = !(WF == 1 && p.dense1x1 && p.epi_wg);
+    if (geom) decode(u, tr, tx0, jb0, cg_valid);
     // per-pixel patch offsets of this tile (pixels that do not exist read
     // offset 0 and are never stored)
     int poff[TPX];
+#pragma unroll
+    for (int k = 0; k < TPX; ++k) poff[k] = 0;
+    if (geom && !(WF == 1 && p.dense1x1))  // dense 1x1 tiles address pixels from one pointer
 #pragma unroll
     for (int k = 0; k < TPX; ++k) {
       const int q = pg + PG * k;

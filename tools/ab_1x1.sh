@@ -1,5 +1,5 @@
-# A/B of the dense 1x1 consumer loop on ResNet-50 b256 1x1 layers
-for args in "1024 256 14 14 1 1 256 3 ffma" "256 1024 14 14 1 1 256 3 ffma_add" "256 64 56 56 1 1 256 3 ffma" "64 256 56 56 1 1 256 3 ffma_add" "512 128 28 28 1 1 256 3 ffma" "128 512 28 28 1 1 256 3 ffma_add" "2048 512 7 7 1 1 256 3 ffma" "512 2048 7 7 1 1 256 3 ffma_add"; do
-  echo "dense:   $(python tools/one_layer.py $args)"
-  echo "general: $(DCONV_NO_DENSE1X1=1 python tools/one_layer.py $args)"
+# A/B of the epilogue warpgroup's L2 skip prefetch on ResNet-50 b256 1x1 + skip layers
+for args in "64 256 56 56 1 1 256 3 ffma_add" "128 512 28 28 1 1 256 3 ffma_add" "256 1024 14 14 1 1 256 3 ffma_add" "512 2048 7 7 1 1 256 3 ffma_add" "256 64 56 56 1 1 256 3 ffma" "1024 256 14 14 1 1 256 3 ffma"; do
+  echo "prefetch:    $(python tools/one_layer.py $args)"
+  echo "no prefetch: $(DCONV_NO_EPI_PREFETCH=1 python tools/one_layer.py $args)"
 done

@@ -1,5 +1,5 @@
 set -u
-O=gpurun_out/s5b; mkdir -p $O
+O=gpurun_out/s5c; mkdir -p $O
 full() {
   local name=$1 k=$2; shift 2
   python tools/one_layer.py "$@" > $O/plain_$name.log 2>&1 && \
@@ -9,10 +9,10 @@ full() {
   ncu -i $O/full_$name.ncu-rep --page source --csv > $O/full_$name.src.csv 2>/dev/null
   rm -f $O/full_$name.ncu-rep
 }
-FS=4 full r50_s3c1 conv_ffma 1024 256 14 14 1 1 256 3 ffma
-FS=4 full r50_s3c3 conv_ffma 256 1024 14 14 1 1 256 3 ffma_add
-FS=4 full r50_s3c2 conv_ffma 256 256 16 16 3 1 256 3 ffma
-for g in 3 5 6 8; do echo G=$g; DCONV_FORCE_G=$g python tools/one_layer.py 1024 256 14 14 1 1 256 3 ffma; done
-echo noepi; DCONV_NO_EPI_WG=1 python tools/one_layer.py 1024 256 14 14 1 1 256 3 ffma
-for b in 16 24 32 48; do echo PB=$b; DCONV_PATCH_BUDGET=$b python tools/one_layer.py 1024 256 14 14 1 1 256 3 ffma; done
-DCONV_DEBUG=1 python tools/one_layer.py 1024 256 14 14 1 1 256 1 ffma 2>&1 | tail -3
+export DCONV_NO_TAILSPLIT=1
+FS=4 full r50_s1c3 conv_ffma 64 256 56 56 1 1 256 3 ffma_add
+FS=4 full r50_s2c3 conv_ffma 128 512 28 28 1 1 256 3 ffma_add
+unset DCONV_NO_TAILSPLIT
+DCONV_DEBUG=1 python tools/one_layer.py 64 256 56 56 1 1 256 1 ffma_add 2>&1 | tail -3
+for t in 1 2 3 4 5; do echo TILE=$t; TILE=$t python tools/one_layer.py 64 256 56 56 1 1 256 3 ffma_add; done
+bash tools/ab_1x1.sh
