@@ -287,7 +287,46 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
   const int rank = blockIdx.x % ks;            // == %cluster_ctarank (1-D cluster)
   const int cluster_id = blockIdx.x / ks, n_clusters = gridDim.x / ks;
   const int st0 = rank * S / ks, st1 = (rank + 1) * S / ks;
-  const bool use_tmem = st1 - st0 > p.flush_every;
+  const bool use_tmem = (p.streamk ? S : st1 - st0) > p.flush_every;
+  // Work pieces of this CTA: (unit, [s0, s1) of its S stages).  Default: the
+  // units cluster_id, cluster_id + n_clusters, ... with the rank's stage
+  // range.  Stream-K: a contiguous range of the launch's units x S stages.
+  struct Pieces {
+    int sk, S, n_units, step, u, st0, st1, g, g_end, sk_base;
+    __device__ bool next(int& uu, int& s0, int& s1) {
+      if (sk) {
+        // whole waves first, round-robin like the default (neighbouring CTAs
+        // on neighbouring tiles: contiguous ranges alone cost the memory-heavy
+        // 1x1 + skip layers 4-5%), then the last 1.x waves as stage ranges
+        if (u + step < sk_base) {
+          u += step;
+          uu = u; s0 = 0; s1 = S;
+          return true;
+        }
+        if (g >= g_end) return false;
+        uu = g / S;
+        s0 = g - uu * S;
+        uu += sk_base;
+        s1 = min(S, s0 + (g_end - g));
+        g += s1 - s0;
+        return true;
+      }
+      u += step;
+      if (u >= n_units) return false;
+      uu = u; s0 = st0; s1 = st1;
+      return true;
+    }
+  };
+  auto make_pieces = [&]() {
+    Pieces it;
+    it.sk = p.streamk; it.S = S; it.n_units = n_units; it.step = n_clusters;
+    it.u = cluster_id - n_clusters; it.st0 = st0; it.st1 = st1;
+    it.sk_base = p.sk_base;
+    const long long W = (long long)(n_units - p.sk_base) * S;
+    it.g = (int)(W * blockIdx.x / gridDim.x);
+    it.g_end = (int)(W * (blockIdx.x + 1) / gridDim.x);
+    return it;
+  };
 
   if (tid == 0) {
     for (int i = 0; i < p.NS; ++i) {
@@ -346,8 +385,10 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
       if (p.epi_wg) {
         const uint32_t tmem_base = *tmem_slot;
         const int qd = warp & 3;  // TMEM lane quarter = compute warps qd, qd + 4
-        int unit_iter = 0;
-        for (int u = cluster_id; u < n_units; u += n_clusters, ++unit_iter) {
+        int unit_iter = 0;  // whole units (the ones handed over through TMEM)
+        Pieces pieces = make_pieces();
+        for (int u, ps0, ps1; pieces.next(u, ps0, ps1);) {
+          if (ps0 != 0) continue;  // a stream-K contributor piece is stored raw by the compute warps
           TileRows tr;
           int tx0, jb0, cg_valid;
           decode(u, tr, tx0, jb0, cg_valid);
@@ -427,6 +468,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
           if (lane == 0) mbar_arrive(&res_empty[rb]);
+          ++unit_iter;
         }
       }
     }
@@ -452,7 +494,8 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
     int pbuf = 0;            // ring slot of stage gs (gs % NS)
     uint32_t pphase = 0u;    // (gs / NS) & 1
     const int seg_rows_full = (p.h_o - 1) * p.sy;  // + Re per full segment
-    for (int u = cluster_id; u < n_units; u += n_clusters) {
+    Pieces pieces = make_pieces();
+    for (int u, st0, st1; pieces.next(u, st0, st1);) {  // (shadow the rank's range)
       TileRows tr;
       int tx0, jb0, cg_valid;
       decode(u, tr, tx0, jb0, cg_valid);
@@ -562,14 +605,22 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
   int gs = 0, unit_iter = 0;
   int rbuf = 0;            // ring slot of stage gs (gs % NS)
   uint32_t rphase = 0u;    // its full-barrier phase ((gs / NS) & 1)
-  for (int u = cluster_id; u < n_units; u += n_clusters, ++unit_iter) {
+  int wu_iter = 0;  // units handed to the epilogue warpgroup (all but stream-K contributor pieces)
+  Pieces pieces = make_pieces();
+  for (int u, st0, st1; pieces.next(u, st0, st1); ++unit_iter) {  // (shadow the rank's range)
+    const bool whole = !p.streamk || (st0 == 0 && st1 == S);
+    // stream-K boundary pieces: 1 = later stages of a unit begun by the
+    // previous CTA (store the raw partial tile into the output map, raise
+    // this CTA's flag), 2 = first stages of a unit continued by the next CTA
+    // (wait for its flag, add its partial, run the epilogue)
+    const int sk_mode = whole ? 0 : (st0 > 0 ? 1 : 2);
     TileRows tr{};
     int tx0 = 0, jb0 = 0, cg_valid = 0;
     // dense 1x1 tiles handed to the epilogue warpgroup need no tile geometry
     // in the compute warps: pixels are addressed from one pointer and the
     // epilogue warps decode the unit themselves (short-K units: the decode's
     // divisions were ~10% of a 64-channel unit)
-    const bool geom = !(WF == 1 && p.dense1x1 && p.epi_wg);
+    const bool geom = !(WF == 1 && p.dense1x1 && p.epi_wg && whole);
     if (geom) decode(u, tr, tx0, jb0, cg_valid);
     // per-pixel patch offsets of this tile (pixels that do not exist read
     // offset 0 and are never stored)
@@ -712,11 +763,59 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
       }
     }
     if (kFfmaProf && p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 3] = clock64() - t_start;  // loop end
-    if (p.epi_wg) {
+    if (sk_mode == 2) {
+      // stream-K finisher: the next CTA stored this unit's later-stage
+      // partial tile into the output map first thing; add it to the
+      // registers (first stages + later stages, in that order) and go on as
+      // for a whole unit.  The flag is cleared for the next launch.
+      if (tid == 0) {
+        unsigned f;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(p.sk_flags + blockIdx.x + 1) : "memory");
+        } while (f == 0u);
+        asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p.sk_flags + blockIdx.x + 1), "r"(0u) : "memory");
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+#pragma unroll
+      for (int bb = 0; bb < NBLK; ++bb) {
+        if (cb + bb >= cg_valid) continue;
+        const int jl = jb0 + cb + bb - p.jb_begin;
+#pragma unroll
+        for (int k4 = 0; k4 < TPX; k4 += 4) {
+          float4 t[8];
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const int q = pg + PG * (k4 + kk);
+            const int ty = (int)__umulhi((unsigned)q, p.tw_magic), tx = q - ty * p.TW;
+            const int x = tx0 + tx;
+            t[2 * kk] = t[2 * kk + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (ty < tr.th && x < p.w_o) {
+              int img, y, prow;
+              tile_row(p, tr, ty, img, y, prow);
+              const float4* o = reinterpret_cast<const float4*>(
+                  p.out + sub_off<CBS>(jl, p.out_blk) + (int64_t)img * p.out_img +
+                  (int64_t)y * p.out_row + (int64_t)x * CBS);
+              t[2 * kk] = __ldcg(o);
+              t[2 * kk + 1] = __ldcg(o + 1);
+            }
+          }
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            uint64_t* a = acc[k4 + kk] + bb * 4;
+            a[0] = fadd2(a[0], pack2(t[2 * kk].x, t[2 * kk].y));
+            a[1] = fadd2(a[1], pack2(t[2 * kk].z, t[2 * kk].w));
+            a[2] = fadd2(a[2], pack2(t[2 * kk + 1].x, t[2 * kk + 1].y));
+            a[3] = fadd2(a[3], pack2(t[2 * kk + 1].z, t[2 * kk + 1].w));
+          }
+        }
+      }
+    }
+    if (p.epi_wg && sk_mode != 1) {
       // hand the finished tile to the epilogue warpgroup (TMEM result buffer
-      // unit_iter & 1) and go on with the next unit
-      const int rb = unit_iter & 1;
-      if (unit_iter >= 2) mbar_wait(&res_empty[rb], ((unit_iter >> 1) - 1) & 1);
+      // wu_iter & 1) and go on with the next unit
+      const int rb = wu_iter & 1;
+      if (wu_iter >= 2) mbar_wait(&res_empty[rb], ((wu_iter >> 1) - 1) & 1);
+      ++wu_iter;
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       tmem_finalize<NP>(taddr, taddr + (uint32_t)(kResCols * (1 + rb)), &acc[0][0], have_total);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -740,6 +839,14 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
       if (ty >= tr.th || x >= p.w_o) return;
       int img, y, prow;
       tile_row(p, tr, ty, img, y, prow);
+      float* o = p.out + sub_off<CBS>(jl, p.out_blk) + (int64_t)img * p.out_img +
+                 (int64_t)y * p.out_row + (int64_t)x * CBS;
+      if (sk_mode == 1) {  // raw partial tile, finished by the previous CTA
+#pragma unroll
+        for (int c = 0; c < 8; c += 4)
+          __stcg(reinterpret_cast<float4*>(o + c), make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]));
+        return;
+      }
       if (p.epi & DCONV_EPI_ADD) {
         const float* sk = p.skip + sub_off<CBS>(jl, p.sk_blk) + (int64_t)img * p.sk_img +
                           (int64_t)y * p.sk_row + (int64_t)x * CBS;
@@ -753,8 +860,6 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
 #pragma unroll
         for (int c = 0; c < 8; ++c) v[c] = fmaxf(v[c], 0.f);
       }
-      float* o = p.out + sub_off<CBS>(jl, p.out_blk) + (int64_t)img * p.out_img +
-                 (int64_t)y * p.out_row + (int64_t)x * CBS;
       DCONV_OWN(o, 8);
 #pragma unroll
       for (int c = 0; c < 8; c += 4)
@@ -908,6 +1013,13 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
           emit(k, jl, v);
         }
       }
+      if (sk_mode == 1) {
+        // partial tile stored: publish it to the finishing CTA
+        __threadfence();
+        asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+        if (tid == 0)
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.sk_flags + blockIdx.x), "r"(1u) : "memory");
+      }
     }
   }
   // (push model: every remote access to this CTA's smem -- the peers'
@@ -976,6 +1088,9 @@ double tail_rounds(int64_t units, int sms) {
     else if (tail * 4 <= sms) t = 0.25 + 0.05;
     else if (tail * 2 <= sms) t = 0.5 + 0.05;
     else t = 1.0;
+    // stream-K balances a ragged tail over all SMs (stage granularity and
+    // the boundary pieces cost ~0.1 of a unit)
+    if (full > 0) t = std::min(t, (double)tail / sms + 0.1);
   }
   return (double)full + t;
 }
@@ -1271,6 +1386,38 @@ int launch_units(K kernel, int threads, FfmaParams p, size_t smem, int unit_begi
   return dconv_host::check_launch("conv_ffma_kernel");
 }
 
+// Stream-K flags: one self-resetting flag per CTA, in a slot owned by the
+// launching stream (launches of one stream never overlap; up to kSkSlots
+// streams per device, later ones run without stream-K).  Module-resident:
+// nothing is allocated.
+constexpr int kSkSlots = 32, kSkFlagsPerSlot = 160;
+__device__ unsigned g_sk_flags[kSkSlots * kSkFlagsPerSlot];
+
+unsigned* sk_flags_for(cudaStream_t stream, int dev) {
+  struct Dev {
+    unsigned* base = nullptr;
+    bool tried = false;
+    std::vector<cudaStream_t> streams;
+  };
+  static std::mutex mu;
+  static std::vector<Dev> devs;
+  std::lock_guard<std::mutex> lock(mu);
+  if ((int)devs.size() <= dev) devs.resize(dev + 1);
+  Dev& d = devs[dev];
+  if (!d.tried) {
+    d.tried = true;
+    void* sym = nullptr;
+    if (cudaGetSymbolAddress(&sym, g_sk_flags) == cudaSuccess) d.base = static_cast<unsigned*>(sym);
+    else cudaGetLastError();
+  }
+  if (!d.base) return nullptr;
+  for (size_t i = 0; i < d.streams.size(); ++i)
+    if (d.streams[i] == stream) return d.base + i * kSkFlagsPerSlot;
+  if ((int)d.streams.size() >= kSkSlots) return nullptr;
+  d.streams.push_back(stream);
+  return d.base + (d.streams.size() - 1) * kSkFlagsPerSlot;
+}
+
 template <int BM, int BN, int WF, int NW, int TPX, int TCO, int CBS>
 int launch_variant(FfmaParams p, cudaStream_t stream) {
   constexpr int threads = (NW + 8) * 32;
@@ -1333,6 +1480,42 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   // of the SMs) runs as a second launch whose units are split over clusters,
   // so the SMs that would idle help finish the tail.
   const int main_units = units / sms * sms, tail = units - main_units;
+  // Stream-K: ragged unit counts (1.3 or 2.65 waves) run as ONE launch whose
+  // CTAs each take units * S / sms stages; the <= 2 cut units per CTA are
+  // finished through the output map (see FfmaParams::streamk).  Needs whole-K
+  // units with a stage count to cut, the plain epilogue, and an output that
+  // is not also the skip input (the partial tile passes through it).
+  static const bool no_streamk = getenv("DCONV_NO_STREAMK") != nullptr;
+  // worth it when the waves + split tail estimate is > 1% over units / sms
+  double est_tail = 1.0;
+  if (!no_split && tail * 4 < sms * 3)
+    for (int ks = kMaxKs; ks >= 2; --ks)
+      if (ks <= S && slots[ks] >= tail) {
+        est_tail = 1.0 / ks + 0.08;
+        break;
+      }
+  static const bool sk_always = getenv("DCONV_STREAMK_ALWAYS") != nullptr;
+  // stream-K estimate: the whole waves but one, then (sms + tail) units cut
+  // at stage granularity, + the boundary pieces' partial store / load
+  const int sk_rr = (units / sms - 1) * sms;
+  const double t_sk = (units / sms - 1) +
+                      (double)(((int64_t)(units - sk_rr) * S + sms - 1) / sms) / S + 0.03;
+  const bool sk_pays = sk_always || t_sk < 0.985 * (units / sms + est_tail);
+  if (!no_streamk && sk_pays && main_units > 0 && tail > 0 && S >= 4 && sms + 1 < kSkFlagsPerSlot &&
+      !(p.epi & DCONV_EPI_MAXPOOL) && p.skip != p.out && (int64_t)units * S < (1 << 30)) {
+    if (unsigned* flags = sk_flags_for(stream, dev)) {
+      const size_t smem_sk = configure<BN, NW, TPX, TCO, CBS>(q, 1, fine);
+      q.streamk = 1;
+      q.sk_flags = flags;
+      static const bool sk_contig = getenv("DCONV_STREAMK_CONTIGUOUS") != nullptr;
+      q.sk_base = sk_contig ? 0 : (units / sms - 1) * sms;
+      if (knobs().debug)
+        fprintf(stderr, "conv_ffma<%d,%d,%d>: stream-K TH=%d TW=%d units=%d S=%d G=%d R=%d NS=%d "
+                "(%.2f waves)\n", BM, BN, WF, q.TH, q.TW, units, S, q.G, q.R, q.NS,
+                (double)units / sms);
+      return launch_units(kernel, threads, q, smem_sk, 0, units, sms, stream);
+    }
+  }
   int tail_ks = 1;
   if (main_units > 0 && tail > 0 && tail * 4 < sms * 3 && !no_split &&
       !knobs().no_tailsplit) {

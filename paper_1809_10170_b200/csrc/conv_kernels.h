@@ -42,6 +42,14 @@ struct FfmaParams {
   int n_peers;
   float* peer_out[kMaxPeers];
   int epi_wg;                  // 1: compute warps hand tiles to the epilogue warpgroup
+  // stream-K (whole-K launches whose units do not fill whole waves): CTA b
+  // runs stages [b*W/P, (b+1)*W/P) of the launch's units x S stages; a unit
+  // cut by a range boundary is finished by the CTA holding its first stages,
+  // which adds the partial tile the next CTA left in the output map itself
+  // (flag sk_flags[b + 1]); no workspace
+  int streamk;
+  int sk_base;                 // units [0, sk_base) run whole, round-robin, before the stream-K range
+  unsigned* sk_flags;          // one flag per CTA (device-resident, self-resetting)
   int dense1x1;                // 1: 1x1/s1 stage whose patch is the tile itself (pixel q at q * c_b)
   long long* dbg;              // DCONV_FFMA_PROFILE: per-CTA phase clocks (else null)
 };

@@ -846,6 +846,56 @@ def test_tail_split_launch():
             assert_tol(got[i, :, r], want[:, r], f"img {i} row {r}")
 
 
+@pytest.mark.parametrize("ci,co,hi,f,n,epi", [
+    (64, 128, 58, 3, 16, 0),                               # 392 units: 2.65 waves, plain
+    (128, 192, 30, 3, 24, _abi.EPI_RELU),                  # ragged C_o group, ReLU
+    (256, 256, 16, 1, 96, _abi.EPI_ADD | _abi.EPI_RELU),   # dense 1x1 + skip-add (epilogue warpgroup)
+    (512, 512, 16, 3, 32, _abi.EPI_ADD),                   # 14x14 maps across images, 1.35 waves
+])
+def test_stream_k_launch(ci, co, hi, f, n, epi):
+    """Ragged unit counts (1.x / 2.65 waves of 148 SMs) run as one stream-K
+    launch: whole waves round-robin, then the last 1.x waves cut at stage
+    granularity, the cut units finished through the output map.  Every
+    element against the fp64 GPU referee at the fp32 tolerance; a second
+    launch (flags self-reset) and a launch on another stream (its own flag
+    slot) are bitwise equal to the first."""
+    from oracle import gpu_oracle as go
+    l = nets.Layer("sk", ci, co, hi, hi, f, f, 1)
+    wd = torch.empty((ci, co, f, f), device="cuda").uniform_(-1, 1)
+    a = nets.Act(n, ci, hi, hi)
+    a.buf.uniform_(-1, 1)
+    sk = None
+    if epi & _abi.EPI_ADD:
+        sk = nets.Act(n, co, l.h_o, l.w_o)
+        sk.buf.uniform_(-1, 1)
+    w = nets.pack_weights(wd, False)
+    y = nets.Act(n, co, l.h_o, l.w_o)
+    launches = _abi.lib().dconv_cuda_launch_count()
+    nets.conv(l, n, a, w, y, epi, sk)
+    torch.cuda.synchronize()
+    # one launch: not the full waves + split-K tail pair
+    assert _abi.lib().dconv_cuda_launch_count() - launches == 1
+    want = go.conv64_act(a, l, wd)
+    if sk is not None:
+        want = want + sk.buf.double()
+    if epi & _abi.EPI_RELU:
+        want = want.clamp_min(0.0)
+    ok, nbad, err, ratio = go.check_tol(y.buf, want)
+    assert ok, f"{nbad} elements out of tolerance, max err {err}"
+    first = y.buf.clone()
+    y.buf.fill_(float("nan"))
+    nets.conv(l, n, a, w, y, epi, sk)
+    torch.cuda.synchronize()
+    assert torch.equal(y.buf, first), "second launch differs (flag not reset?)"
+    side = torch.cuda.Stream()
+    y.buf.fill_(float("nan"))
+    torch.cuda.synchronize()
+    with torch.cuda.stream(side):
+        nets.conv(l, n, a, w, y, epi, sk, stream=side)
+    side.synchronize()
+    assert torch.equal(y.buf, first), "launch on a second stream differs"
+
+
 def test_autotuned_plan_matches_default_tiles():
     """Per-layer tile autotune changes only the CTA tiling: every layer output
     stays within tolerance of the default-tile run (tile choices differ in
