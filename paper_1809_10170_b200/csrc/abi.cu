@@ -19,6 +19,7 @@ std::atomic<int64_t> g_launches{0};
 
 inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
+bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 0; }
 bool aligned16(const void* p) {
   return (reinterpret_cast<uintptr_t>(p) & 15) == 0;
 }
@@ -221,19 +222,24 @@ int conv_direct_impl(const dconv_conv_desc* d, const float* in, const float* w,
   Resolved r;
   int rc = resolve(d, false, 0, in, w, skip, out, &r);
   if (rc) return rc;
+  // input / weight rows move by 16-byte bulk copies; output and skip pencils
+  // (8 channels = 32 bytes = one sector) by one 256-bit access per lane
+  bool peers32 = true;
+  for (int i = 0; i < n_peers; ++i) peers32 = peers32 && aligned32(peers[i]);
   const bool ffma_ok =
       d->c_ib == d->c_ob && (d->c_ib == 8 || d->c_ib == 16 || d->c_ib == 32) &&
       aligned16(in) && aligned16(w) &&
-      aligned16(out) && (!skip || aligned16(skip)) &&
-      ((r.in_img | r.in_blk | r.in_row | r.out_img | r.out_blk | r.out_row |
-        r.sk_img | r.sk_blk | r.sk_row) & 3) == 0;
+      aligned32(out) && (!skip || aligned32(skip)) && peers32 &&
+      ((r.in_img | r.in_blk | r.in_row) & 3) == 0 &&
+      ((r.out_img | r.out_blk | r.out_row | r.sk_img | r.sk_blk | r.sk_row) & 7) == 0;
   int algo = d->algo;
   if (algo == DCONV_ALGO_AUTO) algo = ffma_ok ? DCONV_ALGO_FFMA : DCONV_ALGO_GENERIC;
   if (algo == DCONV_ALGO_FFMA) {
     if (!ffma_ok)
       return set_error(DCONV_EUNSUPPORTED,
-                       "FFMA kernel needs c_ib == c_ob in {8, 16, 32} and 16-byte "
-                       "aligned views (got c_ib=%d c_ob=%d)", d->c_ib, d->c_ob);
+                       "FFMA kernel needs c_ib == c_ob in {8, 16, 32}, 16-byte aligned "
+                       "input / weights and pencil-aligned (32-byte) output / skip views "
+                       "(got c_ib=%d c_ob=%d)", d->c_ib, d->c_ob);
     dconv_dev::FfmaParams p{};
     p.in = in; p.w = w; p.skip = skip; p.out = out;
     p.n = d->n; p.h_i = d->h_i; p.w_i = d->w_i; p.h_o = d->h_o; p.w_o = d->w_o;

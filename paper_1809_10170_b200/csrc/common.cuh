@@ -199,6 +199,21 @@ __device__ __forceinline__ float4 lds128(const float* p) {
   return *reinterpret_cast<const float4*>(p);
 }
 
+// One 8-channel pencil (32 bytes = one DRAM / L2 sector) from / to global
+// memory in a single 256-bit access per lane (sm_100 LDG.256 / STG.256); two
+// 128-bit halves would touch every sector twice, half a sector each time.
+// The pencil must be 32-byte aligned (abi.cu checks the views).
+__device__ __forceinline__ void ldg_pencil(const float* p, float4& a, float4& b) {
+  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+      : "l"(p));
+}
+__device__ __forceinline__ void stg_pencil(float* p, const float (&v)[8]) {
+  asm volatile("st.global.v8.f32 [%8], {%0, %1, %2, %3, %4, %5, %6, %7};" ::"f"(v[0]), "f"(v[1]),
+               "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "l"(p)
+               : "memory");
+}
+
 // Write-ownership debug build (make own -> libdconv_b200_own.so, compiled
 // with -DDCONV_DEBUG_OWNERSHIP -rdc=true): every store of a conv output
 // element also counts itself in a map set by dconv_debug_set_ownership, so a

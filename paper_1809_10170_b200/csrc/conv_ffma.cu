@@ -427,8 +427,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
                   const float4* sk = reinterpret_cast<const float4*>(
                       p.skip + sub_off<CBS>(jl, p.sk_blk) + (int64_t)img * p.sk_img +
                       (int64_t)y * p.sk_row + (int64_t)x * CBS);
-                  sk4[2 * kk] = __ldg(sk);
-                  sk4[2 * kk + 1] = __ldg(sk + 1);
+                  ldg_pencil(reinterpret_cast<const float*>(sk), sk4[2 * kk], sk4[2 * kk + 1]);
                 }
               }
 #pragma unroll
@@ -454,13 +453,8 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
                   }
                   float* dst = p.out + ooff[kk];
                   DCONV_OWN(dst, 8);
-                  *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
-                  *reinterpret_cast<float4*>(dst + 4) = make_float4(o[4], o[5], o[6], o[7]);
-                  for (int pi = 0; pi < p.n_peers; ++pi) {
-                    float* pd = p.peer_out[pi] + ooff[kk];
-                    *reinterpret_cast<float4*>(pd) = make_float4(o[0], o[1], o[2], o[3]);
-                    *reinterpret_cast<float4*>(pd + 4) = make_float4(o[4], o[5], o[6], o[7]);
-                  }
+                  stg_pencil(dst, o);
+                  for (int pi = 0; pi < p.n_peers; ++pi) stg_pencil(p.peer_out[pi] + ooff[kk], o);
                 }
               }
             }
@@ -850,27 +844,19 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
       if (p.epi & DCONV_EPI_ADD) {
         const float* sk = p.skip + sub_off<CBS>(jl, p.sk_blk) + (int64_t)img * p.sk_img +
                           (int64_t)y * p.sk_row + (int64_t)x * CBS;
-#pragma unroll
-        for (int c = 0; c < 8; c += 4) {
-          const float4 s4 = *reinterpret_cast<const float4*>(sk + c);
-          v[c] += s4.x; v[c + 1] += s4.y; v[c + 2] += s4.z; v[c + 3] += s4.w;
-        }
+        float4 s0, s1;
+        ldg_pencil(sk, s0, s1);
+        v[0] += s0.x; v[1] += s0.y; v[2] += s0.z; v[3] += s0.w;
+        v[4] += s1.x; v[5] += s1.y; v[6] += s1.z; v[7] += s1.w;
       }
       if (p.epi & DCONV_EPI_RELU) {
 #pragma unroll
         for (int c = 0; c < 8; ++c) v[c] = fmaxf(v[c], 0.f);
       }
       DCONV_OWN(o, 8);
-#pragma unroll
-      for (int c = 0; c < 8; c += 4)
-        *reinterpret_cast<float4*>(o + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+      stg_pencil(o, v);
       // fused C_o-shard gather: the same pencil into every peer's map
-      for (int pi = 0; pi < p.n_peers; ++pi) {
-        float* po = p.peer_out[pi] + (o - p.out);
-#pragma unroll
-        for (int c = 0; c < 8; c += 4)
-          *reinterpret_cast<float4*>(po + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
-      }
+      for (int pi = 0; pi < p.n_peers; ++pi) stg_pencil(p.peer_out[pi] + (o - p.out), v);
     };
 
     if (TCO == 8 && ks > 1) {
