@@ -385,6 +385,8 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
       if (p.epi_wg) {
         const uint32_t tmem_base = *tmem_slot;
         const int qd = warp & 3;  // TMEM lane quarter = compute warps qd, qd + 4
+        // a lane's consecutive pixels are PG apart in the tile: PG / TW rows, PG % TW columns
+        const int e_dty = (int)__umulhi((unsigned)PG, p.tw_magic), e_dtx = PG - e_dty * p.TW;
         int unit_iter = 0;  // whole units (the ones handed over through TMEM)
         Pieces pieces = make_pieces();
         for (int u, ps0, ps1; pieces.next(u, ps0, ps1);) {
@@ -403,31 +405,49 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
             const int jl = jb0 + cb - p.jb_begin;
             const uint32_t tr_addr = tmem_base + ((uint32_t)(qd * 32) << 16) +
                                      (uint32_t)(kResCols * (1 + rb) + half * TPX * TCO);
-            // 4 pixels at a time: their output offsets and skip pencils first
-            // (8 loads in flight per thread), then the TMEM chunks are read
-            // and stored.  Every lane runs the tcgen05.ld (warp-collective);
-            // blocks past cg_valid only skip their stores.
+            // Every lane runs the tcgen05.ld (warp-collective); blocks past
+            // cg_valid only skip their stores.
             const bool blk_ok = cb < cg_valid;
+            // This lane's pixels are q = pg + PG * k: tile coordinates and
+            // the output / skip offsets advance by a fixed step (dty rows,
+            // dtx columns, a carry when the column wraps), so only pixel 0
+            // pays the divisions and 64-bit multiplies (the epilogue warps
+            // were instruction-bound on short-K 1x1 layers: ~100
+            // instructions per pixel, ncu source page).  Tile row ty is
+            // row vy0 + ty of the batch-stacked output.
+            int ty = (int)__umulhi((unsigned)pg, p.tw_magic), tx = pg - ty * p.TW;
+            int img = div_ho(p, tr.vy0 + ty), y = tr.vy0 + ty - img * p.h_o;
+            int64_t o_off = sub_off<CBS>(jl, p.out_blk) + (int64_t)img * p.out_img +
+                            (int64_t)y * p.out_row + (int64_t)(tx0 + tx) * CBS;
+            int64_t s_off = 0;
+            if (p.epi & DCONV_EPI_ADD)
+              s_off = sub_off<CBS>(jl, p.sk_blk) + (int64_t)img * p.sk_img +
+                      (int64_t)y * p.sk_row + (int64_t)(tx0 + tx) * CBS;
+            // 4 pixels at a time: their skip pencils first (4 256-bit loads
+            // in flight per thread), then the TMEM chunks are read and stored.
 #pragma unroll 1
             for (int k4 = 0; k4 < TPX; k4 += 4) {
               int64_t ooff[4];
               float4 sk4[8];
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk) {
-                const int q = pg + PG * (k4 + kk);
-                const int ty = (int)__umulhi((unsigned)q, p.tw_magic), tx = q - ty * p.TW;
-                const int x = tx0 + tx;
-                const bool ok = blk_ok && ty < tr.th && x < p.w_o;
-                int img = 0, y = 0, prow;
-                if (ok) tile_row(p, tr, ty, img, y, prow);
-                ooff[kk] = ok ? sub_off<CBS>(jl, p.out_blk) + (int64_t)img * p.out_img +
-                                    (int64_t)y * p.out_row + (int64_t)x * CBS
-                              : -1;
-                if ((p.epi & DCONV_EPI_ADD) && ok) {
-                  const float4* sk = reinterpret_cast<const float4*>(
-                      p.skip + sub_off<CBS>(jl, p.sk_blk) + (int64_t)img * p.sk_img +
-                      (int64_t)y * p.sk_row + (int64_t)x * CBS);
-                  ldg_pencil(reinterpret_cast<const float*>(sk), sk4[2 * kk], sk4[2 * kk + 1]);
+                const bool ok = blk_ok && ty < tr.th && tx0 + tx < p.w_o;
+                ooff[kk] = ok ? o_off : -1;
+                if ((p.epi & DCONV_EPI_ADD) && ok)
+                  ldg_pencil(p.skip + s_off, sk4[2 * kk], sk4[2 * kk + 1]);
+                // next pixel of this lane
+                int dy = e_dty;
+                tx += e_dtx;
+                int dx = e_dtx;
+                if (tx >= p.TW) { tx -= p.TW; dx -= p.TW; ++dy; }
+                ty += dy;
+                y += dy;
+                o_off += (int64_t)dy * p.out_row + dx * CBS;
+                s_off += (int64_t)dy * p.sk_row + dx * CBS;
+                while (y >= p.h_o) {  // into the next image of the stack
+                  y -= p.h_o;
+                  o_off += p.out_img - (int64_t)p.h_o * p.out_row;
+                  s_off += p.sk_img - (int64_t)p.h_o * p.sk_row;
                 }
               }
 #pragma unroll
