@@ -334,10 +334,12 @@ int conv_tf32_impl(const dconv_conv_desc* d, const float* in, const float* w_pre
   int rc = resolve(d, false, 0, in, w_prepared, skip, out, &r);
   if (rc) return rc;
   if (d->c_ib != 8 || d->c_ob != 8 || !aligned16(in) || !aligned16(w_prepared) ||
-      !aligned16(out) || (skip && !aligned16(skip)) ||
-      ((r.in_img | r.in_blk | r.in_row | r.out_img | r.out_blk | r.out_row | r.sk_img |
-        r.sk_blk | r.sk_row) & 3) != 0)
-    return set_error(DCONV_EUNSUPPORTED, "TF32 path needs c_ib == c_ob == 8, aligned views");
+      !aligned32(out) || (skip && !aligned32(skip)) ||
+      ((r.in_img | r.in_blk | r.in_row) & 3) != 0 ||
+      ((r.out_img | r.out_blk | r.out_row | r.sk_img | r.sk_blk | r.sk_row) & 7) != 0)
+    return set_error(DCONV_EUNSUPPORTED,
+                     "TF32 path needs c_ib == c_ob == 8, 16-byte aligned input and "
+                     "pencil-aligned (32-byte) output / skip views");
   dconv_dev::FfmaParams p{};
   p.in = in; p.w = nullptr; p.skip = skip; p.out = out;
   p.n = d->n; p.h_i = d->h_i; p.w_i = d->w_i; p.h_o = d->h_o; p.w_o = d->w_o;

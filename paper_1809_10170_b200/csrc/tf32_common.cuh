@@ -172,10 +172,8 @@ __device__ __forceinline__ void emit32(const Tf32Params& p, float (&v)[32], int 
       if (jb >= p.jb_count) break;
       float* o = p.out + (int64_t)img * p.out_img + (int64_t)jb * p.out_blk +
                  (int64_t)(y >> 1) * p.out_row + (int64_t)(x >> 1) * 8;
-      const float* vv = v + b * 8;
       DCONV_OWN(o, 8);
-      *reinterpret_cast<float4*>(o) = make_float4(vv[0], vv[1], vv[2], vv[3]);
-      *reinterpret_cast<float4*>(o + 4) = make_float4(vv[4], vv[5], vv[6], vv[7]);
+      stg_pencil(o, *reinterpret_cast<const float(*)[8]>(v + b * 8));
     }
     return;
   }
@@ -187,11 +185,11 @@ __device__ __forceinline__ void emit32(const Tf32Params& p, float (&v)[32], int 
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int jb = min(cg * (p.N / 8) + (c0 / 8) + b, p.jb_count - 1);
-      const float4* sk = reinterpret_cast<const float4*>(
-          p.skip + (int64_t)img * p.sk_img + (int64_t)jb * p.sk_blk + (int64_t)y * p.sk_row +
-          (int64_t)x * 8);
-      s4[2 * b] = __ldg(sk);
-      s4[2 * b + 1] = __ldg(sk + 1);
+      // one 256-bit load per pencil (a warp's lanes are 32 adjacent pixels:
+      // 1 KB contiguous per instruction)
+      ldg_pencil(p.skip + (int64_t)img * p.sk_img + (int64_t)jb * p.sk_blk + (int64_t)y * p.sk_row +
+                     (int64_t)x * 8,
+                 s4[2 * b], s4[2 * b + 1]);
     }
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
@@ -213,8 +211,7 @@ __device__ __forceinline__ void emit32(const Tf32Params& p, float (&v)[32], int 
       for (int i = 0; i < 8; ++i) vv[i] = fmaxf(vv[i], 0.f);
     }
     DCONV_OWN(o, 8);
-    *reinterpret_cast<float4*>(o) = make_float4(vv[0], vv[1], vv[2], vv[3]);
-    *reinterpret_cast<float4*>(o + 4) = make_float4(vv[4], vv[5], vv[6], vv[7]);
+    stg_pencil(o, *reinterpret_cast<const float(*)[8]>(vv));
   }
 }
 
