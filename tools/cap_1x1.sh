@@ -1,5 +1,5 @@
 set -u
-O=gpurun_out/s5c; mkdir -p $O
+O=gpurun_out/s7; mkdir -p $O
 full() {
   local name=$1 k=$2; shift 2
   python tools/one_layer.py "$@" > $O/plain_$name.log 2>&1 && \
@@ -11,8 +11,3 @@ full() {
 }
 export DCONV_NO_TAILSPLIT=1
 FS=4 full r50_s1c3 conv_ffma 64 256 56 56 1 1 256 3 ffma_add
-FS=4 full r50_s2c3 conv_ffma 128 512 28 28 1 1 256 3 ffma_add
-unset DCONV_NO_TAILSPLIT
-DCONV_DEBUG=1 python tools/one_layer.py 64 256 56 56 1 1 256 1 ffma_add 2>&1 | tail -3
-for t in 1 2 3 4 5; do echo TILE=$t; TILE=$t python tools/one_layer.py 64 256 56 56 1 1 256 3 ffma_add; done
-bash tools/ab_1x1.sh

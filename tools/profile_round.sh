@@ -26,6 +26,13 @@ $T python bench.py --impl reference > $O/bench_reference.log 2>&1
 $T python bench.py --config resnet50 --shard co --no-cpu-baseline > $O/bench_resnet50_co_nccl.log 2>&1
 $T python bench.py --config resnet50 --shard co --gather peer --no-cpu-baseline > $O/bench_resnet50_co_peer.log 2>&1
 
+# per-rank workloads of the batch-sharded configs at 2 / 4 / 8 ranks (no
+# collective on that path: N ranks run N of these side by side), and the
+# stream-K / split-tail A/B of the headline
+for b in 16 8 4; do $T python bench.py --batch $b --extra none --no-cpu-baseline > $O/scale_vgg16_b$b.log 2>&1; done
+for b in 128 64 32; do $T python bench.py --config resnet50 --batch $b --extra none --no-cpu-baseline > $O/scale_resnet50_b$b.log 2>&1; done
+for c in vgg16 resnet50; do DCONV_NO_STREAMK=1 $T python bench.py --config $c --extra none --no-cpu-baseline > $O/nostreamk_$c.log 2>&1; done
+
 L="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-tune --extra none"
 $L > $O/plain_launches.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
   --log-file $O/launches_vgg16.csv $L > $O/ncu_launches.log 2>&1
