@@ -127,7 +127,20 @@ int64_t dconv_conv_flops(int c_i, int c_o, int h_o, int w_o, int h_f, int w_f);
  * skip: blocked map like the output, read when epilogue has ADD (else NULL)
  * out:  blocked output view, c_b == d->c_ob.  Every valid element of the
  *       selected output blocks is written exactly once (no zero-init pass);
- *       padded channel slots are written as exact 0. */
+ *       padded channel slots are written as exact 0.
+ * Alignment (FFMA and tensor-core kernels): `in` and `w` 16 bytes with view
+ * strides that are multiples of 4 floats (bulk copies); `out` and `skip`
+ * pencil-aligned -- 32 bytes, view strides multiples of 8 floats -- because a
+ * pencil moves as one 256-bit access.  cudaMalloc / torch allocations and any
+ * pencil offset into them qualify.  Other views run on the generic kernel
+ * (DCONV_ALGO_AUTO) or return DCONV_EUNSUPPORTED (DCONV_ALGO_FFMA).
+ * Stream-K (layers whose tile count does not fill whole waves of SMs): while
+ * the launch runs, `out` also carries partial tiles, so `out` must not alias
+ * `skip` for such a launch to use it (aliasing launches keep the split-K
+ * tail); its per-stream flags live in the module, nothing is allocated.
+ * Launches of ONE stream never overlap, which the flags rely on: a CUDA
+ * graph captured from stream A must not be replayed concurrently with itself
+ * or with other work captured from / launched on stream A. */
 int dconv_cuda_conv_direct(const dconv_conv_desc* d, const float* in,
                            const float* w, const float* skip, float* out,
                            void* stream);

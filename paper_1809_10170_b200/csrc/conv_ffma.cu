@@ -1497,7 +1497,7 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   if (!no_split && tail * 4 < sms * 3)
     for (int ks = kMaxKs; ks >= 2; --ks)
       if (ks <= S && slots[ks] >= tail) {
-        est_tail = 1.0 / ks + 0.08;
+        est_tail = 1.0 / ks + 0.12;  // cluster launches of 3 / 5 / 6 CTAs run erratically (+-3%)
         break;
       }
   static const bool sk_always = getenv("DCONV_STREAMK_ALWAYS") != nullptr;
@@ -1506,7 +1506,10 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   const int sk_rr = (units / sms - 1) * sms;
   const double t_sk = (units / sms - 1) +
                       (double)(((int64_t)(units - sk_rr) * S + sms - 1) / sms) / S + 0.03;
-  const bool sk_pays = sk_always || t_sk < 0.985 * (units / sms + est_tail);
+  // (short-K skip-add layers lose more at the cut units than the model says:
+  // 256->1024 + skip at 14x14 b256, S = 4: -1.5%)
+  const bool sk_pays = sk_always || (t_sk < units / sms + est_tail &&
+                                     !((p.epi & DCONV_EPI_ADD) && S < 8));
   if (!no_streamk && sk_pays && main_units > 0 && tail > 0 && S >= 4 && sms + 1 < kSkFlagsPerSlot &&
       !(p.epi & DCONV_EPI_MAXPOOL) && p.skip != p.out && (int64_t)units * S < (1 << 30)) {
     if (unsigned* flags = sk_flags_for(stream, dev)) {
