@@ -896,6 +896,35 @@ def test_stream_k_launch(ci, co, hi, f, n, epi):
     assert torch.equal(y.buf, first), "launch on a second stream differs"
 
 
+def test_output_pencil_alignment_contract():
+    """The fast kernels move output / skip pencils by 256-bit accesses: an
+    output view at a 16-byte but not 32-byte aligned address runs on the
+    generic kernel under ALGO_AUTO (same result within the tolerance) and is
+    refused with DCONV_EUNSUPPORTED when the FFMA kernel is forced."""
+    import ctypes
+    ci, co, hi = 16, 24, 12
+    x = po.uniform((ci, hi, hi), 9500, 0)
+    k = po.uniform((ci, co, 3, 3), 9500, 1)
+    shape = D.ConvShape(ci, co, hi, hi, 3, 3, 1)
+    xb = D.BlockedFeatureMap(ci, hi, hi, 8, data=dev(po.pack_feature_map(x, 8)[None]))
+    kb = D.BlockedKernel(ci, co, 3, 3, 8, 8, data=dev(po.pack_kernel(k, 8, 8)))
+    n_out = 3 * shape.h_o * shape.w_o * 8
+    buf = torch.zeros(n_out + 8, dtype=torch.float32, device="cuda")
+    assert buf.data_ptr() % 32 == 0
+    out = buf[4:4 + n_out]  # 16-byte aligned, not pencil-aligned
+    want = po.pack_feature_map(po.conv_oracle64(x, k, 1), 8)
+    for algo, ok in ((_abi.ALGO_AUTO, True), (_abi.ALGO_FFMA, False)):
+        d = D.make_desc(shape, 1, 8, 8, 0, algo)
+        rc = _abi.lib().dconv_cuda_conv_direct(ctypes.byref(d), _abi.ptr(xb.data), _abi.ptr(kb.data),
+                                               0, out.data_ptr(), _abi.stream_ptr(None))
+        if ok:
+            assert rc == _abi.OK, _abi.lib().dconv_cuda_last_error_detail()
+            assert_tol(host(out).reshape(want.shape), want, "generic kernel on the unaligned view")
+        else:
+            assert rc == _abi.EUNSUPPORTED
+            assert b"pencil-aligned" in _abi.lib().dconv_cuda_last_error_detail()
+
+
 def test_autotuned_plan_matches_default_tiles():
     """Per-layer tile autotune changes only the CTA tiling: every layer output
     stays within tolerance of the default-tile run (tile choices differ in
