@@ -1501,6 +1501,7 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
         break;
       }
   static const bool sk_always = getenv("DCONV_STREAMK_ALWAYS") != nullptr;
+  static const int sk_min_s = getenv("DCONV_STREAMK_MIN_S") ? atoi(getenv("DCONV_STREAMK_MIN_S")) : 2;
   // stream-K estimate: the whole waves but one, then (sms + tail) units cut
   // at stage granularity, + the boundary pieces' partial store / load
   const int sk_rr = (units / sms - 1) * sms;
@@ -1510,7 +1511,7 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   // 256->1024 + skip at 14x14 b256, S = 4: -1.5%)
   const bool sk_pays = sk_always || (t_sk < units / sms + est_tail &&
                                      !((p.epi & DCONV_EPI_ADD) && S < 8));
-  if (!no_streamk && sk_pays && main_units > 0 && tail > 0 && S >= 4 && sms + 1 < kSkFlagsPerSlot &&
+  if (!no_streamk && sk_pays && main_units > 0 && tail > 0 && S >= sk_min_s && sms + 1 < kSkFlagsPerSlot &&
       !(p.epi & DCONV_EPI_MAXPOOL) && p.skip != p.out && (int64_t)units * S < (1 << 30)) {
     if (unsigned* flags = sk_flags_for(stream, dev)) {
       const size_t smem_sk = configure<BN, NW, TPX, TCO, CBS>(q, 1, fine);
