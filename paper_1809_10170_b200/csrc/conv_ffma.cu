@@ -1412,9 +1412,14 @@ unsigned* sk_flags_for(cudaStream_t stream, int dev) {
   Dev& d = devs[dev];
   if (!d.tried) {
     d.tried = true;
+    // (the first launch of a process may already be under stream capture:
+    // the symbol lookup is no stream operation, keep it legal there)
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    cudaThreadExchangeStreamCaptureMode(&mode);
     void* sym = nullptr;
     if (cudaGetSymbolAddress(&sym, g_sk_flags) == cudaSuccess) d.base = static_cast<unsigned*>(sym);
     else cudaGetLastError();
+    cudaThreadExchangeStreamCaptureMode(&mode);
   }
   if (!d.base) return nullptr;
   for (size_t i = 0; i < d.streams.size(); ++i)

@@ -896,6 +896,38 @@ def test_stream_k_launch(ci, co, hi, f, n, epi):
     assert torch.equal(y.buf, first), "launch on a second stream differs"
 
 
+def test_first_launch_under_graph_capture():
+    """A fresh process whose very first conv launch (a stream-K one) happens
+    under CUDA-graph capture: the launcher's one-time set-up (kernel
+    attributes, cluster occupancy, the stream-K flag lookup) is legal there,
+    and two replays give the eager result bitwise."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import torch, sys
+sys.path.insert(0, ".")
+from paper_1809_10170_b200 import nets
+n, ci, co, hi = 16, 64, 128, 58
+l = nets.Layer("cap", ci, co, hi, hi, 3, 3, 1)
+a = nets.Act(n, ci, hi, hi); a.buf.uniform_(-1, 1)
+w = nets.pack_weights(torch.empty((ci, co, 3, 3), device="cuda").uniform_(-1, 1), False)
+y = nets.Act(n, co, l.h_o, l.w_o)
+torch.cuda.synchronize()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g):
+    nets.conv(l, n, a, w, y, stream=torch.cuda.current_stream())
+g.replay(); g.replay(); torch.cuda.synchronize()
+got = y.buf.clone(); y.buf.zero_()
+nets.conv(l, n, a, w, y); torch.cuda.synchronize()
+assert torch.equal(got, y.buf) and float(got.abs().max()) > 0
+print("capture ok")
+"""
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "capture ok" in r.stdout, r.stdout + r.stderr
+
+
 def test_output_pencil_alignment_contract():
     """The fast kernels move output / skip pencils by 256-bit accesses: an
     output view at a 16-byte but not 32-byte aligned address runs on the
