@@ -896,6 +896,34 @@ def test_stream_k_launch(ci, co, hi, f, n, epi):
     assert torch.equal(y.buf, first), "launch on a second stream differs"
 
 
+@pytest.mark.parametrize("cb", [16, 32])
+@pytest.mark.parametrize("ci,co,hi,f,n", [(64, 128, 58, 3, 16), (256, 256, 16, 1, 96)])
+def test_stream_k_wide_channel_blocks(cb, ci, co, hi, f, n):
+    """Stream-K launches (ragged unit counts) with c_ib = c_ob = 16 / 32
+    storage blocks -- the 3x3 loop and the dense 1x1 loop, skip-add + ReLU --
+    every element against the fp64 GPU referee."""
+    from oracle import gpu_oracle as go
+    xd = torch.empty((n, ci, hi, hi), device="cuda").uniform_(-1, 1)
+    wd = torch.empty((ci, co, f, f), device="cuda").uniform_(-1, 1)
+    shape = D.ConvShape(ci, co, hi, hi, f, f, 1)
+    xb = D.pack_feature_map(xd, cb)
+    kb = D.pack_kernel(wd, cb, cb)
+    skd = torch.empty((n, co, shape.h_o, shape.w_o), device="cuda").uniform_(-1, 1)
+    sk = D.pack_feature_map(skd, cb)
+    launches = _abi.lib().dconv_cuda_launch_count()
+    y = D.conv_direct(xb, kb, shape, D.BlockingParams(cb, 1, cb), relu=True, skip=sk,
+                      algo=_abi.ALGO_FFMA)
+    torch.cuda.synchronize()
+    assert _abi.lib().dconv_cuda_launch_count() - launches == 1
+    want = go.conv64(xd.data_ptr(), n, ci, hi, hi, 1, ci * hi * hi, hi * hi, hi, wd, 1)
+    want = (want + D.pack_feature_map(skd, 8).data.double()).clamp_min(0.0)
+    # c_b-blocked output -> blocks of 8 channels
+    got = y.data.view(n, co // cb, shape.h_o, shape.w_o, cb // 8, 8).permute(0, 1, 4, 2, 3, 5)
+    got = got.reshape(n, co // 8, shape.h_o, shape.w_o, 8)
+    ok, nbad, err, ratio = go.check_tol(got, want)
+    assert ok, f"c_b {cb}: {nbad} elements out of tolerance, max err {err}"
+
+
 def test_first_launch_under_graph_capture():
     """A fresh process whose very first conv launch (a stream-K one) happens
     under CUDA-graph capture: the launcher's one-time set-up (kernel
