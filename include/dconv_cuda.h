@@ -126,8 +126,10 @@ int64_t dconv_conv_flops(int c_i, int c_o, int h_o, int w_o, int h_f, int w_f);
  * w:    blocked kernel (c_ob, c_ib), full C_o (sharding selects blocks)
  * skip: blocked map like the output, read when epilogue has ADD (else NULL)
  * out:  blocked output view, c_b == d->c_ob.  Every valid element of the
- *       selected output blocks is written exactly once (no zero-init pass);
- *       padded channel slots are written as exact 0.
+ *       selected output blocks is written with its final value exactly once
+ *       (no zero-init pass; a stream-K launch stores a partial tile into the
+ *       <= #SMs tiles it cuts first); padded channel slots are written as
+ *       exact 0.
  * Alignment (FFMA and tensor-core kernels): `in` and `w` 16 bytes with view
  * strides that are multiples of 4 floats (bulk copies); `out` and `skip`
  * pencil-aligned -- 32 bytes, view strides multiples of 8 floats -- because a
