@@ -623,11 +623,13 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
   Pieces pieces = make_pieces();
   for (int u, st0, st1; pieces.next(u, st0, st1); ++unit_iter) {  // (shadow the rank's range)
     const bool whole = !p.streamk || (st0 == 0 && st1 == S);
-    // stream-K boundary pieces: 1 = later stages of a unit begun by the
+    // stream-K boundary pieces: 1 = last stages of a unit begun by the
     // previous CTA (store the raw partial tile into the output map, raise
     // this CTA's flag), 2 = first stages of a unit continued by the next CTA
-    // (wait for its flag, add its partial, run the epilogue)
-    const int sk_mode = whole ? 0 : (st0 > 0 ? 1 : 2);
+    // (wait for its flag, add its partial, run the epilogue), 3 = middle
+    // stages (fewer units than SMs: a unit spans three or more CTAs): wait,
+    // add, store the raw sum back, raise the flag
+    const int sk_mode = whole ? 0 : (st0 > 0 ? (st1 < S ? 3 : 1) : 2);
     TileRows tr{};
     int tx0 = 0, jb0 = 0, cg_valid = 0;
     // dense 1x1 tiles handed to the epilogue warpgroup need no tile geometry
@@ -777,8 +779,8 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
       }
     }
     if (kFfmaProf && p.dbg && tid == 0) p.dbg[blockIdx.x * 16 + 3] = clock64() - t_start;  // loop end
-    if (sk_mode == 2) {
-      // stream-K finisher: the next CTA stored this unit's later-stage
+    if (sk_mode >= 2) {
+      // stream-K finisher (or middle piece): the next CTA stored this unit's later-stage
       // partial tile into the output map first thing; add it to the
       // registers (first stages + later stages, in that order) and go on as
       // for a whole unit.  The flag is cleared for the next launch.
@@ -824,7 +826,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
         }
       }
     }
-    if (p.epi_wg && sk_mode != 1) {
+    if (p.epi_wg && (sk_mode == 0 || sk_mode == 2)) {
       // hand the finished tile to the epilogue warpgroup (TMEM result buffer
       // wu_iter & 1) and go on with the next unit
       const int rb = wu_iter & 1;
@@ -855,7 +857,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
       tile_row(p, tr, ty, img, y, prow);
       float* o = p.out + sub_off<CBS>(jl, p.out_blk) + (int64_t)img * p.out_img +
                  (int64_t)y * p.out_row + (int64_t)x * CBS;
-      if (sk_mode == 1) {  // raw partial tile, finished by the previous CTA
+      if (sk_mode & 1) {  // raw partial tile, finished by the previous CTA
 #pragma unroll
         for (int c = 0; c < 8; c += 4)
           __stcg(reinterpret_cast<float4*>(o + c), make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]));
@@ -1019,7 +1021,7 @@ __global__ void __launch_bounds__((NW + 8) * 32, 1)
           emit(k, jl, v);
         }
       }
-      if (sk_mode == 1) {
+      if (sk_mode & 1) {
         // partial tile stored: publish it to the finishing CTA
         __threadfence();
         asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
@@ -1469,13 +1471,42 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   // (1) fewer units than SMs (batch 1): one split-K launch with the cheapest
   // cluster size (the same cycle model as the tile selector).
   int best_ks = 1;
+  double split_cycles_est = unit_cycles(p, BM, BN) + kLaunchFill;
   if (units < sms && !no_split) {
     FfmaParams t = p;
     if (configure<BN, NW, TPX, TCO, CBS>(t, 2, true))
-      best_ks = best_split(units, slots, t.n_g * t.n_r, unit_cycles(p, BM, BN), nullptr);
+      best_ks = best_split(units, slots, t.n_g * t.n_r, unit_cycles(p, BM, BN), &split_cycles_est);
   }
   if (const int kf = ksplit_knob(); kf && !no_split)
     best_ks = std::max(1, std::min(kf, std::min(kMaxKs, S)));
+  // (1b) between a quarter of the SMs and all of them (small per-rank
+  // batches, VGG b1's 112x112 / 56x56 layers): stream-K over every SM, a unit
+  // cut into up to 5 pieces chained through the output map, when its estimate
+  // (stage-granular share per CTA + ~4K cycles per piece of the chain) beats
+  // the cluster split
+  static const bool no_streamk_few = getenv("DCONV_NO_STREAMK") != nullptr ||
+                                     getenv("DCONV_NO_STREAMK_FEW") != nullptr;
+  if (!no_streamk_few && !ksplit_knob() && units < sms && units * 4 >= sms && S >= 2 &&
+      (int64_t)units * S >= sms &&  // every CTA holds a stage: piece b continues in CTA b + 1
+      sms + 1 < kSkFlagsPerSlot && !(p.epi & DCONV_EPI_MAXPOOL) && p.skip != p.out &&
+      NW == 8 && TCO == 8) {
+    const int64_t per_cta = ((int64_t)units * S + sms - 1) / sms;  // stages
+    const int pieces = (int)((S + per_cta - 1) / per_cta) + 1;
+    const double c_sk = (double)per_cta / S * unit_cycles(p, BM, BN) + pieces * 4000.0 + kLaunchFill;
+    if (c_sk < split_cycles_est) {
+      if (unsigned* flags = sk_flags_for(stream, dev)) {
+        const size_t smem_sk = configure<BN, NW, TPX, TCO, CBS>(q, 1, fine);
+        q.streamk = 1;
+        q.sk_flags = flags;
+        q.sk_base = 0;
+        if (knobs().debug)
+          fprintf(stderr, "conv_ffma<%d,%d,%d>: stream-K (few units) TH=%d TW=%d units=%d S=%d "
+                  "stages/CTA=%lld pieces<=%d\n", BM, BN, WF, q.TH, q.TW, units, S,
+                  (long long)per_cta, pieces);
+        return launch_units(kernel, threads, q, smem_sk, 0, units, sms, stream);
+      }
+    }
+  }
   if (best_ks > 1) {
     FfmaParams r = p;
     const size_t smem = configure<BN, NW, TPX, TCO, CBS>(r, best_ks, true);
