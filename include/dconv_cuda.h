@@ -136,7 +136,8 @@ int64_t dconv_conv_flops(int c_i, int c_o, int h_o, int w_o, int h_f, int w_f);
  * pencil moves as one 256-bit access.  cudaMalloc / torch allocations and any
  * pencil offset into them qualify.  Other views run on the generic kernel
  * (DCONV_ALGO_AUTO) or return DCONV_EUNSUPPORTED (DCONV_ALGO_FFMA).
- * Stream-K (layers whose tile count does not fill whole waves of SMs): while
+ * Stream-K (layers whose tile count does not fill whole waves of SMs, or is
+ * between a quarter of the SMs and all of them): while
  * the launch runs, `out` also carries partial tiles, so `out` must not alias
  * `skip` for such a launch to use it (aliasing launches keep the split-K
  * tail); its per-stream flags live in the module, nothing is allocated.

@@ -851,11 +851,15 @@ def test_tail_split_launch():
     (128, 192, 30, 3, 24, _abi.EPI_RELU),                  # ragged C_o group, ReLU
     (256, 256, 16, 1, 96, _abi.EPI_ADD | _abi.EPI_RELU),   # dense 1x1 + skip-add (epilogue warpgroup)
     (512, 512, 16, 3, 32, _abi.EPI_ADD),                   # 14x14 maps across images, 1.35 waves
+    (512, 512, 30, 3, 4, _abi.EPI_ADD | _abi.EPI_RELU),    # 104 units < 148 SMs: 3-piece chains
+    (512, 512, 16, 3, 8, 0),                               # 56 units: 4-piece chains (middle pieces)
 ])
 def test_stream_k_launch(ci, co, hi, f, n, epi):
-    """Ragged unit counts (1.x / 2.65 waves of 148 SMs) run as one stream-K
-    launch: whole waves round-robin, then the last 1.x waves cut at stage
-    granularity, the cut units finished through the output map.  Every
+    """Ragged unit counts (1.x / 2.65 waves of 148 SMs, or fewer units than
+    SMs) run as one stream-K launch: whole waves round-robin, then the last
+    1.x waves (or everything) cut at stage granularity, the cut units
+    finished through the output map -- through chains of middle pieces when a
+    unit spans three or more CTAs.  Every
     element against the fp64 GPU referee at the fp32 tolerance; a second
     launch (flags self-reset) and a launch on another stream (its own flag
     slot) are bitwise equal to the first."""
