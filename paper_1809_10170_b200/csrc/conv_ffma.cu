@@ -1484,9 +1484,10 @@ int launch_variant(FfmaParams p, cudaStream_t stream) {
   // cut into up to 5 pieces chained through the output map, when its estimate
   // (stage-granular share per CTA + ~4K cycles per piece of the chain) beats
   // the cluster split
+  static const int sk_few_div = getenv("DCONV_STREAMK_FEW_DIV") ? atoi(getenv("DCONV_STREAMK_FEW_DIV")) : 4;
   static const bool no_streamk_few = getenv("DCONV_NO_STREAMK") != nullptr ||
                                      getenv("DCONV_NO_STREAMK_FEW") != nullptr;
-  if (!no_streamk_few && !ksplit_knob() && units < sms && units * 4 >= sms && S >= 2 &&
+  if (!no_streamk_few && !ksplit_knob() && units < sms && units * sk_few_div >= sms && S >= 2 &&
       (int64_t)units * S >= sms &&  // every CTA holds a stage: piece b continues in CTA b + 1
       sms + 1 < kSkFlagsPerSlot && !(p.epi & DCONV_EPI_MAXPOOL) && p.skip != p.out &&
       NW == 8 && TCO == 8) {
